@@ -1,0 +1,180 @@
+"""TEST INFRASTRUCTURE — ctypes bindings for the C restatement (psdf_oracle.c).
+
+``OracleGrid`` holds a grid + MLP in f64 and exposes the restated hot path:
+march, render, per-ray backward, regularizers, G^T fold and a full train step.
+Used only by tests/, __graft_entry__.smoke() and bench.py's CPU legs.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+from .refcore import ORACLE_SO, HERE, RefCamera, RefRenderOpts, RefStepParams, ptr, _dp, _ip, _lp
+
+_lib = None
+
+
+def build_oracle():
+    subprocess.run(["make", "-s", "-C", HERE, "oracle"], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(ORACLE_SO):
+        build_oracle()
+    L = C.CDLL(ORACLE_SO)
+    L.og_create.restype = C.c_void_p
+    L.og_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _ip, C.c_double, _dp,
+                            C.c_double, _ip, _ip, _ip, _dp, _dp, _dp, _dp, _dp, C.c_int]
+    L.og_free.argtypes = [C.c_void_p]
+    L.og_mlp_size.restype = C.c_int64
+    L.og_mlp_size.argtypes = [C.c_void_p]
+    L.og_export.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp]
+    L.og_smooth_all.argtypes = [C.c_void_p]
+    L.og_march_ray.argtypes = [C.c_void_p, _dp, _dp, C.c_int, _dp]
+    L.og_pixel_dir.argtypes = [C.POINTER(RefCamera), C.c_double, C.c_double, _dp]
+    L.og_render_ray.argtypes = [C.c_void_p, _dp, _dp, C.POINTER(RefRenderOpts), _dp]
+    L.og_render_image.argtypes = [C.c_void_p, C.POINTER(RefCamera), C.POINTER(RefRenderOpts), _dp, _dp,
+                                  _dp, _lp]
+    L.og_grads_new.restype = C.c_void_p
+    L.og_grads_new.argtypes = [C.c_void_p]
+    L.og_grads_free.argtypes = [C.c_void_p]
+    L.og_grads_clear.argtypes = [C.c_void_p, C.c_void_p]
+    L.og_grads_export.argtypes = [C.c_void_p, C.c_void_p, _dp, _dp, _dp, _dp, _dp]
+    L.og_ray_backward.argtypes = [C.c_void_p, _dp, _dp, C.POINTER(RefRenderOpts), _dp, C.c_double,
+                                  C.c_void_p]
+    L.og_photo_pixel.argtypes = [_dp, _dp, C.c_int, C.c_double, C.c_double, _dp]
+    L.og_regularizer.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_void_p, _dp]
+    L.og_gt_fold.argtypes = [C.c_void_p, C.c_void_p]
+    L.og_train_reset.argtypes = [C.c_void_p]
+    L.og_train_step.argtypes = [C.c_void_p, C.c_int, C.POINTER(RefCamera), C.POINTER(_dp),
+                                C.POINTER(_dp), C.POINTER(RefStepParams), _dp, _lp, C.c_void_p,
+                                C.c_void_p]
+    _lib = L
+    return L
+
+
+class OracleGrid:
+    """The C restatement's grid, built from a GridArrays description."""
+
+    def __init__(self, a, smooth=True):
+        """a: GridArrays (see refcore.GridArrays). smooth=True installs a.smooth
+        verbatim; False recomputes it from a.raw (grid.cpp:247-250)."""
+        self.L = lib()
+        self.a = a
+        f = lambda x: np.ascontiguousarray(x, np.float64)
+        i = lambda x: np.ascontiguousarray(x, np.int32)
+        res = np.array(a.res, np.int32)
+        org = np.array(a.origin, np.float64)
+        self._keep = [f(a.raw), f(a.smooth), f(a.planes), f(a.probes), f(a.mlp), i(a.tile_coords),
+                      i(a.probe_ids), i(a.probe_coords), res, org]
+        raw, sm, pl, pr, mlp, tc, pid, pc, res, org = self._keep
+        self.h = C.c_void_p(self.L.og_create(a.T, a.P, a.n_s, a.n_a, a.sh_order, ptr(res, _ip),
+                                             a.voxel_size, ptr(org), a.far_field_voxels, ptr(tc, _ip),
+                                             ptr(pid, _ip), ptr(pc, _ip), ptr(raw),
+                                             ptr(sm) if smooth else None, ptr(pl), ptr(pr), ptr(mlp),
+                                             a.ncam))
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.L.og_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def export(self):
+        a = self.a
+        out = dict(raw=np.zeros_like(a.raw, dtype=np.float64), smooth=np.zeros_like(a.smooth, dtype=np.float64),
+                   planes=np.zeros_like(a.planes, dtype=np.float64),
+                   probes=np.zeros_like(a.probes, dtype=np.float64), mlp=np.zeros_like(a.mlp, dtype=np.float64))
+        self.L.og_export(self.h, ptr(out["raw"]), ptr(out["smooth"]), ptr(out["planes"]),
+                         ptr(out["probes"]), ptr(out["mlp"]))
+        return out
+
+    def march_ray(self, o, d, n_max=512):
+        ts = np.zeros(max(n_max, 1))
+        o = np.asarray(o, np.float64)
+        d = np.asarray(d, np.float64)
+        n = self.L.og_march_ray(self.h, ptr(o), ptr(d), n_max, ptr(ts))
+        return ts[:n].copy()
+
+    def render_image(self, cam, opts):
+        w, h = cam.width, cam.height
+        rgb = np.zeros((h, w, 3))
+        alpha = np.zeros((h, w))
+        depth = np.zeros((h, w))
+        counts = np.zeros(5, np.int64)
+        self.L.og_render_image(self.h, C.byref(cam), C.byref(opts), ptr(rgb), ptr(alpha), ptr(depth),
+                               ptr(counts, _lp))
+        return rgb, alpha, depth, counts
+
+    def _grads(self, gb):
+        a = self.a
+        out = dict(raw=np.zeros(a.raw.shape), smooth=np.zeros(a.smooth.shape),
+                   planes=np.zeros(a.planes.shape), probes=np.zeros(a.probes.shape),
+                   mlp=np.zeros(a.mlp.shape))
+        self.L.og_grads_export(self.h, gb, ptr(out["raw"]), ptr(out["smooth"]), ptr(out["planes"]),
+                               ptr(out["probes"]), ptr(out["mlp"]))
+        return out
+
+    def ray_backward(self, o, d, opts, up_color, up_alpha, fold=True):
+        gb = C.c_void_p(self.L.og_grads_new(self.h))
+        o = np.asarray(o, np.float64)
+        d = np.asarray(d, np.float64)
+        uc = np.asarray(up_color, np.float64)
+        self.L.og_ray_backward(self.h, ptr(o), ptr(d), C.byref(opts), ptr(uc), up_alpha, gb)
+        if fold:
+            self.L.og_gt_fold(self.h, gb)
+        g = self._grads(gb)
+        self.L.og_grads_free(gb)
+        return g
+
+    def regularizer(self, which, lam):
+        gb = C.c_void_p(self.L.og_grads_new(self.h))
+        out = np.zeros(2)
+        self.L.og_regularizer(self.h, which, lam, gb, ptr(out))
+        g = self._grads(gb)
+        self.L.og_grads_free(gb)
+        return out, g
+
+    def train_reset(self):
+        self.L.og_train_reset(self.h)
+
+    def train_step(self, cams, gts, masks, hp):
+        n = len(cams)
+        arr = (RefCamera * n)(*cams)
+        gts = [np.ascontiguousarray(g, np.float64) for g in gts]
+        masks = [np.ascontiguousarray(m, np.float64) for m in masks]
+        gp = (_dp * n)(*[ptr(g) for g in gts])
+        mp = (_dp * n)(*[ptr(m) for m in masks])
+        losses = np.zeros(10)
+        counts = np.zeros(6, np.int64)
+        g0 = C.c_void_p(self.L.og_grads_new(self.h))
+        g1 = C.c_void_p(self.L.og_grads_new(self.h))
+        self.L.og_train_step(self.h, n, arr, gp, mp, C.byref(hp), ptr(losses), ptr(counts, _lp), g0, g1)
+        self.last_grads = (self._grads(g0), self._grads(g1))
+        self.L.og_grads_free(g0)
+        self.L.og_grads_free(g1)
+        return losses, counts
+
+
+def pixel_dir(cam, u, v):
+    d = np.zeros(3)
+    lib().og_pixel_dir(C.byref(cam), u, v, ptr(d))
+    return d
+
+
+def step_params(tau, lr_vox, lr_mlp, l_sdf=0.7, l_eik=0.3, l_norm=0.2, l_feat=0.15, l_probe=0.25,
+                photo_scale=20.0, use_camera_bias=False):
+    hp = RefStepParams()
+    hp.tau, hp.lr_vox, hp.lr_mlp = tau, lr_vox, lr_mlp
+    hp.l_sdf, hp.l_eik, hp.l_norm, hp.l_feat, hp.l_probe = l_sdf, l_eik, l_norm, l_feat, l_probe
+    hp.photo_scale = photo_scale
+    hp.use_camera_bias = int(use_camera_bias)
+    return hp
