@@ -1,0 +1,194 @@
+/* psdf.h — C ABI of the B200-native ProbeSDF fused render + train hot path.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj).  The reference exposes it as a C++ static-library
+ * API with no FFI; each entry point below names the
+ * reference interface it replaces.  Plain pointers and sizes only: no C++ or
+ * torch types cross this boundary.  All functions return a status code
+ * (PSDF_OK == 0); psdf_last_error() gives the message.  The C++ drop-in shim
+ * (include/sdfrecon_gpu.hpp) maps the codes back to the reference's exception
+ * types (std::invalid_argument / std::out_of_range / std::runtime_error).
+ *
+ * Threading: one host thread and one CUDA stream per context; one context per
+ * GPU (rank).  Device memory is owned by the context; host buffers are
+ * borrowed for the duration of the call.
+ *
+ * Flat layouts (identical to the reference's storage order):
+ *   tile_coords [T][3] int32          tile lattice coordinates (grid.hpp:25)
+ *   probe_ids   [T][8] int32          corner probes, bit0->x bit1->y bit2->z
+ *                                     (grid.cpp:70-71)
+ *   probe_coords[P][3] int32          probe lattice coordinates (grid.hpp:86)
+ *   raw, smooth [T][4096] f32         x-major (x*16+y)*16+z (grid.hpp:26-27)
+ *   planes      [T][3][256][n_s] f32  plane_x (y,z), plane_y (x,z),
+ *                                     plane_z (x,y) (grid.hpp:28-35)
+ *   probes      [P][l*l][n_a] f32     band-major coefficient blocks (sh.hpp:15-23)
+ *   mlp         f32 w1[32][in] b1[32] w2[32][32] b2[32] w3[3][32] b3[3]
+ *               camera_bias[ncam][32], in = n_s + n_a + 6 (decoder.hpp:17-31)
+ *   images      rgb [h][w][3] f32 row-major, mask [h][w] uint8 (!=0 = in)
+ */
+#ifndef PSDF_H
+#define PSDF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSDF_ABI_VERSION 1
+
+enum {
+    PSDF_OK = 0,
+    PSDF_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+    PSDF_ERR_OUT_OF_RANGE = 2,     /* std::out_of_range */
+    PSDF_ERR_RUNTIME = 3,          /* std::runtime_error */
+    PSDF_ERR_CUDA = 4,
+    PSDF_ERR_NCCL = 5,
+};
+
+typedef struct psdf_ctx psdf_ctx;
+
+/* Camera (camera.hpp:12-17): pinhole, world-from-camera rotation row-major. */
+typedef struct {
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    double rot[9];
+    double pos[3];
+    int32_t id, pad_;
+} psdf_camera;
+
+/* RenderOptions (renderer.hpp:13-27). */
+typedef struct {
+    double tau;
+    double early_stop;   /* early_stop_transmittance; 0 disables */
+    double bg[3];        /* background */
+    int32_t n_max;
+    int32_t camera_id;   /* -1 omits the per-camera bias */
+    int32_t no_spatial, no_angular, no_fresnel, sh_order_override, need_colors;
+} psdf_render_opts;
+
+/* Per-step hyper-parameters, already evaluated for this iteration exactly as
+ * trainer.cpp:126-134 does (brackets, warm-up, tau / voxel_size,
+ * photo_scale = lambda_photo / images_per_batch). */
+typedef struct {
+    double tau, lr_vox, lr_mlp, l_sdf, l_eik, l_norm, l_feat, l_probe, photo_scale;
+    int32_t use_camera_bias; /* TrainSchedule::camera_bias (trainer.cpp:153) */
+    int32_t pad_;
+} psdf_step_params;
+
+/* SparseGrid metadata (grid.hpp:57-70). */
+typedef struct {
+    int32_t T, P;              /* allocated tiles, pool probes */
+    int32_t n_s, n_a, sh_order;
+    int32_t res[3];            /* voxels per axis, multiples of 16 */
+    double voxel_size;
+    double origin[3];
+    double far_field_voxels;
+    int32_t ncam;              /* camera-bias rows in the MLP (0 = disabled) */
+    int32_t pad_;
+} psdf_grid_desc;
+
+/* Statistics of one render / train pass (the oracle's RayWorkspace counts). */
+typedef struct {
+    int64_t n_rays;     /* rays traced */
+    int64_t n_marched;  /* samples kept after early termination (N_m) */
+    int64_t n_extra;    /* rays with >= 1 sample (N_x) */
+    int64_t n_shaded;   /* decoded samples (N_sh) */
+    int64_t n_alpha;    /* samples with alpha > 0 on rays run backward (N_alpha) */
+    int64_t n_bwd_rays; /* rays with a non-zero loss gradient */
+} psdf_counts;
+
+/* Losses of one step — the trainer.cpp:201-207 log line. */
+typedef struct {
+    double photo, sdf, eik, normal, features, probes, total, psnr;
+    double sq_err, mask_px;
+} psdf_losses;
+
+/* ---- context ----------------------------------------------------------- */
+int psdf_abi_version(void);
+int psdf_create(int device, psdf_ctx** out);
+int psdf_destroy(psdf_ctx* ctx);
+/* Message of the last failed call on this thread (ctx may be NULL). */
+const char* psdf_last_error(psdf_ctx* ctx);
+
+/* ---- scene state ---------------------------------------------------------
+ * Replaces constructing a sdfrecon::SparseGrid / DecoderMlp in host memory
+ * (grid.hpp:57-132, decoder.hpp:17-31); uploaded once per LOD.  smooth may be
+ * NULL, in which case it is recomputed on the device (SparseGrid::smooth_all,
+ * grid.cpp:247-250).  Uploading a grid resets the optimizer state. */
+int psdf_upload_grid(psdf_ctx* ctx, const psdf_grid_desc* desc, const int32_t* tile_coords,
+                     const int32_t* probe_ids, const int32_t* probe_coords, const float* raw,
+                     const float* smooth, const float* planes, const float* probes);
+int psdf_upload_mlp(psdf_ctx* ctx, const float* mlp, int64_t n);
+int64_t psdf_mlp_size(int n_s, int n_a, int ncam);
+/* Copies parameters device -> host (any pointer may be NULL). */
+int psdf_download_params(psdf_ctx* ctx, float* raw, float* smooth, float* planes, float* probes,
+                         float* mlp);
+/* Gradient buffers of the last train step (parity / debugging).
+ * stage 0: after the ray pass (GradBuffers after trainer.cpp:184-185);
+ * stage 1: what Adam consumed (after regularizers + G^T fold, trainer.cpp:193).
+ * smooth = the smooth-staged SDF gradient (grads.hpp:15). */
+/* Keep a copy of the stage-0 (post ray pass) gradients on every step. */
+int psdf_set_keep_raypass_grads(psdf_ctx* ctx, int keep);
+int psdf_download_grads(psdf_ctx* ctx, int stage, float* raw, float* smooth, float* planes,
+                        float* probes, float* mlp);
+/* SparseGrid::smooth_all (grid.cpp:247-250) on the device. */
+int psdf_smooth_all(psdf_ctx* ctx);
+
+/* ---- render ----------------------------------------------------------------
+ * render_image (renderer.cpp:321-337 / renderer.hpp:98-99).  Host outputs:
+ * rgb [h][w][3], alpha [h][w] (RenderedImage), depth [h][w] = sum_i w_i t_i
+ * (extension; NULL to skip).  counts may be NULL. */
+int psdf_render(psdf_ctx* ctx, const psdf_camera* cam, const psdf_render_opts* opt, float* rgb,
+                float* alpha, float* depth, psdf_counts* counts);
+/* Same, device-resident outputs (pointers into device memory). */
+int psdf_render_device(psdf_ctx* ctx, const psdf_camera* cam, const psdf_render_opts* opt,
+                       float* d_rgb, float* d_alpha, float* d_depth, psdf_counts* counts);
+
+/* ---- train ------------------------------------------------------------------
+ * One iteration of the train() loop body (trainer.cpp:136-195): clear
+ * gradients, ray pass over every pixel of the batch views (render_ray +
+ * photo_pixel + render_ray_backward), regularizers, G^T fold, Adam, re-smooth.
+ * Host images: gt_rgb[i] [h][w][3] f32, mask[i] [h][w] u8.  With a
+ * communicator (psdf_comm_init) each rank processes its contiguous 1/N slice
+ * of the batch's pixels and the gradients are all-reduced before Adam. */
+int psdf_train_reset(psdf_ctx* ctx); /* fresh Adam state (trainer.cpp:115) */
+int psdf_train_step(psdf_ctx* ctx, int n_views, const psdf_camera* cams,
+                    const float* const* gt_rgb, const uint8_t* const* mask,
+                    const psdf_step_params* hp, psdf_losses* losses, psdf_counts* counts);
+/* Dataset kept resident in HBM: upload once, then step by view index. */
+int psdf_upload_views(psdf_ctx* ctx, int n_views, const psdf_camera* cams,
+                      const float* const* gt_rgb, const uint8_t* const* mask);
+int psdf_train_step_views(psdf_ctx* ctx, int n_batch, const int32_t* view_ids,
+                          const psdf_step_params* hp, psdf_losses* losses, psdf_counts* counts);
+
+/* ---- test hooks for the bit-exact indexing contract ------------------------
+ * march_ray (renderer.cpp:55-86 / renderer.hpp:39-40) for n explicit rays:
+ * ts [n][n_max] (row-major), counts [n] = samples of each ray. */
+int psdf_march_rays(psdf_ctx* ctx, int n, const double* origins, const double* dirs, int n_max,
+                    double* ts, int32_t* counts);
+/* Camera::pixel_dir (camera.hpp:32-35) at every pixel centre: out [h][w][3]. */
+int psdf_pixel_dirs(const psdf_camera* cam, double* out);
+
+/* ---- multi-GPU (ray-batch data parallel) ------------ */
+#define PSDF_UNIQUE_ID_BYTES 128
+int psdf_comm_unique_id(void* out /* PSDF_UNIQUE_ID_BYTES */);
+int psdf_comm_init(psdf_ctx* ctx, const void* unique_id, int rank, int world_size);
+
+/* ---- timing / introspection ------------------------------------------------ */
+/* Device time (ms) of the last call's dominant kernel (the fused ray-pass
+ * kernel), measured with CUDA events on the context's stream, and the number
+ * of kernels the last call launched. */
+int psdf_last_timing(psdf_ctx* ctx, double* ray_kernel_ms, double* step_ms, int* launches);
+/* Raw CUDA stream of the context (cudaStream_t), for callers that time or
+ * overlap work around the context. */
+void* psdf_stream(psdf_ctx* ctx);
+/* Page-locked host memory for staging images (cudaMallocHost). */
+void* psdf_host_alloc(size_t bytes);
+void psdf_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PSDF_H */

@@ -1,0 +1,1020 @@
+// psdf.cu — host side of the C ABI declared in include/psdf.h.
+//
+// One context per GPU.  Device state (SoA fp32):
+//   params  = [raw T*4096 | planes T*3*256*n_s | probes P*l^2*n_a | mlp]
+//   smooth  = [T*4096]                     (SparseGrid smoothed SDF)
+//   grads   = same layout as params        (GradBuffers minus staging)
+//   gsmooth = [T*4096]                     (smooth-staged SDF gradient)
+//   adam m, v = same layout as params
+//   tile_table [nt0*nt1*nt2] int32, probe_table [(nt0+1)(nt1+1)(nt2+1)] int32
+// A train step is the kernel sequence K2 (fused ray pass) -> K3..K6
+// (regularizers) -> K7 (G^T fold) -> [NCCL all-reduce] -> K8 (Adam) -> K9
+// (smoothing), all on the context's stream.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/psdf.h"
+#include "psdf_grid.cuh"
+#include "psdf_raypass.cuh"
+
+using namespace psdf;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Failure {
+    int code;
+};
+
+[[noreturn]] void fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    throw Failure{code};
+}
+
+#define CK(x)                                                                                  \
+    do {                                                                                       \
+        cudaError_t e_ = (x);                                                                  \
+        if (e_ != cudaSuccess) fail(PSDF_ERR_CUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), \
+                                    __FILE__, __LINE__);                                       \
+    } while (0)
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return PSDF_OK;
+    } catch (const Failure& e) {
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return PSDF_ERR_RUNTIME;
+    }
+}
+
+// ------------------------------------------------------------------ NCCL
+struct Nccl {
+    void* so = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+
+    void load() {
+        if (so) return;
+        // NCCL is loaded lazily so single-GPU use has no NCCL dependency; the
+        // process-wide libnccl.so.2 (e.g. torch's) is reused when present.
+        so = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!so) fail(PSDF_ERR_NCCL, "cannot load libnccl.so.2: %s", dlerror());
+        GetUniqueId = (decltype(GetUniqueId))dlsym(so, "ncclGetUniqueId");
+        CommInitRank = (decltype(CommInitRank))dlsym(so, "ncclCommInitRank");
+        AllReduce = (decltype(AllReduce))dlsym(so, "ncclAllReduce");
+        CommDestroy = (decltype(CommDestroy))dlsym(so, "ncclCommDestroy");
+        GetErrorString = (decltype(GetErrorString))dlsym(so, "ncclGetErrorString");
+        if (!GetUniqueId || !CommInitRank || !AllReduce || !CommDestroy || !GetErrorString)
+            fail(PSDF_ERR_NCCL, "libnccl.so.2 lacks the expected symbols");
+    }
+};
+Nccl g_nccl;
+
+#define NK(x)                                                                              \
+    do {                                                                                   \
+        ncclResult_t r_ = (x);                                                             \
+        if (r_ != ncclSuccess) fail(PSDF_ERR_NCCL, "%s: %s", #x, g_nccl.GetErrorString(r_)); \
+    } while (0)
+
+struct DevView {
+    psdf_camera cam;
+    float* rgb = nullptr;
+    uint8_t* mask = nullptr;
+};
+
+// Gaussian taps of grid.cpp:10-22, evaluated in f64.
+Taps gaussian_taps() {
+    double w[5], sum = 0.0;
+    for (int d = -2; d <= 2; ++d) {
+        w[d + 2] = std::exp(-0.5 * d * d);
+        sum += w[d + 2];
+    }
+    Taps t;
+    for (int i = 0; i < 5; ++i) t.w[i] = (float)(w[i] / sum);
+    return t;
+}
+
+bool supported_channels(int ns, int na) {
+#ifdef PSDF_DEV_MINIMAL
+    return (ns == 2 && na == 2) || (ns == 4 && na == 4);
+#endif
+    return (ns == 2 && na == 2) || (ns == 4 && na == 4) || (ns == 8 && na == 8) ||
+           (ns == 4 && na == 8) || (ns == 8 && na == 4);
+}
+
+template <typename F>
+void dispatch_channels(int ns, int na, F&& f) {
+    if (ns == 2 && na == 2) f.template operator()<2, 2>();
+    else if (ns == 4 && na == 4) f.template operator()<4, 4>();
+#ifndef PSDF_DEV_MINIMAL
+    else if (ns == 8 && na == 8) f.template operator()<8, 8>();
+    else if (ns == 4 && na == 8) f.template operator()<4, 8>();
+    else if (ns == 8 && na == 4) f.template operator()<8, 4>();
+#endif
+    else fail(PSDF_ERR_INVALID_ARGUMENT, "unsupported (n_s, n_a) = (%d, %d)", ns, na);
+}
+
+int64_t up4(int64_t x) { return (x + 3) & ~int64_t(3); }
+
+}  // namespace
+
+struct psdf_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev_ray0 = nullptr, ev_ray1 = nullptr, ev_step0 = nullptr, ev_step1 = nullptr;
+
+    bool has_grid = false;
+    psdf_grid_desc desc{};
+    int in_dim = 0;
+    int nt[3] = {0, 0, 0};
+    int64_t off_raw = 0, off_planes = 0, off_probes = 0, off_mlp = 0, n_params = 0;
+    int64_t n_planes = 0, n_probes = 0, mlp_size = 0;
+    int32_t* d_tile_table = nullptr;
+    int4* d_tile_coords = nullptr;
+    int32_t* d_probe_ids = nullptr;
+    int32_t* d_probe_table = nullptr;
+    int4* d_probe_coords = nullptr;
+    float* d_params = nullptr;
+    float* d_smooth = nullptr;
+    float* d_grads = nullptr;
+    float* d_gsmooth = nullptr;
+    float* d_grads0 = nullptr;     // stage-0 copies (keep_raypass)
+    float* d_gsmooth0 = nullptr;
+    float* d_m = nullptr;
+    float* d_v = nullptr;
+    long adam_t = 0;
+    bool keep_raypass = false;
+
+    std::vector<DevView> views;
+    float* d_stage_rgb = nullptr;
+    uint8_t* d_stage_mask = nullptr;
+    size_t stage_px = 0;
+    ViewDev* d_viewdev = nullptr;
+    int viewdev_cap = 0;
+    float* d_render = nullptr;  // render scratch: rgb | alpha | depth
+    size_t render_px = 0;
+
+    unsigned long long* d_work = nullptr;
+    unsigned long long* d_counts = nullptr;
+    double* d_stats = nullptr;
+    double* h_stats = nullptr;              // pinned
+    unsigned long long* h_counts = nullptr;  // pinned
+
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1;
+
+    float last_ray_ms = 0.f, last_step_ms = 0.f;
+    int last_launches = 0;
+
+    GridView view() const {
+        GridView g{};
+        g.T = desc.T;
+        g.P = desc.P;
+        g.n_s = desc.n_s;
+        g.n_a = desc.n_a;
+        g.order = desc.sh_order;
+        for (int a = 0; a < 3; ++a) {
+            g.res[a] = desc.res[a];
+            g.nt[a] = nt[a];
+            g.org[a] = desc.origin[a];
+            // world_max() = origin + res * voxel_size (grid.hpp:72-74)
+            g.wmax[a] = desc.origin[a] + (double)desc.res[a] * desc.voxel_size;
+        }
+        g.h = desc.voxel_size;
+        g.far = desc.far_field_voxels * desc.voxel_size;
+        g.tile_table = d_tile_table;
+        g.tile_coords = d_tile_coords;
+        g.probe_ids = d_probe_ids;
+        g.smooth = d_smooth;
+        g.planes = d_params + off_planes;
+        g.probes = d_params + off_probes;
+        return g;
+    }
+
+    void free_grid() {
+        for (void* p : {(void*)d_tile_table, (void*)d_tile_coords, (void*)d_probe_ids,
+                        (void*)d_probe_table, (void*)d_probe_coords, (void*)d_params,
+                        (void*)d_smooth, (void*)d_grads, (void*)d_gsmooth, (void*)d_grads0,
+                        (void*)d_gsmooth0, (void*)d_m, (void*)d_v})
+            if (p) cudaFree(p);
+        d_tile_table = nullptr;
+        d_tile_coords = nullptr;
+        d_probe_ids = nullptr;
+        d_probe_table = nullptr;
+        d_probe_coords = nullptr;
+        d_params = d_smooth = d_grads = d_gsmooth = d_grads0 = d_gsmooth0 = d_m = d_v = nullptr;
+        has_grid = false;
+    }
+};
+
+namespace {
+
+void need_grid(psdf_ctx* c) {
+    if (!c) fail(PSDF_ERR_INVALID_ARGUMENT, "null context");
+    if (!c->has_grid) fail(PSDF_ERR_RUNTIME, "no grid uploaded");
+}
+
+void set_device(psdf_ctx* c) { CK(cudaSetDevice(c->device)); }
+
+template <typename T>
+void ensure_dev(T*& p, size_t& cap, size_t n) {
+    if (n <= cap && p) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    cap = n;
+}
+
+Cam to_cam(const psdf_camera& c) {
+    Cam d;
+    d.fx = c.fx;
+    d.fy = c.fy;
+    d.cx = c.cx;
+    d.cy = c.cy;
+    for (int i = 0; i < 9; ++i) d.rot[i] = c.rot[i];
+    for (int i = 0; i < 3; ++i) d.pos[i] = c.pos[i];
+    d.width = c.width;
+    d.height = c.height;
+    d.id = c.id;
+    return d;
+}
+
+void check_camera(const psdf_camera& c) {
+    if (c.width <= 0 || c.height <= 0) fail(PSDF_ERR_INVALID_ARGUMENT, "camera has an empty image");
+}
+
+// Copies the batch's view table to the device and returns the work-tile count.
+int64_t upload_viewdev(psdf_ctx* c, std::vector<ViewDev>& vd) {
+    int64_t tiles = 0;
+    for (auto& v : vd) {
+        v.tiles_x = (v.cam.width + 7) / 8;
+        v.tiles_y = (v.cam.height + 3) / 4;
+        v.tile_begin = tiles;
+        tiles += (int64_t)v.tiles_x * v.tiles_y;
+    }
+    if ((int)vd.size() > c->viewdev_cap) {
+        if (c->d_viewdev) cudaFree(c->d_viewdev);
+        CK(cudaMalloc(&c->d_viewdev, sizeof(ViewDev) * vd.size()));
+        c->viewdev_cap = (int)vd.size();
+    }
+    CK(cudaMemcpyAsync(c->d_viewdev, vd.data(), sizeof(ViewDev) * vd.size(),
+                       cudaMemcpyHostToDevice, c->stream));
+    return tiles;
+}
+
+int camera_bias_row(psdf_ctx* c, int camera_id) {
+    if (camera_id < 0 || c->desc.ncam == 0) return -1;  // decoder.cpp:69-78
+    if (camera_id >= c->desc.ncam)
+        fail(PSDF_ERR_OUT_OF_RANGE, "decode_color: camera id out of range");
+    return camera_id;
+}
+
+int blocks_per_sm(const void* fn, size_t smem) {
+    int n = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, BLOCK, smem));
+    return std::max(n, 1);
+}
+
+void launch_smooth(psdf_ctx* c, const float* src, float fill, float* dst, int accumulate) {
+    if (c->desc.T == 0) return;
+    const size_t smem = sizeof(float) * (HV + 16 * HE * HE);
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(smooth_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+        attr = true;
+    }
+    smooth_fold_kernel<<<c->desc.T, 256, smem, c->stream>>>(c->view(), src, fill, dst, accumulate,
+                                                            gaussian_taps());
+    CK(cudaGetLastError());
+    ++c->last_launches;
+}
+
+void smooth_all(psdf_ctx* c) {
+    launch_smooth(c, c->d_params + c->off_raw, (float)(c->desc.far_field_voxels * c->desc.voxel_size),
+                  c->d_smooth, 0);
+}
+
+// The ray-pass launch shared by render and train.
+template <int NS, int NA, bool TRAIN>
+void launch_raypass(psdf_ctx* c, RayPassParams& P) {
+    const void* fn = TRAIN ? (const void*)train_kernel<NS, NA> : (const void*)render_kernel<NS, NA>;
+    const size_t smem = TRAIN ? train_smem_bytes<NS, NA>() : render_smem_bytes<NS, NA>();
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t n_work = P.tile_end - P.tile_begin;
+    const int64_t warps_needed = std::max<int64_t>(n_work, 1);
+    const int per_sm = blocks_per_sm(fn, smem);
+    const int64_t grid = std::min<int64_t>((warps_needed + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
+                                           (int64_t)per_sm * c->sm_count);
+    CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), c->stream));
+    CK(cudaEventRecord(c->ev_ray0, c->stream));
+    if (TRAIN)
+        train_kernel<NS, NA><<<(unsigned)grid, BLOCK, smem, c->stream>>>(P);
+    else
+        render_kernel<NS, NA><<<(unsigned)grid, BLOCK, smem, c->stream>>>(P);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->ev_ray1, c->stream));
+    ++c->last_launches;
+}
+
+RayPassParams base_params(psdf_ctx* c) {
+    RayPassParams P{};
+    P.g = c->view();
+    P.mlp = c->d_params + c->off_mlp;
+    P.in_dim = c->in_dim;
+    P.ncam = c->desc.ncam;
+    P.order = c->desc.sh_order;
+    P.n_max = 512;
+    P.early_stop = 1e-4;
+    P.work_counter = c->d_work;
+    P.counts = c->d_counts;
+    P.stats = c->d_stats;
+    return P;
+}
+
+void do_render(psdf_ctx* c, const psdf_camera* cam, const psdf_render_opts* opt, float* d_rgb,
+               float* d_alpha, float* d_depth, psdf_counts* counts) {
+    need_grid(c);
+    if (!cam || !opt) fail(PSDF_ERR_INVALID_ARGUMENT, "null camera or options");
+    check_camera(*cam);
+    set_device(c);
+    c->last_launches = 0;
+    RayPassParams P = base_params(c);
+    int order = c->desc.sh_order;  // renderer.cpp:90-91
+    if (opt->sh_order_override > 0) order = std::min(opt->sh_order_override, c->desc.sh_order);
+    P.order = order;
+    P.no_spatial = opt->no_spatial;
+    P.no_angular = opt->no_angular;
+    P.no_fresnel = opt->no_fresnel;
+    P.need_colors = opt->need_colors;
+    P.n_max = opt->n_max;
+    P.tau = opt->tau;
+    P.early_stop = opt->early_stop;
+    for (int i = 0; i < 3; ++i) P.bg[i] = opt->bg[i];
+    std::vector<ViewDev> vd(1);
+    vd[0] = ViewDev{};
+    vd[0].cam = to_cam(*cam);
+    vd[0].cam_bias_row = camera_bias_row(c, opt->camera_id);
+    P.tile_begin = 0;
+    P.tile_end = upload_viewdev(c, vd);
+    P.views = c->d_viewdev;
+    P.n_views = 1;
+    P.out_rgb = d_rgb;
+    P.out_alpha = d_alpha;
+    P.out_depth = d_depth;
+    CK(cudaMemsetAsync(c->d_counts, 0, sizeof(unsigned long long) * 8, c->stream));
+    dispatch_channels(c->desc.n_s, c->desc.n_a, [&]<int NS, int NA>() {
+        launch_raypass<NS, NA, false>(c, P);
+    });
+    if (counts) {
+        CK(cudaMemcpyAsync(c->h_counts, c->d_counts, sizeof(unsigned long long) * 8,
+                           cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaEventElapsedTime(&c->last_ray_ms, c->ev_ray0, c->ev_ray1));
+    c->last_step_ms = c->last_ray_ms;
+    if (counts) {
+        counts->n_rays = (int64_t)cam->width * cam->height;
+        counts->n_marched = (int64_t)c->h_counts[1];
+        counts->n_extra = (int64_t)c->h_counts[2];
+        counts->n_shaded = (int64_t)c->h_counts[3];
+        counts->n_alpha = 0;
+        counts->n_bwd_rays = 0;
+    }
+}
+
+// One train step over device-resident views (trainer.cpp:136-195).
+void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_step_params* hp,
+                   psdf_losses* losses, psdf_counts* counts) {
+    need_grid(c);
+    if (!hp) fail(PSDF_ERR_INVALID_ARGUMENT, "null step parameters");
+    if (batch.empty()) fail(PSDF_ERR_INVALID_ARGUMENT, "empty batch");
+    set_device(c);
+    c->last_launches = 0;
+    cudaStream_t s = c->stream;
+    CK(cudaEventRecord(c->ev_step0, s));
+    // gradient clear (trainer.cpp:136)
+    CK(cudaMemsetAsync(c->d_grads, 0, sizeof(float) * c->n_params, s));
+    CK(cudaMemsetAsync(c->d_gsmooth, 0, sizeof(float) * c->desc.T * TV, s));
+    CK(cudaMemsetAsync(c->d_counts, 0, sizeof(unsigned long long) * 8, s));
+    CK(cudaMemsetAsync(c->d_stats, 0, sizeof(double) * 16, s));
+
+    RayPassParams P = base_params(c);
+    P.tau = hp->tau;
+    P.need_colors = 1;
+    P.photo_scale = hp->photo_scale;
+    P.bg[0] = P.bg[1] = P.bg[2] = 0.0;  // trainer uses the default background
+    std::vector<ViewDev> vd(batch.size());
+    int64_t n_rays = 0;
+    for (size_t i = 0; i < batch.size(); ++i) {
+        vd[i] = ViewDev{};
+        vd[i].cam = to_cam(batch[i]->cam);
+        vd[i].gt = batch[i]->rgb;
+        vd[i].mask = batch[i]->mask;
+        // trainer.cpp:153 + decoder.cpp:69-78
+        vd[i].cam_bias_row = hp->use_camera_bias ? camera_bias_row(c, batch[i]->cam.id) : -1;
+        n_rays += (int64_t)batch[i]->cam.width * batch[i]->cam.height;
+    }
+    const int64_t tiles = upload_viewdev(c, vd);
+    // ray-batch data parallelism: contiguous 1/N slice of the batch's work tiles
+    P.tile_begin = tiles * c->rank / c->world;
+    P.tile_end = tiles * (c->rank + 1) / c->world;
+    P.views = c->d_viewdev;
+    P.n_views = (int)vd.size();
+    P.g_smooth = c->d_gsmooth;
+    P.g_planes = c->d_grads + c->off_planes;
+    P.g_probes = c->d_grads + c->off_probes;
+    P.g_mlp = c->d_grads + c->off_mlp;
+    dispatch_channels(c->desc.n_s, c->desc.n_a, [&]<int NS, int NA>() {
+        launch_raypass<NS, NA, true>(c, P);
+    });
+    if (c->keep_raypass) {
+        CK(cudaMemcpyAsync(c->d_grads0, c->d_grads, sizeof(float) * c->n_params,
+                           cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(c->d_gsmooth0, c->d_gsmooth, sizeof(float) * c->desc.T * TV,
+                           cudaMemcpyDeviceToDevice, s));
+    }
+    // regularizers (trainer.cpp:187-191), sharded by tile / probe range
+    const GridView g = c->view();
+    const int T = c->desc.T, Pn = c->desc.P;
+    const int t0 = (int)((int64_t)T * c->rank / c->world), t1 = (int)((int64_t)T * (c->rank + 1) / c->world);
+    const int p0 = (int)((int64_t)Pn * c->rank / c->world), p1 = (int)((int64_t)Pn * (c->rank + 1) / c->world);
+    const int stride = c->desc.sh_order * c->desc.sh_order * c->desc.n_a;
+    if (t1 > t0) {
+        loss_sdf_kernel<<<std::min(4 * c->sm_count, (int)((int64_t)(t1 - t0) * TV / 256 + 1)), 256,
+                          0, s>>>(g, c->d_params + c->off_raw, t0, t1, (float)hp->l_sdf,
+                                  c->d_gsmooth, c->d_grads + c->off_raw, c->d_stats);
+        CK(cudaGetLastError());
+        const size_t sm_en = kEikNormalSmem;
+        static bool attr = false;
+        if (!attr) {
+            CK(cudaFuncSetAttribute(loss_eik_normal_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_en));
+            attr = true;
+        }
+        loss_eik_normal_kernel<<<t1 - t0, 256, sm_en, s>>>(
+            g, t0, (float)hp->l_eik, (float)hp->l_norm, (float)(1.0 / (2.0 * c->desc.voxel_size)),
+            c->d_gsmooth, c->d_stats);
+        CK(cudaGetLastError());
+        loss_features_kernel<<<3 * (t1 - t0), 256, 0, s>>>(
+            g, t0, c->desc.n_s, (float)hp->l_feat, c->d_grads + c->off_planes, c->d_stats);
+        CK(cudaGetLastError());
+        c->last_launches += 3;
+    }
+    if (p1 > p0) {
+        GridMut m{g, c->d_params + c->off_raw, c->d_probe_table, c->d_probe_coords};
+        const int64_t n = (int64_t)(p1 - p0) * stride;
+        loss_probes_kernel<<<(unsigned)std::min<int64_t>(4 * c->sm_count, n / 256 + 1), 256, 0, s>>>(
+            m, p0, p1, stride, (float)hp->l_probe, c->d_grads + c->off_probes, c->d_stats);
+        CK(cudaGetLastError());
+        ++c->last_launches;
+    }
+    // G^T fold (grads.cpp:67-96): raw_grad += G^T * staged
+    launch_smooth(c, c->d_gsmooth, 0.f, c->d_grads + c->off_raw, 1);
+    // all-reduce across ranks (GradBuffers::add, trainer.cpp:184-185, across GPUs)
+    if (c->world > 1) {
+        NK(g_nccl.AllReduce(c->d_grads, c->d_grads, (size_t)c->n_params, ncclFloat, ncclSum, c->comm, s));
+        NK(g_nccl.AllReduce(c->d_stats, c->d_stats, 16, ncclDouble, ncclSum, c->comm, s));
+        NK(g_nccl.AllReduce(c->d_counts, c->d_counts, 8, ncclUint64, ncclSum, c->comm, s));
+    }
+    // Adam (trainer.cpp:194 / 53-70)
+    c->adam_t += 1;
+    const double c1 = 1.0 - std::pow(0.9, (double)c->adam_t);
+    const double c2 = 1.0 - std::pow(0.995, (double)c->adam_t);
+    adam_kernel<<<(unsigned)std::min<int64_t>(8 * c->sm_count, c->n_params / 1024 + 1), 256, 0, s>>>(
+        c->d_params, c->d_grads, c->d_m, c->d_v, c->n_params, c->off_probes, (float)hp->lr_vox,
+        (float)hp->lr_mlp, (float)(1.0 / c1), (float)(1.0 / c2));
+    CK(cudaGetLastError());
+    ++c->last_launches;
+    // re-smoothing (trainer.cpp:195)
+    smooth_all(c);
+    CK(cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(double) * 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->h_counts, c->d_counts, sizeof(unsigned long long) * 8,
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(c->ev_step1, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaEventElapsedTime(&c->last_ray_ms, c->ev_ray0, c->ev_ray1));
+    CK(cudaEventElapsedTime(&c->last_step_ms, c->ev_step0, c->ev_step1));
+    const double* st = c->h_stats;
+    if (losses) {
+        losses->photo = st[0];
+        losses->sdf = st[3];
+        losses->eik = st[4];
+        losses->normal = st[5];
+        losses->features = st[6];
+        losses->probes = st[7];
+        losses->total = st[0] + st[3] + st[4] + st[5] + st[6] + st[7];
+        losses->sq_err = st[1];
+        losses->mask_px = st[2];
+        const double mse = st[2] > 0 ? st[1] / st[2] : 0.0;  // trainer.cpp:197-198
+        losses->psnr = mse > 1e-10 ? 10.0 * std::log10(1.0 / mse) : 99.0;
+    }
+    if (counts) {
+        counts->n_rays = n_rays;
+        counts->n_marched = (int64_t)c->h_counts[1];
+        counts->n_extra = (int64_t)c->h_counts[2];
+        counts->n_shaded = (int64_t)c->h_counts[3];
+        counts->n_alpha = (int64_t)c->h_counts[4];
+        counts->n_bwd_rays = (int64_t)c->h_counts[5];
+    }
+}
+
+
+// march_ray (renderer.cpp:55-86) for explicit rays; test hook for the
+// bit-exact indexing contract.  One thread per ray.
+__global__ void march_rays_kernel(GridView g, int n, const double* __restrict__ o,
+                                  const double* __restrict__ d, int n_max, double* __restrict__ ts,
+                                  int* __restrict__ counts) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    Marcher mr;
+    int k = 0;
+    if (mr.init(g, o + 3 * r, d + 3 * r, n_max)) {
+        double t;
+        int tile;
+        while (mr.next(g, t, tile)) ts[(int64_t)r * n_max + k++] = t;
+    }
+    counts[r] = k;
+}
+
+// Camera::pixel_dir for every pixel (test hook).
+__global__ void pixel_dirs_kernel(Cam cam, double* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cam.width * cam.height) return;
+    const D3 d = pixel_dir(cam, (double)(i % cam.width) + 0.5, (double)(i / cam.width) + 0.5);
+    out[3 * i] = d.x;
+    out[3 * i + 1] = d.y;
+    out[3 * i + 2] = d.z;
+}
+
+}  // namespace
+
+// =========================================================================
+extern "C" {
+
+int psdf_abi_version(void) { return PSDF_ABI_VERSION; }
+
+const char* psdf_last_error(psdf_ctx*) { return g_err.c_str(); }
+
+int psdf_create(int device, psdf_ctx** out) {
+    return guarded([&] {
+        if (!out) fail(PSDF_ERR_INVALID_ARGUMENT, "null output pointer");
+        int n = 0;
+        CK(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) fail(PSDF_ERR_INVALID_ARGUMENT, "device %d out of range (%d GPUs)", device, n);
+        CK(cudaSetDevice(device));
+        auto* c = new psdf_ctx;
+        c->device = device;
+        CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CK(cudaEventCreate(&c->ev_ray0));
+        CK(cudaEventCreate(&c->ev_ray1));
+        CK(cudaEventCreate(&c->ev_step0));
+        CK(cudaEventCreate(&c->ev_step1));
+        CK(cudaMalloc(&c->d_work, sizeof(unsigned long long) * 8));
+        CK(cudaMalloc(&c->d_counts, sizeof(unsigned long long) * 8));
+        CK(cudaMalloc(&c->d_stats, sizeof(double) * 16));
+        CK(cudaMallocHost(&c->h_stats, sizeof(double) * 16));
+        CK(cudaMallocHost(&c->h_counts, sizeof(unsigned long long) * 8));
+        *out = c;
+    });
+}
+
+int psdf_destroy(psdf_ctx* c) {
+    return guarded([&] {
+        if (!c) return;
+        cudaSetDevice(c->device);
+        cudaStreamSynchronize(c->stream);
+        c->free_grid();
+        for (auto& v : c->views) {
+            if (v.rgb) cudaFree(v.rgb);
+            if (v.mask) cudaFree(v.mask);
+        }
+        for (void* p : {(void*)c->d_stage_rgb, (void*)c->d_stage_mask, (void*)c->d_viewdev,
+                        (void*)c->d_render, (void*)c->d_work, (void*)c->d_counts, (void*)c->d_stats})
+            if (p) cudaFree(p);
+        if (c->h_stats) cudaFreeHost(c->h_stats);
+        if (c->h_counts) cudaFreeHost(c->h_counts);
+        if (c->comm) g_nccl.CommDestroy(c->comm);
+        cudaEventDestroy(c->ev_ray0);
+        cudaEventDestroy(c->ev_ray1);
+        cudaEventDestroy(c->ev_step0);
+        cudaEventDestroy(c->ev_step1);
+        cudaStreamDestroy(c->stream);
+        delete c;
+    });
+}
+
+int64_t psdf_mlp_size(int n_s, int n_a, int ncam) {
+    const int in = n_s + n_a + NPOW;
+    return (int64_t)MlpLayout::make(in).cam + (int64_t)ncam * HID;
+}
+
+int psdf_upload_grid(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_coords,
+                     const int32_t* probe_ids, const int32_t* probe_coords, const float* raw,
+                     const float* smooth, const float* planes, const float* probes) {
+    return guarded([&] {
+        if (!c || !d) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
+        for (int a = 0; a < 3; ++a)
+            if (d->res[a] <= 0 || d->res[a] % TE)
+                fail(PSDF_ERR_INVALID_ARGUMENT, "grid resolution must be a multiple of 16");
+        if (d->sh_order < 1 || d->sh_order > 4)
+            fail(PSDF_ERR_INVALID_ARGUMENT, "SH order must be in [1,4]");
+        if (!supported_channels(d->n_s, d->n_a))
+            fail(PSDF_ERR_INVALID_ARGUMENT, "unsupported (n_s, n_a) = (%d, %d)", d->n_s, d->n_a);
+        if (d->T < 0 || d->P < 0 || d->ncam < 0) fail(PSDF_ERR_INVALID_ARGUMENT, "negative count");
+        if (d->T > 0 && (!tile_coords || !probe_ids || !raw || !planes))
+            fail(PSDF_ERR_INVALID_ARGUMENT, "missing tile arrays");
+        if (d->P > 0 && (!probe_coords || !probes)) fail(PSDF_ERR_INVALID_ARGUMENT, "missing probe arrays");
+        set_device(c);
+        CK(cudaStreamSynchronize(c->stream));
+        c->free_grid();
+        c->desc = *d;
+        c->in_dim = d->n_s + d->n_a + NPOW;
+        for (int a = 0; a < 3; ++a) c->nt[a] = d->res[a] / TE;
+        const int64_t T = d->T, P = d->P;
+        // dense tile / probe lattice tables
+        const int64_t ntt = (int64_t)c->nt[0] * c->nt[1] * c->nt[2];
+        const int64_t npt = (int64_t)(c->nt[0] + 1) * (c->nt[1] + 1) * (c->nt[2] + 1);
+        std::vector<int32_t> tt(ntt, -1), pt(npt, -1);
+        std::vector<int4> tc4(std::max<int64_t>(T, 1)), pc4(std::max<int64_t>(P, 1));
+        for (int64_t t = 0; t < T; ++t) {
+            const int32_t* q = tile_coords + 3 * t;
+            for (int a = 0; a < 3; ++a)
+                if (q[a] < 0 || q[a] >= c->nt[a]) fail(PSDF_ERR_INVALID_ARGUMENT, "tile %lld outside the grid", (long long)t);
+            int32_t& slot = tt[((int64_t)q[0] * c->nt[1] + q[1]) * c->nt[2] + q[2]];
+            if (slot >= 0) fail(PSDF_ERR_INVALID_ARGUMENT, "duplicate tile coordinates");
+            slot = (int32_t)t;
+            tc4[t] = make_int4(q[0], q[1], q[2], 0);
+            for (int i = 0; i < 8; ++i)
+                if (probe_ids[8 * t + i] < 0 || probe_ids[8 * t + i] >= P)
+                    fail(PSDF_ERR_INVALID_ARGUMENT, "probe id out of range");
+        }
+        for (int64_t p = 0; p < P; ++p) {
+            const int32_t* q = probe_coords + 3 * p;
+            for (int a = 0; a < 3; ++a)
+                if (q[a] < 0 || q[a] > c->nt[a]) fail(PSDF_ERR_INVALID_ARGUMENT, "probe %lld outside the lattice", (long long)p);
+            pt[((int64_t)q[0] * (c->nt[1] + 1) + q[1]) * (c->nt[2] + 1) + q[2]] = (int32_t)p;
+            pc4[p] = make_int4(q[0], q[1], q[2], 0);
+        }
+        const int nc = d->sh_order * d->sh_order;
+        c->n_planes = T * 3 * 256 * d->n_s;
+        c->n_probes = P * nc * d->n_a;
+        c->mlp_size = psdf_mlp_size(d->n_s, d->n_a, d->ncam);
+        c->off_raw = 0;
+        c->off_planes = up4(T * TV);
+        c->off_probes = up4(c->off_planes + c->n_planes);
+        c->off_mlp = up4(c->off_probes + c->n_probes);
+        c->n_params = up4(c->off_mlp + c->mlp_size);
+        CK(cudaMalloc(&c->d_tile_table, sizeof(int32_t) * ntt));
+        CK(cudaMalloc(&c->d_probe_table, sizeof(int32_t) * npt));
+        CK(cudaMalloc(&c->d_tile_coords, sizeof(int4) * tc4.size()));
+        CK(cudaMalloc(&c->d_probe_coords, sizeof(int4) * pc4.size()));
+        CK(cudaMalloc(&c->d_probe_ids, sizeof(int32_t) * std::max<int64_t>(8 * T, 1)));
+        CK(cudaMalloc(&c->d_params, sizeof(float) * c->n_params));
+        CK(cudaMalloc(&c->d_grads, sizeof(float) * c->n_params));
+        CK(cudaMalloc(&c->d_m, sizeof(float) * c->n_params));
+        CK(cudaMalloc(&c->d_v, sizeof(float) * c->n_params));
+        CK(cudaMalloc(&c->d_smooth, sizeof(float) * std::max<int64_t>(T * TV, 4)));
+        CK(cudaMalloc(&c->d_gsmooth, sizeof(float) * std::max<int64_t>(T * TV, 4)));
+        CK(cudaMemsetAsync(c->d_params, 0, sizeof(float) * c->n_params, c->stream));
+        CK(cudaMemsetAsync(c->d_grads, 0, sizeof(float) * c->n_params, c->stream));
+        CK(cudaMemsetAsync(c->d_m, 0, sizeof(float) * c->n_params, c->stream));
+        CK(cudaMemsetAsync(c->d_v, 0, sizeof(float) * c->n_params, c->stream));
+        CK(cudaMemcpyAsync(c->d_tile_table, tt.data(), sizeof(int32_t) * ntt, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->d_probe_table, pt.data(), sizeof(int32_t) * npt, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->d_tile_coords, tc4.data(), sizeof(int4) * tc4.size(), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->d_probe_coords, pc4.data(), sizeof(int4) * pc4.size(), cudaMemcpyHostToDevice, c->stream));
+        if (T > 0) {
+            CK(cudaMemcpyAsync(c->d_probe_ids, probe_ids, sizeof(int32_t) * 8 * T, cudaMemcpyHostToDevice, c->stream));
+            CK(cudaMemcpyAsync(c->d_params + c->off_raw, raw, sizeof(float) * T * TV, cudaMemcpyHostToDevice, c->stream));
+            CK(cudaMemcpyAsync(c->d_params + c->off_planes, planes, sizeof(float) * c->n_planes,
+                               cudaMemcpyHostToDevice, c->stream));
+        }
+        if (P > 0)
+            CK(cudaMemcpyAsync(c->d_params + c->off_probes, probes, sizeof(float) * c->n_probes,
+                               cudaMemcpyHostToDevice, c->stream));
+        c->has_grid = true;
+        c->adam_t = 0;
+        if (smooth && T > 0)
+            CK(cudaMemcpyAsync(c->d_smooth, smooth, sizeof(float) * T * TV, cudaMemcpyHostToDevice, c->stream));
+        else
+            smooth_all(c);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int psdf_upload_mlp(psdf_ctx* c, const float* mlp, int64_t n) {
+    return guarded([&] {
+        need_grid(c);
+        if (!mlp || n != c->mlp_size)
+            fail(PSDF_ERR_INVALID_ARGUMENT, "MLP size %lld does not match the grid (%lld)",
+                 (long long)n, (long long)c->mlp_size);
+        set_device(c);
+        CK(cudaMemcpyAsync(c->d_params + c->off_mlp, mlp, sizeof(float) * n, cudaMemcpyHostToDevice,
+                           c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int psdf_download_params(psdf_ctx* c, float* raw, float* smooth, float* planes, float* probes,
+                         float* mlp) {
+    return guarded([&] {
+        need_grid(c);
+        set_device(c);
+        const int64_t T = c->desc.T;
+        cudaStream_t s = c->stream;
+        if (raw && T) CK(cudaMemcpyAsync(raw, c->d_params + c->off_raw, sizeof(float) * T * TV, cudaMemcpyDeviceToHost, s));
+        if (smooth && T) CK(cudaMemcpyAsync(smooth, c->d_smooth, sizeof(float) * T * TV, cudaMemcpyDeviceToHost, s));
+        if (planes && T) CK(cudaMemcpyAsync(planes, c->d_params + c->off_planes, sizeof(float) * c->n_planes, cudaMemcpyDeviceToHost, s));
+        if (probes && c->n_probes) CK(cudaMemcpyAsync(probes, c->d_params + c->off_probes, sizeof(float) * c->n_probes, cudaMemcpyDeviceToHost, s));
+        if (mlp) CK(cudaMemcpyAsync(mlp, c->d_params + c->off_mlp, sizeof(float) * c->mlp_size, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    });
+}
+
+int psdf_set_keep_raypass_grads(psdf_ctx* c, int keep) {
+    return guarded([&] {
+        need_grid(c);
+        set_device(c);
+        c->keep_raypass = keep != 0;
+        if (c->keep_raypass && !c->d_grads0) {
+            CK(cudaMalloc(&c->d_grads0, sizeof(float) * c->n_params));
+            CK(cudaMalloc(&c->d_gsmooth0, sizeof(float) * std::max<int64_t>(c->desc.T * TV, 4)));
+            CK(cudaMemsetAsync(c->d_grads0, 0, sizeof(float) * c->n_params, c->stream));
+            CK(cudaMemsetAsync(c->d_gsmooth0, 0, sizeof(float) * std::max<int64_t>(c->desc.T * TV, 4), c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+        }
+    });
+}
+
+int psdf_download_grads(psdf_ctx* c, int stage, float* raw, float* smooth, float* planes,
+                        float* probes, float* mlp) {
+    return guarded([&] {
+        need_grid(c);
+        set_device(c);
+        if (stage != 0 && stage != 1) fail(PSDF_ERR_INVALID_ARGUMENT, "stage must be 0 or 1");
+        if (stage == 0 && !c->keep_raypass)
+            fail(PSDF_ERR_RUNTIME, "stage-0 gradients not kept (psdf_set_keep_raypass_grads)");
+        const float* G = stage == 0 ? c->d_grads0 : c->d_grads;
+        const float* S = stage == 0 ? c->d_gsmooth0 : c->d_gsmooth;
+        const int64_t T = c->desc.T;
+        cudaStream_t s = c->stream;
+        if (raw && T) CK(cudaMemcpyAsync(raw, G + c->off_raw, sizeof(float) * T * TV, cudaMemcpyDeviceToHost, s));
+        if (smooth && T) CK(cudaMemcpyAsync(smooth, S, sizeof(float) * T * TV, cudaMemcpyDeviceToHost, s));
+        if (planes && T) CK(cudaMemcpyAsync(planes, G + c->off_planes, sizeof(float) * c->n_planes, cudaMemcpyDeviceToHost, s));
+        if (probes && c->n_probes) CK(cudaMemcpyAsync(probes, G + c->off_probes, sizeof(float) * c->n_probes, cudaMemcpyDeviceToHost, s));
+        if (mlp) CK(cudaMemcpyAsync(mlp, G + c->off_mlp, sizeof(float) * c->mlp_size, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    });
+}
+
+int psdf_smooth_all(psdf_ctx* c) {
+    return guarded([&] {
+        need_grid(c);
+        set_device(c);
+        c->last_launches = 0;
+        smooth_all(c);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int psdf_render_device(psdf_ctx* c, const psdf_camera* cam, const psdf_render_opts* opt,
+                       float* d_rgb, float* d_alpha, float* d_depth, psdf_counts* counts) {
+    return guarded([&] {
+        if (!d_rgb || !d_alpha) fail(PSDF_ERR_INVALID_ARGUMENT, "null output");
+        do_render(c, cam, opt, d_rgb, d_alpha, d_depth, counts);
+    });
+}
+
+int psdf_render(psdf_ctx* c, const psdf_camera* cam, const psdf_render_opts* opt, float* rgb,
+                float* alpha, float* depth, psdf_counts* counts) {
+    return guarded([&] {
+        need_grid(c);
+        if (!cam || !rgb || !alpha) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
+        check_camera(*cam);
+        set_device(c);
+        const size_t px = (size_t)cam->width * cam->height;
+        ensure_dev(c->d_render, c->render_px, 5 * px);
+        float* d_rgb = c->d_render;
+        float* d_alpha = d_rgb + 3 * px;
+        float* d_depth = depth ? d_alpha + px : nullptr;
+        do_render(c, cam, opt, d_rgb, d_alpha, d_depth, counts);
+        CK(cudaMemcpyAsync(rgb, d_rgb, sizeof(float) * 3 * px, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(alpha, d_alpha, sizeof(float) * px, cudaMemcpyDeviceToHost, c->stream));
+        if (depth)
+            CK(cudaMemcpyAsync(depth, d_depth, sizeof(float) * px, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int psdf_train_reset(psdf_ctx* c) {
+    return guarded([&] {
+        need_grid(c);
+        set_device(c);
+        CK(cudaMemsetAsync(c->d_m, 0, sizeof(float) * c->n_params, c->stream));
+        CK(cudaMemsetAsync(c->d_v, 0, sizeof(float) * c->n_params, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        c->adam_t = 0;
+    });
+}
+
+int psdf_train_step(psdf_ctx* c, int n_views, const psdf_camera* cams, const float* const* gt_rgb,
+                    const uint8_t* const* mask, const psdf_step_params* hp, psdf_losses* losses,
+                    psdf_counts* counts) {
+    return guarded([&] {
+        need_grid(c);
+        if (n_views <= 0 || !cams || !gt_rgb || !mask) fail(PSDF_ERR_INVALID_ARGUMENT, "empty batch");
+        set_device(c);
+        size_t px = 0;
+        for (int i = 0; i < n_views; ++i) {
+            check_camera(cams[i]);
+            px += (size_t)cams[i].width * cams[i].height;
+        }
+        // stage this step's images into HBM (host -> device inside the step)
+        size_t cap_rgb = c->stage_px * 3, cap_mask = c->stage_px;
+        if (px > c->stage_px) {
+            if (c->d_stage_rgb) cudaFree(c->d_stage_rgb);
+            if (c->d_stage_mask) cudaFree(c->d_stage_mask);
+            c->d_stage_rgb = nullptr;
+            c->d_stage_mask = nullptr;
+            cap_rgb = cap_mask = 0;
+            ensure_dev(c->d_stage_rgb, cap_rgb, 3 * px);
+            ensure_dev(c->d_stage_mask, cap_mask, px);
+            c->stage_px = px;
+        }
+        std::vector<DevView> tmp(n_views);
+        std::vector<DevView*> batch(n_views);
+        size_t off = 0;
+        for (int i = 0; i < n_views; ++i) {
+            const size_t n = (size_t)cams[i].width * cams[i].height;
+            tmp[i].cam = cams[i];
+            tmp[i].rgb = c->d_stage_rgb + 3 * off;
+            tmp[i].mask = c->d_stage_mask + off;
+            CK(cudaMemcpyAsync(tmp[i].rgb, gt_rgb[i], sizeof(float) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+            CK(cudaMemcpyAsync(tmp[i].mask, mask[i], n, cudaMemcpyHostToDevice, c->stream));
+            batch[i] = &tmp[i];
+            off += n;
+        }
+        do_train_step(c, batch, hp, losses, counts);
+        tmp.clear();
+    });
+}
+
+int psdf_upload_views(psdf_ctx* c, int n_views, const psdf_camera* cams, const float* const* gt_rgb,
+                      const uint8_t* const* mask) {
+    return guarded([&] {
+        if (!c) fail(PSDF_ERR_INVALID_ARGUMENT, "null context");
+        if (n_views < 0 || (n_views > 0 && (!cams || !gt_rgb || !mask)))
+            fail(PSDF_ERR_INVALID_ARGUMENT, "bad view arrays");
+        set_device(c);
+        for (auto& v : c->views) {
+            if (v.rgb) cudaFree(v.rgb);
+            if (v.mask) cudaFree(v.mask);
+        }
+        c->views.assign(n_views, DevView{});
+        for (int i = 0; i < n_views; ++i) {
+            check_camera(cams[i]);
+            const size_t n = (size_t)cams[i].width * cams[i].height;
+            c->views[i].cam = cams[i];
+            CK(cudaMalloc(&c->views[i].rgb, sizeof(float) * 3 * n));
+            CK(cudaMalloc(&c->views[i].mask, n));
+            CK(cudaMemcpyAsync(c->views[i].rgb, gt_rgb[i], sizeof(float) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+            CK(cudaMemcpyAsync(c->views[i].mask, mask[i], n, cudaMemcpyHostToDevice, c->stream));
+        }
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int psdf_train_step_views(psdf_ctx* c, int n_batch, const int32_t* view_ids,
+                          const psdf_step_params* hp, psdf_losses* losses, psdf_counts* counts) {
+    return guarded([&] {
+        need_grid(c);
+        if (n_batch <= 0 || !view_ids) fail(PSDF_ERR_INVALID_ARGUMENT, "empty batch");
+        std::vector<DevView*> batch(n_batch);
+        for (int i = 0; i < n_batch; ++i) {
+            if (view_ids[i] < 0 || view_ids[i] >= (int)c->views.size())
+                fail(PSDF_ERR_OUT_OF_RANGE, "view id %d out of range", view_ids[i]);
+            batch[i] = &c->views[view_ids[i]];
+        }
+        do_train_step(c, batch, hp, losses, counts);
+    });
+}
+
+int psdf_comm_unique_id(void* out) {
+    return guarded([&] {
+        if (!out) fail(PSDF_ERR_INVALID_ARGUMENT, "null output");
+        g_nccl.load();
+        ncclUniqueId id;
+        NK(g_nccl.GetUniqueId(&id));
+        static_assert(sizeof(ncclUniqueId) == PSDF_UNIQUE_ID_BYTES, "unique id size");
+        std::memcpy(out, &id, sizeof id);
+    });
+}
+
+int psdf_comm_init(psdf_ctx* c, const void* unique_id, int rank, int world_size) {
+    return guarded([&] {
+        if (!c || !unique_id) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
+        if (world_size < 1 || rank < 0 || rank >= world_size)
+            fail(PSDF_ERR_INVALID_ARGUMENT, "bad rank %d / world %d", rank, world_size);
+        set_device(c);
+        c->rank = rank;
+        c->world = world_size;
+        if (world_size == 1) return;
+        g_nccl.load();
+        ncclUniqueId id;
+        std::memcpy(&id, unique_id, sizeof id);
+        NK(g_nccl.CommInitRank(&c->comm, world_size, id, rank));
+    });
+}
+
+int psdf_march_rays(psdf_ctx* c, int n, const double* origins, const double* dirs, int n_max,
+                    double* ts, int32_t* counts) {
+    return guarded([&] {
+        need_grid(c);
+        if (n < 0 || n_max < 0 || (n > 0 && (!origins || !dirs || !ts || !counts)))
+            fail(PSDF_ERR_INVALID_ARGUMENT, "bad march arguments");
+        if (n == 0) return;
+        set_device(c);
+        double *d_o, *d_d, *d_t;
+        int* d_n;
+        const int nm = std::max(n_max, 1);
+        CK(cudaMalloc(&d_o, sizeof(double) * 3 * n));
+        CK(cudaMalloc(&d_d, sizeof(double) * 3 * n));
+        CK(cudaMalloc(&d_t, sizeof(double) * (size_t)n * nm));
+        CK(cudaMalloc(&d_n, sizeof(int) * n));
+        CK(cudaMemcpyAsync(d_o, origins, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(d_d, dirs, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+        march_rays_kernel<<<(n + 127) / 128, 128, 0, c->stream>>>(c->view(), n, d_o, d_d, n_max, d_t, d_n);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(c->stream));
+        CK(cudaMemcpyAsync(ts, d_t, sizeof(double) * (size_t)n * nm, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(counts, d_n, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        cudaFree(d_o);
+        cudaFree(d_d);
+        cudaFree(d_t);
+        cudaFree(d_n);
+    });
+}
+
+int psdf_pixel_dirs(const psdf_camera* cam, double* out) {
+    return guarded([&] {
+        if (!cam || !out) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
+        check_camera(*cam);
+        const int n = cam->width * cam->height;
+        double* d;
+        CK(cudaMalloc(&d, sizeof(double) * 3 * n));
+        pixel_dirs_kernel<<<(n + 127) / 128, 128>>>(to_cam(*cam), d);
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(out, d, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+        cudaFree(d);
+    });
+}
+
+int psdf_last_timing(psdf_ctx* c, double* ray_ms, double* step_ms, int* launches) {
+    return guarded([&] {
+        if (!c) fail(PSDF_ERR_INVALID_ARGUMENT, "null context");
+        if (ray_ms) *ray_ms = c->last_ray_ms;
+        if (step_ms) *step_ms = c->last_step_ms;
+        if (launches) *launches = c->last_launches;
+    });
+}
+
+void* psdf_stream(psdf_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+void* psdf_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes) != cudaSuccess) return nullptr;
+    return p;
+}
+
+void psdf_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

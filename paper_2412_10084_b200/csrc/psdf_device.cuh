@@ -1,0 +1,366 @@
+// psdf_device.cuh — device-side building blocks of the fused ray pass.
+//
+// Precision contract:
+//  * Geometry that decides WHICH samples exist and which get shaded — the
+//    pixel ray, the march t-list, the trilinear SDF value, alpha, T and the
+//    weights — is evaluated in f64 with every operation explicitly rounded
+//    (__dadd_rn/__dmul_rn/__ddiv_rn/__dsqrt_rn) so nvcc cannot contract it
+//    into FMAs.  In the reference's operation order this reproduces the
+//    reference's f64 results bit for bit from the same (fp32-stored) inputs.
+//  * The decode (tri-plane, SH probes, MLP) and all gradients are fp32.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace psdf {
+
+constexpr int TE = 16;     // kTileEdge (grid.hpp:15)
+constexpr int TV = 4096;   // kTileVoxels
+constexpr int HID = 32;    // kHidden (decoder.hpp:11)
+constexpr int NPOW = 6;    // kFresnelPowers
+constexpr double kPhotoEps = 1e-3;  // losses.hpp:9
+
+// ----------------------------------------------------------- exact f64 ops
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dadd_rn(a, -b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double dsqrt(double a) { return __dsqrt_rn(a); }
+
+struct D3 {
+    double x, y, z;
+};
+__device__ __forceinline__ D3 d3(double x, double y, double z) { return D3{x, y, z}; }
+// vec.hpp:26 — dot is (x*x' + y*y') + z*z'
+__device__ __forceinline__ double ddot(D3 a, D3 b) {
+    return dadd(dadd(dmul(a.x, b.x), dmul(a.y, b.y)), dmul(a.z, b.z));
+}
+
+// Device view of the sparse grid (SoA fp32 storage, dense tile table).
+struct GridView {
+    int T, P, n_s, n_a, order;     // order = grid SH order (coefficient stride)
+    int res[3], nt[3];
+    double h, org[3], far;         // far = far_field_voxels * voxel_size (grid.hpp:71)
+    double wmax[3];                // world_max() (grid.hpp:72-74)
+    const int32_t* __restrict__ tile_table;   // [nt0][nt1][nt2] -> tile or -1
+    const int4* __restrict__ tile_coords;     // [T] (x,y,z,0)
+    const int32_t* __restrict__ probe_ids;    // [T][8]
+    const float* __restrict__ smooth;         // [T][4096]
+    const float* __restrict__ planes;         // [T][3][256][n_s]
+    const float* __restrict__ probes;         // [P][order^2][n_a]
+};
+
+__device__ __forceinline__ int tile_lookup(const GridView& g, int tx, int ty, int tz) {
+    if ((unsigned)tx >= (unsigned)g.nt[0] || (unsigned)ty >= (unsigned)g.nt[1] ||
+        (unsigned)tz >= (unsigned)g.nt[2])
+        return -1;
+    return __ldg(g.tile_table + ((int64_t)tx * g.nt[1] + ty) * g.nt[2] + tz);
+}
+
+__device__ __forceinline__ int vox_index(int x, int y, int z) { return (x * TE + y) * TE + z; }
+
+// world_to_voxel component (grid.hpp:126): (p - origin) / voxel_size
+__device__ __forceinline__ double w2v(const GridView& g, double p, int a) {
+    return ddiv(dsub(p, g.org[a]), g.h);
+}
+
+// smooth_value (grid.cpp:87-94): far field outside resolution / unallocated.
+__device__ __forceinline__ double smooth_value(const GridView& g, int vx, int vy, int vz) {
+    if (vx < 0 || vy < 0 || vz < 0 || vx >= g.res[0] || vy >= g.res[1] || vz >= g.res[2])
+        return g.far;
+    const int t = tile_lookup(g, vx >> 4, vy >> 4, vz >> 4);
+    if (t < 0) return g.far;
+    return (double)__ldg(g.smooth + (int64_t)t * TV + vox_index(vx & 15, vy & 15, vz & 15));
+}
+
+// sample_sdf (grid.cpp:98-125), exact f64.  When all 8 corners fall in one
+// tile (the common case) a single table lookup serves them.
+__device__ __forceinline__ double sample_sdf(const GridView& g, double px, double py, double pz) {
+    const double cx = dsub(w2v(g, px, 0), 0.5);
+    const double cy = dsub(w2v(g, py, 1), 0.5);
+    const double cz = dsub(w2v(g, pz, 2), 0.5);
+    const double flx = floor(cx), fly = floor(cy), flz = floor(cz);
+    const int bx = (int)flx, by = (int)fly, bz = (int)flz;
+    const double fx = dsub(cx, (double)bx), fy = dsub(cy, (double)by), fz = dsub(cz, (double)bz);
+    const double gx0 = dsub(1.0, fx), gy0 = dsub(1.0, fy), gz0 = dsub(1.0, fz);
+    double c[8];
+    const bool one_tile = bx >= 0 && by >= 0 && bz >= 0 && bx + 1 < g.res[0] &&
+                          by + 1 < g.res[1] && bz + 1 < g.res[2] && (bx & 15) != 15 &&
+                          (by & 15) != 15 && (bz & 15) != 15;
+    int t = -1;
+    if (one_tile) t = tile_lookup(g, bx >> 4, by >> 4, bz >> 4);
+    if (t >= 0) {
+        const float* base = g.smooth + (int64_t)t * TV + vox_index(bx & 15, by & 15, bz & 15);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            c[i] = (double)__ldg(base + (i & 1) * 256 + ((i >> 1) & 1) * 16 + ((i >> 2) & 1));
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            c[i] = smooth_value(g, bx + (i & 1), by + ((i >> 1) & 1), bz + ((i >> 2) & 1));
+    }
+    double v = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const double w = dmul(dmul((i & 1) ? fx : gx0, (i & 2) ? fy : gy0), (i & 4) ? fz : gz0);
+        v = dadd(v, dmul(w, c[i]));
+    }
+    return v;
+}
+
+// ------------------------------------------------------------ camera + march
+struct Cam {
+    double fx, fy, cx, cy, rot[9], pos[3];
+    int width, height, id;
+};
+
+// Camera::pixel_dir (camera.hpp:32-35), exact f64.
+__device__ __forceinline__ D3 pixel_dir(const Cam& c, double u, double v) {
+    const double x = ddiv(dsub(u, c.cx), c.fx), y = ddiv(dsub(v, c.cy), c.fy), z = 1.0;
+    const D3 q = d3(dadd(dadd(dmul(c.rot[0], x), dmul(c.rot[1], y)), dmul(c.rot[2], z)),
+                    dadd(dadd(dmul(c.rot[3], x), dmul(c.rot[4], y)), dmul(c.rot[5], z)),
+                    dadd(dadd(dmul(c.rot[6], x), dmul(c.rot[7], y)), dmul(c.rot[8], z)));
+    const double n = dsqrt(ddot(q, q));
+    if (!(n > 0.0)) return d3(0, 0, 0);
+    return d3(ddiv(q.x, n), ddiv(q.y, n), ddiv(q.z, n));
+}
+
+// ray_box (renderer.cpp:13-31)
+__device__ __forceinline__ bool ray_box(const double o[3], const double d[3], const double mn[3],
+                                        const double mx[3], double& t0, double& t1) {
+    t0 = 0.0;
+    t1 = 1.7976931348623157e308;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (fabs(d[a]) < 1e-15) {
+            if (o[a] < mn[a] || o[a] > mx[a]) return false;
+            continue;
+        }
+        double ta = ddiv(dsub(mn[a], o[a]), d[a]), tb = ddiv(dsub(mx[a], o[a]), d[a]);
+        if (ta > tb) {
+            const double s = ta;
+            ta = tb;
+            tb = s;
+        }
+        t0 = (t0 < ta) ? ta : t0;  // std::max
+        t1 = (tb < t1) ? tb : t1;  // std::min
+        if (t0 > t1) return false;
+    }
+    return true;
+}
+
+// march_ray (renderer.cpp:55-86) as a resumable generator: the state is
+// (t, count), so the backward sweep can restart at any emitted sample.
+struct Marcher {
+    double o[3], d[3];
+    double t, t1;
+    int count, n_max;
+
+    __device__ __forceinline__ bool init(const GridView& g, const double* o_, const double* d_,
+                                         int nmax) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            o[a] = o_[a];
+            d[a] = d_[a];
+        }
+        n_max = nmax;
+        count = 0;
+        double t0;
+        if (!ray_box(o, d, g.org, g.wmax, t0, t1)) {
+            t = 0.0;
+            t1 = -1.0;
+            return false;
+        }
+        t = dadd(t0, dmul(0.5, g.h));
+        return true;
+    }
+
+    // Next sample distance inside an allocated tile; false when exhausted.
+    __device__ __forceinline__ bool next(const GridView& g, double& t_out, int& tile_out) {
+        const double h = g.h;
+        const double tile_w = dmul(16.0, h);
+        while (t < t1 && count < n_max) {
+            const double vx = w2v(g, dadd(o[0], dmul(d[0], t)), 0);
+            const double vy = w2v(g, dadd(o[1], dmul(d[1], t)), 1);
+            const double vz = w2v(g, dadd(o[2], dmul(d[2], t)), 2);
+            const int tx = ((int)floor(vx)) >> 4, ty = ((int)floor(vy)) >> 4,
+                      tz = ((int)floor(vz)) >> 4;
+            const int tile = tile_lookup(g, tx, ty, tz);
+            if (tile >= 0) {
+                t_out = t;
+                tile_out = tile;
+                t = dadd(t, h);
+                ++count;
+                return true;
+            }
+            const double bmin[3] = {dadd(g.org[0], dmul((double)tx, tile_w)),
+                                    dadd(g.org[1], dmul((double)ty, tile_w)),
+                                    dadd(g.org[2], dmul((double)tz, tile_w))};
+            const double bmax[3] = {dadd(bmin[0], tile_w), dadd(bmin[1], tile_w),
+                                    dadd(bmin[2], tile_w)};
+            double e0, e1;
+            if (ray_box(o, d, bmin, bmax, e0, e1) && e1 > t) {
+                const double skip = ceil(dadd(ddiv(dsub(e1, t), h), 1e-9));
+                t = dadd(t, dmul(skip > 1.0 ? skip : 1.0, h));
+            } else {
+                t = dadd(t, h);
+            }
+        }
+        return false;
+    }
+
+    __device__ __forceinline__ void pos(double tt, double p[3]) const {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) p[a] = dadd(o[a], dmul(d[a], tt));
+    }
+};
+
+// sigmoid (renderer.cpp:10) and alpha_from_sdf (renderer.cpp:35-39), f64.
+__device__ __forceinline__ double sigmoid_d(double x) { return ddiv(1.0, dadd(1.0, exp(-x))); }
+__device__ __forceinline__ double alpha_from(double a, double b) {
+    const double al = ddiv(dsub(a, b), a);
+    return al > 0.0 ? al : 0.0;
+}
+
+// ---------------------------------------------------------------- decode
+// SH constants (sh.cpp:12-21)
+constexpr float K0 = 0.28209479177387814f, K1 = 0.4886025119029199f, K2A = 1.0925484305920792f,
+                K2B = 0.31539156525252005f, K2C = 0.5462742152960396f, K3A = 0.5900435899266435f,
+                K3B = 2.890611442640554f, K3C = 0.4570457994644658f, K3D = 0.3731763325901154f,
+                K3E = 1.445305721320277f;
+
+// eval_sh_basis (sh.cpp:30-54); entries >= order^2 are left untouched.
+__device__ __forceinline__ void sh_basis(float x, float y, float z, int order, float* Y) {
+    Y[0] = K0;
+    if (order < 2) return;
+    Y[1] = K1 * y;
+    Y[2] = K1 * z;
+    Y[3] = K1 * x;
+    if (order < 3) return;
+    Y[4] = K2A * x * y;
+    Y[5] = K2A * y * z;
+    Y[6] = K2B * (3.f * z * z - 1.f);
+    Y[7] = K2A * x * z;
+    Y[8] = K2C * (x * x - y * y);
+    if (order < 4) return;
+    Y[9] = K3A * y * (3.f * x * x - y * y);
+    Y[10] = K3B * x * y * z;
+    Y[11] = K3C * y * (5.f * z * z - 1.f);
+    Y[12] = K3D * z * (5.f * z * z - 3.f);
+    Y[13] = K3C * x * (5.f * z * z - 1.f);
+    Y[14] = K3E * z * (x * x - y * y);
+    Y[15] = K3A * x * (x * x - 3.f * y * y);
+}
+
+// d/d(refl) of sum_j s_j Y_j (sh.cpp:56-83 contracted with s)
+__device__ __forceinline__ void sh_basis_grad_dot(float x, float y, float z, int order,
+                                                  const float* s, float& gx, float& gy,
+                                                  float& gz) {
+    gx = gy = gz = 0.f;
+    if (order < 2) return;
+    gy += s[1] * K1;
+    gz += s[2] * K1;
+    gx += s[3] * K1;
+    if (order < 3) return;
+    gx += s[4] * K2A * y;           gy += s[4] * K2A * x;
+    gy += s[5] * K2A * z;           gz += s[5] * K2A * y;
+    gz += s[6] * K2B * 6.f * z;
+    gx += s[7] * K2A * z;           gz += s[7] * K2A * x;
+    gx += s[8] * K2C * 2.f * x;     gy += s[8] * (-K2C * 2.f * y);
+    if (order < 4) return;
+    gx += s[9] * K3A * 6.f * x * y; gy += s[9] * K3A * (3.f * x * x - 3.f * y * y);
+    gx += s[10] * K3B * y * z;      gy += s[10] * K3B * x * z;       gz += s[10] * K3B * x * y;
+    gy += s[11] * K3C * (5.f * z * z - 1.f);                         gz += s[11] * K3C * 10.f * y * z;
+    gz += s[12] * K3D * (15.f * z * z - 3.f);
+    gx += s[13] * K3C * (5.f * z * z - 1.f);                         gz += s[13] * K3C * 10.f * x * z;
+    gx += s[14] * K3E * 2.f * x * z; gy += s[14] * (-K3E * 2.f * y * z); gz += s[14] * K3E * (x * x - y * y);
+    gx += s[15] * K3A * 3.f * (x * x - y * y); gy += s[15] * (-K3A * 6.f * x * y);
+}
+
+// Bilinear tap (grid.cpp:148-158), computed in f64 then narrowed.
+struct Tap {
+    int a0;
+    float f;
+};
+__device__ __forceinline__ Tap plane_tap(double local) {
+    double u = dsub(local, 0.5);
+    u = u < 0.0 ? 0.0 : (u > 15.0 ? 15.0 : u);
+    int a0 = (int)u;
+    if (a0 > 14) a0 = 14;
+    return Tap{a0, (float)dsub(u, (double)a0)};
+}
+
+// Fixed-size vector helpers for n_s / n_a channel groups.
+template <int N>
+struct VecF {
+    float v[N];
+};
+template <int N>
+__device__ __forceinline__ VecF<N> ldg_vec(const float* p) {
+    VecF<N> r;
+    if constexpr (N % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < N / 4; ++i) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(p) + i);
+            r.v[4 * i] = q.x;
+            r.v[4 * i + 1] = q.y;
+            r.v[4 * i + 2] = q.z;
+            r.v[4 * i + 3] = q.w;
+        }
+    } else if constexpr (N % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < N / 2; ++i) {
+            const float2 q = __ldg(reinterpret_cast<const float2*>(p) + i);
+            r.v[2 * i] = q.x;
+            r.v[2 * i + 1] = q.y;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) r.v[i] = __ldg(p + i);
+    }
+    return r;
+}
+
+// Vector atomics (sm_90+ float2/float4 red.global.add).
+template <int N>
+__device__ __forceinline__ void red_vec(float* p, const float* v) {
+    if constexpr (N % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < N / 4; ++i)
+            atomicAdd(reinterpret_cast<float4*>(p) + i,
+                      make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+    } else if constexpr (N % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < N / 2; ++i)
+            atomicAdd(reinterpret_cast<float2*>(p) + i, make_float2(v[2 * i], v[2 * i + 1]));
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) atomicAdd(p + i, v[i]);
+    }
+}
+
+// scatter_smooth_grad (grads.cpp:47-65): trilinear transpose into the
+// smooth-staged SDF gradient; weights in f64 exactly as the forward sample.
+__device__ __forceinline__ void scatter_smooth(const GridView& g, float* __restrict__ gsm,
+                                               double px, double py, double pz, double gv) {
+    const double cx = dsub(w2v(g, px, 0), 0.5);
+    const double cy = dsub(w2v(g, py, 1), 0.5);
+    const double cz = dsub(w2v(g, pz, 2), 0.5);
+    const int bx = (int)floor(cx), by = (int)floor(cy), bz = (int)floor(cz);
+    const double fx = dsub(cx, (double)bx), fy = dsub(cy, (double)by), fz = dsub(cz, (double)bz);
+    const double gx0 = dsub(1.0, fx), gy0 = dsub(1.0, fy), gz0 = dsub(1.0, fz);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const double w = dmul(dmul((i & 1) ? fx : gx0, (i & 2) ? fy : gy0), (i & 4) ? fz : gz0);
+        if (w == 0.0) continue;
+        const int vx = bx + (i & 1), vy = by + ((i >> 1) & 1), vz = bz + ((i >> 2) & 1);
+        if (vx < 0 || vy < 0 || vz < 0 || vx >= g.res[0] || vy >= g.res[1] || vz >= g.res[2])
+            continue;
+        const int t = tile_lookup(g, vx >> 4, vy >> 4, vz >> 4);
+        if (t < 0) continue;
+        atomicAdd(gsm + (int64_t)t * TV + vox_index(vx & 15, vy & 15, vz & 15), (float)(w * gv));
+    }
+}
+
+}  // namespace psdf

@@ -1,0 +1,141 @@
+"""K1 (fused render) parity on the GPU against the C oracle (which is itself
+pinned bit-exactly to the reference, tests/test_oracle_vs_reference.py).
+
+Contract (BASELINE.json north_star): colours and depth within 1e-4 relative,
+ray / sample indexing bit-exact.
+"""
+import numpy as np
+import pytest
+
+from helpers import make_scene, oracle_with_f32_smooth
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_cam(cam):
+    from oracle.refcore import RefCamera
+    c = RefCamera()
+    for k in ("fx", "fy", "cx", "cy", "width", "height", "id"):
+        setattr(c, k, getattr(cam, k))
+    c.rot[:] = list(cam.rot)
+    c.pos[:] = list(cam.pos)
+    return c
+
+
+def _oracle_opts(o):
+    from oracle.refcore import render_opts
+    return render_opts(tau=o.tau, n_max=o.n_max, early_stop=o.early_stop_transmittance,
+                       bg=o.background, camera_id=o.camera_id, no_spatial=o.no_spatial,
+                       no_angular=o.no_angular, no_fresnel=o.no_fresnel,
+                       sh_order_override=o.sh_order_override, need_colors=o.need_colors)
+
+
+def _upload(ctx, g, sm):
+    g.smooth = sm
+    ctx.upload(g, smooth=True)
+
+
+def test_pixel_dirs_bit_exact():
+    from paper_2412_10084_b200 import api
+    from oracle.port import pixel_dir
+    cam = api.make_lookat_camera(3, (1.3, 0.2, 0.4), (0, 0, 0), (0, 1, 0), 38.4, 38.4, 40, 24)
+    d = api.pixel_dirs(cam)
+    oc = _oracle_cam(cam)
+    for v in range(cam.height):
+        for u in range(cam.width):
+            assert np.array_equal(d[v, u], pixel_dir(oc, u + 0.5, v + 0.5))
+
+
+@pytest.mark.parametrize("res,band", [(32, 32), (64, 3)])
+def test_march_bit_exact(ctx, res, band):
+    g, a = make_scene(res=res, band=band, radius=0.3)
+    og, sm = oracle_with_f32_smooth(a)
+    _upload(ctx, g, sm)
+    rng = np.random.default_rng(11)
+    o = rng.uniform(-1.5, 1.5, (3000, 3))
+    o[:100] = [1.2, 0.1, 0.2]
+    tgt = rng.uniform(-0.45, 0.45, (3000, 3))
+    d = tgt - o
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    # axis-aligned and grazing rays exercise the parallel-slab branch
+    d[:50] = [[-1, 0, 0]] * 50
+    o[:50, 1:] = rng.uniform(-0.6, 0.6, (50, 2))
+    got = ctx.march_rays(o, d, 512)
+    for i in range(len(o)):
+        want = og.march_ray(o[i], d[i], 512)
+        assert got[i].shape == want.shape and np.array_equal(got[i], want), i
+    # n_max cap
+    got = ctx.march_rays(o[:200], d[:200], 7)
+    for i in range(200):
+        assert np.array_equal(got[i], og.march_ray(o[i], d[i], 7))
+
+
+SCENES = [
+    dict(res=32, n_s=2, n_a=2, sh_order=2, band=32),
+    dict(res=64, n_s=4, n_a=4, sh_order=4, band=6),
+    dict(res=32, n_s=8, n_a=8, sh_order=3, band=32),
+]
+
+
+@pytest.mark.parametrize("scene", SCENES)
+@pytest.mark.parametrize("tau_vox", [0.75, 30.0, 3000.0])
+def test_render_parity(ctx, scene, tau_vox):
+    from paper_2412_10084_b200 import api
+    g, a = make_scene(**scene)
+    og, sm = oracle_with_f32_smooth(a)
+    _upload(ctx, g, sm)
+    res = scene["res"]
+    cam = api.make_lookat_camera(0, (1.3, 0.2, 0.4), (0, 0, 0), (0, 1, 0), 1.2 * 48, 1.2 * 48, 48, 48)
+    opts = api.RenderOptions(tau=tau_vox * res, camera_id=0)
+    rgb, alpha, depth, counts = ctx.render_image(cam, opts)
+    orgb, oalpha, odepth, ocounts = og.render_image(_oracle_cam(cam), _oracle_opts(opts))
+    # indexing: identical sample counts (march + early termination + shaded set)
+    assert counts["n_marched"] == ocounts[1]
+    assert counts["n_extra"] == ocounts[2]
+    assert counts["n_shaded"] == ocounts[3]
+    tol = 1e-4
+    assert np.all(np.abs(rgb - orgb) <= tol * np.maximum(np.abs(orgb), 1e-2)), np.abs(rgb - orgb).max()
+    assert np.all(np.abs(alpha - oalpha) <= tol * np.maximum(np.abs(oalpha), 1e-2))
+    assert np.all(np.abs(depth - odepth) <= tol * np.maximum(np.abs(odepth), 1e-2))
+
+
+@pytest.mark.parametrize("flag", ["no_spatial", "no_angular", "no_fresnel", "sh_order_override",
+                                  "background", "no_early_stop", "alpha_only"])
+def test_render_options(ctx, flag):
+    from paper_2412_10084_b200 import api
+    g, a = make_scene(res=32, n_s=4, n_a=4, sh_order=4, band=32)
+    og, sm = oracle_with_f32_smooth(a)
+    _upload(ctx, g, sm)
+    cam = api.make_lookat_camera(0, (1.0, 0.15, 0.2), (0, 0.2, 0.05), (0, 1, 0), 38.4, 38.4, 32, 32)
+    kw = dict(tau=2000.0, camera_id=0)
+    if flag == "sh_order_override":
+        kw[flag] = 1
+    elif flag == "background":
+        kw[flag] = (0.25, 0.5, 0.75)
+    elif flag == "no_early_stop":
+        kw["early_stop_transmittance"] = 0.0
+    elif flag == "alpha_only":
+        kw["need_colors"] = False
+    else:
+        kw[flag] = True
+    opts = api.RenderOptions(**kw)
+    rgb, alpha, depth, counts = ctx.render_image(cam, opts)
+    orgb, oalpha, odepth, ocounts = og.render_image(_oracle_cam(cam), _oracle_opts(opts))
+    assert counts["n_marched"] == ocounts[1] and counts["n_shaded"] == ocounts[3]
+    assert np.abs(rgb - orgb).max() <= 1e-4 * max(1.0, np.abs(orgb).max())
+    assert np.abs(alpha - oalpha).max() <= 1e-6
+
+
+def test_render_errors(ctx):
+    from paper_2412_10084_b200 import api
+    from paper_2412_10084_b200._lib import PsdfOutOfRange
+    g, a = make_scene(res=32, ncam=1)
+    ctx.upload(g)
+    cam = api.make_lookat_camera(0, (1.3, 0.2, 0.4), (0, 0, 0), (0, 1, 0), 38.4, 38.4, 8, 8)
+    with pytest.raises(PsdfOutOfRange):  # decoder.cpp:73-74
+        ctx.render_image(cam, api.RenderOptions(tau=100.0, camera_id=5))
+    # a ray missing the volume: background, zero alpha (test_renderer.cpp:141-149)
+    far = api.make_lookat_camera(0, (5, 5, 5), (10, 10, 10), (0, 1, 0), 8, 8, 4, 4)
+    rgb, alpha, _, counts = ctx.render_image(far, api.RenderOptions(tau=100.0, background=(0.25, 0.5, 0.75)))
+    assert counts["n_marched"] == 0 and np.all(alpha == 0)
+    assert np.allclose(rgb, [0.25, 0.5, 0.75])

@@ -1,0 +1,111 @@
+"""K2..K9 (one full train step) parity on the GPU against the C oracle.
+
+Contract (BASELINE.json north_star): grid gradients within 1e-3 relative (the
+GPU accumulates with non-deterministic fp32 atomics).  Metric (SURVEY.md hard
+part 6): per tensor ||d||_2 / ||g||_2 <= 1e-3 and element-wise
+|d| <= 1e-3 * max|g|.  Sample counts (marched, shaded, alpha > 0, backward
+rays) must match exactly.
+"""
+import numpy as np
+import pytest
+
+from helpers import make_scene, oracle_with_f32_smooth, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+GRAD_TOL = 1e-3
+
+
+def _views(og, cams, seed):
+    """GT = random colours, mask = oracle silhouette (alpha > 0.5) so both
+    in-mask (colour) and out-of-mask (opacity) supervision occur."""
+    from oracle.refcore import render_opts
+    rng = np.random.default_rng(seed)
+    gts, masks = [], []
+    for c in cams:
+        _, alpha, _, _ = og.render_image(c, render_opts(tau=3000.0 * 32))
+        masks.append((alpha > 0.5).astype(np.float64))
+        gts.append(rng.uniform(0, 1, (c.height, c.width, 3)).astype(np.float32).astype(np.float64))
+    return gts, masks
+
+
+def _check_grads(got, want, what):
+    for k in ("raw", "smooth", "planes", "probes", "mlp"):
+        g, w = got[k], want[k]
+        scale = np.abs(w).max()
+        if scale == 0:
+            assert np.abs(g).max() == 0, (what, k)
+            continue
+        assert rel_l2(g, w) <= GRAD_TOL, (what, k, rel_l2(g, w))
+        assert np.abs(g - w).max() <= GRAD_TOL * scale, (what, k, np.abs(g - w).max() / scale)
+
+
+CASES = [
+    dict(scene=dict(res=32, n_s=2, n_a=2, sh_order=2, band=32), tau=30.0, size=24, ncam=4, bias=True),
+    dict(scene=dict(res=64, n_s=4, n_a=4, sh_order=4, band=6), tau=30.0, size=32, ncam=0, bias=False),
+    dict(scene=dict(res=64, n_s=4, n_a=4, sh_order=3, band=6), tau=300.0, size=32, ncam=0, bias=False),
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_train_step_parity(ctx, case):
+    from paper_2412_10084_b200 import api
+    from oracle.port import step_params as ostep
+    from oracle.refcore import RefCamera
+    g, a = make_scene(ncam=case["ncam"], **case["scene"])
+    og, sm = oracle_with_f32_smooth(a)
+    g.smooth = sm
+    ctx.upload(g, smooth=True)
+    ctx.keep_raypass_grads(True)
+    ctx.train_reset()
+    og.train_reset()
+    res = case["scene"]["res"]
+    cams = api.make_ring_cameras(4, case["size"])
+    ocams = []
+    for c in cams:
+        oc = RefCamera()
+        for k in ("fx", "fy", "cx", "cy", "width", "height", "id"):
+            setattr(oc, k, getattr(c, k))
+        oc.rot[:] = list(c.rot)
+        oc.pos[:] = list(c.pos)
+        ocams.append(oc)
+    gts, masks = _views(og, ocams, 5)
+    kw = dict(tau=case["tau"] * res, lr_vox=5e-3 / 50, lr_mlp=3e-3 / 50, photo_scale=40.0 / 2,
+              use_camera_bias=case["bias"])
+    for step, batch in enumerate([[0, 1], [2, 3]]):
+        hp = api.step_params(**kw)
+        losses, counts = ctx.train_step([cams[i] for i in batch], [gts[i] for i in batch],
+                                        [masks[i] for i in batch], hp)
+        ol, oc = og.train_step([ocams[i] for i in batch], [gts[i] for i in batch],
+                               [masks[i] for i in batch], ostep(**kw))
+        assert [counts[k] for k in ("n_rays", "n_marched", "n_extra", "n_shaded", "n_alpha",
+                                    "n_bwd_rays")] == list(oc), (step, counts, oc)
+        for i, k in enumerate(("photo", "sdf", "eik", "normal", "features", "probes")):
+            assert abs(losses[k] - ol[i]) <= 1e-4 * max(abs(ol[i]), 1e-6), (k, losses[k], ol[i])
+        assert abs(losses["psnr"] - ol[7]) <= 1e-3
+        g0, g1 = og.last_grads
+        _check_grads(ctx.grads(0), g0, f"step{step} ray pass")
+        _check_grads(ctx.grads(1), g1, f"step{step} final")
+        # post-step parameters: Adam moves each entry by ~lr * sign(g) at t = 1,
+        # so compare where the oracle gradient is clearly non-zero.
+        p = ctx.download()
+        op = og.export()
+        for k in ("raw", "planes", "probes", "mlp"):
+            gk = g1[k]
+            sig = np.abs(gk) > 1e-4 * max(np.abs(gk).max(), 1e-30)
+            d = np.abs(p[k].astype(np.float64) - op[k])
+            assert d[sig].max(initial=0) <= 2e-3 * kw["lr_vox"] + 1e-6, (step, k, d[sig].max(initial=0))
+        assert np.abs(p["smooth"] - op["smooth"]).max() <= 1e-5, np.abs(p["smooth"] - op["smooth"]).max()
+        # re-sync the oracle onto the GPU's parameters so step 2 compares one
+        # step from identical state (isolates per-step error from drift)
+        b = a.copy()
+        b.raw, b.planes, b.probes, b.mlp = (p[k].astype(np.float64) for k in ("raw", "planes", "probes", "mlp"))
+        b.smooth = p["smooth"].astype(np.float64)
+        from oracle.port import OracleGrid
+        og2 = OracleGrid(b, smooth=True)
+        # carry Adam state: both sides have taken the same number of steps; the
+        # oracle's moments differ only at fp32 rounding, so transplanting the
+        # moments is not needed for a one-step comparison -> restart both.
+        og = og2
+        og.train_reset()
+        ctx.train_reset()
