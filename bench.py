@@ -295,6 +295,7 @@ def main():
     if args.profile:
         for it in range(2):
             print(ctx.train_step_views(batch_ids(args.warmup + it), hp))
+            print(ctx.last_timing(), ctx.last_k2_breakdown())
         print(render_fps(api, torch, ctx, 6455.3, frames=1))
         ctx.close()
         return
@@ -307,13 +308,14 @@ def main():
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     counts_tot = dict(n_rays=0, n_marched=0, n_extra=0, n_shaded=0, n_alpha=0, n_bwd_rays=0)
-    ray_ms, step_ms, launches = [], [], 0
+    ray_ms, step_ms, launches, k2_parts = [], [], 0, []
     bytes_tot = 0
     t_wall0 = time.time()
     ev0.record(stream)
     for it in range(args.steps):
         losses, counts = ctx.train_step_views(batch_ids(args.warmup + it), hp)
         r_ms, s_ms, n_l = ctx.last_timing()
+        k2_parts.append(ctx.last_k2_breakdown()[0])
         ray_ms.append(r_ms)
         step_ms.append(s_ms)
         launches += n_l
@@ -361,7 +363,11 @@ def main():
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "kernel": "train_kernel<4,4> (K2 fused ray pass)",
                 "algorithmic_bytes_per_launch": k2_bytes, "kernel_ms": k2_ms, "peak_source": peak_src,
-                "k2_share_of_step": k2_ms / statistics.mean(step_ms)}
+                "k2_share_of_step": k2_ms / statistics.mean(step_ms),
+                "k2_kernels_ms": dict(zip(["march_fwd", "shade_fwd", "alpha_bwd", "shade_bwd"],
+                                          [statistics.mean(p[k] for p in k2_parts) for k in range(4)])),
+                "note": "K2 = the four ray-pass kernels (psdf_train.cuh), timed together as one "
+                        "ray-pass unit; bytes per SURVEY 8(d)"}
 
     # e2e: the reference-facing C-ABI call with pinned host buffers; H2D of the
     # step's images and the D2H loss read inside the timed region (wall clock)

@@ -181,6 +181,9 @@ int psdf_comm_init(psdf_ctx* ctx, const void* unique_id, int rank, int world_siz
  * kernel), measured with CUDA events on the context's stream, and the number
  * of kernels the last call launched. */
 int psdf_last_timing(psdf_ctx* ctx, double* ray_kernel_ms, double* step_ms, int* launches);
+/* Device time (ms) of the four K2 kernels of the last train step (march_fwd,
+ * shade_fwd, alpha_bwd, shade_bwd) and the ray-entry / shading-record counts. */
+int psdf_last_k2_breakdown(psdf_ctx* ctx, double* ms4, int64_t* entries, int64_t* records);
 /* Raw CUDA stream of the context (cudaStream_t), for callers that time or
  * overlap work around the context. */
 void* psdf_stream(psdf_ctx* ctx);

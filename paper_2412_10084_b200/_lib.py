@@ -81,6 +81,7 @@ EXPORTS = [
     "psdf_train_reset", "psdf_train_step", "psdf_upload_views", "psdf_train_step_views",
     "psdf_comm_unique_id", "psdf_comm_init", "psdf_last_timing", "psdf_stream",
     "psdf_host_alloc", "psdf_host_free", "psdf_march_rays", "psdf_pixel_dirs",
+    "psdf_last_k2_breakdown",
 ]
 
 _lib = None
@@ -134,6 +135,7 @@ def load():
     _dp = C.POINTER(C.c_double)
     L.psdf_march_rays.argtypes = [vp, C.c_int, _dp, _dp, C.c_int, _dp, _ip]
     L.psdf_pixel_dirs.argtypes = [C.POINTER(psdf_camera), _dp]
+    L.psdf_last_k2_breakdown.argtypes = [vp, _dp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     _lib = L
     return L
 

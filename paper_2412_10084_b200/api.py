@@ -463,6 +463,14 @@ class Context:
                                            ts.ctypes.data_as(dp), _iptr(cnt)))
         return [ts[i, :cnt[i]].copy() for i in range(n)]
 
+    def last_k2_breakdown(self):
+        """Device ms of K2a/K2b/K2d/K2e of the last train step, and the number of
+        ray entries / shading records it produced."""
+        ms = (C.c_double * 4)()
+        ne, nr = C.c_int64(), C.c_int64()
+        self._check(self.L.psdf_last_k2_breakdown(self.h, ms, C.byref(ne), C.byref(nr)))
+        return list(ms), ne.value, nr.value
+
     def last_timing(self):
         r, s, n = C.c_double(), C.c_double(), C.c_int()
         self._check(self.L.psdf_last_timing(self.h, C.byref(r), C.byref(s), C.byref(n)))

@@ -25,6 +25,7 @@
 #include "../../include/psdf.h"
 #include "psdf_grid.cuh"
 #include "psdf_raypass.cuh"
+#include "psdf_train.cuh"
 
 using namespace psdf;
 
@@ -188,7 +189,14 @@ struct psdf_ctx {
     int rank = 0, world = 1;
 
     float last_ray_ms = 0.f, last_step_ms = 0.f;
+    float last_k2_ms[4] = {0.f, 0.f, 0.f, 0.f};  // K2a, K2b, K2d, K2e
     int last_launches = 0;
+    int64_t last_entries = 0, last_records = 0;
+    cudaEvent_t ev_k[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+
+    // wavefront buffers of the train ray pass (psdf_train.cuh)
+    WaveBufs wave{};
+    unsigned* h_wave_counters = nullptr;  // pinned [2]
 
     GridView view() const {
         GridView g{};
@@ -205,6 +213,9 @@ struct psdf_ctx {
             g.wmax[a] = desc.origin[a] + (double)desc.res[a] * desc.voxel_size;
         }
         g.h = desc.voxel_size;
+        int ex = 0;
+        g.h_pow2 = desc.voxel_size > 0.0 && std::frexp(desc.voxel_size, &ex) == 0.5;
+        g.inv_h = g.h_pow2 ? 1.0 / desc.voxel_size : 0.0;
         g.far = desc.far_field_voxels * desc.voxel_size;
         g.tile_table = d_tile_table;
         g.tile_coords = d_tile_coords;
@@ -319,11 +330,11 @@ void smooth_all(psdf_ctx* c) {
                   c->d_smooth, 0);
 }
 
-// The ray-pass launch shared by render and train.
-template <int NS, int NA, bool TRAIN>
-void launch_raypass(psdf_ctx* c, RayPassParams& P) {
-    const void* fn = TRAIN ? (const void*)train_kernel<NS, NA> : (const void*)render_kernel<NS, NA>;
-    const size_t smem = TRAIN ? train_smem_bytes<NS, NA>() : render_smem_bytes<NS, NA>();
+// K1 launch (render).
+template <int NS, int NA>
+void launch_render(psdf_ctx* c, RayPassParams& P) {
+    const void* fn = (const void*)render_kernel<NS, NA>;
+    const size_t smem = render_smem_bytes<NS, NA>();
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t n_work = P.tile_end - P.tile_begin;
     const int64_t warps_needed = std::max<int64_t>(n_work, 1);
@@ -332,13 +343,117 @@ void launch_raypass(psdf_ctx* c, RayPassParams& P) {
                                            (int64_t)per_sm * c->sm_count);
     CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), c->stream));
     CK(cudaEventRecord(c->ev_ray0, c->stream));
-    if (TRAIN)
-        train_kernel<NS, NA><<<(unsigned)grid, BLOCK, smem, c->stream>>>(P);
-    else
-        render_kernel<NS, NA><<<(unsigned)grid, BLOCK, smem, c->stream>>>(P);
+    render_kernel<NS, NA><<<(unsigned)grid, BLOCK, smem, c->stream>>>(P);
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev_ray1, c->stream));
     ++c->last_launches;
+}
+
+void free_wave(psdf_ctx* c) {
+    WaveBufs& W = c->wave;
+    for (void* p : {(void*)W.e_slot, (void*)W.e_dir, (void*)W.e_tfirst, (void*)W.e_cfirst,
+                    (void*)W.e_nlive, (void*)W.e_acc, (void*)W.e_head, (void*)W.e_craw,
+                    (void*)W.r_pos, (void*)W.r_w, (void*)W.r_tile, (void*)W.r_entry,
+                    (void*)W.r_next, (void*)W.r_c, (void*)W.r_up})
+        if (p) cudaFree(p);
+    unsigned* keep = W.counters;
+    W = WaveBufs{};
+    W.counters = keep;
+}
+
+// Grows the ray-entry / shading-record buffers (kept across steps).
+void ensure_wave(psdf_ctx* c, int64_t e_cap, int64_t r_cap) {
+    WaveBufs& W = c->wave;
+    if (e_cap <= W.e_cap && r_cap <= W.r_cap) return;
+    e_cap = std::max<int64_t>(e_cap, W.e_cap);
+    r_cap = std::max<int64_t>(r_cap, W.r_cap);
+    if (e_cap > INT32_MAX / 4 || r_cap > INT32_MAX / 4)
+        fail(PSDF_ERR_RUNTIME, "ray pass needs more than 2^29 entries / records");
+    CK(cudaStreamSynchronize(c->stream));
+    free_wave(c);
+    CK(cudaMalloc(&W.e_slot, sizeof(int) * e_cap));
+    CK(cudaMalloc(&W.e_dir, sizeof(double) * 3 * e_cap));
+    CK(cudaMalloc(&W.e_tfirst, sizeof(double) * e_cap));
+    CK(cudaMalloc(&W.e_cfirst, sizeof(int) * e_cap));
+    CK(cudaMalloc(&W.e_nlive, sizeof(int) * e_cap));
+    CK(cudaMalloc(&W.e_acc, sizeof(double) * e_cap));
+    CK(cudaMalloc(&W.e_head, sizeof(int) * e_cap));
+    CK(cudaMalloc(&W.e_craw, sizeof(double) * 3 * e_cap));
+    CK(cudaMalloc(&W.r_pos, sizeof(double) * 3 * r_cap));
+    CK(cudaMalloc(&W.r_w, sizeof(double) * r_cap));
+    CK(cudaMalloc(&W.r_tile, sizeof(int) * r_cap));
+    CK(cudaMalloc(&W.r_entry, sizeof(int) * r_cap));
+    CK(cudaMalloc(&W.r_next, sizeof(int) * r_cap));
+    CK(cudaMalloc(&W.r_c, sizeof(float4) * r_cap));
+    CK(cudaMalloc(&W.r_up, sizeof(float4) * r_cap));
+    W.e_cap = (int)e_cap;
+    W.r_cap = (int)r_cap;
+}
+
+// K2 as the wavefront pipeline K2a -> K2b -> K2d -> K2e (psdf_train.cuh).
+template <int NS, int NA>
+void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
+    cudaStream_t s = c->stream;
+    const int64_t n_work = P.tile_end - P.tile_begin;
+    if (c->wave.e_cap == 0) ensure_wave(c, n_rays / 8 + 65536, n_rays / 8 + 65536);
+    const size_t smem_f = render_smem_bytes<NS, NA>();
+    const size_t smem_b = shade_bwd_smem_bytes<NS, NA>();
+    CK(cudaFuncSetAttribute(shade_fwd_kernel<NS, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
+    CK(cudaFuncSetAttribute(shade_bwd_kernel<NS, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
+    const int per_sm_a = blocks_per_sm((const void*)march_fwd_kernel, 0);
+    const int64_t grid_a = std::max<int64_t>(1, std::min<int64_t>((n_work + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
+                                                                   (int64_t)per_sm_a * c->sm_count));
+    CK(cudaEventRecord(c->ev_ray0, s));
+    CK(cudaEventRecord(c->ev_k[0], s));
+    for (int attempt = 0;; ++attempt) {
+        CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
+        CK(cudaMemsetAsync(c->wave.counters, 0, sizeof(unsigned) * 4, s));
+        P.work_counter = c->d_work;
+        march_fwd_kernel<<<(unsigned)grid_a, BLOCK, 0, s>>>(P, c->wave);
+        CK(cudaGetLastError());
+        ++c->last_launches;
+        CK(cudaMemcpyAsync(c->h_wave_counters, c->wave.counters, sizeof(unsigned) * 2,
+                           cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const int64_t ne = c->h_wave_counters[0], nr = c->h_wave_counters[1];
+        if (ne <= c->wave.e_cap && nr <= c->wave.r_cap) break;
+        if (attempt > 2) fail(PSDF_ERR_RUNTIME, "ray pass buffers failed to grow");
+        ensure_wave(c, ne + ne / 2 + 4096, nr + nr / 2 + 4096);
+        // the failed sweep already accumulated statistics: clear and redo
+        CK(cudaMemsetAsync(c->d_counts, 0, sizeof(unsigned long long) * 8, s));
+        CK(cudaMemsetAsync(c->d_stats, 0, sizeof(double) * 16, s));
+        CK(cudaEventRecord(c->ev_ray0, s));
+        CK(cudaEventRecord(c->ev_k[0], s));
+    }
+    const int n_ent = (int)c->h_wave_counters[0], n_rec = (int)c->h_wave_counters[1];
+    c->last_entries = n_ent;
+    c->last_records = n_rec;
+    CK(cudaEventRecord(c->ev_k[1], s));
+    if (n_rec > 0) {
+        const int per_sm = blocks_per_sm((const void*)shade_fwd_kernel<NS, NA>, smem_f);
+        const int grid = (int)std::min<int64_t>((n_rec + BLOCK - 1) / BLOCK, (int64_t)per_sm * c->sm_count);
+        shade_fwd_kernel<NS, NA><<<grid, BLOCK, smem_f, s>>>(P, c->wave, n_rec);
+        CK(cudaGetLastError());
+        ++c->last_launches;
+    }
+    CK(cudaEventRecord(c->ev_k[2], s));
+    if (n_ent > 0) {
+        const int per_sm = blocks_per_sm((const void*)alpha_bwd_kernel, 0);
+        const int grid = (int)std::min<int64_t>((n_ent + BLOCK - 1) / BLOCK, (int64_t)per_sm * c->sm_count);
+        alpha_bwd_kernel<<<grid, BLOCK, 0, s>>>(P, c->wave, n_ent);
+        CK(cudaGetLastError());
+        ++c->last_launches;
+    }
+    CK(cudaEventRecord(c->ev_k[3], s));
+    if (n_rec > 0) {
+        const int per_sm = blocks_per_sm((const void*)shade_bwd_kernel<NS, NA>, smem_b);
+        const int grid = (int)std::min<int64_t>((n_rec + BLOCK - 1) / BLOCK, (int64_t)per_sm * c->sm_count);
+        shade_bwd_kernel<NS, NA><<<grid, BLOCK, smem_b, s>>>(P, c->wave, n_rec);
+        CK(cudaGetLastError());
+        ++c->last_launches;
+    }
+    CK(cudaEventRecord(c->ev_k[4], s));
+    CK(cudaEventRecord(c->ev_ray1, s));
 }
 
 RayPassParams base_params(psdf_ctx* c) {
@@ -388,7 +503,7 @@ void do_render(psdf_ctx* c, const psdf_camera* cam, const psdf_render_opts* opt,
     P.out_depth = d_depth;
     CK(cudaMemsetAsync(c->d_counts, 0, sizeof(unsigned long long) * 8, c->stream));
     dispatch_channels(c->desc.n_s, c->desc.n_a, [&]<int NS, int NA>() {
-        launch_raypass<NS, NA, false>(c, P);
+        launch_render<NS, NA>(c, P);
     });
     if (counts) {
         CK(cudaMemcpyAsync(c->h_counts, c->d_counts, sizeof(unsigned long long) * 8,
@@ -450,7 +565,7 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
     P.g_probes = c->d_grads + c->off_probes;
     P.g_mlp = c->d_grads + c->off_mlp;
     dispatch_channels(c->desc.n_s, c->desc.n_a, [&]<int NS, int NA>() {
-        launch_raypass<NS, NA, true>(c, P);
+        launch_train_raypass<NS, NA>(c, P, n_rays);
     });
     if (c->keep_raypass) {
         CK(cudaMemcpyAsync(c->d_grads0, c->d_grads, sizeof(float) * c->n_params,
@@ -519,6 +634,7 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
     CK(cudaStreamSynchronize(s));
     CK(cudaEventElapsedTime(&c->last_ray_ms, c->ev_ray0, c->ev_ray1));
     CK(cudaEventElapsedTime(&c->last_step_ms, c->ev_step0, c->ev_step1));
+    for (int k = 0; k < 4; ++k) CK(cudaEventElapsedTime(&c->last_k2_ms[k], c->ev_k[k], c->ev_k[k + 1]));
     const double* st = c->h_stats;
     if (losses) {
         losses->photo = st[0];
@@ -600,6 +716,9 @@ int psdf_create(int device, psdf_ctx** out) {
         CK(cudaMalloc(&c->d_stats, sizeof(double) * 16));
         CK(cudaMallocHost(&c->h_stats, sizeof(double) * 16));
         CK(cudaMallocHost(&c->h_counts, sizeof(unsigned long long) * 8));
+        CK(cudaMallocHost(&c->h_wave_counters, sizeof(unsigned) * 4));
+        CK(cudaMalloc(&c->wave.counters, sizeof(unsigned) * 4));
+        for (auto& e : c->ev_k) CK(cudaEventCreate(&e));
         *out = c;
     });
 }
@@ -617,6 +736,10 @@ int psdf_destroy(psdf_ctx* c) {
         for (void* p : {(void*)c->d_stage_rgb, (void*)c->d_stage_mask, (void*)c->d_viewdev,
                         (void*)c->d_render, (void*)c->d_work, (void*)c->d_counts, (void*)c->d_stats})
             if (p) cudaFree(p);
+        free_wave(c);
+        if (c->wave.counters) cudaFree(c->wave.counters);
+        if (c->h_wave_counters) cudaFreeHost(c->h_wave_counters);
+        for (auto& e : c->ev_k) cudaEventDestroy(e);
         if (c->h_stats) cudaFreeHost(c->h_stats);
         if (c->h_counts) cudaFreeHost(c->h_counts);
         if (c->comm) g_nccl.CommDestroy(c->comm);
@@ -993,6 +1116,16 @@ int psdf_pixel_dirs(const psdf_camera* cam, double* out) {
         CK(cudaGetLastError());
         CK(cudaMemcpy(out, d, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
         cudaFree(d);
+    });
+}
+
+int psdf_last_k2_breakdown(psdf_ctx* c, double* ms4, int64_t* entries, int64_t* records) {
+    return guarded([&] {
+        if (!c) fail(PSDF_ERR_INVALID_ARGUMENT, "null context");
+        for (int k = 0; k < 4; ++k)
+            if (ms4) ms4[k] = c->last_k2_ms[k];
+        if (entries) *entries = c->last_entries;
+        if (records) *records = c->last_records;
     });
 }
 

@@ -42,6 +42,8 @@ struct GridView {
     int T, P, n_s, n_a, order;     // order = grid SH order (coefficient stride)
     int res[3], nt[3];
     double h, org[3], far;         // far = far_field_voxels * voxel_size (grid.hpp:71)
+    double inv_h;                  // 1 / h, used only when h is a power of two
+    int h_pow2;                    // x / h == x * inv_h exactly (power-of-two h)
     double wmax[3];                // world_max() (grid.hpp:72-74)
     const int32_t* __restrict__ tile_table;   // [nt0][nt1][nt2] -> tile or -1
     const int4* __restrict__ tile_coords;     // [T] (x,y,z,0)
@@ -60,9 +62,17 @@ __device__ __forceinline__ int tile_lookup(const GridView& g, int tx, int ty, in
 
 __device__ __forceinline__ int vox_index(int x, int y, int z) { return (x * TE + y) * TE + z; }
 
+// x / voxel_size.  For a power-of-two voxel size (every grid the reference
+// builds: 1/16 halved per LOD, grid.cpp:276) the reciprocal is exact and
+// x * (1/h) is the same correctly-rounded value as x / h, so the f64 software
+// division is skipped without changing a bit.
+__device__ __forceinline__ double div_h(const GridView& g, double x) {
+    return g.h_pow2 ? dmul(x, g.inv_h) : ddiv(x, g.h);
+}
+
 // world_to_voxel component (grid.hpp:126): (p - origin) / voxel_size
 __device__ __forceinline__ double w2v(const GridView& g, double p, int a) {
-    return ddiv(dsub(p, g.org[a]), g.h);
+    return div_h(g, dsub(p, g.org[a]));
 }
 
 // smooth_value (grid.cpp:87-94): far field outside resolution / unallocated.
@@ -201,7 +211,7 @@ struct Marcher {
                                     dadd(bmin[2], tile_w)};
             double e0, e1;
             if (ray_box(o, d, bmin, bmax, e0, e1) && e1 > t) {
-                const double skip = ceil(dadd(ddiv(dsub(e1, t), h), 1e-9));
+                const double skip = ceil(dadd(div_h(g, dsub(e1, t)), 1e-9));
                 t = dadd(t, dmul(skip > 1.0 ? skip : 1.0, h));
             } else {
                 t = dadd(t, h);
@@ -217,7 +227,8 @@ struct Marcher {
 };
 
 // sigmoid (renderer.cpp:10) and alpha_from_sdf (renderer.cpp:35-39), f64.
-__device__ __forceinline__ double sigmoid_d(double x) { return ddiv(1.0, dadd(1.0, exp(-x))); }
+// __drcp_rn is the correctly rounded reciprocal, i.e. the same value as 1.0/x.
+__device__ __forceinline__ double sigmoid_d(double x) { return __drcp_rn(dadd(1.0, exp(-x))); }
 __device__ __forceinline__ double alpha_from(double a, double b) {
     const double al = ddiv(dsub(a, b), a);
     return al > 0.0 ? al : 0.0;

@@ -2,10 +2,8 @@
 //
 //  K1 render_kernel : render_image -> render_ray -> decode_fused
 //                     (renderer.cpp:321-337, 149-210, 88-147)
-//  K2 train_kernel  : the ray pass of one train step (trainer.cpp:157-182):
-//                     render_ray + photo_pixel + render_ray_backward
-//                     (renderer.cpp:239-319) + scatter_smooth_grad
-//                     (grads.cpp:47-65), fused per ray.
+//  (K2, the train ray pass, is the wavefront pipeline in psdf_train.cuh; it
+//   shares decode_forward and the layouts below.)
 //
 // Work decomposition: one ray per lane; a warp owns an 8x4 pixel tile (so its
 // rays are coherent) and pulls tiles from a global work counter (rays vary
@@ -173,7 +171,10 @@ __device__ __forceinline__ void decode_forward(const RayPassParams& P, const flo
     const double szp = sample_sdf(g, p[0], p[1], dadd(p[2], h));
     const double szm = sample_sdf(g, p[0], p[1], dsub(p[2], h));
     const double h2 = dmul(2.0, h);
-    const D3 gv = d3(ddiv(dsub(sxp, sxm), h2), ddiv(dsub(syp, sym), h2), ddiv(dsub(szp, szm), h2));
+    // x / (2h): exact multiply for a power-of-two h (see div_h)
+    const double inv2h = g.h_pow2 ? dmul(0.5, g.inv_h) : 0.0;
+    auto div2h = [&](double x) { return g.h_pow2 ? dmul(x, inv2h) : ddiv(x, h2); };
+    const D3 gv = d3(div2h(dsub(sxp, sxm)), div2h(dsub(syp, sym)), div2h(dsub(szp, szm)));
     const double glen = dsqrt(ddot(gv, gv));
     geo.degenerate = glen < 1e-8;
     geo.glen = glen;
@@ -206,7 +207,7 @@ __device__ __forceinline__ void decode_forward(const RayPassParams& P, const flo
     geo.ty = plane_tap(ly);
     geo.tz = plane_tap(lz);
     {  // trilinear_weights(local/16) (sh.cpp:172-181)
-        const double fx = ddiv(lx, 16.0), fy = ddiv(ly, 16.0), fz = ddiv(lz, 16.0);
+        const double fx = dmul(lx, 0.0625), fy = dmul(ly, 0.0625), fz = dmul(lz, 0.0625);  // exact /16
 #pragma unroll
         for (int i = 0; i < 8; ++i)
             geo.w8[i] = (float)dmul(dmul((i & 1) ? fx : dsub(1.0, fx), (i & 2) ? fy : dsub(1.0, fy)),
@@ -443,575 +444,6 @@ __global__ void __launch_bounds__(BLOCK) render_kernel(RayPassParams P) {
     }
 }
 
-// ----------------------------------------------------------------------- K2
-// MLP-gradient partials go to a per-warp private accumulator in which every
-// entry has exactly one owner lane per stage, so plain read-modify-write is
-// race-free.  (Shared-memory f32 atomics compile to ATOMS.CAST.SPIN CAS loops
-// on sm_100a and were observed to double-count under cross-warp contention;
-// the kernels here use none.)
-#define ACC_ADD(so, go, v) (s_accw[(so)] += (v))
-template <int NS, int NA>
-__global__ void __launch_bounds__(BLOCK) train_kernel(RayPassParams P) {
-    constexpr int IN = NS + NA + NPOW;
-    using SD = ScratchDims<IN>;
-    using GA = GAccDims<IN>;
-    extern __shared__ __align__(16) float smem[];
-    const SmemMlp L = SmemMlp::make(IN);
-    const MlpLayout G = MlpLayout::make(IN);
-    float* s_mlp = smem;
-    float* s_acc = smem + L.total;  // [WARPS_PER_BLOCK][GA::TOTAL]
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* s_accw = s_acc + warp * GA::TOTAL;
-    float* scr = s_acc + WARPS_PER_BLOCK * GA::TOTAL + warp * SD::TOTAL;
-    float* A1 = scr + SD::A1;
-    float* A2 = scr + SD::A2;
-    float* X = scr + SD::X;
-    float* D3s = scr + SD::D3;
-    load_mlp_smem(P.mlp, s_mlp, G, L);
-    for (int i = threadIdx.x; i < WARPS_PER_BLOCK * GA::TOTAL; i += blockDim.x) s_acc[i] = 0.f;
-    __syncthreads();
-
-    const GridView& g = P.g;
-    const double tau = P.tau;
-    double st_photo = 0.0, st_sq = 0.0;
-    unsigned long long st_mask = 0, c_m = 0, c_x = 0, c_sh = 0, c_al = 0, c_bwd = 0;
-    const int n_work = (int)(P.tile_end - P.tile_begin);
-    for (;;) {
-        int wi = 0;
-        if (lane == 0) wi = (int)atomicAdd(P.work_counter, 1ull);
-        wi = __shfl_sync(FULL, wi, 0);
-        if (wi >= n_work) break;
-        const int64_t tile_id = P.tile_begin + wi;
-        const int vi = locate_view(P, tile_id);
-        const ViewDev& V = P.views[vi];
-        const int64_t lt = tile_id - V.tile_begin;
-        const int u = (int)(lt % V.tiles_x) * 8 + (lane & 7);
-        const int vv = (int)(lt / V.tiles_x) * 4 + (lane >> 3);
-        const bool valid = u < V.cam.width && vv < V.cam.height;
-        const float* cam_row = (P.ncam > 0 && V.cam_bias_row >= 0)
-                                   ? P.mlp + G.cam + V.cam_bias_row * HID
-                                   : nullptr;
-        float* gcam_row = cam_row ? P.g_mlp + G.cam + V.cam_bias_row * HID : nullptr;
-        const int64_t px = valid ? (int64_t)vv * V.cam.width + u : 0;
-        const bool in_mask = valid && __ldg(V.mask + px) != 0;
-
-        // ---------------- pass 1: forward (render_ray, renderer.cpp:149-210)
-        D3 dir = d3(0, 0, 0);
-        Marcher mr;
-        double c0 = 0.0, c1 = 0.0, c2 = 0.0, acc = 0.0, trans = 1.0;
-        double t_first = 0.0;
-        int cnt_first = -1, n_live = 0;
-        if (valid) {
-            dir = pixel_dir(V.cam, (double)u + 0.5, (double)vv + 0.5);
-            const double dd[3] = {dir.x, dir.y, dir.z};
-            const double dneg[3] = {-dir.x, -dir.y, -dir.z};
-            double t_cur = 0.0, s_cur, a_cur = 0.0;
-            int tile_cur = -1;
-            bool active = mr.init(g, V.cam.pos, dd, P.n_max) && mr.next(g, t_cur, tile_cur);
-            if (active) {
-                double pc[3];
-                mr.pos(t_cur, pc);
-                s_cur = sample_sdf(g, pc[0], pc[1], pc[2]);
-                a_cur = sigmoid_d(dmul(tau, s_cur));
-                ++c_x;
-            }
-            while (active) {
-                double t_nxt;
-                int tile_nxt;
-                const int idx = mr.count - 1;  // index of t_cur
-                const bool has_next = mr.next(g, t_nxt, tile_nxt);
-                double pn[3];
-                mr.pos(has_next ? t_nxt : dadd(t_cur, g.h), pn);
-                const double s_nxt = sample_sdf(g, pn[0], pn[1], pn[2]);
-                const double a_nxt = sigmoid_d(dmul(tau, s_nxt));
-                const double alpha = alpha_from(a_cur, a_nxt);
-                const double w = dmul(trans, alpha);
-                if (alpha > 0.0 && cnt_first < 0) {
-                    cnt_first = idx;
-                    t_first = t_cur;
-                }
-                if (in_mask && w > 0.0 && tile_cur >= 0) {
-                    double pc[3];
-                    mr.pos(t_cur, pc);
-                    float rgb[3];
-                    ShadeGeo geo;
-                    decode_forward<NS, NA>(P, s_mlp, L, tile_cur, pc, dneg, cam_row, rgb, geo,
-                                           nullptr, nullptr, nullptr);
-                    c0 = dadd(c0, dmul((double)rgb[0], w));
-                    c1 = dadd(c1, dmul((double)rgb[1], w));
-                    c2 = dadd(c2, dmul((double)rgb[2], w));
-                    ++c_sh;
-                }
-                acc = dadd(acc, w);
-                trans = dmul(trans, dsub(1.0, alpha));
-                ++n_live;
-                if ((P.early_stop > 0.0 && trans < P.early_stop) || !has_next) break;
-                t_cur = t_nxt;
-                tile_cur = tile_nxt;
-                a_cur = a_nxt;
-            }
-        }
-        c_m += n_live;
-
-        // ---------------- photometric term (losses.cpp:8-38)
-        double gx = 0.0, gy = 0.0, gz = 0.0, dA = 0.0;
-        bool need_bwd = false;
-        if (valid) {
-            const double om = dsub(1.0, acc);
-            const double col[3] = {dadd(c0, dmul(P.bg[0], om)), dadd(c1, dmul(P.bg[1], om)),
-                                   dadd(c2, dmul(P.bg[2], om))};
-            const float* gtp = V.gt + 3 * px;
-            const double scale = P.photo_scale;
-            if (in_mask) {
-                double gg[3];
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    const double gtk = (double)__ldg(gtp + k);
-                    const double d = dsub(col[k], gtk);
-                    const double wk = ddiv(1.0, dadd(col[k] > gtk ? col[k] : gtk, kPhotoEps));
-                    st_photo = dadd(st_photo, dmul(dmul(scale, d), d));
-                    st_sq = dadd(st_sq, dmul(d, d));
-                    gg[k] = dmul(dmul(dmul(scale, 2.0), wk), d);
-                }
-                gx = gg[0];
-                gy = gg[1];
-                gz = gg[2];
-                st_mask += 3;
-            } else {
-                const double am = acc > 0.0 ? acc : 0.0;
-                const double wa = ddiv(1.0, dadd(am, kPhotoEps));
-                st_photo = dadd(st_photo, dmul(dmul(scale, acc), acc));
-                dA = dmul(dmul(dmul(scale, 2.0), wa), acc);
-            }
-            need_bwd = dadd(dadd(dmul(gx, gx), dmul(gy, gy)), dmul(gz, gz)) > 0.0 || dA != 0.0;
-            if (need_bwd) ++c_bwd;
-        }
-
-        // ---------------- pass 2: backward sweep (renderer.cpp:239-319)
-        bool active2 = need_bwd && cnt_first >= 0;
-        const double total = dadd(dadd(dadd(dmul(gx, dsub(c0, dmul(P.bg[0], acc))),
-                                            dmul(gy, dsub(c1, dmul(P.bg[1], acc)))),
-                                       dmul(gz, dsub(c2, dmul(P.bg[2], acc)))),
-                                  dmul(dA, acc));
-        const double gbg = dadd(dadd(dmul(gx, P.bg[0]), dmul(gy, P.bg[1])), dmul(gz, P.bg[2]));
-        double t_cur = 0.0, a_cur = 0.0, T = 1.0, pre = 0.0, carry = 0.0;
-        int tile_cur = -1, idx = 0;
-        if (active2) {
-            mr.t = t_first;
-            mr.count = cnt_first;
-            mr.next(g, t_cur, tile_cur);  // re-emits t_first
-            double pc[3];
-            mr.pos(t_cur, pc);
-            a_cur = sigmoid_d(dmul(tau, sample_sdf(g, pc[0], pc[1], pc[2])));
-            idx = cnt_first;
-        }
-        const double dneg[3] = {-dir.x, -dir.y, -dir.z};
-        const float fgx = (float)gx, fgy = (float)gy, fgz = (float)gz;
-        while (__any_sync(FULL, active2)) {
-            bool shade = false, has_next = false, last = false;
-            double t_nxt = 0.0, a_nxt = 0.0, alpha = 0.0, w = 0.0;
-            double pc[3] = {0, 0, 0}, pn[3] = {0, 0, 0};
-            int tile_nxt = -1;
-            if (active2) {
-                has_next = mr.next(g, t_nxt, tile_nxt);
-                mr.pos(t_cur, pc);
-                mr.pos(has_next ? t_nxt : dadd(t_cur, g.h), pn);
-                a_nxt = sigmoid_d(dmul(tau, sample_sdf(g, pn[0], pn[1], pn[2])));
-                alpha = alpha_from(a_cur, a_nxt);
-                w = dmul(T, alpha);
-                shade = in_mask && w > 0.0 && tile_cur >= 0;
-            }
-            const unsigned smask = __ballot_sync(FULL, shade);
-            float rgb[3] = {0.f, 0.f, 0.f};
-            ShadeGeo geo;
-            if (smask && shade)
-                decode_forward<NS, NA>(P, s_mlp, L, tile_cur, pc, dneg, cam_row, rgb, geo,
-                                       X + lane * SD::XS, A1 + lane * RS, A2 + lane * RS);
-            if (active2) {
-                // dL/dw_i, the alpha chain and the SDF-sample scatter
-                if (alpha > 0.0) ++c_al;
-                double dw;
-                if (shade)
-                    dw = dadd(dsub(dadd(dadd(dmul(gx, (double)rgb[0]), dmul(gy, (double)rgb[1])),
-                                        dmul(gz, (double)rgb[2])),
-                                   gbg),
-                              dA);
-                else
-                    dw = dadd(-gbg, dA);
-                pre = dadd(pre, dmul(dw, w));
-                const double suffix = dsub(total, pre);
-                const double om = dsub(1.0, alpha);
-                const double dalpha = dsub(dmul(dw, T), om > 1e-12 ? ddiv(suffix, om) : 0.0);
-                double own = 0.0, nxt = 0.0;
-                if (alpha > 0.0 && dalpha != 0.0) {
-                    const double da = dmul(dmul(tau, a_cur), dsub(1.0, a_cur));
-                    const double db = dmul(dmul(tau, a_nxt), dsub(1.0, a_nxt));
-                    own = ddiv(dmul(dmul(dalpha, a_nxt), da), dmul(a_cur, a_cur));
-                    nxt = dmul(dalpha, ddiv(-db, a_cur));
-                }
-                const double ds_i = dadd(carry, own);
-                if (ds_i != 0.0) scatter_smooth(g, P.g_smooth, pc[0], pc[1], pc[2], ds_i);
-                carry = nxt;
-                ++idx;
-                last = idx >= n_live || !has_next;
-                if (last && carry != 0.0) scatter_smooth(g, P.g_smooth, pn[0], pn[1], pn[2], carry);
-            }
-            if (smask) {
-                // ---- decode_backward (decoder.cpp:111-176), warp-cooperative
-                const float ws = (float)w;
-                float dz3[3];
-                if (shade) {
-                    const float up[3] = {ws * fgx, ws * fgy, ws * fgz};
-#pragma unroll
-                    for (int j = 0; j < 3; ++j) {
-                        dz3[j] = up[j] * rgb[j] * (1.f - rgb[j]);
-                        D3s[lane * 4 + j] = dz3[j];
-                    }
-                }
-                __syncwarp();
-                {  // stage A: dW3, db3 (lane = column i)
-                    float a3[3] = {0.f, 0.f, 0.f}, bsum = 0.f;
-                    for (unsigned m = smask; m; m &= m - 1) {
-                        const int s = __ffs(m) - 1;
-                        const float av = A2[s * RS + lane];
-#pragma unroll
-                        for (int j = 0; j < 3; ++j) a3[j] += D3s[s * 4 + j] * av;
-                        if (lane < 3) bsum += D3s[s * 4 + lane];
-                    }
-#pragma unroll
-                    for (int j = 0; j < 3; ++j) ACC_ADD(GA::W3 + j * 32 + lane, G.w3 + j * 32 + lane, a3[j]);
-                    if (lane < 3) ACC_ADD(GA::B3 + lane, G.b3 + lane, bsum);
-                }
-                float dz[HID];
-                if (shade) {  // dz2 = (W3^T dz3) * [a2 > 0]
-#pragma unroll
-                    for (int i = 0; i < HID; ++i) dz[i] = 0.f;
-#pragma unroll
-                    for (int j = 0; j < 3; ++j) {
-                        const float4* row = reinterpret_cast<const float4*>(s_mlp + L.w3 + j * HID);
-#pragma unroll
-                        for (int q = 0; q < HID / 4; ++q) {
-                            const float4 wv = row[q];
-                            dz[4 * q] += wv.x * dz3[j];
-                            dz[4 * q + 1] += wv.y * dz3[j];
-                            dz[4 * q + 2] += wv.z * dz3[j];
-                            dz[4 * q + 3] += wv.w * dz3[j];
-                        }
-                    }
-#pragma unroll
-                    for (int q = 0; q < HID / 4; ++q) {
-                        const float4 a = reinterpret_cast<const float4*>(A2 + lane * RS)[q];
-                        dz[4 * q] = a.x > 0.f ? dz[4 * q] : 0.f;
-                        dz[4 * q + 1] = a.y > 0.f ? dz[4 * q + 1] : 0.f;
-                        dz[4 * q + 2] = a.z > 0.f ? dz[4 * q + 2] : 0.f;
-                        dz[4 * q + 3] = a.w > 0.f ? dz[4 * q + 3] : 0.f;
-                    }
-                }
-                __syncwarp();
-                if (shade) {
-#pragma unroll
-                    for (int q = 0; q < HID / 4; ++q)
-                        reinterpret_cast<float4*>(A2 + lane * RS)[q] =
-                            make_float4(dz[4 * q], dz[4 * q + 1], dz[4 * q + 2], dz[4 * q + 3]);
-                }
-                __syncwarp();
-                {  // stage B: dW2 row j = lane, db2
-                    float accr[HID];
-#pragma unroll
-                    for (int i = 0; i < HID; ++i) accr[i] = 0.f;
-                    float bsum = 0.f;
-                    for (unsigned m = smask; m; m &= m - 1) {
-                        const int s = __ffs(m) - 1;
-                        const float d = A2[s * RS + lane];
-                        bsum += d;
-                        const float4* arow = reinterpret_cast<const float4*>(A1 + s * RS);
-#pragma unroll
-                        for (int q = 0; q < HID / 4; ++q) {
-                            const float4 a = arow[q];
-                            accr[4 * q] += d * a.x;
-                            accr[4 * q + 1] += d * a.y;
-                            accr[4 * q + 2] += d * a.z;
-                            accr[4 * q + 3] += d * a.w;
-                        }
-                    }
-#pragma unroll
-                    for (int i = 0; i < HID; ++i) ACC_ADD(GA::W2 + lane * 33 + i, G.w2 + lane * 32 + i, accr[i]);
-                    ACC_ADD(GA::B2 + lane, G.b2 + lane, bsum);
-                }
-                if (shade) {  // dz1 = (W2^T dz2) * [a1 > 0]
-                    float da1[HID];
-#pragma unroll
-                    for (int i = 0; i < HID; ++i) da1[i] = 0.f;
-#pragma unroll 4
-                    for (int j = 0; j < HID; ++j) {
-                        const float dj = dz[j];
-                        const float4* row = reinterpret_cast<const float4*>(s_mlp + L.w2 + j * HID);
-#pragma unroll
-                        for (int q = 0; q < HID / 4; ++q) {
-                            const float4 wv = row[q];
-                            da1[4 * q] += wv.x * dj;
-                            da1[4 * q + 1] += wv.y * dj;
-                            da1[4 * q + 2] += wv.z * dj;
-                            da1[4 * q + 3] += wv.w * dj;
-                        }
-                    }
-#pragma unroll
-                    for (int q = 0; q < HID / 4; ++q) {
-                        const float4 a = reinterpret_cast<const float4*>(A1 + lane * RS)[q];
-                        dz[4 * q] = a.x > 0.f ? da1[4 * q] : 0.f;
-                        dz[4 * q + 1] = a.y > 0.f ? da1[4 * q + 1] : 0.f;
-                        dz[4 * q + 2] = a.z > 0.f ? da1[4 * q + 2] : 0.f;
-                        dz[4 * q + 3] = a.w > 0.f ? da1[4 * q + 3] : 0.f;
-                    }
-                }
-                __syncwarp();
-                if (shade) {
-#pragma unroll
-                    for (int q = 0; q < HID / 4; ++q)
-                        reinterpret_cast<float4*>(A1 + lane * RS)[q] =
-                            make_float4(dz[4 * q], dz[4 * q + 1], dz[4 * q + 2], dz[4 * q + 3]);
-                }
-                __syncwarp();
-                {  // stage C: dW1 row j = lane, db1, camera bias
-                    float accr[IN];
-#pragma unroll
-                    for (int i = 0; i < IN; ++i) accr[i] = 0.f;
-                    float bsum = 0.f;
-                    for (unsigned m = smask; m; m &= m - 1) {
-                        const int s = __ffs(m) - 1;
-                        const float d = A1[s * RS + lane];
-                        bsum += d;
-#pragma unroll
-                        for (int i = 0; i < IN; ++i) accr[i] += d * X[s * SD::XS + i];
-                    }
-#pragma unroll
-                    for (int i = 0; i < IN; ++i) ACC_ADD(GA::W1 + lane * GA::W1S + i, G.w1 + lane * IN + i, accr[i]);
-                    ACC_ADD(GA::B1 + lane, G.b1 + lane, bsum);
-                    if (gcam_row && bsum != 0.f) atomicAdd(gcam_row + lane, bsum);
-                }
-                float gfs[NS], gfa[NA], d_ndotv = 0.f;
-                float drx = 0.f, dry = 0.f, drz = 0.f;
-                if (shade) {  // din = W1^T dz1
-                    float din[IN];
-#pragma unroll
-                    for (int i = 0; i < IN; ++i) din[i] = 0.f;
-#pragma unroll 4
-                    for (int j = 0; j < HID; ++j) {
-                        const float dj = dz[j];
-                        const float* row = s_mlp + L.w1 + j * IN;
-#pragma unroll
-                        for (int i = 0; i < IN; ++i) din[i] += row[i] * dj;
-                    }
-#pragma unroll
-                    for (int k = 0; k < NS; ++k) gfs[k] = din[k];
-#pragma unroll
-                    for (int k = 0; k < NA; ++k) gfa[k] = din[NS + k];
-                    const float nv = P.no_fresnel ? 1.f : geo.ndv;
-                    if (!P.no_fresnel && nv >= 0.f && nv <= 1.f) {
-                        const float uu = 1.f - nv;
-                        float du = 0.f, upw = 1.f;
-#pragma unroll
-                        for (int k = 1; k < NPOW; ++k) {
-                            du += din[NS + NA + k] * (float)k * upw;
-                            upw *= uu;
-                        }
-                        d_ndotv = -du;
-                    }
-                    // tri-plane backward (grid.cpp:189-202)
-                    if (!P.no_spatial) {
-                        const float* pl = g.planes + (int64_t)tile_cur * 3 * 256 * NS;
-                        float* gpl = P.g_planes + (int64_t)tile_cur * 3 * 256 * NS;
-                        float pv[3][NS];
-#pragma unroll
-                        for (int q = 0; q < 3; ++q) {
-                            const Tap ta = q == 0 ? geo.ty : geo.tx;
-                            const Tap tb = q == 2 ? geo.ty : geo.tz;
-                            const float* base = pl + q * 256 * NS;
-                            const VecF<NS> v00 = ldg_vec<NS>(base + (ta.a0 * TE + tb.a0) * NS);
-                            const VecF<NS> v01 = ldg_vec<NS>(base + (ta.a0 * TE + tb.a0 + 1) * NS);
-                            const VecF<NS> v10 = ldg_vec<NS>(base + ((ta.a0 + 1) * TE + tb.a0) * NS);
-                            const VecF<NS> v11 = ldg_vec<NS>(base + ((ta.a0 + 1) * TE + tb.a0 + 1) * NS);
-#pragma unroll
-                            for (int k = 0; k < NS; ++k)
-                                pv[q][k] = (1.f - ta.f) * ((1.f - tb.f) * v00.v[k] + tb.f * v01.v[k]) +
-                                           ta.f * ((1.f - tb.f) * v10.v[k] + tb.f * v11.v[k]);
-                        }
-#pragma unroll
-                        for (int q = 0; q < 3; ++q) {
-                            const Tap ta = q == 0 ? geo.ty : geo.tx;
-                            const Tap tb = q == 2 ? geo.ty : geo.tz;
-                            float gq[NS];
-#pragma unroll
-                            for (int k = 0; k < NS; ++k)
-                                gq[k] = gfs[k] * (q == 0 ? pv[1][k] * pv[2][k]
-                                                         : (q == 1 ? pv[0][k] * pv[2][k] : pv[0][k] * pv[1][k]));
-                            float* base = gpl + q * 256 * NS;
-                            const float wq[4] = {(1.f - ta.f) * (1.f - tb.f), (1.f - ta.f) * tb.f,
-                                                 ta.f * (1.f - tb.f), ta.f * tb.f};
-                            const int off[4] = {(ta.a0 * TE + tb.a0) * NS, (ta.a0 * TE + tb.a0 + 1) * NS,
-                                                ((ta.a0 + 1) * TE + tb.a0) * NS,
-                                                ((ta.a0 + 1) * TE + tb.a0 + 1) * NS};
-#pragma unroll
-                            for (int c = 0; c < 4; ++c) {
-                                float vv4[NS];
-#pragma unroll
-                                for (int k = 0; k < NS; ++k) vv4[k] = wq[c] * gq[k];
-                                red_vec<NS>(base + off[c], vv4);
-                            }
-                        }
-                    }
-                    // probe direction gradient (sh.cpp:151-169)
-                    if (!P.no_angular) {
-                        const int nc = P.order * P.order;
-                        const int stride = g.order * g.order * NA;
-                        const int32_t* pid = g.probe_ids + (int64_t)tile_cur * 8;
-                        float sj[16];
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) sj[j] = 0.f;
-#pragma unroll 1
-                        for (int i = 0; i < 8; ++i) {
-                            const float wi8 = geo.w8[i];
-                            if (wi8 == 0.f) continue;
-                            const float* c = g.probes + (int64_t)__ldg(pid + i) * stride;
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) {
-                                if (j < nc) {
-                                    const VecF<NA> cv = ldg_vec<NA>(c + j * NA);
-                                    float sacc = 0.f;
-#pragma unroll
-                                    for (int k = 0; k < NA; ++k) sacc += cv.v[k] * gfa[k];
-                                    sj[j] += wi8 * sacc;
-                                }
-                            }
-                        }
-                        sh_basis_grad_dot(geo.refl[0], geo.refl[1], geo.refl[2], P.order, sj, drx, dry,
-                                          drz);
-                    }
-                }
-                __syncwarp();
-                // ---- probe coefficient gradients, aggregated over lanes sharing a tile
-                if (!P.no_angular) {
-                    float* PW = A2;  // per row: w8[8] | Y[16] | gfa[NA]
-                    if (shade) {
-                        float Y[16];
-                        sh_basis(geo.refl[0], geo.refl[1], geo.refl[2], P.order, Y);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) PW[lane * RS + i] = geo.w8[i];
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) PW[lane * RS + 8 + j] = Y[j];
-#pragma unroll
-                        for (int k = 0; k < NA; ++k) PW[lane * RS + 24 + k] = gfa[k];
-                    }
-                    __syncwarp();
-                    const int nc = P.order * P.order;
-                    const int stride = g.order * g.order * NA;
-                    unsigned rem = smask;
-                    while (rem) {
-                        const int leader = __ffs(rem) - 1;
-                        const int t0 = __shfl_sync(FULL, tile_cur, leader);
-                        const unsigned grp =
-                            __ballot_sync(FULL, ((rem >> lane) & 1u) && tile_cur == t0);
-                        rem &= ~grp;
-                        const int32_t* pid = g.probe_ids + (int64_t)t0 * 8;
-                        for (int e = lane; e < 8 * nc; e += 32) {
-                            const int i = e / nc, j = e - (e / nc) * nc;
-                            float a[NA];
-#pragma unroll
-                            for (int k = 0; k < NA; ++k) a[k] = 0.f;
-                            bool any = false;
-                            for (unsigned m = grp; m; m &= m - 1) {
-                                const int s = __ffs(m) - 1;
-                                const float wi8 = PW[s * RS + i];
-                                if (wi8 == 0.f) continue;
-                                any = true;
-                                const float f = wi8 * PW[s * RS + 8 + j];
-#pragma unroll
-                                for (int k = 0; k < NA; ++k) a[k] += f * PW[s * RS + 24 + k];
-                            }
-                            if (any) red_vec<NA>(P.g_probes + (int64_t)__ldg(pid + i) * stride + j * NA, a);
-                        }
-                    }
-                }
-                // ---- normal chain (renderer.cpp:216-235)
-                if (shade && !geo.degenerate) {
-                    const double n[3] = {geo.n[0], geo.n[1], geo.n[2]};
-                    const double dr[3] = {(double)drx, (double)dry, (double)drz};
-                    const double drn = dr[0] * n[0] + dr[1] * n[1] + dr[2] * n[2];
-                    const double nv = n[0] * dneg[0] + n[1] * dneg[1] + n[2] * dneg[2];
-                    double dn[3], dg[3];
-#pragma unroll
-                    for (int a = 0; a < 3; ++a)
-                        dn[a] = 2.0 * drn * dneg[a] + 2.0 * nv * dr[a] + (double)d_ndotv * dneg[a];
-                    const double dnn = dn[0] * n[0] + dn[1] * n[1] + dn[2] * n[2];
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) dg[a] = (dn[a] - n[a] * dnn) / geo.glen;
-                    const double inv2h = 1.0 / (2.0 * g.h);
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) {
-                        if (dg[a] == 0.0) continue;
-                        double pp[3] = {pc[0], pc[1], pc[2]};
-                        pp[a] = dadd(pc[a], g.h);
-                        scatter_smooth(g, P.g_smooth, pp[0], pp[1], pp[2], dg[a] * inv2h);
-                        pp[a] = dsub(pc[a], g.h);
-                        scatter_smooth(g, P.g_smooth, pp[0], pp[1], pp[2], -dg[a] * inv2h);
-                    }
-                }
-                __syncwarp();
-            }
-            if (active2) {
-                T = dmul(T, dsub(1.0, alpha));
-                if (last) {
-                    active2 = false;
-                } else {
-                    t_cur = t_nxt;
-                    tile_cur = tile_nxt;
-                    a_cur = a_nxt;
-                }
-            }
-        }
-    }
-
-    // ---------------- flush statistics and the block's MLP gradients
-    st_photo = warp_sum_d(st_photo);
-    st_sq = warp_sum_d(st_sq);
-    st_mask = warp_sum_u(st_mask);
-    c_m = warp_sum_u(c_m);
-    c_x = warp_sum_u(c_x);
-    c_sh = warp_sum_u(c_sh);
-    c_al = warp_sum_u(c_al);
-    c_bwd = warp_sum_u(c_bwd);
-    if (lane == 0) {
-        atomicAdd(P.stats + 0, st_photo);
-        atomicAdd(P.stats + 1, st_sq);
-        atomicAdd(P.stats + 2, (double)st_mask);
-        atomicAdd(P.counts + 1, c_m);
-        atomicAdd(P.counts + 2, c_x);
-        atomicAdd(P.counts + 3, c_sh);
-        atomicAdd(P.counts + 4, c_al);
-        atomicAdd(P.counts + 5, c_bwd);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < G.total_nocam; i += blockDim.x) {
-        int a;
-        if (i < G.b1) a = GA::W1 + (i / IN) * GA::W1S + (i % IN);
-        else if (i < G.w2) a = GA::B1 + (i - G.b1);
-        else if (i < G.b2) a = GA::W2 + ((i - G.w2) >> 5) * 33 + ((i - G.w2) & 31);
-        else if (i < G.w3) a = GA::B2 + (i - G.b2);
-        else if (i < G.b3) a = GA::W3 + (i - G.w3);
-        else a = GA::B3 + (i - G.b3);
-        float v = 0.f;
-#pragma unroll
-        for (int w = 0; w < WARPS_PER_BLOCK; ++w) v += s_acc[w * GA::TOTAL + a];
-        if (v != 0.f) atomicAdd(P.g_mlp + i, v);
-    }
-}
-
-template <int NS, int NA>
-size_t train_smem_bytes() {
-    constexpr int IN = NS + NA + NPOW;
-    return sizeof(float) * (SmemMlp::make(IN).total +
-                            WARPS_PER_BLOCK * (GAccDims<IN>::TOTAL + ScratchDims<IN>::TOTAL));
-}
 template <int NS, int NA>
 size_t render_smem_bytes() {
     return sizeof(float) * SmemMlp::make(NS + NA + NPOW).total;

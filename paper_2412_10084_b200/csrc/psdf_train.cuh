@@ -1,0 +1,769 @@
+// psdf_train.cuh — K2, the ray pass of one train step (trainer.cpp:157-182:
+// render_ray + photo_pixel + render_ray_backward + scatter_smooth_grad) as a
+// wavefront pipeline of four kernels.
+//
+//  K2a march_fwd    one lane per ray (8x4 pixel tile per warp): the exact f64
+//                   march / alpha / T / weight chain.  Samples that the
+//                   reference decodes (w > 0 on an in-mask ray) are appended
+//                   to a record queue (warp-aggregated atomics) linked per
+//                   ray; rays with an alpha > 0 sample get a ray entry.  Rays
+//                   without one finish here (their loss needs no colour).
+//  K2b shade_fwd    one lane per record: decode_fused, colour stored in the
+//                   record, c_raw[ray] += w C (f64 atomics).
+//  K2d alpha_bwd    one lane per ray entry: photo_pixel, then a second sweep
+//                   from the first alpha > 0 sample that applies the alpha /
+//                   transmittance chain of renderer.cpp:247-276 and scatters
+//                   the SDF-sample gradients; writes each record's upstream
+//                   dL/dC = w g.
+//  K2e shade_bwd    one lane per record, 32 records per warp: decode forward
+//                   again + decode_backward with warp-cooperative MLP weight
+//                   gradients (lane j owns row j), tri-plane atomics, probe
+//                   gradients aggregated over lanes of the same tile, and the
+//                   normal chain (renderer.cpp:216-235).
+//
+// The per-lane register footprint of the march sweeps no longer carries the
+// decoder, and the decode passes run with every lane busy.
+//
+// Suffix sums: the reverse traversal of renderer.cpp:254-261 is replaced by
+// suffix_i = Total - prefix_i, Total = g.(c_raw - bg acc) + dA acc (known
+// after K2b); the subtraction's rounding error enters ds only multiplied by
+// (1 - alpha_i).
+#pragma once
+
+#include "psdf_raypass.cuh"
+
+namespace psdf {
+
+struct WaveBufs {
+    // ray entries: rays with at least one alpha > 0 sample
+    int* e_slot;       // local work tile * 32 + lane
+    double* e_dir;     // [cap][3] unit ray direction
+    double* e_tfirst;  // t of the first alpha > 0 sample
+    int* e_cfirst;     // its sample index
+    int* e_nlive;      // samples kept after early termination
+    double* e_acc;     // accumulated opacity
+    int* e_head;       // first record of the ray, -1 if none
+    double* e_craw;    // [cap][3] sum_i w_i C_i (K2b)
+    // shading records: samples with w > 0 on in-mask rays, append order
+    double* r_pos;     // [cap][3]
+    double* r_w;
+    int* r_tile;
+    int* r_entry;
+    int* r_next;       // next record of the same ray, -1 at the end
+    float* r_c;        // [cap][4] decoded colour (K2b)
+    float* r_up;       // [cap][4] upstream w g (K2d)
+    unsigned* counters;  // [0] entries, [1] records
+    int e_cap, r_cap;
+};
+
+// Warp-aggregated slot allocation inside divergent code.
+__device__ __forceinline__ int warp_alloc(unsigned* counter, bool want, int lane) {
+    const unsigned am = __activemask();
+    const unsigned m = __ballot_sync(am, want);
+    if (!want) return -1;
+    const int leader = __ffs(m) - 1;
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(counter, (unsigned)__popc(m));
+    base = __shfl_sync(m, base, leader);
+    return (int)(base + __popc(m & ((1u << lane) - 1u)));
+}
+
+struct LaneRay {
+    const ViewDev* V;
+    int u, v;
+    bool valid;
+    int64_t px;
+};
+
+__device__ __forceinline__ LaneRay lane_ray(const RayPassParams& P, int wi, int lane) {
+    const int64_t tile_id = P.tile_begin + wi;
+    const int vi = locate_view(P, tile_id);
+    LaneRay r;
+    r.V = &P.views[vi];
+    const int64_t lt = tile_id - r.V->tile_begin;
+    r.u = (int)(lt % r.V->tiles_x) * 8 + (lane & 7);
+    r.v = (int)(lt / r.V->tiles_x) * 4 + (lane >> 3);
+    r.valid = r.u < r.V->cam.width && r.v < r.V->cam.height;
+    r.px = r.valid ? (int64_t)r.v * r.V->cam.width + r.u : 0;
+    return r;
+}
+
+// photo_pixel (losses.cpp:8-38) in f64; returns whether the ray has a
+// non-zero gradient (trainer.cpp:179).
+__device__ __forceinline__ bool photo_term(const RayPassParams& P, bool in_mask, const float* gtp,
+                                           const double col[3], double acc, double& g0, double& g1,
+                                           double& g2, double& dA, double& st_photo,
+                                           double& st_sq, unsigned long long& st_mask) {
+    const double scale = P.photo_scale;
+    g0 = g1 = g2 = dA = 0.0;
+    if (in_mask) {
+        double gg[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const double gtk = (double)__ldg(gtp + k);
+            const double d = dsub(col[k], gtk);
+            const double wk = ddiv(1.0, dadd(col[k] > gtk ? col[k] : gtk, kPhotoEps));
+            st_photo = dadd(st_photo, dmul(dmul(scale, d), d));
+            st_sq = dadd(st_sq, dmul(d, d));
+            gg[k] = dmul(dmul(dmul(scale, 2.0), wk), d);
+        }
+        g0 = gg[0];
+        g1 = gg[1];
+        g2 = gg[2];
+        st_mask += 3;
+    } else {
+        const double am = acc > 0.0 ? acc : 0.0;
+        const double wa = ddiv(1.0, dadd(am, kPhotoEps));
+        st_photo = dadd(st_photo, dmul(dmul(scale, acc), acc));
+        dA = dmul(dmul(dmul(scale, 2.0), wa), acc);
+    }
+    return dadd(dadd(dmul(g0, g0), dmul(g1, g1)), dmul(g2, g2)) > 0.0 || dA != 0.0;
+}
+
+// ------------------------------------------------------------------ K2a
+__global__ void __launch_bounds__(BLOCK) march_fwd_kernel(RayPassParams P, WaveBufs W) {
+    const int lane = threadIdx.x & 31;
+    const GridView& g = P.g;
+    const double tau = P.tau;
+    double st_photo = 0.0, st_sq = 0.0;
+    unsigned long long st_mask = 0, c_m = 0, c_x = 0, c_sh = 0, c_bwd = 0;
+    const int n_work = (int)(P.tile_end - P.tile_begin);
+    for (;;) {
+        int wi = 0;
+        if (lane == 0) wi = (int)atomicAdd(P.work_counter, 1ull);
+        wi = __shfl_sync(FULL, wi, 0);
+        if (wi >= n_work) break;
+        const LaneRay R = lane_ray(P, wi, lane);
+        if (!R.valid) continue;
+        const bool in_mask = __ldg(R.V->mask + R.px) != 0;
+        const D3 dir = pixel_dir(R.V->cam, (double)R.u + 0.5, (double)R.v + 0.5);
+        const double dd[3] = {dir.x, dir.y, dir.z};
+        Marcher mr;
+        double t_cur = 0.0, a_cur = 0.0, acc = 0.0, trans = 1.0;
+        int tile_cur = -1, n_live = 0, entry = -1, prev = -1, head = -1;
+        double t_first = 0.0;
+        int cnt_first = -1;
+        bool active = mr.init(g, R.V->cam.pos, dd, P.n_max) && mr.next(g, t_cur, tile_cur);
+        if (active) {
+            double pc[3];
+            mr.pos(t_cur, pc);
+            a_cur = sigmoid_d(dmul(tau, sample_sdf(g, pc[0], pc[1], pc[2])));
+            ++c_x;
+        }
+        while (active) {
+            double t_nxt;
+            int tile_nxt;
+            const int idx = mr.count - 1;
+            const bool has_next = mr.next(g, t_nxt, tile_nxt);
+            double pn[3];
+            mr.pos(has_next ? t_nxt : dadd(t_cur, g.h), pn);
+            const double a_nxt = sigmoid_d(dmul(tau, sample_sdf(g, pn[0], pn[1], pn[2])));
+            const double alpha = alpha_from(a_cur, a_nxt);
+            const double w = dmul(trans, alpha);
+            if (alpha > 0.0 && cnt_first < 0) {
+                cnt_first = idx;
+                t_first = t_cur;
+            }
+            const bool want_entry = alpha > 0.0 && entry < 0;
+            const int e = warp_alloc(W.counters + 0, want_entry, lane);
+            if (want_entry) entry = e < W.e_cap ? e : -2;  // -2: overflow, host retries
+            const bool shade = in_mask && w > 0.0 && tile_cur >= 0;
+            const int r = warp_alloc(W.counters + 1, shade, lane);
+            if (shade) {
+                ++c_sh;
+                if (r < W.r_cap && entry >= 0) {
+                    double pc[3];
+                    mr.pos(t_cur, pc);
+                    W.r_pos[3 * (int64_t)r] = pc[0];
+                    W.r_pos[3 * (int64_t)r + 1] = pc[1];
+                    W.r_pos[3 * (int64_t)r + 2] = pc[2];
+                    W.r_w[r] = w;
+                    W.r_tile[r] = tile_cur;
+                    W.r_entry[r] = entry;
+                    W.r_next[r] = -1;
+                    if (prev >= 0) W.r_next[prev] = r;
+                    else head = r;
+                    prev = r;
+                }
+            }
+            acc = dadd(acc, w);
+            trans = dmul(trans, dsub(1.0, alpha));
+            ++n_live;
+            if ((P.early_stop > 0.0 && trans < P.early_stop) || !has_next) break;
+            t_cur = t_nxt;
+            tile_cur = tile_nxt;
+            a_cur = a_nxt;
+        }
+        c_m += n_live;
+        if (entry >= 0) {
+            W.e_slot[entry] = wi * 32 + lane;
+            W.e_dir[3 * (int64_t)entry] = dir.x;
+            W.e_dir[3 * (int64_t)entry + 1] = dir.y;
+            W.e_dir[3 * (int64_t)entry + 2] = dir.z;
+            W.e_tfirst[entry] = t_first;
+            W.e_cfirst[entry] = cnt_first;
+            W.e_nlive[entry] = n_live;
+            W.e_acc[entry] = acc;
+            W.e_head[entry] = head;
+            W.e_craw[3 * (int64_t)entry] = 0.0;
+            W.e_craw[3 * (int64_t)entry + 1] = 0.0;
+            W.e_craw[3 * (int64_t)entry + 2] = 0.0;
+        } else if (cnt_first < 0) {
+            // no alpha > 0 sample: acc = 0, no shaded sample, nothing to
+            // back-propagate; the loss is final now
+            const double om = dsub(1.0, acc);
+            const double col[3] = {dmul(P.bg[0], om), dmul(P.bg[1], om), dmul(P.bg[2], om)};
+            double g0, g1, g2, dA;
+            if (photo_term(P, in_mask, R.V->gt + 3 * R.px, col, acc, g0, g1, g2, dA, st_photo,
+                           st_sq, st_mask))
+                ++c_bwd;
+        }
+    }
+    st_photo = warp_sum_d(st_photo);
+    st_sq = warp_sum_d(st_sq);
+    st_mask = warp_sum_u(st_mask);
+    c_m = warp_sum_u(c_m);
+    c_x = warp_sum_u(c_x);
+    c_sh = warp_sum_u(c_sh);
+    c_bwd = warp_sum_u(c_bwd);
+    if (lane == 0) {
+        atomicAdd(P.stats + 0, st_photo);
+        atomicAdd(P.stats + 1, st_sq);
+        atomicAdd(P.stats + 2, (double)st_mask);
+        atomicAdd(P.counts + 1, c_m);
+        atomicAdd(P.counts + 2, c_x);
+        atomicAdd(P.counts + 3, c_sh);
+        atomicAdd(P.counts + 5, c_bwd);
+    }
+}
+
+// Camera-bias row of a ray entry's view.
+__device__ __forceinline__ const ViewDev& entry_view(const RayPassParams& P, const WaveBufs& W,
+                                                     int e) {
+    const int slot = __ldg(W.e_slot + e);
+    return P.views[locate_view(P, P.tile_begin + (slot >> 5))];
+}
+
+// ------------------------------------------------------------------ K2b
+template <int NS, int NA>
+__global__ void __launch_bounds__(BLOCK) shade_fwd_kernel(RayPassParams P, WaveBufs W, int n_rec) {
+    constexpr int IN = NS + NA + NPOW;
+    extern __shared__ __align__(16) float smem[];
+    const SmemMlp L = SmemMlp::make(IN);
+    const MlpLayout G = MlpLayout::make(IN);
+    load_mlp_smem(P.mlp, smem, G, L);
+    __syncthreads();
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_rec; i += gridDim.x * blockDim.x) {
+        const int e = W.r_entry[i];
+        const ViewDev& V = entry_view(P, W, e);
+        const float* cam_row =
+            (P.ncam > 0 && V.cam_bias_row >= 0) ? P.mlp + G.cam + V.cam_bias_row * HID : nullptr;
+        const double pc[3] = {W.r_pos[3 * (int64_t)i], W.r_pos[3 * (int64_t)i + 1],
+                              W.r_pos[3 * (int64_t)i + 2]};
+        const double dneg[3] = {-W.e_dir[3 * (int64_t)e], -W.e_dir[3 * (int64_t)e + 1],
+                                -W.e_dir[3 * (int64_t)e + 2]};
+        float rgb[3];
+        ShadeGeo geo;
+        decode_forward<NS, NA>(P, smem, L, W.r_tile[i], pc, dneg, cam_row, rgb, geo, nullptr,
+                               nullptr, nullptr);
+        reinterpret_cast<float4*>(W.r_c)[i] = make_float4(rgb[0], rgb[1], rgb[2], 0.f);
+        const double w = W.r_w[i];
+        atomicAdd(W.e_craw + 3 * (int64_t)e, dmul((double)rgb[0], w));
+        atomicAdd(W.e_craw + 3 * (int64_t)e + 1, dmul((double)rgb[1], w));
+        atomicAdd(W.e_craw + 3 * (int64_t)e + 2, dmul((double)rgb[2], w));
+    }
+}
+
+// ------------------------------------------------------------------ K2d
+__global__ void __launch_bounds__(BLOCK) alpha_bwd_kernel(RayPassParams P, WaveBufs W, int n_ent) {
+    const int lane = threadIdx.x & 31;
+    const GridView& g = P.g;
+    const double tau = P.tau;
+    double st_photo = 0.0, st_sq = 0.0;
+    unsigned long long st_mask = 0, c_al = 0, c_bwd = 0;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_ent; e += gridDim.x * blockDim.x) {
+        const int slot = W.e_slot[e];
+        const LaneRay R = lane_ray(P, slot >> 5, slot & 31);
+        const bool in_mask = __ldg(R.V->mask + R.px) != 0;
+        const double acc = W.e_acc[e];
+        const double om = dsub(1.0, acc);
+        const double c0 = W.e_craw[3 * (int64_t)e], c1 = W.e_craw[3 * (int64_t)e + 1],
+                     c2 = W.e_craw[3 * (int64_t)e + 2];
+        const double col[3] = {dadd(c0, dmul(P.bg[0], om)), dadd(c1, dmul(P.bg[1], om)),
+                               dadd(c2, dmul(P.bg[2], om))};
+        double gx, gy, gz, dA;
+        const bool need_bwd = photo_term(P, in_mask, R.V->gt + 3 * R.px, col, acc, gx, gy, gz, dA,
+                                         st_photo, st_sq, st_mask);
+        int rec = W.e_head[e];
+        if (!need_bwd) {  // no gradient: records carry a zero upstream
+            for (; rec >= 0; rec = W.r_next[rec])
+                reinterpret_cast<float4*>(W.r_up)[rec] = make_float4(0.f, 0.f, 0.f, 0.f);
+            continue;
+        }
+        ++c_bwd;
+        const double total = dadd(dadd(dadd(dmul(gx, dsub(c0, dmul(P.bg[0], acc))),
+                                            dmul(gy, dsub(c1, dmul(P.bg[1], acc)))),
+                                       dmul(gz, dsub(c2, dmul(P.bg[2], acc)))),
+                                  dmul(dA, acc));
+        const double gbg = dadd(dadd(dmul(gx, P.bg[0]), dmul(gy, P.bg[1])), dmul(gz, P.bg[2]));
+        const double dd[3] = {W.e_dir[3 * (int64_t)e], W.e_dir[3 * (int64_t)e + 1],
+                              W.e_dir[3 * (int64_t)e + 2]};
+        Marcher mr;
+        mr.init(g, R.V->cam.pos, dd, P.n_max);
+        mr.t = W.e_tfirst[e];
+        mr.count = W.e_cfirst[e];
+        const int n_live = W.e_nlive[e];
+        double t_cur = 0.0;
+        int tile_cur = -1;
+        mr.next(g, t_cur, tile_cur);  // re-emits the first alpha > 0 sample
+        double pc[3];
+        mr.pos(t_cur, pc);
+        double a_cur = sigmoid_d(dmul(tau, sample_sdf(g, pc[0], pc[1], pc[2])));
+        double T = 1.0, pre = 0.0, carry = 0.0;
+        int idx = W.e_cfirst[e];
+        for (;;) {
+            double t_nxt = 0.0;
+            int tile_nxt = -1;
+            const bool has_next = mr.next(g, t_nxt, tile_nxt);
+            double pn[3];
+            mr.pos(has_next ? t_nxt : dadd(t_cur, g.h), pn);
+            const double a_nxt = sigmoid_d(dmul(tau, sample_sdf(g, pn[0], pn[1], pn[2])));
+            const double alpha = alpha_from(a_cur, a_nxt);
+            const double w = dmul(T, alpha);
+            if (alpha > 0.0) ++c_al;
+            const bool shade = in_mask && w > 0.0 && tile_cur >= 0;
+            // dL/dw_i = g.(C_i - bg) + dA (renderer.cpp:249-253)
+            double dw = dadd(-gbg, dA);
+            if (shade && rec >= 0) {
+                const float4 cr = reinterpret_cast<const float4*>(W.r_c)[rec];
+                dw = dadd(dsub(dadd(dadd(dmul(gx, (double)cr.x), dmul(gy, (double)cr.y)),
+                                    dmul(gz, (double)cr.z)),
+                               gbg),
+                          dA);
+                reinterpret_cast<float4*>(W.r_up)[rec] =
+                    make_float4((float)(w * gx), (float)(w * gy), (float)(w * gz), 0.f);
+                rec = W.r_next[rec];
+            }
+            pre = dadd(pre, dmul(dw, w));
+            const double suffix = dsub(total, pre);
+            const double om_a = dsub(1.0, alpha);
+            const double dalpha = dsub(dmul(dw, T), om_a > 1e-12 ? ddiv(suffix, om_a) : 0.0);
+            double own = 0.0, nxt = 0.0;
+            if (alpha > 0.0 && dalpha != 0.0) {  // renderer.cpp:266-276
+                const double da = dmul(dmul(tau, a_cur), dsub(1.0, a_cur));
+                const double db = dmul(dmul(tau, a_nxt), dsub(1.0, a_nxt));
+                own = ddiv(dmul(dmul(dalpha, a_nxt), da), dmul(a_cur, a_cur));
+                nxt = dmul(dalpha, ddiv(-db, a_cur));
+            }
+            mr.pos(t_cur, pc);
+            const double ds_i = dadd(carry, own);
+            if (ds_i != 0.0) scatter_smooth(g, P.g_smooth, pc[0], pc[1], pc[2], ds_i);
+            carry = nxt;
+            ++idx;
+            if (idx >= n_live || !has_next) {
+                if (carry != 0.0) scatter_smooth(g, P.g_smooth, pn[0], pn[1], pn[2], carry);
+                break;
+            }
+            T = dmul(T, dsub(1.0, alpha));
+            t_cur = t_nxt;
+            tile_cur = tile_nxt;
+            a_cur = a_nxt;
+        }
+    }
+    st_photo = warp_sum_d(st_photo);
+    st_sq = warp_sum_d(st_sq);
+    st_mask = warp_sum_u(st_mask);
+    c_al = warp_sum_u(c_al);
+    c_bwd = warp_sum_u(c_bwd);
+    if (lane == 0) {
+        atomicAdd(P.stats + 0, st_photo);
+        atomicAdd(P.stats + 1, st_sq);
+        atomicAdd(P.stats + 2, (double)st_mask);
+        atomicAdd(P.counts + 4, c_al);
+        atomicAdd(P.counts + 5, c_bwd);
+    }
+}
+
+// ------------------------------------------------------------------ K2e
+template <int NS, int NA>
+__global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveBufs W, int n_rec) {
+    constexpr int IN = NS + NA + NPOW;
+    using SD = ScratchDims<IN>;
+    using GA = GAccDims<IN>;
+    extern __shared__ __align__(16) float smem[];
+    const SmemMlp L = SmemMlp::make(IN);
+    const MlpLayout G = MlpLayout::make(IN);
+    float* s_mlp = smem;
+    float* s_acc = smem + L.total;  // [WARPS_PER_BLOCK][GA::TOTAL]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* s_accw = s_acc + warp * GA::TOTAL;
+    float* scr = s_acc + WARPS_PER_BLOCK * GA::TOTAL + warp * SD::TOTAL;
+    float* A1 = scr + SD::A1;
+    float* A2 = scr + SD::A2;
+    float* X = scr + SD::X;
+    float* D3s = scr + SD::D3;
+    load_mlp_smem(P.mlp, s_mlp, G, L);
+    for (int i = threadIdx.x; i < WARPS_PER_BLOCK * GA::TOTAL; i += blockDim.x) s_acc[i] = 0.f;
+    __syncthreads();
+    const GridView& g = P.g;
+    const int warps_total = gridDim.x * WARPS_PER_BLOCK;
+    for (int base = (blockIdx.x * WARPS_PER_BLOCK + warp) * 32; base < n_rec; base += warps_total * 32) {
+        const int i = base + lane;
+        float4 up = make_float4(0.f, 0.f, 0.f, 0.f);
+        int e = -1, tile = -1, cam_bias_row = -1;
+        if (i < n_rec) {
+            up = reinterpret_cast<const float4*>(W.r_up)[i];
+            e = W.r_entry[i];
+            tile = W.r_tile[i];
+            if (P.ncam > 0) cam_bias_row = entry_view(P, W, e).cam_bias_row;
+        }
+        const bool shade = i < n_rec && (up.x != 0.f || up.y != 0.f || up.z != 0.f);
+        const unsigned smask = __ballot_sync(FULL, shade);
+        if (!smask) continue;
+        double pc[3] = {0, 0, 0}, dneg[3] = {0, 0, 0};
+        float rgb[3] = {0.f, 0.f, 0.f};
+        ShadeGeo geo;
+        if (shade) {
+            pc[0] = W.r_pos[3 * (int64_t)i];
+            pc[1] = W.r_pos[3 * (int64_t)i + 1];
+            pc[2] = W.r_pos[3 * (int64_t)i + 2];
+            dneg[0] = -W.e_dir[3 * (int64_t)e];
+            dneg[1] = -W.e_dir[3 * (int64_t)e + 1];
+            dneg[2] = -W.e_dir[3 * (int64_t)e + 2];
+            const float* cam_row = cam_bias_row >= 0 ? P.mlp + G.cam + cam_bias_row * HID : nullptr;
+            decode_forward<NS, NA>(P, s_mlp, L, tile, pc, dneg, cam_row, rgb, geo,
+                                   X + lane * SD::XS, A1 + lane * RS, A2 + lane * RS);
+        }
+        // ---- decode_backward (decoder.cpp:111-176), warp-cooperative
+        float dz3[3];
+        if (shade) {
+            const float upv[3] = {up.x, up.y, up.z};
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                dz3[j] = upv[j] * rgb[j] * (1.f - rgb[j]);
+                D3s[lane * 4 + j] = dz3[j];
+            }
+        }
+        __syncwarp();
+        {  // stage A: dW3, db3 (lane = column i)
+            float a3[3] = {0.f, 0.f, 0.f}, bsum = 0.f;
+            for (unsigned m = smask; m; m &= m - 1) {
+                const int s = __ffs(m) - 1;
+                const float av = A2[s * RS + lane];
+#pragma unroll
+                for (int j = 0; j < 3; ++j) a3[j] += D3s[s * 4 + j] * av;
+                if (lane < 3) bsum += D3s[s * 4 + lane];
+            }
+#pragma unroll
+            for (int j = 0; j < 3; ++j) s_accw[GA::W3 + j * 32 + lane] += a3[j];
+            if (lane < 3) s_accw[GA::B3 + lane] += bsum;
+        }
+        float dz[HID];
+        if (shade) {  // dz2 = (W3^T dz3) * [a2 > 0]
+#pragma unroll
+            for (int q = 0; q < HID; ++q) dz[q] = 0.f;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const float4* row = reinterpret_cast<const float4*>(s_mlp + L.w3 + j * HID);
+#pragma unroll
+                for (int q = 0; q < HID / 4; ++q) {
+                    const float4 wv = row[q];
+                    dz[4 * q] += wv.x * dz3[j];
+                    dz[4 * q + 1] += wv.y * dz3[j];
+                    dz[4 * q + 2] += wv.z * dz3[j];
+                    dz[4 * q + 3] += wv.w * dz3[j];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < HID / 4; ++q) {
+                const float4 a = reinterpret_cast<const float4*>(A2 + lane * RS)[q];
+                dz[4 * q] = a.x > 0.f ? dz[4 * q] : 0.f;
+                dz[4 * q + 1] = a.y > 0.f ? dz[4 * q + 1] : 0.f;
+                dz[4 * q + 2] = a.z > 0.f ? dz[4 * q + 2] : 0.f;
+                dz[4 * q + 3] = a.w > 0.f ? dz[4 * q + 3] : 0.f;
+            }
+        }
+        __syncwarp();
+        if (shade) {
+#pragma unroll
+            for (int q = 0; q < HID / 4; ++q)
+                reinterpret_cast<float4*>(A2 + lane * RS)[q] =
+                    make_float4(dz[4 * q], dz[4 * q + 1], dz[4 * q + 2], dz[4 * q + 3]);
+        }
+        __syncwarp();
+        {  // stage B: dW2 row j = lane, db2
+            float accr[HID];
+#pragma unroll
+            for (int q = 0; q < HID; ++q) accr[q] = 0.f;
+            float bsum = 0.f;
+            for (unsigned m = smask; m; m &= m - 1) {
+                const int s = __ffs(m) - 1;
+                const float d = A2[s * RS + lane];
+                bsum += d;
+                const float4* arow = reinterpret_cast<const float4*>(A1 + s * RS);
+#pragma unroll
+                for (int q = 0; q < HID / 4; ++q) {
+                    const float4 a = arow[q];
+                    accr[4 * q] += d * a.x;
+                    accr[4 * q + 1] += d * a.y;
+                    accr[4 * q + 2] += d * a.z;
+                    accr[4 * q + 3] += d * a.w;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < HID; ++q) s_accw[GA::W2 + lane * 33 + q] += accr[q];
+            s_accw[GA::B2 + lane] += bsum;
+        }
+        if (shade) {  // dz1 = (W2^T dz2) * [a1 > 0]
+            float da1[HID];
+#pragma unroll
+            for (int q = 0; q < HID; ++q) da1[q] = 0.f;
+#pragma unroll
+            for (int j = 0; j < HID; ++j) {
+                const float dj = dz[j];
+                const float4* row = reinterpret_cast<const float4*>(s_mlp + L.w2 + j * HID);
+#pragma unroll
+                for (int q = 0; q < HID / 4; ++q) {
+                    const float4 wv = row[q];
+                    da1[4 * q] += wv.x * dj;
+                    da1[4 * q + 1] += wv.y * dj;
+                    da1[4 * q + 2] += wv.z * dj;
+                    da1[4 * q + 3] += wv.w * dj;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < HID / 4; ++q) {
+                const float4 a = reinterpret_cast<const float4*>(A1 + lane * RS)[q];
+                dz[4 * q] = a.x > 0.f ? da1[4 * q] : 0.f;
+                dz[4 * q + 1] = a.y > 0.f ? da1[4 * q + 1] : 0.f;
+                dz[4 * q + 2] = a.z > 0.f ? da1[4 * q + 2] : 0.f;
+                dz[4 * q + 3] = a.w > 0.f ? da1[4 * q + 3] : 0.f;
+            }
+        }
+        __syncwarp();
+        if (shade) {
+#pragma unroll
+            for (int q = 0; q < HID / 4; ++q)
+                reinterpret_cast<float4*>(A1 + lane * RS)[q] =
+                    make_float4(dz[4 * q], dz[4 * q + 1], dz[4 * q + 2], dz[4 * q + 3]);
+        }
+        __syncwarp();
+        {  // stage C: dW1 row j = lane, db1, camera bias (grouped by camera row)
+            float accr[IN];
+#pragma unroll
+            for (int q = 0; q < IN; ++q) accr[q] = 0.f;
+            float bsum = 0.f;
+            for (unsigned m = smask; m; m &= m - 1) {
+                const int s = __ffs(m) - 1;
+                const float d = A1[s * RS + lane];
+                bsum += d;
+#pragma unroll
+                for (int q = 0; q < IN; ++q) accr[q] += d * X[s * SD::XS + q];
+            }
+#pragma unroll
+            for (int q = 0; q < IN; ++q) s_accw[GA::W1 + lane * GA::W1S + q] += accr[q];
+            s_accw[GA::B1 + lane] += bsum;
+            if (P.ncam > 0) {
+                unsigned rem = __ballot_sync(FULL, shade && cam_bias_row >= 0);
+                while (rem) {
+                    const int row = __shfl_sync(FULL, cam_bias_row, __ffs(rem) - 1);
+                    const unsigned grp = __ballot_sync(FULL, ((rem >> lane) & 1u) && cam_bias_row == row);
+                    rem &= ~grp;
+                    float cs = 0.f;
+                    for (unsigned m = grp; m; m &= m - 1) cs += A1[(__ffs(m) - 1) * RS + lane];
+                    if (cs != 0.f) atomicAdd(P.g_mlp + G.cam + row * HID + lane, cs);
+                }
+            }
+        }
+        float gfs[NS], gfa[NA], d_ndotv = 0.f;
+        float drx = 0.f, dry = 0.f, drz = 0.f;
+        if (shade) {  // din = W1^T dz1
+            float din[IN];
+#pragma unroll
+            for (int q = 0; q < IN; ++q) din[q] = 0.f;
+#pragma unroll 4
+            for (int j = 0; j < HID; ++j) {
+                const float dj = dz[j];
+                const float* row = s_mlp + L.w1 + j * IN;
+#pragma unroll
+                for (int q = 0; q < IN; ++q) din[q] += row[q] * dj;
+            }
+#pragma unroll
+            for (int k = 0; k < NS; ++k) gfs[k] = din[k];
+#pragma unroll
+            for (int k = 0; k < NA; ++k) gfa[k] = din[NS + k];
+            const float nv = geo.ndv;
+            if (!P.no_fresnel && nv >= 0.f && nv <= 1.f) {  // decoder.cpp:162-175
+                const float uu = 1.f - nv;
+                float du = 0.f, upw = 1.f;
+#pragma unroll
+                for (int k = 1; k < NPOW; ++k) {
+                    du += din[NS + NA + k] * (float)k * upw;
+                    upw *= uu;
+                }
+                d_ndotv = -du;
+            }
+            // tri-plane backward (grid.cpp:189-202)
+            if (!P.no_spatial) {
+                const float* pl = g.planes + (int64_t)tile * 3 * 256 * NS;
+                float* gpl = P.g_planes + (int64_t)tile * 3 * 256 * NS;
+                float pv[3][NS];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const Tap ta = q == 0 ? geo.ty : geo.tx;
+                    const Tap tb = q == 2 ? geo.ty : geo.tz;
+                    const float* bp = pl + q * 256 * NS;
+                    const VecF<NS> v00 = ldg_vec<NS>(bp + (ta.a0 * TE + tb.a0) * NS);
+                    const VecF<NS> v01 = ldg_vec<NS>(bp + (ta.a0 * TE + tb.a0 + 1) * NS);
+                    const VecF<NS> v10 = ldg_vec<NS>(bp + ((ta.a0 + 1) * TE + tb.a0) * NS);
+                    const VecF<NS> v11 = ldg_vec<NS>(bp + ((ta.a0 + 1) * TE + tb.a0 + 1) * NS);
+#pragma unroll
+                    for (int k = 0; k < NS; ++k)
+                        pv[q][k] = (1.f - ta.f) * ((1.f - tb.f) * v00.v[k] + tb.f * v01.v[k]) +
+                                   ta.f * ((1.f - tb.f) * v10.v[k] + tb.f * v11.v[k]);
+                }
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const Tap ta = q == 0 ? geo.ty : geo.tx;
+                    const Tap tb = q == 2 ? geo.ty : geo.tz;
+                    float gq[NS];
+#pragma unroll
+                    for (int k = 0; k < NS; ++k)
+                        gq[k] = gfs[k] * (q == 0 ? pv[1][k] * pv[2][k]
+                                                 : (q == 1 ? pv[0][k] * pv[2][k] : pv[0][k] * pv[1][k]));
+                    float* bp = gpl + q * 256 * NS;
+                    const float wq[4] = {(1.f - ta.f) * (1.f - tb.f), (1.f - ta.f) * tb.f,
+                                         ta.f * (1.f - tb.f), ta.f * tb.f};
+                    const int off[4] = {(ta.a0 * TE + tb.a0) * NS, (ta.a0 * TE + tb.a0 + 1) * NS,
+                                        ((ta.a0 + 1) * TE + tb.a0) * NS,
+                                        ((ta.a0 + 1) * TE + tb.a0 + 1) * NS};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        float vv4[NS];
+#pragma unroll
+                        for (int k = 0; k < NS; ++k) vv4[k] = wq[c] * gq[k];
+                        red_vec<NS>(bp + off[c], vv4);
+                    }
+                }
+            }
+            // probe direction gradient (sh.cpp:151-169)
+            if (!P.no_angular) {
+                const int nc = P.order * P.order;
+                const int stride = g.order * g.order * NA;
+                const int32_t* pid = g.probe_ids + (int64_t)tile * 8;
+                float sj[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) sj[j] = 0.f;
+#pragma unroll 1
+                for (int c = 0; c < 8; ++c) {
+                    const float wc = geo.w8[c];
+                    if (wc == 0.f) continue;
+                    const float* cp = g.probes + (int64_t)__ldg(pid + c) * stride;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        if (j < nc) {
+                            const VecF<NA> cv = ldg_vec<NA>(cp + j * NA);
+                            float sacc = 0.f;
+#pragma unroll
+                            for (int k = 0; k < NA; ++k) sacc += cv.v[k] * gfa[k];
+                            sj[j] += wc * sacc;
+                        }
+                    }
+                }
+                sh_basis_grad_dot(geo.refl[0], geo.refl[1], geo.refl[2], P.order, sj, drx, dry, drz);
+            }
+        }
+        __syncwarp();
+        // ---- probe coefficient gradients, aggregated over lanes sharing a tile
+        if (!P.no_angular) {
+            float* PW = A2;  // per row: w8[8] | Y[16] | gfa[NA]
+            if (shade) {
+                float Y[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) Y[j] = 0.f;
+                sh_basis(geo.refl[0], geo.refl[1], geo.refl[2], P.order, Y);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) PW[lane * RS + c] = geo.w8[c];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) PW[lane * RS + 8 + j] = Y[j];
+#pragma unroll
+                for (int k = 0; k < NA; ++k) PW[lane * RS + 24 + k] = gfa[k];
+            }
+            __syncwarp();
+            const int nc = P.order * P.order;
+            const int stride = g.order * g.order * NA;
+            unsigned rem = smask;
+            while (rem) {
+                const int t0 = __shfl_sync(FULL, tile, __ffs(rem) - 1);
+                const unsigned grp = __ballot_sync(FULL, ((rem >> lane) & 1u) && tile == t0);
+                rem &= ~grp;
+                const int32_t* pid = g.probe_ids + (int64_t)t0 * 8;
+                for (int q = lane; q < 8 * nc; q += 32) {
+                    const int c = q / nc, j = q - (q / nc) * nc;
+                    float a[NA];
+#pragma unroll
+                    for (int k = 0; k < NA; ++k) a[k] = 0.f;
+                    bool any = false;
+                    for (unsigned m = grp; m; m &= m - 1) {
+                        const int s = __ffs(m) - 1;
+                        const float wc = PW[s * RS + c];
+                        if (wc == 0.f) continue;
+                        any = true;
+                        const float f = wc * PW[s * RS + 8 + j];
+#pragma unroll
+                        for (int k = 0; k < NA; ++k) a[k] += f * PW[s * RS + 24 + k];
+                    }
+                    if (any) red_vec<NA>(P.g_probes + (int64_t)__ldg(pid + c) * stride + j * NA, a);
+                }
+            }
+        }
+        // ---- normal chain (renderer.cpp:216-235)
+        if (shade && !geo.degenerate) {
+            const double n[3] = {geo.n[0], geo.n[1], geo.n[2]};
+            const double dr[3] = {(double)drx, (double)dry, (double)drz};
+            const double drn = dr[0] * n[0] + dr[1] * n[1] + dr[2] * n[2];
+            const double nv = n[0] * dneg[0] + n[1] * dneg[1] + n[2] * dneg[2];
+            double dn[3], dgv[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                dn[a] = 2.0 * drn * dneg[a] + 2.0 * nv * dr[a] + (double)d_ndotv * dneg[a];
+            const double dnn = dn[0] * n[0] + dn[1] * n[1] + dn[2] * n[2];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) dgv[a] = (dn[a] - n[a] * dnn) / geo.glen;
+            const double inv2h = 1.0 / (2.0 * g.h);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                if (dgv[a] == 0.0) continue;
+                double pp[3] = {pc[0], pc[1], pc[2]};
+                pp[a] = dadd(pc[a], g.h);
+                scatter_smooth(g, P.g_smooth, pp[0], pp[1], pp[2], dgv[a] * inv2h);
+                pp[a] = dsub(pc[a], g.h);
+                scatter_smooth(g, P.g_smooth, pp[0], pp[1], pp[2], -dgv[a] * inv2h);
+            }
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < G.total_nocam; i += blockDim.x) {
+        int a;
+        if (i < G.b1) a = GA::W1 + (i / IN) * GA::W1S + (i % IN);
+        else if (i < G.w2) a = GA::B1 + (i - G.b1);
+        else if (i < G.b2) a = GA::W2 + ((i - G.w2) >> 5) * 33 + ((i - G.w2) & 31);
+        else if (i < G.w3) a = GA::B2 + (i - G.b2);
+        else if (i < G.b3) a = GA::W3 + (i - G.w3);
+        else a = GA::B3 + (i - G.b3);
+        float v = 0.f;
+#pragma unroll
+        for (int w = 0; w < WARPS_PER_BLOCK; ++w) v += s_acc[w * GA::TOTAL + a];
+        if (v != 0.f) atomicAdd(P.g_mlp + i, v);
+    }
+}
+
+template <int NS, int NA>
+size_t shade_bwd_smem_bytes() {
+    constexpr int IN = NS + NA + NPOW;
+    return sizeof(float) * (SmemMlp::make(IN).total +
+                            WARPS_PER_BLOCK * (GAccDims<IN>::TOTAL + ScratchDims<IN>::TOTAL));
+}
+
+}  // namespace psdf
