@@ -140,6 +140,9 @@ void dispatch_channels(int ns, int na, F&& f) {
 
 int64_t up4(int64_t x) { return (x + 3) & ~int64_t(3); }
 
+// Tile bitmaps up to 32 KB (1024^3 grids) are staged in shared memory.
+constexpr int kMaxSmemBitWords = 8192;
+
 }  // namespace
 
 struct psdf_ctx {
@@ -155,12 +158,15 @@ struct psdf_ctx {
     int64_t off_raw = 0, off_planes = 0, off_probes = 0, off_mlp = 0, n_params = 0;
     int64_t n_planes = 0, n_probes = 0, mlp_size = 0;
     int32_t* d_tile_table = nullptr;
+    uint32_t* d_tile_bits = nullptr;
+    int bit_words = 0;
     int4* d_tile_coords = nullptr;
     int32_t* d_probe_ids = nullptr;
     int32_t* d_probe_table = nullptr;
     int4* d_probe_coords = nullptr;
     float* d_params = nullptr;
     float* d_smooth = nullptr;
+    float* d_smooth_ap = nullptr;  // smoothed SDF with a 1-voxel apron (sampling layout)
     float* d_grads = nullptr;
     float* d_gsmooth = nullptr;
     float* d_grads0 = nullptr;     // stage-0 copies (keep_raypass)
@@ -218,26 +224,30 @@ struct psdf_ctx {
         g.inv_h = g.h_pow2 ? 1.0 / desc.voxel_size : 0.0;
         g.far = desc.far_field_voxels * desc.voxel_size;
         g.tile_table = d_tile_table;
+        g.tile_bits = d_tile_bits;
+        g.bit_words = bit_words;
         g.tile_coords = d_tile_coords;
         g.probe_ids = d_probe_ids;
         g.smooth = d_smooth;
+        g.smooth_ap = d_smooth_ap;
         g.planes = d_params + off_planes;
         g.probes = d_params + off_probes;
         return g;
     }
 
     void free_grid() {
-        for (void* p : {(void*)d_tile_table, (void*)d_tile_coords, (void*)d_probe_ids,
+        for (void* p : {(void*)d_tile_table, (void*)d_tile_bits, (void*)d_tile_coords, (void*)d_probe_ids,
                         (void*)d_probe_table, (void*)d_probe_coords, (void*)d_params,
-                        (void*)d_smooth, (void*)d_grads, (void*)d_gsmooth, (void*)d_grads0,
+                        (void*)d_smooth, (void*)d_smooth_ap, (void*)d_grads, (void*)d_gsmooth, (void*)d_grads0,
                         (void*)d_gsmooth0, (void*)d_m, (void*)d_v})
             if (p) cudaFree(p);
         d_tile_table = nullptr;
+        d_tile_bits = nullptr;
         d_tile_coords = nullptr;
         d_probe_ids = nullptr;
         d_probe_table = nullptr;
         d_probe_coords = nullptr;
-        d_params = d_smooth = d_grads = d_gsmooth = d_grads0 = d_gsmooth0 = d_m = d_v = nullptr;
+        d_params = d_smooth = d_smooth_ap = d_grads = d_gsmooth = d_grads0 = d_gsmooth0 = d_m = d_v = nullptr;
         has_grid = false;
     }
 };
@@ -325,16 +335,25 @@ void launch_smooth(psdf_ctx* c, const float* src, float fill, float* dst, int ac
     ++c->last_launches;
 }
 
+// Refreshes the apron copy of the smoothed SDF used by the samplers.
+void fill_apron(psdf_ctx* c) {
+    if (c->desc.T == 0) return;
+    apron_fill_kernel<<<c->desc.T, 256, 0, c->stream>>>(c->view(), c->d_smooth, c->d_smooth_ap);
+    CK(cudaGetLastError());
+    ++c->last_launches;
+}
+
 void smooth_all(psdf_ctx* c) {
     launch_smooth(c, c->d_params + c->off_raw, (float)(c->desc.far_field_voxels * c->desc.voxel_size),
                   c->d_smooth, 0);
+    fill_apron(c);
 }
 
 // K1 launch (render).
 template <int NS, int NA>
 void launch_render(psdf_ctx* c, RayPassParams& P) {
     const void* fn = (const void*)render_kernel<NS, NA>;
-    const size_t smem = render_smem_bytes<NS, NA>();
+    const size_t smem = render_smem_bytes<NS, NA>(P.bits_sm_words);
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t n_work = P.tile_end - P.tile_begin;
     const int64_t warps_needed = std::max<int64_t>(n_work, 1);
@@ -354,7 +373,7 @@ void free_wave(psdf_ctx* c) {
     for (void* p : {(void*)W.e_slot, (void*)W.e_dir, (void*)W.e_tfirst, (void*)W.e_cfirst,
                     (void*)W.e_nlive, (void*)W.e_acc, (void*)W.e_head, (void*)W.e_craw,
                     (void*)W.r_pos, (void*)W.r_w, (void*)W.r_tile, (void*)W.r_entry,
-                    (void*)W.r_next, (void*)W.r_c, (void*)W.r_up})
+                    (void*)W.r_next, (void*)W.r_c, (void*)W.r_up, (void*)W.r_geo})
         if (p) cudaFree(p);
     unsigned* keep = W.counters;
     W = WaveBufs{};
@@ -386,6 +405,8 @@ void ensure_wave(psdf_ctx* c, int64_t e_cap, int64_t r_cap) {
     CK(cudaMalloc(&W.r_next, sizeof(int) * r_cap));
     CK(cudaMalloc(&W.r_c, sizeof(float4) * r_cap));
     CK(cudaMalloc(&W.r_up, sizeof(float4) * r_cap));
+    // geometry records sized for the widest supported channel configuration
+    CK(cudaMalloc(&W.r_geo, sizeof(float) * (size_t)GeoRec<8, 8>::STRIDE * r_cap));
     W.e_cap = (int)e_cap;
     W.r_cap = (int)r_cap;
 }
@@ -400,7 +421,10 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     const size_t smem_b = shade_bwd_smem_bytes<NS, NA>();
     CK(cudaFuncSetAttribute(shade_fwd_kernel<NS, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
     CK(cudaFuncSetAttribute(shade_bwd_kernel<NS, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
-    const int per_sm_a = blocks_per_sm((const void*)march_fwd_kernel, 0);
+    const size_t smem_bits = sizeof(uint32_t) * P.bits_sm_words;
+    CK(cudaFuncSetAttribute(march_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bits));
+    CK(cudaFuncSetAttribute(alpha_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bits));
+    const int per_sm_a = blocks_per_sm((const void*)march_fwd_kernel, smem_bits);
     const int64_t grid_a = std::max<int64_t>(1, std::min<int64_t>((n_work + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
                                                                    (int64_t)per_sm_a * c->sm_count));
     CK(cudaEventRecord(c->ev_ray0, s));
@@ -409,7 +433,7 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
         CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
         CK(cudaMemsetAsync(c->wave.counters, 0, sizeof(unsigned) * 4, s));
         P.work_counter = c->d_work;
-        march_fwd_kernel<<<(unsigned)grid_a, BLOCK, 0, s>>>(P, c->wave);
+        march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, c->wave);
         CK(cudaGetLastError());
         ++c->last_launches;
         CK(cudaMemcpyAsync(c->h_wave_counters, c->wave.counters, sizeof(unsigned) * 2,
@@ -438,9 +462,9 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     }
     CK(cudaEventRecord(c->ev_k[2], s));
     if (n_ent > 0) {
-        const int per_sm = blocks_per_sm((const void*)alpha_bwd_kernel, 0);
+        const int per_sm = blocks_per_sm((const void*)alpha_bwd_kernel, smem_bits);
         const int grid = (int)std::min<int64_t>((n_ent + BLOCK - 1) / BLOCK, (int64_t)per_sm * c->sm_count);
-        alpha_bwd_kernel<<<grid, BLOCK, 0, s>>>(P, c->wave, n_ent);
+        alpha_bwd_kernel<<<grid, BLOCK, smem_bits, s>>>(P, c->wave, n_ent);
         CK(cudaGetLastError());
         ++c->last_launches;
     }
@@ -465,6 +489,7 @@ RayPassParams base_params(psdf_ctx* c) {
     P.order = c->desc.sh_order;
     P.n_max = 512;
     P.early_stop = 1e-4;
+    P.bits_sm_words = c->bit_words <= kMaxSmemBitWords ? c->bit_words : 0;
     P.work_counter = c->d_work;
     P.counts = c->d_counts;
     P.stats = c->d_stats;
@@ -672,7 +697,7 @@ __global__ void march_rays_kernel(GridView g, int n, const double* __restrict__ 
     if (mr.init(g, o + 3 * r, d + 3 * r, n_max)) {
         double t;
         int tile;
-        while (mr.next(g, t, tile)) ts[(int64_t)r * n_max + k++] = t;
+        while (mr.next(g, t, tile, g.tile_bits)) ts[(int64_t)r * n_max + k++] = t;
     }
     counts[r] = k;
 }
@@ -814,6 +839,13 @@ int psdf_upload_grid(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_c
         c->off_mlp = up4(c->off_probes + c->n_probes);
         c->n_params = up4(c->off_mlp + c->mlp_size);
         CK(cudaMalloc(&c->d_tile_table, sizeof(int32_t) * ntt));
+        c->bit_words = (int)((ntt + 31) / 32);
+        std::vector<uint32_t> bits(c->bit_words, 0u);
+        for (int64_t i = 0; i < ntt; ++i)
+            if (tt[i] >= 0) bits[i >> 5] |= 1u << (i & 31);
+        CK(cudaMalloc(&c->d_tile_bits, sizeof(uint32_t) * c->bit_words));
+        CK(cudaMemcpyAsync(c->d_tile_bits, bits.data(), sizeof(uint32_t) * c->bit_words,
+                           cudaMemcpyHostToDevice, c->stream));
         CK(cudaMalloc(&c->d_probe_table, sizeof(int32_t) * npt));
         CK(cudaMalloc(&c->d_tile_coords, sizeof(int4) * tc4.size()));
         CK(cudaMalloc(&c->d_probe_coords, sizeof(int4) * pc4.size()));
@@ -823,6 +855,7 @@ int psdf_upload_grid(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_c
         CK(cudaMalloc(&c->d_m, sizeof(float) * c->n_params));
         CK(cudaMalloc(&c->d_v, sizeof(float) * c->n_params));
         CK(cudaMalloc(&c->d_smooth, sizeof(float) * std::max<int64_t>(T * TV, 4)));
+        CK(cudaMalloc(&c->d_smooth_ap, sizeof(float) * std::max<int64_t>(T * AV, 4)));
         CK(cudaMalloc(&c->d_gsmooth, sizeof(float) * std::max<int64_t>(T * TV, 4)));
         CK(cudaMemsetAsync(c->d_params, 0, sizeof(float) * c->n_params, c->stream));
         CK(cudaMemsetAsync(c->d_grads, 0, sizeof(float) * c->n_params, c->stream));
@@ -843,10 +876,12 @@ int psdf_upload_grid(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_c
                                cudaMemcpyHostToDevice, c->stream));
         c->has_grid = true;
         c->adam_t = 0;
-        if (smooth && T > 0)
+        if (smooth && T > 0) {
             CK(cudaMemcpyAsync(c->d_smooth, smooth, sizeof(float) * T * TV, cudaMemcpyHostToDevice, c->stream));
-        else
+            fill_apron(c);
+        } else {
             smooth_all(c);
+        }
         CK(cudaStreamSynchronize(c->stream));
     });
 }

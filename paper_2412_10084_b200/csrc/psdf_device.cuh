@@ -46,9 +46,12 @@ struct GridView {
     int h_pow2;                    // x / h == x * inv_h exactly (power-of-two h)
     double wmax[3];                // world_max() (grid.hpp:72-74)
     const int32_t* __restrict__ tile_table;   // [nt0][nt1][nt2] -> tile or -1
+    const uint32_t* __restrict__ tile_bits;   // occupancy bitmap of tile_table
+    int bit_words;                            // 32-bit words in tile_bits
     const int4* __restrict__ tile_coords;     // [T] (x,y,z,0)
     const int32_t* __restrict__ probe_ids;    // [T][8]
     const float* __restrict__ smooth;         // [T][4096]
+    const float* __restrict__ smooth_ap;      // [T][18^3] smooth with a 1-voxel apron
     const float* __restrict__ planes;         // [T][3][256][n_s]
     const float* __restrict__ probes;         // [P][order^2][n_a]
 };
@@ -84,9 +87,61 @@ __device__ __forceinline__ double smooth_value(const GridView& g, int vx, int vy
     return (double)__ldg(g.smooth + (int64_t)t * TV + vox_index(vx & 15, vy & 15, vz & 15));
 }
 
-// sample_sdf (grid.cpp:98-125), exact f64.  When all 8 corners fall in one
-// tile (the common case) a single table lookup serves them.
+// The 8 trilinear corners when they straddle tiles / the grid boundary.
+__device__ __noinline__ void corners_slow(const GridView& g, int bx, int by, int bz, double c[8]) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        c[i] = smooth_value(g, bx + (i & 1), by + ((i >> 1) & 1), bz + ((i >> 2) & 1));
+}
+
+constexpr int AE = 18;            // apron brick edge (16 + 2)
+constexpr int AV = AE * AE * AE;  // 5832
+
+// Trilinear sum of sample_trilinear (grid.cpp:104-110) in its exact f64
+// operation order.
+__device__ __forceinline__ double trilerp8(double fx, double fy, double fz, const double c[8]) {
+    const double gx0 = dsub(1.0, fx), gy0 = dsub(1.0, fy), gz0 = dsub(1.0, fz);
+    double v = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const double w = dmul(dmul((i & 1) ? fx : gx0, (i & 2) ? fy : gy0), (i & 4) ? fz : gz0);
+        v = dadd(v, dmul(w, c[i]));
+    }
+    return v;
+}
+
+// sample_sdf (grid.cpp:98-125) at a point whose containing voxel lies in the
+// allocated tile `tile` (tile coordinates tc): every corner is inside the
+// tile's apron brick, so no table lookup is needed.  Exact f64.
+__device__ __forceinline__ double sample_sdf_in(const GridView& g, double px, double py, double pz,
+                                                int tile, int4 tc) {
+    const double cx = dsub(w2v(g, px, 0), 0.5);
+    const double cy = dsub(w2v(g, py, 1), 0.5);
+    const double cz = dsub(w2v(g, pz, 2), 0.5);
+    const int bx = (int)floor(cx), by = (int)floor(cy), bz = (int)floor(cz);
+    const double fx = dsub(cx, (double)bx), fy = dsub(cy, (double)by), fz = dsub(cz, (double)bz);
+    // corner b - 16 tc in [-1, 15]: apron index +1
+    const float* base = g.smooth_ap + (int64_t)tile * AV +
+                        ((bx - 16 * tc.x + 1) * AE + (by - 16 * tc.y + 1)) * AE + (bz - 16 * tc.z + 1);
+    double c[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        c[i] = (double)__ldg(base + (i & 1) * (AE * AE) + ((i >> 1) & 1) * AE + ((i >> 2) & 1));
+    return trilerp8(fx, fy, fz, c);
+}
+
+// sample_sdf (grid.cpp:98-125), exact f64, for an arbitrary point: one table
+// lookup finds the containing tile; outside allocated tiles the corners are
+// fetched one by one.
 __device__ __forceinline__ double sample_sdf(const GridView& g, double px, double py, double pz) {
+    {
+        const double vx = w2v(g, px, 0), vy = w2v(g, py, 1), vz = w2v(g, pz, 2);
+        const int ix = (int)floor(vx), iy = (int)floor(vy), iz = (int)floor(vz);
+        if (ix >= 0 && iy >= 0 && iz >= 0 && ix < g.res[0] && iy < g.res[1] && iz < g.res[2]) {
+            const int t = tile_lookup(g, ix >> 4, iy >> 4, iz >> 4);
+            if (t >= 0) return sample_sdf_in(g, px, py, pz, t, make_int4(ix >> 4, iy >> 4, iz >> 4, 0));
+        }
+    }
     const double cx = dsub(w2v(g, px, 0), 0.5);
     const double cy = dsub(w2v(g, py, 1), 0.5);
     const double cz = dsub(w2v(g, pz, 2), 0.5);
@@ -106,9 +161,7 @@ __device__ __forceinline__ double sample_sdf(const GridView& g, double px, doubl
         for (int i = 0; i < 8; ++i)
             c[i] = (double)__ldg(base + (i & 1) * 256 + ((i >> 1) & 1) * 16 + ((i >> 2) & 1));
     } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-            c[i] = smooth_value(g, bx + (i & 1), by + ((i >> 1) & 1), bz + ((i >> 2) & 1));
+        corners_slow(g, bx, by, bz, c);
     }
     double v = 0.0;
 #pragma unroll
@@ -125,8 +178,8 @@ struct Cam {
     int width, height, id;
 };
 
-// Camera::pixel_dir (camera.hpp:32-35), exact f64.
-__device__ __forceinline__ D3 pixel_dir(const Cam& c, double u, double v) {
+// Camera::pixel_dir (camera.hpp:32-35), exact f64 (out of line: once per ray).
+__device__ __noinline__ D3 pixel_dir(const Cam& c, double u, double v) {
     const double x = ddiv(dsub(u, c.cx), c.fx), y = ddiv(dsub(v, c.cy), c.fy), z = 1.0;
     const D3 q = d3(dadd(dadd(dmul(c.rot[0], x), dmul(c.rot[1], y)), dmul(c.rot[2], z)),
                     dadd(dadd(dmul(c.rot[3], x), dmul(c.rot[4], y)), dmul(c.rot[5], z)),
@@ -136,8 +189,10 @@ __device__ __forceinline__ D3 pixel_dir(const Cam& c, double u, double v) {
     return d3(ddiv(q.x, n), ddiv(q.y, n), ddiv(q.z, n));
 }
 
-// ray_box (renderer.cpp:13-31)
-__device__ __forceinline__ bool ray_box(const double o[3], const double d[3], const double mn[3],
+// ray_box (renderer.cpp:13-31).  Out of line: it runs once per ray and on
+// the rare exact fallbacks, and its six f64 divisions would bloat every
+// inlined march loop.
+__device__ __noinline__ bool ray_box(const double o[3], const double d[3], const double mn[3],
                                         const double mx[3], double& t0, double& t1) {
     t0 = 0.0;
     t1 = 1.7976931348623157e308;
@@ -160,19 +215,109 @@ __device__ __forceinline__ bool ray_box(const double o[3], const double d[3], co
     return true;
 }
 
+// Copies the tile occupancy bitmap into shared memory (call before a
+// __syncthreads) and returns the pointer the marcher should use.
+__device__ __forceinline__ const uint32_t* stage_tile_bits(const GridView& g, uint32_t* sm_bits,
+                                                           int sm_words) {
+    if (g.bit_words > sm_words) return g.tile_bits;  // too large: read through L1
+    for (int i = threadIdx.x; i < g.bit_words; i += blockDim.x) sm_bits[i] = __ldg(g.tile_bits + i);
+    return sm_bits;
+}
+
+// Exit distance of the ray from an (unallocated) tile box and the skip
+// decision of renderer.cpp:73-82, computed with reciprocal multiplies.  The
+// reference divides, (mn - o) / d; the product with the correctly rounded
+// reciprocal is within ~2 ulp of it.  Every decision the result feeds (the
+// box test t0 <= t1, e1 > t, and the integer ceil((e1 - t) / h + 1e-9)) is
+// taken on the fast value only when it is farther than a safe margin from
+// the decision boundary; otherwise the exact ray_box reruns.  So the emitted
+// t-list is bit-identical to the reference's either way.
+// Returns the new t.
+__device__ __noinline__ double skip_tile(const GridView& g, const double o[3],
+                                         const double d[3], const double inv_d[3], const int tc[3],
+                                         double t) {
+    const double h = g.h;
+    const double tile_w = dmul(16.0, h);  // renderer.cpp:74-75
+    const double bmin[3] = {dadd(g.org[0], dmul((double)tc[0], tile_w)),
+                            dadd(g.org[1], dmul((double)tc[1], tile_w)),
+                            dadd(g.org[2], dmul((double)tc[2], tile_w))};
+    const double bmax[3] = {dadd(bmin[0], tile_w), dadd(bmin[1], tile_w), dadd(bmin[2], tile_w)};
+    bool ok = true, exact = false;
+    double t0 = 0.0, t1 = 1.7976931348623157e308;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (fabs(d[a]) < 1e-15) {
+            if (o[a] < bmin[a] || o[a] > bmax[a]) ok = false;
+            continue;
+        }
+        double ta = dmul(dsub(bmin[a], o[a]), inv_d[a]), tb = dmul(dsub(bmax[a], o[a]), inv_d[a]);
+        if (ta > tb) {
+            const double s = ta;
+            ta = tb;
+            tb = s;
+        }
+        t0 = (t0 < ta) ? ta : t0;
+        t1 = (tb < t1) ? tb : t1;
+    }
+    const double m = 1e-12 * (fabs(t) + 1.0);  // >> the ~1e-15 relative error
+    const double mq = m * (g.h_pow2 ? g.inv_h : 1.0 / g.h);
+    if (ok && fabs(t0 - t1) <= m) exact = true;
+    ok = ok && t0 <= t1;
+    double q = 0.0;
+    if (!exact && ok) {
+        if (fabs(t1 - t) <= m) exact = true;
+        else if (t1 > t) {
+            q = dadd(div_h(g, dsub(t1, t)), 1e-9);
+            const double fq = q - floor(q);
+            if (fq <= mq || fq >= 1.0 - mq) exact = true;
+        }
+    }
+    if (exact) {  // rare: redo with the reference's divisions
+        double e0, e1;
+        ok = ray_box(o, d, bmin, bmax, e0, e1);
+        t1 = e1;
+        if (ok && e1 > t) q = dadd(div_h(g, dsub(e1, t)), 1e-9);
+    }
+    if (ok && t1 > t) {
+        const double skip = ceil(q);
+        return dadd(t, dmul(skip > 1.0 ? skip : 1.0, h));
+    }
+    return dadd(t, h);
+}
+
+// Tile of p(t) exactly as the reference computes it: floor((o + t d - org)/h) >> 4.
+__device__ __noinline__ void exact_tile(const GridView& g, const double o[3], const double d[3],
+                                        double t, int tc[3]) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) tc[a] = ((int)floor(w2v(g, dadd(o[a], dmul(d[a], t)), a))) >> 4;
+}
+
 // march_ray (renderer.cpp:55-86) as a resumable generator: the state is
 // (t, count), so the backward sweep can restart at any emitted sample.
+//
+// t is advanced with exactly the reference's f64 additions.  The two integer
+// decisions taken per iteration — which tile p(t) lies in, and the skip count
+// ceil((e1 - t)/h + 1e-9) past an empty tile — are first evaluated in f32 in
+// voxel units (v = (o - org)/h + (d/h) t); when the f32 value is farther than
+// a margin (>= 10x its error bound) from the decision boundary the result is
+// provably the exact one, otherwise the exact f64 path decides.
 struct Marcher {
-    double o[3], d[3];
+    double o[3], d[3], inv_d[3];
     double t, t1;
     int count, n_max;
+    float vo[3], vd[3], rd[3];  // (o - org)/h, d/h, 1/d in f32
 
     __device__ __forceinline__ bool init(const GridView& g, const double* o_, const double* d_,
                                          int nmax) {
+        const double inv_h = g.h_pow2 ? g.inv_h : 1.0 / g.h;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             o[a] = o_[a];
             d[a] = d_[a];
+            inv_d[a] = fabs(d[a]) < 1e-15 ? 0.0 : __drcp_rn(d[a]);
+            vo[a] = (float)((o[a] - g.org[a]) * inv_h);
+            vd[a] = (float)(d[a] * inv_h);
+            rd[a] = fabs(d[a]) < 1e-15 ? 0.f : (float)inv_d[a];
         }
         n_max = nmax;
         count = 0;
@@ -187,35 +332,74 @@ struct Marcher {
     }
 
     // Next sample distance inside an allocated tile; false when exhausted.
-    __device__ __forceinline__ bool next(const GridView& g, double& t_out, int& tile_out) {
+    // `bits` is the tile occupancy bitmap (usually a shared-memory copy), so
+    // skipping empty tiles needs no global memory access.
+    __device__ __forceinline__ bool next(const GridView& g, double& t_out, int& tile_out,
+                                         const uint32_t* bits, int4* tc_out = nullptr) {
         const double h = g.h;
-        const double tile_w = dmul(16.0, h);
         while (t < t1 && count < n_max) {
-            const double vx = w2v(g, dadd(o[0], dmul(d[0], t)), 0);
-            const double vy = w2v(g, dadd(o[1], dmul(d[1], t)), 1);
-            const double vz = w2v(g, dadd(o[2], dmul(d[2], t)), 2);
-            const int tx = ((int)floor(vx)) >> 4, ty = ((int)floor(vy)) >> 4,
-                      tz = ((int)floor(vz)) >> 4;
-            const int tile = tile_lookup(g, tx, ty, tz);
-            if (tile >= 0) {
+            // --- tile of p(t): f32 fast path
+            const float tf = (float)t;
+            float v[3], ev[3];
+            int tc[3];
+            bool near = false;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                v[a] = fmaf(vd[a], tf, vo[a]);
+                // error bound of v: roundings of vo, vd, tf and the fma, each
+                // <= 2^-24 of the magnitudes involved (plus a floor for tiny ones)
+                ev[a] = 1e-5f + 2.5e-7f * (fabsf(vo[a]) + fabsf(vd[a] * tf) + fabsf(v[a]));
+                const float r16 = v[a] * 0.0625f;
+                const float dist = fabsf(r16 - rintf(r16)) * 16.f;
+                near |= dist < 16.f * ev[a];
+                tc[a] = ((int)floorf(v[a])) >> 4;
+            }
+            if (near) exact_tile(g, o, d, t, tc);
+            bool occupied = false;
+            if ((unsigned)tc[0] < (unsigned)g.nt[0] && (unsigned)tc[1] < (unsigned)g.nt[1] &&
+                (unsigned)tc[2] < (unsigned)g.nt[2]) {
+                const int b = (tc[0] * g.nt[1] + tc[1]) * g.nt[2] + tc[2];
+                occupied = (bits[b >> 5] >> (b & 31)) & 1u;
+            }
+            if (occupied) {
                 t_out = t;
-                tile_out = tile;
+                tile_out = tile_lookup(g, tc[0], tc[1], tc[2]);
+                if (tc_out) *tc_out = make_int4(tc[0], tc[1], tc[2], 0);
                 t = dadd(t, h);
                 ++count;
                 return true;
             }
-            const double bmin[3] = {dadd(g.org[0], dmul((double)tx, tile_w)),
-                                    dadd(g.org[1], dmul((double)ty, tile_w)),
-                                    dadd(g.org[2], dmul((double)tz, tile_w))};
-            const double bmax[3] = {dadd(bmin[0], tile_w), dadd(bmin[1], tile_w),
-                                    dadd(bmin[2], tile_w)};
-            double e0, e1;
-            if (ray_box(o, d, bmin, bmax, e0, e1) && e1 > t) {
-                const double skip = ceil(dadd(div_h(g, dsub(e1, t)), 1e-9));
-                t = dadd(t, dmul(skip > 1.0 ? skip : 1.0, h));
-            } else {
-                t = dadd(t, h);
+            // --- skip the empty tile: f32 fast path for the skip count.  p(t)
+            // is inside the tile and off its faces (not `near`), so the box
+            // test passes and e1 > t; q = (e1 - t)/h = min_a (B_a - v_a)/d_a.
+            bool fast = !near;
+            float q = 3.0e38f;
+            int qa = -1;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                if (rd[a] == 0.f) continue;
+                const float B = 16.f * (float)(tc[a] + (d[a] > 0.0 ? 1 : 0));
+                const float qq = (B - v[a]) * rd[a];
+                if (qq < q) {
+                    q = qq;
+                    qa = a;
+                }
             }
+            if (fast && qa >= 0) {
+                // q error: ev * |1/d| plus the roundings of the subtraction,
+                // 1/d and the product (~3 ulp of the magnitudes)
+                const float err = (ev[qa] + 16.f * 6e-8f * fabsf(v[qa])) * fabsf(rd[qa]) + q * 4e-7f + 1e-6f;
+                const float fq = q - floorf(q);
+                if (fq <= 8.f * err || fq >= 1.f - 8.f * err) fast = false;
+            } else {
+                fast = false;
+            }
+            if (fast) {
+                const float k = ceilf(q);  // + 1e-9 is inside the margin
+                t = dadd(t, dmul(k > 1.f ? (double)k : 1.0, h));
+                continue;
+            }
+            t = skip_tile(g, o, d, inv_d, tc, t);
         }
         return false;
     }
@@ -228,9 +412,17 @@ struct Marcher {
 
 // sigmoid (renderer.cpp:10) and alpha_from_sdf (renderer.cpp:35-39), f64.
 // __drcp_rn is the correctly rounded reciprocal, i.e. the same value as 1.0/x.
+#ifdef PSDF_ABL_EXPF
+__device__ __forceinline__ double sigmoid_d(double x) { return 1.0 / (1.0 + (double)__expf((float)-x)); }
+#else
 __device__ __forceinline__ double sigmoid_d(double x) { return __drcp_rn(dadd(1.0, exp(-x))); }
+#endif
 __device__ __forceinline__ double alpha_from(double a, double b) {
+#ifdef PSDF_ABL_ALPHA
+    const double al = (a - b) * __drcp_rn(a);
+#else
     const double al = ddiv(dsub(a, b), a);
+#endif
     return al > 0.0 ? al : 0.0;
 }
 

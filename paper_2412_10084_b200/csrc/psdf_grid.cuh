@@ -109,6 +109,27 @@ __global__ void __launch_bounds__(256) smooth_fold_kernel(GridView g, const floa
     }
 }
 
+// Apron copy of the smoothed SDF (psdf_device.cuh, sample_sdf_in): cell
+// (x, y, z) in [-1, 16]^3 of tile t holds smooth_value at that global voxel,
+// i.e. the owning tile's value or the far field.
+__global__ void __launch_bounds__(256) apron_fill_kernel(GridView g, const float* __restrict__ smooth,
+                                                         float* __restrict__ ap) {
+    const int t = blockIdx.x;
+    const int4 tc = __ldg(g.tile_coords + t);
+    for (int i = threadIdx.x; i < AV; i += blockDim.x) {
+        const int x = i / (AE * AE) - 1, y = (i / AE) % AE - 1, z = i % AE - 1;
+        const int vx = tc.x * TE + x, vy = tc.y * TE + y, vz = tc.z * TE + z;
+        float v = (float)g.far;
+        if ((unsigned)x < 16u && (unsigned)y < 16u && (unsigned)z < 16u) {
+            v = smooth[(int64_t)t * TV + vox_index(x, y, z)];
+        } else if (vx >= 0 && vy >= 0 && vz >= 0 && vx < g.res[0] && vy < g.res[1] && vz < g.res[2]) {
+            const int nt = tile_lookup(g, vx >> 4, vy >> 4, vz >> 4);
+            if (nt >= 0) v = smooth[(int64_t)nt * TV + vox_index(vx & 15, vy & 15, vz & 15)];
+        }
+        ap[(int64_t)t * AV + i] = v;
+    }
+}
+
 __device__ __forceinline__ void block_add_f64(double* dst, double v, double* red) {
     // block-wide sum of one double per thread, one atomic per block
 #pragma unroll

@@ -54,6 +54,7 @@ struct RayPassParams {
     int order;            // effective SH order (sh_order_override applied)
     int no_spatial, no_angular, no_fresnel, need_colors;
     int n_max;
+    int bits_sm_words;    // words of the tile bitmap staged in shared memory (0 = use global)
     double tau, early_stop, bg[3];
     double photo_scale;
     const ViewDev* views;
@@ -151,16 +152,25 @@ struct ShadeGeo {
     float w8[8];
 };
 
-// decode_fused (renderer.cpp:88-147) for one sample at p (f64 world point).
-// dneg = -dir = view vector toward the camera.  Writes rgb; when x_row /
-// a1_row / a2_row are non-null the MLP activations are stored there (train).
+// Per-record geometry + features written by K2b for K2e (floats):
+//   [0,3) normal  [3] |grad|  [4,7) refl  [7] n.v  [8,11) tap fractions
+//   [11] tap a0 | degenerate flag (int bits)  [12,20) probe corner weights
+//   [20, 20+3 NS) plane samples  [20+3 NS, +IN) MLP input
 template <int NS, int NA>
-__device__ __forceinline__ void decode_forward(const RayPassParams& P, const float* __restrict__ sm,
-                                               const SmemMlp& L, int tile, const double p[3],
-                                               const double dneg[3], const float* cam_row,
-                                               float rgb[3], ShadeGeo& geo, float* x_row,
-                                               float* a1_row, float* a2_row) {
-    constexpr int IN = NS + NA + NPOW;
+struct GeoRec {
+    static constexpr int IN = NS + NA + NPOW;
+    static constexpr int PV = 20;
+    static constexpr int X = PV + 3 * NS;
+    static constexpr int STRIDE = (X + IN + 3) & ~3;
+};
+
+// decode_fused (renderer.cpp:88-147), geometry + feature part, for one sample
+// at p (f64 world point); dneg = -dir = view vector toward the camera.
+// Produces the MLP input x and the tri-plane samples pv.
+template <int NS, int NA>
+__device__ __forceinline__ void decode_features(const RayPassParams& P, int tile, const double p[3],
+                                                const double dneg[3], ShadeGeo& geo,
+                                                float x[NS + NA + NPOW], float pv[3][NS]) {
     const GridView& g = P.g;
     const double h = g.h;
     // central-difference normal of the smoothed SDF, exact f64
@@ -173,7 +183,7 @@ __device__ __forceinline__ void decode_forward(const RayPassParams& P, const flo
     const double h2 = dmul(2.0, h);
     // x / (2h): exact multiply for a power-of-two h (see div_h)
     const double inv2h = g.h_pow2 ? dmul(0.5, g.inv_h) : 0.0;
-    auto div2h = [&](double x) { return g.h_pow2 ? dmul(x, inv2h) : ddiv(x, h2); };
+    auto div2h = [&](double x_) { return g.h_pow2 ? dmul(x_, inv2h) : ddiv(x_, h2); };
     const D3 gv = d3(div2h(dsub(sxp, sxm)), div2h(dsub(syp, sym)), div2h(dsub(szp, szm)));
     const double glen = dsqrt(ddot(gv, gv));
     geo.degenerate = glen < 1e-8;
@@ -206,20 +216,22 @@ __device__ __forceinline__ void decode_forward(const RayPassParams& P, const flo
     geo.tx = plane_tap(lx);
     geo.ty = plane_tap(ly);
     geo.tz = plane_tap(lz);
-    {  // trilinear_weights(local/16) (sh.cpp:172-181)
-        const double fx = dmul(lx, 0.0625), fy = dmul(ly, 0.0625), fz = dmul(lz, 0.0625);  // exact /16
+    {  // trilinear_weights(local/16) (sh.cpp:172-181); /16 is an exact multiply
+        const double fx = dmul(lx, 0.0625), fy = dmul(ly, 0.0625), fz = dmul(lz, 0.0625);
 #pragma unroll
         for (int i = 0; i < 8; ++i)
             geo.w8[i] = (float)dmul(dmul((i & 1) ? fx : dsub(1.0, fx), (i & 2) ? fy : dsub(1.0, fy)),
                                     (i & 4) ? fz : dsub(1.0, fz));
     }
-    float x[IN];
 #pragma unroll
     for (int k = 0; k < NS + NA; ++k) x[k] = 0.f;
     // F_s: channel-wise tri-plane product (grid.cpp:179-187)
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int k = 0; k < NS; ++k) pv[q][k] = 0.f;
     if (!P.no_spatial) {
         const float* pl = g.planes + (int64_t)tile * 3 * 256 * NS;
-        float pv[3][NS];
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
             const Tap ta = q == 0 ? geo.ty : geo.tx;
@@ -240,6 +252,8 @@ __device__ __forceinline__ void decode_forward(const RayPassParams& P, const flo
     // F_a: coefficient-blended probes evaluated along refl (sh.cpp:104-123)
     if (!P.no_angular) {
         float Y[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) Y[j] = 0.f;
         sh_basis(geo.refl[0], geo.refl[1], geo.refl[2], P.order, Y);
         const int nc = P.order * P.order;
         const int stride = g.order * g.order * NA;
@@ -252,11 +266,13 @@ __device__ __forceinline__ void decode_forward(const RayPassParams& P, const flo
             float acc[NA];
 #pragma unroll
             for (int k = 0; k < NA; ++k) acc[k] = 0.f;
-#pragma unroll 4
-            for (int j = 0; j < nc; ++j) {
-                const VecF<NA> cv = ldg_vec<NA>(c + j * NA);
 #pragma unroll
-                for (int k = 0; k < NA; ++k) acc[k] += Y[j] * cv.v[k];
+            for (int j = 0; j < 16; ++j) {
+                if (j < nc) {
+                    const VecF<NA> cv = ldg_vec<NA>(c + j * NA);
+#pragma unroll
+                    for (int k = 0; k < NA; ++k) acc[k] += Y[j] * cv.v[k];
+                }
             }
 #pragma unroll
             for (int k = 0; k < NA; ++k) x[NS + k] += w * acc[k];
@@ -269,7 +285,14 @@ __device__ __forceinline__ void decode_forward(const RayPassParams& P, const flo
 #pragma unroll
         for (int k = 1; k < NPOW; ++k) x[NS + NA + k] = x[NS + NA + k - 1] * u;
     }
-    // MLP (decoder.cpp:61-109)
+}
+
+// decode_color (decoder.cpp:61-109) from the MLP input; a1 / a2 optional
+// outputs (post-ReLU activations).
+template <int IN>
+__device__ __forceinline__ void mlp_forward(const float* __restrict__ sm, const SmemMlp& L,
+                                            const float x[IN], const float* cam_row, float rgb[3],
+                                            float* a1_row, float* a2_row) {
     float a1[HID];
 #pragma unroll
     for (int j = 0; j < HID; ++j) {
@@ -302,9 +325,7 @@ __device__ __forceinline__ void decode_forward(const RayPassParams& P, const flo
         }
         rgb[j] = sigmoidf_(z);
     }
-    if (x_row) {
-#pragma unroll
-        for (int i = 0; i < IN; ++i) x_row[i] = x[i];
+    if (a1_row) {
 #pragma unroll
         for (int i = 0; i < HID / 4; ++i) {
             reinterpret_cast<float4*>(a1_row)[i] =
@@ -312,6 +333,49 @@ __device__ __forceinline__ void decode_forward(const RayPassParams& P, const flo
             reinterpret_cast<float4*>(a2_row)[i] =
                 make_float4(a2[4 * i], a2[4 * i + 1], a2[4 * i + 2], a2[4 * i + 3]);
         }
+    }
+}
+
+// decode_fused (renderer.cpp:88-147): features + MLP.  geo_out (optional)
+// receives the GeoRec block for the backward.
+template <int NS, int NA>
+__device__ __forceinline__ void decode_forward(const RayPassParams& P, const float* __restrict__ sm,
+                                               const SmemMlp& L, int tile, const double p[3],
+                                               const double dneg[3], const float* cam_row,
+                                               float rgb[3], ShadeGeo& geo, float* geo_out) {
+    constexpr int IN = NS + NA + NPOW;
+    float x[IN], pv[3][NS];
+    decode_features<NS, NA>(P, tile, p, dneg, geo, x, pv);
+    mlp_forward<IN>(sm, L, x, cam_row, rgb, nullptr, nullptr);
+    if (geo_out) {
+        using GR = GeoRec<NS, NA>;
+        float r[GR::STRIDE];
+        r[0] = (float)geo.n[0];
+        r[1] = (float)geo.n[1];
+        r[2] = (float)geo.n[2];
+        r[3] = (float)geo.glen;
+        r[4] = geo.refl[0];
+        r[5] = geo.refl[1];
+        r[6] = geo.refl[2];
+        r[7] = geo.ndv;
+        r[8] = geo.tx.f;
+        r[9] = geo.ty.f;
+        r[10] = geo.tz.f;
+        r[11] = __int_as_float(geo.tx.a0 | (geo.ty.a0 << 4) | (geo.tz.a0 << 8) |
+                               (geo.degenerate ? (1 << 12) : 0));
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r[12 + i] = geo.w8[i];
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+#pragma unroll
+            for (int k = 0; k < NS; ++k) r[GR::PV + q * NS + k] = pv[q][k];
+#pragma unroll
+        for (int i = 0; i < IN; ++i) r[GR::X + i] = x[i];
+#pragma unroll
+        for (int i = GR::X + IN; i < GR::STRIDE; ++i) r[i] = 0.f;
+#pragma unroll
+        for (int i = 0; i < GR::STRIDE / 4; ++i)
+            reinterpret_cast<float4*>(geo_out)[i] = make_float4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
     }
 }
 
@@ -357,9 +421,11 @@ __global__ void __launch_bounds__(BLOCK) render_kernel(RayPassParams P) {
     const SmemMlp L = SmemMlp::make(IN);
     const MlpLayout G = MlpLayout::make(IN);
     load_mlp_smem(P.mlp, smem, G, L);
+    const GridView& g = P.g;
+    const uint32_t* bits =
+        stage_tile_bits(g, reinterpret_cast<uint32_t*>(smem + L.total), P.bits_sm_words);
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const GridView& g = P.g;
     unsigned long long c_m = 0, c_x = 0, c_sh = 0;
     const int n_work = (int)(P.tile_end - P.tile_begin);
     for (;;) {
@@ -385,21 +451,24 @@ __global__ void __launch_bounds__(BLOCK) render_kernel(RayPassParams P) {
             Marcher mr;
             double t_cur = 0.0, s_cur = 0.0, a_cur = 0.0;
             int tile_cur = -1;
-            bool active = mr.init(g, V.cam.pos, dd, P.n_max) && mr.next(g, t_cur, tile_cur);
+            int4 tc_cur;
+            bool active = mr.init(g, V.cam.pos, dd, P.n_max) && mr.next(g, t_cur, tile_cur, bits, &tc_cur);
             if (active) {
                 double pc[3];
                 mr.pos(t_cur, pc);
-                s_cur = sample_sdf(g, pc[0], pc[1], pc[2]);
+                s_cur = sample_sdf_in(g, pc[0], pc[1], pc[2], tile_cur, tc_cur);
                 a_cur = sigmoid_d(dmul(P.tau, s_cur));
                 ++c_x;
             }
             while (active) {
                 double t_nxt;
                 int tile_nxt;
-                const bool has_next = mr.next(g, t_nxt, tile_nxt);
+                int4 tc_nxt;
+                const bool has_next = mr.next(g, t_nxt, tile_nxt, bits, &tc_nxt);
                 double pn[3];
                 mr.pos(has_next ? t_nxt : dadd(t_cur, g.h), pn);
-                const double s_nxt = sample_sdf(g, pn[0], pn[1], pn[2]);
+                const double s_nxt = has_next ? sample_sdf_in(g, pn[0], pn[1], pn[2], tile_nxt, tc_nxt)
+                                              : sample_sdf(g, pn[0], pn[1], pn[2]);
                 const double a_nxt = sigmoid_d(dmul(P.tau, s_nxt));
                 const double alpha = alpha_from(a_cur, a_nxt);
                 const double w = dmul(trans, alpha);
@@ -409,7 +478,7 @@ __global__ void __launch_bounds__(BLOCK) render_kernel(RayPassParams P) {
                     float rgb[3];
                     ShadeGeo geo;
                     decode_forward<NS, NA>(P, smem, L, tile_cur, pc, dneg, cam_row, rgb, geo,
-                                           nullptr, nullptr, nullptr);
+                                           nullptr);
                     c0 = dadd(c0, dmul((double)rgb[0], w));
                     c1 = dadd(c1, dmul((double)rgb[1], w));
                     c2 = dadd(c2, dmul((double)rgb[2], w));
@@ -447,6 +516,10 @@ __global__ void __launch_bounds__(BLOCK) render_kernel(RayPassParams P) {
 template <int NS, int NA>
 size_t render_smem_bytes() {
     return sizeof(float) * SmemMlp::make(NS + NA + NPOW).total;
+}
+template <int NS, int NA>
+size_t render_smem_bytes(int bit_words) {
+    return render_smem_bytes<NS, NA>() + sizeof(uint32_t) * bit_words;
 }
 
 }  // namespace psdf

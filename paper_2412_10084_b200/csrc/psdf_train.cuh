@@ -32,6 +32,10 @@
 
 #include "psdf_raypass.cuh"
 
+#ifndef PSDF_MARCH_MINB
+#define PSDF_MARCH_MINB 4
+#endif
+
 namespace psdf {
 
 struct WaveBufs {
@@ -52,6 +56,7 @@ struct WaveBufs {
     int* r_next;       // next record of the same ray, -1 at the end
     float* r_c;        // [cap][4] decoded colour (K2b)
     float* r_up;       // [cap][4] upstream w g (K2d)
+    float* r_geo;      // [cap][GeoRec::STRIDE] geometry + features (K2b -> K2e)
     unsigned* counters;  // [0] entries, [1] records
     int e_cap, r_cap;
 };
@@ -121,9 +126,12 @@ __device__ __forceinline__ bool photo_term(const RayPassParams& P, bool in_mask,
 }
 
 // ------------------------------------------------------------------ K2a
-__global__ void __launch_bounds__(BLOCK) march_fwd_kernel(RayPassParams P, WaveBufs W) {
+__global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPassParams P, WaveBufs W) {
+    extern __shared__ __align__(16) uint32_t sm_bits[];
     const int lane = threadIdx.x & 31;
     const GridView& g = P.g;
+    const uint32_t* bits = stage_tile_bits(g, sm_bits, P.bits_sm_words);
+    __syncthreads();
     const double tau = P.tau;
     double st_photo = 0.0, st_sq = 0.0;
     unsigned long long st_mask = 0, c_m = 0, c_x = 0, c_sh = 0, c_bwd = 0;
@@ -143,53 +151,68 @@ __global__ void __launch_bounds__(BLOCK) march_fwd_kernel(RayPassParams P, WaveB
         int tile_cur = -1, n_live = 0, entry = -1, prev = -1, head = -1;
         double t_first = 0.0;
         int cnt_first = -1;
-        bool active = mr.init(g, R.V->cam.pos, dd, P.n_max) && mr.next(g, t_cur, tile_cur);
-        if (active) {
-            double pc[3];
-            mr.pos(t_cur, pc);
-            a_cur = sigmoid_d(dmul(tau, sample_sdf(g, pc[0], pc[1], pc[2])));
-            ++c_x;
-        }
-        while (active) {
-            double t_nxt;
-            int tile_nxt;
-            const int idx = mr.count - 1;
-            const bool has_next = mr.next(g, t_nxt, tile_nxt);
+        bool have_cur = false;
+        bool alive = mr.init(g, R.V->cam.pos, dd, P.n_max);
+        // One sample per iteration (single call sites keep the loop small):
+        // fetch the next march sample (or the one-past-the-end position),
+        // evaluate its sigmoid, then settle the alpha of the previous sample.
+        while (alive) {
+            double t_nxt = 0.0;
+            int tile_nxt = -1;
+            int4 tc_nxt;
+            const int idx = mr.count - 1;  // index of t_cur
+            const bool has_next = mr.next(g, t_nxt, tile_nxt, bits, &tc_nxt);
+            if (!has_next && !have_cur) break;  // no sample at all
             double pn[3];
             mr.pos(has_next ? t_nxt : dadd(t_cur, g.h), pn);
-            const double a_nxt = sigmoid_d(dmul(tau, sample_sdf(g, pn[0], pn[1], pn[2])));
-            const double alpha = alpha_from(a_cur, a_nxt);
-            const double w = dmul(trans, alpha);
-            if (alpha > 0.0 && cnt_first < 0) {
-                cnt_first = idx;
-                t_first = t_cur;
-            }
-            const bool want_entry = alpha > 0.0 && entry < 0;
-            const int e = warp_alloc(W.counters + 0, want_entry, lane);
-            if (want_entry) entry = e < W.e_cap ? e : -2;  // -2: overflow, host retries
-            const bool shade = in_mask && w > 0.0 && tile_cur >= 0;
-            const int r = warp_alloc(W.counters + 1, shade, lane);
-            if (shade) {
-                ++c_sh;
-                if (r < W.r_cap && entry >= 0) {
-                    double pc[3];
-                    mr.pos(t_cur, pc);
-                    W.r_pos[3 * (int64_t)r] = pc[0];
-                    W.r_pos[3 * (int64_t)r + 1] = pc[1];
-                    W.r_pos[3 * (int64_t)r + 2] = pc[2];
-                    W.r_w[r] = w;
-                    W.r_tile[r] = tile_cur;
-                    W.r_entry[r] = entry;
-                    W.r_next[r] = -1;
-                    if (prev >= 0) W.r_next[prev] = r;
-                    else head = r;
-                    prev = r;
+            const double s_nxt = has_next ? sample_sdf_in(g, pn[0], pn[1], pn[2], tile_nxt, tc_nxt)
+                                          : sample_sdf(g, pn[0], pn[1], pn[2]);
+            const double a_nxt = sigmoid_d(dmul(tau, s_nxt));
+            if (!have_cur) {
+                have_cur = true;
+                ++c_x;
+            } else {
+                const double alpha = alpha_from(a_cur, a_nxt);
+                const double w = dmul(trans, alpha);
+                if (alpha > 0.0 && cnt_first < 0) {
+                    cnt_first = idx;
+                    t_first = t_cur;
                 }
+                const bool want_entry = alpha > 0.0 && entry < 0;
+#ifdef PSDF_ABL_NOALLOC
+                const int e = want_entry ? atomicAdd(W.counters + 0, 1u) : -1;
+#else
+                const int e = warp_alloc(W.counters + 0, want_entry, lane);
+#endif
+                if (want_entry) entry = e < W.e_cap ? e : -2;  // -2: overflow, host retries
+                const bool shade = in_mask && w > 0.0 && tile_cur >= 0;
+#ifdef PSDF_ABL_NOALLOC
+                const int r = shade ? atomicAdd(W.counters + 1, 1u) : -1;
+#else
+                const int r = warp_alloc(W.counters + 1, shade, lane);
+#endif
+                if (shade) {
+                    ++c_sh;
+                    if (r < W.r_cap && entry >= 0) {
+                        double pc[3];
+                        mr.pos(t_cur, pc);
+                        W.r_pos[3 * (int64_t)r] = pc[0];
+                        W.r_pos[3 * (int64_t)r + 1] = pc[1];
+                        W.r_pos[3 * (int64_t)r + 2] = pc[2];
+                        W.r_w[r] = w;
+                        W.r_tile[r] = tile_cur;
+                        W.r_entry[r] = entry;
+                        W.r_next[r] = -1;
+                        if (prev >= 0) W.r_next[prev] = r;
+                        else head = r;
+                        prev = r;
+                    }
+                }
+                acc = dadd(acc, w);
+                trans = dmul(trans, dsub(1.0, alpha));
+                ++n_live;
+                if ((P.early_stop > 0.0 && trans < P.early_stop) || !has_next) break;
             }
-            acc = dadd(acc, w);
-            trans = dmul(trans, dsub(1.0, alpha));
-            ++n_live;
-            if ((P.early_stop > 0.0 && trans < P.early_stop) || !has_next) break;
             t_cur = t_nxt;
             tile_cur = tile_nxt;
             a_cur = a_nxt;
@@ -264,8 +287,8 @@ __global__ void __launch_bounds__(BLOCK) shade_fwd_kernel(RayPassParams P, WaveB
                                 -W.e_dir[3 * (int64_t)e + 2]};
         float rgb[3];
         ShadeGeo geo;
-        decode_forward<NS, NA>(P, smem, L, W.r_tile[i], pc, dneg, cam_row, rgb, geo, nullptr,
-                               nullptr, nullptr);
+        decode_forward<NS, NA>(P, smem, L, W.r_tile[i], pc, dneg, cam_row, rgb, geo,
+                               W.r_geo + (int64_t)i * GeoRec<NS, NA>::STRIDE);
         reinterpret_cast<float4*>(W.r_c)[i] = make_float4(rgb[0], rgb[1], rgb[2], 0.f);
         const double w = W.r_w[i];
         atomicAdd(W.e_craw + 3 * (int64_t)e, dmul((double)rgb[0], w));
@@ -275,9 +298,12 @@ __global__ void __launch_bounds__(BLOCK) shade_fwd_kernel(RayPassParams P, WaveB
 }
 
 // ------------------------------------------------------------------ K2d
-__global__ void __launch_bounds__(BLOCK) alpha_bwd_kernel(RayPassParams P, WaveBufs W, int n_ent) {
+__global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) alpha_bwd_kernel(RayPassParams P, WaveBufs W, int n_ent) {
+    extern __shared__ __align__(16) uint32_t sm_bits[];
     const int lane = threadIdx.x & 31;
     const GridView& g = P.g;
+    const uint32_t* bits = stage_tile_bits(g, sm_bits, P.bits_sm_words);
+    __syncthreads();
     const double tau = P.tau;
     double st_photo = 0.0, st_sq = 0.0;
     unsigned long long st_mask = 0, c_al = 0, c_bwd = 0;
@@ -315,19 +341,23 @@ __global__ void __launch_bounds__(BLOCK) alpha_bwd_kernel(RayPassParams P, WaveB
         const int n_live = W.e_nlive[e];
         double t_cur = 0.0;
         int tile_cur = -1;
-        mr.next(g, t_cur, tile_cur);  // re-emits the first alpha > 0 sample
+        int4 tc_cur;
+        mr.next(g, t_cur, tile_cur, bits, &tc_cur);  // re-emits the first alpha > 0 sample
         double pc[3];
         mr.pos(t_cur, pc);
-        double a_cur = sigmoid_d(dmul(tau, sample_sdf(g, pc[0], pc[1], pc[2])));
+        double a_cur = sigmoid_d(dmul(tau, sample_sdf_in(g, pc[0], pc[1], pc[2], tile_cur, tc_cur)));
         double T = 1.0, pre = 0.0, carry = 0.0;
         int idx = W.e_cfirst[e];
         for (;;) {
             double t_nxt = 0.0;
             int tile_nxt = -1;
-            const bool has_next = mr.next(g, t_nxt, tile_nxt);
+            int4 tc_nxt;
+            const bool has_next = mr.next(g, t_nxt, tile_nxt, bits, &tc_nxt);
             double pn[3];
             mr.pos(has_next ? t_nxt : dadd(t_cur, g.h), pn);
-            const double a_nxt = sigmoid_d(dmul(tau, sample_sdf(g, pn[0], pn[1], pn[2])));
+            const double s_nxt = has_next ? sample_sdf_in(g, pn[0], pn[1], pn[2], tile_nxt, tc_nxt)
+                                          : sample_sdf(g, pn[0], pn[1], pn[2]);
+            const double a_nxt = sigmoid_d(dmul(tau, s_nxt));
             const double alpha = alpha_from(a_cur, a_nxt);
             const double w = dmul(T, alpha);
             if (alpha > 0.0) ++c_al;
@@ -423,16 +453,59 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
         double pc[3] = {0, 0, 0}, dneg[3] = {0, 0, 0};
         float rgb[3] = {0.f, 0.f, 0.f};
         ShadeGeo geo;
+        float pv[3][NS];
         if (shade) {
+            using GR = GeoRec<NS, NA>;
             pc[0] = W.r_pos[3 * (int64_t)i];
             pc[1] = W.r_pos[3 * (int64_t)i + 1];
             pc[2] = W.r_pos[3 * (int64_t)i + 2];
             dneg[0] = -W.e_dir[3 * (int64_t)e];
             dneg[1] = -W.e_dir[3 * (int64_t)e + 1];
             dneg[2] = -W.e_dir[3 * (int64_t)e + 2];
+            // geometry and features of the forward decode (stored by K2b)
+            float r[GR::STRIDE];
+            const float4* src = reinterpret_cast<const float4*>(W.r_geo + (int64_t)i * GR::STRIDE);
+#pragma unroll
+            for (int q = 0; q < GR::STRIDE / 4; ++q) {
+                const float4 v4 = src[q];
+                r[4 * q] = v4.x;
+                r[4 * q + 1] = v4.y;
+                r[4 * q + 2] = v4.z;
+                r[4 * q + 3] = v4.w;
+            }
+            geo.n[0] = r[0];
+            geo.n[1] = r[1];
+            geo.n[2] = r[2];
+            geo.glen = r[3];
+            geo.refl[0] = r[4];
+            geo.refl[1] = r[5];
+            geo.refl[2] = r[6];
+            geo.ndv = r[7];
+            const int packed = __float_as_int(r[11]);
+            geo.tx = Tap{packed & 15, r[8]};
+            geo.ty = Tap{(packed >> 4) & 15, r[9]};
+            geo.tz = Tap{(packed >> 8) & 15, r[10]};
+            geo.degenerate = (packed >> 12) & 1;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) geo.w8[c] = r[12 + c];
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+#pragma unroll
+                for (int k = 0; k < NS; ++k) pv[q][k] = r[GR::PV + q * NS + k];
+            float x[IN];
+#pragma unroll
+            for (int q = 0; q < IN; ++q) {
+                x[q] = r[GR::X + q];
+                X[lane * SD::XS + q] = x[q];
+            }
+            const float4 cr = reinterpret_cast<const float4*>(W.r_c)[i];
+            rgb[0] = cr.x;
+            rgb[1] = cr.y;
+            rgb[2] = cr.z;
+            // the MLP forward is recomputed (its activations are not stored)
             const float* cam_row = cam_bias_row >= 0 ? P.mlp + G.cam + cam_bias_row * HID : nullptr;
-            decode_forward<NS, NA>(P, s_mlp, L, tile, pc, dneg, cam_row, rgb, geo,
-                                   X + lane * SD::XS, A1 + lane * RS, A2 + lane * RS);
+            float rgb2[3];
+            mlp_forward<IN>(s_mlp, L, x, cam_row, rgb2, A1 + lane * RS, A2 + lane * RS);
         }
         // ---- decode_backward (decoder.cpp:111-176), warp-cooperative
         float dz3[3];
@@ -603,25 +676,9 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
                 }
                 d_ndotv = -du;
             }
-            // tri-plane backward (grid.cpp:189-202)
+            // tri-plane backward (grid.cpp:189-202), plane samples from the record
             if (!P.no_spatial) {
-                const float* pl = g.planes + (int64_t)tile * 3 * 256 * NS;
                 float* gpl = P.g_planes + (int64_t)tile * 3 * 256 * NS;
-                float pv[3][NS];
-#pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    const Tap ta = q == 0 ? geo.ty : geo.tx;
-                    const Tap tb = q == 2 ? geo.ty : geo.tz;
-                    const float* bp = pl + q * 256 * NS;
-                    const VecF<NS> v00 = ldg_vec<NS>(bp + (ta.a0 * TE + tb.a0) * NS);
-                    const VecF<NS> v01 = ldg_vec<NS>(bp + (ta.a0 * TE + tb.a0 + 1) * NS);
-                    const VecF<NS> v10 = ldg_vec<NS>(bp + ((ta.a0 + 1) * TE + tb.a0) * NS);
-                    const VecF<NS> v11 = ldg_vec<NS>(bp + ((ta.a0 + 1) * TE + tb.a0 + 1) * NS);
-#pragma unroll
-                    for (int k = 0; k < NS; ++k)
-                        pv[q][k] = (1.f - ta.f) * ((1.f - tb.f) * v00.v[k] + tb.f * v01.v[k]) +
-                                   ta.f * ((1.f - tb.f) * v10.v[k] + tb.f * v11.v[k]);
-                }
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
                     const Tap ta = q == 0 ? geo.ty : geo.tx;
