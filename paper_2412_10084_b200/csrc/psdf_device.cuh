@@ -297,15 +297,16 @@ __device__ __noinline__ void exact_tile(const GridView& g, const double o[3], co
 //
 // t is advanced with exactly the reference's f64 additions.  The two integer
 // decisions taken per iteration — which tile p(t) lies in, and the skip count
-// ceil((e1 - t)/h + 1e-9) past an empty tile — are first evaluated in f32 in
-// voxel units (v = (o - org)/h + (d/h) t); when the f32 value is farther than
-// a margin (>= 10x its error bound) from the decision boundary the result is
-// provably the exact one, otherwise the exact f64 path decides.
+// ceil((e1 - t)/h + 1e-9) past an empty tile — are first evaluated with a
+// cheap FMA form in voxel units, v = (o - org)/h + (d/h) t, whose error is
+// ~1e-12 voxel; when the value is farther than a 1e-8 margin from the
+// decision boundary the result is provably the reference's, otherwise the
+// exact f64 path decides.
 struct Marcher {
     double o[3], d[3], inv_d[3];
     double t, t1;
     int count, n_max;
-    float vo[3], vd[3], rd[3];  // (o - org)/h, d/h, 1/d in f32
+    double vo[3], vd[3];  // (o - org)/h, d/h
 
     __device__ __forceinline__ bool init(const GridView& g, const double* o_, const double* d_,
                                          int nmax) {
@@ -315,9 +316,8 @@ struct Marcher {
             o[a] = o_[a];
             d[a] = d_[a];
             inv_d[a] = fabs(d[a]) < 1e-15 ? 0.0 : __drcp_rn(d[a]);
-            vo[a] = (float)((o[a] - g.org[a]) * inv_h);
-            vd[a] = (float)(d[a] * inv_h);
-            rd[a] = fabs(d[a]) < 1e-15 ? 0.f : (float)inv_d[a];
+            vo[a] = (o[a] - g.org[a]) * inv_h;
+            vd[a] = d[a] * inv_h;
         }
         n_max = nmax;
         count = 0;
@@ -337,22 +337,19 @@ struct Marcher {
     __device__ __forceinline__ bool next(const GridView& g, double& t_out, int& tile_out,
                                          const uint32_t* bits, int4* tc_out = nullptr) {
         const double h = g.h;
+        constexpr double kMargin = 1e-8;  // voxels; the FMA form is within ~1e-12
         while (t < t1 && count < n_max) {
-            // --- tile of p(t): f32 fast path
-            const float tf = (float)t;
-            float v[3], ev[3];
+            // --- tile of p(t)
+            double v[3];
             int tc[3];
             bool near = false;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                v[a] = fmaf(vd[a], tf, vo[a]);
-                // error bound of v: roundings of vo, vd, tf and the fma, each
-                // <= 2^-24 of the magnitudes involved (plus a floor for tiny ones)
-                ev[a] = 1e-5f + 2.5e-7f * (fabsf(vo[a]) + fabsf(vd[a] * tf) + fabsf(v[a]));
-                const float r16 = v[a] * 0.0625f;
-                const float dist = fabsf(r16 - rintf(r16)) * 16.f;
-                near |= dist < 16.f * ev[a];
-                tc[a] = ((int)floorf(v[a])) >> 4;
+                v[a] = fma(vd[a], t, vo[a]);
+                const double fl16 = floor(v[a] * 0.0625);
+                const double r = v[a] - 16.0 * fl16;  // position inside the tile, [0, 16)
+                near |= r < kMargin || r > 16.0 - kMargin;
+                tc[a] = (int)fl16;
             }
             if (near) exact_tile(g, o, d, t, tc);
             bool occupied = false;
@@ -369,34 +366,22 @@ struct Marcher {
                 ++count;
                 return true;
             }
-            // --- skip the empty tile: f32 fast path for the skip count.  p(t)
-            // is inside the tile and off its faces (not `near`), so the box
-            // test passes and e1 > t; q = (e1 - t)/h = min_a (B_a - v_a)/d_a.
-            bool fast = !near;
-            float q = 3.0e38f;
-            int qa = -1;
+            // --- skip the empty tile.  p(t) is inside the tile and off its
+            // faces (not `near`), so the box test passes and e1 > t; the skip
+            // is ceil(q + 1e-9) with q = (e1 - t)/h = min_a (B_a - v_a) / d_a.
+            double q = 1e300, rmax = 0.0;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                if (rd[a] == 0.f) continue;
-                const float B = 16.f * (float)(tc[a] + (d[a] > 0.0 ? 1 : 0));
-                const float qq = (B - v[a]) * rd[a];
-                if (qq < q) {
-                    q = qq;
-                    qa = a;
-                }
+                if (inv_d[a] == 0.0) continue;
+                const double B = 16.0 * (double)(tc[a] + (d[a] > 0.0 ? 1 : 0));
+                q = fmin(q, (B - v[a]) * inv_d[a]);
+                rmax = fmax(rmax, fabs(inv_d[a]));
             }
-            if (fast && qa >= 0) {
-                // q error: ev * |1/d| plus the roundings of the subtraction,
-                // 1/d and the product (~3 ulp of the magnitudes)
-                const float err = (ev[qa] + 16.f * 6e-8f * fabsf(v[qa])) * fabsf(rd[qa]) + q * 4e-7f + 1e-6f;
-                const float fq = q - floorf(q);
-                if (fq <= 8.f * err || fq >= 1.f - 8.f * err) fast = false;
-            } else {
-                fast = false;
-            }
-            if (fast) {
-                const float k = ceilf(q);  // + 1e-9 is inside the margin
-                t = dadd(t, dmul(k > 1.f ? (double)k : 1.0, h));
+            const double fq = q - floor(q);
+            const double mq = kMargin + 1e-11 * rmax;  // q error <~ 1e-12 |1/d|
+            if (!near && q < 1e300 && fq > mq && fq < 1.0 - mq) {
+                const double k = ceil(q);  // the + 1e-9 is inside the margin
+                t = dadd(t, dmul(k > 1.0 ? k : 1.0, h));
                 continue;
             }
             t = skip_tile(g, o, d, inv_d, tc, t);
