@@ -450,6 +450,11 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
         CK(cudaEventRecord(c->ev_k[0], s));
     }
     const int n_ent = (int)c->h_wave_counters[0], n_rec = (int)c->h_wave_counters[1];
+    if (getenv("PSDF_DEBUG_MARCH")) {
+        unsigned long long cc[8];
+        CK(cudaMemcpy(cc, c->d_counts, sizeof cc, cudaMemcpyDeviceToHost));
+        fprintf(stderr, "[psdf] march exact fallbacks: %llu\n", cc[6]);
+    }
     c->last_entries = n_ent;
     c->last_records = n_rec;
     CK(cudaEventRecord(c->ev_k[1], s));

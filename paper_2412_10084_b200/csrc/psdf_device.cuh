@@ -87,13 +87,6 @@ __device__ __forceinline__ double smooth_value(const GridView& g, int vx, int vy
     return (double)__ldg(g.smooth + (int64_t)t * TV + vox_index(vx & 15, vy & 15, vz & 15));
 }
 
-// The 8 trilinear corners when they straddle tiles / the grid boundary.
-__device__ __noinline__ void corners_slow(const GridView& g, int bx, int by, int bz, double c[8]) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-        c[i] = smooth_value(g, bx + (i & 1), by + ((i >> 1) & 1), bz + ((i >> 2) & 1));
-}
-
 constexpr int AE = 18;            // apron brick edge (16 + 2)
 constexpr int AV = AE * AE * AE;  // 5832
 
@@ -130,46 +123,63 @@ __device__ __forceinline__ double sample_sdf_in(const GridView& g, double px, do
     return trilerp8(fx, fy, fz, c);
 }
 
+// The fields the out-of-line exact paths need, passed by value: handing
+// them the kernel-parameter GridView by reference would force a local copy
+// of the whole parameter block (and local-memory reads in the hot loops).
+struct GridLite {
+    const int32_t* tile_table;
+    const float* smooth;
+    double org[3], h, inv_h, far;
+    int nt[3], res[3], h_pow2;
+};
+__device__ __forceinline__ GridLite lite(const GridView& g) {
+    GridLite l;
+    l.tile_table = g.tile_table;
+    l.smooth = g.smooth;
+    for (int a = 0; a < 3; ++a) {
+        l.org[a] = g.org[a];
+        l.nt[a] = g.nt[a];
+        l.res[a] = g.res[a];
+    }
+    l.h = g.h;
+    l.inv_h = g.inv_h;
+    l.far = g.far;
+    l.h_pow2 = g.h_pow2;
+    return l;
+}
+
+// sample_trilinear with per-corner lookups (corners straddling tiles or the
+// grid boundary).  Out of line, arguments by value (no pointer escapes).
+__device__ __noinline__ double sample_slow(GridLite g, int bx, int by, int bz, double fx,
+                                           double fy, double fz) {
+    double c[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int vx = bx + (i & 1), vy = by + ((i >> 1) & 1), vz = bz + ((i >> 2) & 1);
+        double v = g.far;  // smooth_value (grid.cpp:87-94)
+        if (vx >= 0 && vy >= 0 && vz >= 0 && vx < g.res[0] && vy < g.res[1] && vz < g.res[2]) {
+            const int t = __ldg(g.tile_table + ((int64_t)(vx >> 4) * g.nt[1] + (vy >> 4)) * g.nt[2] + (vz >> 4));
+            if (t >= 0) v = (double)__ldg(g.smooth + (int64_t)t * TV + vox_index(vx & 15, vy & 15, vz & 15));
+        }
+        c[i] = v;
+    }
+    return trilerp8(fx, fy, fz, c);
+}
+
 // sample_sdf (grid.cpp:98-125), exact f64, for an arbitrary point: one table
 // lookup finds the containing tile; outside allocated tiles the corners are
 // fetched one by one.
 __device__ __forceinline__ double sample_sdf(const GridView& g, double px, double py, double pz) {
-    {
-        const double vx = w2v(g, px, 0), vy = w2v(g, py, 1), vz = w2v(g, pz, 2);
-        const int ix = (int)floor(vx), iy = (int)floor(vy), iz = (int)floor(vz);
-        if (ix >= 0 && iy >= 0 && iz >= 0 && ix < g.res[0] && iy < g.res[1] && iz < g.res[2]) {
-            const int t = tile_lookup(g, ix >> 4, iy >> 4, iz >> 4);
-            if (t >= 0) return sample_sdf_in(g, px, py, pz, t, make_int4(ix >> 4, iy >> 4, iz >> 4, 0));
-        }
+    const double vx = w2v(g, px, 0), vy = w2v(g, py, 1), vz = w2v(g, pz, 2);
+    const int ix = (int)floor(vx), iy = (int)floor(vy), iz = (int)floor(vz);
+    if (ix >= 0 && iy >= 0 && iz >= 0 && ix < g.res[0] && iy < g.res[1] && iz < g.res[2]) {
+        const int t = tile_lookup(g, ix >> 4, iy >> 4, iz >> 4);
+        if (t >= 0) return sample_sdf_in(g, px, py, pz, t, make_int4(ix >> 4, iy >> 4, iz >> 4, 0));
     }
-    const double cx = dsub(w2v(g, px, 0), 0.5);
-    const double cy = dsub(w2v(g, py, 1), 0.5);
-    const double cz = dsub(w2v(g, pz, 2), 0.5);
-    const double flx = floor(cx), fly = floor(cy), flz = floor(cz);
-    const int bx = (int)flx, by = (int)fly, bz = (int)flz;
-    const double fx = dsub(cx, (double)bx), fy = dsub(cy, (double)by), fz = dsub(cz, (double)bz);
-    const double gx0 = dsub(1.0, fx), gy0 = dsub(1.0, fy), gz0 = dsub(1.0, fz);
-    double c[8];
-    const bool one_tile = bx >= 0 && by >= 0 && bz >= 0 && bx + 1 < g.res[0] &&
-                          by + 1 < g.res[1] && bz + 1 < g.res[2] && (bx & 15) != 15 &&
-                          (by & 15) != 15 && (bz & 15) != 15;
-    int t = -1;
-    if (one_tile) t = tile_lookup(g, bx >> 4, by >> 4, bz >> 4);
-    if (t >= 0) {
-        const float* base = g.smooth + (int64_t)t * TV + vox_index(bx & 15, by & 15, bz & 15);
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-            c[i] = (double)__ldg(base + (i & 1) * 256 + ((i >> 1) & 1) * 16 + ((i >> 2) & 1));
-    } else {
-        corners_slow(g, bx, by, bz, c);
-    }
-    double v = 0.0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const double w = dmul(dmul((i & 1) ? fx : gx0, (i & 2) ? fy : gy0), (i & 4) ? fz : gz0);
-        v = dadd(v, dmul(w, c[i]));
-    }
-    return v;
+    const double cx = dsub(vx, 0.5), cy = dsub(vy, 0.5), cz = dsub(vz, 0.5);
+    const int bx = (int)floor(cx), by = (int)floor(cy), bz = (int)floor(cz);
+    return sample_slow(lite(g), bx, by, bz, dsub(cx, (double)bx), dsub(cy, (double)by),
+                       dsub(cz, (double)bz));
 }
 
 // ------------------------------------------------------------ camera + march
@@ -189,31 +199,42 @@ __device__ __noinline__ D3 pixel_dir(const Cam& c, double u, double v) {
     return d3(ddiv(q.x, n), ddiv(q.y, n), ddiv(q.z, n));
 }
 
-// ray_box (renderer.cpp:13-31).  Out of line: it runs once per ray and on
-// the rare exact fallbacks, and its six f64 divisions would bloat every
-// inlined march loop.
-__device__ __noinline__ bool ray_box(const double o[3], const double d[3], const double mn[3],
-                                        const double mx[3], double& t0, double& t1) {
-    t0 = 0.0;
-    t1 = 1.7976931348623157e308;
+// ray_box (renderer.cpp:13-31), by value: no pointer to the caller's
+// arrays escapes (that would force them into local memory).
+struct BoxHit {
+    bool ok;
+    double t0, t1;
+};
+__device__ __forceinline__ BoxHit ray_box_inl(D3 o, D3 d, D3 mn, D3 mx) {
+    BoxHit r{true, 0.0, 1.7976931348623157e308};
+    const double oo[3] = {o.x, o.y, o.z}, dd[3] = {d.x, d.y, d.z};
+    const double lo[3] = {mn.x, mn.y, mn.z}, hi[3] = {mx.x, mx.y, mx.z};
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        if (fabs(d[a]) < 1e-15) {
-            if (o[a] < mn[a] || o[a] > mx[a]) return false;
+        if (fabs(dd[a]) < 1e-15) {
+            if (oo[a] < lo[a] || oo[a] > hi[a]) {
+                r.ok = false;
+                return r;
+            }
             continue;
         }
-        double ta = ddiv(dsub(mn[a], o[a]), d[a]), tb = ddiv(dsub(mx[a], o[a]), d[a]);
+        double ta = ddiv(dsub(lo[a], oo[a]), dd[a]), tb = ddiv(dsub(hi[a], oo[a]), dd[a]);
         if (ta > tb) {
             const double s = ta;
             ta = tb;
             tb = s;
         }
-        t0 = (t0 < ta) ? ta : t0;  // std::max
-        t1 = (tb < t1) ? tb : t1;  // std::min
-        if (t0 > t1) return false;
+        r.t0 = (r.t0 < ta) ? ta : r.t0;  // std::max
+        r.t1 = (tb < r.t1) ? tb : r.t1;  // std::min
+        if (r.t0 > r.t1) {
+            r.ok = false;
+            return r;
+        }
     }
-    return true;
+    return r;
 }
+// Out of line (runs once per ray; six f64 divisions).
+__device__ __noinline__ BoxHit ray_box(D3 o, D3 d, D3 mn, D3 mx) { return ray_box_inl(o, d, mn, mx); }
 
 // Copies the tile occupancy bitmap into shared memory (call before a
 // __syncthreads) and returns the pointer the marcher should use.
@@ -224,72 +245,34 @@ __device__ __forceinline__ const uint32_t* stage_tile_bits(const GridView& g, ui
     return sm_bits;
 }
 
-// Exit distance of the ray from an (unallocated) tile box and the skip
-// decision of renderer.cpp:73-82, computed with reciprocal multiplies.  The
-// reference divides, (mn - o) / d; the product with the correctly rounded
-// reciprocal is within ~2 ulp of it.  Every decision the result feeds (the
-// box test t0 <= t1, e1 > t, and the integer ceil((e1 - t) / h + 1e-9)) is
-// taken on the fast value only when it is farther than a safe margin from
-// the decision boundary; otherwise the exact ray_box reruns.  So the emitted
-// t-list is bit-identical to the reference's either way.
-// Returns the new t.
-__device__ __noinline__ double skip_tile(const GridView& g, const double o[3],
-                                         const double d[3], const double inv_d[3], const int tc[3],
-                                         double t) {
+// The reference's skip past an unallocated tile (renderer.cpp:73-82), exactly:
+// ray_box against the tile, then t += max(1, ceil((e1 - t)/h + 1e-9)) h.
+// Out of line: only taken when the fast form is within its error margin.
+__device__ __noinline__ double exact_skip(GridLite g, D3 o, D3 d, int tx, int ty, int tz,
+                                          double t) {
     const double h = g.h;
-    const double tile_w = dmul(16.0, h);  // renderer.cpp:74-75
-    const double bmin[3] = {dadd(g.org[0], dmul((double)tc[0], tile_w)),
-                            dadd(g.org[1], dmul((double)tc[1], tile_w)),
-                            dadd(g.org[2], dmul((double)tc[2], tile_w))};
-    const double bmax[3] = {dadd(bmin[0], tile_w), dadd(bmin[1], tile_w), dadd(bmin[2], tile_w)};
-    bool ok = true, exact = false;
-    double t0 = 0.0, t1 = 1.7976931348623157e308;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        if (fabs(d[a]) < 1e-15) {
-            if (o[a] < bmin[a] || o[a] > bmax[a]) ok = false;
-            continue;
-        }
-        double ta = dmul(dsub(bmin[a], o[a]), inv_d[a]), tb = dmul(dsub(bmax[a], o[a]), inv_d[a]);
-        if (ta > tb) {
-            const double s = ta;
-            ta = tb;
-            tb = s;
-        }
-        t0 = (t0 < ta) ? ta : t0;
-        t1 = (tb < t1) ? tb : t1;
-    }
-    const double m = 1e-12 * (fabs(t) + 1.0);  // >> the ~1e-15 relative error
-    const double mq = m * (g.h_pow2 ? g.inv_h : 1.0 / g.h);
-    if (ok && fabs(t0 - t1) <= m) exact = true;
-    ok = ok && t0 <= t1;
-    double q = 0.0;
-    if (!exact && ok) {
-        if (fabs(t1 - t) <= m) exact = true;
-        else if (t1 > t) {
-            q = dadd(div_h(g, dsub(t1, t)), 1e-9);
-            const double fq = q - floor(q);
-            if (fq <= mq || fq >= 1.0 - mq) exact = true;
-        }
-    }
-    if (exact) {  // rare: redo with the reference's divisions
-        double e0, e1;
-        ok = ray_box(o, d, bmin, bmax, e0, e1);
-        t1 = e1;
-        if (ok && e1 > t) q = dadd(div_h(g, dsub(e1, t)), 1e-9);
-    }
-    if (ok && t1 > t) {
-        const double skip = ceil(q);
+    auto div_h = [&](double x) { return g.h_pow2 ? dmul(x, g.inv_h) : ddiv(x, g.h); };
+    const double tile_w = dmul(16.0, h);
+    const D3 bmin = d3(dadd(g.org[0], dmul((double)tx, tile_w)), dadd(g.org[1], dmul((double)ty, tile_w)),
+                       dadd(g.org[2], dmul((double)tz, tile_w)));
+    const D3 bmax = d3(dadd(bmin.x, tile_w), dadd(bmin.y, tile_w), dadd(bmin.z, tile_w));
+    const BoxHit b = ray_box_inl(o, d, bmin, bmax);
+    if (b.ok && b.t1 > t) {
+        const double skip = ceil(dadd(div_h(dsub(b.t1, t)), 1e-9));
         return dadd(t, dmul(skip > 1.0 ? skip : 1.0, h));
     }
     return dadd(t, h);
 }
 
 // Tile of p(t) exactly as the reference computes it: floor((o + t d - org)/h) >> 4.
-__device__ __noinline__ void exact_tile(const GridView& g, const double o[3], const double d[3],
-                                        double t, int tc[3]) {
-#pragma unroll
-    for (int a = 0; a < 3; ++a) tc[a] = ((int)floor(w2v(g, dadd(o[a], dmul(d[a], t)), a))) >> 4;
+__device__ __noinline__ int4 exact_tile(GridLite g, D3 o, D3 d, double t) {
+    auto w2v_ = [&](double p, int a) {
+        const double x = dsub(p, g.org[a]);
+        return g.h_pow2 ? dmul(x, g.inv_h) : ddiv(x, g.h);
+    };
+    return make_int4(((int)floor(w2v_(dadd(o.x, dmul(d.x, t)), 0))) >> 4,
+                     ((int)floor(w2v_(dadd(o.y, dmul(d.y, t)), 1))) >> 4,
+                     ((int)floor(w2v_(dadd(o.z, dmul(d.z, t)), 2))) >> 4, 0);
 }
 
 // march_ray (renderer.cpp:55-86) as a resumable generator: the state is
@@ -307,6 +290,7 @@ struct Marcher {
     double t, t1;
     int count, n_max;
     double vo[3], vd[3];  // (o - org)/h, d/h
+    unsigned n_exact;     // exact-path fallbacks taken (diagnostics)
 
     __device__ __forceinline__ bool init(const GridView& g, const double* o_, const double* d_,
                                          int nmax) {
@@ -321,13 +305,16 @@ struct Marcher {
         }
         n_max = nmax;
         count = 0;
-        double t0;
-        if (!ray_box(o, d, g.org, g.wmax, t0, t1)) {
+        n_exact = 0;
+        const BoxHit b = ray_box(d3(o[0], o[1], o[2]), d3(d[0], d[1], d[2]),
+                                 d3(g.org[0], g.org[1], g.org[2]), d3(g.wmax[0], g.wmax[1], g.wmax[2]));
+        if (!b.ok) {
             t = 0.0;
             t1 = -1.0;
             return false;
         }
-        t = dadd(t0, dmul(0.5, g.h));
+        t1 = b.t1;
+        t = dadd(b.t0, dmul(0.5, g.h));
         return true;
     }
 
@@ -351,7 +338,13 @@ struct Marcher {
                 near |= r < kMargin || r > 16.0 - kMargin;
                 tc[a] = (int)fl16;
             }
-            if (near) exact_tile(g, o, d, t, tc);
+            if (near) {
+                const int4 e = exact_tile(lite(g), d3(o[0], o[1], o[2]), d3(d[0], d[1], d[2]), t);
+                tc[0] = e.x;
+                tc[1] = e.y;
+                tc[2] = e.z;
+                ++n_exact;
+            }
             bool occupied = false;
             if ((unsigned)tc[0] < (unsigned)g.nt[0] && (unsigned)tc[1] < (unsigned)g.nt[1] &&
                 (unsigned)tc[2] < (unsigned)g.nt[2]) {
@@ -384,7 +377,8 @@ struct Marcher {
                 t = dadd(t, dmul(k > 1.0 ? k : 1.0, h));
                 continue;
             }
-            t = skip_tile(g, o, d, inv_d, tc, t);
+            t = exact_skip(lite(g), d3(o[0], o[1], o[2]), d3(d[0], d[1], d[2]), tc[0], tc[1], tc[2], t);
+            ++n_exact;
         }
         return false;
     }

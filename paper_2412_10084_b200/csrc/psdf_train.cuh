@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
     __syncthreads();
     const double tau = P.tau;
     double st_photo = 0.0, st_sq = 0.0;
-    unsigned long long st_mask = 0, c_m = 0, c_x = 0, c_sh = 0, c_bwd = 0;
+    unsigned long long st_mask = 0, c_m = 0, c_x = 0, c_sh = 0, c_bwd = 0, c_ex = 0;
     const int n_work = (int)(P.tile_end - P.tile_begin);
     for (;;) {
         int wi = 0;
@@ -142,9 +142,8 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
         wi = __shfl_sync(FULL, wi, 0);
         if (wi >= n_work) break;
         const LaneRay R = lane_ray(P, wi, lane);
-        if (!R.valid) continue;
-        const bool in_mask = __ldg(R.V->mask + R.px) != 0;
-        const D3 dir = pixel_dir(R.V->cam, (double)R.u + 0.5, (double)R.v + 0.5);
+        const bool in_mask = R.valid && __ldg(R.V->mask + R.px) != 0;
+        const D3 dir = R.valid ? pixel_dir(R.V->cam, (double)R.u + 0.5, (double)R.v + 0.5) : d3(0, 0, 1);
         const double dd[3] = {dir.x, dir.y, dir.z};
         Marcher mr;
         double t_cur = 0.0, a_cur = 0.0, acc = 0.0, trans = 1.0;
@@ -152,47 +151,63 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
         double t_first = 0.0;
         int cnt_first = -1;
         bool have_cur = false;
-        bool alive = mr.init(g, R.V->cam.pos, dd, P.n_max);
-        // One sample per iteration (single call sites keep the loop small):
-        // fetch the next march sample (or the one-past-the-end position),
-        // evaluate its sigmoid, then settle the alpha of the previous sample.
-        while (alive) {
-            double t_nxt = 0.0;
+        bool alive = R.valid && mr.init(g, R.V->cam.pos, dd, P.n_max);
+        // One sample per iteration, warp-synchronous so that the record
+        // allocation below uses full-warp ballots (single call sites also
+        // keep the loop small): fetch the next march sample (or the
+        // one-past-the-end position), evaluate its sigmoid, then settle the
+        // alpha of the previous sample.
+        while (__any_sync(FULL, alive)) {
+            double t_nxt = 0.0, w = 0.0;
             int tile_nxt = -1;
-            int4 tc_nxt;
-            const int idx = mr.count - 1;  // index of t_cur
-            const bool has_next = mr.next(g, t_nxt, tile_nxt, bits, &tc_nxt);
-            if (!has_next && !have_cur) break;  // no sample at all
-            double pn[3];
-            mr.pos(has_next ? t_nxt : dadd(t_cur, g.h), pn);
-            const double s_nxt = has_next ? sample_sdf_in(g, pn[0], pn[1], pn[2], tile_nxt, tc_nxt)
-                                          : sample_sdf(g, pn[0], pn[1], pn[2]);
-            const double a_nxt = sigmoid_d(dmul(tau, s_nxt));
-            if (!have_cur) {
-                have_cur = true;
-                ++c_x;
-            } else {
-                const double alpha = alpha_from(a_cur, a_nxt);
-                const double w = dmul(trans, alpha);
-                if (alpha > 0.0 && cnt_first < 0) {
-                    cnt_first = idx;
-                    t_first = t_cur;
+            bool has_next = false, settle = false, want_entry = false, shade = false;
+            double a_nxt = 0.0, alpha = 0.0;
+            if (alive) {
+                int4 tc_nxt;
+                has_next = mr.next(g, t_nxt, tile_nxt, bits, &tc_nxt);
+                if (!has_next && !have_cur) {
+                    alive = false;  // no sample at all
+                } else {
+                    double pn[3];
+                    mr.pos(has_next ? t_nxt : dadd(t_cur, g.h), pn);
+                    const double s_nxt = has_next ? sample_sdf_in(g, pn[0], pn[1], pn[2], tile_nxt, tc_nxt)
+                                                  : sample_sdf(g, pn[0], pn[1], pn[2]);
+                    a_nxt = sigmoid_d(dmul(tau, s_nxt));
+                    if (!have_cur) {
+                        have_cur = true;
+                        ++c_x;
+                    } else {
+                        settle = true;
+                        alpha = alpha_from(a_cur, a_nxt);
+                        w = dmul(trans, alpha);
+                        if (alpha > 0.0 && cnt_first < 0) {
+                            cnt_first = mr.count - 1 - (has_next ? 1 : 0);
+                            t_first = t_cur;
+                        }
+                        want_entry = alpha > 0.0 && entry < 0;
+                        shade = in_mask && w > 0.0 && tile_cur >= 0;
+                    }
                 }
-                const bool want_entry = alpha > 0.0 && entry < 0;
-#ifdef PSDF_ABL_NOALLOC
-                const int e = want_entry ? atomicAdd(W.counters + 0, 1u) : -1;
-#else
-                const int e = warp_alloc(W.counters + 0, want_entry, lane);
-#endif
-                if (want_entry) entry = e < W.e_cap ? e : -2;  // -2: overflow, host retries
-                const bool shade = in_mask && w > 0.0 && tile_cur >= 0;
-#ifdef PSDF_ABL_NOALLOC
-                const int r = shade ? atomicAdd(W.counters + 1, 1u) : -1;
-#else
-                const int r = warp_alloc(W.counters + 1, shade, lane);
-#endif
+            }
+            // warp-aggregated allocation of ray entries / shading records
+            {
+                const unsigned me = __ballot_sync(FULL, want_entry);
+                const unsigned mr_ = __ballot_sync(FULL, shade);
+                const unsigned below = (1u << lane) - 1u;
+                unsigned be = 0, br = 0;
+                if (lane == 0) {
+                    if (me) be = atomicAdd(W.counters + 0, (unsigned)__popc(me));
+                    if (mr_) br = atomicAdd(W.counters + 1, (unsigned)__popc(mr_));
+                }
+                be = __shfl_sync(FULL, be, 0);
+                br = __shfl_sync(FULL, br, 0);
+                if (want_entry) {
+                    const int e = (int)(be + __popc(me & below));
+                    entry = e < W.e_cap ? e : -2;  // -2: overflow, host retries
+                }
                 if (shade) {
                     ++c_sh;
+                    const int r = (int)(br + __popc(mr_ & below));
                     if (r < W.r_cap && entry >= 0) {
                         double pc[3];
                         mr.pos(t_cur, pc);
@@ -208,16 +223,21 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
                         prev = r;
                     }
                 }
-                acc = dadd(acc, w);
-                trans = dmul(trans, dsub(1.0, alpha));
-                ++n_live;
-                if ((P.early_stop > 0.0 && trans < P.early_stop) || !has_next) break;
             }
-            t_cur = t_nxt;
-            tile_cur = tile_nxt;
-            a_cur = a_nxt;
+            if (alive) {
+                if (settle) {
+                    acc = dadd(acc, w);
+                    trans = dmul(trans, dsub(1.0, alpha));
+                    ++n_live;
+                    if ((P.early_stop > 0.0 && trans < P.early_stop) || !has_next) alive = false;
+                }
+                t_cur = t_nxt;
+                tile_cur = tile_nxt;
+                a_cur = a_nxt;
+            }
         }
         c_m += n_live;
+        if (R.valid) c_ex += mr.n_exact;
         if (entry >= 0) {
             W.e_slot[entry] = wi * 32 + lane;
             W.e_dir[3 * (int64_t)entry] = dir.x;
@@ -231,7 +251,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
             W.e_craw[3 * (int64_t)entry] = 0.0;
             W.e_craw[3 * (int64_t)entry + 1] = 0.0;
             W.e_craw[3 * (int64_t)entry + 2] = 0.0;
-        } else if (cnt_first < 0) {
+        } else if (R.valid && cnt_first < 0) {
             // no alpha > 0 sample: acc = 0, no shaded sample, nothing to
             // back-propagate; the loss is final now
             const double om = dsub(1.0, acc);
@@ -249,7 +269,9 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
     c_x = warp_sum_u(c_x);
     c_sh = warp_sum_u(c_sh);
     c_bwd = warp_sum_u(c_bwd);
+    c_ex = warp_sum_u(c_ex);
     if (lane == 0) {
+        atomicAdd(P.counts + 6, c_ex);
         atomicAdd(P.stats + 0, st_photo);
         atomicAdd(P.stats + 1, st_sq);
         atomicAdd(P.stats + 2, (double)st_mask);
