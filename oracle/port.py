@@ -55,6 +55,16 @@ def lib():
     L.og_train_step.argtypes = [C.c_void_p, C.c_int, C.POINTER(RefCamera), C.POINTER(_dp),
                                 C.POINTER(_dp), C.POINTER(RefStepParams), _dp, _lp, C.c_void_p,
                                 C.c_void_p]
+    L.og_regularizer_range.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_int, C.c_void_p, _dp]
+    L.og_raypass_tiles.argtypes = [C.c_void_p, C.c_int, C.POINTER(RefCamera), C.POINTER(_dp),
+                                   C.POINTER(_dp), C.POINTER(RefStepParams), C.c_int64, C.c_int64,
+                                   C.c_void_p, _dp]
+    L.og_alpha_from_sdf.restype = C.c_double
+    L.og_alpha_from_sdf.argtypes = [C.c_double, C.c_double, C.c_double]
+    L.og_sh_basis.argtypes = [_dp, C.c_int, _dp]
+    L.og_fresnel_powers.argtypes = [C.c_double, _dp]
+    L.og_gaussian_taps.argtypes = [_dp]
+    L.og_adam_steps.argtypes = [C.c_int, _dp, _dp, C.c_int, _dp]
     _lib = L
     return L
 
@@ -146,6 +156,35 @@ class OracleGrid:
     def train_reset(self):
         self.L.og_train_reset(self.h)
 
+    def new_grads(self):
+        return C.c_void_p(self.L.og_grads_new(self.h))
+
+    def free_grads(self, gb):
+        self.L.og_grads_free(gb)
+
+    def grads_of(self, gb):
+        return self._grads(gb)
+
+    def raypass_tiles(self, cams, gts, masks, hp, tile_begin, tile_end, gb):
+        """Ray pass over work tiles [tile_begin, tile_end) into gb (data-parallel shard)."""
+        n = len(cams)
+        arr = (RefCamera * n)(*cams)
+        gts = [np.ascontiguousarray(g, np.float64) for g in gts]
+        masks = [np.ascontiguousarray(m, np.float64) for m in masks]
+        gp = (_dp * n)(*[ptr(g) for g in gts])
+        mp = (_dp * n)(*[ptr(m) for m in masks])
+        out = np.zeros(3)
+        self.L.og_raypass_tiles(self.h, n, arr, gp, mp, C.byref(hp), tile_begin, tile_end, gb, ptr(out))
+        return out
+
+    def regularizer_range(self, which, lam, begin, end, gb):
+        out = np.zeros(2)
+        self.L.og_regularizer_range(self.h, which, lam, begin, end, gb, ptr(out))
+        return out
+
+    def gt_fold_into(self, gb):
+        self.L.og_gt_fold(self.h, gb)
+
     def train_step(self, cams, gts, masks, hp):
         n = len(cams)
         arr = (RefCamera * n)(*cams)
@@ -178,3 +217,39 @@ def step_params(tau, lr_vox, lr_mlp, l_sdf=0.7, l_eik=0.3, l_norm=0.2, l_feat=0.
     hp.photo_scale = photo_scale
     hp.use_camera_bias = int(use_camera_bias)
     return hp
+
+
+def work_tiles(cams):
+    """Number of 8x4-pixel work tiles of a batch (the CUDA path's ray partition)."""
+    return sum(((c.width + 7) // 8) * ((c.height + 3) // 4) for c in cams)
+
+
+def kat_alpha(si, sn, tau):
+    return lib().og_alpha_from_sdf(si, sn, tau)
+
+
+def kat_sh(direction, order):
+    out = np.zeros(16)
+    d = np.asarray(direction, np.float64)
+    lib().og_sh_basis(ptr(d), order, ptr(out))
+    return out[: order * order]
+
+
+def kat_fresnel(ndv):
+    out = np.zeros(6)
+    lib().og_fresnel_powers(ndv, ptr(out))
+    return out
+
+
+def kat_gaussian():
+    out = np.zeros(5)
+    lib().og_gaussian_taps(ptr(out))
+    return out
+
+
+def kat_adam(params, grads_seq, lrs):
+    p = np.ascontiguousarray(params, np.float64).copy()
+    g = np.ascontiguousarray(grads_seq, np.float64)
+    lr = np.ascontiguousarray(lrs, np.float64)
+    lib().og_adam_steps(p.size, ptr(p), ptr(g), len(lr), ptr(lr))
+    return p

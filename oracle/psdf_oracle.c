@@ -940,12 +940,13 @@ static void halo_stencil(Halo* hl, int x, int y, int z, V3 dg, double inv2h) {
     hl->grad[hidx(x, y, z - 1)] -= dg.z * inv2h;
 }
 
-void og_regularizer(const OGrid* g, int which, double lambda, OGrads* gb, double* out) {
+void og_regularizer_range(const OGrid* g, int which, double lambda, int begin, int end, OGrads* gb,
+                          double* out) {
     double plain = 0.0, weighted = 0.0;
     const double inv2h = 1.0 / (2.0 * g->h);
     static Halo hl;
     if (which == 0) { /* loss_sdf, losses.cpp:121-142 */
-        for (int t = 0; t < g->T; ++t)
+        for (int t = begin; t < end; ++t)
             for (int v = 0; v < TV; ++v) {
                 const double sm = g->smooth[(int64_t)t * TV + v], rw = g->raw[(int64_t)t * TV + v];
                 const double r = sm - rw;
@@ -959,7 +960,7 @@ void og_regularizer(const OGrid* g, int which, double lambda, OGrads* gb, double
                 }
             }
     } else if (which == 1) { /* loss_eikonal, losses.cpp:144-171 */
-        for (int t = 0; t < g->T; ++t) {
+        for (int t = begin; t < end; ++t) {
             halo_load(g, t, &hl);
             for (int x = 0; x < TE; ++x)
                 for (int y = 0; y < TE; ++y)
@@ -976,7 +977,7 @@ void og_regularizer(const OGrid* g, int which, double lambda, OGrads* gb, double
             if (gb) halo_flush(g, &hl, gb);
         }
     } else if (which == 2) { /* loss_normal, losses.cpp:173-220 */
-        for (int t = 0; t < g->T; ++t) {
+        for (int t = begin; t < end; ++t) {
             halo_load(g, t, &hl);
             for (int x = 0; x < TE; ++x)
                 for (int y = 0; y < TE; ++y)
@@ -1013,7 +1014,7 @@ void og_regularizer(const OGrid* g, int which, double lambda, OGrads* gb, double
         }
     } else if (which == 3) { /* loss_features, losses.cpp:222-257 */
         const int n_s = g->n_s;
-        for (int t = 0; t < g->T; ++t)
+        for (int t = begin; t < end; ++t)
             for (int pp = 0; pp < 3; ++pp) {
                 const double* p = g->planes + ((int64_t)t * 3 + pp) * plane_stride(g);
                 double* gp = gb ? gb->planes + ((int64_t)t * 3 + pp) * plane_stride(g) : NULL;
@@ -1040,7 +1041,7 @@ void og_regularizer(const OGrid* g, int which, double lambda, OGrads* gb, double
             }
     } else if (which == 4) { /* loss_probes, losses.cpp:259-283 */
         const int64_t stride = probe_stride(g);
-        for (int pi = 0; pi < g->P; ++pi) {
+        for (int pi = begin; pi < end; ++pi) {
             const int32_t* c = g->probe_coords + 3 * pi;
             static const int off[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
             for (int a = 0; a < 3; ++a) {
@@ -1063,6 +1064,10 @@ void og_regularizer(const OGrid* g, int which, double lambda, OGrads* gb, double
     }
     out[0] = plain;
     out[1] = weighted;
+}
+
+void og_regularizer(const OGrid* g, int which, double lambda, OGrads* gb, double* out) {
+    og_regularizer_range(g, which, lambda, 0, which == 4 ? g->P : g->T, gb, out);
 }
 
 /* grads.cpp:67-96 */
@@ -1201,4 +1206,73 @@ void og_train_step(OGrid* g, int n_views, const OCamera* cams, const double* con
         counts[0] = n_rays; counts[1] = n_m; counts[2] = n_x; counts[3] = n_sh; counts[4] = n_al;
         counts[5] = n_bwd;
     }
+}
+
+/* ---------------------------------------------------- known-answer hooks */
+double og_alpha_from_sdf(double si, double sn, double tau) { return alpha_from_sdf(si, sn, tau); }
+void og_sh_basis(const double* dir, int order, double* out) { sh_basis(v3(dir[0], dir[1], dir[2]), order, out); }
+void og_fresnel_powers(double ndv, double* out) { fresnel_powers(ndv, out); }
+void og_gaussian_taps(double* out) { gaussian_taps(out); }
+void og_adam_steps(int n, double* params, const double* grads_seq, int steps, const double* lrs) {
+    double* m = (double*)calloc((size_t)n, sizeof(double));
+    double* v = (double*)calloc((size_t)n, sizeof(double));
+    for (int t = 0; t < steps; ++t) adam_range(params, grads_seq + (size_t)t * n, m, v, n, lrs[t], t + 1);
+    free(m);
+    free(v);
+}
+
+/* The ray pass of trainer.cpp:149-182 restricted to the 8x4-pixel work tiles
+ * [tile_begin, tile_end) of the batch (views concatenated, tiles row-major per
+ * view): the data-parallel partition the CUDA path gives each rank
+ * (psdf.cu do_train_step).  Accumulates into gb; losses[3] = photo plain,
+ * sq_err, mask_px. */
+void og_raypass_tiles(const OGrid* g, int n_views, const OCamera* cams, const double* const* gt_rgb,
+                      const double* const* mask, const OStepParams* hp, int64_t tile_begin,
+                      int64_t tile_end, OGrads* gb, double* losses) {
+    double photo_plain = 0.0, sq_err = 0.0, mask_px = 0.0;
+    Ray ws = {0};
+    int64_t tile0 = 0;
+    for (int vi = 0; vi < n_views; ++vi) {
+        const OCamera* cam = &cams[vi];
+        const int w = cam->width, h = cam->height;
+        const int tx = (w + 7) / 8, ty = (h + 3) / 4;
+        ORenderOpts ro;
+        memset(&ro, 0, sizeof ro);
+        ro.tau = hp->tau;
+        ro.n_max = 512;
+        ro.early_stop = 1e-4;
+        ro.camera_id = hp->use_camera_bias ? cam->id : -1;
+        ro.sh_order_override = -1;
+        for (int64_t lt = 0; lt < (int64_t)tx * ty; ++lt) {
+            const int64_t tile = tile0 + lt;
+            if (tile < tile_begin || tile >= tile_end) continue;
+            for (int lane = 0; lane < 32; ++lane) {
+                const int u = (int)(lt % tx) * 8 + (lane & 7), v = (int)(lt / tx) * 4 + (lane >> 3);
+                if (u >= w || v >= h) continue;
+                const int64_t px = (int64_t)v * w + u;
+                const int in_mask = mask[vi][px] > 0.5;
+                ro.need_colors = in_mask;
+                double d[3], res[6], pp[6];
+                og_pixel_dir(cam, u + 0.5, v + 0.5, d);
+                render_ray(g, v3(cam->pos[0], cam->pos[1], cam->pos[2]), v3(d[0], d[1], d[2]), &ro,
+                           &ws, res);
+                const double* gt = gt_rgb[vi] + 3 * px;
+                og_photo_pixel(res, gt, in_mask, res[3], hp->photo_scale, pp);
+                photo_plain += pp[0];
+                if (in_mask) {
+                    const double e0 = res[0] - gt[0], e1 = res[1] - gt[1], e2 = res[2] - gt[2];
+                    sq_err += e0 * e0 + e1 * e1 + e2 * e2;
+                    mask_px += 3;
+                }
+                if (pp[2] * pp[2] + pp[3] * pp[3] + pp[4] * pp[4] > 0.0 || pp[5] != 0.0)
+                    ray_backward(g, &ro, &ws, pp + 2, pp[5], gb);
+            }
+        }
+        tile0 += (int64_t)tx * ty;
+    }
+    free(ws.s);
+    free(ws.shade);
+    losses[0] = photo_plain;
+    losses[1] = sq_err;
+    losses[2] = mask_px;
 }

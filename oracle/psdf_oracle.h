@@ -80,6 +80,20 @@ void og_photo_pixel(const double* c, const double* gt, int in_mask, double acc, 
 /* which: 0 sdf, 1 eik, 2 normal, 3 features, 4 probes; out: plain, weighted */
 void og_regularizer(const OGrid* g, int which, double lambda, OGrads* gb, double* out);
 void og_gt_fold(const OGrid* g, OGrads* gb);
+/* loss over tiles [begin, end) (which 0..3) or probes [begin, end) (which 4) */
+void og_regularizer_range(const OGrid* g, int which, double lambda, int begin, int end, OGrads* gb,
+                          double* out);
+/* ray pass over the 8x4 work tiles [tile_begin, tile_end) of the batch */
+void og_raypass_tiles(const OGrid* g, int n_views, const OCamera* cams, const double* const* gt_rgb,
+                      const double* const* mask, const OStepParams* hp, int64_t tile_begin,
+                      int64_t tile_end, OGrads* gb, double* losses);
+
+/* known-answer hooks (the reference's unit-test constants) */
+double og_alpha_from_sdf(double si, double sn, double tau);
+void og_sh_basis(const double* dir, int order, double* out);
+void og_fresnel_powers(double ndv, double* out);
+void og_gaussian_taps(double* out);
+void og_adam_steps(int n, double* params, const double* grads_seq, int steps, const double* lrs);
 
 /* Training: Adam state lives in the grid object. */
 void og_train_reset(OGrid* g);

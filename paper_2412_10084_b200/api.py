@@ -498,6 +498,19 @@ def pixel_dirs(camera) -> np.ndarray:
     return out
 
 
+def shard(n, rank, world):
+    """Contiguous 1/world slice [begin, end) of n units: the data-parallel
+    partition psdf.cu applies to the batch's 8x4 work tiles (ray pass), the
+    allocated tiles (sdf / eikonal / normal / feature regularizers) and the
+    probe pool (probe regularizer) — SURVEY.md section 8e."""
+    return (n * rank) // world, (n * (rank + 1)) // world
+
+
+def work_tiles(cameras):
+    """8x4-pixel work tiles of a batch (views concatenated, row-major per view)."""
+    return sum(((c.width + 7) // 8) * ((c.height + 3) // 4) for c in cameras)
+
+
 def render_image(ctx: Context, camera, opts: RenderOptions):
     """render_image(grid, mlp, camera, opt) (renderer.hpp:98-99) on the GPU."""
     return ctx.render_image(camera, opts)
