@@ -361,7 +361,7 @@ def main():
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "kernel": "train_kernel<4,4> (K2 fused ray pass)",
+                "frac": achieved / peak, "traffic": traffic, "kernel": "K2 ray pass: march_fwd + shade_fwd<4,4> + alpha_bwd + shade_bwd<4,4>",
                 "algorithmic_bytes_per_launch": k2_bytes, "kernel_ms": k2_ms, "peak_source": peak_src,
                 "k2_share_of_step": k2_ms / statistics.mean(step_ms),
                 "k2_kernels_ms": dict(zip(["march_fwd", "shade_fwd", "alpha_bwd", "shade_bwd"],
