@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libpsdf.so")
+# PSDF_LIB selects a diagnostics build (e.g. lib/libpsdf_stats.so) by name
+LIB_PATH = os.path.join(HERE, "lib", os.environ.get("PSDF_LIB", "libpsdf.so"))
 
 PSDF_OK = 0
 ERRORS = {1: "invalid_argument", 2: "out_of_range", 3: "runtime_error", 4: "cuda", 5: "nccl"}

@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -159,6 +160,10 @@ struct psdf_ctx {
     int64_t n_planes = 0, n_probes = 0, mlp_size = 0;
     int32_t* d_tile_table = nullptr;
     uint32_t* d_tile_bits = nullptr;
+    uint8_t* d_tile_dist = nullptr;
+    float* d_tile_min = nullptr;   // [T] minimum of each tile's apron brick
+    float* d_block_min = nullptr;  // [T][64] minimum of each 4^3 block's brick
+    int32_t* d_tile_nbr = nullptr; // [T][27] neighbour tile ids
     int bit_words = 0;
     int4* d_tile_coords = nullptr;
     int32_t* d_probe_ids = nullptr;
@@ -225,6 +230,14 @@ struct psdf_ctx {
         g.far = desc.far_field_voxels * desc.voxel_size;
         g.tile_table = d_tile_table;
         g.tile_bits = d_tile_bits;
+        g.tile_dist = d_tile_dist;
+        g.tile_min = d_tile_min;
+        g.block_min = d_block_min;
+        g.tile_nbr = d_tile_nbr;
+        // decision margin of the marcher's fast paths; PSDF_TEST_MARGIN widens
+        // it so the tests drive the exact / rewind paths on most decisions
+        g.margin = 1e-8;
+        if (const char* m = std::getenv("PSDF_TEST_MARGIN")) g.margin = std::max(1e-8, std::atof(m));
         g.bit_words = bit_words;
         g.tile_coords = d_tile_coords;
         g.probe_ids = d_probe_ids;
@@ -236,13 +249,17 @@ struct psdf_ctx {
     }
 
     void free_grid() {
-        for (void* p : {(void*)d_tile_table, (void*)d_tile_bits, (void*)d_tile_coords, (void*)d_probe_ids,
+        for (void* p : {(void*)d_tile_table, (void*)d_tile_bits, (void*)d_tile_dist, (void*)d_tile_min, (void*)d_block_min, (void*)d_tile_nbr, (void*)d_tile_coords, (void*)d_probe_ids,
                         (void*)d_probe_table, (void*)d_probe_coords, (void*)d_params,
                         (void*)d_smooth, (void*)d_smooth_ap, (void*)d_grads, (void*)d_gsmooth, (void*)d_grads0,
                         (void*)d_gsmooth0, (void*)d_m, (void*)d_v})
             if (p) cudaFree(p);
         d_tile_table = nullptr;
         d_tile_bits = nullptr;
+        d_tile_dist = nullptr;
+        d_tile_min = nullptr;
+        d_block_min = nullptr;
+        d_tile_nbr = nullptr;
         d_tile_coords = nullptr;
         d_probe_ids = nullptr;
         d_probe_table = nullptr;
@@ -320,33 +337,44 @@ int blocks_per_sm(const void* fn, size_t smem) {
     return std::max(n, 1);
 }
 
-void launch_smooth(psdf_ctx* c, const float* src, float fill, float* dst, int accumulate) {
+// G^T fold: dst += G * src (src filled with 0 outside allocated tiles).
+void launch_fold(psdf_ctx* c, const float* src, float* dst) {
     if (c->desc.T == 0) return;
-    const size_t smem = sizeof(float) * (HV + 16 * HE * HE);
     static bool attr = false;
     if (!attr) {
         CK(cudaFuncSetAttribute(smooth_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
+                                (int)kFoldSmem));
         attr = true;
     }
-    smooth_fold_kernel<<<c->desc.T, 256, smem, c->stream>>>(c->view(), src, fill, dst, accumulate,
-                                                            gaussian_taps());
+    smooth_fold_kernel<<<c->desc.T, 256, kFoldSmem, c->stream>>>(c->view(), src, 0.f, dst, 1,
+                                                                 gaussian_taps());
     CK(cudaGetLastError());
     ++c->last_launches;
 }
 
-// Refreshes the apron copy of the smoothed SDF used by the samplers.
+// Refreshes the apron copy (and brick minima) from the current smoothed grid.
 void fill_apron(psdf_ctx* c) {
     if (c->desc.T == 0) return;
-    apron_fill_kernel<<<c->desc.T, 256, 0, c->stream>>>(c->view(), c->d_smooth, c->d_smooth_ap);
+    apron_fill_kernel<<<c->desc.T, 256, 0, c->stream>>>(c->view(), c->d_smooth, c->d_smooth_ap,
+                                                         c->d_tile_min, c->d_block_min);
     CK(cudaGetLastError());
     ++c->last_launches;
 }
 
+// SparseGrid::smooth_all (grid.cpp:247-250) + apron + brick minima, one pass.
 void smooth_all(psdf_ctx* c) {
-    launch_smooth(c, c->d_params + c->off_raw, (float)(c->desc.far_field_voxels * c->desc.voxel_size),
-                  c->d_smooth, 0);
-    fill_apron(c);
+    if (c->desc.T == 0) return;
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(smooth_apron_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kSmoothApronSmem));
+        attr = true;
+    }
+    smooth_apron_kernel<<<c->desc.T, 256, kSmoothApronSmem, c->stream>>>(
+        c->view(), c->d_params + c->off_raw, (float)(c->desc.far_field_voxels * c->desc.voxel_size),
+        c->d_smooth, c->d_smooth_ap, c->d_tile_min, c->d_block_min, gaussian_taps());
+    CK(cudaGetLastError());
+    ++c->last_launches;
 }
 
 // K1 launch (render).
@@ -454,6 +482,14 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
         unsigned long long cc[8];
         CK(cudaMemcpy(cc, c->d_counts, sizeof cc, cudaMemcpyDeviceToHost));
         fprintf(stderr, "[psdf] march exact fallbacks: %llu\n", cc[6]);
+#ifdef PSDF_MARCH_STATS
+        unsigned long long st[12];
+        CK(cudaMemcpyFromSymbol(st, g_march_stats, sizeof st));
+        const unsigned long long zero[12] = {};
+        CK(cudaMemcpyToSymbol(g_march_stats, zero, sizeof zero));
+        fprintf(stderr, "[psdf] march stats: rays %llu in-box %llu iters %llu samples %llu jumps %llu "
+                "skips %llu exact %llu rewinds %llu sat-runs %llu run-samples %llu - %llu\n", st[0], st[1], st[2], st[3], st[4], st[5], st[6], st[7], st[8], st[9], st[10]);
+#endif
     }
     c->last_entries = n_ent;
     c->last_records = n_rec;
@@ -610,25 +646,20 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
     const int p0 = (int)((int64_t)Pn * c->rank / c->world), p1 = (int)((int64_t)Pn * (c->rank + 1) / c->world);
     const int stride = c->desc.sh_order * c->desc.sh_order * c->desc.n_a;
     if (t1 > t0) {
-        loss_sdf_kernel<<<std::min(4 * c->sm_count, (int)((int64_t)(t1 - t0) * TV / 256 + 1)), 256,
-                          0, s>>>(g, c->d_params + c->off_raw, t0, t1, (float)hp->l_sdf,
-                                  c->d_gsmooth, c->d_grads + c->off_raw, c->d_stats);
-        CK(cudaGetLastError());
-        const size_t sm_en = kEikNormalSmem;
         static bool attr = false;
         if (!attr) {
-            CK(cudaFuncSetAttribute(loss_eik_normal_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_en));
+            CK(cudaFuncSetAttribute(loss_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kLossGridSmem));
             attr = true;
         }
-        loss_eik_normal_kernel<<<t1 - t0, 256, sm_en, s>>>(
-            g, t0, (float)hp->l_eik, (float)hp->l_norm, (float)(1.0 / (2.0 * c->desc.voxel_size)),
-            c->d_gsmooth, c->d_stats);
+        loss_grid_kernel<<<t1 - t0, LG_THREADS, kLossGridSmem, s>>>(
+            g, c->d_params + c->off_raw, t0, (float)hp->l_sdf, (float)hp->l_eik, (float)hp->l_norm,
+            (float)(1.0 / (2.0 * c->desc.voxel_size)), c->d_gsmooth, c->d_grads + c->off_raw, c->d_stats);
         CK(cudaGetLastError());
         loss_features_kernel<<<3 * (t1 - t0), 256, 0, s>>>(
             g, t0, c->desc.n_s, (float)hp->l_feat, c->d_grads + c->off_planes, c->d_stats);
         CK(cudaGetLastError());
-        c->last_launches += 3;
+        c->last_launches += 2;
     }
     if (p1 > p0) {
         GridMut m{g, c->d_params + c->off_raw, c->d_probe_table, c->d_probe_coords};
@@ -639,7 +670,7 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
         ++c->last_launches;
     }
     // G^T fold (grads.cpp:67-96): raw_grad += G^T * staged
-    launch_smooth(c, c->d_gsmooth, 0.f, c->d_grads + c->off_raw, 1);
+    launch_fold(c, c->d_gsmooth, c->d_grads + c->off_raw);
     // all-reduce across ranks (GradBuffers::add, trainer.cpp:184-185, across GPUs)
     if (c->world > 1) {
         NK(g_nccl.AllReduce(c->d_grads, c->d_grads, (size_t)c->n_params, ncclFloat, ncclSum, c->comm, s));
@@ -787,6 +818,32 @@ int64_t psdf_mlp_size(int n_s, int n_a, int ncam) {
     return (int64_t)MlpLayout::make(in).cam + (int64_t)ncam * HID;
 }
 
+// Chebyshev (L-inf) distance, in tiles, from every tile to the nearest
+// allocated one (0 = allocated, capped at kMaxTileDist; the marcher's
+// empty-space jumps, psdf_device.cuh).  Separable: an L-inf ball is the
+// product of three 1-D intervals, so three passes of
+// d(x) = min_x' max(|x - x'|, d_prev(x')) over a window of kMaxTileDist.
+static std::vector<uint8_t> tile_distance(const std::vector<int32_t>& tt, const int nt[3]) {
+    constexpr int kMaxTileDist = 32;
+    const int64_t n = (int64_t)nt[0] * nt[1] * nt[2];
+    std::vector<uint8_t> a(n), b(n);
+    for (int64_t i = 0; i < n; ++i) a[i] = tt[i] >= 0 ? 0 : kMaxTileDist;
+    const int64_t stride[3] = {(int64_t)nt[1] * nt[2], nt[2], 1};
+    for (int ax = 0; ax < 3; ++ax) {
+        for (int64_t i = 0; i < n; ++i) {
+            const int x = (int)((i / stride[ax]) % nt[ax]);
+            int best = a[i];
+            for (int r = 1; r < best; ++r) {
+                if (x - r >= 0) best = std::min(best, std::max(r, (int)a[i - r * stride[ax]]));
+                if (x + r < nt[ax]) best = std::min(best, std::max(r, (int)a[i + r * stride[ax]]));
+            }
+            b[i] = (uint8_t)best;
+        }
+        a.swap(b);
+    }
+    return a;
+}
+
 int psdf_upload_grid(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_coords,
                      const int32_t* probe_ids, const int32_t* probe_coords, const float* raw,
                      const float* smooth, const float* planes, const float* probes) {
@@ -851,6 +908,20 @@ int psdf_upload_grid(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_c
         CK(cudaMalloc(&c->d_tile_bits, sizeof(uint32_t) * c->bit_words));
         CK(cudaMemcpyAsync(c->d_tile_bits, bits.data(), sizeof(uint32_t) * c->bit_words,
                            cudaMemcpyHostToDevice, c->stream));
+        const std::vector<uint8_t> dist = tile_distance(tt, c->nt);
+        std::vector<int32_t> nbr(27 * std::max<int64_t>(T, 1), -1);
+        for (int64_t t = 0; t < T; ++t)
+            for (int k = 0; k < 27; ++k) {
+                const int q[3] = {tc4[t].x + k / 9 - 1, tc4[t].y + (k / 3) % 3 - 1, tc4[t].z + k % 3 - 1};
+                if (q[0] >= 0 && q[1] >= 0 && q[2] >= 0 && q[0] < c->nt[0] && q[1] < c->nt[1] && q[2] < c->nt[2])
+                    nbr[27 * t + k] = tt[((int64_t)q[0] * c->nt[1] + q[1]) * c->nt[2] + q[2]];
+            }
+        CK(cudaMalloc(&c->d_tile_nbr, sizeof(int32_t) * nbr.size()));
+        CK(cudaMemcpyAsync(c->d_tile_nbr, nbr.data(), sizeof(int32_t) * nbr.size(), cudaMemcpyHostToDevice,
+                           c->stream));
+        CK(cudaMalloc(&c->d_tile_dist, std::max<int64_t>(ntt, 1)));
+        CK(cudaMemcpyAsync(c->d_tile_dist, dist.data(), ntt, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));  // the host vectors above are about to go
         CK(cudaMalloc(&c->d_probe_table, sizeof(int32_t) * npt));
         CK(cudaMalloc(&c->d_tile_coords, sizeof(int4) * tc4.size()));
         CK(cudaMalloc(&c->d_probe_coords, sizeof(int4) * pc4.size()));
@@ -861,6 +932,8 @@ int psdf_upload_grid(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_c
         CK(cudaMalloc(&c->d_v, sizeof(float) * c->n_params));
         CK(cudaMalloc(&c->d_smooth, sizeof(float) * std::max<int64_t>(T * TV, 4)));
         CK(cudaMalloc(&c->d_smooth_ap, sizeof(float) * std::max<int64_t>(T * AV, 4)));
+        CK(cudaMalloc(&c->d_tile_min, sizeof(float) * std::max<int64_t>(T, 1)));
+        CK(cudaMalloc(&c->d_block_min, sizeof(float) * std::max<int64_t>(64 * T, 1)));
         CK(cudaMalloc(&c->d_gsmooth, sizeof(float) * std::max<int64_t>(T * TV, 4)));
         CK(cudaMemsetAsync(c->d_params, 0, sizeof(float) * c->n_params, c->stream));
         CK(cudaMemsetAsync(c->d_grads, 0, sizeof(float) * c->n_params, c->stream));

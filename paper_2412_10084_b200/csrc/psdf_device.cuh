@@ -47,11 +47,16 @@ struct GridView {
     double wmax[3];                // world_max() (grid.hpp:72-74)
     const int32_t* __restrict__ tile_table;   // [nt0][nt1][nt2] -> tile or -1
     const uint32_t* __restrict__ tile_bits;   // occupancy bitmap of tile_table
+    const uint8_t* __restrict__ tile_dist;    // L-inf distance (tiles) to the nearest allocated tile
+    const int32_t* __restrict__ tile_nbr;     // [T][27] neighbour tile ids (-1: none), (dx,dy,dz) in {-1,0,1}^3
     int bit_words;                            // 32-bit words in tile_bits
+    double margin;                            // marcher decision margin, voxels (1e-8; tests widen it)
     const int4* __restrict__ tile_coords;     // [T] (x,y,z,0)
     const int32_t* __restrict__ probe_ids;    // [T][8]
     const float* __restrict__ smooth;         // [T][4096]
     const float* __restrict__ smooth_ap;      // [T][18^3] smooth with a 1-voxel apron
+    const float* __restrict__ tile_min;       // [T] min of each apron brick
+    const float* __restrict__ block_min;      // [T][64] min over each 4^3 block's 6^3 brick
     const float* __restrict__ planes;         // [T][3][256][n_s]
     const float* __restrict__ probes;         // [P][order^2][n_a]
 };
@@ -275,6 +280,33 @@ __device__ __noinline__ int4 exact_tile(GridLite g, D3 o, D3 d, double t) {
                      ((int)floor(w2v_(dadd(o.z, dmul(d.z, t)), 2))) >> 4, 0);
 }
 
+#ifdef PSDF_MARCH_STATS
+// diagnostics build only: [rays, in box, loop iterations, samples, jumps,
+// fast skips, exact fallbacks, rewinds]
+__device__ unsigned long long g_march_stats[12];
+#define PSDF_STAT(i) atomicAdd(&g_march_stats[i], 1ull)
+#else
+#define PSDF_STAT(i) ((void)0)
+#endif
+
+// t + m h exactly as the reference's own chain of additions would produce it
+// (see Marcher): every lattice step is a multiple of h, exact inside a
+// binade, rounded once when t crosses a power of two; adding m h in chunks
+// that each cross at most one power of two gives the same bits as any other
+// such chunking.  Needs t >= 64 h (then a binade is wider than any single
+// reference step).
+__device__ __forceinline__ double lattice_advance(double t, double m, double h) {
+    for (;;) {
+        int e;
+        frexp(t, &e);
+        const double p2 = ldexp(1.0, e);                // next power of two above t
+        if (t + m * h < 2.0 * p2) return dadd(t, dmul(m, h));
+        const double m1 = ceil((p2 - t) / h);          // any m1 >= 1 landing in [p2, 2 p2)
+        t = dadd(t, dmul(m1, h));
+        m -= m1;
+    }
+}
+
 // march_ray (renderer.cpp:55-86) as a resumable generator: the state is
 // (t, count), so the backward sweep can restart at any emitted sample.
 //
@@ -285,16 +317,44 @@ __device__ __noinline__ int4 exact_tile(GridLite g, D3 o, D3 d, double t) {
 // ~1e-12 voxel; when the value is farther than a 1e-8 margin from the
 // decision boundary the result is provably the reference's, otherwise the
 // exact f64 path decides.
+//
+// Empty space.  Every t the reference produces is t0 + K h for an integer K
+// (each step adds h or k h), rounded only where t crosses a power of two, so
+// the reference's t-sequence is the lattice {t0 + K h} and its samples are
+// the lattice points inside allocated tiles: the tile-by-tile skip of
+// renderer.cpp:73-82 only decides which lattice points are visited on the
+// way.  The marcher therefore jumps m lattice steps at once through the
+// L-inf ball of empty tiles around p(t) (g.tile_dist), landing on a lattice
+// point the reference never visits but whose successor it computes
+// identically (same tile, skip count = reference's minus the integer offset)
+// unless a decision is inside the margin.  In that case — and only while
+// desynchronised by a jump — the marcher rewinds to the last point the
+// reference itself visited (t_sync) and replays tile by tile without jumps,
+// so every emitted sample is bit-identical to the reference.
+// sigmoid(x) == 1.0 exactly for x >= kSatX: exp(-37.5) < 2^-54, so 1 + exp(-x)
+// rounds to 1 (renderer.cpp:10), and alpha_from(a, 1.0) == 0 for any a.
+constexpr double kSatX = 37.5 * (1.0 + 1e-9);
+
+struct SampleRun {
+    int n;          // samples in the run (>= 1)
+    bool sat;       // every sample of the run has sigmoid == 1 exactly
+    double t_last;  // t of the run's last sample
+};
+
 struct Marcher {
     double o[3], d[3], inv_d[3];
     double t, t1;
     int count, n_max;
     double vo[3], vd[3];  // (o - org)/h, d/h
+    double dinv_max;      // 1 / max_a |d_a|: lattice steps per voxel of L-inf travel
+    double t_sync;        // < 0: synchronised with the reference; else its last t
+    bool no_jump;         // replaying after a rewind
     unsigned n_exact;     // exact-path fallbacks taken (diagnostics)
 
     __device__ __forceinline__ bool init(const GridView& g, const double* o_, const double* d_,
                                          int nmax) {
         const double inv_h = g.h_pow2 ? g.inv_h : 1.0 / g.h;
+        double dm = 0.0;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             o[a] = o_[a];
@@ -302,12 +362,18 @@ struct Marcher {
             inv_d[a] = fabs(d[a]) < 1e-15 ? 0.0 : __drcp_rn(d[a]);
             vo[a] = (o[a] - g.org[a]) * inv_h;
             vd[a] = d[a] * inv_h;
+            dm = fmax(dm, fabs(d[a]));
         }
+        dinv_max = dm > 0.0 ? 1.0 / dm : 0.0;
+        t_sync = -1.0;
+        no_jump = false;
         n_max = nmax;
         count = 0;
         n_exact = 0;
         const BoxHit b = ray_box(d3(o[0], o[1], o[2]), d3(d[0], d[1], d[2]),
                                  d3(g.org[0], g.org[1], g.org[2]), d3(g.wmax[0], g.wmax[1], g.wmax[2]));
+        PSDF_STAT(0);
+        if (b.ok) PSDF_STAT(1);
         if (!b.ok) {
             t = 0.0;
             t1 = -1.0;
@@ -318,46 +384,169 @@ struct Marcher {
         return true;
     }
 
+    // Rewinds to the reference's last visited point (after an ambiguous
+    // decision while desynchronised); returns false if synchronised.
+    __device__ __forceinline__ bool rewind() {
+        if (t_sync < 0.0) return false;
+        PSDF_STAT(7);
+        t = t_sync;
+        t_sync = -1.0;
+        no_jump = true;
+        return true;
+    }
+
+    // Lattice points t + j h (j >= 0) still inside the current tile and
+    // before the box exit t1, or 1 when either boundary is within the
+    // decision margin (then the caller steps one sample at a time).  Only
+    // with the lattice preconditions (power-of-two h, t >= 64 h).
+    __device__ __forceinline__ double run_length(const GridView& g, const double v[3], double t,
+                                                 double h) const {
+        if (!g.h_pow2 || t < 64.0 * h) return 1.0;
+        double q = 1e300, rmax = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            if (inv_d[a] == 0.0) continue;
+            const double B = 16.0 * (floor(v[a] * 0.0625) + (d[a] > 0.0 ? 1.0 : 0.0));
+            q = fmin(q, (B - v[a]) * inv_d[a]);
+            rmax = fmax(rmax, fabs(inv_d[a]));
+        }
+        const double mq = g.margin + 1e-11 * rmax;
+        const double fq = q - floor(q);
+        if (!(q < 1e300) || fq <= mq || fq >= 1.0 - mq) return 1.0;
+        // the reference's own loop test t_j < t1, t_j = t + j h exactly
+        const double r1 = (t1 - t) * g.inv_h;
+        const double f1 = r1 - floor(r1);
+        if (f1 <= 1e-9 || f1 >= 1.0 - 1e-9) return 1.0;
+        return fmin(ceil(q), ceil(r1));
+    }
+
     // Next sample distance inside an allocated tile; false when exhausted.
     // `bits` is the tile occupancy bitmap (usually a shared-memory copy), so
     // skipping empty tiles needs no global memory access.
     __device__ __forceinline__ bool next(const GridView& g, double& t_out, int& tile_out,
                                          const uint32_t* bits, int4* tc_out = nullptr) {
+        SampleRun run;
+        return next_impl<false>(g, t_out, tile_out, bits, tc_out, 0.0, run);
+    }
+
+    // As next(), but when the sample's tile is saturated — tau * (minimum of
+    // its apron brick) >= kSatX, so every sample in it has sigmoid exactly 1
+    // and alpha exactly 0 — returns the whole run of the ray's consecutive
+    // lattice points in that tile at once: run.n samples from t_out to
+    // run.t_last (the reference visits them one by one with t += h; the
+    // count is exact, the t values follow from the lattice argument above).
+    __device__ __forceinline__ bool next_run(const GridView& g, double& t_out, int& tile_out,
+                                             const uint32_t* bits, int4* tc_out, double tau,
+                                             SampleRun& run) {
+        return next_impl<true>(g, t_out, tile_out, bits, tc_out, tau, run);
+    }
+
+    template <bool RUNS>
+    __device__ __forceinline__ bool next_impl(const GridView& g, double& t_out, int& tile_out,
+                                              const uint32_t* bits, int4* tc_out, double tau,
+                                              SampleRun& run) {
         const double h = g.h;
-        constexpr double kMargin = 1e-8;  // voxels; the FMA form is within ~1e-12
+        const double kMargin = g.margin;  // voxels (1e-8); the FMA form is within ~1e-12
         while (t < t1 && count < n_max) {
+            PSDF_STAT(2);
             // --- tile of p(t)
-            double v[3];
+            double v[3], r[3];
             int tc[3];
             bool near = false;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 v[a] = fma(vd[a], t, vo[a]);
                 const double fl16 = floor(v[a] * 0.0625);
-                const double r = v[a] - 16.0 * fl16;  // position inside the tile, [0, 16)
-                near |= r < kMargin || r > 16.0 - kMargin;
+                r[a] = v[a] - 16.0 * fl16;  // position inside the tile, [0, 16)
+                near |= r[a] < kMargin || r[a] > 16.0 - kMargin;
                 tc[a] = (int)fl16;
             }
             if (near) {
+                if (rewind()) continue;
                 const int4 e = exact_tile(lite(g), d3(o[0], o[1], o[2]), d3(d[0], d[1], d[2]), t);
                 tc[0] = e.x;
                 tc[1] = e.y;
                 tc[2] = e.z;
                 ++n_exact;
             }
-            bool occupied = false;
+            bool occupied = false, in_grid = false;
+            int b = 0;
             if ((unsigned)tc[0] < (unsigned)g.nt[0] && (unsigned)tc[1] < (unsigned)g.nt[1] &&
                 (unsigned)tc[2] < (unsigned)g.nt[2]) {
-                const int b = (tc[0] * g.nt[1] + tc[1]) * g.nt[2] + tc[2];
+                in_grid = true;
+                b = (tc[0] * g.nt[1] + tc[1]) * g.nt[2] + tc[2];
                 occupied = (bits[b >> 5] >> (b & 31)) & 1u;
             }
             if (occupied) {
+                // a sample: only reachable synchronised (jumps never cross an
+                // allocated tile)
+                PSDF_STAT(3);
                 t_out = t;
                 tile_out = tile_lookup(g, tc[0], tc[1], tc[2]);
                 if (tc_out) *tc_out = make_int4(tc[0], tc[1], tc[2], 0);
+                if constexpr (RUNS) {
+                    run.n = 1;
+                    run.sat = false;
+                    run.t_last = t;
+                    if (!near && tau > 0.0) {
+                        const float mn = __ldg(g.tile_min + tile_out);
+                        if (mn > 0.0f && dmul(tau, (double)mn) >= kSatX) {
+                            run.sat = true;
+                            const double n = run_length(g, v, t, h);
+                            if (n > 1.0) {
+                                const int ni = (int)fmin(n, (double)(n_max - count));
+                                run.n = ni;
+                                if (ni > 1) run.t_last = lattice_advance(t, (double)(ni - 1), h);
+                            }
+                        } else {
+                            // single sample: the 4^3 block holding its voxel
+                            // (p(t) off the block faces by the margin)
+                            int bi = 0;
+                            bool ok = true;
+#pragma unroll
+                            for (int a = 0; a < 3; ++a) {
+                                const double fb = floor(r[a] * 0.25);
+                                const double rb = r[a] - 4.0 * fb;
+                                ok &= rb > kMargin && rb < 4.0 - kMargin;
+                                bi = bi * 4 + (int)fb;
+                            }
+                            if (ok) {
+                                const float bm = __ldg(g.block_min + (int64_t)tile_out * 64 + bi);
+                                run.sat = bm > 0.0f && dmul(tau, (double)bm) >= kSatX;
+                            }
+                        }
+                    }
+#ifdef PSDF_MARCH_STATS
+                    if (run.sat) {
+                        PSDF_STAT(8);
+                        atomicAdd(&g_march_stats[9], (unsigned long long)run.n);
+                    }
+#endif
+                    t = dadd(run.t_last, h);
+                    count += run.n;
+                    return true;
+                }
                 t = dadd(t, h);
                 ++count;
                 return true;
+            }
+            // --- jump through the empty L-inf ball around p(t): every
+            // lattice point within m steps moves at most m max|d_a| voxels
+            // (the lattice argument needs a power-of-two h and t >= 64 h)
+            if (in_grid && !near && !no_jump && g.h_pow2 && t >= 64.0 * h) {
+                const int D = __ldg(g.tile_dist + b);
+                if (D >= 2) {
+                    double edge = 16.0;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) edge = fmin(edge, fmin(r[a], 16.0 - r[a]));
+                    const double m = floor((16.0 * (D - 1) + edge - 1e-6) * dinv_max);
+                    if (m >= 2.0) {
+                        PSDF_STAT(4);
+                        if (t_sync < 0.0) t_sync = t;
+                        t = lattice_advance(t, m, h);
+                        continue;
+                    }
+                }
             }
             // --- skip the empty tile.  p(t) is inside the tile and off its
             // faces (not `near`), so the box test passes and e1 > t; the skip
@@ -375,9 +564,15 @@ struct Marcher {
             if (!near && q < 1e300 && fq > mq && fq < 1.0 - mq) {
                 const double k = ceil(q);  // the + 1e-9 is inside the margin
                 t = dadd(t, dmul(k > 1.0 ? k : 1.0, h));
+                PSDF_STAT(5);
+                t_sync = -1.0;  // the reference lands on the same lattice point
+                no_jump = false;
                 continue;
             }
+            if (rewind()) continue;
+            PSDF_STAT(6);
             t = exact_skip(lite(g), d3(o[0], o[1], o[2]), d3(d[0], d[1], d[2]), tc[0], tc[1], tc[2], t);
+            no_jump = false;
             ++n_exact;
         }
         return false;
@@ -396,6 +591,9 @@ __device__ __forceinline__ double sigmoid_d(double x) { return 1.0 / (1.0 + (dou
 #else
 __device__ __forceinline__ double sigmoid_d(double x) { return __drcp_rn(dadd(1.0, exp(-x))); }
 #endif
+// sigmoid_d with the saturation shortcut: bit-identical (see kSatX).
+__device__ __forceinline__ double sigmoid_sat(double x) { return x >= kSatX ? 1.0 : sigmoid_d(x); }
+
 __device__ __forceinline__ double alpha_from(double a, double b) {
 #ifdef PSDF_ABL_ALPHA
     const double al = (a - b) * __drcp_rn(a);

@@ -42,40 +42,69 @@ struct Taps {
     float w[5];
 };
 
-// Loads a 20^3 halo of `src` around tile t; missing voxels get `fill`.
-// Optionally records the allocation mask.
-__device__ __forceinline__ void load_halo(const GridView& g, const float* __restrict__ src, int t,
-                                          float fill, float* __restrict__ buf,
-                                          unsigned char* __restrict__ alloc) {
-    const int4 tc = __ldg(g.tile_coords + t);
-    const int ox = tc.x * TE - 2, oy = tc.y * TE - 2, oz = tc.z * TE - 2;
-    for (int i = threadIdx.x; i < HV; i += blockDim.x) {
-        const int x = i / (HE * HE), y = (i / HE) % HE, z = i % HE;
-        const int vx = ox + x, vy = oy + y, vz = oz + z;
-        float v = fill;
-        bool in = false;
-        if (vx >= 0 && vy >= 0 && vz >= 0 && vx < g.res[0] && vy < g.res[1] && vz < g.res[2]) {
-            const int nt = tile_lookup(g, vx >> 4, vy >> 4, vz >> 4);
-            if (nt >= 0) {
-                v = __ldg(src + (int64_t)nt * TV + vox_index(vx & 15, vy & 15, vz & 15));
-                in = true;
+// The 27 neighbour tile ids of tile t (g.tile_nbr, -1 = unallocated or
+// outside the grid) into shared memory; call before a __syncthreads.
+__device__ __forceinline__ void stage_nbr(const GridView& g, int t, int* nb) {
+    if (threadIdx.x < 27) nb[threadIdx.x] = __ldg(g.tile_nbr + (int64_t)t * 27 + threadIdx.x);
+}
+
+// Cube of E^3 voxels around a tile, local voxel coordinates [LO, LO + E) per
+// axis (tile voxels are [0, 16)), from the per-tile array `src`; voxels of
+// unallocated tiles or outside the grid get `fill`.  With `alloc` (one bit
+// per cell, E^3 / 32 words) the allocation mask is recorded too.  Loads are
+// issued four at a time (no dependent table lookups: the neighbour ids are
+// in shared memory).
+template <int E, int LO>
+__device__ __forceinline__ void load_region(const float* __restrict__ src, const int* nb, float fill,
+                                            float* __restrict__ buf, uint32_t* __restrict__ alloc) {
+    constexpr int N = E * E * E;
+    const int step = blockDim.x;
+    for (int i0 = threadIdx.x; i0 < N; i0 += 4 * step) {
+        float v[4];
+        bool in[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = i0 + k * step;
+            v[k] = fill;
+            in[k] = false;
+            if (i < N) {
+                const int lx = i / (E * E) + LO, ly = (i / E) % E + LO, lz = i % E + LO;
+                const int n = nb[((lx >> 4) + 1) * 9 + ((ly >> 4) + 1) * 3 + (lz >> 4) + 1];
+                if (n >= 0) {
+                    v[k] = __ldg(src + (int64_t)n * TV + vox_index(lx & 15, ly & 15, lz & 15));
+                    in[k] = true;
+                }
             }
         }
-        buf[i] = v;
-        if (alloc) alloc[i] = in;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = i0 + k * step;
+            if (alloc) {
+                const unsigned m = __ballot_sync(0xffffffffu, in[k]);
+                if ((threadIdx.x & 31) == 0 && i < N) alloc[i >> 5] = m;
+            }
+            if (i < N) buf[i] = v[k];
+        }
     }
 }
 
-// Separable 5-tap pass over the halo: out(tile voxels) = G * halo.
-// mode 0: dst[t] = result (smoothing); mode 1: dst[t] += result (fold).
+__device__ __forceinline__ bool bit_at(const uint32_t* bits, int i) { return (bits[i >> 5] >> (i & 31)) & 1u; }
+
+// K7: the G^T fold (grads.cpp:67-96): dst[t] += G * src over a 20^3 halo of
+// src filled with 0 (the reference skips unallocated / out-of-range taps, and
+// the Gaussian is symmetric, so G^T is the same stencil).  Separable 5-tap
+// passes in shared memory.
 __global__ void __launch_bounds__(256) smooth_fold_kernel(GridView g, const float* __restrict__ src,
                                                           float fill, float* __restrict__ dst,
                                                           int accumulate, Taps taps) {
     extern __shared__ __align__(16) float sh[];
+    __shared__ int nb[27];
     float* A = sh;           // [20][20][20]
     float* B = sh + HV;      // [16][20][20] after the x pass
     const int t = blockIdx.x;
-    load_halo(g, src, t, fill, A, nullptr);
+    stage_nbr(g, t, nb);
+    __syncthreads();
+    load_region<HE, -2>(src, nb, fill, A, nullptr);
     __syncthreads();
     // x pass: B[x][y][z] = sum_d w[d] A[x+d+2][y][z], x in [0,16)
     for (int i = threadIdx.x; i < 16 * HE * HE; i += blockDim.x) {
@@ -108,192 +137,314 @@ __global__ void __launch_bounds__(256) smooth_fold_kernel(GridView g, const floa
             out[i] = s;
     }
 }
+constexpr size_t kFoldSmem = sizeof(float) * (HV + 16 * HE * HE);
 
-// Apron copy of the smoothed SDF (psdf_device.cuh, sample_sdf_in): cell
-// (x, y, z) in [-1, 16]^3 of tile t holds smooth_value at that global voxel,
-// i.e. the owning tile's value or the far field.
-__global__ void __launch_bounds__(256) apron_fill_kernel(GridView g, const float* __restrict__ smooth,
-                                                         float* __restrict__ ap) {
+// K9: SparseGrid::smooth_all (grid.cpp:204-250) fused with the samplers'
+// apron copy.  The tile's smoothed values AND its 1-voxel apron (18^3, the
+// neighbours' smoothed values or the far field where the neighbour tile is
+// unallocated / outside the grid) come from one 22^3 raw halo, so no second
+// pass over the smoothed grid is needed; every smoothed value is the same
+// fp32 expression (same taps, same summation order) whichever tile's block
+// computes it.  Also writes the brick minima of the saturation test
+// (tile_min, block_min; psdf_device.cuh kSatX).
+constexpr int SE = 22;  // raw halo edge: local voxels [-3, 19)
+constexpr size_t kSmoothApronSmem = sizeof(float) * (SE * SE * SE + AE * SE * SE);
+__global__ void __launch_bounds__(256) smooth_apron_kernel(GridView g, const float* __restrict__ raw,
+                                                           float fill, float* __restrict__ smooth,
+                                                           float* __restrict__ ap, float* __restrict__ tmin,
+                                                           float* __restrict__ bmin, Taps taps) {
+    extern __shared__ __align__(16) float sh[];
+    __shared__ int nb[27];
+    __shared__ float red[2];
+    float* A = sh;                  // [22][22][22] raw halo; later [18][18][22]
+    float* B = sh + SE * SE * SE;   // [18][22][22] after the x pass; later the 18^3 apron
     const int t = blockIdx.x;
-    const int4 tc = __ldg(g.tile_coords + t);
+    stage_nbr(g, t, nb);
+    __syncthreads();
+    load_region<SE, -3>(raw, nb, fill, A, nullptr);
+    __syncthreads();
+    for (int i = threadIdx.x; i < AE * SE * SE; i += blockDim.x) {
+        const int x = i / (SE * SE), yz = i % (SE * SE);
+        float s = 0.f;
+#pragma unroll
+        for (int d = 0; d < 5; ++d) s += taps.w[d] * A[(x + d) * SE * SE + yz];
+        B[i] = s;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < AE * AE * SE; i += blockDim.x) {
+        const int x = i / (AE * SE), y = (i / SE) % AE, z = i % SE;
+        float s = 0.f;
+#pragma unroll
+        for (int d = 0; d < 5; ++d) s += taps.w[d] * B[(x * SE + y + d) * SE + z];
+        A[i] = s;
+    }
+    __syncthreads();
+    float* apt = ap + (int64_t)t * AV;
+    float* sm = smooth + (int64_t)t * TV;
     for (int i = threadIdx.x; i < AV; i += blockDim.x) {
-        const int x = i / (AE * AE) - 1, y = (i / AE) % AE - 1, z = i % AE - 1;
-        const int vx = tc.x * TE + x, vy = tc.y * TE + y, vz = tc.z * TE + z;
-        float v = (float)g.far;
-        if ((unsigned)x < 16u && (unsigned)y < 16u && (unsigned)z < 16u) {
-            v = smooth[(int64_t)t * TV + vox_index(x, y, z)];
-        } else if (vx >= 0 && vy >= 0 && vz >= 0 && vx < g.res[0] && vy < g.res[1] && vz < g.res[2]) {
-            const int nt = tile_lookup(g, vx >> 4, vy >> 4, vz >> 4);
-            if (nt >= 0) v = smooth[(int64_t)nt * TV + vox_index(vx & 15, vy & 15, vz & 15)];
+        const int x = i / (AE * AE), y = (i / AE) % AE, z = i % AE;  // local voxel = (x,y,z) - 1
+        float s = 0.f;
+#pragma unroll
+        for (int d = 0; d < 5; ++d) s += taps.w[d] * A[(x * AE + y) * SE + z + d];
+        const int lx = x - 1, ly = y - 1, lz = z - 1;
+        const bool own = (unsigned)lx < 16u && (unsigned)ly < 16u && (unsigned)lz < 16u;
+        if (own) {
+            sm[vox_index(lx, ly, lz)] = s;
+        } else if (nb[((lx >> 4) + 1) * 9 + ((ly >> 4) + 1) * 3 + (lz >> 4) + 1] < 0) {
+            s = (float)g.far;  // smooth_value (grid.cpp:87-94)
         }
-        ap[(int64_t)t * AV + i] = v;
+        apt[i] = s;
+        B[i] = s;
+    }
+    __syncthreads();
+    // brick minima: each 4^3 block's 6^3 brick (voxels 4b-1 .. 4b+4) and the tile
+    if (threadIdx.x < 64) {
+        const int bx = threadIdx.x >> 4, by = (threadIdx.x >> 2) & 3, bz = threadIdx.x & 3;
+        float mn = 3.4e38f;
+        for (int x = 0; x < 6; ++x)
+            for (int y = 0; y < 6; ++y)
+#pragma unroll
+                for (int z = 0; z < 6; ++z) mn = fminf(mn, B[((4 * bx + x) * AE + 4 * by + y) * AE + 4 * bz + z]);
+        bmin[(int64_t)t * 64 + threadIdx.x] = mn;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mn;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) tmin[t] = fminf(red[0], red[1]);
+}
+
+// The apron copy (and brick minima) from an already smoothed grid: used when
+// the host uploads its own smoothed values (psdf_upload_grid with `smooth`).
+__global__ void __launch_bounds__(256) apron_fill_kernel(GridView g, const float* __restrict__ smooth,
+                                                         float* __restrict__ ap, float* __restrict__ tmin,
+                                                         float* __restrict__ bmin) {
+    __shared__ float B[AV];
+    __shared__ int nb[27];
+    __shared__ float red[2];
+    const int t = blockIdx.x;
+    stage_nbr(g, t, nb);
+    __syncthreads();
+    load_region<AE, -1>(smooth, nb, (float)g.far, B, nullptr);
+    __syncthreads();
+    float* apt = ap + (int64_t)t * AV;
+    for (int i = threadIdx.x; i < AV; i += blockDim.x) apt[i] = B[i];
+    if (threadIdx.x < 64) {
+        const int bx = threadIdx.x >> 4, by = (threadIdx.x >> 2) & 3, bz = threadIdx.x & 3;
+        float mn = 3.4e38f;
+        for (int x = 0; x < 6; ++x)
+            for (int y = 0; y < 6; ++y)
+#pragma unroll
+                for (int z = 0; z < 6; ++z) mn = fminf(mn, B[((4 * bx + x) * AE + 4 * by + y) * AE + 4 * bz + z]);
+        bmin[(int64_t)t * 64 + threadIdx.x] = mn;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mn;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) tmin[t] = fminf(red[0], red[1]);
+}
+
+// Block-wide sums of NV doubles, one atomic per value per block.
+template <int NV>
+__device__ __forceinline__ void block_add_f64v(double* const* dst, double* v, double* red) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (l == 0)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) red[k * 32 + w] = v[k];
+    __syncthreads();
+    if (threadIdx.x < NV) {
+        double s = 0.0;
+        for (int i = 0; i < nw; ++i) s += red[threadIdx.x * 32 + i];
+        if (s != 0.0) atomicAdd(dst[threadIdx.x], s);
     }
 }
 
 __device__ __forceinline__ void block_add_f64(double* dst, double v, double* red) {
-    // block-wide sum of one double per thread, one atomic per block
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    __syncthreads();
-    if (l == 0) red[w] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
-        if (s != 0.0) atomicAdd(dst, s);
-    }
+    double* d[1] = {dst};
+    double vv[1] = {v};
+    block_add_f64v<1>(d, vv, red);
 }
 
-// K3: loss_sdf (losses.cpp:121-142) over tiles [t0, t1)
-__global__ void __launch_bounds__(256) loss_sdf_kernel(GridView g, const float* __restrict__ raw,
-                                                       int t0, int t1, float lambda,
-                                                       float* __restrict__ g_smooth,
-                                                       float* __restrict__ g_raw, double* stats) {
-    __shared__ double red[8];
-    const int64_t n = (int64_t)(t1 - t0) * TV;
-    const int64_t base = (int64_t)t0 * TV;
-    double pl = 0.0, wt = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const float s = g.smooth[base + i], r = raw[base + i];
-        const float d = s - r;
-        const float as = fabsf(s), ar = fabsf(r);
-        const float w = (1.f / ((as > ar ? as : ar) + (float)kPhotoEps)) * (1.f / (1.f + as * 5.f));
-        pl += (double)(lambda * d * d);
-        wt += (double)(lambda * w * d * d);
-        const float gg = 2.f * lambda * w * d;
-        if (gg != 0.f) {
-            g_smooth[base + i] += gg;
-            g_raw[base + i] -= gg;
-        }
-    }
-    block_add_f64(stats + 3, pl, red);
-    block_add_f64(stats + 8, wt, red);
-}
-
-// K4: loss_eikonal + loss_normal (losses.cpp:144-220) for tile blockIdx.x + t0.
+// K3 + K4: loss_sdf, loss_eikonal and loss_normal (losses.cpp:121-220) of tile
+// t0 + blockIdx.x in one pass over its 20^3 smoothed halo (TileHalo,
+// losses.cpp:61-117).
 //
-// Atomic-free gather form of the TileHalo stencil scatter (losses.cpp:61-117):
-// every term deposits a vector dg at a centre w and the stencil adds
-// +-dg_b * inv2h at w -+ e_b.  Phase 1 sums, per centre w in the tile plus its
-// +1 shell ([2,18]^3 in halo coordinates), the vectors of all terms centred
-// there: the eikonal term of w, dg1 of the normal pairs (w, w+e_a) and dg2 of
-// the pairs (w-e_a, w).  Phase 2 gathers the stencil at every halo cell.
-constexpr int DE = 17;  // centres [2, 18] in halo coordinates
-__global__ void __launch_bounds__(256) loss_eik_normal_kernel(GridView g, int t0, float l_eik,
-                                                              float l_norm, float inv2h,
-                                                              float* __restrict__ g_smooth,
-                                                              double* stats) {
+// Atomic-free gather form of the TileHalo stencil scatter: every term
+// deposits a vector dg at a centre w and the stencil adds +-dg_b * inv2h at
+// w -+ e_b.  Phase A stores the central-difference gradient at every centre
+// of the tile plus its +1 shell ([2,18]^3 in halo coordinates); phase B sums,
+// per centre, the vectors of all terms centred there (the eikonal term of w,
+// dg1 of the normal pairs (w, w+e_a), dg2 of the pairs (w-e_a, w)) into
+// registers, which then overwrite the gradients; phase C gathers the stencil
+// at every allocated cell it reaches, adds the sdf term on the tile's own
+// voxels and flushes with global atomics (neighbour tiles' blocks reach the
+// same cells).
+constexpr int DE = 17;                 // centres [2, 18] in halo coordinates
+constexpr int DN = DE * DE * DE;       // 4913
+constexpr int LG_THREADS = 512;
+constexpr int LG_PER = (DN + LG_THREADS - 1) / LG_THREADS;  // centres per thread
+constexpr size_t kLossGridSmem = sizeof(float) * (HV + 3 * DN + TV) + sizeof(uint32_t) * (HV / 32);
+__global__ void __launch_bounds__(LG_THREADS, 2) loss_grid_kernel(GridView g, const float* __restrict__ raw,
+                                                                 int t0, float l_sdf, float l_eik,
+                                                                 float l_norm, float inv2h,
+                                                                 float* __restrict__ g_smooth,
+                                                                 float* __restrict__ g_raw, double* stats) {
     extern __shared__ __align__(16) float sh[];
-    float* val = sh;                          // [20^3] smoothed values (far field outside)
-    float* D = sh + HV;                       // [17^3][3] stencil vectors per centre
-    unsigned char* alloc = reinterpret_cast<unsigned char*>(sh + HV + 3 * DE * DE * DE);
-    __shared__ double red[8];
+    float* val = sh;                  // [20^3] smoothed values (far field outside)
+    float* P = sh + HV;               // [17^3][3] gradients, then stencil vectors D
+    float* W = P + 3 * DN;            // [16^3] proximity weights (losses.hpp:20)
+    uint32_t* alloc = reinterpret_cast<uint32_t*>(W + TV);  // [20^3] bits
+    __shared__ int nb[27];
+    __shared__ double red[6 * 32];
     const int t = t0 + blockIdx.x;
-    load_halo(g, g.smooth, t, (float)g.far, val, alloc);
+    stage_nbr(g, t, nb);
     __syncthreads();
-    auto grad_at = [&](int x, int y, int z, float& gx, float& gy, float& gz) {
-        gx = (val[hidx(x + 1, y, z)] - val[hidx(x - 1, y, z)]) * inv2h;
-        gy = (val[hidx(x, y + 1, z)] - val[hidx(x, y - 1, z)]) * inv2h;
-        gz = (val[hidx(x, y, z + 1)] - val[hidx(x, y, z - 1)]) * inv2h;
-    };
+    load_region<HE, -2>(g.smooth, nb, (float)g.far, val, alloc);
+    __syncthreads();
     auto in_tile = [](int x, int y, int z) {
         return x >= 2 && x < 18 && y >= 2 && y < 18 && z >= 2 && z < 18;
     };
-    double e_pl = 0.0, e_wt = 0.0, n_pl = 0.0, n_wt = 0.0;
-    for (int i = threadIdx.x; i < DE * DE * DE; i += blockDim.x) {
+    // phase A
+    for (int i = threadIdx.x; i < DN; i += LG_THREADS) {
         const int x = i / (DE * DE) + 2, y = (i / DE) % DE + 2, z = i % DE + 2;
+        P[3 * i] = (val[hidx(x + 1, y, z)] - val[hidx(x - 1, y, z)]) * inv2h;
+        P[3 * i + 1] = (val[hidx(x, y + 1, z)] - val[hidx(x, y - 1, z)]) * inv2h;
+        P[3 * i + 2] = (val[hidx(x, y, z + 1)] - val[hidx(x, y, z - 1)]) * inv2h;
+    }
+    for (int j = threadIdx.x; j < TV; j += LG_THREADS) {
+        const int x = (j >> 8) + 2, y = ((j >> 4) & 15) + 2, z = (j & 15) + 2;
+        W[j] = 1.f / (1.f + fabsf(val[hidx(x, y, z)]) * 5.f);
+    }
+    __syncthreads();
+    // phase B
+    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // sdf pl/wt, eik pl/wt, normal pl/wt
+    float D[LG_PER][3];
+    constexpr int SX = DE * DE, SY = DE;
+#pragma unroll
+    for (int k = 0; k < LG_PER; ++k) {
+        const int i = threadIdx.x + k * LG_THREADS;
         float dx = 0.f, dy = 0.f, dz = 0.f;
-        float gx, gy, gz;
-        grad_at(x, y, z, gx, gy, gz);
-        const float len = sqrtf(gx * gx + gy * gy + gz * gz);
-        const bool own = in_tile(x, y, z);
-        if (own) {
-            const float w = 1.f / (1.f + fabsf(val[hidx(x, y, z)]) * 5.f);  // losses.hpp:20
-            const float e = len - 1.f;
-            e_pl += (double)(l_eik * e * e);
-            e_wt += (double)(l_eik * w * e * e);
-            if (len > 1e-12f) {
-                const float c = 2.f * l_eik * w * e / len;
-                dx += c * gx;
-                dy += c * gy;
-                dz += c * gz;
+        if (i < DN) {
+            const int x = i / (DE * DE) + 2, y = (i / DE) % DE + 2, z = i % DE + 2;
+            const float gx = P[3 * i], gy = P[3 * i + 1], gz = P[3 * i + 2];
+            const float len = sqrtf(gx * gx + gy * gy + gz * gz);
+            const float inv = 1.f / len;
+            if (in_tile(x, y, z)) {
+                const float w = W[((x - 2) * 16 + (y - 2)) * 16 + (z - 2)];
+                const float e = len - 1.f;
+                acc[2] += (double)(l_eik * e * e);
+                acc[3] += (double)(l_eik * w * e * e);
+                if (len > 1e-12f) {
+                    const float c = 2.f * l_eik * w * e * inv;
+                    dx += c * gx;
+                    dy += c * gy;
+                    dz += c * gz;
+                }
+                if (len >= 1e-8f) {  // pairs (w, w + e_a): the dg1 side, and the loss
+                    const float n1x = gx * inv, n1y = gy * inv, n1z = gz * inv;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        const int nx = x + (a == 0), ny = y + (a == 1), nz = z + (a == 2);
+                        if (!bit_at(alloc, hidx(nx, ny, nz))) continue;
+                        const int j = i + (a == 0 ? SX : a == 1 ? SY : 1);
+                        const float hx = P[3 * j], hy = P[3 * j + 1], hz = P[3 * j + 2];
+                        const float l2 = sqrtf(hx * hx + hy * hy + hz * hz);
+                        if (l2 < 1e-8f) continue;
+                        const float i2 = 1.f / l2;
+                        const float ddx = hx * i2 - n1x, ddy = hy * i2 - n1y, ddz = hz * i2 - n1z;
+                        const float vv = ddx * ddx + ddy * ddy + ddz * ddz;
+                        acc[4] += (double)(l_norm * vv);
+                        acc[5] += (double)(l_norm * w * vv);
+                        const float c = 2.f * l_norm * w;
+                        // dn1 = -c d ; dg1 = (dn1 - n1 (dn1 . n1)) / l1
+                        const float m1x = -c * ddx, m1y = -c * ddy, m1z = -c * ddz;
+                        const float p1 = m1x * n1x + m1y * n1y + m1z * n1z;
+                        dx += (m1x - n1x * p1) * inv;
+                        dy += (m1y - n1y * p1) * inv;
+                        dz += (m1z - n1z * p1) * inv;
+                    }
+                }
             }
-            if (len >= 1e-8f) {  // pairs (w, w + e_a): the dg1 side, and the loss
-                const float n1x = gx / len, n1y = gy / len, n1z = gz / len;
+            // pairs (w - e_a, w) with w - e_a in the tile: the dg2 side
+            if (len >= 1e-8f && bit_at(alloc, hidx(x, y, z))) {
+                const float n2x = gx * inv, n2y = gy * inv, n2z = gz * inv;
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
-                    const int nx = x + (a == 0), ny = y + (a == 1), nz = z + (a == 2);
-                    if (!alloc[hidx(nx, ny, nz)]) continue;
-                    float hx, hy, hz;
-                    grad_at(nx, ny, nz, hx, hy, hz);
-                    const float l2 = sqrtf(hx * hx + hy * hy + hz * hz);
-                    if (l2 < 1e-8f) continue;
-                    const float ddx = hx / l2 - n1x, ddy = hy / l2 - n1y, ddz = hz / l2 - n1z;
-                    const float vv = ddx * ddx + ddy * ddy + ddz * ddz;
-                    n_pl += (double)(l_norm * vv);
-                    n_wt += (double)(l_norm * w * vv);
+                    const int px = x - (a == 0), py = y - (a == 1), pz = z - (a == 2);
+                    if (!in_tile(px, py, pz)) continue;
+                    const int j = i - (a == 0 ? SX : a == 1 ? SY : 1);
+                    const float hx = P[3 * j], hy = P[3 * j + 1], hz = P[3 * j + 2];
+                    const float l1 = sqrtf(hx * hx + hy * hy + hz * hz);
+                    if (l1 < 1e-8f) continue;
+                    const float i1 = 1.f / l1;
+                    const float w = W[((px - 2) * 16 + (py - 2)) * 16 + (pz - 2)];
                     const float c = 2.f * l_norm * w;
-                    // dn1 = -c d ; dg1 = (dn1 - n1 (dn1 . n1)) / l1
-                    const float m1x = -c * ddx, m1y = -c * ddy, m1z = -c * ddz;
-                    const float p1 = m1x * n1x + m1y * n1y + m1z * n1z;
-                    dx += (m1x - n1x * p1) / len;
-                    dy += (m1y - n1y * p1) / len;
-                    dz += (m1z - n1z * p1) / len;
+                    const float m2x = c * (n2x - hx * i1), m2y = c * (n2y - hy * i1),
+                                m2z = c * (n2z - hz * i1);
+                    const float p2 = m2x * n2x + m2y * n2y + m2z * n2z;
+                    dx += (m2x - n2x * p2) * inv;
+                    dy += (m2y - n2y * p2) * inv;
+                    dz += (m2z - n2z * p2) * inv;
                 }
             }
         }
-        // pairs (w - e_a, w) with w - e_a in the tile: the dg2 side
-        if (len >= 1e-8f && alloc[hidx(x, y, z)]) {
-            const float n2x = gx / len, n2y = gy / len, n2z = gz / len;
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                const int px = x - (a == 0), py = y - (a == 1), pz = z - (a == 2);
-                if (!in_tile(px, py, pz)) continue;
-                float hx, hy, hz;
-                grad_at(px, py, pz, hx, hy, hz);
-                const float l1 = sqrtf(hx * hx + hy * hy + hz * hz);
-                if (l1 < 1e-8f) continue;
-                const float w = 1.f / (1.f + fabsf(val[hidx(px, py, pz)]) * 5.f);
-                const float c = 2.f * l_norm * w;
-                const float m2x = c * (n2x - hx / l1), m2y = c * (n2y - hy / l1),
-                            m2z = c * (n2z - hz / l1);
-                const float p2 = m2x * n2x + m2y * n2y + m2z * n2z;
-                dx += (m2x - n2x * p2) / len;
-                dy += (m2y - n2y * p2) / len;
-                dz += (m2z - n2z * p2) / len;
-            }
-        }
-        D[3 * i] = dx;
-        D[3 * i + 1] = dy;
-        D[3 * i + 2] = dz;
+        D[k][0] = dx;
+        D[k][1] = dy;
+        D[k][2] = dz;
     }
     __syncthreads();
-    // phase 2: gather the stencils and flush (TileHalo::flush, losses.cpp:87-97)
-    const int4 tc = __ldg(g.tile_coords + t);
-    const int ox = tc.x * TE - 2, oy = tc.y * TE - 2, oz = tc.z * TE - 2;
-    auto dval = [&](int x, int y, int z, int b) -> float {
-        if (x < 2 || x > 18 || y < 2 || y > 18 || z < 2 || z > 18) return 0.f;
-        return D[3 * (((x - 2) * DE + (y - 2)) * DE + (z - 2)) + b];
-    };
-    for (int i = threadIdx.x; i < HV; i += blockDim.x) {
-        if (!alloc[i]) continue;
-        const int x = i / (HE * HE), y = (i / HE) % HE, z = i % HE;
-        const float gv = (dval(x - 1, y, z, 0) - dval(x + 1, y, z, 0) + dval(x, y - 1, z, 1) -
-                          dval(x, y + 1, z, 1) + dval(x, y, z - 1, 2) - dval(x, y, z + 1, 2)) *
-                         inv2h;
-        if (gv == 0.f) continue;
-        const int vx = ox + x, vy = oy + y, vz = oz + z;
-        const int nt = tile_lookup(g, vx >> 4, vy >> 4, vz >> 4);
-        atomicAdd(g_smooth + (int64_t)nt * TV + vox_index(vx & 15, vy & 15, vz & 15), gv);
+#pragma unroll
+    for (int k = 0; k < LG_PER; ++k) {
+        const int i = threadIdx.x + k * LG_THREADS;
+        if (i < DN) {
+            P[3 * i] = D[k][0];
+            P[3 * i + 1] = D[k][1];
+            P[3 * i + 2] = D[k][2];
+        }
     }
-    block_add_f64(stats + 4, e_pl, red);
-    block_add_f64(stats + 9, e_wt, red);
-    block_add_f64(stats + 5, n_pl, red);
-    block_add_f64(stats + 10, n_wt, red);
+    __syncthreads();
+    // phase C: cells [1, 19]^3 (everything the stencils reach)
+    auto dv = [&](int x, int y, int z, int b) -> float {
+        if (x < 2 || x > 18 || y < 2 || y > 18 || z < 2 || z > 18) return 0.f;
+        return P[3 * (((x - 2) * DE + (y - 2)) * DE + (z - 2)) + b];
+    };
+    constexpr int CE = 19;
+    const float* rt = raw + (int64_t)t * TV;
+    float* grt = g_raw + (int64_t)t * TV;
+    for (int i = threadIdx.x; i < CE * CE * CE; i += LG_THREADS) {
+        const int x = i / (CE * CE) + 1, y = (i / CE) % CE + 1, z = i % CE + 1;
+        if (!bit_at(alloc, hidx(x, y, z))) continue;
+        float gv = (dv(x - 1, y, z, 0) - dv(x + 1, y, z, 0) + dv(x, y - 1, z, 1) - dv(x, y + 1, z, 1) +
+                    dv(x, y, z - 1, 2) - dv(x, y, z + 1, 2)) *
+                   inv2h;
+        const int lx = x - 2, ly = y - 2, lz = z - 2;
+        if (in_tile(x, y, z)) {  // loss_sdf (losses.cpp:121-142) on the tile's own voxels
+            const int v = vox_index(lx, ly, lz);
+            const float sv = val[hidx(x, y, z)], r = __ldg(rt + v);
+            const float d = sv - r;
+            const float as = fabsf(sv), ar = fabsf(r);
+            const float w = (1.f / ((as > ar ? as : ar) + (float)kPhotoEps)) * (1.f / (1.f + as * 5.f));
+            acc[0] += (double)(l_sdf * d * d);
+            acc[1] += (double)(l_sdf * w * d * d);
+            const float gg = 2.f * l_sdf * w * d;
+            if (gg != 0.f) {
+                gv += gg;
+                grt[v] -= gg;
+            }
+        }
+        if (gv == 0.f) continue;
+        const int n = nb[((lx >> 4) + 1) * 9 + ((ly >> 4) + 1) * 3 + (lz >> 4) + 1];
+        atomicAdd(g_smooth + (int64_t)n * TV + vox_index(lx & 15, ly & 15, lz & 15), gv);
+    }
+    double* dst[6] = {stats + 3, stats + 8, stats + 4, stats + 9, stats + 5, stats + 10};
+    block_add_f64v<6>(dst, acc, red);
 }
-constexpr size_t kEikNormalSmem = sizeof(float) * (HV + 3 * DE * DE * DE) + HV;
 
 // K5: loss_features (losses.cpp:222-257); block = one (tile, plane), one
 // thread per texel channel, gathering the pair terms it belongs to (no

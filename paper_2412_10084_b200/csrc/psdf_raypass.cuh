@@ -428,6 +428,10 @@ __global__ void __launch_bounds__(BLOCK) render_kernel(RayPassParams P) {
     const int lane = threadIdx.x & 31;
     unsigned long long c_m = 0, c_x = 0, c_sh = 0;
     const int n_work = (int)(P.tile_end - P.tile_begin);
+    // saturated runs skip the per-sample early-stop test, valid while the
+    // transmittance they leave unchanged is not already below the threshold
+    // (only possible for a threshold above 1)
+    const double tau_run = P.early_stop > 1.0 ? 0.0 : P.tau;
     for (;;) {
         int wi = 0;
         if (lane == 0) wi = (int)atomicAdd(P.work_counter, 1ull);
@@ -452,25 +456,42 @@ __global__ void __launch_bounds__(BLOCK) render_kernel(RayPassParams P) {
             double t_cur = 0.0, s_cur = 0.0, a_cur = 0.0;
             int tile_cur = -1;
             int4 tc_cur;
-            bool active = mr.init(g, V.cam.pos, dd, P.n_max) && mr.next(g, t_cur, tile_cur, bits, &tc_cur);
+            SampleRun run;
+            bool active = mr.init(g, V.cam.pos, dd, P.n_max) &&
+                          mr.next_run(g, t_cur, tile_cur, bits, &tc_cur, tau_run, run);
             if (active) {
-                double pc[3];
-                mr.pos(t_cur, pc);
-                s_cur = sample_sdf_in(g, pc[0], pc[1], pc[2], tile_cur, tc_cur);
-                a_cur = sigmoid_d(dmul(P.tau, s_cur));
                 ++c_x;
+                if (run.sat) {  // saturated run: sigmoid 1, alpha 0 (kSatX)
+                    a_cur = 1.0;
+                    c_m += run.n - 1;
+                    t_cur = run.t_last;
+                } else {
+                    double pc[3];
+                    mr.pos(t_cur, pc);
+                    s_cur = sample_sdf_in(g, pc[0], pc[1], pc[2], tile_cur, tc_cur);
+                    a_cur = sigmoid_sat(dmul(P.tau, s_cur));
+                }
             }
             while (active) {
                 double t_nxt;
                 int tile_nxt;
                 int4 tc_nxt;
-                const bool has_next = mr.next(g, t_nxt, tile_nxt, bits, &tc_nxt);
+                const bool has_next = mr.next_run(g, t_nxt, tile_nxt, bits, &tc_nxt, tau_run, run);
+                if (has_next && run.sat) {
+                    // the pending sample and the run's first n-1 settle with
+                    // alpha 0: no weight, colour, depth or transmittance change
+                    c_m += run.n;
+                    t_cur = run.t_last;
+                    tile_cur = tile_nxt;
+                    a_cur = 1.0;
+                    continue;
+                }
                 double pn[3];
                 mr.pos(has_next ? t_nxt : dadd(t_cur, g.h), pn);
                 const double s_nxt = has_next ? sample_sdf_in(g, pn[0], pn[1], pn[2], tile_nxt, tc_nxt)
                                               : sample_sdf(g, pn[0], pn[1], pn[2]);
-                const double a_nxt = sigmoid_d(dmul(P.tau, s_nxt));
-                const double alpha = alpha_from(a_cur, a_nxt);
+                const double a_nxt = sigmoid_sat(dmul(P.tau, s_nxt));
+                const double alpha = a_nxt == 1.0 ? 0.0 : alpha_from(a_cur, a_nxt);
                 const double w = dmul(trans, alpha);
                 if (P.need_colors && w > 0.0 && tile_cur >= 0) {
                     double pc[3];

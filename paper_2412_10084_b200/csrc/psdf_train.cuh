@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
     const uint32_t* bits = stage_tile_bits(g, sm_bits, P.bits_sm_words);
     __syncthreads();
     const double tau = P.tau;
+    const double tau_run = P.early_stop > 1.0 ? 0.0 : tau;  // see render_kernel
     double st_photo = 0.0, st_sq = 0.0;
     unsigned long long st_mask = 0, c_m = 0, c_x = 0, c_sh = 0, c_bwd = 0, c_ex = 0;
     const int n_work = (int)(P.tile_end - P.tile_begin);
@@ -162,23 +163,39 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
             int tile_nxt = -1;
             bool has_next = false, settle = false, want_entry = false, shade = false;
             double a_nxt = 0.0, alpha = 0.0;
+            int n_settle = 0;
             if (alive) {
                 int4 tc_nxt;
-                has_next = mr.next(g, t_nxt, tile_nxt, bits, &tc_nxt);
+                SampleRun run;
+                has_next = mr.next_run(g, t_nxt, tile_nxt, bits, &tc_nxt, tau_run, run);
                 if (!has_next && !have_cur) {
                     alive = false;  // no sample at all
+                } else if (has_next && run.sat) {
+                    // a run of saturated samples: sigmoid 1, every alpha
+                    // settled against them is exactly 0 (no weight, no entry,
+                    // no record, transmittance unchanged); the run's last
+                    // sample becomes the pending one
+                    a_nxt = 1.0;
+                    n_settle = run.n - (have_cur ? 0 : 1);
+                    if (!have_cur) {
+                        have_cur = true;
+                        ++c_x;
+                    }
+                    settle = n_settle > 0;
+                    t_nxt = run.t_last;
                 } else {
                     double pn[3];
                     mr.pos(has_next ? t_nxt : dadd(t_cur, g.h), pn);
                     const double s_nxt = has_next ? sample_sdf_in(g, pn[0], pn[1], pn[2], tile_nxt, tc_nxt)
                                                   : sample_sdf(g, pn[0], pn[1], pn[2]);
-                    a_nxt = sigmoid_d(dmul(tau, s_nxt));
+                    a_nxt = sigmoid_sat(dmul(tau, s_nxt));
                     if (!have_cur) {
                         have_cur = true;
                         ++c_x;
                     } else {
                         settle = true;
-                        alpha = alpha_from(a_cur, a_nxt);
+                        n_settle = 1;
+                        alpha = a_nxt == 1.0 ? 0.0 : alpha_from(a_cur, a_nxt);
                         w = dmul(trans, alpha);
                         if (alpha > 0.0 && cnt_first < 0) {
                             cnt_first = mr.count - 1 - (has_next ? 1 : 0);
@@ -228,7 +245,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
                 if (settle) {
                     acc = dadd(acc, w);
                     trans = dmul(trans, dsub(1.0, alpha));
-                    ++n_live;
+                    n_live += n_settle;
                     if ((P.early_stop > 0.0 && trans < P.early_stop) || !has_next) alive = false;
                 }
                 t_cur = t_nxt;
@@ -367,7 +384,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) alpha_bwd_kernel(RayPa
         mr.next(g, t_cur, tile_cur, bits, &tc_cur);  // re-emits the first alpha > 0 sample
         double pc[3];
         mr.pos(t_cur, pc);
-        double a_cur = sigmoid_d(dmul(tau, sample_sdf_in(g, pc[0], pc[1], pc[2], tile_cur, tc_cur)));
+        double a_cur = sigmoid_sat(dmul(tau, sample_sdf_in(g, pc[0], pc[1], pc[2], tile_cur, tc_cur)));
         double T = 1.0, pre = 0.0, carry = 0.0;
         int idx = W.e_cfirst[e];
         for (;;) {
@@ -379,8 +396,8 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) alpha_bwd_kernel(RayPa
             mr.pos(has_next ? t_nxt : dadd(t_cur, g.h), pn);
             const double s_nxt = has_next ? sample_sdf_in(g, pn[0], pn[1], pn[2], tile_nxt, tc_nxt)
                                           : sample_sdf(g, pn[0], pn[1], pn[2]);
-            const double a_nxt = sigmoid_d(dmul(tau, s_nxt));
-            const double alpha = alpha_from(a_cur, a_nxt);
+            const double a_nxt = sigmoid_sat(dmul(tau, s_nxt));
+            const double alpha = a_nxt == 1.0 ? 0.0 : alpha_from(a_cur, a_nxt);
             const double w = dmul(T, alpha);
             if (alpha > 0.0) ++c_al;
             const bool shade = in_mask && w > 0.0 && tile_cur >= 0;
@@ -397,10 +414,10 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) alpha_bwd_kernel(RayPa
                 rec = W.r_next[rec];
             }
             pre = dadd(pre, dmul(dw, w));
-            const double suffix = dsub(total, pre);
-            const double om_a = dsub(1.0, alpha);
-            const double dalpha = dsub(dmul(dw, T), om_a > 1e-12 ? ddiv(suffix, om_a) : 0.0);
             double own = 0.0, nxt = 0.0;
+            const double om_a = dsub(1.0, alpha);
+            const double dalpha =
+                alpha > 0.0 ? dsub(dmul(dw, T), om_a > 1e-12 ? ddiv(dsub(total, pre), om_a) : 0.0) : 0.0;
             if (alpha > 0.0 && dalpha != 0.0) {  // renderer.cpp:266-276
                 const double da = dmul(dmul(tau, a_cur), dsub(1.0, a_cur));
                 const double db = dmul(dmul(tau, a_nxt), dsub(1.0, a_nxt));

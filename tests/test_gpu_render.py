@@ -46,20 +46,30 @@ def test_pixel_dirs_bit_exact():
             assert np.array_equal(d[v, u], pixel_dir(oc, u + 0.5, v + 0.5))
 
 
-@pytest.mark.parametrize("res,band", [(32, 32), (64, 3)])
-def test_march_bit_exact(ctx, res, band):
-    g, a = make_scene(res=res, band=band, radius=0.3)
-    og, sm = oracle_with_f32_smooth(a)
-    _upload(ctx, g, sm)
-    rng = np.random.default_rng(11)
-    o = rng.uniform(-1.5, 1.5, (3000, 3))
+def _march_rays(n, seed, span=1.5, tgt_span=0.45):
+    rng = np.random.default_rng(seed)
+    o = rng.uniform(-span, span, (n, 3))
     o[:100] = [1.2, 0.1, 0.2]
-    tgt = rng.uniform(-0.45, 0.45, (3000, 3))
+    # far cameras: t crosses several powers of two before the grid
+    o[100:400] *= rng.uniform(2.0, 12.0, (300, 1))
+    tgt = rng.uniform(-tgt_span, tgt_span, (n, 3))
     d = tgt - o
     d /= np.linalg.norm(d, axis=1, keepdims=True)
     # axis-aligned and grazing rays exercise the parallel-slab branch
     d[:50] = [[-1, 0, 0]] * 50
     o[:50, 1:] = rng.uniform(-0.6, 0.6, (50, 2))
+    return o, d
+
+
+@pytest.mark.parametrize("res,band,radius,n", [(32, 32, 0.3, 3000), (64, 3, 0.3, 3000),
+                                               (256, 3, 0.25, 20000), (512, 2, 0.3, 20000)])
+def test_march_bit_exact(ctx, res, band, radius, n):
+    """march_ray t-lists bit for bit, including the empty-space jumps of the
+    tile distance field (tile_dist, psdf_device.cuh Marcher)."""
+    g, a = make_scene(res=res, band=band, radius=radius)
+    og, sm = oracle_with_f32_smooth(a)
+    _upload(ctx, g, sm)
+    o, d = _march_rays(n, 11)
     got = ctx.march_rays(o, d, 512)
     for i in range(len(o)):
         want = og.march_ray(o[i], d[i], 512)
@@ -70,10 +80,31 @@ def test_march_bit_exact(ctx, res, band):
         assert np.array_equal(got[i], og.march_ray(o[i], d[i], 7))
 
 
+@pytest.mark.parametrize("margin", ["0.02", "0.45"])
+def test_march_exact_paths(ctx, monkeypatch, margin):
+    """A widened decision margin sends most tile / skip decisions (and every
+    decision after an empty-space jump near a face) down the exact and rewind
+    paths; the t-lists must not change by a bit."""
+    g, a = make_scene(res=256, band=3, radius=0.25)
+    og, sm = oracle_with_f32_smooth(a)
+    _upload(ctx, g, sm)
+    o, d = _march_rays(6000, 12)
+    # rays along tile faces / through tile edges (lattice-aligned decisions)
+    h = 1.0 / 256
+    o[400:600] = [[-1.3, -0.5 + 16 * h * k, -0.5 + 16 * h * (k % 7)] for k in range(200)]
+    d[400:600] = [[1.0, 0.0, 0.0]] * 200
+    monkeypatch.setenv("PSDF_TEST_MARGIN", margin)
+    got = ctx.march_rays(o, d, 512)
+    for i in range(len(o)):
+        want = og.march_ray(o[i], d[i], 512)
+        assert got[i].shape == want.shape and np.array_equal(got[i], want), i
+
+
 SCENES = [
     dict(res=32, n_s=2, n_a=2, sh_order=2, band=32),
     dict(res=64, n_s=4, n_a=4, sh_order=4, band=6),
     dict(res=32, n_s=8, n_a=8, sh_order=3, band=32),
+    dict(res=256, n_s=4, n_a=4, sh_order=4, band=3),  # empty-space jumps
 ]
 
 
@@ -100,7 +131,7 @@ def test_render_parity(ctx, scene, tau_vox):
 
 
 @pytest.mark.parametrize("flag", ["no_spatial", "no_angular", "no_fresnel", "sh_order_override",
-                                  "background", "no_early_stop", "alpha_only"])
+                                  "background", "no_early_stop", "early_stop_above_one", "alpha_only"])
 def test_render_options(ctx, flag):
     from paper_2412_10084_b200 import api
     g, a = make_scene(res=32, n_s=4, n_a=4, sh_order=4, band=32)
@@ -114,6 +145,8 @@ def test_render_options(ctx, flag):
         kw[flag] = (0.25, 0.5, 0.75)
     elif flag == "no_early_stop":
         kw["early_stop_transmittance"] = 0.0
+    elif flag == "early_stop_above_one":  # stops after the first settled sample
+        kw["early_stop_transmittance"] = 1.5
     elif flag == "alpha_only":
         kw["need_colors"] = False
     else:

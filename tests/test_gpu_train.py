@@ -44,6 +44,9 @@ CASES = [
     dict(scene=dict(res=32, n_s=2, n_a=2, sh_order=2, band=32), tau=30.0, size=24, ncam=4, bias=True),
     dict(scene=dict(res=64, n_s=4, n_a=4, sh_order=4, band=6), tau=30.0, size=32, ncam=0, bias=False),
     dict(scene=dict(res=64, n_s=4, n_a=4, sh_order=3, band=6), tau=300.0, size=32, ncam=0, bias=False),
+    # 16^3 tiles, thin band: rays cross long empty stretches (marcher jumps)
+    dict(scene=dict(res=256, n_s=4, n_a=4, sh_order=4, band=3, radius=0.25), tau=300.0, size=40, ncam=0,
+         bias=False),
 ]
 
 
