@@ -256,11 +256,11 @@ __device__ __forceinline__ void block_add_f64v(double* const* dst, double* v, do
     __syncthreads();
     if (l == 0)
 #pragma unroll
-        for (int k = 0; k < NV; ++k) red[k * 32 + w] = v[k];
+        for (int k = 0; k < NV; ++k) red[k * nw + w] = v[k];
     __syncthreads();
     if (threadIdx.x < NV) {
         double s = 0.0;
-        for (int i = 0; i < nw; ++i) s += red[threadIdx.x * 32 + i];
+        for (int i = 0; i < nw; ++i) s += red[threadIdx.x * nw + i];
         if (s != 0.0) atomicAdd(dst[threadIdx.x], s);
     }
 }
@@ -271,37 +271,58 @@ __device__ __forceinline__ void block_add_f64(double* dst, double v, double* red
     block_add_f64v<1>(d, vv, red);
 }
 
+// (x, y, z) of a flat index over an E^3 cube, advanced by a constant stride
+// without divisions.
+template <int E, int S>
+struct Walk3 {
+    static constexpr int SX = S / (E * E), SY = (S / E) % E, SZ = S % E;
+    int x, y, z;
+    __device__ __forceinline__ explicit Walk3(int i) : x(i / (E * E)), y((i / E) % E), z(i % E) {}
+    __device__ __forceinline__ void step() {
+        z += SZ;
+        if (z >= E) {
+            z -= E;
+            ++y;
+        }
+        y += SY;
+        if (y >= E) {
+            y -= E;
+            ++x;
+        }
+        x += SX;
+    }
+};
+
 // K3 + K4: loss_sdf, loss_eikonal and loss_normal (losses.cpp:121-220) of tile
 // t0 + blockIdx.x in one pass over its 20^3 smoothed halo (TileHalo,
 // losses.cpp:61-117).
 //
 // Atomic-free gather form of the TileHalo stencil scatter: every term
 // deposits a vector dg at a centre w and the stencil adds +-dg_b * inv2h at
-// w -+ e_b.  Phase A stores the central-difference gradient at every centre
-// of the tile plus its +1 shell ([2,18]^3 in halo coordinates); phase B sums,
-// per centre, the vectors of all terms centred there (the eikonal term of w,
-// dg1 of the normal pairs (w, w+e_a), dg2 of the pairs (w-e_a, w)) into
-// registers, which then overwrite the gradients; phase C gathers the stencil
-// at every allocated cell it reaches, adds the sdf term on the tile's own
-// voxels and flushes with global atomics (neighbour tiles' blocks reach the
-// same cells).
+// w -+ e_b.  Phase A stores the central-difference gradient and its inverse
+// length at every centre of the tile plus its +1 shell ([2,18]^3 in halo
+// coordinates); phase B sums, per centre, the vectors of all terms centred
+// there (the eikonal term of w, dg1 of the normal pairs (w, w+e_a), dg2 of the
+// pairs (w-e_a, w)) into registers, which then overwrite the gradients; the
+// sdf term of the tile's own voxels replaces their smoothed values; phase C
+// gathers the stencil at every allocated cell it reaches and flushes with
+// global atomics (neighbour tiles' blocks reach the same cells).
 constexpr int DE = 17;                 // centres [2, 18] in halo coordinates
 constexpr int DN = DE * DE * DE;       // 4913
 constexpr int LG_THREADS = 512;
 constexpr int LG_PER = (DN + LG_THREADS - 1) / LG_THREADS;  // centres per thread
-constexpr size_t kLossGridSmem = sizeof(float) * (HV + 3 * DN + TV) + sizeof(uint32_t) * (HV / 32);
+constexpr size_t kLossGridSmem = sizeof(float) * (HV + 4 * DN) + sizeof(uint32_t) * (HV / 32);
 __global__ void __launch_bounds__(LG_THREADS, 2) loss_grid_kernel(GridView g, const float* __restrict__ raw,
                                                                  int t0, float l_sdf, float l_eik,
                                                                  float l_norm, float inv2h,
                                                                  float* __restrict__ g_smooth,
                                                                  float* __restrict__ g_raw, double* stats) {
     extern __shared__ __align__(16) float sh[];
-    float* val = sh;                  // [20^3] smoothed values (far field outside)
-    float* P = sh + HV;               // [17^3][3] gradients, then stencil vectors D
-    float* W = P + 3 * DN;            // [16^3] proximity weights (losses.hpp:20)
-    uint32_t* alloc = reinterpret_cast<uint32_t*>(W + TV);  // [20^3] bits
+    float* val = sh;                                    // [20^3] smoothed values (far field outside)
+    float4* P = reinterpret_cast<float4*>(sh + HV);     // [17^3] (gradient, 1/|gradient|), then D
+    uint32_t* alloc = reinterpret_cast<uint32_t*>(sh + HV + 4 * DN);  // [20^3] bits
     __shared__ int nb[27];
-    __shared__ double red[6 * 32];
+    __shared__ double red[6 * (LG_THREADS / 32)];
     const int t = t0 + blockIdx.x;
     stage_nbr(g, t, nb);
     __syncthreads();
@@ -310,137 +331,155 @@ __global__ void __launch_bounds__(LG_THREADS, 2) loss_grid_kernel(GridView g, co
     auto in_tile = [](int x, int y, int z) {
         return x >= 2 && x < 18 && y >= 2 && y < 18 && z >= 2 && z < 18;
     };
+    auto weight = [&](int x, int y, int z) {  // proximity_weight (losses.hpp:20)
+        return __frcp_rn(1.f + fabsf(val[hidx(x, y, z)]) * 5.f);
+    };
     // phase A
-    for (int i = threadIdx.x; i < DN; i += LG_THREADS) {
-        const int x = i / (DE * DE) + 2, y = (i / DE) % DE + 2, z = i % DE + 2;
-        P[3 * i] = (val[hidx(x + 1, y, z)] - val[hidx(x - 1, y, z)]) * inv2h;
-        P[3 * i + 1] = (val[hidx(x, y + 1, z)] - val[hidx(x, y - 1, z)]) * inv2h;
-        P[3 * i + 2] = (val[hidx(x, y, z + 1)] - val[hidx(x, y, z - 1)]) * inv2h;
-    }
-    for (int j = threadIdx.x; j < TV; j += LG_THREADS) {
-        const int x = (j >> 8) + 2, y = ((j >> 4) & 15) + 2, z = (j & 15) + 2;
-        W[j] = 1.f / (1.f + fabsf(val[hidx(x, y, z)]) * 5.f);
+    {
+        Walk3<DE, LG_THREADS> c(threadIdx.x);
+        for (int i = threadIdx.x; i < DN; i += LG_THREADS, c.step()) {
+            const int x = c.x + 2, y = c.y + 2, z = c.z + 2;
+            const float gx = (val[hidx(x + 1, y, z)] - val[hidx(x - 1, y, z)]) * inv2h;
+            const float gy = (val[hidx(x, y + 1, z)] - val[hidx(x, y - 1, z)]) * inv2h;
+            const float gz = (val[hidx(x, y, z + 1)] - val[hidx(x, y, z - 1)]) * inv2h;
+            const float q = gx * gx + gy * gy + gz * gz;
+            P[i] = make_float4(gx, gy, gz, q > 0.f ? rsqrtf(q) : 0.f);
+        }
     }
     __syncthreads();
     // phase B
     double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // sdf pl/wt, eik pl/wt, normal pl/wt
     float D[LG_PER][3];
     constexpr int SX = DE * DE, SY = DE;
+    {
+        Walk3<DE, LG_THREADS> c(threadIdx.x);
 #pragma unroll
-    for (int k = 0; k < LG_PER; ++k) {
-        const int i = threadIdx.x + k * LG_THREADS;
-        float dx = 0.f, dy = 0.f, dz = 0.f;
-        if (i < DN) {
-            const int x = i / (DE * DE) + 2, y = (i / DE) % DE + 2, z = i % DE + 2;
-            const float gx = P[3 * i], gy = P[3 * i + 1], gz = P[3 * i + 2];
-            const float len = sqrtf(gx * gx + gy * gy + gz * gz);
-            const float inv = 1.f / len;
-            if (in_tile(x, y, z)) {
-                const float w = W[((x - 2) * 16 + (y - 2)) * 16 + (z - 2)];
-                const float e = len - 1.f;
-                acc[2] += (double)(l_eik * e * e);
-                acc[3] += (double)(l_eik * w * e * e);
-                if (len > 1e-12f) {
-                    const float c = 2.f * l_eik * w * e * inv;
-                    dx += c * gx;
-                    dy += c * gy;
-                    dz += c * gz;
+        for (int k = 0; k < LG_PER; ++k, c.step()) {
+            const int i = threadIdx.x + k * LG_THREADS;
+            float dx = 0.f, dy = 0.f, dz = 0.f;
+            if (i < DN) {
+                const int x = c.x + 2, y = c.y + 2, z = c.z + 2;
+                const float4 pc = P[i];
+                const float q = pc.x * pc.x + pc.y * pc.y + pc.z * pc.z;
+                const float inv = pc.w;
+                const float len = q * inv;  // |g|
+                if (in_tile(x, y, z)) {
+                    const float w = weight(x, y, z);
+                    const float e = len - 1.f;
+                    acc[2] += (double)(l_eik * e * e);
+                    acc[3] += (double)(l_eik * w * e * e);
+                    if (q > 1e-24f) {  // len > 1e-12
+                        const float cc = 2.f * l_eik * w * e * inv;
+                        dx += cc * pc.x;
+                        dy += cc * pc.y;
+                        dz += cc * pc.z;
+                    }
+                    if (q >= 1e-16f) {  // len >= 1e-8: pairs (w, w + e_a), the dg1 side and the loss
+                        const float n1x = pc.x * inv, n1y = pc.y * inv, n1z = pc.z * inv;
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) {
+                            const int nx = x + (a == 0), ny = y + (a == 1), nz = z + (a == 2);
+                            if (!bit_at(alloc, hidx(nx, ny, nz))) continue;
+                            const float4 ph = P[i + (a == 0 ? SX : a == 1 ? SY : 1)];
+                            if (ph.x * ph.x + ph.y * ph.y + ph.z * ph.z < 1e-16f) continue;
+                            const float ddx = ph.x * ph.w - n1x, ddy = ph.y * ph.w - n1y, ddz = ph.z * ph.w - n1z;
+                            const float vv = ddx * ddx + ddy * ddy + ddz * ddz;
+                            acc[4] += (double)(l_norm * vv);
+                            acc[5] += (double)(l_norm * w * vv);
+                            const float cn = 2.f * l_norm * w;
+                            // dn1 = -c d ; dg1 = (dn1 - n1 (dn1 . n1)) / l1
+                            const float m1x = -cn * ddx, m1y = -cn * ddy, m1z = -cn * ddz;
+                            const float p1 = m1x * n1x + m1y * n1y + m1z * n1z;
+                            dx += (m1x - n1x * p1) * inv;
+                            dy += (m1y - n1y * p1) * inv;
+                            dz += (m1z - n1z * p1) * inv;
+                        }
+                    }
                 }
-                if (len >= 1e-8f) {  // pairs (w, w + e_a): the dg1 side, and the loss
-                    const float n1x = gx * inv, n1y = gy * inv, n1z = gz * inv;
+                // pairs (w - e_a, w) with w - e_a in the tile: the dg2 side
+                if (q >= 1e-16f && bit_at(alloc, hidx(x, y, z))) {
+                    const float n2x = pc.x * inv, n2y = pc.y * inv, n2z = pc.z * inv;
 #pragma unroll
                     for (int a = 0; a < 3; ++a) {
-                        const int nx = x + (a == 0), ny = y + (a == 1), nz = z + (a == 2);
-                        if (!bit_at(alloc, hidx(nx, ny, nz))) continue;
-                        const int j = i + (a == 0 ? SX : a == 1 ? SY : 1);
-                        const float hx = P[3 * j], hy = P[3 * j + 1], hz = P[3 * j + 2];
-                        const float l2 = sqrtf(hx * hx + hy * hy + hz * hz);
-                        if (l2 < 1e-8f) continue;
-                        const float i2 = 1.f / l2;
-                        const float ddx = hx * i2 - n1x, ddy = hy * i2 - n1y, ddz = hz * i2 - n1z;
-                        const float vv = ddx * ddx + ddy * ddy + ddz * ddz;
-                        acc[4] += (double)(l_norm * vv);
-                        acc[5] += (double)(l_norm * w * vv);
-                        const float c = 2.f * l_norm * w;
-                        // dn1 = -c d ; dg1 = (dn1 - n1 (dn1 . n1)) / l1
-                        const float m1x = -c * ddx, m1y = -c * ddy, m1z = -c * ddz;
-                        const float p1 = m1x * n1x + m1y * n1y + m1z * n1z;
-                        dx += (m1x - n1x * p1) * inv;
-                        dy += (m1y - n1y * p1) * inv;
-                        dz += (m1z - n1z * p1) * inv;
+                        const int px = x - (a == 0), py = y - (a == 1), pz = z - (a == 2);
+                        if (!in_tile(px, py, pz)) continue;
+                        const float4 ph = P[i - (a == 0 ? SX : a == 1 ? SY : 1)];
+                        if (ph.x * ph.x + ph.y * ph.y + ph.z * ph.z < 1e-16f) continue;
+                        const float cn = 2.f * l_norm * weight(px, py, pz);
+                        const float m2x = cn * (n2x - ph.x * ph.w), m2y = cn * (n2y - ph.y * ph.w),
+                                    m2z = cn * (n2z - ph.z * ph.w);
+                        const float p2 = m2x * n2x + m2y * n2y + m2z * n2z;
+                        dx += (m2x - n2x * p2) * inv;
+                        dy += (m2y - n2y * p2) * inv;
+                        dz += (m2z - n2z * p2) * inv;
                     }
                 }
             }
-            // pairs (w - e_a, w) with w - e_a in the tile: the dg2 side
-            if (len >= 1e-8f && bit_at(alloc, hidx(x, y, z))) {
-                const float n2x = gx * inv, n2y = gy * inv, n2z = gz * inv;
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    const int px = x - (a == 0), py = y - (a == 1), pz = z - (a == 2);
-                    if (!in_tile(px, py, pz)) continue;
-                    const int j = i - (a == 0 ? SX : a == 1 ? SY : 1);
-                    const float hx = P[3 * j], hy = P[3 * j + 1], hz = P[3 * j + 2];
-                    const float l1 = sqrtf(hx * hx + hy * hy + hz * hz);
-                    if (l1 < 1e-8f) continue;
-                    const float i1 = 1.f / l1;
-                    const float w = W[((px - 2) * 16 + (py - 2)) * 16 + (pz - 2)];
-                    const float c = 2.f * l_norm * w;
-                    const float m2x = c * (n2x - hx * i1), m2y = c * (n2y - hy * i1),
-                                m2z = c * (n2z - hz * i1);
-                    const float p2 = m2x * n2x + m2y * n2y + m2z * n2z;
-                    dx += (m2x - n2x * p2) * inv;
-                    dy += (m2y - n2y * p2) * inv;
-                    dz += (m2z - n2z * p2) * inv;
-                }
-            }
+            D[k][0] = dx;
+            D[k][1] = dy;
+            D[k][2] = dz;
         }
-        D[k][0] = dx;
-        D[k][1] = dy;
-        D[k][2] = dz;
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < LG_PER; ++k) {
         const int i = threadIdx.x + k * LG_THREADS;
-        if (i < DN) {
-            P[3 * i] = D[k][0];
-            P[3 * i + 1] = D[k][1];
-            P[3 * i + 2] = D[k][2];
+        if (i < DN) P[i] = make_float4(D[k][0], D[k][1], D[k][2], 0.f);
+    }
+    // loss_sdf (losses.cpp:121-142) on the tile's own voxels, vectorised; the
+    // smooth-side gradient replaces the voxel's smoothed value in val
+    {
+        const float4* r4 = reinterpret_cast<const float4*>(raw + (int64_t)t * TV);
+        float4* g4 = reinterpret_cast<float4*>(g_raw + (int64_t)t * TV);
+        for (int j = threadIdx.x; j < TV / 4; j += LG_THREADS) {
+            const float4 r = __ldg(r4 + j);
+            float4 gr = g4[j];
+            const int x = (j >> 6) + 2, y = ((j >> 2) & 15) + 2, z0 = ((j & 3) << 2) + 2;
+            const float* ra = &r.x;
+            float* ga = &gr.x;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                float& cell = val[hidx(x, y, z0 + k)];
+                const float sv = cell;
+                const float d = sv - ra[k];
+                const float as = fabsf(sv), ar = fabsf(ra[k]);
+                const float w = __frcp_rn((as > ar ? as : ar) + (float)kPhotoEps) * __frcp_rn(1.f + as * 5.f);
+                acc[0] += (double)(l_sdf * d * d);
+                acc[1] += (double)(l_sdf * w * d * d);
+                const float gg = 2.f * l_sdf * w * d;
+                ga[k] -= gg;
+                cell = gg;
+            }
+            g4[j] = gr;
         }
     }
     __syncthreads();
     // phase C: cells [1, 19]^3 (everything the stencils reach)
-    auto dv = [&](int x, int y, int z, int b) -> float {
-        if (x < 2 || x > 18 || y < 2 || y > 18 || z < 2 || z > 18) return 0.f;
-        return P[3 * (((x - 2) * DE + (y - 2)) * DE + (z - 2)) + b];
+    auto dv = [&](int x, int y, int z) -> const float4* {
+        if (x < 2 || x > 18 || y < 2 || y > 18 || z < 2 || z > 18) return nullptr;
+        return P + (((x - 2) * DE + (y - 2)) * DE + (z - 2));
     };
     constexpr int CE = 19;
-    const float* rt = raw + (int64_t)t * TV;
-    float* grt = g_raw + (int64_t)t * TV;
-    for (int i = threadIdx.x; i < CE * CE * CE; i += LG_THREADS) {
-        const int x = i / (CE * CE) + 1, y = (i / CE) % CE + 1, z = i % CE + 1;
-        if (!bit_at(alloc, hidx(x, y, z))) continue;
-        float gv = (dv(x - 1, y, z, 0) - dv(x + 1, y, z, 0) + dv(x, y - 1, z, 1) - dv(x, y + 1, z, 1) +
-                    dv(x, y, z - 1, 2) - dv(x, y, z + 1, 2)) *
-                   inv2h;
-        const int lx = x - 2, ly = y - 2, lz = z - 2;
-        if (in_tile(x, y, z)) {  // loss_sdf (losses.cpp:121-142) on the tile's own voxels
-            const int v = vox_index(lx, ly, lz);
-            const float sv = val[hidx(x, y, z)], r = __ldg(rt + v);
-            const float d = sv - r;
-            const float as = fabsf(sv), ar = fabsf(r);
-            const float w = (1.f / ((as > ar ? as : ar) + (float)kPhotoEps)) * (1.f / (1.f + as * 5.f));
-            acc[0] += (double)(l_sdf * d * d);
-            acc[1] += (double)(l_sdf * w * d * d);
-            const float gg = 2.f * l_sdf * w * d;
-            if (gg != 0.f) {
-                gv += gg;
-                grt[v] -= gg;
-            }
+    {
+        Walk3<CE, LG_THREADS> c(threadIdx.x);
+        for (int i = threadIdx.x; i < CE * CE * CE; i += LG_THREADS, c.step()) {
+            const int x = c.x + 1, y = c.y + 1, z = c.z + 1;
+            if (!bit_at(alloc, hidx(x, y, z))) continue;
+            float s = 0.f;
+            const float4* p;
+            if ((p = dv(x - 1, y, z))) s += p->x;
+            if ((p = dv(x + 1, y, z))) s -= p->x;
+            if ((p = dv(x, y - 1, z))) s += p->y;
+            if ((p = dv(x, y + 1, z))) s -= p->y;
+            if ((p = dv(x, y, z - 1))) s += p->z;
+            if ((p = dv(x, y, z + 1))) s -= p->z;
+            float gv = s * inv2h;
+            if (in_tile(x, y, z)) gv += val[hidx(x, y, z)];
+            if (gv == 0.f) continue;
+            const int lx = x - 2, ly = y - 2, lz = z - 2;
+            const int n = nb[((lx >> 4) + 1) * 9 + ((ly >> 4) + 1) * 3 + (lz >> 4) + 1];
+            atomicAdd(g_smooth + (int64_t)n * TV + vox_index(lx & 15, ly & 15, lz & 15), gv);
         }
-        if (gv == 0.f) continue;
-        const int n = nb[((lx >> 4) + 1) * 9 + ((ly >> 4) + 1) * 3 + (lz >> 4) + 1];
-        atomicAdd(g_smooth + (int64_t)n * TV + vox_index(lx & 15, ly & 15, lz & 15), gv);
     }
     double* dst[6] = {stats + 3, stats + 8, stats + 4, stats + 9, stats + 5, stats + 10};
     block_add_f64v<6>(dst, acc, red);
