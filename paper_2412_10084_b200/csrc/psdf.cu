@@ -164,6 +164,7 @@ struct psdf_ctx {
     float* d_tile_min = nullptr;   // [T] minimum of each tile's apron brick
     float* d_block_min = nullptr;  // [T][64] minimum of each 4^3 block's brick
     int32_t* d_tile_nbr = nullptr; // [T][27] neighbour tile ids
+    uint8_t* d_sat_dist = nullptr; // [T][64] saturation distances of the current ray pass
     int bit_words = 0;
     int4* d_tile_coords = nullptr;
     int32_t* d_probe_ids = nullptr;
@@ -234,6 +235,7 @@ struct psdf_ctx {
         g.tile_min = d_tile_min;
         g.block_min = d_block_min;
         g.tile_nbr = d_tile_nbr;
+        g.sat_dist = d_sat_dist;
         // decision margin of the marcher's fast paths; PSDF_TEST_MARGIN widens
         // it so the tests drive the exact / rewind paths on most decisions
         g.margin = 1e-8;
@@ -249,7 +251,7 @@ struct psdf_ctx {
     }
 
     void free_grid() {
-        for (void* p : {(void*)d_tile_table, (void*)d_tile_bits, (void*)d_tile_dist, (void*)d_tile_min, (void*)d_block_min, (void*)d_tile_nbr, (void*)d_tile_coords, (void*)d_probe_ids,
+        for (void* p : {(void*)d_tile_table, (void*)d_tile_bits, (void*)d_tile_dist, (void*)d_tile_min, (void*)d_block_min, (void*)d_tile_nbr, (void*)d_sat_dist, (void*)d_tile_coords, (void*)d_probe_ids,
                         (void*)d_probe_table, (void*)d_probe_coords, (void*)d_params,
                         (void*)d_smooth, (void*)d_smooth_ap, (void*)d_grads, (void*)d_gsmooth, (void*)d_grads0,
                         (void*)d_gsmooth0, (void*)d_m, (void*)d_v})
@@ -260,6 +262,7 @@ struct psdf_ctx {
         d_tile_min = nullptr;
         d_block_min = nullptr;
         d_tile_nbr = nullptr;
+        d_sat_dist = nullptr;
         d_tile_coords = nullptr;
         d_probe_ids = nullptr;
         d_probe_table = nullptr;
@@ -377,6 +380,15 @@ void smooth_all(psdf_ctx* c) {
     ++c->last_launches;
 }
 
+// Saturation distances for a ray pass with this tau (the marcher's runs);
+// with runs disabled (tau_run <= 0) every block reads as unsaturated.
+void prepare_sat(psdf_ctx* c, double tau_run) {
+    if (c->desc.T == 0) return;
+    sat_dist_kernel<<<c->desc.T, 64, 0, c->stream>>>(c->view(), tau_run, c->d_sat_dist);
+    CK(cudaGetLastError());
+    ++c->last_launches;
+}
+
 // K1 launch (render).
 template <int NS, int NA>
 void launch_render(psdf_ctx* c, RayPassParams& P) {
@@ -401,7 +413,9 @@ void free_wave(psdf_ctx* c) {
     for (void* p : {(void*)W.e_slot, (void*)W.e_dir, (void*)W.e_tfirst, (void*)W.e_cfirst,
                     (void*)W.e_nlive, (void*)W.e_acc, (void*)W.e_head, (void*)W.e_craw,
                     (void*)W.r_pos, (void*)W.r_w, (void*)W.r_tile, (void*)W.r_entry,
-                    (void*)W.r_next, (void*)W.r_c, (void*)W.r_up, (void*)W.r_geo})
+                    (void*)W.r_next, (void*)W.r_c, (void*)W.r_up, (void*)W.r_geo, (void*)W.h_slot,
+                    (void*)W.h_count, (void*)W.h_tileprev, (void*)W.h_t, (void*)W.h_tprev, (void*)W.h_dir,
+                    (void*)W.h_t1})
         if (p) cudaFree(p);
     unsigned* keep = W.counters;
     W = WaveBufs{};
@@ -409,12 +423,13 @@ void free_wave(psdf_ctx* c) {
 }
 
 // Grows the ray-entry / shading-record buffers (kept across steps).
-void ensure_wave(psdf_ctx* c, int64_t e_cap, int64_t r_cap) {
+void ensure_wave(psdf_ctx* c, int64_t e_cap, int64_t r_cap, int64_t h_cap) {
     WaveBufs& W = c->wave;
-    if (e_cap <= W.e_cap && r_cap <= W.r_cap) return;
+    if (e_cap <= W.e_cap && r_cap <= W.r_cap && h_cap <= W.h_cap) return;
     e_cap = std::max<int64_t>(e_cap, W.e_cap);
     r_cap = std::max<int64_t>(r_cap, W.r_cap);
-    if (e_cap > INT32_MAX / 4 || r_cap > INT32_MAX / 4)
+    h_cap = std::max<int64_t>(h_cap, W.h_cap);
+    if (e_cap > INT32_MAX / 4 || r_cap > INT32_MAX / 4 || h_cap > INT32_MAX / 4)
         fail(PSDF_ERR_RUNTIME, "ray pass needs more than 2^29 entries / records");
     CK(cudaStreamSynchronize(c->stream));
     free_wave(c);
@@ -435,8 +450,16 @@ void ensure_wave(psdf_ctx* c, int64_t e_cap, int64_t r_cap) {
     CK(cudaMalloc(&W.r_up, sizeof(float4) * r_cap));
     // geometry records sized for the widest supported channel configuration
     CK(cudaMalloc(&W.r_geo, sizeof(float) * (size_t)GeoRec<8, 8>::STRIDE * r_cap));
+    CK(cudaMalloc(&W.h_slot, sizeof(int) * h_cap));
+    CK(cudaMalloc(&W.h_count, sizeof(int) * h_cap));
+    CK(cudaMalloc(&W.h_tileprev, sizeof(int) * h_cap));
+    CK(cudaMalloc(&W.h_t, sizeof(double) * h_cap));
+    CK(cudaMalloc(&W.h_tprev, sizeof(double) * h_cap));
+    CK(cudaMalloc(&W.h_dir, sizeof(double) * 3 * h_cap));
+    CK(cudaMalloc(&W.h_t1, sizeof(double) * h_cap));
     W.e_cap = (int)e_cap;
     W.r_cap = (int)r_cap;
+    W.h_cap = (int)h_cap;
 }
 
 // K2 as the wavefront pipeline K2a -> K2b -> K2d -> K2e (psdf_train.cuh).
@@ -444,33 +467,39 @@ template <int NS, int NA>
 void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     cudaStream_t s = c->stream;
     const int64_t n_work = P.tile_end - P.tile_begin;
-    if (c->wave.e_cap == 0) ensure_wave(c, n_rays / 8 + 65536, n_rays / 8 + 65536);
+    if (c->wave.e_cap == 0) ensure_wave(c, n_rays / 8 + 65536, n_rays / 8 + 65536, n_rays / 2 + 65536);
     const size_t smem_f = render_smem_bytes<NS, NA>();
     const size_t smem_b = shade_bwd_smem_bytes<NS, NA>();
     CK(cudaFuncSetAttribute(shade_fwd_kernel<NS, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
     CK(cudaFuncSetAttribute(shade_bwd_kernel<NS, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
     const size_t smem_bits = sizeof(uint32_t) * P.bits_sm_words;
     CK(cudaFuncSetAttribute(march_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bits));
+    CK(cudaFuncSetAttribute(march_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bits));
     CK(cudaFuncSetAttribute(alpha_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bits));
+    const int per_sm_s = blocks_per_sm((const void*)march_scan_kernel, smem_bits);
+    const int64_t grid_s = std::max<int64_t>(1, std::min<int64_t>((n_work + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
+                                                                   (int64_t)per_sm_s * c->sm_count));
     const int per_sm_a = blocks_per_sm((const void*)march_fwd_kernel, smem_bits);
-    const int64_t grid_a = std::max<int64_t>(1, std::min<int64_t>((n_work + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
-                                                                   (int64_t)per_sm_a * c->sm_count));
+    const int64_t grid_a = (int64_t)per_sm_a * c->sm_count;
     CK(cudaEventRecord(c->ev_ray0, s));
     CK(cudaEventRecord(c->ev_k[0], s));
     for (int attempt = 0;; ++attempt) {
         CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
         CK(cudaMemsetAsync(c->wave.counters, 0, sizeof(unsigned) * 4, s));
         P.work_counter = c->d_work;
+        march_scan_kernel<<<(unsigned)grid_s, BLOCK, smem_bits, s>>>(P, c->wave);
+        CK(cudaGetLastError());
+        CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
         march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, c->wave);
         CK(cudaGetLastError());
-        ++c->last_launches;
-        CK(cudaMemcpyAsync(c->h_wave_counters, c->wave.counters, sizeof(unsigned) * 2,
+        c->last_launches += 2;
+        CK(cudaMemcpyAsync(c->h_wave_counters, c->wave.counters, sizeof(unsigned) * 3,
                            cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        const int64_t ne = c->h_wave_counters[0], nr = c->h_wave_counters[1];
-        if (ne <= c->wave.e_cap && nr <= c->wave.r_cap) break;
+        const int64_t ne = c->h_wave_counters[0], nr = c->h_wave_counters[1], nh = c->h_wave_counters[2];
+        if (ne <= c->wave.e_cap && nr <= c->wave.r_cap && nh <= c->wave.h_cap) break;
         if (attempt > 2) fail(PSDF_ERR_RUNTIME, "ray pass buffers failed to grow");
-        ensure_wave(c, ne + ne / 2 + 4096, nr + nr / 2 + 4096);
+        ensure_wave(c, ne + ne / 2 + 4096, nr + nr / 2 + 4096, nh + nh / 2 + 4096);
         // the failed sweep already accumulated statistics: clear and redo
         CK(cudaMemsetAsync(c->d_counts, 0, sizeof(unsigned long long) * 8, s));
         CK(cudaMemsetAsync(c->d_stats, 0, sizeof(double) * 16, s));
@@ -568,6 +597,7 @@ void do_render(psdf_ctx* c, const psdf_camera* cam, const psdf_render_opts* opt,
     P.out_alpha = d_alpha;
     P.out_depth = d_depth;
     CK(cudaMemsetAsync(c->d_counts, 0, sizeof(unsigned long long) * 8, c->stream));
+    prepare_sat(c, P.early_stop > 1.0 ? 0.0 : P.tau);
     dispatch_channels(c->desc.n_s, c->desc.n_a, [&]<int NS, int NA>() {
         launch_render<NS, NA>(c, P);
     });
@@ -630,6 +660,7 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
     P.g_planes = c->d_grads + c->off_planes;
     P.g_probes = c->d_grads + c->off_probes;
     P.g_mlp = c->d_grads + c->off_mlp;
+    prepare_sat(c, P.early_stop > 1.0 ? 0.0 : P.tau);
     dispatch_channels(c->desc.n_s, c->desc.n_a, [&]<int NS, int NA>() {
         launch_train_raypass<NS, NA>(c, P, n_rays);
     });
@@ -934,6 +965,7 @@ int psdf_upload_grid(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_c
         CK(cudaMalloc(&c->d_smooth_ap, sizeof(float) * std::max<int64_t>(T * AV, 4)));
         CK(cudaMalloc(&c->d_tile_min, sizeof(float) * std::max<int64_t>(T, 1)));
         CK(cudaMalloc(&c->d_block_min, sizeof(float) * std::max<int64_t>(64 * T, 1)));
+        CK(cudaMalloc(&c->d_sat_dist, std::max<int64_t>(64 * T, 1)));
         CK(cudaMalloc(&c->d_gsmooth, sizeof(float) * std::max<int64_t>(T * TV, 4)));
         CK(cudaMemsetAsync(c->d_params, 0, sizeof(float) * c->n_params, c->stream));
         CK(cudaMemsetAsync(c->d_grads, 0, sizeof(float) * c->n_params, c->stream));

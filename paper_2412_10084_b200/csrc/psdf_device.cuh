@@ -57,6 +57,7 @@ struct GridView {
     const float* __restrict__ smooth_ap;      // [T][18^3] smooth with a 1-voxel apron
     const float* __restrict__ tile_min;       // [T] min of each apron brick
     const float* __restrict__ block_min;      // [T][64] min over each 4^3 block's 6^3 brick
+    const uint8_t* __restrict__ sat_dist;     // [T][64] saturation distances of this pass (sat_dist_kernel)
     const float* __restrict__ planes;         // [T][3][256][n_s]
     const float* __restrict__ probes;         // [P][order^2][n_a]
 };
@@ -350,9 +351,10 @@ struct Marcher {
     double t_sync;        // < 0: synchronised with the reference; else its last t
     bool no_jump;         // replaying after a rewind
     unsigned n_exact;     // exact-path fallbacks taken (diagnostics)
+    int c_b, c_tile;      // last tile-grid cell looked up and its tile id
+    int c_blk, c_ds;      // last block (tile * 64 + block) and its saturation distance
 
-    __device__ __forceinline__ bool init(const GridView& g, const double* o_, const double* d_,
-                                         int nmax) {
+    __device__ __forceinline__ void setup(const GridView& g, const double* o_, const double* d_, int nmax) {
         const double inv_h = g.h_pow2 ? g.inv_h : 1.0 / g.h;
         double dm = 0.0;
 #pragma unroll
@@ -367,9 +369,16 @@ struct Marcher {
         dinv_max = dm > 0.0 ? 1.0 / dm : 0.0;
         t_sync = -1.0;
         no_jump = false;
+        c_b = c_blk = -1;
+        c_tile = c_ds = 0;
         n_max = nmax;
         count = 0;
         n_exact = 0;
+    }
+
+    __device__ __forceinline__ bool init(const GridView& g, const double* o_, const double* d_,
+                                         int nmax) {
+        setup(g, o_, d_, nmax);
         const BoxHit b = ray_box(d3(o[0], o[1], o[2]), d3(d[0], d[1], d[2]),
                                  d3(g.org[0], g.org[1], g.org[2]), d3(g.wmax[0], g.wmax[1], g.wmax[2]));
         PSDF_STAT(0);
@@ -382,6 +391,15 @@ struct Marcher {
         t1 = b.t1;
         t = dadd(b.t0, dmul(0.5, g.h));
         return true;
+    }
+
+    // Resumes a ray whose box exit t1 is known (the caller sets t and count
+    // to a point the reference visited).
+    __device__ __forceinline__ void init_from(const GridView& g, const double* o_, const double* d_,
+                                              int nmax, double t1_) {
+        setup(g, o_, d_, nmax);
+        t1 = t1_;
+        t = t1_;
     }
 
     // Rewinds to the reference's last visited point (after an ambiguous
@@ -482,37 +500,50 @@ struct Marcher {
                 // allocated tile)
                 PSDF_STAT(3);
                 t_out = t;
-                tile_out = tile_lookup(g, tc[0], tc[1], tc[2]);
+                if (b != c_b) {  // consecutive samples mostly share the tile
+                    c_b = b;
+                    c_tile = __ldg(g.tile_table + b);
+                }
+                tile_out = c_tile;
                 if (tc_out) *tc_out = make_int4(tc[0], tc[1], tc[2], 0);
                 if constexpr (RUNS) {
                     run.n = 1;
                     run.sat = false;
                     run.t_last = t;
                     if (!near && tau > 0.0) {
-                        const float mn = __ldg(g.tile_min + tile_out);
-                        if (mn > 0.0f && dmul(tau, (double)mn) >= kSatX) {
+                        // the 4^3 block holding the sample's voxel (p(t) off
+                        // the block faces by the margin) and its saturation
+                        // distance: every lattice point within L-inf
+                        // 4 (Ds - 1) + (distance to the block faces) voxels,
+                        // up to the tile exit, lies in a saturated block
+                        int bi = 0;
+                        bool ok = true;
+                        double edge = 4.0;
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) {
+                            const double fb = floor(r[a] * 0.25);
+                            const double rb = r[a] - 4.0 * fb;
+                            ok &= rb > kMargin && rb < 4.0 - kMargin;
+                            edge = fmin(edge, fmin(rb, 4.0 - rb));
+                            bi = bi * 4 + (int)fb;
+                        }
+                        int ds = 0;
+                        if (ok) {
+                            const int blk = tile_out * 64 + bi;
+                            if (blk != c_blk) {
+                                c_blk = blk;
+                                c_ds = __ldg(g.sat_dist + blk);
+                            }
+                            ds = c_ds;
+                        }
+                        if (ds > 0) {
                             run.sat = true;
-                            const double n = run_length(g, v, t, h);
+                            double n = run_length(g, v, t, h);  // lattice points left in the tile
+                            if (ds < 4) n = fmin(n, floor((4.0 * (ds - 1) + edge - 1e-6) * dinv_max) + 1.0);
                             if (n > 1.0) {
                                 const int ni = (int)fmin(n, (double)(n_max - count));
                                 run.n = ni;
                                 if (ni > 1) run.t_last = lattice_advance(t, (double)(ni - 1), h);
-                            }
-                        } else {
-                            // single sample: the 4^3 block holding its voxel
-                            // (p(t) off the block faces by the margin)
-                            int bi = 0;
-                            bool ok = true;
-#pragma unroll
-                            for (int a = 0; a < 3; ++a) {
-                                const double fb = floor(r[a] * 0.25);
-                                const double rb = r[a] - 4.0 * fb;
-                                ok &= rb > kMargin && rb < 4.0 - kMargin;
-                                bi = bi * 4 + (int)fb;
-                            }
-                            if (ok) {
-                                const float bm = __ldg(g.block_min + (int64_t)tile_out * 64 + bi);
-                                run.sat = bm > 0.0f && dmul(tau, (double)bm) >= kSatX;
                             }
                         }
                     }

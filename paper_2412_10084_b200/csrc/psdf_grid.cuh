@@ -245,6 +245,30 @@ __global__ void __launch_bounds__(256) apron_fill_kernel(GridView g, const float
     if (threadIdx.x == 0) tmin[t] = fminf(red[0], red[1]);
 }
 
+// Saturation distances for one ray pass (its tau): per 4^3 block of each tile,
+// the L-inf distance, in blocks, to the nearest block of the same tile whose
+// brick can hold a sample with sigmoid < 1 (tau * block_min < kSatX);
+// 0 = that block itself, 4 = none in the tile.  The marcher's saturated runs
+// (psdf_device.cuh, Marcher::next_run) read it.
+__global__ void __launch_bounds__(64) sat_dist_kernel(GridView g, double tau, uint8_t* __restrict__ sd) {
+    __shared__ unsigned long long unsat;
+    const int t = blockIdx.x, b = threadIdx.x;
+    if (b == 0) unsat = 0ull;
+    __syncthreads();
+    const float bm = __ldg(g.block_min + (int64_t)t * 64 + b);
+    const bool sat = tau > 0.0 && bm > 0.0f && dmul(tau, (double)bm) >= kSatX;
+    if (!sat) atomicOr(&unsat, 1ull << b);
+    __syncthreads();
+    const int bx = b >> 4, by = (b >> 2) & 3, bz = b & 3;
+    int best = 4;
+    for (unsigned long long m = unsat; m; m &= m - 1) {
+        const int o = __ffsll((long long)m) - 1;
+        const int d = max(max(abs((o >> 4) - bx), abs(((o >> 2) & 3) - by)), abs((o & 3) - bz));
+        best = min(best, d);
+    }
+    sd[(int64_t)t * 64 + b] = (uint8_t)best;
+}
+
 // Block-wide sums of NV doubles, one atomic per value per block.
 template <int NV>
 __device__ __forceinline__ void block_add_f64v(double* const* dst, double* v, double* red) {

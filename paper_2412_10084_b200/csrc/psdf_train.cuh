@@ -57,8 +57,17 @@ struct WaveBufs {
     float* r_c;        // [cap][4] decoded colour (K2b)
     float* r_up;       // [cap][4] upstream w g (K2d)
     float* r_geo;      // [cap][GeoRec::STRIDE] geometry + features (K2b -> K2e)
-    unsigned* counters;  // [0] entries, [1] records
-    int e_cap, r_cap;
+    // handovers K2a-scan -> K2a: rays that reach a sample which can have
+    // sigmoid < 1 (or whose final settle can), with the scan's state there
+    int* h_slot;       // local work tile * 32 + lane
+    int* h_count;      // samples before it (all saturated)
+    int* h_tileprev;   // tile of the last of them
+    double* h_t;       // t of that sample (marcher t at exhaustion for a final settle)
+    double* h_tprev;   // t of the last saturated sample
+    double* h_dir;     // [cap][3]
+    double* h_t1;      // box exit
+    unsigned* counters;  // [0] entries, [1] records, [2] handovers
+    int e_cap, r_cap, h_cap;
 };
 
 // Warp-aggregated slot allocation inside divergent code.
@@ -125,8 +134,14 @@ __device__ __forceinline__ bool photo_term(const RayPassParams& P, bool in_mask,
     return dadd(dadd(dmul(g0, g0), dmul(g1, g1)), dmul(g2, g2)) > 0.0 || dA != 0.0;
 }
 
-// ------------------------------------------------------------------ K2a
-__global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPassParams P, WaveBufs W) {
+// ------------------------------------------------------------------ K2a-scan
+// The saturated prefix of every ray: march (jumps, skips, saturated runs)
+// until the first sample whose block can hold sigmoid < 1, with no SDF
+// evaluation.  Saturated samples settle with alpha exactly 0 and change
+// nothing but the counts, so a ray that never leaves them (or misses the
+// grid) is finished here — its loss is the empty-ray term — and the others
+// are handed over, compacted, to K2a with the state at that sample.
+__global__ void __launch_bounds__(BLOCK) march_scan_kernel(RayPassParams P, WaveBufs W) {
     extern __shared__ __align__(16) uint32_t sm_bits[];
     const int lane = threadIdx.x & 31;
     const GridView& g = P.g;
@@ -135,7 +150,8 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
     const double tau = P.tau;
     const double tau_run = P.early_stop > 1.0 ? 0.0 : tau;  // see render_kernel
     double st_photo = 0.0, st_sq = 0.0;
-    unsigned long long st_mask = 0, c_m = 0, c_x = 0, c_sh = 0, c_bwd = 0, c_ex = 0;
+    unsigned long long st_mask = 0;
+    unsigned c_m = 0, c_x = 0, c_bwd = 0, c_ex = 0;
     const int n_work = (int)(P.tile_end - P.tile_begin);
     for (;;) {
         int wi = 0;
@@ -143,16 +159,127 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
         wi = __shfl_sync(FULL, wi, 0);
         if (wi >= n_work) break;
         const LaneRay R = lane_ray(P, wi, lane);
-        const bool in_mask = R.valid && __ldg(R.V->mask + R.px) != 0;
-        const D3 dir = R.valid ? pixel_dir(R.V->cam, (double)R.u + 0.5, (double)R.v + 0.5) : d3(0, 0, 1);
-        const double dd[3] = {dir.x, dir.y, dir.z};
         Marcher mr;
-        double t_cur = 0.0, a_cur = 0.0, acc = 0.0, trans = 1.0;
+        int k = 0, tile_prev = -1;
+        double t_prev = 0.0, h_t = 0.0;
+        bool hand = false;
+        if (R.valid) {
+            const D3 dir = pixel_dir(R.V->cam, (double)R.u + 0.5, (double)R.v + 0.5);
+            const double dd[3] = {dir.x, dir.y, dir.z};
+            if (mr.init(g, R.V->cam.pos, dd, P.n_max)) {
+                for (;;) {
+                    double ts;
+                    int tile;
+                    int4 tc;
+                    SampleRun run;
+                    if (!mr.next_run(g, ts, tile, bits, &tc, tau_run, run)) {
+                        if (k > 0) {  // the final settle against the one-past-the-end point
+                            double pn[3];
+                            mr.pos(dadd(t_prev, g.h), pn);
+                            if (sigmoid_sat(dmul(tau, sample_sdf(g, pn[0], pn[1], pn[2]))) != 1.0) {
+                                hand = true;
+                                h_t = mr.t;
+                            }
+                        }
+                        break;
+                    }
+                    if (!run.sat) {
+                        hand = true;
+                        h_t = ts;
+                        break;
+                    }
+                    k += run.n;
+                    t_prev = run.t_last;
+                    tile_prev = tile;
+                }
+            }
+            c_ex += mr.n_exact;
+            if (k > 0) ++c_x;  // the ray's first sample (n_extra)
+        }
+        const int h = warp_alloc(W.counters + 2, hand, lane);
+        if (hand) {
+            if (h < W.h_cap) {
+                W.h_slot[h] = wi * 32 + lane;
+                W.h_count[h] = k;
+                W.h_tileprev[h] = tile_prev;
+                W.h_t[h] = h_t;
+                W.h_tprev[h] = t_prev;
+                W.h_dir[3 * (int64_t)h] = mr.d[0];
+                W.h_dir[3 * (int64_t)h + 1] = mr.d[1];
+                W.h_dir[3 * (int64_t)h + 2] = mr.d[2];
+                W.h_t1[h] = mr.t1;
+            }
+        } else if (R.valid) {
+            // every settle had alpha 0: acc = 0, nothing shaded, nothing to
+            // back-propagate; the loss is final now
+            c_m += k;
+            const bool in_mask = __ldg(R.V->mask + R.px) != 0;
+            const double col[3] = {P.bg[0], P.bg[1], P.bg[2]};
+            double g0, g1, g2, dA;
+            if (photo_term(P, in_mask, R.V->gt + 3 * R.px, col, 0.0, g0, g1, g2, dA, st_photo, st_sq,
+                           st_mask))
+                ++c_bwd;
+        }
+    }
+    st_photo = warp_sum_d(st_photo);
+    st_sq = warp_sum_d(st_sq);
+    st_mask = warp_sum_u(st_mask);
+    const unsigned long long m = warp_sum_u(c_m), x = warp_sum_u(c_x), bw = warp_sum_u(c_bwd),
+                             ex = warp_sum_u(c_ex);
+    if (lane == 0) {
+        atomicAdd(P.counts + 6, ex);
+        atomicAdd(P.stats + 0, st_photo);
+        atomicAdd(P.stats + 1, st_sq);
+        atomicAdd(P.stats + 2, (double)st_mask);
+        atomicAdd(P.counts + 1, m);
+        atomicAdd(P.counts + 2, x);
+        atomicAdd(P.counts + 5, bw);
+    }
+}
+
+// ------------------------------------------------------------------ K2a
+// The rest of each handed-over ray, one lane per handover (full warps):
+// sigmoid, alpha compositing, early termination, ray entries and shading
+// records.
+__global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPassParams P, WaveBufs W) {
+    extern __shared__ __align__(16) uint32_t sm_bits[];
+    const int n_hand = (int)min(*(volatile unsigned*)(W.counters + 2), (unsigned)W.h_cap);
+    const int lane = threadIdx.x & 31;
+    const GridView& g = P.g;
+    const uint32_t* bits = stage_tile_bits(g, sm_bits, P.bits_sm_words);
+    __syncthreads();
+    const double tau = P.tau;
+    const double tau_run = P.early_stop > 1.0 ? 0.0 : tau;  // see render_kernel
+    double st_photo = 0.0, st_sq = 0.0;
+    unsigned long long st_mask = 0, c_m = 0, c_x = 0, c_sh = 0, c_bwd = 0, c_ex = 0;
+    for (;;) {
+        int base = 0;
+        if (lane == 0) base = (int)atomicAdd(P.work_counter, 32ull);
+        base = __shfl_sync(FULL, base, 0);
+        if (base >= n_hand) break;
+        const int hi = base + lane;
+        const bool valid = hi < n_hand;
+        const int slot = valid ? W.h_slot[hi] : 0;
+        const LaneRay R = lane_ray(P, slot >> 5, slot & 31);
+        const bool in_mask = valid && __ldg(R.V->mask + R.px) != 0;
+        const double dd[3] = {valid ? W.h_dir[3 * (int64_t)hi] : 0.0, valid ? W.h_dir[3 * (int64_t)hi + 1] : 0.0,
+                              valid ? W.h_dir[3 * (int64_t)hi + 2] : 1.0};
+        Marcher mr;
+        double t_cur = 0.0, a_cur = 1.0, acc = 0.0, trans = 1.0;
         int tile_cur = -1, n_live = 0, entry = -1, prev = -1, head = -1;
         double t_first = 0.0;
         int cnt_first = -1;
         bool have_cur = false;
-        bool alive = R.valid && mr.init(g, R.V->cam.pos, dd, P.n_max);
+        bool alive = valid;
+        if (valid) {
+            mr.init_from(g, R.V->cam.pos, dd, P.n_max, W.h_t1[hi]);
+            mr.t = W.h_t[hi];
+            mr.count = W.h_count[hi];
+            have_cur = mr.count > 0;
+            n_live = have_cur ? mr.count - 1 : 0;  // settles among the saturated prefix
+            t_cur = W.h_tprev[hi];
+            tile_cur = W.h_tileprev[hi];
+        }
         // One sample per iteration, warp-synchronous so that the record
         // allocation below uses full-warp ballots (single call sites also
         // keep the loop small): fetch the next march sample (or the
@@ -254,12 +381,12 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
             }
         }
         c_m += n_live;
-        if (R.valid) c_ex += mr.n_exact;
+        if (valid) c_ex += mr.n_exact;
         if (entry >= 0) {
-            W.e_slot[entry] = wi * 32 + lane;
-            W.e_dir[3 * (int64_t)entry] = dir.x;
-            W.e_dir[3 * (int64_t)entry + 1] = dir.y;
-            W.e_dir[3 * (int64_t)entry + 2] = dir.z;
+            W.e_slot[entry] = slot;
+            W.e_dir[3 * (int64_t)entry] = dd[0];
+            W.e_dir[3 * (int64_t)entry + 1] = dd[1];
+            W.e_dir[3 * (int64_t)entry + 2] = dd[2];
             W.e_tfirst[entry] = t_first;
             W.e_cfirst[entry] = cnt_first;
             W.e_nlive[entry] = n_live;
@@ -268,7 +395,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
             W.e_craw[3 * (int64_t)entry] = 0.0;
             W.e_craw[3 * (int64_t)entry + 1] = 0.0;
             W.e_craw[3 * (int64_t)entry + 2] = 0.0;
-        } else if (R.valid && cnt_first < 0) {
+        } else if (valid && cnt_first < 0) {
             // no alpha > 0 sample: acc = 0, no shaded sample, nothing to
             // back-propagate; the loss is final now
             const double om = dsub(1.0, acc);
