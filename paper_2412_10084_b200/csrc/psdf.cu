@@ -517,7 +517,7 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
         const unsigned long long zero[12] = {};
         CK(cudaMemcpyToSymbol(g_march_stats, zero, sizeof zero));
         fprintf(stderr, "[psdf] march stats: rays %llu in-box %llu iters %llu samples %llu jumps %llu "
-                "skips %llu exact %llu rewinds %llu sat-runs %llu run-samples %llu - %llu\n", st[0], st[1], st[2], st[3], st[4], st[5], st[6], st[7], st[8], st[9], st[10]);
+                "skips %llu exact %llu rewinds %llu sat-runs %llu run-samples %llu | probe groups %llu members %llu\n", st[0], st[1], st[2], st[3], st[4], st[5], st[6], st[7], st[8], st[9], st[10], st[11]);
 #endif
     }
     c->last_entries = n_ent;

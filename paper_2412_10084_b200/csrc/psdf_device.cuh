@@ -774,4 +774,69 @@ __device__ __forceinline__ void scatter_smooth(const GridView& g, float* __restr
     }
 }
 
+// The six scatter_smooth_grad calls of the normal chain (renderer.cpp:216-235:
+// +-c_a at p +- h e_a) merged: the shifted points share p's trilinear
+// fractions (a shift by one voxel moves the base corner by one), so their
+// 48 corner deposits fall on 32 distinct voxels — the 2^3 core around p and
+// a 4-voxel arm at -1 and +2 along each axis.  Neighbour tiles come from
+// g.tile_nbr (every voxel is within 2 of the sample's voxel, which lies in
+// `tile`); unallocated / outside voxels are skipped like smooth_value.
+__device__ __forceinline__ void scatter_gradient_stencil(const GridView& g, float* __restrict__ gsm,
+                                                         int tile, const double p[3], double c0,
+                                                         double c1, double c2) {
+    const double cc[3] = {c0, c1, c2};
+    int b[3];
+    double f[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double x = dsub(w2v(g, p[a], a), 0.5);
+        b[a] = (int)floor(x);
+        f[a] = dsub(x, (double)b[a]);
+    }
+    auto wgt = [&](int ox, int oy, int oz) {
+        return (ox ? f[0] : 1.0 - f[0]) * (oy ? f[1] : 1.0 - f[1]) * (oz ? f[2] : 1.0 - f[2]);
+    };
+    const int4 tc = __ldg(g.tile_coords + tile);
+    const int32_t* nbr = g.tile_nbr + (int64_t)tile * 27;
+    auto deposit = [&](int dx, int dy, int dz, double v) {
+        if (v == 0.0) return;
+        const int vx = b[0] + dx, vy = b[1] + dy, vz = b[2] + dz;
+        const int n = __ldg(nbr + (((vx >> 4) - tc.x + 1) * 3 + ((vy >> 4) - tc.y + 1)) * 3 + ((vz >> 4) - tc.z + 1));
+        if (n < 0) return;
+        atomicAdd(gsm + (int64_t)n * TV + vox_index(vx & 15, vy & 15, vz & 15), (float)v);
+    };
+    // core: +c_a w(o - e_a) where o_a = 1, -c_a w(o + e_a) where o_a = 0
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int o[3] = {i & 1, (i >> 1) & 1, (i >> 2) & 1};
+        double v = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            int q[3] = {o[0], o[1], o[2]};
+            q[a] ^= 1;
+            v += (o[a] ? cc[a] : -cc[a]) * wgt(q[0], q[1], q[2]);
+        }
+        deposit(o[0], o[1], o[2], v);
+    }
+    // arms: +c_a w(o') at o' + e_a (o'_a = 1), -c_a w(o') at o' - e_a (o'_a = 0)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            int o[3];
+            o[a] = 1;
+            o[(a + 1) % 3] = i & 1;
+            o[(a + 2) % 3] = (i >> 1) & 1;
+            const double wp = wgt(o[0], o[1], o[2]);
+            int d[3] = {o[0], o[1], o[2]};
+            d[a] = 2;
+            deposit(d[0], d[1], d[2], cc[a] * wp);
+            o[a] = 0;
+            const double wn = wgt(o[0], o[1], o[2]);
+            d[a] = -1;
+            deposit(d[0], d[1], d[2], -cc[a] * wn);
+        }
+    }
+}
+
 }  // namespace psdf

@@ -920,6 +920,12 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
                 const int t0 = __shfl_sync(FULL, tile, __ffs(rem) - 1);
                 const unsigned grp = __ballot_sync(FULL, ((rem >> lane) & 1u) && tile == t0);
                 rem &= ~grp;
+#ifdef PSDF_MARCH_STATS
+                if (lane == 0) {
+                    atomicAdd(&g_march_stats[10], 1ull);
+                    atomicAdd(&g_march_stats[11], (unsigned long long)__popc(grp));
+                }
+#endif
                 const int32_t* pid = g.probe_ids + (int64_t)t0 * 8;
                 for (int q = lane; q < 8 * nc; q += 32) {
                     const int c = q / nc, j = q - (q / nc) * nc;
@@ -954,15 +960,8 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
 #pragma unroll
             for (int a = 0; a < 3; ++a) dgv[a] = (dn[a] - n[a] * dnn) / geo.glen;
             const double inv2h = 1.0 / (2.0 * g.h);
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                if (dgv[a] == 0.0) continue;
-                double pp[3] = {pc[0], pc[1], pc[2]};
-                pp[a] = dadd(pc[a], g.h);
-                scatter_smooth(g, P.g_smooth, pp[0], pp[1], pp[2], dgv[a] * inv2h);
-                pp[a] = dsub(pc[a], g.h);
-                scatter_smooth(g, P.g_smooth, pp[0], pp[1], pp[2], -dgv[a] * inv2h);
-            }
+            scatter_gradient_stencil(g, P.g_smooth, tile, pc, dgv[0] * inv2h, dgv[1] * inv2h,
+                                     dgv[2] * inv2h);
         }
         __syncwarp();
     }
