@@ -10,6 +10,7 @@
 // A train step is the kernel sequence K2 (fused ray pass) -> K3..K6
 // (regularizers) -> K7 (G^T fold) -> [NCCL all-reduce] -> K8 (Adam) -> K9
 // (smoothing), all on the context's stream.
+#include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -165,6 +166,10 @@ struct psdf_ctx {
     float* d_block_min = nullptr;  // [T][64] minimum of each 4^3 block's brick
     int32_t* d_tile_nbr = nullptr; // [T][27] neighbour tile ids
     uint8_t* d_sat_dist = nullptr; // [T][64] saturation distances of the current ray pass
+    int* h_keys = nullptr;         // handover sort: keys out, iota values in, CUB temp
+    int* h_iota = nullptr;
+    void* sort_tmp = nullptr;
+    size_t sort_tmp_bytes = 0;
     int bit_words = 0;
     int4* d_tile_coords = nullptr;
     int32_t* d_probe_ids = nullptr;
@@ -408,6 +413,11 @@ void launch_render(psdf_ctx* c, RayPassParams& P) {
     ++c->last_launches;
 }
 
+__global__ void iota_kernel(int* __restrict__ v, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = i;
+}
+
 void free_wave(psdf_ctx* c) {
     WaveBufs& W = c->wave;
     for (void* p : {(void*)W.e_slot, (void*)W.e_dir, (void*)W.e_tfirst, (void*)W.e_cfirst,
@@ -415,11 +425,14 @@ void free_wave(psdf_ctx* c) {
                     (void*)W.r_pos, (void*)W.r_w, (void*)W.r_tile, (void*)W.r_entry,
                     (void*)W.r_next, (void*)W.r_c, (void*)W.r_up, (void*)W.r_geo, (void*)W.h_slot,
                     (void*)W.h_count, (void*)W.h_tileprev, (void*)W.h_t, (void*)W.h_tprev, (void*)W.h_dir,
-                    (void*)W.h_t1})
+                    (void*)W.h_t1, (void*)W.h_perm, (void*)W.r_perm, (void*)c->h_keys, (void*)c->h_iota, c->sort_tmp})
         if (p) cudaFree(p);
     unsigned* keep = W.counters;
     W = WaveBufs{};
     W.counters = keep;
+    c->h_keys = c->h_iota = nullptr;
+    c->sort_tmp = nullptr;
+    c->sort_tmp_bytes = 0;
 }
 
 // Grows the ray-entry / shading-record buffers (kept across steps).
@@ -457,6 +470,20 @@ void ensure_wave(psdf_ctx* c, int64_t e_cap, int64_t r_cap, int64_t h_cap) {
     CK(cudaMalloc(&W.h_tprev, sizeof(double) * h_cap));
     CK(cudaMalloc(&W.h_dir, sizeof(double) * 3 * h_cap));
     CK(cudaMalloc(&W.h_t1, sizeof(double) * h_cap));
+    CK(cudaMalloc(&W.h_perm, sizeof(int) * h_cap));
+    CK(cudaMalloc(&W.r_perm, sizeof(int) * r_cap));
+    const int64_t k_cap = std::max(h_cap, r_cap);
+    CK(cudaMalloc(&c->h_keys, sizeof(int) * k_cap));
+    CK(cudaMalloc(&c->h_iota, sizeof(int) * k_cap));
+    iota_kernel<<<(unsigned)((k_cap + 255) / 256), 256, 0, c->stream>>>(c->h_iota, (int)k_cap);
+    CK(cudaGetLastError());
+    size_t tb_h = 0, tb_r = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb_h, W.h_slot, c->h_keys, c->h_iota, W.h_perm,
+                                       (int)h_cap, 0, 31, c->stream));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb_r, W.r_tile, c->h_keys, c->h_iota, W.r_perm,
+                                       (int)r_cap, 0, 31, c->stream));
+    c->sort_tmp_bytes = std::max(tb_h, tb_r);
+    CK(cudaMalloc(&c->sort_tmp, c->sort_tmp_bytes));
     W.e_cap = (int)e_cap;
     W.r_cap = (int)r_cap;
     W.h_cap = (int)h_cap;
@@ -489,15 +516,31 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
         P.work_counter = c->d_work;
         march_scan_kernel<<<(unsigned)grid_s, BLOCK, smem_bits, s>>>(P, c->wave);
         CK(cudaGetLastError());
-        CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
-        march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, c->wave);
-        CK(cudaGetLastError());
-        c->last_launches += 2;
-        CK(cudaMemcpyAsync(c->h_wave_counters, c->wave.counters, sizeof(unsigned) * 3,
+        CK(cudaMemcpyAsync(c->h_wave_counters + 2, c->wave.counters + 2, sizeof(unsigned),
                            cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        const int64_t ne = c->h_wave_counters[0], nr = c->h_wave_counters[1], nh = c->h_wave_counters[2];
-        if (ne <= c->wave.e_cap && nr <= c->wave.r_cap && nh <= c->wave.h_cap) break;
+        const int64_t nh = c->h_wave_counters[2];
+        int64_t ne = 0, nr = 0;
+        if (nh <= c->wave.h_cap) {
+            // handovers in image order: coherent warps in K2a and coherent
+            // shading records downstream
+            if (nh > 0) {
+                int end_bit = 1;
+                while (end_bit < 31 && ((int64_t)1 << end_bit) < n_work * 32) ++end_bit;
+                CK(cub::DeviceRadixSort::SortPairs(c->sort_tmp, c->sort_tmp_bytes, c->wave.h_slot, c->h_keys,
+                                                   c->h_iota, c->wave.h_perm, (int)nh, 0, end_bit, s));
+            }
+            CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
+            march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, c->wave);
+            CK(cudaGetLastError());
+            c->last_launches += 2;
+            CK(cudaMemcpyAsync(c->h_wave_counters, c->wave.counters, sizeof(unsigned) * 2,
+                               cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            ne = c->h_wave_counters[0];
+            nr = c->h_wave_counters[1];
+            if (ne <= c->wave.e_cap && nr <= c->wave.r_cap) break;
+        }
         if (attempt > 2) fail(PSDF_ERR_RUNTIME, "ray pass buffers failed to grow");
         ensure_wave(c, ne + ne / 2 + 4096, nr + nr / 2 + 4096, nh + nh / 2 + 4096);
         // the failed sweep already accumulated statistics: clear and redo
@@ -522,6 +565,14 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     }
     c->last_entries = n_ent;
     c->last_records = n_rec;
+    // shading records in tile order (K2b / K2e): decode gathers and the
+    // per-tile probe / plane gradient aggregation see runs of one tile
+    if (n_rec > 0) {
+        int end_bit = 1;
+        while (end_bit < 31 && ((int64_t)1 << end_bit) < c->desc.T) ++end_bit;
+        CK(cub::DeviceRadixSort::SortPairs(c->sort_tmp, c->sort_tmp_bytes, c->wave.r_tile, c->h_keys, c->h_iota,
+                                           c->wave.r_perm, n_rec, 0, end_bit, s));
+    }
     CK(cudaEventRecord(c->ev_k[1], s));
     if (n_rec > 0) {
         const int per_sm = blocks_per_sm((const void*)shade_fwd_kernel<NS, NA>, smem_f);

@@ -66,6 +66,8 @@ struct WaveBufs {
     double* h_tprev;   // t of the last saturated sample
     double* h_dir;     // [cap][3]
     double* h_t1;      // box exit
+    int* h_perm;       // handovers sorted by slot (image order; CUB radix sort)
+    int* r_perm;       // shading records sorted by tile (K2b / K2e order)
     unsigned* counters;  // [0] entries, [1] records, [2] handovers
     int e_cap, r_cap, h_cap;
 };
@@ -257,8 +259,8 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
         if (lane == 0) base = (int)atomicAdd(P.work_counter, 32ull);
         base = __shfl_sync(FULL, base, 0);
         if (base >= n_hand) break;
-        const int hi = base + lane;
-        const bool valid = hi < n_hand;
+        const bool valid = base + lane < n_hand;
+        const int hi = valid ? W.h_perm[base + lane] : 0;
         const int slot = valid ? W.h_slot[hi] : 0;
         const LaneRay R = lane_ray(P, slot >> 5, slot & 31);
         const bool in_mask = valid && __ldg(R.V->mask + R.px) != 0;
@@ -442,7 +444,8 @@ __global__ void __launch_bounds__(BLOCK) shade_fwd_kernel(RayPassParams P, WaveB
     const MlpLayout G = MlpLayout::make(IN);
     load_mlp_smem(P.mlp, smem, G, L);
     __syncthreads();
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_rec; i += gridDim.x * blockDim.x) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_rec; q += gridDim.x * blockDim.x) {
+        const int i = W.r_perm[q];
         const int e = W.r_entry[i];
         const ViewDev& V = entry_view(P, W, e);
         const float* cam_row =
@@ -604,16 +607,17 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
     const GridView& g = P.g;
     const int warps_total = gridDim.x * WARPS_PER_BLOCK;
     for (int base = (blockIdx.x * WARPS_PER_BLOCK + warp) * 32; base < n_rec; base += warps_total * 32) {
-        const int i = base + lane;
+        const bool in_range = base + lane < n_rec;
+        const int i = in_range ? W.r_perm[base + lane] : 0;
         float4 up = make_float4(0.f, 0.f, 0.f, 0.f);
         int e = -1, tile = -1, cam_bias_row = -1;
-        if (i < n_rec) {
+        if (in_range) {
             up = reinterpret_cast<const float4*>(W.r_up)[i];
             e = W.r_entry[i];
             tile = W.r_tile[i];
             if (P.ncam > 0) cam_bias_row = entry_view(P, W, e).cam_bias_row;
         }
-        const bool shade = i < n_rec && (up.x != 0.f || up.y != 0.f || up.z != 0.f);
+        const bool shade = in_range && (up.x != 0.f || up.y != 0.f || up.z != 0.f);
         const unsigned smask = __ballot_sync(FULL, shade);
         if (!smask) continue;
         double pc[3] = {0, 0, 0}, dneg[3] = {0, 0, 0};
