@@ -293,8 +293,16 @@ def main():
     for it in range(args.warmup):
         ctx.train_step_views(batch_ids(it), hp)
     if args.profile:
+        # the second step runs inside cudaProfilerStart/Stop, so
+        # `ncu --profile-from-start off` captures exactly one train step
         for it in range(2):
+            if it == 1:
+                torch.cuda.synchronize()
+                torch.cuda.cudart().cudaProfilerStart()
             print(ctx.train_step_views(batch_ids(args.warmup + it), hp))
+            if it == 1:
+                torch.cuda.synchronize()
+                torch.cuda.cudart().cudaProfilerStop()
             print(ctx.last_timing(), ctx.last_k2_breakdown())
         print(render_fps(api, torch, ctx, 6455.3, frames=1))
         ctx.close()
