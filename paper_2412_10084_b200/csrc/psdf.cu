@@ -421,7 +421,7 @@ __global__ void iota_kernel(int* __restrict__ v, int n) {
 void free_wave(psdf_ctx* c) {
     WaveBufs& W = c->wave;
     for (void* p : {(void*)W.e_slot, (void*)W.e_dir, (void*)W.e_tfirst, (void*)W.e_cfirst,
-                    (void*)W.e_nlive, (void*)W.e_acc, (void*)W.e_head, (void*)W.e_craw,
+                    (void*)W.e_nlive, (void*)W.e_acc, (void*)W.e_head, (void*)W.e_craw, (void*)W.e_t1,
                     (void*)W.r_pos, (void*)W.r_w, (void*)W.r_tile, (void*)W.r_entry,
                     (void*)W.r_next, (void*)W.r_c, (void*)W.r_up, (void*)W.r_geo, (void*)W.h_slot,
                     (void*)W.h_count, (void*)W.h_tileprev, (void*)W.h_t, (void*)W.h_tprev, (void*)W.h_dir,
@@ -454,6 +454,7 @@ void ensure_wave(psdf_ctx* c, int64_t e_cap, int64_t r_cap, int64_t h_cap) {
     CK(cudaMalloc(&W.e_acc, sizeof(double) * e_cap));
     CK(cudaMalloc(&W.e_head, sizeof(int) * e_cap));
     CK(cudaMalloc(&W.e_craw, sizeof(double) * 3 * e_cap));
+    CK(cudaMalloc(&W.e_t1, sizeof(double) * e_cap));
     CK(cudaMalloc(&W.r_pos, sizeof(double) * 3 * r_cap));
     CK(cudaMalloc(&W.r_w, sizeof(double) * r_cap));
     CK(cudaMalloc(&W.r_tile, sizeof(int) * r_cap));

@@ -774,6 +774,34 @@ __device__ __forceinline__ void scatter_smooth(const GridView& g, float* __restr
     }
 }
 
+// scatter_smooth at a sample p of tile `tile` (coordinates tc): every corner
+// lies in the tile's brick, so the owning tiles come from g.tile_nbr (no
+// table lookups, all eight inside the tile in the common case).
+__device__ __forceinline__ void scatter_smooth_in(const GridView& g, float* __restrict__ gsm, int tile,
+                                                  int4 tc, const double p[3], double gv) {
+    const double cx = dsub(w2v(g, p[0], 0), 0.5);
+    const double cy = dsub(w2v(g, p[1], 1), 0.5);
+    const double cz = dsub(w2v(g, p[2], 2), 0.5);
+    const int bx = (int)floor(cx), by = (int)floor(cy), bz = (int)floor(cz);
+    const double fx = dsub(cx, (double)bx), fy = dsub(cy, (double)by), fz = dsub(cz, (double)bz);
+    const double gx0 = dsub(1.0, fx), gy0 = dsub(1.0, fy), gz0 = dsub(1.0, fz);
+    const int lx = bx - 16 * tc.x, ly = by - 16 * tc.y, lz = bz - 16 * tc.z;  // in [-1, 15]
+    const bool inside = (unsigned)lx < 15u && (unsigned)ly < 15u && (unsigned)lz < 15u;
+    const int32_t* nbr = g.tile_nbr + (int64_t)tile * 27;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const double w = dmul(dmul((i & 1) ? fx : gx0, (i & 2) ? fy : gy0), (i & 4) ? fz : gz0);
+        if (w == 0.0) continue;
+        const int vx = lx + (i & 1), vy = ly + ((i >> 1) & 1), vz = lz + ((i >> 2) & 1);
+        int t = tile;
+        if (!inside) {
+            t = __ldg(nbr + (((vx >> 4) + 1) * 3 + ((vy >> 4) + 1)) * 3 + ((vz >> 4) + 1));
+            if (t < 0) continue;
+        }
+        atomicAdd(gsm + (int64_t)t * TV + vox_index(vx & 15, vy & 15, vz & 15), (float)(w * gv));
+    }
+}
+
 // The six scatter_smooth_grad calls of the normal chain (renderer.cpp:216-235:
 // +-c_a at p +- h e_a) merged: the shifted points share p's trilinear
 // fractions (a shift by one voxel moves the base corner by one), so their

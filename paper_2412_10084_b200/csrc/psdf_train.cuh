@@ -48,6 +48,7 @@ struct WaveBufs {
     double* e_acc;     // accumulated opacity
     int* e_head;       // first record of the ray, -1 if none
     double* e_craw;    // [cap][3] sum_i w_i C_i (K2b)
+    double* e_t1;      // box exit of the ray
     // shading records: samples with w > 0 on in-mask rays, append order
     double* r_pos;     // [cap][3]
     double* r_w;
@@ -393,6 +394,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
             W.e_cfirst[entry] = cnt_first;
             W.e_nlive[entry] = n_live;
             W.e_acc[entry] = acc;
+            W.e_t1[entry] = mr.t1;
             W.e_head[entry] = head;
             W.e_craw[3 * (int64_t)entry] = 0.0;
             W.e_craw[3 * (int64_t)entry + 1] = 0.0;
@@ -504,7 +506,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) alpha_bwd_kernel(RayPa
         const double dd[3] = {W.e_dir[3 * (int64_t)e], W.e_dir[3 * (int64_t)e + 1],
                               W.e_dir[3 * (int64_t)e + 2]};
         Marcher mr;
-        mr.init(g, R.V->cam.pos, dd, P.n_max);
+        mr.init_from(g, R.V->cam.pos, dd, P.n_max, W.e_t1[e]);
         mr.t = W.e_tfirst[e];
         mr.count = W.e_cfirst[e];
         const int n_live = W.e_nlive[e];
@@ -556,7 +558,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) alpha_bwd_kernel(RayPa
             }
             mr.pos(t_cur, pc);
             const double ds_i = dadd(carry, own);
-            if (ds_i != 0.0) scatter_smooth(g, P.g_smooth, pc[0], pc[1], pc[2], ds_i);
+            if (ds_i != 0.0) scatter_smooth_in(g, P.g_smooth, tile_cur, tc_cur, pc, ds_i);
             carry = nxt;
             ++idx;
             if (idx >= n_live || !has_next) {
@@ -566,6 +568,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) alpha_bwd_kernel(RayPa
             T = dmul(T, dsub(1.0, alpha));
             t_cur = t_nxt;
             tile_cur = tile_nxt;
+            tc_cur = tc_nxt;
             a_cur = a_nxt;
         }
     }
