@@ -38,6 +38,7 @@ def lib():
     L.og_smooth_all.argtypes = [C.c_void_p]
     L.og_march_ray.argtypes = [C.c_void_p, _dp, _dp, C.c_int, _dp]
     L.og_pixel_dir.argtypes = [C.POINTER(RefCamera), C.c_double, C.c_double, _dp]
+    L.og_pixel_dirs.argtypes = [C.POINTER(RefCamera), _dp]
     L.og_render_ray.argtypes = [C.c_void_p, _dp, _dp, C.POINTER(RefRenderOpts), _dp]
     L.og_render_image.argtypes = [C.c_void_p, C.POINTER(RefCamera), C.POINTER(RefRenderOpts), _dp, _dp,
                                   _dp, _lp]
@@ -206,6 +207,13 @@ class OracleGrid:
 def pixel_dir(cam, u, v):
     d = np.zeros(3)
     lib().og_pixel_dir(C.byref(cam), u, v, ptr(d))
+    return d
+
+
+def pixel_dirs(cam):
+    """og_pixel_dir at every pixel centre, [height][width][3]."""
+    d = np.zeros((cam.height, cam.width, 3))
+    lib().og_pixel_dirs(C.byref(cam), ptr(d))
     return d
 
 

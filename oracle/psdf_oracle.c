@@ -293,6 +293,13 @@ void og_pixel_dir(const OCamera* c, double u, double v, double* out) {
     out[0] = res.x; out[1] = res.y; out[2] = res.z;
 }
 
+/* every pixel centre of a camera (test helper, batch of og_pixel_dir) */
+void og_pixel_dirs(const OCamera* c, double* out) {
+    for (int v = 0; v < c->height; ++v)
+        for (int u = 0; u < c->width; ++u)
+            og_pixel_dir(c, u + 0.5, v + 0.5, out + 3 * ((size_t)v * c->width + u));
+}
+
 /* ----------------------------------------------------------------- decode */
 
 static double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); } /* renderer.cpp:10 */

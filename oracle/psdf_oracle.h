@@ -56,6 +56,7 @@ void og_smooth_all(OGrid* g);
 
 int og_march_ray(const OGrid* g, const double* o, const double* d, int n_max, double* ts);
 void og_pixel_dir(const OCamera* c, double u, double v, double* d);
+void og_pixel_dirs(const OCamera* c, double* out);
 /* per-ray: result[6] = color xyz, acc, trans_end, depth; returns #samples */
 int og_render_ray(const OGrid* g, const double* o, const double* d, const ORenderOpts* opt,
                   double* result);

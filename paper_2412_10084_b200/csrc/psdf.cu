@@ -301,6 +301,8 @@ Cam to_cam(const psdf_camera& c) {
     d.fy = c.fy;
     d.cx = c.cx;
     d.cy = c.cy;
+    d.rfx = 1.0 / c.fx;  // correctly rounded reciprocals for ddiv_r (psdf_device.cuh)
+    d.rfy = 1.0 / c.fy;
     for (int i = 0; i < 9; ++i) d.rot[i] = c.rot[i];
     for (int i = 0; i < 3; ++i) d.pos[i] = c.pos[i];
     d.width = c.width;

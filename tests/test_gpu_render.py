@@ -61,6 +61,14 @@ def _march_rays(n, seed, span=1.5, tgt_span=0.45):
     return o, d
 
 
+def test_pixel_dirs_bit_exact_full_view():
+    """A bench-sized view (1600x1200): every ray direction bit for bit."""
+    from paper_2412_10084_b200 import api
+    from oracle.port import pixel_dirs
+    for cam in api.make_ring_cameras(3, 1600, height=1200):
+        assert np.array_equal(api.pixel_dirs(cam), pixel_dirs(_oracle_cam(cam)))
+
+
 @pytest.mark.parametrize("res,band,radius,n", [(32, 32, 0.3, 3000), (64, 3, 0.3, 3000),
                                                (256, 3, 0.25, 20000), (512, 2, 0.3, 20000)])
 def test_march_bit_exact(ctx, res, band, radius, n):
