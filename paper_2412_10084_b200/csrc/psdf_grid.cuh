@@ -90,51 +90,68 @@ __device__ __forceinline__ void load_region(const float* __restrict__ src, const
 
 __device__ __forceinline__ bool bit_at(const uint32_t* bits, int i) { return (bits[i >> 5] >> (i & 31)) & 1u; }
 
+// One separable 5-tap pass along a column: out[o * os] = sum_d w[d] in[(o + d) * is],
+// o in [0, NO), with the NO + 4 inputs held in registers (one load per input
+// instead of five per output).  Summation order d = 0..4 (same fp32 value
+// whichever block computes the voxel).
+template <int NO>
+__device__ __forceinline__ void column_5tap(const float* __restrict__ in, int is, float* __restrict__ out,
+                                            int os, const Taps& taps) {
+    float v[NO + 4];
+#pragma unroll
+    for (int k = 0; k < NO + 4; ++k) v[k] = in[k * is];
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+        float s = 0.f;
+#pragma unroll
+        for (int d = 0; d < 5; ++d) s += taps.w[d] * v[o + d];
+        out[o * os] = s;
+    }
+}
+
 // K7: the G^T fold (grads.cpp:67-96): dst[t] += G * src over a 20^3 halo of
 // src filled with 0 (the reference skips unallocated / out-of-range taps, and
 // the Gaussian is symmetric, so G^T is the same stencil).  Separable 5-tap
-// passes in shared memory.
+// column passes in shared memory.
+constexpr int FZ = HE + 1;  // padded z stride of the y-pass output (conflict-free z columns)
 __global__ void __launch_bounds__(256) smooth_fold_kernel(GridView g, const float* __restrict__ src,
                                                           float fill, float* __restrict__ dst,
                                                           int accumulate, Taps taps) {
     extern __shared__ __align__(16) float sh[];
     __shared__ int nb[27];
-    float* A = sh;           // [20][20][20]
+    float* A = sh;           // [20][20][20] halo; later [16][16][21] after the y pass
     float* B = sh + HV;      // [16][20][20] after the x pass
     const int t = blockIdx.x;
     stage_nbr(g, t, nb);
     __syncthreads();
     load_region<HE, -2>(src, nb, fill, A, nullptr);
     __syncthreads();
-    // x pass: B[x][y][z] = sum_d w[d] A[x+d+2][y][z], x in [0,16)
-    for (int i = threadIdx.x; i < 16 * HE * HE; i += blockDim.x) {
-        const int x = i / (HE * HE), yz = i % (HE * HE);
-        float s = 0.f;
-#pragma unroll
-        for (int d = 0; d < 5; ++d) s += taps.w[d] * A[(x + d) * HE * HE + yz];
-        B[i] = s;
+    for (int c = threadIdx.x; c < HE * HE; c += blockDim.x)  // x pass, column (y, z)
+        column_5tap<16>(A + c, HE * HE, B + c, HE * HE, taps);
+    __syncthreads();
+    for (int c = threadIdx.x; c < 16 * HE; c += blockDim.x) {  // y pass, column (x, z)
+        const int x = c / HE, z = c % HE;
+        column_5tap<16>(B + x * HE * HE + z, HE, A + x * 16 * FZ + z, FZ, taps);
     }
     __syncthreads();
-    // y pass: A'[x][y][z] = sum_d w[d] B[x][y+d][z], y in [0,16)  (reuse A as [16][16][20])
-    for (int i = threadIdx.x; i < 16 * 16 * HE; i += blockDim.x) {
-        const int x = i / (16 * HE), y = (i / HE) % 16, z = i % HE;
-        float s = 0.f;
-#pragma unroll
-        for (int d = 0; d < 5; ++d) s += taps.w[d] * B[(x * HE + y + d) * HE + z];
-        A[i] = s;
-    }
-    __syncthreads();
-    // z pass into the tile
     float* out = dst + (int64_t)t * TV;
-    for (int i = threadIdx.x; i < TV; i += blockDim.x) {
-        const int x = i >> 8, y = (i >> 4) & 15, z = i & 15;
-        float s = 0.f;
+    {  // z pass, column (x, y): 16 consecutive voxels of the tile
+        const int c = threadIdx.x;  // 256 columns
+        float r[16];
+        column_5tap<16>(A + c * FZ, 1, r, 1, taps);
+        float4* o4 = reinterpret_cast<float4*>(out + c * 16);
 #pragma unroll
-        for (int d = 0; d < 5; ++d) s += taps.w[d] * A[(x * 16 + y) * HE + z + d];
-        if (accumulate)
-            out[i] += s;
-        else
-            out[i] = s;
+        for (int q = 0; q < 4; ++q) {
+            float4 v = make_float4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+            if (accumulate) {
+                const float4 o = o4[q];
+                v.x += o.x;
+                v.y += o.y;
+                v.z += o.z;
+                v.w += o.w;
+            }
+            o4[q] = v;
+        }
     }
 }
 constexpr size_t kFoldSmem = sizeof(float) * (HV + 16 * HE * HE);
@@ -148,6 +165,7 @@ constexpr size_t kFoldSmem = sizeof(float) * (HV + 16 * HE * HE);
 // computes it.  Also writes the brick minima of the saturation test
 // (tile_min, block_min; psdf_device.cuh kSatX).
 constexpr int SE = 22;  // raw halo edge: local voxels [-3, 19)
+constexpr int SZ = SE + 1;  // padded z stride of the y-pass output
 constexpr size_t kSmoothApronSmem = sizeof(float) * (SE * SE * SE + AE * SE * SE);
 __global__ void __launch_bounds__(256) smooth_apron_kernel(GridView g, const float* __restrict__ raw,
                                                            float fill, float* __restrict__ smooth,
@@ -156,45 +174,38 @@ __global__ void __launch_bounds__(256) smooth_apron_kernel(GridView g, const flo
     extern __shared__ __align__(16) float sh[];
     __shared__ int nb[27];
     __shared__ float red[2];
-    float* A = sh;                  // [22][22][22] raw halo; later [18][18][22]
+    float* A = sh;                  // [22][22][22] raw halo; later [18][18][23]
     float* B = sh + SE * SE * SE;   // [18][22][22] after the x pass; later the 18^3 apron
     const int t = blockIdx.x;
     stage_nbr(g, t, nb);
     __syncthreads();
     load_region<SE, -3>(raw, nb, fill, A, nullptr);
     __syncthreads();
-    for (int i = threadIdx.x; i < AE * SE * SE; i += blockDim.x) {
-        const int x = i / (SE * SE), yz = i % (SE * SE);
-        float s = 0.f;
-#pragma unroll
-        for (int d = 0; d < 5; ++d) s += taps.w[d] * A[(x + d) * SE * SE + yz];
-        B[i] = s;
+    for (int c = threadIdx.x; c < SE * SE; c += blockDim.x)  // x pass, column (y, z)
+        column_5tap<AE>(A + c, SE * SE, B + c, SE * SE, taps);
+    __syncthreads();
+    for (int c = threadIdx.x; c < AE * SE; c += blockDim.x) {  // y pass, column (x, z)
+        const int x = c / SE, z = c % SE;
+        column_5tap<AE>(B + x * SE * SE + z, SE, A + x * AE * SZ + z, SZ, taps);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < AE * AE * SE; i += blockDim.x) {
-        const int x = i / (AE * SE), y = (i / SE) % AE, z = i % SE;
-        float s = 0.f;
-#pragma unroll
-        for (int d = 0; d < 5; ++d) s += taps.w[d] * B[(x * SE + y + d) * SE + z];
-        A[i] = s;
-    }
+    for (int c = threadIdx.x; c < AE * AE; c += blockDim.x)  // z pass, column (x, y)
+        column_5tap<AE>(A + c * SZ, 1, B + c * AE, 1, taps);
     __syncthreads();
     float* apt = ap + (int64_t)t * AV;
     float* sm = smooth + (int64_t)t * TV;
     for (int i = threadIdx.x; i < AV; i += blockDim.x) {
         const int x = i / (AE * AE), y = (i / AE) % AE, z = i % AE;  // local voxel = (x,y,z) - 1
-        float s = 0.f;
-#pragma unroll
-        for (int d = 0; d < 5; ++d) s += taps.w[d] * A[(x * AE + y) * SE + z + d];
+        float s = B[i];
         const int lx = x - 1, ly = y - 1, lz = z - 1;
         const bool own = (unsigned)lx < 16u && (unsigned)ly < 16u && (unsigned)lz < 16u;
         if (own) {
             sm[vox_index(lx, ly, lz)] = s;
         } else if (nb[((lx >> 4) + 1) * 9 + ((ly >> 4) + 1) * 3 + (lz >> 4) + 1] < 0) {
             s = (float)g.far;  // smooth_value (grid.cpp:87-94)
+            B[i] = s;
         }
         apt[i] = s;
-        B[i] = s;
     }
     __syncthreads();
     // brick minima: each 4^3 block's 6^3 brick (voxels 4b-1 .. 4b+4) and the tile

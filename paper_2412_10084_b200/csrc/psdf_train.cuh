@@ -144,7 +144,10 @@ __device__ __forceinline__ bool photo_term(const RayPassParams& P, bool in_mask,
 // nothing but the counts, so a ray that never leaves them (or misses the
 // grid) is finished here — its loss is the empty-ray term — and the others
 // are handed over, compacted, to K2a with the state at that sample.
-__global__ void __launch_bounds__(BLOCK) march_scan_kernel(RayPassParams P, WaveBufs W) {
+#ifndef PSDF_SCAN_MINB
+#define PSDF_SCAN_MINB 6
+#endif
+__global__ void __launch_bounds__(BLOCK, PSDF_SCAN_MINB) march_scan_kernel(RayPassParams P, WaveBufs W) {
     extern __shared__ __align__(16) uint32_t sm_bits[];
     const int lane = threadIdx.x & 31;
     const GridView& g = P.g;
