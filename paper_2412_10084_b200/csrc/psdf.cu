@@ -427,7 +427,7 @@ void free_wave(psdf_ctx* c) {
                     (void*)W.r_pos, (void*)W.r_w, (void*)W.r_tile, (void*)W.r_entry,
                     (void*)W.r_next, (void*)W.r_c, (void*)W.r_up, (void*)W.r_geo, (void*)W.h_slot,
                     (void*)W.h_count, (void*)W.h_tileprev, (void*)W.h_t, (void*)W.h_tprev, (void*)W.h_dir,
-                    (void*)W.h_t1, (void*)W.h_perm, (void*)W.r_perm, (void*)c->h_keys, (void*)c->h_iota, c->sort_tmp})
+                    (void*)W.h_t1, (void*)W.h_perm, (void*)W.r_perm, (void*)W.r_fg, (void*)c->h_keys, (void*)c->h_iota, c->sort_tmp})
         if (p) cudaFree(p);
     unsigned* keep = W.counters;
     W = WaveBufs{};
@@ -475,6 +475,7 @@ void ensure_wave(psdf_ctx* c, int64_t e_cap, int64_t r_cap, int64_t h_cap) {
     CK(cudaMalloc(&W.h_t1, sizeof(double) * h_cap));
     CK(cudaMalloc(&W.h_perm, sizeof(int) * h_cap));
     CK(cudaMalloc(&W.r_perm, sizeof(int) * r_cap));
+    CK(cudaMalloc(&W.r_fg, sizeof(float) * (size_t)FgDims<8, 8>::STRIDE * r_cap));
     const int64_t k_cap = std::max(h_cap, r_cap);
     CK(cudaMalloc(&c->h_keys, sizeof(int) * k_cap));
     CK(cudaMalloc(&c->h_iota, sizeof(int) * k_cap));
@@ -598,7 +599,11 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
         const int grid = (int)std::min<int64_t>((n_rec + BLOCK - 1) / BLOCK, (int64_t)per_sm * c->sm_count);
         shade_bwd_kernel<NS, NA><<<grid, BLOCK, smem_b, s>>>(P, c->wave, n_rec);
         CK(cudaGetLastError());
-        ++c->last_launches;
+        const int per_sm_g = blocks_per_sm((const void*)shade_geo_kernel<NS, NA>, 0);
+        const int grid_g = (int)std::min<int64_t>((n_rec + BLOCK - 1) / BLOCK, (int64_t)per_sm_g * c->sm_count);
+        shade_geo_kernel<NS, NA><<<grid_g, BLOCK, 0, s>>>(P, c->wave, n_rec);
+        CK(cudaGetLastError());
+        c->last_launches += 2;
     }
     CK(cudaEventRecord(c->ev_k[4], s));
     CK(cudaEventRecord(c->ev_ray1, s));

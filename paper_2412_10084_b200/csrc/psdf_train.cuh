@@ -69,6 +69,7 @@ struct WaveBufs {
     double* h_t1;      // box exit
     int* h_perm;       // handovers sorted by slot (image order; CUB radix sort)
     int* r_perm;       // shading records sorted by tile (K2b / K2e order)
+    float* r_fg;       // [cap][FgDims::STRIDE] feature gradients (K2e-mlp -> K2e-geo)
     unsigned* counters;  // [0] entries, [1] records, [2] handovers
     int e_cap, r_cap, h_cap;
 };
@@ -589,6 +590,13 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) alpha_bwd_kernel(RayPa
     }
 }
 
+// Per-record feature gradients handed from the MLP backward to the geometry
+// backward: gfs[NS] | gfa[NA] | d(n.v), padded to a float4 multiple.
+template <int NS, int NA>
+struct FgDims {
+    static constexpr int STRIDE = ((NS + NA + 1) + 3) & ~3;
+};
+
 // ------------------------------------------------------------------ K2e
 template <int NS, int NA>
 __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveBufs W, int n_rec) {
@@ -852,6 +860,100 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
                 }
                 d_ndotv = -du;
             }
+            // feature gradients for K2e-geo: gfs | gfa | d(n.v)
+            float* fg = W.r_fg + (int64_t)i * FgDims<NS, NA>::STRIDE;
+#pragma unroll
+            for (int k = 0; k < NS; ++k) fg[k] = gfs[k];
+#pragma unroll
+            for (int k = 0; k < NA; ++k) fg[NS + k] = gfa[k];
+            fg[NS + NA] = d_ndotv;
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < G.total_nocam; i += blockDim.x) {
+        int a;
+        if (i < G.b1) a = GA::W1 + (i / IN) * GA::W1S + (i % IN);
+        else if (i < G.w2) a = GA::B1 + (i - G.b1);
+        else if (i < G.b2) a = GA::W2 + ((i - G.w2) >> 5) * 33 + ((i - G.w2) & 31);
+        else if (i < G.w3) a = GA::B2 + (i - G.b2);
+        else if (i < G.b3) a = GA::W3 + (i - G.w3);
+        else a = GA::B3 + (i - G.b3);
+        float v = 0.f;
+#pragma unroll
+        for (int w = 0; w < WARPS_PER_BLOCK; ++w) v += s_acc[w * GA::TOTAL + a];
+        if (v != 0.f) atomicAdd(P.g_mlp + i, v);
+    }
+}
+
+// ------------------------------------------------------------------ K2e-geo
+// The geometry half of decode_backward and the normal chain, one lane per
+// shading record in tile order (no MLP state: high occupancy): tri-plane
+// atomics (grid.cpp:189-202), the probe direction gradient (sh.cpp:151-169),
+// probe coefficient gradients aggregated over the warp's lanes sharing a
+// tile, and the SDF-gradient chain of the normal (renderer.cpp:216-235).
+constexpr int PWS = 33;  // row stride of the per-warp probe staging (w8 | Y[16] | gfa)
+template <int NS, int NA>
+__global__ void __launch_bounds__(BLOCK) shade_geo_kernel(RayPassParams P, WaveBufs W, int n_rec) {
+    __shared__ float s_pw[WARPS_PER_BLOCK][32 * PWS];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* PW = s_pw[warp];
+    const GridView& g = P.g;
+    const int warps_total = gridDim.x * WARPS_PER_BLOCK;
+    using GR = GeoRec<NS, NA>;
+    for (int base = (blockIdx.x * WARPS_PER_BLOCK + warp) * 32; base < n_rec; base += warps_total * 32) {
+        const bool in_range = base + lane < n_rec;
+        const int i = in_range ? W.r_perm[base + lane] : 0;
+        float4 up = make_float4(0.f, 0.f, 0.f, 0.f);
+        int e = -1, tile = -1;
+        if (in_range) {
+            up = reinterpret_cast<const float4*>(W.r_up)[i];
+            e = W.r_entry[i];
+            tile = W.r_tile[i];
+        }
+        const bool shade = in_range && (up.x != 0.f || up.y != 0.f || up.z != 0.f);
+        const unsigned smask = __ballot_sync(FULL, shade);
+        if (!smask) continue;
+        float gfs[NS], gfa[NA], d_ndotv = 0.f, drx = 0.f, dry = 0.f, drz = 0.f;
+        ShadeGeo geo;
+        float pv[3][NS];
+        if (shade) {
+            constexpr int NQ = (GR::X + 3) / 4;
+            float r[4 * NQ];
+            const float4* src = reinterpret_cast<const float4*>(W.r_geo + (int64_t)i * GR::STRIDE);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const float4 v4 = src[q];
+                r[4 * q] = v4.x;
+                r[4 * q + 1] = v4.y;
+                r[4 * q + 2] = v4.z;
+                r[4 * q + 3] = v4.w;
+            }
+            geo.n[0] = r[0];
+            geo.n[1] = r[1];
+            geo.n[2] = r[2];
+            geo.glen = r[3];
+            geo.refl[0] = r[4];
+            geo.refl[1] = r[5];
+            geo.refl[2] = r[6];
+            geo.ndv = r[7];
+            const int packed = __float_as_int(r[11]);
+            geo.tx = Tap{packed & 15, r[8]};
+            geo.ty = Tap{(packed >> 4) & 15, r[9]};
+            geo.tz = Tap{(packed >> 8) & 15, r[10]};
+            geo.degenerate = (packed >> 12) & 1;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) geo.w8[c] = r[12 + c];
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+#pragma unroll
+                for (int k = 0; k < NS; ++k) pv[q][k] = r[GR::PV + q * NS + k];
+            const float* fg = W.r_fg + (int64_t)i * FgDims<NS, NA>::STRIDE;
+#pragma unroll
+            for (int k = 0; k < NS; ++k) gfs[k] = fg[k];
+#pragma unroll
+            for (int k = 0; k < NA; ++k) gfa[k] = fg[NS + k];
+            d_ndotv = fg[NS + NA];
             // tri-plane backward (grid.cpp:189-202), plane samples from the record
             if (!P.no_spatial) {
                 float* gpl = P.g_planes + (int64_t)tile * 3 * 256 * NS;
@@ -906,21 +1008,19 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
                 sh_basis_grad_dot(geo.refl[0], geo.refl[1], geo.refl[2], P.order, sj, drx, dry, drz);
             }
         }
-        __syncwarp();
         // ---- probe coefficient gradients, aggregated over lanes sharing a tile
         if (!P.no_angular) {
-            float* PW = A2;  // per row: w8[8] | Y[16] | gfa[NA]
             if (shade) {
                 float Y[16];
 #pragma unroll
                 for (int j = 0; j < 16; ++j) Y[j] = 0.f;
                 sh_basis(geo.refl[0], geo.refl[1], geo.refl[2], P.order, Y);
 #pragma unroll
-                for (int c = 0; c < 8; ++c) PW[lane * RS + c] = geo.w8[c];
+                for (int c = 0; c < 8; ++c) PW[lane * PWS + c] = geo.w8[c];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) PW[lane * RS + 8 + j] = Y[j];
+                for (int j = 0; j < 16; ++j) PW[lane * PWS + 8 + j] = Y[j];
 #pragma unroll
-                for (int k = 0; k < NA; ++k) PW[lane * RS + 24 + k] = gfa[k];
+                for (int k = 0; k < NA; ++k) PW[lane * PWS + 24 + k] = gfa[k];
             }
             __syncwarp();
             const int nc = P.order * P.order;
@@ -930,12 +1030,6 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
                 const int t0 = __shfl_sync(FULL, tile, __ffs(rem) - 1);
                 const unsigned grp = __ballot_sync(FULL, ((rem >> lane) & 1u) && tile == t0);
                 rem &= ~grp;
-#ifdef PSDF_MARCH_STATS
-                if (lane == 0) {
-                    atomicAdd(&g_march_stats[10], 1ull);
-                    atomicAdd(&g_march_stats[11], (unsigned long long)__popc(grp));
-                }
-#endif
                 const int32_t* pid = g.probe_ids + (int64_t)t0 * 8;
                 for (int q = lane; q < 8 * nc; q += 32) {
                     const int c = q / nc, j = q - (q / nc) * nc;
@@ -945,20 +1039,25 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
                     bool any = false;
                     for (unsigned m = grp; m; m &= m - 1) {
                         const int s = __ffs(m) - 1;
-                        const float wc = PW[s * RS + c];
+                        const float wc = PW[s * PWS + c];
                         if (wc == 0.f) continue;
                         any = true;
-                        const float f = wc * PW[s * RS + 8 + j];
+                        const float f = wc * PW[s * PWS + 8 + j];
 #pragma unroll
-                        for (int k = 0; k < NA; ++k) a[k] += f * PW[s * RS + 24 + k];
+                        for (int k = 0; k < NA; ++k) a[k] += f * PW[s * PWS + 24 + k];
                     }
                     if (any) red_vec<NA>(P.g_probes + (int64_t)__ldg(pid + c) * stride + j * NA, a);
                 }
             }
+            __syncwarp();
         }
         // ---- normal chain (renderer.cpp:216-235)
         if (shade && !geo.degenerate) {
             const double n[3] = {geo.n[0], geo.n[1], geo.n[2]};
+            const double dneg[3] = {-W.e_dir[3 * (int64_t)e], -W.e_dir[3 * (int64_t)e + 1],
+                                    -W.e_dir[3 * (int64_t)e + 2]};
+            const double pc[3] = {W.r_pos[3 * (int64_t)i], W.r_pos[3 * (int64_t)i + 1],
+                                  W.r_pos[3 * (int64_t)i + 2]};
             const double dr[3] = {(double)drx, (double)dry, (double)drz};
             const double drn = dr[0] * n[0] + dr[1] * n[1] + dr[2] * n[2];
             const double nv = n[0] * dneg[0] + n[1] * dneg[1] + n[2] * dneg[2];
@@ -973,21 +1072,6 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
             scatter_gradient_stencil(g, P.g_smooth, tile, pc, dgv[0] * inv2h, dgv[1] * inv2h,
                                      dgv[2] * inv2h);
         }
-        __syncwarp();
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < G.total_nocam; i += blockDim.x) {
-        int a;
-        if (i < G.b1) a = GA::W1 + (i / IN) * GA::W1S + (i % IN);
-        else if (i < G.w2) a = GA::B1 + (i - G.b1);
-        else if (i < G.b2) a = GA::W2 + ((i - G.w2) >> 5) * 33 + ((i - G.w2) & 31);
-        else if (i < G.w3) a = GA::B2 + (i - G.b2);
-        else if (i < G.b3) a = GA::W3 + (i - G.w3);
-        else a = GA::B3 + (i - G.b3);
-        float v = 0.f;
-#pragma unroll
-        for (int w = 0; w < WARPS_PER_BLOCK; ++w) v += s_acc[w * GA::TOTAL + a];
-        if (v != 0.f) atomicAdd(P.g_mlp + i, v);
     }
 }
 
