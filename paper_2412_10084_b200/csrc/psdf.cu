@@ -151,6 +151,8 @@ struct psdf_ctx {
     int device = 0;
     int sm_count = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // host->device image staging of psdf_train_step
+    cudaEvent_t ev_copied = nullptr, ev_copy_free = nullptr;
     cudaEvent_t ev_ray0 = nullptr, ev_ray1 = nullptr, ev_step0 = nullptr, ev_step1 = nullptr;
 
     bool has_grid = false;
@@ -679,7 +681,7 @@ void do_render(psdf_ctx* c, const psdf_camera* cam, const psdf_render_opts* opt,
 
 // One train step over device-resident views (trainer.cpp:136-195).
 void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_step_params* hp,
-                   psdf_losses* losses, psdf_counts* counts) {
+                   psdf_losses* losses, psdf_counts* counts, cudaEvent_t images_ready = nullptr) {
     need_grid(c);
     if (!hp) fail(PSDF_ERR_INVALID_ARGUMENT, "null step parameters");
     if (batch.empty()) fail(PSDF_ERR_INVALID_ARGUMENT, "empty batch");
@@ -709,6 +711,44 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
         vd[i].cam_bias_row = hp->use_camera_bias ? camera_bias_row(c, batch[i]->cam.id) : -1;
         n_rays += (int64_t)batch[i]->cam.width * batch[i]->cam.height;
     }
+    // regularizers (trainer.cpp:187-191), sharded by tile / probe range.  They
+    // read only parameters and the smoothed grid, so they run first (under
+    // the host->device copy of the step's images when there is one) unless
+    // the ray-pass-only gradients are kept for inspection.
+    auto regularizers = [&]() {
+        const GridView g = c->view();
+        const int T = c->desc.T, Pn = c->desc.P;
+        const int t0 = (int)((int64_t)T * c->rank / c->world), t1 = (int)((int64_t)T * (c->rank + 1) / c->world);
+        const int p0 = (int)((int64_t)Pn * c->rank / c->world), p1 = (int)((int64_t)Pn * (c->rank + 1) / c->world);
+        const int stride = c->desc.sh_order * c->desc.sh_order * c->desc.n_a;
+        if (t1 > t0) {
+            static bool attr = false;
+            if (!attr) {
+                CK(cudaFuncSetAttribute(loss_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kLossGridSmem));
+                attr = true;
+            }
+            loss_grid_kernel<<<t1 - t0, LG_THREADS, kLossGridSmem, s>>>(
+                g, c->d_params + c->off_raw, t0, (float)hp->l_sdf, (float)hp->l_eik, (float)hp->l_norm,
+                (float)(1.0 / (2.0 * c->desc.voxel_size)), c->d_gsmooth, c->d_grads + c->off_raw, c->d_stats);
+            CK(cudaGetLastError());
+            loss_features_kernel<<<3 * (t1 - t0), 256, 0, s>>>(
+                g, t0, c->desc.n_s, (float)hp->l_feat, c->d_grads + c->off_planes, c->d_stats);
+            CK(cudaGetLastError());
+            c->last_launches += 2;
+        }
+        if (p1 > p0) {
+            GridMut m{g, c->d_params + c->off_raw, c->d_probe_table, c->d_probe_coords};
+            const int64_t n = (int64_t)(p1 - p0) * stride;
+            loss_probes_kernel<<<(unsigned)std::min<int64_t>(4 * c->sm_count, n / 256 + 1), 256, 0, s>>>(
+                m, p0, p1, stride, (float)hp->l_probe, c->d_grads + c->off_probes, c->d_stats);
+            CK(cudaGetLastError());
+            ++c->last_launches;
+        }
+    };
+    const bool regs_first = !c->keep_raypass;
+    if (regs_first) regularizers();
+    if (images_ready) CK(cudaStreamWaitEvent(s, images_ready, 0));
     const int64_t tiles = upload_viewdev(c, vd);
     // ray-batch data parallelism: contiguous 1/N slice of the batch's work tiles
     P.tile_begin = tiles * c->rank / c->world;
@@ -729,36 +769,7 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
         CK(cudaMemcpyAsync(c->d_gsmooth0, c->d_gsmooth, sizeof(float) * c->desc.T * TV,
                            cudaMemcpyDeviceToDevice, s));
     }
-    // regularizers (trainer.cpp:187-191), sharded by tile / probe range
-    const GridView g = c->view();
-    const int T = c->desc.T, Pn = c->desc.P;
-    const int t0 = (int)((int64_t)T * c->rank / c->world), t1 = (int)((int64_t)T * (c->rank + 1) / c->world);
-    const int p0 = (int)((int64_t)Pn * c->rank / c->world), p1 = (int)((int64_t)Pn * (c->rank + 1) / c->world);
-    const int stride = c->desc.sh_order * c->desc.sh_order * c->desc.n_a;
-    if (t1 > t0) {
-        static bool attr = false;
-        if (!attr) {
-            CK(cudaFuncSetAttribute(loss_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)kLossGridSmem));
-            attr = true;
-        }
-        loss_grid_kernel<<<t1 - t0, LG_THREADS, kLossGridSmem, s>>>(
-            g, c->d_params + c->off_raw, t0, (float)hp->l_sdf, (float)hp->l_eik, (float)hp->l_norm,
-            (float)(1.0 / (2.0 * c->desc.voxel_size)), c->d_gsmooth, c->d_grads + c->off_raw, c->d_stats);
-        CK(cudaGetLastError());
-        loss_features_kernel<<<3 * (t1 - t0), 256, 0, s>>>(
-            g, t0, c->desc.n_s, (float)hp->l_feat, c->d_grads + c->off_planes, c->d_stats);
-        CK(cudaGetLastError());
-        c->last_launches += 2;
-    }
-    if (p1 > p0) {
-        GridMut m{g, c->d_params + c->off_raw, c->d_probe_table, c->d_probe_coords};
-        const int64_t n = (int64_t)(p1 - p0) * stride;
-        loss_probes_kernel<<<(unsigned)std::min<int64_t>(4 * c->sm_count, n / 256 + 1), 256, 0, s>>>(
-            m, p0, p1, stride, (float)hp->l_probe, c->d_grads + c->off_probes, c->d_stats);
-        CK(cudaGetLastError());
-        ++c->last_launches;
-    }
+    if (!regs_first) regularizers();
     // G^T fold (grads.cpp:67-96): raw_grad += G^T * staged
     launch_fold(c, c->d_gsmooth, c->d_grads + c->off_raw);
     // all-reduce across ranks (GradBuffers::add, trainer.cpp:184-185, across GPUs)
@@ -858,6 +869,10 @@ int psdf_create(int device, psdf_ctx** out) {
         c->device = device;
         CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_copied, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_copy_free, cudaEventDisableTiming));
+        CK(cudaEventRecord(c->ev_copy_free, c->stream));
         CK(cudaEventCreate(&c->ev_ray0));
         CK(cudaEventCreate(&c->ev_ray1));
         CK(cudaEventCreate(&c->ev_step0));
@@ -899,6 +914,9 @@ int psdf_destroy(psdf_ctx* c) {
         cudaEventDestroy(c->ev_step0);
         cudaEventDestroy(c->ev_step1);
         cudaStreamDestroy(c->stream);
+        cudaStreamDestroy(c->copy_stream);
+        cudaEventDestroy(c->ev_copied);
+        cudaEventDestroy(c->ev_copy_free);
         delete c;
     });
 }
@@ -1202,12 +1220,17 @@ int psdf_train_step(psdf_ctx* c, int n_views, const psdf_camera* cams, const flo
             tmp[i].cam = cams[i];
             tmp[i].rgb = c->d_stage_rgb + 3 * off;
             tmp[i].mask = c->d_stage_mask + off;
-            CK(cudaMemcpyAsync(tmp[i].rgb, gt_rgb[i], sizeof(float) * 3 * n, cudaMemcpyHostToDevice, c->stream));
-            CK(cudaMemcpyAsync(tmp[i].mask, mask[i], n, cudaMemcpyHostToDevice, c->stream));
+            CK(cudaMemcpyAsync(tmp[i].rgb, gt_rgb[i], sizeof(float) * 3 * n, cudaMemcpyHostToDevice,
+                               c->copy_stream));
+            CK(cudaMemcpyAsync(tmp[i].mask, mask[i], n, cudaMemcpyHostToDevice, c->copy_stream));
             batch[i] = &tmp[i];
             off += n;
         }
-        do_train_step(c, batch, hp, losses, counts);
+        // the copies overlap the step's image-independent kernels (regularizers)
+        CK(cudaStreamWaitEvent(c->copy_stream, c->ev_copy_free, 0));  // staging no longer read
+        CK(cudaEventRecord(c->ev_copied, c->copy_stream));
+        do_train_step(c, batch, hp, losses, counts, c->ev_copied);
+        CK(cudaEventRecord(c->ev_copy_free, c->stream));
         tmp.clear();
     });
 }
