@@ -153,6 +153,9 @@ struct psdf_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;  // host->device image staging of psdf_train_step
     cudaEvent_t ev_copied = nullptr, ev_copy_free = nullptr;
+    std::vector<cudaEvent_t> view_ready;   // per staged view: its images are in HBM
+    int n_view_ready = 0;                  // > 0 only inside psdf_train_step
+    std::vector<int64_t> view_tiles;       // first global work tile per view (+ end)
     cudaEvent_t ev_ray0 = nullptr, ev_ray1 = nullptr, ev_step0 = nullptr, ev_step1 = nullptr;
 
     bool has_grid = false;
@@ -520,8 +523,30 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
         CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
         CK(cudaMemsetAsync(c->wave.counters, 0, sizeof(unsigned) * 4, s));
         P.work_counter = c->d_work;
-        march_scan_kernel<<<(unsigned)grid_s, BLOCK, smem_bits, s>>>(P, c->wave);
-        CK(cudaGetLastError());
+        if (c->n_view_ready == 0) {
+            P.scan_lo = 0;
+            P.scan_hi = n_work;
+            march_scan_kernel<<<(unsigned)grid_s, BLOCK, smem_bits, s>>>(P, c->wave);
+            CK(cudaGetLastError());
+        } else {
+            // psdf_train_step: each view's scan starts as soon as its images
+            // have arrived (the copies of the next views overlap it)
+            for (int v = 0; v < c->n_view_ready; ++v) {
+                const int64_t lo = std::max<int64_t>(c->view_tiles[v], P.tile_begin) - P.tile_begin;
+                const int64_t hi = std::min<int64_t>(c->view_tiles[v + 1], P.tile_end) - P.tile_begin;
+                if (hi <= lo) continue;
+                CK(cudaStreamWaitEvent(s, c->view_ready[v], 0));
+                CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
+                RayPassParams Pv = P;
+                Pv.scan_lo = lo;
+                Pv.scan_hi = hi;
+                const int64_t gv = std::max<int64_t>(1, std::min<int64_t>((hi - lo + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
+                                                                          (int64_t)per_sm_s * c->sm_count));
+                march_scan_kernel<<<(unsigned)gv, BLOCK, smem_bits, s>>>(Pv, c->wave);
+                CK(cudaGetLastError());
+                ++c->last_launches;
+            }
+        }
         CK(cudaMemcpyAsync(c->h_wave_counters + 2, c->wave.counters + 2, sizeof(unsigned),
                            cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -917,6 +942,7 @@ int psdf_destroy(psdf_ctx* c) {
         cudaStreamDestroy(c->copy_stream);
         cudaEventDestroy(c->ev_copied);
         cudaEventDestroy(c->ev_copy_free);
+        for (auto e : c->view_ready) cudaEventDestroy(e);
         delete c;
     });
 }
@@ -1215,6 +1241,13 @@ int psdf_train_step(psdf_ctx* c, int n_views, const psdf_camera* cams, const flo
         std::vector<DevView> tmp(n_views);
         std::vector<DevView*> batch(n_views);
         size_t off = 0;
+        while ((int)c->view_ready.size() < n_views) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c->view_ready.push_back(e);
+        }
+        c->view_tiles.assign(n_views + 1, 0);
+        CK(cudaStreamWaitEvent(c->copy_stream, c->ev_copy_free, 0));  // staging no longer read
         for (int i = 0; i < n_views; ++i) {
             const size_t n = (size_t)cams[i].width * cams[i].height;
             tmp[i].cam = cams[i];
@@ -1223,13 +1256,23 @@ int psdf_train_step(psdf_ctx* c, int n_views, const psdf_camera* cams, const flo
             CK(cudaMemcpyAsync(tmp[i].rgb, gt_rgb[i], sizeof(float) * 3 * n, cudaMemcpyHostToDevice,
                                c->copy_stream));
             CK(cudaMemcpyAsync(tmp[i].mask, mask[i], n, cudaMemcpyHostToDevice, c->copy_stream));
+            CK(cudaEventRecord(c->view_ready[i], c->copy_stream));
+            c->view_tiles[i + 1] = c->view_tiles[i] + (int64_t)((cams[i].width + 7) / 8) * ((cams[i].height + 3) / 4);
             batch[i] = &tmp[i];
             off += n;
         }
         // the copies overlap the step's image-independent kernels (regularizers)
-        CK(cudaStreamWaitEvent(c->copy_stream, c->ev_copy_free, 0));  // staging no longer read
+        // and, view by view, the saturated-prefix scans
         CK(cudaEventRecord(c->ev_copied, c->copy_stream));
-        do_train_step(c, batch, hp, losses, counts, c->ev_copied);
+        c->n_view_ready = n_views;
+        try {
+            do_train_step(c, batch, hp, losses, counts, nullptr);
+        } catch (...) {
+            c->n_view_ready = 0;
+            throw;
+        }
+        c->n_view_ready = 0;
+        CK(cudaStreamWaitEvent(c->stream, c->ev_copied, 0));
         CK(cudaEventRecord(c->ev_copy_free, c->stream));
         tmp.clear();
     });

@@ -60,6 +60,7 @@ struct RayPassParams {
     const ViewDev* views;
     int n_views;
     int64_t tile_begin, tile_end;  // this rank's slice of the global work tiles
+    int64_t scan_lo, scan_hi;      // K2a-scan: local work tiles [lo, hi) of this launch
     unsigned long long* work_counter;
     // render outputs (K1)
     float* out_rgb;

@@ -159,12 +159,11 @@ __global__ void __launch_bounds__(BLOCK, PSDF_SCAN_MINB) march_scan_kernel(RayPa
     double st_photo = 0.0, st_sq = 0.0;
     unsigned long long st_mask = 0;
     unsigned c_m = 0, c_x = 0, c_bwd = 0, c_ex = 0;
-    const int n_work = (int)(P.tile_end - P.tile_begin);
     for (;;) {
         int wi = 0;
-        if (lane == 0) wi = (int)atomicAdd(P.work_counter, 1ull);
+        if (lane == 0) wi = (int)(P.scan_lo + atomicAdd(P.work_counter, 1ull));
         wi = __shfl_sync(FULL, wi, 0);
-        if (wi >= n_work) break;
+        if (wi >= P.scan_hi) break;
         const LaneRay R = lane_ray(P, wi, lane);
         Marcher mr;
         int k = 0, tile_prev = -1;
