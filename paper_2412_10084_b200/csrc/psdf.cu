@@ -170,6 +170,7 @@ struct psdf_ctx {
     float* d_tile_min = nullptr;   // [T] minimum of each tile's apron brick
     float* d_block_min = nullptr;  // [T][64] minimum of each 4^3 block's brick
     int32_t* d_tile_nbr = nullptr; // [T][27] neighbour tile ids
+    int occ_tlo[3] = {0, 0, 0}, occ_thi[3] = {-1, -1, -1};  // allocated tiles' bounding box (tile coords)
     uint8_t* d_sat_dist = nullptr; // [T][64] saturation distances of the current ray pass
     int* h_keys = nullptr;         // handover sort: keys out, iota values in, CUB temp
     int* h_iota = nullptr;
@@ -233,12 +234,15 @@ struct psdf_ctx {
             g.org[a] = desc.origin[a];
             // world_max() = origin + res * voxel_size (grid.hpp:72-74)
             g.wmax[a] = desc.origin[a] + (double)desc.res[a] * desc.voxel_size;
+            g.occ_lo[a] = desc.origin[a] + (double)(occ_tlo[a] * TE - 1) * desc.voxel_size;
+            g.occ_hi[a] = desc.origin[a] + (double)((occ_thi[a] + 1) * TE + 1) * desc.voxel_size;
         }
         g.h = desc.voxel_size;
         int ex = 0;
         g.h_pow2 = desc.voxel_size > 0.0 && std::frexp(desc.voxel_size, &ex) == 0.5;
         g.inv_h = g.h_pow2 ? 1.0 / desc.voxel_size : 0.0;
         g.far = desc.far_field_voxels * desc.voxel_size;
+        g.occ_any = occ_thi[0] >= occ_tlo[0];
         g.tile_table = d_tile_table;
         g.tile_bits = d_tile_bits;
         g.tile_dist = d_tile_dist;
@@ -999,6 +1003,10 @@ int psdf_upload_grid(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_c
         c->free_grid();
         c->desc = *d;
         c->in_dim = d->n_s + d->n_a + NPOW;
+        for (int a = 0; a < 3; ++a) {
+            c->occ_tlo[a] = 0;
+            c->occ_thi[a] = -1;
+        }
         for (int a = 0; a < 3; ++a) c->nt[a] = d->res[a] / TE;
         const int64_t T = d->T, P = d->P;
         // dense tile / probe lattice tables
@@ -1014,6 +1022,10 @@ int psdf_upload_grid(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_c
             if (slot >= 0) fail(PSDF_ERR_INVALID_ARGUMENT, "duplicate tile coordinates");
             slot = (int32_t)t;
             tc4[t] = make_int4(q[0], q[1], q[2], 0);
+            for (int a = 0; a < 3; ++a) {
+                if (t == 0 || q[a] < c->occ_tlo[a]) c->occ_tlo[a] = q[a];
+                if (t == 0 || q[a] > c->occ_thi[a]) c->occ_thi[a] = q[a];
+            }
             for (int i = 0; i < 8; ++i)
                 if (probe_ids[8 * t + i] < 0 || probe_ids[8 * t + i] >= P)
                     fail(PSDF_ERR_INVALID_ARGUMENT, "probe id out of range");

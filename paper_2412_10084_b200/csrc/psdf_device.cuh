@@ -53,6 +53,8 @@ struct GridView {
     double inv_h;                  // 1 / h, used only when h is a power of two
     int h_pow2;                    // x / h == x * inv_h exactly (power-of-two h)
     double wmax[3];                // world_max() (grid.hpp:72-74)
+    double occ_lo[3], occ_hi[3];   // bounding box of the allocated tiles, one voxel margin
+    int occ_any;                   // any tile allocated
     const int32_t* __restrict__ tile_table;   // [nt0][nt1][nt2] -> tile or -1
     const uint32_t* __restrict__ tile_bits;   // occupancy bitmap of tile_table
     const uint8_t* __restrict__ tile_dist;    // L-inf distance (tiles) to the nearest allocated tile
@@ -429,6 +431,16 @@ struct Marcher {
         t1 = b.t1;
         t = dadd(b.t0, dmul(0.5, g.h));
         return true;
+    }
+
+    // false when the ray (t >= 0) misses the bounding box of the allocated
+    // tiles (with a one-voxel margin): then no lattice point lies in an
+    // allocated tile and march_ray yields no sample.  Call after init().
+    __device__ __forceinline__ bool may_hit(const GridView& g) const {
+        if (!g.occ_any) return false;
+        return ray_box(d3(o[0], o[1], o[2]), d3(d[0], d[1], d[2]), d3(inv_d[0], inv_d[1], inv_d[2]),
+                       d3(g.occ_lo[0], g.occ_lo[1], g.occ_lo[2]), d3(g.occ_hi[0], g.occ_hi[1], g.occ_hi[2]))
+            .ok;
     }
 
     // Resumes a ray whose box exit t1 is known (the caller sets t and count

@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(BLOCK) render_kernel(RayPassParams P) {
             int tile_cur = -1;
             int4 tc_cur;
             SampleRun run;
-            bool active = mr.init(g, V.cam.pos, dd, P.n_max) &&
+            bool active = mr.init(g, V.cam.pos, dd, P.n_max) && mr.may_hit(g) &&
                           mr.next_run(g, t_cur, tile_cur, bits, &tc_cur, tau_run, run);
             if (active) {
                 ++c_x;
