@@ -405,24 +405,6 @@ void prepare_sat(psdf_ctx* c, double tau_run) {
     ++c->last_launches;
 }
 
-// K1 launch (render).
-template <int NS, int NA>
-void launch_render(psdf_ctx* c, RayPassParams& P) {
-    const void* fn = (const void*)render_kernel<NS, NA>;
-    const size_t smem = render_smem_bytes<NS, NA>(P.bits_sm_words);
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t n_work = P.tile_end - P.tile_begin;
-    const int64_t warps_needed = std::max<int64_t>(n_work, 1);
-    const int per_sm = blocks_per_sm(fn, smem);
-    const int64_t grid = std::min<int64_t>((warps_needed + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
-                                           (int64_t)per_sm * c->sm_count);
-    CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), c->stream));
-    CK(cudaEventRecord(c->ev_ray0, c->stream));
-    render_kernel<NS, NA><<<(unsigned)grid, BLOCK, smem, c->stream>>>(P);
-    CK(cudaGetLastError());
-    CK(cudaEventRecord(c->ev_ray1, c->stream));
-    ++c->last_launches;
-}
 
 __global__ void iota_kernel(int* __restrict__ v, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -510,7 +492,8 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     if (c->wave.e_cap == 0) ensure_wave(c, n_rays / 8 + 65536, n_rays / 8 + 65536, n_rays / 2 + 65536);
     const size_t smem_f = render_smem_bytes<NS, NA>();
     const size_t smem_b = shade_bwd_smem_bytes<NS, NA>();
-    CK(cudaFuncSetAttribute(shade_fwd_kernel<NS, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
+    CK(cudaFuncSetAttribute(shade_fwd_kernel<NS, NA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
+    CK(cudaFuncSetAttribute(shade_fwd_kernel<NS, NA, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
     CK(cudaFuncSetAttribute(shade_bwd_kernel<NS, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
     const size_t smem_bits = sizeof(uint32_t) * P.bits_sm_words;
     CK(cudaFuncSetAttribute(march_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bits));
@@ -610,13 +593,27 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     }
     CK(cudaEventRecord(c->ev_k[1], s));
     if (n_rec > 0) {
-        const int per_sm = blocks_per_sm((const void*)shade_fwd_kernel<NS, NA>, smem_f);
+        const int per_sm = blocks_per_sm((const void*)shade_fwd_kernel<NS, NA, true>, smem_f);
         const int grid = (int)std::min<int64_t>((n_rec + BLOCK - 1) / BLOCK, (int64_t)per_sm * c->sm_count);
-        shade_fwd_kernel<NS, NA><<<grid, BLOCK, smem_f, s>>>(P, c->wave, n_rec);
+        if (P.mode == 1)  // render: no geometry records for a backward
+            shade_fwd_kernel<NS, NA, false><<<grid, BLOCK, smem_f, s>>>(P, c->wave, n_rec);
+        else
+            shade_fwd_kernel<NS, NA, true><<<grid, BLOCK, smem_f, s>>>(P, c->wave, n_rec);
         CK(cudaGetLastError());
         ++c->last_launches;
     }
     CK(cudaEventRecord(c->ev_k[2], s));
+    if (P.mode == 1) {  // render: colours of the shaded rays, no backward
+        if (n_ent > 0) {
+            render_finish_kernel<<<(unsigned)std::min<int64_t>((n_ent + BLOCK - 1) / BLOCK, 4 * c->sm_count), BLOCK, 0,
+                                   s>>>(P, c->wave, n_ent);
+            CK(cudaGetLastError());
+            ++c->last_launches;
+        }
+        for (int k = 3; k <= 4; ++k) CK(cudaEventRecord(c->ev_k[k], s));
+        CK(cudaEventRecord(c->ev_ray1, s));
+        return;
+    }
     if (n_ent > 0) {
         const int per_sm = blocks_per_sm((const void*)alpha_bwd_kernel, smem_bits);
         const int grid = (int)std::min<int64_t>((n_ent + BLOCK - 1) / BLOCK, (int64_t)per_sm * c->sm_count);
@@ -687,9 +684,13 @@ void do_render(psdf_ctx* c, const psdf_camera* cam, const psdf_render_opts* opt,
     P.out_alpha = d_alpha;
     P.out_depth = d_depth;
     CK(cudaMemsetAsync(c->d_counts, 0, sizeof(unsigned long long) * 8, c->stream));
+    CK(cudaMemsetAsync(c->d_stats, 0, sizeof(double) * 16, c->stream));
     prepare_sat(c, P.early_stop > 1.0 ? 0.0 : P.tau);
+    // K1 through the ray-pass pipeline (scan -> composite -> decode -> finish)
+    P.mode = 1;
+    const int64_t n_rays = (int64_t)cam->width * cam->height;
     dispatch_channels(c->desc.n_s, c->desc.n_a, [&]<int NS, int NA>() {
-        launch_render<NS, NA>(c, P);
+        launch_train_raypass<NS, NA>(c, P, n_rays);
     });
     if (counts) {
         CK(cudaMemcpyAsync(c->h_counts, c->d_counts, sizeof(unsigned long long) * 8,

@@ -1,16 +1,15 @@
-// psdf_raypass.cuh — the fused per-ray kernels.
+// psdf_raypass.cuh — shared pieces of the ray pass (psdf_train.cuh):
+// parameters, MLP layouts, decode_fused (renderer.cpp:88-147) as
+// decode_features + mlp_forward, and the geometry record the shading
+// backward reads.  K1 (render_image, renderer.cpp:321-337) runs through the
+// same pipeline as the train ray pass with RayPassParams::mode = 1.
 //
-//  K1 render_kernel : render_image -> render_ray -> decode_fused
-//                     (renderer.cpp:321-337, 149-210, 88-147)
-//  (K2, the train ray pass, is the wavefront pipeline in psdf_train.cuh; it
-//   shares decode_forward and the layouts below.)
-//
-// Work decomposition: one ray per lane; a warp owns an 8x4 pixel tile (so its
-// rays are coherent) and pulls tiles from a global work counter (rays vary
-// from 0 to 512 samples).  The march / alpha / compositing chain is exact f64
+// Work decomposition of the march kernels: one ray per lane; a warp owns an
+// 8x4 pixel tile (so its rays are coherent) and pulls tiles from a global
+// work counter.  The march / alpha / compositing chain is exact f64
 // (psdf_device.cuh).  Shaded samples are decoded in fp32.
 //
-// K2's backward is a second forward sweep instead of the reference's reverse
+// The backward is a second forward sweep instead of the reference's reverse
 // traversal over a cached RayWorkspace: the suffix sum of renderer.cpp:254-261
 // is rewritten as  suffix_i = Total - prefix_i  with
 //   Total = sum_k dw_k w_k = g.(c_raw - bg*acc) + dA*acc
@@ -18,12 +17,6 @@
 // restarts at the first sample with alpha > 0 (samples before it have w = 0
 // and contribute nothing), with T = 1 exactly.  The rounding error of the
 // subtraction enters ds only multiplied by (1 - alpha_i), see DESIGN.md.
-//
-// Gradient scatter: SDF (smooth-staged) and tri-plane texels by fp32 / float4
-// red.global.add; probe coefficients aggregated across the warp's shading
-// lanes that share a tile before the atomics; MLP weight gradients reduced
-// warp-cooperatively through shared memory (lane j owns output row j) into a
-// per-warp accumulator flushed once per block.
 #pragma once
 
 #include "psdf_device.cuh"
@@ -54,6 +47,7 @@ struct RayPassParams {
     int order;            // effective SH order (sh_order_override applied)
     int no_spatial, no_angular, no_fresnel, need_colors;
     int n_max;
+    int mode;             // 0: train ray pass, 1: render (K1 through the same pipeline)
     int bits_sm_words;    // words of the tile bitmap staged in shared memory (0 = use global)
     double tau, early_stop, bg[3];
     double photo_scale;
@@ -414,134 +408,9 @@ __device__ __forceinline__ void load_mlp_smem(const float* __restrict__ mlp, flo
     }
 }
 
-// ----------------------------------------------------------------------- K1
-template <int NS, int NA>
-__global__ void __launch_bounds__(BLOCK) render_kernel(RayPassParams P) {
-    constexpr int IN = NS + NA + NPOW;
-    extern __shared__ __align__(16) float smem[];
-    const SmemMlp L = SmemMlp::make(IN);
-    const MlpLayout G = MlpLayout::make(IN);
-    load_mlp_smem(P.mlp, smem, G, L);
-    const GridView& g = P.g;
-    const uint32_t* bits =
-        stage_tile_bits(g, reinterpret_cast<uint32_t*>(smem + L.total), P.bits_sm_words);
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    unsigned long long c_m = 0, c_x = 0, c_sh = 0;
-    const int n_work = (int)(P.tile_end - P.tile_begin);
-    // saturated runs skip the per-sample early-stop test, valid while the
-    // transmittance they leave unchanged is not already below the threshold
-    // (only possible for a threshold above 1)
-    const double tau_run = P.early_stop > 1.0 ? 0.0 : P.tau;
-    for (;;) {
-        int wi = 0;
-        if (lane == 0) wi = (int)atomicAdd(P.work_counter, 1ull);
-        wi = __shfl_sync(FULL, wi, 0);
-        if (wi >= n_work) break;
-        const int64_t tile_id = P.tile_begin + wi;
-        const int vi = locate_view(P, tile_id);
-        const ViewDev& V = P.views[vi];
-        const int64_t lt = tile_id - V.tile_begin;
-        const int u = (int)(lt % V.tiles_x) * 8 + (lane & 7);
-        const int vv = (int)(lt / V.tiles_x) * 4 + (lane >> 3);
-        const bool valid = u < V.cam.width && vv < V.cam.height;
-        const float* cam_row = (P.ncam > 0 && V.cam_bias_row >= 0)
-                                   ? P.mlp + G.cam + V.cam_bias_row * HID
-                                   : nullptr;
-        double c0 = 0.0, c1 = 0.0, c2 = 0.0, acc = 0.0, trans = 1.0, depth = 0.0;
-        if (valid) {
-            const D3 d = pixel_dir(V.cam, (double)u + 0.5, (double)vv + 0.5);
-            const double dd[3] = {d.x, d.y, d.z};
-            const double dneg[3] = {-d.x, -d.y, -d.z};
-            Marcher mr;
-            double t_cur = 0.0, s_cur = 0.0, a_cur = 0.0;
-            int tile_cur = -1;
-            int4 tc_cur;
-            SampleRun run;
-            bool active = mr.init(g, V.cam.pos, dd, P.n_max) && mr.may_hit(g) &&
-                          mr.next_run(g, t_cur, tile_cur, bits, &tc_cur, tau_run, run);
-            if (active) {
-                ++c_x;
-                if (run.sat) {  // saturated run: sigmoid 1, alpha 0 (kSatX)
-                    a_cur = 1.0;
-                    c_m += run.n - 1;
-                    t_cur = run.t_last;
-                } else {
-                    double pc[3];
-                    mr.pos(t_cur, pc);
-                    s_cur = sample_sdf_in(g, pc[0], pc[1], pc[2], tile_cur, tc_cur);
-                    a_cur = sigmoid_sat(dmul(P.tau, s_cur));
-                }
-            }
-            while (active) {
-                double t_nxt;
-                int tile_nxt;
-                int4 tc_nxt;
-                const bool has_next = mr.next_run(g, t_nxt, tile_nxt, bits, &tc_nxt, tau_run, run);
-                if (has_next && run.sat) {
-                    // the pending sample and the run's first n-1 settle with
-                    // alpha 0: no weight, colour, depth or transmittance change
-                    c_m += run.n;
-                    t_cur = run.t_last;
-                    tile_cur = tile_nxt;
-                    a_cur = 1.0;
-                    continue;
-                }
-                double pn[3];
-                mr.pos(has_next ? t_nxt : dadd(t_cur, g.h), pn);
-                const double s_nxt = has_next ? sample_sdf_in(g, pn[0], pn[1], pn[2], tile_nxt, tc_nxt)
-                                              : sample_sdf(g, pn[0], pn[1], pn[2]);
-                const double a_nxt = sigmoid_sat(dmul(P.tau, s_nxt));
-                const double alpha = a_nxt == 1.0 ? 0.0 : alpha_from(a_cur, a_nxt);
-                const double w = dmul(trans, alpha);
-                if (P.need_colors && w > 0.0 && tile_cur >= 0) {
-                    double pc[3];
-                    mr.pos(t_cur, pc);
-                    float rgb[3];
-                    ShadeGeo geo;
-                    decode_forward<NS, NA>(P, smem, L, tile_cur, pc, dneg, cam_row, rgb, geo,
-                                           nullptr);
-                    c0 = dadd(c0, dmul((double)rgb[0], w));
-                    c1 = dadd(c1, dmul((double)rgb[1], w));
-                    c2 = dadd(c2, dmul((double)rgb[2], w));
-                    ++c_sh;
-                }
-                acc = dadd(acc, w);
-                depth = dadd(depth, dmul(w, t_cur));
-                trans = dmul(trans, dsub(1.0, alpha));
-                ++c_m;
-                if ((P.early_stop > 0.0 && trans < P.early_stop) || !has_next) break;
-                t_cur = t_nxt;
-                tile_cur = tile_nxt;
-                s_cur = s_nxt;
-                a_cur = a_nxt;
-            }
-            const int64_t px = (int64_t)vv * V.cam.width + u;
-            const double om = dsub(1.0, acc);
-            P.out_rgb[3 * px + 0] = (float)dadd(c0, dmul(P.bg[0], om));
-            P.out_rgb[3 * px + 1] = (float)dadd(c1, dmul(P.bg[1], om));
-            P.out_rgb[3 * px + 2] = (float)dadd(c2, dmul(P.bg[2], om));
-            P.out_alpha[px] = (float)acc;
-            if (P.out_depth) P.out_depth[px] = (float)depth;
-        }
-    }
-    c_m = warp_sum_u(c_m);
-    c_x = warp_sum_u(c_x);
-    c_sh = warp_sum_u(c_sh);
-    if (lane == 0) {
-        atomicAdd(P.counts + 1, c_m);
-        atomicAdd(P.counts + 2, c_x);
-        atomicAdd(P.counts + 3, c_sh);
-    }
-}
-
 template <int NS, int NA>
 size_t render_smem_bytes() {
     return sizeof(float) * SmemMlp::make(NS + NA + NPOW).total;
-}
-template <int NS, int NA>
-size_t render_smem_bytes(int bit_words) {
-    return render_smem_bytes<NS, NA>() + sizeof(uint32_t) * bit_words;
 }
 
 }  // namespace psdf

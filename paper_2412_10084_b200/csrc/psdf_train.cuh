@@ -215,6 +215,13 @@ __global__ void __launch_bounds__(BLOCK, PSDF_SCAN_MINB) march_scan_kernel(RayPa
                 W.h_dir[3 * (int64_t)h + 2] = mr.d[2];
                 W.h_t1[h] = mr.t1;
             }
+        } else if (R.valid && P.mode == 1) {  // render: background, zero opacity and depth
+            c_m += k;
+            P.out_rgb[3 * R.px] = (float)P.bg[0];
+            P.out_rgb[3 * R.px + 1] = (float)P.bg[1];
+            P.out_rgb[3 * R.px + 2] = (float)P.bg[2];
+            P.out_alpha[R.px] = 0.f;
+            if (P.out_depth) P.out_depth[R.px] = 0.f;
         } else if (R.valid) {
             // every settle had alpha 0: acc = 0, nothing shaded, nothing to
             // back-propagate; the loss is final now
@@ -267,11 +274,12 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
         const int hi = valid ? W.h_perm[base + lane] : 0;
         const int slot = valid ? W.h_slot[hi] : 0;
         const LaneRay R = lane_ray(P, slot >> 5, slot & 31);
-        const bool in_mask = valid && __ldg(R.V->mask + R.px) != 0;
+        // train: only in-mask rays are shaded (trainer.cpp:163); render: all, if colours are wanted
+        const bool in_mask = valid && (P.mode == 1 ? P.need_colors != 0 : __ldg(R.V->mask + R.px) != 0);
         const double dd[3] = {valid ? W.h_dir[3 * (int64_t)hi] : 0.0, valid ? W.h_dir[3 * (int64_t)hi + 1] : 0.0,
                               valid ? W.h_dir[3 * (int64_t)hi + 2] : 1.0};
         Marcher mr;
-        double t_cur = 0.0, a_cur = 1.0, acc = 0.0, trans = 1.0;
+        double t_cur = 0.0, a_cur = 1.0, acc = 0.0, trans = 1.0, depth = 0.0;
         int tile_cur = -1, n_live = 0, entry = -1, prev = -1, head = -1;
         double t_first = 0.0;
         int cnt_first = -1;
@@ -377,6 +385,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
             if (alive) {
                 if (settle) {
                     acc = dadd(acc, w);
+                    if (P.mode == 1) depth = dadd(depth, dmul(w, t_cur));  // render_ray (renderer.cpp:149-210)
                     trans = dmul(trans, dsub(1.0, alpha));
                     n_live += n_settle;
                     if ((P.early_stop > 0.0 && trans < P.early_stop) || !has_next) alive = false;
@@ -402,7 +411,19 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
             W.e_craw[3 * (int64_t)entry] = 0.0;
             W.e_craw[3 * (int64_t)entry + 1] = 0.0;
             W.e_craw[3 * (int64_t)entry + 2] = 0.0;
-        } else if (valid && cnt_first < 0) {
+        }
+        if (valid && P.mode == 1) {
+            // render outputs; with shaded samples the colour is completed by
+            // render_finish after K2b (c_raw + bg (1 - acc))
+            P.out_alpha[R.px] = (float)acc;
+            if (P.out_depth) P.out_depth[R.px] = (float)depth;
+            if (head < 0) {
+                const double om = dsub(1.0, acc);
+                P.out_rgb[3 * R.px] = (float)dmul(P.bg[0], om);
+                P.out_rgb[3 * R.px + 1] = (float)dmul(P.bg[1], om);
+                P.out_rgb[3 * R.px + 2] = (float)dmul(P.bg[2], om);
+            }
+        } else if (valid && entry < 0 && cnt_first < 0) {
             // no alpha > 0 sample: acc = 0, no shaded sample, nothing to
             // back-propagate; the loss is final now
             const double om = dsub(1.0, acc);
@@ -433,6 +454,20 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
     }
 }
 
+// K1 tail: colour of every rendered ray with shaded samples, c_raw + bg (1 - acc)
+// (renderer.cpp:330-335).
+__global__ void __launch_bounds__(BLOCK) render_finish_kernel(RayPassParams P, WaveBufs W, int n_ent) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_ent; e += gridDim.x * blockDim.x) {
+        if (W.e_head[e] < 0) continue;
+        const int slot = W.e_slot[e];
+        const LaneRay R = lane_ray(P, slot >> 5, slot & 31);
+        const double om = dsub(1.0, W.e_acc[e]);
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            P.out_rgb[3 * R.px + k] = (float)dadd(W.e_craw[3 * (int64_t)e + k], dmul(P.bg[k], om));
+    }
+}
+
 // Camera-bias row of a ray entry's view.
 __device__ __forceinline__ const ViewDev& entry_view(const RayPassParams& P, const WaveBufs& W,
                                                      int e) {
@@ -441,7 +476,7 @@ __device__ __forceinline__ const ViewDev& entry_view(const RayPassParams& P, con
 }
 
 // ------------------------------------------------------------------ K2b
-template <int NS, int NA>
+template <int NS, int NA, bool GEO>
 __global__ void __launch_bounds__(BLOCK) shade_fwd_kernel(RayPassParams P, WaveBufs W, int n_rec) {
     constexpr int IN = NS + NA + NPOW;
     extern __shared__ __align__(16) float smem[];
@@ -462,7 +497,7 @@ __global__ void __launch_bounds__(BLOCK) shade_fwd_kernel(RayPassParams P, WaveB
         float rgb[3];
         ShadeGeo geo;
         decode_forward<NS, NA>(P, smem, L, W.r_tile[i], pc, dneg, cam_row, rgb, geo,
-                               W.r_geo + (int64_t)i * GeoRec<NS, NA>::STRIDE);
+                               GEO ? W.r_geo + (int64_t)i * GeoRec<NS, NA>::STRIDE : nullptr);
         reinterpret_cast<float4*>(W.r_c)[i] = make_float4(rgb[0], rgb[1], rgb[2], 0.f);
         const double w = W.r_w[i];
         atomicAdd(W.e_craw + 3 * (int64_t)e, dmul((double)rgb[0], w));
