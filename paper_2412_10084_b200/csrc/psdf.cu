@@ -140,6 +140,14 @@ void dispatch_channels(int ns, int na, F&& f) {
     else fail(PSDF_ERR_INVALID_ARGUMENT, "unsupported (n_s, n_a) = (%d, %d)", ns, na);
 }
 
+template <class F>
+void dispatch_ns(int ns, F&& f) {
+    if (ns == 2) f.template operator()<2>();
+    else if (ns == 4) f.template operator()<4>();
+    else if (ns == 8) f.template operator()<8>();
+    else fail(PSDF_ERR_INVALID_ARGUMENT, "unsupported n_s = %d", ns);
+}
+
 int64_t up4(int64_t x) { return (x + 3) & ~int64_t(3); }
 
 // Tile bitmaps up to 32 KB (1024^3 grids) are staged in shared memory.
@@ -762,8 +770,10 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
                 g, c->d_params + c->off_raw, t0, (float)hp->l_sdf, (float)hp->l_eik, (float)hp->l_norm,
                 (float)(1.0 / (2.0 * c->desc.voxel_size)), c->d_gsmooth, c->d_grads + c->off_raw, c->d_stats);
             CK(cudaGetLastError());
-            loss_features_kernel<<<3 * (t1 - t0), 256, 0, s>>>(
-                g, t0, c->desc.n_s, (float)hp->l_feat, c->d_grads + c->off_planes, c->d_stats);
+            dispatch_ns(c->desc.n_s, [&]<int NS>() {
+                loss_features_kernel<NS><<<3 * (t1 - t0), 256, 0, s>>>(g, t0, (float)hp->l_feat,
+                                                                       c->d_grads + c->off_planes, c->d_stats);
+            });
             CK(cudaGetLastError());
             c->last_launches += 2;
         }

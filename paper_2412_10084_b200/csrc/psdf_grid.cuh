@@ -520,51 +520,49 @@ __global__ void __launch_bounds__(LG_THREADS, 2) loss_grid_kernel(GridView g, co
     block_add_f64v<6>(dst, acc, red);
 }
 
-// K5: loss_features (losses.cpp:222-257); block = one (tile, plane), one
-// thread per texel channel, gathering the pair terms it belongs to (no
+// K5: loss_features (losses.cpp:222-257); block = one (tile, plane), thread =
+// one texel with its NS channels, gathering the pair terms it belongs to (no
 // atomics: the plane's gradient is owned by this block).
-__global__ void __launch_bounds__(256) loss_features_kernel(GridView g, int t0, int n_s,
-                                                            float lambda,
+template <int NS>
+__global__ void __launch_bounds__(256) loss_features_kernel(GridView g, int t0, float lambda,
                                                             float* __restrict__ g_planes,
                                                             double* stats) {
+    __shared__ __align__(16) float pl[256 * NS];
     __shared__ double red[8];
     const int t = t0 + blockIdx.x / 3, q = blockIdx.x % 3;
-    const int n = 256 * n_s;
-    const float* p = g.planes + ((int64_t)t * 3 + q) * n;
-    float* gp = g_planes + ((int64_t)t * 3 + q) * n;
-    double pl = 0.0, wt = 0.0;
-    auto term = [&](int i0, int i1, float& d, float& w) {
-        d = p[i1] - p[i0];
-        const float a0 = fabsf(p[i0]), a1 = fabsf(p[i1]);
-        w = 1.f / ((a0 > a1 ? a0 : a1) + (float)kPhotoEps);
+    const float* p = g.planes + ((int64_t)t * 3 + q) * 256 * NS;
+    float* gp = g_planes + ((int64_t)t * 3 + q) * 256 * NS;
+    for (int i = threadIdx.x; i < 64 * NS; i += blockDim.x)
+        reinterpret_cast<float4*>(pl)[i] = __ldg(reinterpret_cast<const float4*>(p) + i);
+    __syncthreads();
+    const int ab = threadIdx.x, a = ab >> 4, b = ab & 15;
+    float pw = 0.f, ww = 0.f;  // this texel's share of the loss (pairs it starts)
+    float gsum[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) gsum[k] = 0.f;
+    auto pair = [&](int i0, int i1, bool starts, float sign) {
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            const float v0 = pl[i0 * NS + k], v1 = pl[i1 * NS + k];
+            const float d = v1 - v0;
+            const float a0 = fabsf(v0), a1 = fabsf(v1);
+            const float w = __frcp_rn((a0 > a1 ? a0 : a1) + (float)kPhotoEps);
+            if (starts) {
+                pw += lambda * d * d;
+                ww += lambda * w * d * d;
+            }
+            gsum[k] += sign * 2.f * lambda * w * d;
+        }
     };
-    for (int i0 = threadIdx.x; i0 < n; i0 += blockDim.x) {
-        const int ab = i0 / n_s, k = i0 % n_s, a = ab >> 4, b = ab & 15;
-        float gsum = 0.f, d, w;
-        if (a + 1 < 16) {  // pair (i0, (a+1, b)): loss counted here, -g to i0
-            term(i0, ((a + 1) * 16 + b) * n_s + k, d, w);
-            pl += (double)(lambda * d * d);
-            wt += (double)(lambda * w * d * d);
-            gsum -= 2.f * lambda * w * d;
-        }
-        if (b + 1 < 16) {  // pair (i0, (a, b+1))
-            term(i0, (a * 16 + b + 1) * n_s + k, d, w);
-            pl += (double)(lambda * d * d);
-            wt += (double)(lambda * w * d * d);
-            gsum -= 2.f * lambda * w * d;
-        }
-        if (a >= 1) {  // pair ((a-1, b), i0): +g to i0
-            term(((a - 1) * 16 + b) * n_s + k, i0, d, w);
-            gsum += 2.f * lambda * w * d;
-        }
-        if (b >= 1) {  // pair ((a, b-1), i0)
-            term((a * 16 + b - 1) * n_s + k, i0, d, w);
-            gsum += 2.f * lambda * w * d;
-        }
-        if (gsum != 0.f) gp[i0] += gsum;
-    }
-    block_add_f64(stats + 6, pl, red);
-    block_add_f64(stats + 11, wt, red);
+    if (a + 1 < 16) pair(ab, ab + 16, true, -1.f);   // pair (i0, (a+1, b)): loss counted here, -g to i0
+    if (b + 1 < 16) pair(ab, ab + 1, true, -1.f);    // pair (i0, (a, b+1))
+    if (a >= 1) pair(ab - 16, ab, false, 1.f);       // pair ((a-1, b), i0): +g to i0
+    if (b >= 1) pair(ab - 1, ab, false, 1.f);        // pair ((a, b-1), i0)
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+        if (gsum[k] != 0.f) gp[ab * NS + k] += gsum[k];
+    block_add_f64(stats + 6, (double)pw, red);
+    block_add_f64(stats + 11, (double)ww, red);
 }
 
 // K6: loss_probes (losses.cpp:259-283) over probes [p0, p1); one thread per
