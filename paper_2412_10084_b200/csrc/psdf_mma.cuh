@@ -1,0 +1,102 @@
+// psdf_mma.cuh — warp-level tensor-core GEMM helpers for the decoder MLP
+// (2 x 32 hidden, decoder.hpp:17-31) on shading-record batches of 32.
+//
+// mma.sync m16n8k8 TF32 with the 3xTF32 split (x = hi + lo, both TF32;
+// a b ~ a_hi b_hi + a_hi b_lo + a_lo b_hi, fp32 accumulate): fp32-level
+// accuracy (~1e-6 relative) from the tensor pipe, which the decoder's
+// 1e-4 colour / 1e-3 gradient tolerances need (plain TF32 is ~5e-4).
+//
+// Fragment layouts (PTX ISA, mma.m16n8k8 .tf32): g = lane / 4, t = lane % 4;
+//   A (16x8, row): a0 (g, t), a1 (g+8, t), a2 (g, t+4), a3 (g+8, t+4)
+//   B (8x8,  col): b0 (k=t, n=g), b1 (k=t+4, n=g)
+//   C (16x8):      c0 (g, 2t), c1 (g, 2t+1), c2 (g+8, 2t), c3 (g+8, 2t+1)
+#pragma once
+
+#include <cstdint>
+
+namespace psdf {
+
+__device__ __forceinline__ uint32_t tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ void mma_tf32(float c[4], const uint32_t a[4], const uint32_t b[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+struct Split4 {
+    uint32_t hi[4], lo[4];
+};
+struct Split2 {
+    uint32_t hi[2], lo[2];
+};
+template <int N, class S>
+__device__ __forceinline__ void split(const float* v, S& s) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        s.hi[i] = tf32(v[i]);
+        s.lo[i] = tf32(v[i] - __uint_as_float(s.hi[i]));
+    }
+}
+
+// C[MT*16 x NT*8] += A(m, k) B(n, k) over k in [0, KT*8); A and B are element
+// accessors (m, k) -> float and (n, k) -> float.
+template <int MT, int NT, int KT, class FA, class FB>
+__device__ __forceinline__ void warp_gemm3(float (&c)[MT][NT][4], FA A, FB B) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) {
+        const int k0 = kt * 8;
+        Split4 a[MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            const int m0 = mt * 16;
+            const float v[4] = {A(m0 + g, k0 + t), A(m0 + g + 8, k0 + t), A(m0 + g, k0 + t + 4),
+                                A(m0 + g + 8, k0 + t + 4)};
+            split<4>(v, a[mt]);
+        }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            const int n0 = nt * 8;
+            const float v[2] = {B(n0 + g, k0 + t), B(n0 + g, k0 + t + 4)};
+            Split2 b;
+            split<2>(v, b);
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                mma_tf32(c[mt][nt], a[mt].lo, b.hi);
+                mma_tf32(c[mt][nt], a[mt].hi, b.lo);
+                mma_tf32(c[mt][nt], a[mt].hi, b.hi);
+            }
+        }
+    }
+}
+
+// Visits every C element held by this lane: f(m, n, value&).
+template <int MT, int NT, class F>
+__device__ __forceinline__ void for_c(float (&c)[MT][NT][4], F f) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) f(mt * 16 + g + ((i >> 1) << 3), nt * 8 + 2 * t + (i & 1), c[mt][nt][i]);
+}
+
+template <int MT, int NT>
+__device__ __forceinline__ void zero_c(float (&c)[MT][NT][4]) {
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) c[mt][nt][i] = 0.f;
+}
+
+}  // namespace psdf

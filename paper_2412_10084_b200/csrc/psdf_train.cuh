@@ -30,6 +30,7 @@
 // (1 - alpha_i).
 #pragma once
 
+#include "psdf_mma.cuh"
 #include "psdf_raypass.cuh"
 
 #ifndef PSDF_MARCH_MINB
@@ -632,260 +633,246 @@ struct FgDims {
 };
 
 // ------------------------------------------------------------------ K2e
+// decode_backward's MLP half (decoder.cpp:111-176) for batches of 32 shading
+// records per warp (tile order), every product on the tensor cores
+// (psdf_mma.cuh, 3xTF32): the forward is recomputed (A1 = relu(X W1^T + b1),
+// A2 = relu(A1 W2^T + b2)), then DZ2 = (DZ3 W3) [A2 > 0], DZ1 = (DZ2 W2) [A1 > 0],
+// DIN = DZ1 W1 and the weight gradients dW3 += DZ3^T A2, dW2 += DZ2^T A1,
+// dW1 += DZ1^T X into per-warp accumulators (C fragments kept in shared
+// memory), flushed once per block.  Rows of non-shading lanes are zero.
+template <int IN>
+struct MmaDims {
+    static constexpr int K1 = (IN + 7) & ~7;  // input width padded to the MMA k step
+    static constexpr int XS = K1 + 4;         // row stride of X / W1 (conflict-free fragments)
+    static constexpr int HS = 36;             // row stride of 32-wide rows
+    static constexpr int DS = 12;             // row stride of DZ3 (8 used)
+    // shared MLP copy
+    static constexpr int W1 = 0;              // [32][XS]   W1, zero padded
+    static constexpr int W1T = W1 + 32 * XS;  // [K1][HS]   W1^T
+    static constexpr int W2 = W1T + K1 * HS;  // [32][HS]
+    static constexpr int W2T = W2 + 32 * HS;  // [32][HS]   W2^T
+    static constexpr int W3 = W2T + 32 * HS;  // [8][HS]    rows 3..7 zero
+    static constexpr int B1 = W3 + 8 * HS, B2 = B1 + 32, B3 = B2 + 32;
+    static constexpr int MLP = B3 + 4;
+    // per-warp scratch
+    static constexpr int SX = 0;                // [32][XS]  X, later DIN
+    static constexpr int SA1 = SX + 32 * XS;    // [32][HS]  A1, later DZ1
+    static constexpr int SA2 = SA1 + 32 * HS;   // [32][HS]  A2, later DZ2
+    static constexpr int SD3 = SA2 + 32 * HS;   // [32][DS]  DZ3
+    static constexpr int SCR = SD3 + 32 * DS;
+    // per-warp gradient accumulators
+    static constexpr int GW1 = 0;               // [32][XS]
+    static constexpr int GW2 = GW1 + 32 * XS;   // [32][HS]
+    static constexpr int GW3 = GW2 + 32 * HS;   // [3][HS]
+    static constexpr int GB1 = GW3 + 3 * HS, GB2 = GB1 + 32, GB3 = GB2 + 32;
+    static constexpr int GACC = (GB3 + 4 + 3) & ~3;
+};
+
 template <int NS, int NA>
 __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveBufs W, int n_rec) {
     constexpr int IN = NS + NA + NPOW;
-    using SD = ScratchDims<IN>;
-    using GA = GAccDims<IN>;
+    using D = MmaDims<IN>;
+    using GR = GeoRec<NS, NA>;
     extern __shared__ __align__(16) float smem[];
-    const SmemMlp L = SmemMlp::make(IN);
     const MlpLayout G = MlpLayout::make(IN);
-    float* s_mlp = smem;
-    float* s_acc = smem + L.total;  // [WARPS_PER_BLOCK][GA::TOTAL]
+    float* sm = smem;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* s_accw = s_acc + warp * GA::TOTAL;
-    float* scr = s_acc + WARPS_PER_BLOCK * GA::TOTAL + warp * SD::TOTAL;
-    float* A1 = scr + SD::A1;
-    float* A2 = scr + SD::A2;
-    float* X = scr + SD::X;
-    float* D3s = scr + SD::D3;
-    load_mlp_smem(P.mlp, s_mlp, G, L);
-    for (int i = threadIdx.x; i < WARPS_PER_BLOCK * GA::TOTAL; i += blockDim.x) s_acc[i] = 0.f;
+    float* gacc = smem + D::MLP + warp * D::GACC;
+    float* scr = smem + D::MLP + WARPS_PER_BLOCK * D::GACC + warp * D::SCR;
+    __shared__ int s_cam[WARPS_PER_BLOCK][32];
+    int* cam = s_cam[warp];
+    // MLP into shared memory: padded W1 / W1^T / W2 / W2^T / W3, biases
+    for (int i = threadIdx.x; i < D::MLP; i += blockDim.x) sm[i] = 0.f;
     __syncthreads();
-    const GridView& g = P.g;
+    for (int i = threadIdx.x; i < 32 * IN; i += blockDim.x) {
+        const int j = i / IN, k = i % IN;
+        const float v = __ldg(P.mlp + G.w1 + i);
+        sm[D::W1 + j * D::XS + k] = v;
+        sm[D::W1T + k * D::HS + j] = v;
+    }
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
+        const float v = __ldg(P.mlp + G.w2 + i);
+        sm[D::W2 + (i >> 5) * D::HS + (i & 31)] = v;
+        sm[D::W2T + (i & 31) * D::HS + (i >> 5)] = v;
+    }
+    for (int i = threadIdx.x; i < 96; i += blockDim.x) sm[D::W3 + (i >> 5) * D::HS + (i & 31)] = __ldg(P.mlp + G.w3 + i);
+    for (int i = threadIdx.x; i < 32; i += blockDim.x) {
+        sm[D::B1 + i] = __ldg(P.mlp + G.b1 + i);
+        sm[D::B2 + i] = __ldg(P.mlp + G.b2 + i);
+    }
+    for (int i = threadIdx.x; i < WARPS_PER_BLOCK * D::GACC; i += blockDim.x) smem[D::MLP + i] = 0.f;
+    __syncthreads();
+    const float* cam_base = P.mlp + G.cam;
+    float* X = scr + D::SX;
+    float* A1 = scr + D::SA1;
+    float* A2 = scr + D::SA2;
+    float* D3 = scr + D::SD3;
     const int warps_total = gridDim.x * WARPS_PER_BLOCK;
     for (int base = (blockIdx.x * WARPS_PER_BLOCK + warp) * 32; base < n_rec; base += warps_total * 32) {
         const bool in_range = base + lane < n_rec;
         const int i = in_range ? W.r_perm[base + lane] : 0;
         float4 up = make_float4(0.f, 0.f, 0.f, 0.f);
-        int e = -1, tile = -1, cam_bias_row = -1;
+        int cam_row = -1;
         if (in_range) {
             up = reinterpret_cast<const float4*>(W.r_up)[i];
-            e = W.r_entry[i];
-            tile = W.r_tile[i];
-            if (P.ncam > 0) cam_bias_row = entry_view(P, W, e).cam_bias_row;
+            if (P.ncam > 0) cam_row = entry_view(P, W, W.r_entry[i]).cam_bias_row;
         }
         const bool shade = in_range && (up.x != 0.f || up.y != 0.f || up.z != 0.f);
         const unsigned smask = __ballot_sync(FULL, shade);
         if (!smask) continue;
-        double pc[3] = {0, 0, 0}, dneg[3] = {0, 0, 0};
-        float rgb[3] = {0.f, 0.f, 0.f};
-        ShadeGeo geo;
-        float pv[3][NS];
-        if (shade) {
-            using GR = GeoRec<NS, NA>;
-            pc[0] = W.r_pos[3 * (int64_t)i];
-            pc[1] = W.r_pos[3 * (int64_t)i + 1];
-            pc[2] = W.r_pos[3 * (int64_t)i + 2];
-            dneg[0] = -W.e_dir[3 * (int64_t)e];
-            dneg[1] = -W.e_dir[3 * (int64_t)e + 1];
-            dneg[2] = -W.e_dir[3 * (int64_t)e + 2];
-            // geometry and features of the forward decode (stored by K2b)
-            float r[GR::STRIDE];
-            const float4* src = reinterpret_cast<const float4*>(W.r_geo + (int64_t)i * GR::STRIDE);
+        // row `lane` of X and DZ3 (zero for non-shading lanes)
+        float ndv = 0.f;
+        {
+            float x[D::K1];
 #pragma unroll
-            for (int q = 0; q < GR::STRIDE / 4; ++q) {
-                const float4 v4 = src[q];
-                r[4 * q] = v4.x;
-                r[4 * q + 1] = v4.y;
-                r[4 * q + 2] = v4.z;
-                r[4 * q + 3] = v4.w;
+            for (int q = 0; q < D::K1; ++q) x[q] = 0.f;
+            float d3[3] = {0.f, 0.f, 0.f};
+            if (shade) {
+                const float* rg = W.r_geo + (int64_t)i * GR::STRIDE;
+#pragma unroll
+                for (int q = 0; q < IN; ++q) x[q] = rg[GR::X + q];
+                ndv = rg[7];
+                const float4 cr = reinterpret_cast<const float4*>(W.r_c)[i];
+                d3[0] = up.x * cr.x * (1.f - cr.x);  // sigmoid'
+                d3[1] = up.y * cr.y * (1.f - cr.y);
+                d3[2] = up.z * cr.z * (1.f - cr.z);
             }
-            geo.n[0] = r[0];
-            geo.n[1] = r[1];
-            geo.n[2] = r[2];
-            geo.glen = r[3];
-            geo.refl[0] = r[4];
-            geo.refl[1] = r[5];
-            geo.refl[2] = r[6];
-            geo.ndv = r[7];
-            const int packed = __float_as_int(r[11]);
-            geo.tx = Tap{packed & 15, r[8]};
-            geo.ty = Tap{(packed >> 4) & 15, r[9]};
-            geo.tz = Tap{(packed >> 8) & 15, r[10]};
-            geo.degenerate = (packed >> 12) & 1;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) geo.w8[c] = r[12 + c];
+            for (int q = 0; q < D::K1; ++q) X[lane * D::XS + q] = x[q];
 #pragma unroll
-            for (int q = 0; q < 3; ++q)
-#pragma unroll
-                for (int k = 0; k < NS; ++k) pv[q][k] = r[GR::PV + q * NS + k];
-            float x[IN];
-#pragma unroll
-            for (int q = 0; q < IN; ++q) {
-                x[q] = r[GR::X + q];
-                X[lane * SD::XS + q] = x[q];
-            }
-            const float4 cr = reinterpret_cast<const float4*>(W.r_c)[i];
-            rgb[0] = cr.x;
-            rgb[1] = cr.y;
-            rgb[2] = cr.z;
-            // the MLP forward is recomputed (its activations are not stored)
-            const float* cam_row = cam_bias_row >= 0 ? P.mlp + G.cam + cam_bias_row * HID : nullptr;
-            float rgb2[3];
-            mlp_forward<IN>(s_mlp, L, x, cam_row, rgb2, A1 + lane * RS, A2 + lane * RS);
+            for (int q = 0; q < 8; ++q) D3[lane * D::DS + q] = q < 3 ? d3[q] : 0.f;
+            cam[lane] = shade ? cam_row : -1;
         }
-        // ---- decode_backward (decoder.cpp:111-176), warp-cooperative
-        float dz3[3];
-        if (shade) {
-            const float upv[3] = {up.x, up.y, up.z};
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                dz3[j] = upv[j] * rgb[j] * (1.f - rgb[j]);
-                D3s[lane * 4 + j] = dz3[j];
+        __syncwarp();
+        // A1 = relu(X W1^T + b1 (+ camera bias))
+        {
+            float c[2][4][4];
+            zero_c(c);
+            warp_gemm3<2, 4, D::K1 / 8>(
+                c, [&](int m, int k) { return X[m * D::XS + k]; },
+                [&](int n, int k) { return sm[D::W1 + n * D::XS + k]; });
+            for_c(c, [&](int m, int n, float& v) {
+                float z = v + sm[D::B1 + n];
+                if (cam[m] >= 0) z += __ldg(cam_base + cam[m] * HID + n);
+                A1[m * D::HS + n] = z > 0.f ? z : 0.f;
+            });
+        }
+        __syncwarp();
+        // A2 = relu(A1 W2^T + b2)
+        {
+            float c[2][4][4];
+            zero_c(c);
+            warp_gemm3<2, 4, 4>(
+                c, [&](int m, int k) { return A1[m * D::HS + k]; },
+                [&](int n, int k) { return sm[D::W2 + n * D::HS + k]; });
+            for_c(c, [&](int m, int n, float& v) {
+                const float z = v + sm[D::B2 + n];
+                A2[m * D::HS + n] = z > 0.f ? z : 0.f;
+            });
+        }
+        __syncwarp();
+        // dW3 += DZ3^T A2 (rows 0..2 of one 16-row tile), db3
+        {
+            float c[1][4][4];
+            zero_c(c);
+            warp_gemm3<1, 4, 4>(
+                c, [&](int m, int k) { return m < 3 ? D3[k * D::DS + m] : 0.f; },
+                [&](int n, int k) { return A2[k * D::HS + n]; });
+            for_c(c, [&](int m, int n, float& v) {
+                if (m < 3) gacc[D::GW3 + m * D::HS + n] += v;
+            });
+            if (lane < 3) {
+                float s = 0.f;
+                for (int r = 0; r < 32; ++r) s += D3[r * D::DS + lane];
+                gacc[D::GB3 + lane] += s;
             }
         }
         __syncwarp();
-        {  // stage A: dW3, db3 (lane = column i)
-            float a3[3] = {0.f, 0.f, 0.f}, bsum = 0.f;
-            for (unsigned m = smask; m; m &= m - 1) {
-                const int s = __ffs(m) - 1;
-                const float av = A2[s * RS + lane];
-#pragma unroll
-                for (int j = 0; j < 3; ++j) a3[j] += D3s[s * 4 + j] * av;
-                if (lane < 3) bsum += D3s[s * 4 + lane];
-            }
-#pragma unroll
-            for (int j = 0; j < 3; ++j) s_accw[GA::W3 + j * 32 + lane] += a3[j];
-            if (lane < 3) s_accw[GA::B3 + lane] += bsum;
-        }
-        float dz[HID];
-        if (shade) {  // dz2 = (W3^T dz3) * [a2 > 0]
-#pragma unroll
-            for (int q = 0; q < HID; ++q) dz[q] = 0.f;
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                const float4* row = reinterpret_cast<const float4*>(s_mlp + L.w3 + j * HID);
-#pragma unroll
-                for (int q = 0; q < HID / 4; ++q) {
-                    const float4 wv = row[q];
-                    dz[4 * q] += wv.x * dz3[j];
-                    dz[4 * q + 1] += wv.y * dz3[j];
-                    dz[4 * q + 2] += wv.z * dz3[j];
-                    dz[4 * q + 3] += wv.w * dz3[j];
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < HID / 4; ++q) {
-                const float4 a = reinterpret_cast<const float4*>(A2 + lane * RS)[q];
-                dz[4 * q] = a.x > 0.f ? dz[4 * q] : 0.f;
-                dz[4 * q + 1] = a.y > 0.f ? dz[4 * q + 1] : 0.f;
-                dz[4 * q + 2] = a.z > 0.f ? dz[4 * q + 2] : 0.f;
-                dz[4 * q + 3] = a.w > 0.f ? dz[4 * q + 3] : 0.f;
-            }
+        // DZ2 = (DZ3 W3) [A2 > 0]  (in place of A2)
+        {
+            float c[2][4][4];
+            zero_c(c);
+            warp_gemm3<2, 4, 1>(
+                c, [&](int m, int k) { return D3[m * D::DS + k]; },
+                [&](int n, int k) { return sm[D::W3 + k * D::HS + n]; });
+            __syncwarp();
+            for_c(c, [&](int m, int n, float& v) {
+                float& a = A2[m * D::HS + n];
+                a = a > 0.f ? v : 0.f;
+            });
         }
         __syncwarp();
-        if (shade) {
-#pragma unroll
-            for (int q = 0; q < HID / 4; ++q)
-                reinterpret_cast<float4*>(A2 + lane * RS)[q] =
-                    make_float4(dz[4 * q], dz[4 * q + 1], dz[4 * q + 2], dz[4 * q + 3]);
+        // dW2 += DZ2^T A1, db2
+        {
+            float c[2][4][4];
+            zero_c(c);
+            warp_gemm3<2, 4, 4>(
+                c, [&](int m, int k) { return A2[k * D::HS + m]; },
+                [&](int n, int k) { return A1[k * D::HS + n]; });
+            for_c(c, [&](int m, int n, float& v) { gacc[D::GW2 + m * D::HS + n] += v; });
+            float s = 0.f;
+            for (int r = 0; r < 32; ++r) s += A2[r * D::HS + lane];
+            gacc[D::GB2 + lane] += s;
         }
         __syncwarp();
-        {  // stage B: dW2 row j = lane, db2
-            float accr[HID];
-#pragma unroll
-            for (int q = 0; q < HID; ++q) accr[q] = 0.f;
-            float bsum = 0.f;
-            for (unsigned m = smask; m; m &= m - 1) {
-                const int s = __ffs(m) - 1;
-                const float d = A2[s * RS + lane];
-                bsum += d;
-                const float4* arow = reinterpret_cast<const float4*>(A1 + s * RS);
-#pragma unroll
-                for (int q = 0; q < HID / 4; ++q) {
-                    const float4 a = arow[q];
-                    accr[4 * q] += d * a.x;
-                    accr[4 * q + 1] += d * a.y;
-                    accr[4 * q + 2] += d * a.z;
-                    accr[4 * q + 3] += d * a.w;
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < HID; ++q) s_accw[GA::W2 + lane * 33 + q] += accr[q];
-            s_accw[GA::B2 + lane] += bsum;
-        }
-        if (shade) {  // dz1 = (W2^T dz2) * [a1 > 0]
-            float da1[HID];
-#pragma unroll
-            for (int q = 0; q < HID; ++q) da1[q] = 0.f;
-#pragma unroll
-            for (int j = 0; j < HID; ++j) {
-                const float dj = dz[j];
-                const float4* row = reinterpret_cast<const float4*>(s_mlp + L.w2 + j * HID);
-#pragma unroll
-                for (int q = 0; q < HID / 4; ++q) {
-                    const float4 wv = row[q];
-                    da1[4 * q] += wv.x * dj;
-                    da1[4 * q + 1] += wv.y * dj;
-                    da1[4 * q + 2] += wv.z * dj;
-                    da1[4 * q + 3] += wv.w * dj;
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < HID / 4; ++q) {
-                const float4 a = reinterpret_cast<const float4*>(A1 + lane * RS)[q];
-                dz[4 * q] = a.x > 0.f ? da1[4 * q] : 0.f;
-                dz[4 * q + 1] = a.y > 0.f ? da1[4 * q + 1] : 0.f;
-                dz[4 * q + 2] = a.z > 0.f ? da1[4 * q + 2] : 0.f;
-                dz[4 * q + 3] = a.w > 0.f ? da1[4 * q + 3] : 0.f;
-            }
+        // DZ1 = (DZ2 W2) [A1 > 0]  (in place of A1)
+        {
+            float c[2][4][4];
+            zero_c(c);
+            warp_gemm3<2, 4, 4>(
+                c, [&](int m, int k) { return A2[m * D::HS + k]; },
+                [&](int n, int k) { return sm[D::W2T + n * D::HS + k]; });
+            __syncwarp();
+            for_c(c, [&](int m, int n, float& v) {
+                float& a = A1[m * D::HS + n];
+                a = a > 0.f ? v : 0.f;
+            });
         }
         __syncwarp();
-        if (shade) {
-#pragma unroll
-            for (int q = 0; q < HID / 4; ++q)
-                reinterpret_cast<float4*>(A1 + lane * RS)[q] =
-                    make_float4(dz[4 * q], dz[4 * q + 1], dz[4 * q + 2], dz[4 * q + 3]);
-        }
-        __syncwarp();
-        {  // stage C: dW1 row j = lane, db1, camera bias (grouped by camera row)
-            float accr[IN];
-#pragma unroll
-            for (int q = 0; q < IN; ++q) accr[q] = 0.f;
-            float bsum = 0.f;
-            for (unsigned m = smask; m; m &= m - 1) {
-                const int s = __ffs(m) - 1;
-                const float d = A1[s * RS + lane];
-                bsum += d;
-#pragma unroll
-                for (int q = 0; q < IN; ++q) accr[q] += d * X[s * SD::XS + q];
-            }
-#pragma unroll
-            for (int q = 0; q < IN; ++q) s_accw[GA::W1 + lane * GA::W1S + q] += accr[q];
-            s_accw[GA::B1 + lane] += bsum;
+        // dW1 += DZ1^T X, db1, camera-bias rows (grouped by camera row)
+        {
+            float c[2][D::K1 / 8][4];
+            zero_c(c);
+            warp_gemm3<2, D::K1 / 8, 4>(
+                c, [&](int m, int k) { return A1[k * D::HS + m]; },
+                [&](int n, int k) { return X[k * D::XS + n]; });
+            for_c(c, [&](int m, int n, float& v) { gacc[D::GW1 + m * D::XS + n] += v; });
+            float s = 0.f;
+            for (int r = 0; r < 32; ++r) s += A1[r * D::HS + lane];
+            gacc[D::GB1 + lane] += s;
             if (P.ncam > 0) {
-                unsigned rem = __ballot_sync(FULL, shade && cam_bias_row >= 0);
+                const int my = cam[lane];
+                unsigned rem = __ballot_sync(FULL, my >= 0);
                 while (rem) {
-                    const int row = __shfl_sync(FULL, cam_bias_row, __ffs(rem) - 1);
-                    const unsigned grp = __ballot_sync(FULL, ((rem >> lane) & 1u) && cam_bias_row == row);
+                    const int row = __shfl_sync(FULL, my, __ffs(rem) - 1);
+                    const unsigned grp = __ballot_sync(FULL, ((rem >> lane) & 1u) && my == row);
                     rem &= ~grp;
                     float cs = 0.f;
-                    for (unsigned m = grp; m; m &= m - 1) cs += A1[(__ffs(m) - 1) * RS + lane];
+                    for (unsigned m = grp; m; m &= m - 1) cs += A1[(__ffs(m) - 1) * D::HS + lane];
                     if (cs != 0.f) atomicAdd(P.g_mlp + G.cam + row * HID + lane, cs);
                 }
             }
         }
-        float gfs[NS], gfa[NA], d_ndotv = 0.f;
-        float drx = 0.f, dry = 0.f, drz = 0.f;
-        if (shade) {  // din = W1^T dz1
-            float din[IN];
+        __syncwarp();
+        // DIN = DZ1 W1  (into X)
+        {
+            float c[2][D::K1 / 8][4];
+            zero_c(c);
+            warp_gemm3<2, D::K1 / 8, 4>(
+                c, [&](int m, int k) { return A1[m * D::HS + k]; },
+                [&](int n, int k) { return sm[D::W1T + n * D::HS + k]; });
+            __syncwarp();
+            for_c(c, [&](int m, int n, float& v) { X[m * D::XS + n] = v; });
+        }
+        __syncwarp();
+        if (shade) {  // feature gradients for K2e-geo: gfs | gfa | d(n.v)
+            const float* din = X + lane * D::XS;
+            float* fg = W.r_fg + (int64_t)i * FgDims<NS, NA>::STRIDE;
 #pragma unroll
-            for (int q = 0; q < IN; ++q) din[q] = 0.f;
-#pragma unroll 4
-            for (int j = 0; j < HID; ++j) {
-                const float dj = dz[j];
-                const float* row = s_mlp + L.w1 + j * IN;
-#pragma unroll
-                for (int q = 0; q < IN; ++q) din[q] += row[q] * dj;
-            }
-#pragma unroll
-            for (int k = 0; k < NS; ++k) gfs[k] = din[k];
-#pragma unroll
-            for (int k = 0; k < NA; ++k) gfa[k] = din[NS + k];
-            const float nv = geo.ndv;
-            if (!P.no_fresnel && nv >= 0.f && nv <= 1.f) {  // decoder.cpp:162-175
-                const float uu = 1.f - nv;
+            for (int k = 0; k < NS + NA; ++k) fg[k] = din[k];
+            float d_ndotv = 0.f;
+            if (!P.no_fresnel && ndv >= 0.f && ndv <= 1.f) {  // decoder.cpp:162-175
+                const float uu = 1.f - ndv;
                 float du = 0.f, upw = 1.f;
 #pragma unroll
                 for (int k = 1; k < NPOW; ++k) {
@@ -894,29 +881,24 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
                 }
                 d_ndotv = -du;
             }
-            // feature gradients for K2e-geo: gfs | gfa | d(n.v)
-            float* fg = W.r_fg + (int64_t)i * FgDims<NS, NA>::STRIDE;
-#pragma unroll
-            for (int k = 0; k < NS; ++k) fg[k] = gfs[k];
-#pragma unroll
-            for (int k = 0; k < NA; ++k) fg[NS + k] = gfa[k];
             fg[NS + NA] = d_ndotv;
         }
         __syncwarp();
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < G.total_nocam; i += blockDim.x) {
+    // flush: sum the warps' accumulators, one atomic per weight
+    for (int q = threadIdx.x; q < G.total_nocam; q += blockDim.x) {
         int a;
-        if (i < G.b1) a = GA::W1 + (i / IN) * GA::W1S + (i % IN);
-        else if (i < G.w2) a = GA::B1 + (i - G.b1);
-        else if (i < G.b2) a = GA::W2 + ((i - G.w2) >> 5) * 33 + ((i - G.w2) & 31);
-        else if (i < G.w3) a = GA::B2 + (i - G.b2);
-        else if (i < G.b3) a = GA::W3 + (i - G.w3);
-        else a = GA::B3 + (i - G.b3);
+        if (q < G.b1) a = D::GW1 + (q / IN) * D::XS + (q % IN);
+        else if (q < G.w2) a = D::GB1 + (q - G.b1);
+        else if (q < G.b2) a = D::GW2 + ((q - G.w2) >> 5) * D::HS + ((q - G.w2) & 31);
+        else if (q < G.w3) a = D::GB2 + (q - G.b2);
+        else if (q < G.b3) a = D::GW3 + ((q - G.w3) >> 5) * D::HS + ((q - G.w3) & 31);
+        else a = D::GB3 + (q - G.b3);
         float v = 0.f;
 #pragma unroll
-        for (int w = 0; w < WARPS_PER_BLOCK; ++w) v += s_acc[w * GA::TOTAL + a];
-        if (v != 0.f) atomicAdd(P.g_mlp + i, v);
+        for (int w = 0; w < WARPS_PER_BLOCK; ++w) v += smem[D::MLP + w * D::GACC + a];
+        if (v != 0.f) atomicAdd(P.g_mlp + q, v);
     }
 }
 
@@ -1111,9 +1093,8 @@ __global__ void __launch_bounds__(BLOCK) shade_geo_kernel(RayPassParams P, WaveB
 
 template <int NS, int NA>
 size_t shade_bwd_smem_bytes() {
-    constexpr int IN = NS + NA + NPOW;
-    return sizeof(float) * (SmemMlp::make(IN).total +
-                            WARPS_PER_BLOCK * (GAccDims<IN>::TOTAL + ScratchDims<IN>::TOTAL));
+    using D = MmaDims<NS + NA + NPOW>;
+    return sizeof(float) * (D::MLP + WARPS_PER_BLOCK * (D::GACC + D::SCR));
 }
 
 }  // namespace psdf
