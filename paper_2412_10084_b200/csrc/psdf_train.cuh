@@ -677,8 +677,7 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
     const MlpLayout G = MlpLayout::make(IN);
     float* sm = smem;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* gacc = smem + D::MLP + warp * D::GACC;
-    float* scr = smem + D::MLP + WARPS_PER_BLOCK * D::GACC + warp * D::SCR;
+    float* scr = smem + D::MLP + warp * D::SCR;
     __shared__ int s_cam[WARPS_PER_BLOCK][32];
     int* cam = s_cam[warp];
     // MLP into shared memory: padded W1 / W1^T / W2 / W2^T / W3, biases
@@ -700,8 +699,14 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
         sm[D::B1 + i] = __ldg(P.mlp + G.b1 + i);
         sm[D::B2 + i] = __ldg(P.mlp + G.b2 + i);
     }
-    for (int i = threadIdx.x; i < WARPS_PER_BLOCK * D::GACC; i += blockDim.x) smem[D::MLP + i] = 0.f;
     __syncthreads();
+    // weight-gradient accumulators: this warp's C fragments, kept in registers
+    // across its batches (dW2 32x32, dW1 32xK1, dW3 rows 0..2) + bias sums
+    float gw2[2][4][4], gw1[2][D::K1 / 8][4], gw3[1][4][4];
+    zero_c(gw2);
+    zero_c(gw1);
+    zero_c(gw3);
+    float gb1 = 0.f, gb2 = 0.f, gb3 = 0.f;
     const float* cam_base = P.mlp + G.cam;
     float* X = scr + D::SX;
     float* A1 = scr + D::SA1;
@@ -773,19 +778,11 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
         __syncwarp();
         // dW3 += DZ3^T A2 (rows 0..2 of one 16-row tile), db3
         {
-            float c[1][4][4];
-            zero_c(c);
             warp_gemm3<1, 4, 4>(
-                c, [&](int m, int k) { return m < 3 ? D3[k * D::DS + m] : 0.f; },
+                gw3, [&](int m, int k) { return m < 3 ? D3[k * D::DS + m] : 0.f; },
                 [&](int n, int k) { return A2[k * D::HS + n]; });
-            for_c(c, [&](int m, int n, float& v) {
-                if (m < 3) gacc[D::GW3 + m * D::HS + n] += v;
-            });
-            if (lane < 3) {
-                float s = 0.f;
-                for (int r = 0; r < 32; ++r) s += D3[r * D::DS + lane];
-                gacc[D::GB3 + lane] += s;
-            }
+            if (lane < 3)
+                for (int r = 0; r < 32; ++r) gb3 += D3[r * D::DS + lane];
         }
         __syncwarp();
         // DZ2 = (DZ3 W3) [A2 > 0]  (in place of A2)
@@ -804,15 +801,10 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
         __syncwarp();
         // dW2 += DZ2^T A1, db2
         {
-            float c[2][4][4];
-            zero_c(c);
             warp_gemm3<2, 4, 4>(
-                c, [&](int m, int k) { return A2[k * D::HS + m]; },
+                gw2, [&](int m, int k) { return A2[k * D::HS + m]; },
                 [&](int n, int k) { return A1[k * D::HS + n]; });
-            for_c(c, [&](int m, int n, float& v) { gacc[D::GW2 + m * D::HS + n] += v; });
-            float s = 0.f;
-            for (int r = 0; r < 32; ++r) s += A2[r * D::HS + lane];
-            gacc[D::GB2 + lane] += s;
+            for (int r = 0; r < 32; ++r) gb2 += A2[r * D::HS + lane];
         }
         __syncwarp();
         // DZ1 = (DZ2 W2) [A1 > 0]  (in place of A1)
@@ -831,15 +823,10 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
         __syncwarp();
         // dW1 += DZ1^T X, db1, camera-bias rows (grouped by camera row)
         {
-            float c[2][D::K1 / 8][4];
-            zero_c(c);
             warp_gemm3<2, D::K1 / 8, 4>(
-                c, [&](int m, int k) { return A1[k * D::HS + m]; },
+                gw1, [&](int m, int k) { return A1[k * D::HS + m]; },
                 [&](int n, int k) { return X[k * D::XS + n]; });
-            for_c(c, [&](int m, int n, float& v) { gacc[D::GW1 + m * D::XS + n] += v; });
-            float s = 0.f;
-            for (int r = 0; r < 32; ++r) s += A1[r * D::HS + lane];
-            gacc[D::GB1 + lane] += s;
+            for (int r = 0; r < 32; ++r) gb1 += A1[r * D::HS + lane];
             if (P.ncam > 0) {
                 const int my = cam[lane];
                 unsigned rem = __ballot_sync(FULL, my >= 0);
@@ -885,8 +872,19 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
         }
         __syncwarp();
     }
+    // flush: each warp's accumulators into its scratch (GACC layout), then the
+    // block sums the warps, one atomic per weight
+    __syncwarp();
+    float* gacc = scr;
+    for_c(gw2, [&](int m, int n, float& v) { gacc[D::GW2 + m * D::HS + n] = v; });
+    for_c(gw1, [&](int m, int n, float& v) { gacc[D::GW1 + m * D::XS + n] = v; });
+    for_c(gw3, [&](int m, int n, float& v) {
+        if (m < 3) gacc[D::GW3 + m * D::HS + n] = v;
+    });
+    gacc[D::GB1 + lane] = gb1;
+    gacc[D::GB2 + lane] = gb2;
+    if (lane < 3) gacc[D::GB3 + lane] = gb3;
     __syncthreads();
-    // flush: sum the warps' accumulators, one atomic per weight
     for (int q = threadIdx.x; q < G.total_nocam; q += blockDim.x) {
         int a;
         if (q < G.b1) a = D::GW1 + (q / IN) * D::XS + (q % IN);
@@ -897,7 +895,7 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
         else a = D::GB3 + (q - G.b3);
         float v = 0.f;
 #pragma unroll
-        for (int w = 0; w < WARPS_PER_BLOCK; ++w) v += smem[D::MLP + w * D::GACC + a];
+        for (int w = 0; w < WARPS_PER_BLOCK; ++w) v += smem[D::MLP + w * D::SCR + a];
         if (v != 0.f) atomicAdd(P.g_mlp + q, v);
     }
 }
@@ -1094,7 +1092,8 @@ __global__ void __launch_bounds__(BLOCK) shade_geo_kernel(RayPassParams P, WaveB
 template <int NS, int NA>
 size_t shade_bwd_smem_bytes() {
     using D = MmaDims<NS + NA + NPOW>;
-    return sizeof(float) * (D::MLP + WARPS_PER_BLOCK * (D::GACC + D::SCR));
+    static_assert(D::GACC <= D::SCR, "accumulator flush reuses the warp scratch");
+    return sizeof(float) * (D::MLP + WARPS_PER_BLOCK * D::SCR);
 }
 
 }  // namespace psdf
