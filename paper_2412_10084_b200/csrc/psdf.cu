@@ -16,6 +16,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -149,6 +150,9 @@ void dispatch_ns(int ns, F&& f) {
 }
 
 int64_t up4(int64_t x) { return (x + 3) & ~int64_t(3); }
+
+// K2a round 0 steps before the remaining rays continue, compacted, in round 1.
+constexpr int kComposite0Steps = 16;
 
 // Tile bitmaps up to 32 KB (1024^3 grids) are staged in shared memory.
 constexpr int kMaxSmemBitWords = 8192;
@@ -426,7 +430,7 @@ void free_wave(psdf_ctx* c) {
                     (void*)W.r_pos, (void*)W.r_w, (void*)W.r_tile, (void*)W.r_entry,
                     (void*)W.r_next, (void*)W.r_c, (void*)W.r_up, (void*)W.r_geo, (void*)W.h_slot,
                     (void*)W.h_count, (void*)W.h_tileprev, (void*)W.h_t, (void*)W.h_tprev, (void*)W.h_dir,
-                    (void*)W.h_t1, (void*)W.h_perm, (void*)W.r_perm, (void*)W.r_fg, (void*)c->h_keys, (void*)c->h_iota, c->sort_tmp})
+                    (void*)W.h_t1, (void*)W.h_perm, (void*)W.r_perm, (void*)W.r_fg, (void*)W.k_rec, (void*)c->h_keys, (void*)c->h_iota, c->sort_tmp})
         if (p) cudaFree(p);
     unsigned* keep = W.counters;
     W = WaveBufs{};
@@ -437,12 +441,13 @@ void free_wave(psdf_ctx* c) {
 }
 
 // Grows the ray-entry / shading-record buffers (kept across steps).
-void ensure_wave(psdf_ctx* c, int64_t e_cap, int64_t r_cap, int64_t h_cap) {
+void ensure_wave(psdf_ctx* c, int64_t e_cap, int64_t r_cap, int64_t h_cap, int64_t k_cap) {
     WaveBufs& W = c->wave;
-    if (e_cap <= W.e_cap && r_cap <= W.r_cap && h_cap <= W.h_cap) return;
+    if (e_cap <= W.e_cap && r_cap <= W.r_cap && h_cap <= W.h_cap && k_cap <= W.k_cap) return;
     e_cap = std::max<int64_t>(e_cap, W.e_cap);
     r_cap = std::max<int64_t>(r_cap, W.r_cap);
     h_cap = std::max<int64_t>(h_cap, W.h_cap);
+    k_cap = std::max<int64_t>(k_cap, W.k_cap);
     if (e_cap > INT32_MAX / 4 || r_cap > INT32_MAX / 4 || h_cap > INT32_MAX / 4)
         fail(PSDF_ERR_RUNTIME, "ray pass needs more than 2^29 entries / records");
     CK(cudaStreamSynchronize(c->stream));
@@ -475,10 +480,10 @@ void ensure_wave(psdf_ctx* c, int64_t e_cap, int64_t r_cap, int64_t h_cap) {
     CK(cudaMalloc(&W.h_perm, sizeof(int) * h_cap));
     CK(cudaMalloc(&W.r_perm, sizeof(int) * r_cap));
     CK(cudaMalloc(&W.r_fg, sizeof(float) * (size_t)FgDims<8, 8>::STRIDE * r_cap));
-    const int64_t k_cap = std::max(h_cap, r_cap);
-    CK(cudaMalloc(&c->h_keys, sizeof(int) * k_cap));
-    CK(cudaMalloc(&c->h_iota, sizeof(int) * k_cap));
-    iota_kernel<<<(unsigned)((k_cap + 255) / 256), 256, 0, c->stream>>>(c->h_iota, (int)k_cap);
+    const int64_t key_cap = std::max(h_cap, r_cap);
+    CK(cudaMalloc(&c->h_keys, sizeof(int) * key_cap));
+    CK(cudaMalloc(&c->h_iota, sizeof(int) * key_cap));
+    iota_kernel<<<(unsigned)((key_cap + 255) / 256), 256, 0, c->stream>>>(c->h_iota, (int)key_cap);
     CK(cudaGetLastError());
     size_t tb_h = 0, tb_r = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tb_h, W.h_slot, c->h_keys, c->h_iota, W.h_perm,
@@ -490,6 +495,8 @@ void ensure_wave(psdf_ctx* c, int64_t e_cap, int64_t r_cap, int64_t h_cap) {
     W.e_cap = (int)e_cap;
     W.r_cap = (int)r_cap;
     W.h_cap = (int)h_cap;
+    CK(cudaMalloc(&W.k_rec, sizeof(ContRec) * k_cap));
+    W.k_cap = (int)k_cap;
 }
 
 // K2 as the wavefront pipeline K2a -> K2b -> K2d -> K2e (psdf_train.cuh).
@@ -497,7 +504,8 @@ template <int NS, int NA>
 void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     cudaStream_t s = c->stream;
     const int64_t n_work = P.tile_end - P.tile_begin;
-    if (c->wave.e_cap == 0) ensure_wave(c, n_rays / 8 + 65536, n_rays / 8 + 65536, n_rays / 2 + 65536);
+    if (c->wave.e_cap == 0)
+        ensure_wave(c, n_rays / 8 + 65536, n_rays / 8 + 65536, n_rays / 2 + 65536, n_rays / 16 + 65536);
     const size_t smem_f = render_smem_bytes<NS, NA>();
     const size_t smem_b = shade_bwd_smem_bytes<NS, NA>();
     CK(cudaFuncSetAttribute(shade_fwd_kernel<NS, NA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
@@ -546,7 +554,7 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
                            cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         const int64_t nh = c->h_wave_counters[2];
-        int64_t ne = 0, nr = 0;
+        int64_t ne = 0, nr = 0, nk = 0;
         if (nh <= c->wave.h_cap) {
             // handovers in image order: coherent warps in K2a and coherent
             // shading records downstream
@@ -557,18 +565,22 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
                                                    c->h_iota, c->wave.h_perm, (int)nh, 0, end_bit, s));
             }
             CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
-            march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, c->wave);
+            march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, c->wave, 0, kComposite0Steps);
             CK(cudaGetLastError());
-            c->last_launches += 2;
-            CK(cudaMemcpyAsync(c->h_wave_counters, c->wave.counters, sizeof(unsigned) * 2,
+            CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
+            march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, c->wave, 1, INT_MAX);
+            CK(cudaGetLastError());
+            c->last_launches += 3;
+            CK(cudaMemcpyAsync(c->h_wave_counters, c->wave.counters, sizeof(unsigned) * 4,
                                cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             ne = c->h_wave_counters[0];
             nr = c->h_wave_counters[1];
-            if (ne <= c->wave.e_cap && nr <= c->wave.r_cap) break;
+            nk = c->h_wave_counters[3];
+            if (ne <= c->wave.e_cap && nr <= c->wave.r_cap && nk <= c->wave.k_cap) break;
         }
         if (attempt > 2) fail(PSDF_ERR_RUNTIME, "ray pass buffers failed to grow");
-        ensure_wave(c, ne + ne / 2 + 4096, nr + nr / 2 + 4096, nh + nh / 2 + 4096);
+        ensure_wave(c, ne + ne / 2 + 4096, nr + nr / 2 + 4096, nh + nh / 2 + 4096, nk + nk / 2 + 4096);
         // the failed sweep already accumulated statistics: clear and redo
         CK(cudaMemsetAsync(c->d_counts, 0, sizeof(unsigned long long) * 8, s));
         CK(cudaMemsetAsync(c->d_stats, 0, sizeof(double) * 16, s));

@@ -39,6 +39,14 @@
 
 namespace psdf {
 
+// Full state of a K2a ray at a sample boundary (the marcher is synchronised
+// with the reference there), for the compacted second round.
+struct ContRec {
+    double t, t_cur, a_cur, acc, trans, depth, t_first, t1, dir[3];
+    int slot, count, tile, n_live, entry, prev, head, cnt_first, flags;  // flags: have_cur | in_mask << 1
+    unsigned n_exact;
+};
+
 struct WaveBufs {
     // ray entries: rays with at least one alpha > 0 sample
     int* e_slot;       // local work tile * 32 + lane
@@ -71,8 +79,9 @@ struct WaveBufs {
     int* h_perm;       // handovers sorted by slot (image order; CUB radix sort)
     int* r_perm;       // shading records sorted by tile (K2b / K2e order)
     float* r_fg;       // [cap][FgDims::STRIDE] feature gradients (K2e-mlp -> K2e-geo)
-    unsigned* counters;  // [0] entries, [1] records, [2] handovers
-    int e_cap, r_cap, h_cap;
+    ContRec* k_rec;    // continuations: rays still alive after K2a's first round
+    unsigned* counters;  // [0] entries, [1] records, [2] handovers, [3] continuations
+    int e_cap, r_cap, h_cap, k_cap;
 };
 
 // Warp-aggregated slot allocation inside divergent code.
@@ -255,9 +264,15 @@ __global__ void __launch_bounds__(BLOCK, PSDF_SCAN_MINB) march_scan_kernel(RayPa
 // The rest of each handed-over ray, one lane per handover (full warps):
 // sigmoid, alpha compositing, early termination, ray entries and shading
 // records.
-__global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPassParams P, WaveBufs W) {
+//
+// Round 0 takes the handovers and stops after `cap` steps: rays still alive
+// then (grazing rays with long tails, a few per warp) are written out as
+// continuations and finished, compacted into full warps, by round 1.
+__global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPassParams P, WaveBufs W, int round,
+                                                                          int cap) {
     extern __shared__ __align__(16) uint32_t sm_bits[];
-    const int n_hand = (int)min(*(volatile unsigned*)(W.counters + 2), (unsigned)W.h_cap);
+    const int n_hand = round == 0 ? (int)min(*(volatile unsigned*)(W.counters + 2), (unsigned)W.h_cap)
+                                  : (int)min(*(volatile unsigned*)(W.counters + 3), (unsigned)W.k_cap);
     const int lane = threadIdx.x & 31;
     const GridView& g = P.g;
     const uint32_t* bits = stage_tile_bits(g, sm_bits, P.bits_sm_words);
@@ -272,21 +287,21 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
         base = __shfl_sync(FULL, base, 0);
         if (base >= n_hand) break;
         const bool valid = base + lane < n_hand;
-        const int hi = valid ? W.h_perm[base + lane] : 0;
-        const int slot = valid ? W.h_slot[hi] : 0;
+        const int hi = valid ? (round == 0 ? W.h_perm[base + lane] : base + lane) : 0;
+        const ContRec* kr = W.k_rec + hi;
+        const int slot = valid ? (round == 0 ? W.h_slot[hi] : kr->slot) : 0;
         const LaneRay R = lane_ray(P, slot >> 5, slot & 31);
-        // train: only in-mask rays are shaded (trainer.cpp:163); render: all, if colours are wanted
-        const bool in_mask = valid && (P.mode == 1 ? P.need_colors != 0 : __ldg(R.V->mask + R.px) != 0);
-        const double dd[3] = {valid ? W.h_dir[3 * (int64_t)hi] : 0.0, valid ? W.h_dir[3 * (int64_t)hi + 1] : 0.0,
-                              valid ? W.h_dir[3 * (int64_t)hi + 2] : 1.0};
         Marcher mr;
         double t_cur = 0.0, a_cur = 1.0, acc = 0.0, trans = 1.0, depth = 0.0;
         int tile_cur = -1, n_live = 0, entry = -1, prev = -1, head = -1;
         double t_first = 0.0;
         int cnt_first = -1;
-        bool have_cur = false;
+        bool have_cur = false, in_mask = false, cont = false;
         bool alive = valid;
-        if (valid) {
+        if (valid && round == 0) {
+            // train: only in-mask rays are shaded (trainer.cpp:163); render: all, if colours are wanted
+            in_mask = P.mode == 1 ? P.need_colors != 0 : __ldg(R.V->mask + R.px) != 0;
+            const double dd[3] = {W.h_dir[3 * (int64_t)hi], W.h_dir[3 * (int64_t)hi + 1], W.h_dir[3 * (int64_t)hi + 2]};
             mr.init_from(g, R.V->cam.pos, dd, P.n_max, W.h_t1[hi]);
             mr.t = W.h_t[hi];
             mr.count = W.h_count[hi];
@@ -294,13 +309,67 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
             n_live = have_cur ? mr.count - 1 : 0;  // settles among the saturated prefix
             t_cur = W.h_tprev[hi];
             tile_cur = W.h_tileprev[hi];
+        } else if (valid) {
+            mr.init_from(g, R.V->cam.pos, kr->dir, P.n_max, kr->t1);
+            mr.t = kr->t;
+            mr.count = kr->count;
+            mr.n_exact = kr->n_exact;
+            t_cur = kr->t_cur;
+            a_cur = kr->a_cur;
+            acc = kr->acc;
+            trans = kr->trans;
+            depth = kr->depth;
+            t_first = kr->t_first;
+            tile_cur = kr->tile;
+            n_live = kr->n_live;
+            entry = kr->entry;
+            prev = kr->prev;
+            head = kr->head;
+            cnt_first = kr->cnt_first;
+            have_cur = kr->flags & 1;
+            in_mask = (kr->flags >> 1) & 1;
         }
         // One sample per iteration, warp-synchronous so that the record
         // allocation below uses full-warp ballots (single call sites also
         // keep the loop small): fetch the next march sample (or the
         // one-past-the-end position), evaluate its sigmoid, then settle the
         // alpha of the previous sample.
-        while (__any_sync(FULL, alive)) {
+        for (int step = 0; __any_sync(FULL, alive); ++step) {
+            if (step == cap) {  // warp-uniform: hand the remaining rays to round 1
+                const unsigned km = __ballot_sync(FULL, alive);
+                unsigned kb = 0;
+                if (lane == 0) kb = atomicAdd(W.counters + 3, (unsigned)__popc(km));
+                kb = __shfl_sync(FULL, kb, 0);
+                if (alive) {
+                    cont = true;
+                    const int k = (int)(kb + __popc(km & ((1u << lane) - 1u)));
+                    if (k < W.k_cap) {
+                        ContRec& o = W.k_rec[k];
+                        o.t = mr.t;
+                        o.t_cur = t_cur;
+                        o.a_cur = a_cur;
+                        o.acc = acc;
+                        o.trans = trans;
+                        o.depth = depth;
+                        o.t_first = t_first;
+                        o.t1 = mr.t1;
+                        o.dir[0] = mr.d[0];
+                        o.dir[1] = mr.d[1];
+                        o.dir[2] = mr.d[2];
+                        o.slot = slot;
+                        o.count = mr.count;
+                        o.tile = tile_cur;
+                        o.n_live = n_live;
+                        o.entry = entry;
+                        o.prev = prev;
+                        o.head = head;
+                        o.cnt_first = cnt_first;
+                        o.flags = (have_cur ? 1 : 0) | (in_mask ? 2 : 0);
+                        o.n_exact = mr.n_exact;
+                    }
+                }
+                break;
+            }
             double t_nxt = 0.0, w = 0.0;
             int tile_nxt = -1;
             bool has_next = false, settle = false, want_entry = false, shade = false;
@@ -396,13 +465,14 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
                 a_cur = a_nxt;
             }
         }
+        if (cont) continue;
         c_m += n_live;
         if (valid) c_ex += mr.n_exact;
         if (entry >= 0) {
             W.e_slot[entry] = slot;
-            W.e_dir[3 * (int64_t)entry] = dd[0];
-            W.e_dir[3 * (int64_t)entry + 1] = dd[1];
-            W.e_dir[3 * (int64_t)entry + 2] = dd[2];
+            W.e_dir[3 * (int64_t)entry] = mr.d[0];
+            W.e_dir[3 * (int64_t)entry + 1] = mr.d[1];
+            W.e_dir[3 * (int64_t)entry + 2] = mr.d[2];
             W.e_tfirst[entry] = t_first;
             W.e_cfirst[entry] = cnt_first;
             W.e_nlive[entry] = n_live;
