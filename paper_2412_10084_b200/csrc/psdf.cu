@@ -152,7 +152,7 @@ void dispatch_ns(int ns, F&& f) {
 int64_t up4(int64_t x) { return (x + 3) & ~int64_t(3); }
 
 // K2a round 0 steps before the remaining rays continue, compacted, in round 1.
-constexpr int kComposite0Steps = 16;
+constexpr int kComposite0Steps = 16;  // default; PSDF_COMPOSITE_STEPS overrides (tuning)
 
 // Tile bitmaps up to 32 KB (1024^3 grids) are staged in shared memory.
 constexpr int kMaxSmemBitWords = 8192;
@@ -184,6 +184,7 @@ struct psdf_ctx {
     int32_t* d_tile_nbr = nullptr; // [T][27] neighbour tile ids
     int occ_tlo[3] = {0, 0, 0}, occ_thi[3] = {-1, -1, -1};  // allocated tiles' bounding box (tile coords)
     uint8_t* d_sat_dist = nullptr; // [T][64] saturation distances of the current ray pass
+    int composite_steps = kComposite0Steps;
     int* h_keys = nullptr;         // handover sort: keys out, iota values in, CUB temp
     int* h_iota = nullptr;
     void* sort_tmp = nullptr;
@@ -565,7 +566,9 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
                                                    c->h_iota, c->wave.h_perm, (int)nh, 0, end_bit, s));
             }
             CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
-            march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, c->wave, 0, kComposite0Steps);
+            // (render: one round; its rays are short at the render tau)
+            march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, c->wave, 0,
+                                                                        P.mode == 1 ? INT_MAX : c->composite_steps);
             CK(cudaGetLastError());
             CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
             march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, c->wave, 1, INT_MAX);
@@ -921,6 +924,7 @@ int psdf_create(int device, psdf_ctx** out) {
         c->device = device;
         CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        if (const char* e = std::getenv("PSDF_COMPOSITE_STEPS")) c->composite_steps = std::max(1, std::atoi(e));
         CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&c->ev_copied, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_copy_free, cudaEventDisableTiming));
