@@ -232,7 +232,7 @@ struct psdf_ctx {
 
     // wavefront buffers of the train ray pass (psdf_train.cuh)
     WaveBufs wave{};
-    unsigned* h_wave_counters = nullptr;  // pinned [2]
+    unsigned* h_wave_counters = nullptr;  // pinned [8]
 
     GridView view() const {
         GridView g{};
@@ -431,7 +431,7 @@ void free_wave(psdf_ctx* c) {
                     (void*)W.r_pos, (void*)W.r_w, (void*)W.r_tile, (void*)W.r_entry,
                     (void*)W.r_next, (void*)W.r_c, (void*)W.r_up, (void*)W.r_geo, (void*)W.h_slot,
                     (void*)W.h_count, (void*)W.h_tileprev, (void*)W.h_t, (void*)W.h_tprev, (void*)W.h_dir,
-                    (void*)W.h_t1, (void*)W.h_perm, (void*)W.r_perm, (void*)W.r_fg, (void*)W.k_rec, (void*)c->h_keys, (void*)c->h_iota, c->sort_tmp})
+                    (void*)W.h_t1, (void*)W.h_perm, (void*)W.r_perm, (void*)W.r_fg, (void*)W.k_rec, (void*)W.a_t, (void*)W.a_s, (void*)W.a_i, (void*)W.e_ahead, (void*)c->h_keys, (void*)c->h_iota, c->sort_tmp})
         if (p) cudaFree(p);
     unsigned* keep = W.counters;
     W = WaveBufs{};
@@ -442,14 +442,15 @@ void free_wave(psdf_ctx* c) {
 }
 
 // Grows the ray-entry / shading-record buffers (kept across steps).
-void ensure_wave(psdf_ctx* c, int64_t e_cap, int64_t r_cap, int64_t h_cap, int64_t k_cap) {
+void ensure_wave(psdf_ctx* c, int64_t e_cap, int64_t r_cap, int64_t h_cap, int64_t k_cap, int64_t a_cap) {
     WaveBufs& W = c->wave;
-    if (e_cap <= W.e_cap && r_cap <= W.r_cap && h_cap <= W.h_cap && k_cap <= W.k_cap) return;
+    if (e_cap <= W.e_cap && r_cap <= W.r_cap && h_cap <= W.h_cap && k_cap <= W.k_cap && a_cap <= W.a_cap) return;
     e_cap = std::max<int64_t>(e_cap, W.e_cap);
     r_cap = std::max<int64_t>(r_cap, W.r_cap);
     h_cap = std::max<int64_t>(h_cap, W.h_cap);
     k_cap = std::max<int64_t>(k_cap, W.k_cap);
-    if (e_cap > INT32_MAX / 4 || r_cap > INT32_MAX / 4 || h_cap > INT32_MAX / 4)
+    a_cap = std::max<int64_t>(a_cap, W.a_cap);
+    if (e_cap > INT32_MAX / 4 || r_cap > INT32_MAX / 4 || h_cap > INT32_MAX / 4 || a_cap > INT32_MAX / 4)
         fail(PSDF_ERR_RUNTIME, "ray pass needs more than 2^29 entries / records");
     CK(cudaStreamSynchronize(c->stream));
     free_wave(c);
@@ -498,6 +499,11 @@ void ensure_wave(psdf_ctx* c, int64_t e_cap, int64_t r_cap, int64_t h_cap, int64
     W.h_cap = (int)h_cap;
     CK(cudaMalloc(&W.k_rec, sizeof(ContRec) * k_cap));
     W.k_cap = (int)k_cap;
+    CK(cudaMalloc(&W.a_t, sizeof(double) * 2 * a_cap));
+    CK(cudaMalloc(&W.a_s, sizeof(double) * 3 * a_cap));
+    CK(cudaMalloc(&W.a_i, sizeof(int4) * a_cap));
+    CK(cudaMalloc(&W.e_ahead, sizeof(int) * e_cap));
+    W.a_cap = (int)a_cap;
 }
 
 // K2 as the wavefront pipeline K2a -> K2b -> K2d -> K2e (psdf_train.cuh).
@@ -506,7 +512,8 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     cudaStream_t s = c->stream;
     const int64_t n_work = P.tile_end - P.tile_begin;
     if (c->wave.e_cap == 0)
-        ensure_wave(c, n_rays / 8 + 65536, n_rays / 8 + 65536, n_rays / 2 + 65536, n_rays / 16 + 65536);
+        ensure_wave(c, n_rays / 8 + 65536, n_rays / 8 + 65536, n_rays / 2 + 65536, n_rays / 16 + 65536,
+                    n_rays / 8 + 65536);
     const size_t smem_f = render_smem_bytes<NS, NA>();
     const size_t smem_b = shade_bwd_smem_bytes<NS, NA>();
     CK(cudaFuncSetAttribute(shade_fwd_kernel<NS, NA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
@@ -515,7 +522,6 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     const size_t smem_bits = sizeof(uint32_t) * P.bits_sm_words;
     CK(cudaFuncSetAttribute(march_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bits));
     CK(cudaFuncSetAttribute(march_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bits));
-    CK(cudaFuncSetAttribute(alpha_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bits));
     const int per_sm_s = blocks_per_sm((const void*)march_scan_kernel, smem_bits);
     const int64_t grid_s = std::max<int64_t>(1, std::min<int64_t>((n_work + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
                                                                    (int64_t)per_sm_s * c->sm_count));
@@ -525,7 +531,7 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     CK(cudaEventRecord(c->ev_k[0], s));
     for (int attempt = 0;; ++attempt) {
         CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
-        CK(cudaMemsetAsync(c->wave.counters, 0, sizeof(unsigned) * 4, s));
+        CK(cudaMemsetAsync(c->wave.counters, 0, sizeof(unsigned) * 8, s));
         P.work_counter = c->d_work;
         if (c->n_view_ready == 0) {
             P.scan_lo = 0;
@@ -555,7 +561,7 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
                            cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         const int64_t nh = c->h_wave_counters[2];
-        int64_t ne = 0, nr = 0, nk = 0;
+        int64_t ne = 0, nr = 0, nk = 0, na = 0;
         if (nh <= c->wave.h_cap) {
             // handovers in image order: coherent warps in K2a and coherent
             // shading records downstream
@@ -574,16 +580,18 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
             march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, c->wave, 1, INT_MAX);
             CK(cudaGetLastError());
             c->last_launches += 3;
-            CK(cudaMemcpyAsync(c->h_wave_counters, c->wave.counters, sizeof(unsigned) * 4,
+            CK(cudaMemcpyAsync(c->h_wave_counters, c->wave.counters, sizeof(unsigned) * 8,
                                cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             ne = c->h_wave_counters[0];
             nr = c->h_wave_counters[1];
             nk = c->h_wave_counters[3];
-            if (ne <= c->wave.e_cap && nr <= c->wave.r_cap && nk <= c->wave.k_cap) break;
+            na = c->h_wave_counters[4];
+            if (ne <= c->wave.e_cap && nr <= c->wave.r_cap && nk <= c->wave.k_cap && na <= c->wave.a_cap) break;
         }
         if (attempt > 2) fail(PSDF_ERR_RUNTIME, "ray pass buffers failed to grow");
-        ensure_wave(c, ne + ne / 2 + 4096, nr + nr / 2 + 4096, nh + nh / 2 + 4096, nk + nk / 2 + 4096);
+        ensure_wave(c, ne + ne / 2 + 4096, nr + nr / 2 + 4096, nh + nh / 2 + 4096, nk + nk / 2 + 4096,
+                    na + na / 2 + 4096);
         // the failed sweep already accumulated statistics: clear and redo
         CK(cudaMemsetAsync(c->d_counts, 0, sizeof(unsigned long long) * 8, s));
         CK(cudaMemsetAsync(c->d_stats, 0, sizeof(double) * 16, s));
@@ -594,7 +602,9 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     if (getenv("PSDF_DEBUG_MARCH")) {
         unsigned long long cc[8];
         CK(cudaMemcpy(cc, c->d_counts, sizeof cc, cudaMemcpyDeviceToHost));
-        fprintf(stderr, "[psdf] march exact fallbacks: %llu\n", cc[6]);
+        fprintf(stderr, "[psdf] march exact fallbacks: %llu; handovers %u entries %u records %u continuations %u alpha samples %u\n",
+                cc[6], c->h_wave_counters[2], c->h_wave_counters[0], c->h_wave_counters[1], c->h_wave_counters[3],
+                c->h_wave_counters[4]);
 #ifdef PSDF_MARCH_STATS
         unsigned long long st[12];
         CK(cudaMemcpyFromSymbol(st, g_march_stats, sizeof st));
@@ -638,9 +648,9 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
         return;
     }
     if (n_ent > 0) {
-        const int per_sm = blocks_per_sm((const void*)alpha_bwd_kernel, smem_bits);
+        const int per_sm = blocks_per_sm((const void*)alpha_bwd_kernel, 0);
         const int grid = (int)std::min<int64_t>((n_ent + BLOCK - 1) / BLOCK, (int64_t)per_sm * c->sm_count);
-        alpha_bwd_kernel<<<grid, BLOCK, smem_bits, s>>>(P, c->wave, n_ent);
+        alpha_bwd_kernel<<<grid, BLOCK, 0, s>>>(P, c->wave, n_ent);
         CK(cudaGetLastError());
         ++c->last_launches;
     }
@@ -938,8 +948,8 @@ int psdf_create(int device, psdf_ctx** out) {
         CK(cudaMalloc(&c->d_stats, sizeof(double) * 16));
         CK(cudaMallocHost(&c->h_stats, sizeof(double) * 16));
         CK(cudaMallocHost(&c->h_counts, sizeof(unsigned long long) * 8));
-        CK(cudaMallocHost(&c->h_wave_counters, sizeof(unsigned) * 4));
-        CK(cudaMalloc(&c->wave.counters, sizeof(unsigned) * 4));
+        CK(cudaMallocHost(&c->h_wave_counters, sizeof(unsigned) * 8));
+        CK(cudaMalloc(&c->wave.counters, sizeof(unsigned) * 8));
         for (auto& e : c->ev_k) CK(cudaEventCreate(&e));
         *out = c;
     });

@@ -10,10 +10,10 @@
 //                   without one finish here (their loss needs no colour).
 //  K2b shade_fwd    one lane per record: decode_fused, colour stored in the
 //                   record, c_raw[ray] += w C (f64 atomics).
-//  K2d alpha_bwd    one lane per ray entry: photo_pixel, then a second sweep
-//                   from the first alpha > 0 sample that applies the alpha /
-//                   transmittance chain of renderer.cpp:247-276 and scatters
-//                   the SDF-sample gradients; writes each record's upstream
+//  K2d alpha_bwd    one lane per ray entry: photo_pixel, then the alpha /
+//                   transmittance chain of renderer.cpp:247-276 over the ray's
+//                   alpha > 0 samples (listed by K2a, no second march), SDF-
+//                   sample gradient scatters; writes each record's upstream
 //                   dL/dC = w g.
 //  K2e shade_bwd    one lane per record, 32 records per warp: decode forward
 //                   again + decode_backward with warp-cooperative MLP weight
@@ -44,6 +44,7 @@ namespace psdf {
 struct ContRec {
     double t, t_cur, a_cur, acc, trans, depth, t_first, t1, dir[3];
     int slot, count, tile, n_live, entry, prev, head, cnt_first, flags;  // flags: have_cur | in_mask << 1
+    int ahead, aprev;
     unsigned n_exact;
 };
 
@@ -80,8 +81,16 @@ struct WaveBufs {
     int* r_perm;       // shading records sorted by tile (K2b / K2e order)
     float* r_fg;       // [cap][FgDims::STRIDE] feature gradients (K2e-mlp -> K2e-geo)
     ContRec* k_rec;    // continuations: rays still alive after K2a's first round
-    unsigned* counters;  // [0] entries, [1] records, [2] handovers, [3] continuations
-    int e_cap, r_cap, h_cap, k_cap;
+    // alpha samples (K2a -> K2d): every settle with alpha > 0, linked per ray
+    // entry in march order — all the backward's alpha / transmittance chain
+    // needs, so K2d does not march again
+    double* a_t;       // [cap][2] t of the sample, t of the point it settled against
+    double* a_s;       // [cap][3] sigmoid at both, transmittance before the sample
+    int4* a_i;         // [cap] (tile of the sample, tile of the next point or -1 for the
+                       //        one-past-the-end point, record or -1, next alpha sample or -1)
+    int* e_ahead;      // first alpha sample of the entry
+    unsigned* counters;  // [0] entries, [1] records, [2] handovers, [3] continuations, [4] alpha samples
+    int e_cap, r_cap, h_cap, k_cap, a_cap;
 };
 
 // Warp-aggregated slot allocation inside divergent code.
@@ -293,7 +302,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
         const LaneRay R = lane_ray(P, slot >> 5, slot & 31);
         Marcher mr;
         double t_cur = 0.0, a_cur = 1.0, acc = 0.0, trans = 1.0, depth = 0.0;
-        int tile_cur = -1, n_live = 0, entry = -1, prev = -1, head = -1;
+        int tile_cur = -1, n_live = 0, entry = -1, prev = -1, head = -1, ahead = -1, aprev = -1;
         double t_first = 0.0;
         int cnt_first = -1;
         bool have_cur = false, in_mask = false, cont = false;
@@ -326,6 +335,8 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
             prev = kr->prev;
             head = kr->head;
             cnt_first = kr->cnt_first;
+            ahead = kr->ahead;
+            aprev = kr->aprev;
             have_cur = kr->flags & 1;
             in_mask = (kr->flags >> 1) & 1;
         }
@@ -364,6 +375,8 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
                         o.prev = prev;
                         o.head = head;
                         o.cnt_first = cnt_first;
+                        o.ahead = ahead;
+                        o.aprev = aprev;
                         o.flags = (have_cur ? 1 : 0) | (in_mask ? 2 : 0);
                         o.n_exact = mr.n_exact;
                     }
@@ -372,7 +385,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
             }
             double t_nxt = 0.0, w = 0.0;
             int tile_nxt = -1;
-            bool has_next = false, settle = false, want_entry = false, shade = false;
+            bool has_next = false, settle = false, want_entry = false, shade = false, want_alpha = false;
             double a_nxt = 0.0, alpha = 0.0;
             int n_settle = 0;
             if (alive) {
@@ -413,6 +426,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
                             t_first = t_cur;
                         }
                         want_entry = alpha > 0.0 && entry < 0;
+                        want_alpha = alpha > 0.0 && P.mode != 1;
                         shade = in_mask && w > 0.0 && tile_cur >= 0;
                     }
                 }
@@ -421,22 +435,27 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
             {
                 const unsigned me = __ballot_sync(FULL, want_entry);
                 const unsigned mr_ = __ballot_sync(FULL, shade);
+                const unsigned ma = __ballot_sync(FULL, want_alpha);
                 const unsigned below = (1u << lane) - 1u;
-                unsigned be = 0, br = 0;
+                unsigned be = 0, br = 0, ba = 0;
                 if (lane == 0) {
                     if (me) be = atomicAdd(W.counters + 0, (unsigned)__popc(me));
                     if (mr_) br = atomicAdd(W.counters + 1, (unsigned)__popc(mr_));
+                    if (ma) ba = atomicAdd(W.counters + 4, (unsigned)__popc(ma));
                 }
                 be = __shfl_sync(FULL, be, 0);
                 br = __shfl_sync(FULL, br, 0);
+                ba = __shfl_sync(FULL, ba, 0);
                 if (want_entry) {
                     const int e = (int)(be + __popc(me & below));
                     entry = e < W.e_cap ? e : -2;  // -2: overflow, host retries
                 }
+                int rec_now = -1;
                 if (shade) {
                     ++c_sh;
                     const int r = (int)(br + __popc(mr_ & below));
                     if (r < W.r_cap && entry >= 0) {
+                        rec_now = r;
                         double pc[3];
                         mr.pos(t_cur, pc);
                         W.r_pos[3 * (int64_t)r] = pc[0];
@@ -449,6 +468,20 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
                         if (prev >= 0) W.r_next[prev] = r;
                         else head = r;
                         prev = r;
+                    }
+                }
+                if (want_alpha) {
+                    const int a = (int)(ba + __popc(ma & below));
+                    if (a < W.a_cap && entry >= 0) {
+                        W.a_t[2 * (int64_t)a] = t_cur;
+                        W.a_t[2 * (int64_t)a + 1] = has_next ? t_nxt : dadd(t_cur, g.h);
+                        W.a_s[3 * (int64_t)a] = a_cur;
+                        W.a_s[3 * (int64_t)a + 1] = a_nxt;
+                        W.a_s[3 * (int64_t)a + 2] = trans;
+                        W.a_i[a] = make_int4(tile_cur, has_next ? tile_nxt : -1, rec_now, -1);
+                        if (aprev >= 0) W.a_i[aprev].w = a;
+                        else ahead = a;
+                        aprev = a;
                     }
                 }
             }
@@ -479,6 +512,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
             W.e_acc[entry] = acc;
             W.e_t1[entry] = mr.t1;
             W.e_head[entry] = head;
+            W.e_ahead[entry] = ahead;
             W.e_craw[3 * (int64_t)entry] = 0.0;
             W.e_craw[3 * (int64_t)entry + 1] = 0.0;
             W.e_craw[3 * (int64_t)entry + 2] = 0.0;
@@ -578,12 +612,9 @@ __global__ void __launch_bounds__(BLOCK) shade_fwd_kernel(RayPassParams P, WaveB
 }
 
 // ------------------------------------------------------------------ K2d
-__global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) alpha_bwd_kernel(RayPassParams P, WaveBufs W, int n_ent) {
-    extern __shared__ __align__(16) uint32_t sm_bits[];
+__global__ void __launch_bounds__(BLOCK) alpha_bwd_kernel(RayPassParams P, WaveBufs W, int n_ent) {
     const int lane = threadIdx.x & 31;
     const GridView& g = P.g;
-    const uint32_t* bits = stage_tile_bits(g, sm_bits, P.bits_sm_words);
-    __syncthreads();
     const double tau = P.tau;
     double st_photo = 0.0, st_sq = 0.0;
     unsigned long long st_mask = 0, c_al = 0, c_bwd = 0;
@@ -612,73 +643,73 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) alpha_bwd_kernel(RayPa
                                        dmul(gz, dsub(c2, dmul(P.bg[2], acc)))),
                                   dmul(dA, acc));
         const double gbg = dadd(dadd(dmul(gx, P.bg[0]), dmul(gy, P.bg[1])), dmul(gz, P.bg[2]));
+        const double* o = R.V->cam.pos;
         const double dd[3] = {W.e_dir[3 * (int64_t)e], W.e_dir[3 * (int64_t)e + 1],
                               W.e_dir[3 * (int64_t)e + 2]};
-        Marcher mr;
-        mr.init_from(g, R.V->cam.pos, dd, P.n_max, W.e_t1[e]);
-        mr.t = W.e_tfirst[e];
-        mr.count = W.e_cfirst[e];
-        const int n_live = W.e_nlive[e];
-        double t_cur = 0.0;
-        int tile_cur = -1;
-        int4 tc_cur;
-        mr.next(g, t_cur, tile_cur, bits, &tc_cur);  // re-emits the first alpha > 0 sample
-        double pc[3];
-        mr.pos(t_cur, pc);
-        double a_cur = sigmoid_sat(dmul(tau, sample_sdf_in(g, pc[0], pc[1], pc[2], tile_cur, tc_cur)));
-        double T = 1.0, pre = 0.0, carry = 0.0;
-        int idx = W.e_cfirst[e];
-        for (;;) {
-            double t_nxt = 0.0;
-            int tile_nxt = -1;
-            int4 tc_nxt;
-            const bool has_next = mr.next(g, t_nxt, tile_nxt, bits, &tc_nxt);
-            double pn[3];
-            mr.pos(has_next ? t_nxt : dadd(t_cur, g.h), pn);
-            const double s_nxt = has_next ? sample_sdf_in(g, pn[0], pn[1], pn[2], tile_nxt, tc_nxt)
-                                          : sample_sdf(g, pn[0], pn[1], pn[2]);
-            const double a_nxt = sigmoid_sat(dmul(tau, s_nxt));
-            const double alpha = a_nxt == 1.0 ? 0.0 : alpha_from(a_cur, a_nxt);
+        auto pos = [&](double t, double p[3]) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) p[k] = dadd(o[k], dmul(dd[k], t));
+        };
+        // the alpha > 0 samples in march order; the samples between them have
+        // alpha == 0 and w == 0 and only pass the previous sample's
+        // d/ds_{i+1} term on to their own position (renderer.cpp:254-276)
+        double pre = 0.0, carry = 0.0, t_carry = -1.0;
+        int tile_carry = -1;
+        for (int a = W.e_ahead[e]; a >= 0;) {
+            const int4 ai = W.a_i[a];
+            const double t_i = W.a_t[2 * (int64_t)a], t_n = W.a_t[2 * (int64_t)a + 1];
+            const double a_cur = W.a_s[3 * (int64_t)a], a_nxt = W.a_s[3 * (int64_t)a + 1],
+                         T = W.a_s[3 * (int64_t)a + 2];
+            const double alpha = alpha_from(a_cur, a_nxt);
             const double w = dmul(T, alpha);
-            if (alpha > 0.0) ++c_al;
-            const bool shade = in_mask && w > 0.0 && tile_cur >= 0;
+            ++c_al;
             // dL/dw_i = g.(C_i - bg) + dA (renderer.cpp:249-253)
             double dw = dadd(-gbg, dA);
-            if (shade && rec >= 0) {
-                const float4 cr = reinterpret_cast<const float4*>(W.r_c)[rec];
+            if (ai.z >= 0) {
+                const float4 cr = reinterpret_cast<const float4*>(W.r_c)[ai.z];
                 dw = dadd(dsub(dadd(dadd(dmul(gx, (double)cr.x), dmul(gy, (double)cr.y)),
                                     dmul(gz, (double)cr.z)),
                                gbg),
                           dA);
-                reinterpret_cast<float4*>(W.r_up)[rec] =
+                reinterpret_cast<float4*>(W.r_up)[ai.z] =
                     make_float4((float)(w * gx), (float)(w * gy), (float)(w * gz), 0.f);
-                rec = W.r_next[rec];
             }
             pre = dadd(pre, dmul(dw, w));
             double own = 0.0, nxt = 0.0;
             const double om_a = dsub(1.0, alpha);
-            const double dalpha =
-                alpha > 0.0 ? dsub(dmul(dw, T), om_a > 1e-12 ? ddiv(dsub(total, pre), om_a) : 0.0) : 0.0;
-            if (alpha > 0.0 && dalpha != 0.0) {  // renderer.cpp:266-276
+            const double dalpha = dsub(dmul(dw, T), om_a > 1e-12 ? ddiv(dsub(total, pre), om_a) : 0.0);
+            if (dalpha != 0.0) {  // renderer.cpp:266-276
                 const double da = dmul(dmul(tau, a_cur), dsub(1.0, a_cur));
                 const double db = dmul(dmul(tau, a_nxt), dsub(1.0, a_nxt));
                 own = ddiv(dmul(dmul(dalpha, a_nxt), da), dmul(a_cur, a_cur));
                 nxt = dmul(dalpha, ddiv(-db, a_cur));
             }
-            mr.pos(t_cur, pc);
-            const double ds_i = dadd(carry, own);
-            if (ds_i != 0.0) scatter_smooth_in(g, P.g_smooth, tile_cur, tc_cur, pc, ds_i);
-            carry = nxt;
-            ++idx;
-            if (idx >= n_live || !has_next) {
-                if (carry != 0.0) scatter_smooth(g, P.g_smooth, pn[0], pn[1], pn[2], carry);
-                break;
+            double p[3];
+            // the previous alpha sample's term lands here, or at a sample of its own
+            double ds_i = own;
+            if (carry != 0.0) {
+                if (t_carry == t_i) {
+                    ds_i = dadd(carry, own);
+                } else {
+                    pos(t_carry, p);
+                    scatter_smooth_in(g, P.g_smooth, tile_carry, __ldg(g.tile_coords + tile_carry), p, carry);
+                }
             }
-            T = dmul(T, dsub(1.0, alpha));
-            t_cur = t_nxt;
-            tile_cur = tile_nxt;
-            tc_cur = tc_nxt;
-            a_cur = a_nxt;
+            if (ds_i != 0.0) {
+                pos(t_i, p);
+                scatter_smooth_in(g, P.g_smooth, ai.x, __ldg(g.tile_coords + ai.x), p, ds_i);
+            }
+            carry = nxt;
+            t_carry = t_n;
+            tile_carry = ai.y;
+            a = ai.w;
+            if (a < 0 && carry != 0.0) {
+                pos(t_n, p);
+                if (tile_carry >= 0)
+                    scatter_smooth_in(g, P.g_smooth, tile_carry, __ldg(g.tile_coords + tile_carry), p, carry);
+                else  // the one-past-the-end point
+                    scatter_smooth(g, P.g_smooth, p[0], p[1], p[2], carry);
+            }
         }
     }
     st_photo = warp_sum_d(st_photo);
