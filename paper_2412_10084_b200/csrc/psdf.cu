@@ -10,7 +10,7 @@
 // A train step is the kernel sequence K2 (fused ray pass) -> K3..K6
 // (regularizers) -> K7 (G^T fold) -> [NCCL all-reduce] -> K8 (Adam) -> K9
 // (smoothing), all on the context's stream.
-#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -185,10 +185,11 @@ struct psdf_ctx {
     int occ_tlo[3] = {0, 0, 0}, occ_thi[3] = {-1, -1, -1};  // allocated tiles' bounding box (tile coords)
     uint8_t* d_sat_dist = nullptr; // [T][64] saturation distances of the current ray pass
     int composite_steps = kComposite0Steps;
-    int* h_keys = nullptr;         // handover sort: keys out, iota values in, CUB temp
-    int* h_iota = nullptr;
-    void* sort_tmp = nullptr;
-    size_t sort_tmp_bytes = 0;
+    int* d_tile_cnt = nullptr;     // [2T] shading records per tile, then their offsets
+    void* scan_tmp = nullptr;      // CUB scan storage of the counting sort
+    size_t scan_tmp_bytes = 0;
+    int tsort_cap = 0;
+    int wave_init = 0;             // PSDF_WAVE_INIT: initial ray-pass buffer capacity (tests)
     int bit_words = 0;
     int4* d_tile_coords = nullptr;
     int32_t* d_probe_ids = nullptr;
@@ -419,10 +420,6 @@ void prepare_sat(psdf_ctx* c, double tau_run) {
 }
 
 
-__global__ void iota_kernel(int* __restrict__ v, int n) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) v[i] = i;
-}
 
 void free_wave(psdf_ctx* c) {
     WaveBufs& W = c->wave;
@@ -431,17 +428,15 @@ void free_wave(psdf_ctx* c) {
                     (void*)W.r_pos, (void*)W.r_w, (void*)W.r_tile, (void*)W.r_entry,
                     (void*)W.r_next, (void*)W.r_c, (void*)W.r_up, (void*)W.r_geo, (void*)W.h_slot,
                     (void*)W.h_count, (void*)W.h_tileprev, (void*)W.h_t, (void*)W.h_tprev, (void*)W.h_dir,
-                    (void*)W.h_t1, (void*)W.h_perm, (void*)W.r_perm, (void*)W.r_fg, (void*)W.k_rec, (void*)W.a_t, (void*)W.a_s, (void*)W.a_i, (void*)W.e_ahead, (void*)c->h_keys, (void*)c->h_iota, c->sort_tmp})
+                    (void*)W.h_t1, (void*)W.r_perm, (void*)W.r_fg, (void*)W.k_rec, (void*)W.a_t,
+                    (void*)W.a_s, (void*)W.a_i, (void*)W.e_ahead})
         if (p) cudaFree(p);
     unsigned* keep = W.counters;
     W = WaveBufs{};
     W.counters = keep;
-    c->h_keys = c->h_iota = nullptr;
-    c->sort_tmp = nullptr;
-    c->sort_tmp_bytes = 0;
 }
 
-// Grows the ray-entry / shading-record buffers (kept across steps).
+// Grows the ray-pass buffers (kept across steps).
 void ensure_wave(psdf_ctx* c, int64_t e_cap, int64_t r_cap, int64_t h_cap, int64_t k_cap, int64_t a_cap) {
     WaveBufs& W = c->wave;
     if (e_cap <= W.e_cap && r_cap <= W.r_cap && h_cap <= W.h_cap && k_cap <= W.k_cap && a_cap <= W.a_cap) return;
@@ -463,6 +458,7 @@ void ensure_wave(psdf_ctx* c, int64_t e_cap, int64_t r_cap, int64_t h_cap, int64
     CK(cudaMalloc(&W.e_head, sizeof(int) * e_cap));
     CK(cudaMalloc(&W.e_craw, sizeof(double) * 3 * e_cap));
     CK(cudaMalloc(&W.e_t1, sizeof(double) * e_cap));
+    CK(cudaMalloc(&W.e_ahead, sizeof(int) * e_cap));
     CK(cudaMalloc(&W.r_pos, sizeof(double) * 3 * r_cap));
     CK(cudaMalloc(&W.r_w, sizeof(double) * r_cap));
     CK(cudaMalloc(&W.r_tile, sizeof(int) * r_cap));
@@ -472,6 +468,8 @@ void ensure_wave(psdf_ctx* c, int64_t e_cap, int64_t r_cap, int64_t h_cap, int64
     CK(cudaMalloc(&W.r_up, sizeof(float4) * r_cap));
     // geometry records sized for the widest supported channel configuration
     CK(cudaMalloc(&W.r_geo, sizeof(float) * (size_t)GeoRec<8, 8>::STRIDE * r_cap));
+    CK(cudaMalloc(&W.r_perm, sizeof(int) * r_cap));
+    CK(cudaMalloc(&W.r_fg, sizeof(float) * (size_t)FgDims<8, 8>::STRIDE * r_cap));
     CK(cudaMalloc(&W.h_slot, sizeof(int) * h_cap));
     CK(cudaMalloc(&W.h_count, sizeof(int) * h_cap));
     CK(cudaMalloc(&W.h_tileprev, sizeof(int) * h_cap));
@@ -479,132 +477,130 @@ void ensure_wave(psdf_ctx* c, int64_t e_cap, int64_t r_cap, int64_t h_cap, int64
     CK(cudaMalloc(&W.h_tprev, sizeof(double) * h_cap));
     CK(cudaMalloc(&W.h_dir, sizeof(double) * 3 * h_cap));
     CK(cudaMalloc(&W.h_t1, sizeof(double) * h_cap));
-    CK(cudaMalloc(&W.h_perm, sizeof(int) * h_cap));
-    CK(cudaMalloc(&W.r_perm, sizeof(int) * r_cap));
-    CK(cudaMalloc(&W.r_fg, sizeof(float) * (size_t)FgDims<8, 8>::STRIDE * r_cap));
-    const int64_t key_cap = std::max(h_cap, r_cap);
-    CK(cudaMalloc(&c->h_keys, sizeof(int) * key_cap));
-    CK(cudaMalloc(&c->h_iota, sizeof(int) * key_cap));
-    iota_kernel<<<(unsigned)((key_cap + 255) / 256), 256, 0, c->stream>>>(c->h_iota, (int)key_cap);
-    CK(cudaGetLastError());
-    size_t tb_h = 0, tb_r = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb_h, W.h_slot, c->h_keys, c->h_iota, W.h_perm,
-                                       (int)h_cap, 0, 31, c->stream));
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb_r, W.r_tile, c->h_keys, c->h_iota, W.r_perm,
-                                       (int)r_cap, 0, 31, c->stream));
-    c->sort_tmp_bytes = std::max(tb_h, tb_r);
-    CK(cudaMalloc(&c->sort_tmp, c->sort_tmp_bytes));
-    W.e_cap = (int)e_cap;
-    W.r_cap = (int)r_cap;
-    W.h_cap = (int)h_cap;
     CK(cudaMalloc(&W.k_rec, sizeof(ContRec) * k_cap));
-    W.k_cap = (int)k_cap;
     CK(cudaMalloc(&W.a_t, sizeof(double) * 2 * a_cap));
     CK(cudaMalloc(&W.a_s, sizeof(double) * 3 * a_cap));
     CK(cudaMalloc(&W.a_i, sizeof(int4) * a_cap));
-    CK(cudaMalloc(&W.e_ahead, sizeof(int) * e_cap));
+    W.e_cap = (int)e_cap;
+    W.r_cap = (int)r_cap;
+    W.h_cap = (int)h_cap;
+    W.k_cap = (int)k_cap;
     W.a_cap = (int)a_cap;
 }
 
-// K2 as the wavefront pipeline K2a -> K2b -> K2d -> K2e (psdf_train.cuh).
+// Per-tile record counts / offsets of the counting sort, and its scan storage.
+void ensure_tile_sort(psdf_ctx* c) {
+    const int T = c->desc.T;
+    if (T <= c->tsort_cap) return;
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->d_tile_cnt) cudaFree(c->d_tile_cnt);
+    if (c->scan_tmp) cudaFree(c->scan_tmp);
+    c->d_tile_cnt = nullptr;
+    c->scan_tmp = nullptr;
+    CK(cudaMalloc(&c->d_tile_cnt, sizeof(int) * 2 * (size_t)T));
+    c->scan_tmp_bytes = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, c->scan_tmp_bytes, c->d_tile_cnt, c->d_tile_cnt + T, T, c->stream));
+    CK(cudaMalloc(&c->scan_tmp, std::max<size_t>(c->scan_tmp_bytes, 16)));
+    c->tsort_cap = T;
+}
+
+// After the step's final synchronisation: true (and larger buffers) when the
+// ray pass overflowed one of them; the caller redoes the pass.
+bool wave_overflowed(psdf_ctx* c) {
+    const unsigned* h = c->h_wave_counters;
+    const WaveBufs& W = c->wave;
+    if (h[0] <= (unsigned)W.e_cap && h[1] <= (unsigned)W.r_cap && h[2] <= (unsigned)W.h_cap &&
+        h[3] <= (unsigned)W.k_cap && h[4] <= (unsigned)W.a_cap)
+        return false;
+    auto grow = [](unsigned n) { return (int64_t)n + n / 2 + 4096; };
+    ensure_wave(c, grow(h[0]), grow(h[1]), grow(h[2]), grow(h[3]), grow(h[4]));
+    return true;
+}
+
+// K2 as the wavefront pipeline K2a-scan -> K2a (two rounds) -> [records by
+// tile] -> K2b -> K2d -> K2e (psdf_train.cuh), with no host round trip: the
+// kernels read their item counts on device, the counters are copied back with
+// the step's results (wave_overflowed() checks them).
 template <int NS, int NA>
 void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     cudaStream_t s = c->stream;
     const int64_t n_work = P.tile_end - P.tile_begin;
-    if (c->wave.e_cap == 0)
-        ensure_wave(c, n_rays / 8 + 65536, n_rays / 8 + 65536, n_rays / 2 + 65536, n_rays / 16 + 65536,
-                    n_rays / 8 + 65536);
+    if (c->wave.e_cap == 0) {
+        if (c->wave_init > 0)  // tests: force the overflow / redo path
+            ensure_wave(c, c->wave_init, c->wave_init, c->wave_init, c->wave_init, c->wave_init);
+        else
+            ensure_wave(c, n_rays / 8 + 65536, n_rays / 8 + 65536, n_rays / 2 + 65536, n_rays / 16 + 65536,
+                        n_rays / 8 + 65536);
+    }
+    ensure_tile_sort(c);
     const size_t smem_f = render_smem_bytes<NS, NA>();
     const size_t smem_b = shade_bwd_smem_bytes<NS, NA>();
-    CK(cudaFuncSetAttribute(shade_fwd_kernel<NS, NA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
-    CK(cudaFuncSetAttribute(shade_fwd_kernel<NS, NA, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
-    CK(cudaFuncSetAttribute(shade_bwd_kernel<NS, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
     const size_t smem_bits = sizeof(uint32_t) * P.bits_sm_words;
-    CK(cudaFuncSetAttribute(march_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bits));
-    CK(cudaFuncSetAttribute(march_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bits));
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(shade_fwd_kernel<NS, NA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
+        CK(cudaFuncSetAttribute(shade_fwd_kernel<NS, NA, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
+        CK(cudaFuncSetAttribute(shade_bwd_kernel<NS, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
+        CK(cudaFuncSetAttribute(march_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(sizeof(uint32_t) * kMaxSmemBitWords)));
+        CK(cudaFuncSetAttribute(march_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(sizeof(uint32_t) * kMaxSmemBitWords)));
+        attr = true;
+    }
     const int per_sm_s = blocks_per_sm((const void*)march_scan_kernel, smem_bits);
     const int64_t grid_s = std::max<int64_t>(1, std::min<int64_t>((n_work + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
                                                                    (int64_t)per_sm_s * c->sm_count));
-    const int per_sm_a = blocks_per_sm((const void*)march_fwd_kernel, smem_bits);
-    const int64_t grid_a = (int64_t)per_sm_a * c->sm_count;
+    const int grid_a = blocks_per_sm((const void*)march_fwd_kernel, smem_bits) * c->sm_count;
+    const WaveBufs& W = c->wave;
     CK(cudaEventRecord(c->ev_ray0, s));
     CK(cudaEventRecord(c->ev_k[0], s));
-    for (int attempt = 0;; ++attempt) {
-        CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
-        CK(cudaMemsetAsync(c->wave.counters, 0, sizeof(unsigned) * 8, s));
-        P.work_counter = c->d_work;
-        if (c->n_view_ready == 0) {
-            P.scan_lo = 0;
-            P.scan_hi = n_work;
-            march_scan_kernel<<<(unsigned)grid_s, BLOCK, smem_bits, s>>>(P, c->wave);
-            CK(cudaGetLastError());
-        } else {
-            // psdf_train_step: each view's scan starts as soon as its images
-            // have arrived (the copies of the next views overlap it)
-            for (int v = 0; v < c->n_view_ready; ++v) {
-                const int64_t lo = std::max<int64_t>(c->view_tiles[v], P.tile_begin) - P.tile_begin;
-                const int64_t hi = std::min<int64_t>(c->view_tiles[v + 1], P.tile_end) - P.tile_begin;
-                if (hi <= lo) continue;
-                CK(cudaStreamWaitEvent(s, c->view_ready[v], 0));
-                CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
-                RayPassParams Pv = P;
-                Pv.scan_lo = lo;
-                Pv.scan_hi = hi;
-                const int64_t gv = std::max<int64_t>(1, std::min<int64_t>((hi - lo + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
-                                                                          (int64_t)per_sm_s * c->sm_count));
-                march_scan_kernel<<<(unsigned)gv, BLOCK, smem_bits, s>>>(Pv, c->wave);
-                CK(cudaGetLastError());
-                ++c->last_launches;
-            }
-        }
-        CK(cudaMemcpyAsync(c->h_wave_counters + 2, c->wave.counters + 2, sizeof(unsigned),
-                           cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        const int64_t nh = c->h_wave_counters[2];
-        int64_t ne = 0, nr = 0, nk = 0, na = 0;
-        if (nh <= c->wave.h_cap) {
-            // handovers in image order: coherent warps in K2a and coherent
-            // shading records downstream
-            if (nh > 0) {
-                int end_bit = 1;
-                while (end_bit < 31 && ((int64_t)1 << end_bit) < n_work * 32) ++end_bit;
-                CK(cub::DeviceRadixSort::SortPairs(c->sort_tmp, c->sort_tmp_bytes, c->wave.h_slot, c->h_keys,
-                                                   c->h_iota, c->wave.h_perm, (int)nh, 0, end_bit, s));
-            }
+    CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(W.counters, 0, sizeof(unsigned) * 8, s));
+    P.work_counter = c->d_work;
+    if (c->n_view_ready == 0) {
+        P.scan_lo = 0;
+        P.scan_hi = n_work;
+        march_scan_kernel<<<(unsigned)grid_s, BLOCK, smem_bits, s>>>(P, W);
+        CK(cudaGetLastError());
+        ++c->last_launches;
+    } else {
+        // psdf_train_step: each view's scan starts as soon as its images have
+        // arrived (the copies of the next views overlap it)
+        for (int v = 0; v < c->n_view_ready; ++v) {
+            const int64_t lo = std::max<int64_t>(c->view_tiles[v], P.tile_begin) - P.tile_begin;
+            const int64_t hi = std::min<int64_t>(c->view_tiles[v + 1], P.tile_end) - P.tile_begin;
+            if (hi <= lo) continue;
+            CK(cudaStreamWaitEvent(s, c->view_ready[v], 0));
             CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
-            // (render: one round; its rays are short at the render tau)
-            march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, c->wave, 0,
-                                                                        P.mode == 1 ? INT_MAX : c->composite_steps);
+            RayPassParams Pv = P;
+            Pv.scan_lo = lo;
+            Pv.scan_hi = hi;
+            const int64_t gv = std::max<int64_t>(1, std::min<int64_t>((hi - lo + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
+                                                                      (int64_t)per_sm_s * c->sm_count));
+            march_scan_kernel<<<(unsigned)gv, BLOCK, smem_bits, s>>>(Pv, W);
             CK(cudaGetLastError());
-            CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
-            march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, c->wave, 1, INT_MAX);
-            CK(cudaGetLastError());
-            c->last_launches += 3;
-            CK(cudaMemcpyAsync(c->h_wave_counters, c->wave.counters, sizeof(unsigned) * 8,
-                               cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            ne = c->h_wave_counters[0];
-            nr = c->h_wave_counters[1];
-            nk = c->h_wave_counters[3];
-            na = c->h_wave_counters[4];
-            if (ne <= c->wave.e_cap && nr <= c->wave.r_cap && nk <= c->wave.k_cap && na <= c->wave.a_cap) break;
+            ++c->last_launches;
         }
-        if (attempt > 2) fail(PSDF_ERR_RUNTIME, "ray pass buffers failed to grow");
-        ensure_wave(c, ne + ne / 2 + 4096, nr + nr / 2 + 4096, nh + nh / 2 + 4096, nk + nk / 2 + 4096,
-                    na + na / 2 + 4096);
-        // the failed sweep already accumulated statistics: clear and redo
-        CK(cudaMemsetAsync(c->d_counts, 0, sizeof(unsigned long long) * 8, s));
-        CK(cudaMemsetAsync(c->d_stats, 0, sizeof(double) * 16, s));
-        CK(cudaEventRecord(c->ev_ray0, s));
-        CK(cudaEventRecord(c->ev_k[0], s));
     }
-    const int n_ent = (int)c->h_wave_counters[0], n_rec = (int)c->h_wave_counters[1];
+    // handovers in append order: a warp's handovers come from one 8x4 pixel
+    // tile and neighbouring warps from neighbouring work tiles (a sort by
+    // pixel measured slower than it saved)
+    CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
+    // (render: one round; its rays are short at the render tau)
+    march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, W, 0, P.mode == 1 ? INT_MAX : c->composite_steps);
+    CK(cudaGetLastError());
+    CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
+    march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, W, 1, INT_MAX);
+    CK(cudaGetLastError());
+    c->last_launches += 2;
     if (getenv("PSDF_DEBUG_MARCH")) {
         unsigned long long cc[8];
+        unsigned hw[8];
+        CK(cudaStreamSynchronize(s));
         CK(cudaMemcpy(cc, c->d_counts, sizeof cc, cudaMemcpyDeviceToHost));
-        fprintf(stderr, "[psdf] march exact fallbacks: %llu; handovers %u entries %u records %u continuations %u alpha samples %u\n",
-                cc[6], c->h_wave_counters[2], c->h_wave_counters[0], c->h_wave_counters[1], c->h_wave_counters[3],
-                c->h_wave_counters[4]);
+        CK(cudaMemcpy(hw, W.counters, sizeof hw, cudaMemcpyDeviceToHost));
+        fprintf(stderr, "[psdf] march exact fallbacks: %llu; handovers %u entries %u records %u continuations %u "
+                "alpha samples %u\n", cc[6], hw[2], hw[0], hw[1], hw[3], hw[4]);
 #ifdef PSDF_MARCH_STATS
         unsigned long long st[12];
         CK(cudaMemcpyFromSymbol(st, g_march_stats, sizeof st));
@@ -612,62 +608,58 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
         CK(cudaMemcpyToSymbol(g_march_stats, zero, sizeof zero));
         fprintf(stderr, "[psdf] march stats: rays %llu in-box %llu iters %llu samples %llu jumps %llu "
                 "skips %llu exact %llu rewinds %llu sat-runs %llu run-samples %llu | probe groups %llu members %llu\n", st[0], st[1], st[2], st[3], st[4], st[5], st[6], st[7], st[8], st[9], st[10], st[11]);
+        unsigned long long hh[2][16];
+        CK(cudaMemcpyFromSymbol(hh, g_cont_hist, sizeof hh));
+        const unsigned long long z2[2][16] = {};
+        CK(cudaMemcpyToSymbol(g_cont_hist, z2, sizeof z2));
+        for (int r = 0; r < 2; ++r) {
+            fprintf(stderr, "[psdf] K2a round %d rays by steps [2^(b-1), 2^b):", r);
+            for (int b = 0; b < 16; ++b) fprintf(stderr, " %llu", hh[r][b]);
+            fprintf(stderr, "\n");
+        }
 #endif
     }
-    c->last_entries = n_ent;
-    c->last_records = n_rec;
-    // shading records in tile order (K2b / K2e): decode gathers and the
-    // per-tile probe / plane gradient aggregation see runs of one tile
-    if (n_rec > 0) {
-        int end_bit = 1;
-        while (end_bit < 31 && ((int64_t)1 << end_bit) < c->desc.T) ++end_bit;
-        CK(cub::DeviceRadixSort::SortPairs(c->sort_tmp, c->sort_tmp_bytes, c->wave.r_tile, c->h_keys, c->h_iota,
-                                           c->wave.r_perm, n_rec, 0, end_bit, s));
-    }
+    // shading records grouped by tile (K2b / K2e order)
+    const int T = c->desc.T;
+    const int grid_c = 4 * c->sm_count;
+    CK(cudaMemsetAsync(c->d_tile_cnt, 0, sizeof(int) * T, s));
+    rec_tile_count_kernel<<<grid_c, 256, 0, s>>>(W, c->d_tile_cnt);
+    CK(cudaGetLastError());
+    CK(cub::DeviceScan::ExclusiveSum(c->scan_tmp, c->scan_tmp_bytes, c->d_tile_cnt, c->d_tile_cnt + T, T, s));
+    rec_tile_scatter_kernel<<<grid_c, 256, 0, s>>>(W, c->d_tile_cnt + T);
+    CK(cudaGetLastError());
+    c->last_launches += 3;
     CK(cudaEventRecord(c->ev_k[1], s));
-    if (n_rec > 0) {
-        const int per_sm = blocks_per_sm((const void*)shade_fwd_kernel<NS, NA, true>, smem_f);
-        const int grid = (int)std::min<int64_t>((n_rec + BLOCK - 1) / BLOCK, (int64_t)per_sm * c->sm_count);
-        if (P.mode == 1)  // render: no geometry records for a backward
-            shade_fwd_kernel<NS, NA, false><<<grid, BLOCK, smem_f, s>>>(P, c->wave, n_rec);
-        else
-            shade_fwd_kernel<NS, NA, true><<<grid, BLOCK, smem_f, s>>>(P, c->wave, n_rec);
-        CK(cudaGetLastError());
-        ++c->last_launches;
-    }
+    const int grid_f = blocks_per_sm((const void*)shade_fwd_kernel<NS, NA, true>, smem_f) * c->sm_count;
+    if (P.mode == 1)  // render: no geometry records for a backward
+        shade_fwd_kernel<NS, NA, false><<<grid_f, BLOCK, smem_f, s>>>(P, W);
+    else
+        shade_fwd_kernel<NS, NA, true><<<grid_f, BLOCK, smem_f, s>>>(P, W);
+    CK(cudaGetLastError());
+    ++c->last_launches;
     CK(cudaEventRecord(c->ev_k[2], s));
     if (P.mode == 1) {  // render: colours of the shaded rays, no backward
-        if (n_ent > 0) {
-            render_finish_kernel<<<(unsigned)std::min<int64_t>((n_ent + BLOCK - 1) / BLOCK, 4 * c->sm_count), BLOCK, 0,
-                                   s>>>(P, c->wave, n_ent);
-            CK(cudaGetLastError());
-            ++c->last_launches;
-        }
-        for (int k = 3; k <= 4; ++k) CK(cudaEventRecord(c->ev_k[k], s));
-        CK(cudaEventRecord(c->ev_ray1, s));
-        return;
-    }
-    if (n_ent > 0) {
-        const int per_sm = blocks_per_sm((const void*)alpha_bwd_kernel, 0);
-        const int grid = (int)std::min<int64_t>((n_ent + BLOCK - 1) / BLOCK, (int64_t)per_sm * c->sm_count);
-        alpha_bwd_kernel<<<grid, BLOCK, 0, s>>>(P, c->wave, n_ent);
+        render_finish_kernel<<<4 * c->sm_count, BLOCK, 0, s>>>(P, W);
         CK(cudaGetLastError());
         ++c->last_launches;
-    }
-    CK(cudaEventRecord(c->ev_k[3], s));
-    if (n_rec > 0) {
-        const int per_sm = blocks_per_sm((const void*)shade_bwd_kernel<NS, NA>, smem_b);
-        const int grid = (int)std::min<int64_t>((n_rec + BLOCK - 1) / BLOCK, (int64_t)per_sm * c->sm_count);
-        shade_bwd_kernel<NS, NA><<<grid, BLOCK, smem_b, s>>>(P, c->wave, n_rec);
+        for (int k = 3; k <= 4; ++k) CK(cudaEventRecord(c->ev_k[k], s));
+    } else {
+        const int grid_ab = blocks_per_sm((const void*)alpha_bwd_kernel, 0) * c->sm_count;
+        alpha_bwd_kernel<<<grid_ab, BLOCK, 0, s>>>(P, W);
         CK(cudaGetLastError());
-        const int per_sm_g = blocks_per_sm((const void*)shade_geo_kernel<NS, NA>, 0);
-        const int grid_g = (int)std::min<int64_t>((n_rec + BLOCK - 1) / BLOCK, (int64_t)per_sm_g * c->sm_count);
-        shade_geo_kernel<NS, NA><<<grid_g, BLOCK, 0, s>>>(P, c->wave, n_rec);
+        CK(cudaEventRecord(c->ev_k[3], s));
+        const int grid_b = blocks_per_sm((const void*)shade_bwd_kernel<NS, NA>, smem_b) * c->sm_count;
+        shade_bwd_kernel<NS, NA><<<grid_b, BLOCK, smem_b, s>>>(P, W);
         CK(cudaGetLastError());
-        c->last_launches += 2;
+        const int grid_g = blocks_per_sm((const void*)shade_geo_kernel<NS, NA>, 0) * c->sm_count;
+        shade_geo_kernel<NS, NA><<<grid_g, BLOCK, 0, s>>>(P, W);
+        CK(cudaGetLastError());
+        c->last_launches += 3;
+        CK(cudaEventRecord(c->ev_k[4], s));
     }
-    CK(cudaEventRecord(c->ev_k[4], s));
     CK(cudaEventRecord(c->ev_ray1, s));
+    // the pass's counters come back with the step's results
+    CK(cudaMemcpyAsync(c->h_wave_counters, W.counters, sizeof(unsigned) * 8, cudaMemcpyDeviceToHost, s));
 }
 
 RayPassParams base_params(psdf_ctx* c) {
@@ -716,20 +708,24 @@ void do_render(psdf_ctx* c, const psdf_camera* cam, const psdf_render_opts* opt,
     P.out_rgb = d_rgb;
     P.out_alpha = d_alpha;
     P.out_depth = d_depth;
-    CK(cudaMemsetAsync(c->d_counts, 0, sizeof(unsigned long long) * 8, c->stream));
-    CK(cudaMemsetAsync(c->d_stats, 0, sizeof(double) * 16, c->stream));
-    prepare_sat(c, P.early_stop > 1.0 ? 0.0 : P.tau);
     // K1 through the ray-pass pipeline (scan -> composite -> decode -> finish)
     P.mode = 1;
     const int64_t n_rays = (int64_t)cam->width * cam->height;
-    dispatch_channels(c->desc.n_s, c->desc.n_a, [&]<int NS, int NA>() {
-        launch_train_raypass<NS, NA>(c, P, n_rays);
-    });
-    if (counts) {
-        CK(cudaMemcpyAsync(c->h_counts, c->d_counts, sizeof(unsigned long long) * 8,
-                           cudaMemcpyDeviceToHost, c->stream));
+    for (int attempt = 0;; ++attempt) {
+        CK(cudaMemsetAsync(c->d_counts, 0, sizeof(unsigned long long) * 8, c->stream));
+        CK(cudaMemsetAsync(c->d_stats, 0, sizeof(double) * 16, c->stream));
+        prepare_sat(c, P.early_stop > 1.0 ? 0.0 : P.tau);
+        dispatch_channels(c->desc.n_s, c->desc.n_a, [&]<int NS, int NA>() {
+            launch_train_raypass<NS, NA>(c, P, n_rays);
+        });
+        if (counts) {
+            CK(cudaMemcpyAsync(c->h_counts, c->d_counts, sizeof(unsigned long long) * 8,
+                               cudaMemcpyDeviceToHost, c->stream));
+        }
+        CK(cudaStreamSynchronize(c->stream));
+        if (!wave_overflowed(c)) break;
+        if (attempt >= 2) fail(PSDF_ERR_RUNTIME, "ray pass buffers failed to grow");
     }
-    CK(cudaStreamSynchronize(c->stream));
     CK(cudaEventElapsedTime(&c->last_ray_ms, c->ev_ray0, c->ev_ray1));
     c->last_step_ms = c->last_ray_ms;
     if (counts) {
@@ -744,7 +740,8 @@ void do_render(psdf_ctx* c, const psdf_camera* cam, const psdf_render_opts* opt,
 
 // One train step over device-resident views (trainer.cpp:136-195).
 void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_step_params* hp,
-                   psdf_losses* losses, psdf_counts* counts, cudaEvent_t images_ready = nullptr) {
+                   psdf_losses* losses, psdf_counts* counts, cudaEvent_t images_ready = nullptr,
+                   int attempt = 0) {
     need_grid(c);
     if (!hp) fail(PSDF_ERR_INVALID_ARGUMENT, "null step parameters");
     if (batch.empty()) fail(PSDF_ERR_INVALID_ARGUMENT, "empty batch");
@@ -828,6 +825,10 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
     dispatch_channels(c->desc.n_s, c->desc.n_a, [&]<int NS, int NA>() {
         launch_train_raypass<NS, NA>(c, P, n_rays);
     });
+    // counts[7]: a wave buffer overflowed (summed over ranks below, so every
+    // rank skips Adam and redoes the step)
+    wave_overflow_kernel<<<1, 32, 0, s>>>(c->wave, c->d_counts + 7);
+    CK(cudaGetLastError());
     if (c->keep_raypass) {
         CK(cudaMemcpyAsync(c->d_grads0, c->d_grads, sizeof(float) * c->n_params,
                            cudaMemcpyDeviceToDevice, s));
@@ -849,7 +850,7 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
     const double c2 = 1.0 - std::pow(0.995, (double)c->adam_t);
     adam_kernel<<<(unsigned)std::min<int64_t>(8 * c->sm_count, c->n_params / 1024 + 1), 256, 0, s>>>(
         c->d_params, c->d_grads, c->d_m, c->d_v, c->n_params, c->off_probes, (float)hp->lr_vox,
-        (float)hp->lr_mlp, (float)(1.0 / c1), (float)(1.0 / c2));
+        (float)hp->lr_mlp, (float)(1.0 / c1), (float)(1.0 / c2), c->d_counts + 7);
     CK(cudaGetLastError());
     ++c->last_launches;
     // re-smoothing (trainer.cpp:195)
@@ -859,6 +860,15 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
                        cudaMemcpyDeviceToHost, s));
     CK(cudaEventRecord(c->ev_step1, s));
     CK(cudaStreamSynchronize(s));
+    if (c->h_counts[7] != 0) {  // some rank's ray pass overflowed: Adam was skipped
+        c->adam_t -= 1;
+        wave_overflowed(c);
+        if (attempt >= 2) fail(PSDF_ERR_RUNTIME, "ray pass buffers failed to grow");
+        do_train_step(c, batch, hp, losses, counts, nullptr, attempt + 1);
+        return;
+    }
+    c->last_entries = c->h_wave_counters[0];
+    c->last_records = c->h_wave_counters[1];
     CK(cudaEventElapsedTime(&c->last_ray_ms, c->ev_ray0, c->ev_ray1));
     CK(cudaEventElapsedTime(&c->last_step_ms, c->ev_step0, c->ev_step1));
     for (int k = 0; k < 4; ++k) CK(cudaEventElapsedTime(&c->last_k2_ms[k], c->ev_k[k], c->ev_k[k + 1]));
@@ -935,6 +945,7 @@ int psdf_create(int device, psdf_ctx** out) {
         CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         if (const char* e = std::getenv("PSDF_COMPOSITE_STEPS")) c->composite_steps = std::max(1, std::atoi(e));
+        if (const char* e = std::getenv("PSDF_WAVE_INIT")) c->wave_init = std::max(0, std::atoi(e));
         CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&c->ev_copied, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_copy_free, cudaEventDisableTiming));
@@ -970,6 +981,8 @@ int psdf_destroy(psdf_ctx* c) {
             if (p) cudaFree(p);
         free_wave(c);
         if (c->wave.counters) cudaFree(c->wave.counters);
+        if (c->d_tile_cnt) cudaFree(c->d_tile_cnt);
+        if (c->scan_tmp) cudaFree(c->scan_tmp);
         if (c->h_wave_counters) cudaFreeHost(c->h_wave_counters);
         for (auto& e : c->ev_k) cudaEventDestroy(e);
         if (c->h_stats) cudaFreeHost(c->h_stats);

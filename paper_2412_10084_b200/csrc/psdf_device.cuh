@@ -325,6 +325,7 @@ __device__ __noinline__ int4 exact_tile(GridLite g, D3 o, D3 d, double t) {
 // diagnostics build only: [rays, in box, loop iterations, samples, jumps,
 // fast skips, exact fallbacks, rewinds]
 __device__ unsigned long long g_march_stats[12];
+__device__ unsigned long long g_cont_hist[2][16];  // K2a rays by log2(steps), per round
 #define PSDF_STAT(i) atomicAdd(&g_march_stats[i], 1ull)
 #else
 #define PSDF_STAT(i) ((void)0)

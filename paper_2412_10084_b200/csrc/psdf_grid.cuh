@@ -603,7 +603,9 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p,
                                                    const float* __restrict__ gr,
                                                    float* __restrict__ m, float* __restrict__ v,
                                                    int64_t n, int64_t n_vox, float lr_vox,
-                                                   float lr_mlp, float inv_c1, float inv_c2) {
+                                                   float lr_mlp, float inv_c1, float inv_c2,
+                                                   const unsigned long long* __restrict__ skip) {
+    if (*skip) return;  // the ray pass overflowed a buffer: the step is redone
     const float b1 = 0.9f, b2 = 0.995f, eps = 1e-8f;
     const int64_t n4 = n >> 2;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;

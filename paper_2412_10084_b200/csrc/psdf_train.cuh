@@ -77,8 +77,7 @@ struct WaveBufs {
     double* h_tprev;   // t of the last saturated sample
     double* h_dir;     // [cap][3]
     double* h_t1;      // box exit
-    int* h_perm;       // handovers sorted by slot (image order; CUB radix sort)
-    int* r_perm;       // shading records sorted by tile (K2b / K2e order)
+    int* r_perm;       // shading records grouped by tile (K2b / K2e order; rec_tile_*_kernel)
     float* r_fg;       // [cap][FgDims::STRIDE] feature gradients (K2e-mlp -> K2e-geo)
     ContRec* k_rec;    // continuations: rays still alive after K2a's first round
     // alpha samples (K2a -> K2d): every settle with alpha > 0, linked per ray
@@ -92,6 +91,10 @@ struct WaveBufs {
     unsigned* counters;  // [0] entries, [1] records, [2] handovers, [3] continuations, [4] alpha samples
     int e_cap, r_cap, h_cap, k_cap, a_cap;
 };
+
+// Items in the entry / record queues, read on device (clamped to capacity).
+__device__ __forceinline__ int n_entries(const WaveBufs& W) { return (int)min(*(volatile unsigned*)W.counters, (unsigned)W.e_cap); }
+__device__ __forceinline__ int n_records(const WaveBufs& W) { return (int)min(*(volatile unsigned*)(W.counters + 1), (unsigned)W.r_cap); }
 
 // Warp-aggregated slot allocation inside divergent code.
 __device__ __forceinline__ int warp_alloc(unsigned* counter, bool want, int lane) {
@@ -296,7 +299,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
         base = __shfl_sync(FULL, base, 0);
         if (base >= n_hand) break;
         const bool valid = base + lane < n_hand;
-        const int hi = valid ? (round == 0 ? W.h_perm[base + lane] : base + lane) : 0;
+        const int hi = valid ? base + lane : 0;
         const ContRec* kr = W.k_rec + hi;
         const int slot = valid ? (round == 0 ? W.h_slot[hi] : kr->slot) : 0;
         const LaneRay R = lane_ray(P, slot >> 5, slot & 31);
@@ -345,7 +348,13 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
         // keep the loop small): fetch the next march sample (or the
         // one-past-the-end position), evaluate its sigmoid, then settle the
         // alpha of the previous sample.
+#ifdef PSDF_MARCH_STATS
+        int nsteps = 0;
+#endif
         for (int step = 0; __any_sync(FULL, alive); ++step) {
+#ifdef PSDF_MARCH_STATS
+            nsteps += alive ? 1 : 0;
+#endif
             if (step == cap) {  // warp-uniform: hand the remaining rays to round 1
                 const unsigned km = __ballot_sync(FULL, alive);
                 unsigned kb = 0;
@@ -498,6 +507,9 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
                 a_cur = a_nxt;
             }
         }
+#ifdef PSDF_MARCH_STATS
+        if (valid && !cont) atomicAdd(&g_cont_hist[round][min(15, 32 - __clz(nsteps))], 1ull);
+#endif
         if (cont) continue;
         c_m += n_live;
         if (valid) c_ex += mr.n_exact;
@@ -561,7 +573,8 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
 
 // K1 tail: colour of every rendered ray with shaded samples, c_raw + bg (1 - acc)
 // (renderer.cpp:330-335).
-__global__ void __launch_bounds__(BLOCK) render_finish_kernel(RayPassParams P, WaveBufs W, int n_ent) {
+__global__ void __launch_bounds__(BLOCK) render_finish_kernel(RayPassParams P, WaveBufs W) {
+    const int n_ent = n_entries(W);
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_ent; e += gridDim.x * blockDim.x) {
         if (W.e_head[e] < 0) continue;
         const int slot = W.e_slot[e];
@@ -580,9 +593,56 @@ __device__ __forceinline__ const ViewDev& entry_view(const RayPassParams& P, con
     return P.views[locate_view(P, P.tile_begin + (slot >> 5))];
 }
 
+// ------------------------------------------------------------------ counts
+// The ray pass runs without host round trips: every kernel after K2a reads
+// its item count from the wave counters (clamped to the buffer capacity; an
+// overflow is detected by the host after the step and the step is redone with
+// larger buffers, Adam being skipped on device meanwhile).
+
+// 1 in *flag when any wave buffer overflowed this pass (the step is redone).
+__global__ void wave_overflow_kernel(WaveBufs W, unsigned long long* flag) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const unsigned* c = W.counters;
+        const bool over = c[0] > (unsigned)W.e_cap || c[1] > (unsigned)W.r_cap || c[2] > (unsigned)W.h_cap ||
+                          c[3] > (unsigned)W.k_cap || c[4] > (unsigned)W.a_cap;
+        *flag = over ? 1ull : 0ull;
+    }
+}
+
+// Shading records grouped by tile (K2b / K2e order: decode gathers and the
+// per-tile probe / plane gradient aggregation see runs of one tile): a
+// counting sort, warp-aggregated per tile with __match_any_sync.
+__global__ void __launch_bounds__(256) rec_tile_count_kernel(WaveBufs W, int* __restrict__ cnt) {
+    const int n = n_records(W);
+    const int lane = threadIdx.x & 31;
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    for (int b = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; b < n; b += warps * 32) {
+        const int i = b + lane;
+        const int t = i < n ? W.r_tile[i] : -1;
+        const unsigned m = __match_any_sync(FULL, t);
+        if (t >= 0 && lane == __ffs(m) - 1) atomicAdd(cnt + t, __popc(m));
+    }
+}
+__global__ void __launch_bounds__(256) rec_tile_scatter_kernel(WaveBufs W, int* __restrict__ off) {
+    const int n = n_records(W);
+    const int lane = threadIdx.x & 31;
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    for (int b = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; b < n; b += warps * 32) {
+        const int i = b + lane;
+        const int t = i < n ? W.r_tile[i] : -1;
+        const unsigned m = __match_any_sync(FULL, t);
+        const int leader = __ffs(m) - 1;
+        int base = 0;
+        if (t >= 0 && lane == leader) base = atomicAdd(off + t, __popc(m));
+        base = __shfl_sync(FULL, base, leader);
+        if (t >= 0) W.r_perm[base + __popc(m & ((1u << lane) - 1u))] = i;
+    }
+}
+
 // ------------------------------------------------------------------ K2b
 template <int NS, int NA, bool GEO>
-__global__ void __launch_bounds__(BLOCK) shade_fwd_kernel(RayPassParams P, WaveBufs W, int n_rec) {
+__global__ void __launch_bounds__(BLOCK) shade_fwd_kernel(RayPassParams P, WaveBufs W) {
+    const int n_rec = n_records(W);
     constexpr int IN = NS + NA + NPOW;
     extern __shared__ __align__(16) float smem[];
     const SmemMlp L = SmemMlp::make(IN);
@@ -612,7 +672,8 @@ __global__ void __launch_bounds__(BLOCK) shade_fwd_kernel(RayPassParams P, WaveB
 }
 
 // ------------------------------------------------------------------ K2d
-__global__ void __launch_bounds__(BLOCK) alpha_bwd_kernel(RayPassParams P, WaveBufs W, int n_ent) {
+__global__ void __launch_bounds__(BLOCK) alpha_bwd_kernel(RayPassParams P, WaveBufs W) {
+    const int n_ent = n_entries(W);
     const int lane = threadIdx.x & 31;
     const GridView& g = P.g;
     const double tau = P.tau;
@@ -770,7 +831,8 @@ struct MmaDims {
 };
 
 template <int NS, int NA>
-__global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveBufs W, int n_rec) {
+__global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveBufs W) {
+    const int n_rec = n_records(W);
     constexpr int IN = NS + NA + NPOW;
     using D = MmaDims<IN>;
     using GR = GeoRec<NS, NA>;
@@ -1009,7 +1071,8 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
 // tile, and the SDF-gradient chain of the normal (renderer.cpp:216-235).
 constexpr int PWS = 33;  // row stride of the per-warp probe staging (w8 | Y[16] | gfa)
 template <int NS, int NA>
-__global__ void __launch_bounds__(BLOCK) shade_geo_kernel(RayPassParams P, WaveBufs W, int n_rec) {
+__global__ void __launch_bounds__(BLOCK) shade_geo_kernel(RayPassParams P, WaveBufs W) {
+    const int n_rec = n_records(W);
     __shared__ float s_pw[WARPS_PER_BLOCK][32 * PWS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* PW = s_pw[warp];

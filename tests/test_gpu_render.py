@@ -119,6 +119,21 @@ SCENES = [
 @pytest.mark.parametrize("scene", SCENES)
 @pytest.mark.parametrize("tau_vox", [0.75, 30.0, 3000.0])
 def test_render_parity(ctx, scene, tau_vox):
+    _render_parity(ctx, scene, tau_vox)
+
+
+def test_render_parity_wave_overflow(monkeypatch):
+    """Undersized ray-pass buffers: the render overflows, grows and redoes."""
+    from paper_2412_10084_b200 import api
+    monkeypatch.setenv("PSDF_WAVE_INIT", "32")
+    c = api.Context(0)
+    try:
+        _render_parity(c, SCENES[1], 0.75)
+    finally:
+        c.close()
+
+
+def _render_parity(ctx, scene, tau_vox):
     from paper_2412_10084_b200 import api
     g, a = make_scene(**scene)
     og, sm = oracle_with_f32_smooth(a)

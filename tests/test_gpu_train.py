@@ -52,6 +52,23 @@ CASES = [
 
 @pytest.mark.parametrize("case", CASES)
 def test_train_step_parity(ctx, case):
+    _train_parity(ctx, case)
+
+
+def test_train_step_parity_wave_overflow(monkeypatch):
+    """Ray-pass buffers far too small for the batch: the step overflows, Adam
+    is skipped on device, the host grows the buffers and redoes the step —
+    results identical in contract to a first-time fit."""
+    from paper_2412_10084_b200 import api
+    monkeypatch.setenv("PSDF_WAVE_INIT", "64")
+    c = api.Context(0)
+    try:
+        _train_parity(c, CASES[2])
+    finally:
+        c.close()
+
+
+def _train_parity(ctx, case):
     from paper_2412_10084_b200 import api
     from oracle.port import step_params as ostep
     from oracle.refcore import RefCamera
