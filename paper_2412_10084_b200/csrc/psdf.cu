@@ -164,6 +164,9 @@ struct psdf_ctx {
     int sm_count = 148;
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;  // host->device image staging of psdf_train_step
+    cudaStream_t side_stream = nullptr;  // low priority: regularizers under the ray pass
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool fork_regs = false;              // the ray pass records ev_fork (do_train_step)
     cudaEvent_t ev_copied = nullptr, ev_copy_free = nullptr;
     std::vector<cudaEvent_t> view_ready;   // per staged view: its images are in HBM
     int n_view_ready = 0;                  // > 0 only inside psdf_train_step
@@ -590,6 +593,7 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, W, 0, P.mode == 1 ? INT_MAX : c->composite_steps);
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
+    if (c->fork_regs) CK(cudaEventRecord(c->ev_fork, s));
     march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, W, 1, INT_MAX);
     CK(cudaGetLastError());
     c->last_launches += 2;
@@ -775,7 +779,7 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
     // read only parameters and the smoothed grid, so they run first (under
     // the host->device copy of the step's images when there is one) unless
     // the ray-pass-only gradients are kept for inspection.
-    auto regularizers = [&]() {
+    auto regularizers = [&](bool overlap) {
         const GridView g = c->view();
         const int T = c->desc.T, Pn = c->desc.P;
         const int t0 = (int)((int64_t)T * c->rank / c->world), t1 = (int)((int64_t)T * (c->rank + 1) / c->world);
@@ -788,10 +792,20 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
                                         (int)kLossGridSmem));
                 attr = true;
             }
-            loss_grid_kernel<<<t1 - t0, LG_THREADS, kLossGridSmem, s>>>(
+            // with `overlap`, the eikonal / normal / sdf kernel (the one that
+            // touches only raw gradients and, atomically, the staged SDF
+            // gradient) runs on the low-priority side stream under the ray
+            // pass, filling the SMs its kernels' tails leave idle
+            cudaStream_t sl = s;
+            if (overlap) {  // ev_fork: recorded by the ray pass after its first composite round
+                CK(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+                sl = c->side_stream;
+            }
+            loss_grid_kernel<<<t1 - t0, LG_THREADS, kLossGridSmem, sl>>>(
                 g, c->d_params + c->off_raw, t0, (float)hp->l_sdf, (float)hp->l_eik, (float)hp->l_norm,
                 (float)(1.0 / (2.0 * c->desc.voxel_size)), c->d_gsmooth, c->d_grads + c->off_raw, c->d_stats);
             CK(cudaGetLastError());
+            if (overlap) CK(cudaEventRecord(c->ev_join, c->side_stream));
             dispatch_ns(c->desc.n_s, [&]<int NS>() {
                 loss_features_kernel<NS><<<3 * (t1 - t0), 256, 0, s>>>(g, t0, (float)hp->l_feat,
                                                                        c->d_grads + c->off_planes, c->d_stats);
@@ -808,8 +822,11 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
             ++c->last_launches;
         }
     };
-    const bool regs_first = !c->keep_raypass;
-    if (regs_first) regularizers();
+    const bool overlap = !c->keep_raypass;
+    // images still arriving (psdf_train_step): the regularizer runs under the
+    // copies; resident images: under the ray pass's tail (forked by it)
+    c->fork_regs = overlap && c->n_view_ready == 0;
+    if (overlap && !c->fork_regs) CK(cudaEventRecord(c->ev_fork, s));
     if (images_ready) CK(cudaStreamWaitEvent(s, images_ready, 0));
     const int64_t tiles = upload_viewdev(c, vd);
     // ray-batch data parallelism: contiguous 1/N slice of the batch's work tiles
@@ -835,7 +852,9 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
         CK(cudaMemcpyAsync(c->d_gsmooth0, c->d_gsmooth, sizeof(float) * c->desc.T * TV,
                            cudaMemcpyDeviceToDevice, s));
     }
-    if (!regs_first) regularizers();
+    c->fork_regs = false;
+    regularizers(overlap);
+    if (overlap) CK(cudaStreamWaitEvent(s, c->ev_join, 0));
     // G^T fold (grads.cpp:67-96): raw_grad += G^T * staged
     launch_fold(c, c->d_gsmooth, c->d_grads + c->off_raw);
     // all-reduce across ranks (GradBuffers::add, trainer.cpp:184-185, across GPUs)
@@ -943,10 +962,15 @@ int psdf_create(int device, psdf_ctx** out) {
         auto* c = new psdf_ctx;
         c->device = device;
         CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
-        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        int prio_lo = 0, prio_hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi));
         if (const char* e = std::getenv("PSDF_COMPOSITE_STEPS")) c->composite_steps = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("PSDF_WAVE_INIT")) c->wave_init = std::max(0, std::atoi(e));
         CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithPriority(&c->side_stream, cudaStreamNonBlocking, prio_lo));
+        CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_copied, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_copy_free, cudaEventDisableTiming));
         CK(cudaEventRecord(c->ev_copy_free, c->stream));
@@ -994,6 +1018,9 @@ int psdf_destroy(psdf_ctx* c) {
         cudaEventDestroy(c->ev_step1);
         cudaStreamDestroy(c->stream);
         cudaStreamDestroy(c->copy_stream);
+        cudaStreamDestroy(c->side_stream);
+        cudaEventDestroy(c->ev_fork);
+        cudaEventDestroy(c->ev_join);
         cudaEventDestroy(c->ev_copied);
         cudaEventDestroy(c->ev_copy_free);
         for (auto e : c->view_ready) cudaEventDestroy(e);
