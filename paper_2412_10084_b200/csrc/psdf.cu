@@ -382,7 +382,7 @@ void launch_fold(psdf_ctx* c, const float* src, float* dst) {
                                 (int)kFoldSmem));
         attr = true;
     }
-    smooth_fold_kernel<<<c->desc.T, 256, kFoldSmem, c->stream>>>(c->view(), src, 0.f, dst, 1,
+    smooth_fold_kernel<<<c->desc.T, PSDF_FOLD_THREADS, kFoldSmem, c->stream>>>(c->view(), src, 0.f, dst, 1,
                                                                  gaussian_taps());
     CK(cudaGetLastError());
     ++c->last_launches;
@@ -406,7 +406,7 @@ void smooth_all(psdf_ctx* c) {
                                 (int)kSmoothApronSmem));
         attr = true;
     }
-    smooth_apron_kernel<<<c->desc.T, 256, kSmoothApronSmem, c->stream>>>(
+    smooth_apron_kernel<<<c->desc.T, PSDF_SMOOTH_THREADS, kSmoothApronSmem, c->stream>>>(
         c->view(), c->d_params + c->off_raw, (float)(c->desc.far_field_voxels * c->desc.voxel_size),
         c->d_smooth, c->d_smooth_ap, c->d_tile_min, c->d_block_min, gaussian_taps());
     CK(cudaGetLastError());

@@ -114,7 +114,10 @@ __device__ __forceinline__ void column_5tap(const float* __restrict__ in, int is
 // the Gaussian is symmetric, so G^T is the same stencil).  Separable 5-tap
 // column passes in shared memory.
 constexpr int FZ = HE + 1;  // padded z stride of the y-pass output (conflict-free z columns)
-__global__ void __launch_bounds__(256) smooth_fold_kernel(GridView g, const float* __restrict__ src,
+#ifndef PSDF_FOLD_THREADS
+#define PSDF_FOLD_THREADS 512
+#endif
+__global__ void __launch_bounds__(PSDF_FOLD_THREADS) smooth_fold_kernel(GridView g, const float* __restrict__ src,
                                                           float fill, float* __restrict__ dst,
                                                           int accumulate, Taps taps) {
     extern __shared__ __align__(16) float sh[];
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(256) smooth_fold_kernel(GridView g, const floa
     }
     __syncthreads();
     float* out = dst + (int64_t)t * TV;
-    {  // z pass, column (x, y): 16 consecutive voxels of the tile
+    if (threadIdx.x < 256) {  // z pass, column (x, y): 16 consecutive voxels of the tile
         const int c = threadIdx.x;  // 256 columns
         float r[16];
         column_5tap<16>(A + c * FZ, 1, r, 1, taps);
@@ -167,7 +170,10 @@ constexpr size_t kFoldSmem = sizeof(float) * (HV + 16 * HE * HE);
 constexpr int SE = 22;  // raw halo edge: local voxels [-3, 19)
 constexpr int SZ = SE + 1;  // padded z stride of the y-pass output
 constexpr size_t kSmoothApronSmem = sizeof(float) * (SE * SE * SE + AE * SE * SE);
-__global__ void __launch_bounds__(256) smooth_apron_kernel(GridView g, const float* __restrict__ raw,
+#ifndef PSDF_SMOOTH_THREADS
+#define PSDF_SMOOTH_THREADS 1024
+#endif
+__global__ void __launch_bounds__(PSDF_SMOOTH_THREADS) smooth_apron_kernel(GridView g, const float* __restrict__ raw,
                                                            float fill, float* __restrict__ smooth,
                                                            float* __restrict__ ap, float* __restrict__ tmin,
                                                            float* __restrict__ bmin, Taps taps) {

@@ -10,7 +10,7 @@ import csv
 import json
 import sys
 
-K2 = ("march_scan", "march_fwd", "RadixSort", "shade_fwd", "alpha_bwd", "shade_bwd")
+K2 = ("march_scan", "march_fwd", "rec_tile", "DeviceScan", "shade_fwd", "alpha_bwd", "shade_bwd", "shade_geo")
 COLS = {
     "time_us": ("gpu__time_duration.sum", 1e-3),
     "dram_read_MB": ("dram__bytes_read.sum", 1e-6),
