@@ -186,7 +186,7 @@ struct psdf_ctx {
     float* d_block_min = nullptr;  // [T][64] minimum of each 4^3 block's brick
     int32_t* d_tile_nbr = nullptr; // [T][27] neighbour tile ids
     int occ_tlo[3] = {0, 0, 0}, occ_thi[3] = {-1, -1, -1};  // allocated tiles' bounding box (tile coords)
-    uint8_t* d_sat_dist = nullptr; // [T][64] saturation distances of the current ray pass
+    uint8_t* d_sat_dist = nullptr; // [T][17^3] per-cell saturation distances of the current ray pass
     int composite_steps = kComposite0Steps;
     int* d_tile_cnt = nullptr;     // [2T] shading records per tile, then their offsets
     void* scan_tmp = nullptr;      // CUB scan storage of the counting sort
@@ -417,7 +417,7 @@ void smooth_all(psdf_ctx* c) {
 // with runs disabled (tau_run <= 0) every block reads as unsaturated.
 void prepare_sat(psdf_ctx* c, double tau_run) {
     if (c->desc.T == 0) return;
-    sat_dist_kernel<<<c->desc.T, 64, 0, c->stream>>>(c->view(), tau_run, c->d_sat_dist);
+    sat_dist_kernel<<<c->desc.T, 256, 0, c->stream>>>(c->view(), tau_run, c->d_sat_dist);
     CK(cudaGetLastError());
     ++c->last_launches;
 }
@@ -1157,7 +1157,7 @@ int psdf_upload_grid(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_c
         CK(cudaMalloc(&c->d_smooth_ap, sizeof(float) * std::max<int64_t>(T * AV, 4)));
         CK(cudaMalloc(&c->d_tile_min, sizeof(float) * std::max<int64_t>(T, 1)));
         CK(cudaMalloc(&c->d_block_min, sizeof(float) * std::max<int64_t>(64 * T, 1)));
-        CK(cudaMalloc(&c->d_sat_dist, std::max<int64_t>(64 * T, 1)));
+        CK(cudaMalloc(&c->d_sat_dist, std::max<int64_t>((int64_t)kCellN * T, 1)));
         CK(cudaMalloc(&c->d_gsmooth, sizeof(float) * std::max<int64_t>(T * TV, 4)));
         CK(cudaMemsetAsync(c->d_params, 0, sizeof(float) * c->n_params, c->stream));
         CK(cudaMemsetAsync(c->d_grads, 0, sizeof(float) * c->n_params, c->stream));

@@ -67,7 +67,7 @@ struct GridView {
     const float* __restrict__ smooth_ap;      // [T][18^3] smooth with a 1-voxel apron
     const float* __restrict__ tile_min;       // [T] min of each apron brick
     const float* __restrict__ block_min;      // [T][64] min over each 4^3 block's 6^3 brick
-    const uint8_t* __restrict__ sat_dist;     // [T][64] saturation distances of this pass (sat_dist_kernel)
+    const uint8_t* __restrict__ sat_dist;     // [T][17^3] per-cell saturation distances of this pass (sat_dist_kernel)
     const float* __restrict__ planes;         // [T][3][256][n_s]
     const float* __restrict__ probes;         // [P][order^2][n_a]
 };
@@ -105,6 +105,9 @@ __device__ __forceinline__ double smooth_value(const GridView& g, int vx, int vy
 
 constexpr int AE = 18;            // apron brick edge (16 + 2)
 constexpr int AV = AE * AE * AE;  // 5832
+constexpr int kCellE = 17;                          // trilinear cells b in [-1, 15] per axis
+constexpr int kCellN = kCellE * kCellE * kCellE;    // 4913
+constexpr uint8_t kCellNone = 255;                  // sat_dist: no unsaturated cell in the tile
 
 // Trilinear sum of sample_trilinear (grid.cpp:104-110) in its exact f64
 // operation order.
@@ -393,7 +396,7 @@ struct Marcher {
     bool no_jump;         // replaying after a rewind
     unsigned n_exact;     // exact-path fallbacks taken (diagnostics)
     int c_b, c_tile;      // last tile-grid cell looked up and its tile id
-    int c_blk, c_ds;      // last block (tile * 64 + block) and its saturation distance
+    int c_blk, c_ds;      // last cell (tile * 17^3 + cell) and its saturation distance
 
     __device__ __forceinline__ void setup(const GridView& g, const double* o_, const double* d_, int nmax) {
         const double inv_h = g.h_pow2 ? g.inv_h : 1.0 / g.h;
@@ -562,25 +565,27 @@ struct Marcher {
                     run.sat = false;
                     run.t_last = t;
                     if (!near && tau > 0.0) {
-                        // the 4^3 block holding the sample's voxel (p(t) off
-                        // the block faces by the margin) and its saturation
-                        // distance: every lattice point within L-inf
-                        // 4 (Ds - 1) + (distance to the block faces) voxels,
-                        // up to the tile exit, lies in a saturated block
-                        int bi = 0;
+                        // the trilinear cell holding the sample (c = v - 1/2
+                        // off the cell faces by the margin) and its
+                        // saturation distance Ds: every lattice point within
+                        // L-inf (Ds - 1) + (distance to the cell faces)
+                        // voxels, up to the tile exit, lies in a saturated
+                        // cell
+                        int ci = 0;
                         bool ok = true;
-                        double edge = 4.0;
+                        double edge = 1.0;
 #pragma unroll
                         for (int a = 0; a < 3; ++a) {
-                            const double fb = floor(r[a] * 0.25);
-                            const double rb = r[a] - 4.0 * fb;
-                            ok &= rb > kMargin && rb < 4.0 - kMargin;
-                            edge = fmin(edge, fmin(rb, 4.0 - rb));
-                            bi = bi * 4 + (int)fb;
+                            const double cc = r[a] - 0.5;
+                            const double fb = floor(cc);
+                            const double f = cc - fb;
+                            ok &= f > kMargin && f < 1.0 - kMargin;
+                            edge = fmin(edge, fmin(f, 1.0 - f));
+                            ci = ci * kCellE + ((int)fb + 1);
                         }
                         int ds = 0;
                         if (ok) {
-                            const int blk = tile_out * 64 + bi;
+                            const int blk = tile_out * kCellN + ci;
                             if (blk != c_blk) {
                                 c_blk = blk;
                                 c_ds = __ldg(g.sat_dist + blk);
@@ -590,7 +595,7 @@ struct Marcher {
                         if (ds > 0) {
                             run.sat = true;
                             double n = run_length(g, v, t, h);  // lattice points left in the tile
-                            if (ds < 4) n = fmin(n, floor((4.0 * (ds - 1) + edge - 1e-6) * dinv_max) + 1.0);
+                            if (ds != kCellNone) n = fmin(n, floor(((double)(ds - 1) + edge - 1e-6) * dinv_max) + 1.0);
                             if (n > 1.0) {
                                 const int ni = (int)fmin(n, (double)(n_max - count));
                                 run.n = ni;

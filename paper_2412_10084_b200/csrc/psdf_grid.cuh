@@ -262,28 +262,70 @@ __global__ void __launch_bounds__(256) apron_fill_kernel(GridView g, const float
     if (threadIdx.x == 0) tmin[t] = fminf(red[0], red[1]);
 }
 
-// Saturation distances for one ray pass (its tau): per 4^3 block of each tile,
-// the L-inf distance, in blocks, to the nearest block of the same tile whose
-// brick can hold a sample with sigmoid < 1 (tau * block_min < kSatX);
-// 0 = that block itself, 4 = none in the tile.  The marcher's saturated runs
-// (psdf_device.cuh, Marcher::next_run) read it.
-__global__ void __launch_bounds__(64) sat_dist_kernel(GridView g, double tau, uint8_t* __restrict__ sd) {
-    __shared__ unsigned long long unsat;
-    const int t = blockIdx.x, b = threadIdx.x;
-    if (b == 0) unsat = 0ull;
+// Saturation distances for one ray pass (its tau), per trilinear cell: cell b
+// of tile t (b in [-1, 15]^3, index b + 1 over 17^3) holds the samples whose
+// eight corners are voxels b .. b + 1 (apron brick entries b + 1 .. b + 2).  A
+// cell is unsaturated when tau * (minimum of its corners) < kSatX (a sample in
+// it can have sigmoid < 1); the value is the exact L-inf distance, in cells,
+// to the nearest unsaturated cell of the same tile (0 = the cell itself), or
+// kCellNone when the tile has none.  Separable chessboard transform: 1-D
+// distances along x, then min over y' of max(|y - y'|, d), then over z'.
+// The marcher's saturated runs (psdf_device.cuh, Marcher::next_run) read it.
+__global__ void __launch_bounds__(256) sat_dist_kernel(GridView g, double tau, uint8_t* __restrict__ sd) {
+    __shared__ float ap[AV];
+    __shared__ uint8_t A[kCellN], B[kCellN];
+    const int t = blockIdx.x;
+    const float* src = g.smooth_ap + (int64_t)t * AV;
+    for (int i = threadIdx.x; i < AV; i += blockDim.x) ap[i] = __ldg(src + i);
     __syncthreads();
-    const float bm = __ldg(g.block_min + (int64_t)t * 64 + b);
-    const bool sat = tau > 0.0 && bm > 0.0f && dmul(tau, (double)bm) >= kSatX;
-    if (!sat) atomicOr(&unsat, 1ull << b);
-    __syncthreads();
-    const int bx = b >> 4, by = (b >> 2) & 3, bz = b & 3;
-    int best = 4;
-    for (unsigned long long m = unsat; m; m &= m - 1) {
-        const int o = __ffsll((long long)m) - 1;
-        const int d = max(max(abs((o >> 4) - bx), abs(((o >> 2) & 3) - by)), abs((o & 3) - bz));
-        best = min(best, d);
+    constexpr uint8_t INF = 200;
+    int any = 0;
+    for (int i = threadIdx.x; i < kCellN; i += blockDim.x) {
+        const int bx = i / (kCellE * kCellE), by = (i / kCellE) % kCellE, bz = i % kCellE;
+        const float* p = ap + (bx * AE + by) * AE + bz;
+        float mn = fminf(fminf(fminf(p[0], p[1]), fminf(p[AE], p[AE + 1])),
+                         fminf(fminf(p[AE * AE], p[AE * AE + 1]), fminf(p[AE * AE + AE], p[AE * AE + AE + 1])));
+        const bool sat = tau > 0.0 && mn > 0.0f && dmul(tau, (double)mn) >= kSatX;
+        A[i] = sat ? INF : 0;
+        any |= !sat;
     }
-    sd[(int64_t)t * 64 + b] = (uint8_t)best;
+    uint8_t* out = sd + (int64_t)t * kCellN;
+    if (!__syncthreads_or(any)) {
+        for (int i = threadIdx.x; i < kCellN; i += blockDim.x) out[i] = kCellNone;
+        return;
+    }
+    constexpr int E = kCellE, E2 = kCellE * kCellE;
+    // x: 1-D distance along each (y, z) line, two sweeps
+    for (int l = threadIdx.x; l < E2; l += blockDim.x) {
+        uint8_t d = INF;
+        for (int x = 0; x < E; ++x) {
+            const int i = x * E2 + l;
+            d = A[i] == 0 ? 0 : (d < INF ? d + 1 : INF);
+            B[i] = d;
+        }
+        d = INF;
+        for (int x = E - 1; x >= 0; --x) {
+            const int i = x * E2 + l;
+            d = A[i] == 0 ? 0 : (d < INF ? d + 1 : INF);
+            if (d < B[i]) B[i] = d;
+        }
+    }
+    __syncthreads();
+    // y: min over y' of max(|y - y'|, B)
+    for (int i = threadIdx.x; i < kCellN; i += blockDim.x) {
+        const int x = i / E2, y = (i / E) % E, z = i % E;
+        int best = INF;
+        for (int y2 = 0; y2 < E; ++y2) best = min(best, max(abs(y - y2), (int)B[(x * E + y2) * E + z]));
+        A[i] = (uint8_t)best;
+    }
+    __syncthreads();
+    // z: min over z' of max(|z - z'|, A)
+    for (int i = threadIdx.x; i < kCellN; i += blockDim.x) {
+        const int xy = i / E, z = i % E;
+        int best = INF;
+        for (int z2 = 0; z2 < E; ++z2) best = min(best, max(abs(z - z2), (int)A[xy * E + z2]));
+        out[i] = (uint8_t)best;
+    }
 }
 
 // Block-wide sums of NV doubles, one atomic per value per block.
