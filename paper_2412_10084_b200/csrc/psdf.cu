@@ -417,7 +417,7 @@ void smooth_all(psdf_ctx* c) {
 // with runs disabled (tau_run <= 0) every block reads as unsaturated.
 void prepare_sat(psdf_ctx* c, double tau_run) {
     if (c->desc.T == 0) return;
-    sat_dist_kernel<<<c->desc.T, 256, 0, c->stream>>>(c->view(), tau_run, c->d_sat_dist);
+    sat_dist_kernel<<<c->desc.T, kSatThreads, 0, c->stream>>>(c->view(), tau_run, c->d_sat_dist);
     CK(cudaGetLastError());
     ++c->last_launches;
 }

@@ -271,61 +271,61 @@ __global__ void __launch_bounds__(256) apron_fill_kernel(GridView g, const float
 // kCellNone when the tile has none.  Separable chessboard transform: 1-D
 // distances along x, then min over y' of max(|y - y'|, d), then over z'.
 // The marcher's saturated runs (psdf_device.cuh, Marcher::next_run) read it.
-__global__ void __launch_bounds__(256) sat_dist_kernel(GridView g, double tau, uint8_t* __restrict__ sd) {
+constexpr int kSatThreads = 320;  // >= 17 * 17 rows of cells
+__global__ void __launch_bounds__(kSatThreads) sat_dist_kernel(GridView g, double tau, uint8_t* __restrict__ sd) {
+    constexpr int E = kCellE, NR = kCellE * kCellE;  // rows (x, y) of 17 cells along z: one bit each
+    constexpr uint32_t FULLROW = (1u << kCellE) - 1u;
     __shared__ float ap[AV];
-    __shared__ uint8_t A[kCellN], B[kCellN];
-    const int t = blockIdx.x;
+    __shared__ uint32_t M[2][NR];
+    __shared__ uint8_t out[kCellN];
+    const int t = blockIdx.x, r = threadIdx.x;
     const float* src = g.smooth_ap + (int64_t)t * AV;
     for (int i = threadIdx.x; i < AV; i += blockDim.x) ap[i] = __ldg(src + i);
     __syncthreads();
-    constexpr uint8_t INF = 200;
-    int any = 0;
-    for (int i = threadIdx.x; i < kCellN; i += blockDim.x) {
-        const int bx = i / (kCellE * kCellE), by = (i / kCellE) % kCellE, bz = i % kCellE;
-        const float* p = ap + (bx * AE + by) * AE + bz;
-        float mn = fminf(fminf(fminf(p[0], p[1]), fminf(p[AE], p[AE + 1])),
-                         fminf(fminf(p[AE * AE], p[AE * AE + 1]), fminf(p[AE * AE + AE], p[AE * AE + AE + 1])));
-        const bool sat = tau > 0.0 && mn > 0.0f && dmul(tau, (double)mn) >= kSatX;
-        A[i] = sat ? INF : 0;
-        any |= !sat;
-    }
-    uint8_t* out = sd + (int64_t)t * kCellN;
-    if (!__syncthreads_or(any)) {
-        for (int i = threadIdx.x; i < kCellN; i += blockDim.x) out[i] = kCellNone;
-        return;
-    }
-    constexpr int E = kCellE, E2 = kCellE * kCellE;
-    // x: 1-D distance along each (y, z) line, two sweeps
-    for (int l = threadIdx.x; l < E2; l += blockDim.x) {
-        uint8_t d = INF;
-        for (int x = 0; x < E; ++x) {
-            const int i = x * E2 + l;
-            d = A[i] == 0 ? 0 : (d < INF ? d + 1 : INF);
-            B[i] = d;
+    // unsaturated cells of row r as a bit mask
+    uint32_t m = 0;
+    const int x = r / E, y = r % E;
+    if (r < NR) {
+        const float* p = ap + (x * AE + y) * AE;
+        float c0 = fminf(fminf(p[0], p[AE]), fminf(p[AE * AE], p[AE * AE + AE]));
+        for (int z = 0; z < E; ++z) {
+            const float c1 = fminf(fminf(p[z + 1], p[AE + z + 1]), fminf(p[AE * AE + z + 1], p[AE * AE + AE + z + 1]));
+            const float mn = fminf(c0, c1);
+            const bool sat = tau > 0.0 && mn > 0.0f && dmul(tau, (double)mn) >= kSatX;
+            if (!sat) m |= 1u << z;
+            c0 = c1;
         }
-        d = INF;
-        for (int x = E - 1; x >= 0; --x) {
-            const int i = x * E2 + l;
-            d = A[i] == 0 ? 0 : (d < INF ? d + 1 : INF);
-            if (d < B[i]) B[i] = d;
+        M[0][r] = m;
+#pragma unroll
+        for (int z = 0; z < E; ++z) out[r * E + z] = ((m >> z) & 1u) ? 0 : kCellNone;
+    }
+    uint8_t* dst = sd + (int64_t)t * kCellN;
+    const int any = __syncthreads_or(m != 0);
+    if (any && !__syncthreads_and(r >= NR || m == FULLROW)) {
+        // L-inf (chessboard) distance = number of 3x3x3 dilations that reach the cell
+        int cur = 0;
+        for (int k = 1; k < E; ++k) {
+            bool full = true;
+            if (r < NR) {
+                uint32_t n = 0;
+#pragma unroll
+                for (int dx = -1; dx <= 1; ++dx)
+#pragma unroll
+                    for (int dy = -1; dy <= 1; ++dy) {
+                        const int xx = x + dx, yy = y + dy;
+                        if ((unsigned)xx < (unsigned)E && (unsigned)yy < (unsigned)E) n |= M[cur][xx * E + yy];
+                    }
+                n = (n | (n << 1) | (n >> 1)) & FULLROW;
+                for (uint32_t nw = n & ~M[cur][r]; nw; nw &= nw - 1) out[r * E + __ffs(nw) - 1] = (uint8_t)k;
+                M[cur ^ 1][r] = n;
+                full = n == FULLROW;
+            }
+            cur ^= 1;
+            if (__syncthreads_and(full)) break;
         }
     }
     __syncthreads();
-    // y: min over y' of max(|y - y'|, B)
-    for (int i = threadIdx.x; i < kCellN; i += blockDim.x) {
-        const int x = i / E2, y = (i / E) % E, z = i % E;
-        int best = INF;
-        for (int y2 = 0; y2 < E; ++y2) best = min(best, max(abs(y - y2), (int)B[(x * E + y2) * E + z]));
-        A[i] = (uint8_t)best;
-    }
-    __syncthreads();
-    // z: min over z' of max(|z - z'|, A)
-    for (int i = threadIdx.x; i < kCellN; i += blockDim.x) {
-        const int xy = i / E, z = i % E;
-        int best = INF;
-        for (int z2 = 0; z2 < E; ++z2) best = min(best, max(abs(z - z2), (int)A[xy * E + z2]));
-        out[i] = (uint8_t)best;
-    }
+    for (int i = threadIdx.x; i < kCellN; i += blockDim.x) dst[i] = out[i];
 }
 
 // Block-wide sums of NV doubles, one atomic per value per block.
