@@ -447,6 +447,27 @@ struct Marcher {
             .ok;
     }
 
+    // may_hit(), and when the ray does meet the allocated tiles' bounding box
+    // (one-voxel margin) further along, a jump (lattice argument, as in
+    // next_impl) to the last lattice point before it: every lattice point up
+    // to there lies in unallocated tiles.  Call right after init().
+    __device__ __forceinline__ bool enter_occupied(const GridView& g) {
+        if (!g.occ_any) return false;
+        const BoxHit b = ray_box(d3(o[0], o[1], o[2]), d3(d[0], d[1], d[2]), d3(inv_d[0], inv_d[1], inv_d[2]),
+                                 d3(g.occ_lo[0], g.occ_lo[1], g.occ_lo[2]),
+                                 d3(g.occ_hi[0], g.occ_hi[1], g.occ_hi[2]));
+        if (!b.ok) return false;
+        if (g.h_pow2 && t >= 64.0 * g.h && b.t0 > t) {
+            const double m = floor((b.t0 - t) * g.inv_h) - 1.0;
+            if (m >= 2.0) {
+                PSDF_STAT(4);
+                t_sync = t;
+                t = lattice_advance(t, m, g.h);
+            }
+        }
+        return true;
+    }
+
     // Resumes a ray whose box exit t1 is known (the caller sets t and count
     // to a point the reference visited).
     __device__ __forceinline__ void init_from(const GridView& g, const double* o_, const double* d_,

@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_SCAN_MINB) march_scan_kernel(RayPa
         if (R.valid) {
             const D3 dir = pixel_dir(R.V->cam, (double)R.u + 0.5, (double)R.v + 0.5);
             const double dd[3] = {dir.x, dir.y, dir.z};
-            if (mr.init(g, R.V->cam.pos, dd, P.n_max) && mr.may_hit(g)) {
+            if (mr.init(g, R.V->cam.pos, dd, P.n_max) && mr.enter_occupied(g)) {
                 for (;;) {
                     double ts;
                     int tile;
