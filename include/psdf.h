@@ -129,6 +129,24 @@ int psdf_download_params(psdf_ctx* ctx, float* raw, float* smooth, float* planes
  * stage 0: after the ray pass (GradBuffers after trainer.cpp:184-185);
  * stage 1: what Adam consumed (after regularizers + G^T fold, trainer.cpp:193).
  * smooth = the smooth-staged SDF gradient (grads.hpp:15). */
+/* ---- LOD transitions ---------------------------------
+ * The current grid's description and its tile / probe structure (the order
+ * of SparseGrid::tiles / probes, grid.hpp:103-107; arrays of 3 T, 8 T and
+ * 3 P ints; any pointer may be NULL). */
+int psdf_grid_info(psdf_ctx* ctx, psdf_grid_desc* out);
+int psdf_download_structure(psdf_ctx* ctx, int32_t* tile_coords, int32_t* probe_ids, int32_t* probe_coords);
+/* Replaces grid = grid.subdivide() (SparseGrid::subdivide, grid.cpp:271-345;
+ * called at trainer.cpp:213): the device grid becomes its 2x subdivision —
+ * children kept unless min |raw| > band_voxels * h_new with no sign change,
+ * planes upsampled, probes re-interpolated on the doubled lattice, smoothed;
+ * same tile / probe order as the reference.  Optimizer state is reset.
+ * out_T / out_P (may be NULL) receive the new counts. */
+int psdf_subdivide(psdf_ctx* ctx, double band_voxels, int32_t* out_T, int32_t* out_P);
+/* Replaces SparseGrid::raise_sh_order (grid.cpp:252-262, trainer.cpp:105):
+ * std::invalid_argument (PSDF_ERR_INVALID_ARGUMENT) if the order decreases or
+ * exceeds 4; new bands start at zero.  Optimizer state is reset. */
+int psdf_raise_sh_order(psdf_ctx* ctx, int new_order);
+
 /* Keep a copy of the stage-0 (post ray pass) gradients on every step. */
 int psdf_set_keep_raypass_grads(psdf_ctx* ctx, int keep);
 int psdf_download_grads(psdf_ctx* ctx, int stage, float* raw, float* smooth, float* planes,

@@ -391,6 +391,26 @@ void ref_scene_import(RefScene* s, const double* raw, const double* smooth, cons
 
 void ref_smooth_all(RefScene* s) { s->grid.smooth_all(); }
 
+// LOD transitions through the reference's own members (grid.cpp:252-345).
+int ref_subdivide(RefScene* s) {
+    try {
+        s->grid = s->grid.subdivide();
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+int ref_raise_sh_order(RefScene* s, int order) {
+    try {
+        s->grid.raise_sh_order(order);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 // MLP flat layout: w1 [32][in], b1 [32], w2 [32][32], b2 [32], w3 [3][32],
 // b3 [3], camera_bias [ncam][32]  (decoder.hpp:17-31 field order).
 static void mlp_copy(DecoderMlp& m, double* out, const double* in) {

@@ -105,6 +105,8 @@ def reflib():
                                      C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, _ip,
                                      _dp, _dp, C.c_int, C.c_uint64]
     L.ref_scene_free.argtypes = [C.c_void_p]
+    L.ref_subdivide.argtypes = [C.c_void_p]
+    L.ref_raise_sh_order.argtypes = [C.c_void_p, C.c_int]
     L.ref_scene_randomize.argtypes = [C.c_void_p, C.c_uint64, C.c_double, C.c_double, C.c_double,
                                       C.c_double]
     L.ref_scene_info.argtypes = [C.c_void_p, _lp, _dp]
@@ -236,6 +238,15 @@ class RefScene:
                                 ptr(a.probes))
         self.L.ref_mlp_export(self.h, ptr(a.mlp))
         return a
+
+    def subdivide(self):
+        """grid = grid.subdivide() (grid.cpp:271-345), the reference's own member."""
+        _check(self.L.ref_subdivide(self.h), self.L)
+
+    def raise_sh_order(self, order):
+        """SparseGrid::raise_sh_order (grid.cpp:252-262); ValueError when the reference throws."""
+        if self.L.ref_raise_sh_order(self.h, int(order)) != 0:
+            raise ValueError(self.L.ref_last_error().decode())
 
     def import_(self, raw=None, smooth=None, planes=None, probes=None, mlp=None):
         c = lambda x: None if x is None else np.ascontiguousarray(x, dtype=np.float64)

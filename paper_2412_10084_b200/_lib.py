@@ -82,7 +82,8 @@ EXPORTS = [
     "psdf_train_reset", "psdf_train_step", "psdf_upload_views", "psdf_train_step_views",
     "psdf_comm_unique_id", "psdf_comm_init", "psdf_last_timing", "psdf_stream",
     "psdf_host_alloc", "psdf_host_free", "psdf_march_rays", "psdf_pixel_dirs",
-    "psdf_last_k2_breakdown",
+    "psdf_last_k2_breakdown", "psdf_grid_info", "psdf_download_structure", "psdf_subdivide",
+    "psdf_raise_sh_order",
 ]
 
 _lib = None
@@ -137,6 +138,10 @@ def load():
     L.psdf_march_rays.argtypes = [vp, C.c_int, _dp, _dp, C.c_int, _dp, _ip]
     L.psdf_pixel_dirs.argtypes = [C.POINTER(psdf_camera), _dp]
     L.psdf_last_k2_breakdown.argtypes = [vp, _dp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    L.psdf_grid_info.argtypes = [vp, C.POINTER(psdf_grid_desc)]
+    L.psdf_download_structure.argtypes = [vp, _ip, _ip, _ip]
+    L.psdf_subdivide.argtypes = [vp, C.c_double, _ip, _ip]
+    L.psdf_raise_sh_order.argtypes = [vp, C.c_int]
     _lib = L
     return L
 

@@ -389,6 +389,40 @@ class Context:
                                                 _fptr(out["mlp"])))
         return out
 
+    # -- LOD transitions (trainer.cpp:105, 213)
+    def _refresh_grid(self):
+        """Re-reads the device grid's structure and parameters into self.grid."""
+        d = psdf_grid_desc()
+        self._check(self.L.psdf_grid_info(self.h, C.byref(d)))
+        old = self.grid.cfg
+        cfg = GridConfig(voxel_size=d.voxel_size, origin=tuple(d.origin), resolution=tuple(d.res),
+                         n_s=d.n_s, n_a=d.n_a, sh_order=d.sh_order, far_field_voxels=d.far_field_voxels,
+                         band_voxels=old.band_voxels)
+        tc = np.zeros((d.T, 3), np.int32)
+        pid = np.zeros((d.T, 8), np.int32)
+        pco = np.zeros((d.P, 3), np.int32)
+        self._check(self.L.psdf_download_structure(self.h, _iptr(tc), _iptr(pid), _iptr(pco)))
+        nc = d.sh_order * d.sh_order
+        g = HostGrid(cfg, tc, pid, pco, np.zeros((d.T, 4096), np.float32),
+                     np.zeros(d.T * 3 * 256 * d.n_s, np.float32), np.zeros(d.P * nc * d.n_a, np.float32),
+                     np.zeros(self.grid.mlp.shape, np.float32), ncam=d.ncam,
+                     smooth=np.zeros((d.T, 4096), np.float32))
+        self._check(self.L.psdf_download_params(self.h, _fptr(g.raw), _fptr(g.smooth), _fptr(g.planes),
+                                                _fptr(g.probes), _fptr(g.mlp)))
+        self.grid = g
+        return g
+
+    def subdivide(self, band_voxels=None):
+        """grid = grid.subdivide() (grid.cpp:271-345) on the device; returns the new HostGrid."""
+        bv = self.grid.cfg.band_voxels if band_voxels is None else band_voxels
+        self._check(self.L.psdf_subdivide(self.h, float(bv), None, None))
+        return self._refresh_grid()
+
+    def raise_sh_order(self, order):
+        """SparseGrid::raise_sh_order (grid.cpp:252-262) on the device."""
+        self._check(self.L.psdf_raise_sh_order(self.h, int(order)))
+        return self._refresh_grid()
+
     def grads(self, stage=1):
         g = self.grid
         out = dict(raw=np.zeros((g.T, 4096), np.float32), smooth=np.zeros((g.T, 4096), np.float32),

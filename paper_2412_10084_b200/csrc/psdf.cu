@@ -23,12 +23,14 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/psdf.h"
 #include "psdf_grid.cuh"
 #include "psdf_raypass.cuh"
 #include "psdf_train.cuh"
+#include "psdf_lod.cuh"
 
 using namespace psdf;
 
@@ -1214,6 +1216,174 @@ int psdf_download_params(psdf_ctx* c, float* raw, float* smooth, float* planes, 
         if (probes && c->n_probes) CK(cudaMemcpyAsync(probes, c->d_params + c->off_probes, sizeof(float) * c->n_probes, cudaMemcpyDeviceToHost, s));
         if (mlp) CK(cudaMemcpyAsync(mlp, c->d_params + c->off_mlp, sizeof(float) * c->mlp_size, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
+    });
+}
+
+int psdf_grid_info(psdf_ctx* c, psdf_grid_desc* out) {
+    return guarded([&] {
+        need_grid(c);
+        if (!out) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
+        *out = c->desc;
+    });
+}
+
+int psdf_download_structure(psdf_ctx* c, int32_t* tile_coords, int32_t* probe_ids, int32_t* probe_coords) {
+    return guarded([&] {
+        need_grid(c);
+        set_device(c);
+        const int64_t T = c->desc.T, P = c->desc.P;
+        std::vector<int4> tc(std::max<int64_t>(T, 1)), pc(std::max<int64_t>(P, 1));
+        if (T) CK(cudaMemcpy(tc.data(), c->d_tile_coords, sizeof(int4) * T, cudaMemcpyDeviceToHost));
+        if (P) CK(cudaMemcpy(pc.data(), c->d_probe_coords, sizeof(int4) * P, cudaMemcpyDeviceToHost));
+        if (probe_ids && T) CK(cudaMemcpy(probe_ids, c->d_probe_ids, sizeof(int32_t) * 8 * T, cudaMemcpyDeviceToHost));
+        for (int64_t t = 0; tile_coords && t < T; ++t) {
+            tile_coords[3 * t] = tc[t].x;
+            tile_coords[3 * t + 1] = tc[t].y;
+            tile_coords[3 * t + 2] = tc[t].z;
+        }
+        for (int64_t p = 0; probe_coords && p < P; ++p) {
+            probe_coords[3 * p] = pc[p].x;
+            probe_coords[3 * p + 1] = pc[p].y;
+            probe_coords[3 * p + 2] = pc[p].z;
+        }
+    });
+}
+
+// SparseGrid::raise_sh_order (grid.cpp:252-262): band-major probes, the new
+// bands start at zero.  Re-lays the parameter buffer out (the optimizer state
+// is reset, as the reference rebuilds it every LOD, trainer.cpp:115).
+int psdf_raise_sh_order(psdf_ctx* c, int new_order) {
+    return guarded([&] {
+        need_grid(c);
+        if (new_order < c->desc.sh_order || new_order > 4)
+            fail(PSDF_ERR_INVALID_ARGUMENT, "raise_sh_order: order must not decrease and must be <= 4");
+        if (new_order == c->desc.sh_order) return;
+        set_device(c);
+        psdf_grid_desc d = c->desc;
+        const int64_t T = d.T, P = d.P;
+        std::vector<int32_t> tc(3 * std::max<int64_t>(T, 1)), pid(8 * std::max<int64_t>(T, 1)),
+            pco(3 * std::max<int64_t>(P, 1));
+        std::vector<float> raw((size_t)T * TV), sm((size_t)T * TV), planes(c->n_planes), probes(c->n_probes),
+            mlp(c->mlp_size);
+        if (psdf_download_structure(c, tc.data(), pid.data(), pco.data()) != PSDF_OK ||
+            psdf_download_params(c, raw.data(), sm.data(), planes.data(), probes.data(), mlp.data()) != PSDF_OK)
+            fail(PSDF_ERR_RUNTIME, "%s", g_err.c_str());
+        const int oc = d.sh_order * d.sh_order * d.n_a, nc = new_order * new_order * d.n_a;
+        std::vector<float> np((size_t)P * nc, 0.f);
+        for (int64_t p = 0; p < P; ++p)
+            std::copy(probes.begin() + p * oc, probes.begin() + (p + 1) * oc, np.begin() + p * nc);
+        d.sh_order = new_order;
+        if (psdf_upload_grid(c, &d, tc.data(), pid.data(), pco.data(), raw.data(), sm.data(), planes.data(),
+                             np.data()) != PSDF_OK ||
+            psdf_upload_mlp(c, mlp.data(), (int64_t)mlp.size()) != PSDF_OK)
+            fail(PSDF_ERR_RUNTIME, "%s", g_err.c_str());
+    });
+}
+
+// SparseGrid::subdivide (grid.cpp:271-345) on the device: child raw values,
+// allocation decisions, plane upsampling and probe re-interpolation are
+// kernels (psdf_lod.cuh); the new tile / probe lists are built on the host in
+// the reference's allocate_tile / ensure_probe order, and the new grid is
+// then uploaded (smoothed on the device, optimizer state reset).
+int psdf_subdivide(psdf_ctx* c, double band_voxels, int32_t* out_T, int32_t* out_P) {
+    return guarded([&] {
+        need_grid(c);
+        set_device(c);
+        cudaStream_t s = c->stream;
+        const psdf_grid_desc d0 = c->desc;
+        const int64_t T0 = d0.T;
+        psdf_grid_desc d = d0;
+        d.voxel_size = d0.voxel_size * 0.5;
+        for (int a = 0; a < 3; ++a) d.res[a] = d0.res[a] * 2;
+        const int nt1[3] = {d.res[0] / TE, d.res[1] / TE, d.res[2] / TE};
+        // 1. child raw values + allocation decisions
+        float* d_child = nullptr;
+        uint8_t* d_keep = nullptr;
+        CK(cudaMalloc(&d_child, sizeof(float) * TV * std::max<int64_t>(8 * T0, 1)));
+        CK(cudaMalloc(&d_keep, std::max<int64_t>(8 * T0, 1)));
+        std::vector<uint8_t> keep(8 * T0);
+        std::vector<int4> tc0(std::max<int64_t>(T0, 1));
+        if (T0) {
+            subdiv_raw_kernel<<<(unsigned)(8 * T0), 256, 0, s>>>(c->view(), c->d_params + c->off_raw, d.voxel_size,
+                                                               band_voxels * d.voxel_size, d_child, d_keep);
+            CK(cudaGetLastError());
+            CK(cudaMemcpyAsync(keep.data(), d_keep, 8 * T0, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(tc0.data(), c->d_tile_coords, sizeof(int4) * T0, cudaMemcpyDeviceToHost, s));
+        }
+        CK(cudaStreamSynchronize(s));
+        // 2. new tiles in the reference's order (parent order, child 0..7),
+        //    probes by first touch (allocate_tile -> ensure_probe)
+        std::vector<int32_t> tc, pid, pco;
+        std::vector<int> src;
+        std::unordered_map<int64_t, int> probe_of;
+        auto key = [&](int x, int y, int z) { return ((int64_t)x * (nt1[1] + 1) + y) * (nt1[2] + 1) + z; };
+        for (int64_t t = 0; t < T0; ++t)
+            for (int ch = 0; ch < 8; ++ch) {
+                if (!keep[8 * t + ch]) continue;
+                const int q[3] = {2 * tc0[t].x + (ch & 1), 2 * tc0[t].y + ((ch >> 1) & 1), 2 * tc0[t].z + ((ch >> 2) & 1)};
+                tc.insert(tc.end(), q, q + 3);
+                src.push_back((int)(8 * t + ch));
+                for (int i = 0; i < 8; ++i) {
+                    const int g[3] = {q[0] + (i & 1), q[1] + ((i >> 1) & 1), q[2] + ((i >> 2) & 1)};
+                    auto it = probe_of.find(key(g[0], g[1], g[2]));
+                    int id;
+                    if (it == probe_of.end()) {
+                        id = (int)(pco.size() / 3);
+                        probe_of.emplace(key(g[0], g[1], g[2]), id);
+                        pco.insert(pco.end(), g, g + 3);
+                    } else {
+                        id = it->second;
+                    }
+                    pid.push_back(id);
+                }
+            }
+        const int64_t T1 = (int64_t)src.size(), P1 = (int64_t)(pco.size() / 3);
+        d.T = (int)T1;
+        d.P = (int)P1;
+        // 3. resampled parameters on the device
+        const int stride = d0.sh_order * d0.sh_order * d0.n_a;
+        int* d_src = nullptr;
+        int4* d_pc = nullptr;
+        float *d_raw = nullptr, *d_planes = nullptr, *d_probes = nullptr;
+        std::vector<int4> pc4(std::max<int64_t>(P1, 1));
+        for (int64_t p = 0; p < P1; ++p) pc4[p] = make_int4(pco[3 * p], pco[3 * p + 1], pco[3 * p + 2], 0);
+        CK(cudaMalloc(&d_src, sizeof(int) * std::max<int64_t>(T1, 1)));
+        CK(cudaMalloc(&d_pc, sizeof(int4) * std::max<int64_t>(P1, 1)));
+        CK(cudaMalloc(&d_raw, sizeof(float) * TV * std::max<int64_t>(T1, 1)));
+        CK(cudaMalloc(&d_planes, sizeof(float) * 3 * 256 * d0.n_s * std::max<int64_t>(T1, 1)));
+        CK(cudaMalloc(&d_probes, sizeof(float) * stride * std::max<int64_t>(P1, 1)));
+        if (T1) CK(cudaMemcpyAsync(d_src, src.data(), sizeof(int) * T1, cudaMemcpyHostToDevice, s));
+        if (P1) CK(cudaMemcpyAsync(d_pc, pc4.data(), sizeof(int4) * P1, cudaMemcpyHostToDevice, s));
+        if (T1) {
+            subdiv_gather_raw_kernel<<<(unsigned)T1, 256, 0, s>>>(d_child, d_src, (int)T1, d_raw);
+            CK(cudaGetLastError());
+            subdiv_planes_kernel<<<(unsigned)T1, 256, 0, s>>>(c->d_params + c->off_planes, d0.n_s, d_src, (int)T1,
+                                                             d_planes);
+            CK(cudaGetLastError());
+        }
+        if (P1) {
+            const int3 pdim = make_int3(c->nt[0] + 1, c->nt[1] + 1, c->nt[2] + 1);
+            subdiv_probes_kernel<<<(unsigned)P1, 128, 0, s>>>(c->d_probe_table, pdim, c->d_params + c->off_probes,
+                                                              stride, d_pc, (int)P1, d_probes);
+            CK(cudaGetLastError());
+        }
+        std::vector<float> raw((size_t)T1 * TV), planes((size_t)T1 * 3 * 256 * d0.n_s), probes((size_t)P1 * stride),
+            mlp(c->mlp_size);
+        if (T1) CK(cudaMemcpyAsync(raw.data(), d_raw, sizeof(float) * raw.size(), cudaMemcpyDeviceToHost, s));
+        if (T1) CK(cudaMemcpyAsync(planes.data(), d_planes, sizeof(float) * planes.size(), cudaMemcpyDeviceToHost, s));
+        if (P1) CK(cudaMemcpyAsync(probes.data(), d_probes, sizeof(float) * probes.size(), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(mlp.data(), c->d_params + c->off_mlp, sizeof(float) * mlp.size(), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        for (void* p : {(void*)d_child, (void*)d_keep, (void*)d_src, (void*)d_pc, (void*)d_raw, (void*)d_planes,
+                        (void*)d_probes})
+            cudaFree(p);
+        // 4. the new grid (smoothed on the device, grid.cpp:340)
+        if (psdf_upload_grid(c, &d, tc.data(), pid.data(), pco.data(), raw.data(), nullptr, planes.data(),
+                             probes.data()) != PSDF_OK ||
+            psdf_upload_mlp(c, mlp.data(), (int64_t)mlp.size()) != PSDF_OK)
+            fail(PSDF_ERR_RUNTIME, "%s", g_err.c_str());
+        if (out_T) *out_T = (int32_t)T1;
+        if (out_P) *out_P = (int32_t)P1;
     });
 }
 

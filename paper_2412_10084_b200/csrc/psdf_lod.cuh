@@ -1,0 +1,160 @@
+// psdf_lod.cuh — LOD transition kernels: the GPU side
+// of SparseGrid::subdivide (grid.cpp:271-338).  The allocation decision and
+// every resampled value are computed in f64 in the reference's operation
+// order from the (fp32) parent parameters; only the host-side bookkeeping of
+// the new tile / probe lists (allocate_tile / ensure_probe order,
+// grid.cpp:44-72) runs on the CPU.
+#pragma once
+
+#include "psdf_device.cuh"
+
+namespace psdf {
+
+// raw_value (grid.cpp:74-81) of the parent grid.
+__device__ __forceinline__ double raw_value(const GridView& g, const float* __restrict__ raw, int vx, int vy,
+                                            int vz) {
+    if (vx < 0 || vy < 0 || vz < 0 || vx >= g.res[0] || vy >= g.res[1] || vz >= g.res[2]) return g.far;
+    const int t = tile_lookup(g, vx >> 4, vy >> 4, vz >> 4);
+    if (t < 0) return g.far;
+    return (double)__ldg(raw + (int64_t)t * TV + vox_index(vx & 15, vy & 15, vz & 15));
+}
+
+// One block per (parent tile, child): the child's 16^3 raw values, sampled
+// from the parent's raw grid at the child voxel centres (sample_raw,
+// grid.cpp:120-125 / 96-117), and whether the child is allocated: it is
+// dropped only when min |s| > band and the values do not change sign
+// (grid.cpp:294-305).
+__global__ void __launch_bounds__(256) subdiv_raw_kernel(GridView g, const float* __restrict__ raw,
+                                                         double h_new, double band,
+                                                         float* __restrict__ child_raw,
+                                                         uint8_t* __restrict__ keep) {
+    const int tile = blockIdx.x >> 3, child = blockIdx.x & 7;
+    const int4 tc = __ldg(g.tile_coords + tile);
+    const int cx = 2 * tc.x + (child & 1), cy = 2 * tc.y + ((child >> 1) & 1), cz = 2 * tc.z + ((child >> 2) & 1);
+    double mn = 1.79769313486231570e308;
+    bool pos = false, neg = false;
+    float* out = child_raw + (int64_t)blockIdx.x * TV;
+    for (int i = threadIdx.x; i < TV; i += blockDim.x) {
+        const int x = i >> 8, y = (i >> 4) & 15, z = i & 15;
+        // voxel_center (grid.hpp:75-77) of the child grid
+        const double p[3] = {dadd(g.org[0], dmul((double)(cx * TE + x) + 0.5, h_new)),
+                             dadd(g.org[1], dmul((double)(cy * TE + y) + 0.5, h_new)),
+                             dadd(g.org[2], dmul((double)(cz * TE + z) + 0.5, h_new))};
+        double c[3];
+        int b[3];
+        double f[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            c[a] = dsub(w2v(g, p[a], a), 0.5);
+            b[a] = (int)floor(c[a]);
+            f[a] = dsub(c[a], (double)b[a]);
+        }
+        double v8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v8[k] = raw_value(g, raw, b[0] + (k & 1), b[1] + ((k >> 1) & 1), b[2] + ((k >> 2) & 1));
+        const double s = trilerp8(f[0], f[1], f[2], v8);
+        out[vox_index(x, y, z)] = (float)s;
+        mn = fmin(mn, fabs(s));
+        (s >= 0.0 ? pos : neg) = true;
+    }
+    __shared__ double s_mn[8];
+    __shared__ int s_flags[8];
+    int fl = (pos ? 1 : 0) | (neg ? 2 : 0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        fl |= __shfl_xor_sync(0xffffffffu, fl, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_mn[threadIdx.x >> 5] = mn;
+        s_flags[threadIdx.x >> 5] = fl;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            mn = fmin(mn, s_mn[w]);
+            fl |= s_flags[w];
+        }
+        keep[blockIdx.x] = (mn > band && fl != 3) ? 0 : 1;
+    }
+}
+
+// Child raw values of the kept children, in the new tile order.
+__global__ void __launch_bounds__(256) subdiv_gather_raw_kernel(const float* __restrict__ child_raw,
+                                                                const int* __restrict__ src, int n_new,
+                                                                float* __restrict__ raw_new) {
+    const int t = blockIdx.x;
+    if (t >= n_new) return;
+    const float4* s4 = reinterpret_cast<const float4*>(child_raw + (int64_t)__ldg(src + t) * TV);
+    float4* d4 = reinterpret_cast<float4*>(raw_new + (int64_t)t * TV);
+    for (int i = threadIdx.x; i < TV / 4; i += blockDim.x) d4[i] = __ldg(s4 + i);
+}
+
+// Planes of a child: each 16x16 plane covers half of the parent's
+// (grid.cpp:309-322): bilinear plane_sample at offs*8 + (a + 1/2)/2.
+__global__ void __launch_bounds__(256) subdiv_planes_kernel(const float* __restrict__ planes, int n_s,
+                                                            const int* __restrict__ src, int n_new,
+                                                            float* __restrict__ planes_new) {
+    const int t = blockIdx.x;
+    if (t >= n_new) return;
+    const int s = __ldg(src + t);
+    const int parent = s >> 3, child = s & 7;
+    const int offs[3] = {child & 1, (child >> 1) & 1, (child >> 2) & 1};
+    const int per_plane = 256 * n_s;
+    for (int i = threadIdx.x; i < 3 * per_plane; i += blockDim.x) {
+        const int q = i / per_plane, r = i - q * per_plane;
+        const int a = r / (TE * n_s), bb = (r / n_s) % TE, k = r % n_s;
+        // plane_x: axes (y, z); plane_y: (x, z); plane_z: (x, y)
+        const int axis_a = q == 0 ? 1 : 0, axis_b = q == 2 ? 1 : 2;
+        const Tap ta = plane_tap(offs[axis_a] * 8.0 + ((double)a + 0.5) * 0.5);
+        const Tap tb = plane_tap(offs[axis_b] * 8.0 + ((double)bb + 0.5) * 0.5);
+        const float* P = planes + ((int64_t)parent * 3 + q) * per_plane;
+        const double v00 = P[(ta.a0 * TE + tb.a0) * n_s + k], v01 = P[(ta.a0 * TE + tb.a0 + 1) * n_s + k];
+        const double v10 = P[((ta.a0 + 1) * TE + tb.a0) * n_s + k], v11 = P[((ta.a0 + 1) * TE + tb.a0 + 1) * n_s + k];
+        const double fa = ta.f, fb = tb.f;
+        const double v = dadd(dmul(dsub(1.0, fa), dadd(dmul(dsub(1.0, fb), v00), dmul(fb, v01))),
+                              dmul(fa, dadd(dmul(dsub(1.0, fb), v10), dmul(fb, v11))));
+        planes_new[((int64_t)t * 3 + q) * per_plane + r] = (float)v;
+    }
+}
+
+// Probe coefficients on the twice-as-dense lattice (grid.cpp:325-345):
+// weighted over the existing parent-lattice neighbours, renormalised.
+__global__ void __launch_bounds__(128) subdiv_probes_kernel(const int32_t* __restrict__ probe_table,
+                                                            int3 pdim, const float* __restrict__ probes,
+                                                            int stride, const int4* __restrict__ coords_new,
+                                                            int n_new, float* __restrict__ probes_new) {
+    const int p = blockIdx.x;
+    if (p >= n_new) return;
+    const int4 gc = __ldg(coords_new + p);
+    int ids[8];
+    double ws[8];
+    double total = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int gx = gc.x / 2 + ((gc.x & 1) ? (i & 1) : 0);
+        const int gy = gc.y / 2 + ((gc.y & 1) ? ((i >> 1) & 1) : 0);
+        const int gz = gc.z / 2 + ((gc.z & 1) ? ((i >> 2) & 1) : 0);
+        const double w = dmul(dmul((gc.x & 1) ? 0.5 : ((i & 1) ? 0.0 : 1.0),
+                                   (gc.y & 1) ? 0.5 : ((i & 2) ? 0.0 : 1.0)),
+                              (gc.z & 1) ? 0.5 : ((i & 4) ? 0.0 : 1.0));
+        ids[i] = -1;
+        ws[i] = 0.0;
+        if (w == 0.0) continue;
+        if (gx < 0 || gy < 0 || gz < 0 || gx >= pdim.x || gy >= pdim.y || gz >= pdim.z) continue;
+        const int opi = __ldg(probe_table + ((int64_t)gx * pdim.y + gy) * pdim.z + gz);
+        if (opi < 0) continue;
+        total = dadd(total, w);
+        ids[i] = opi;
+        ws[i] = w;
+    }
+    for (int q = threadIdx.x; q < stride; q += blockDim.x) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (ids[i] >= 0) acc = dadd(acc, dmul(ws[i], (double)__ldg(probes + (int64_t)ids[i] * stride + q)));
+        probes_new[(int64_t)p * stride + q] = (float)(total > 0.0 ? ddiv(acc, total) : acc);
+    }
+}
+
+}  // namespace psdf
