@@ -198,11 +198,43 @@ inline sdfrecon::RenderedImage render_image(const sdfrecon::SparseGrid& grid,
     return render_image(dev, camera, opt);
 }
 
-// train (trainer.cpp:81-220) with the step body on the GPU.  Identical
-// schedule arithmetic, batch order (mt19937_64 shuffle, trainer.cpp:98,
-// 119-145), per-LOD Adam reset, log line and checkpoint cursor handling; the
-// between-LOD work (raise_sh_order, per-LOD downscale, subdivide) is the
-// reference's host code.
+// The device grid's structure as a host SparseGrid (allocate_tile in the
+// device's tile order reproduces the probe pool order, grid.cpp:44-72), with
+// its values downloaded.
+inline void sync_grid_from_device(const Device& dev, const sdfrecon::SparseGrid& like, int lod,
+                                  sdfrecon::SparseGrid& out, sdfrecon::DecoderMlp& mlp) {
+    psdf_grid_desc d{};
+    check(psdf_grid_info(dev.ctx(), &d), dev.ctx());
+    std::vector<int32_t> tc(3 * (size_t)d.T), pid(8 * (size_t)d.T), pco(3 * (size_t)d.P);
+    check(psdf_download_structure(dev.ctx(), tc.data(), pid.data(), pco.data()), dev.ctx());
+    sdfrecon::SparseGrid g;
+    g.voxel_size = d.voxel_size;
+    g.origin = sdfrecon::Vec3(d.origin[0], d.origin[1], d.origin[2]);
+    g.resolution = {d.res[0], d.res[1], d.res[2]};
+    g.n_s = d.n_s;
+    g.n_a = d.n_a;
+    g.sh_order = d.sh_order;
+    g.lod = lod;
+    g.far_field_voxels = d.far_field_voxels;
+    g.band_voxels = like.band_voxels;
+    for (int t = 0; t < d.T; ++t) {
+        const int ti = g.allocate_tile(tc[3 * t], tc[3 * t + 1], tc[3 * t + 2]);
+        for (int i = 0; i < 8; ++i)
+            if (ti != t || g.tiles[t].probe_ids[i] != pid[8 * t + i])
+                throw std::runtime_error("sync_grid_from_device: tile / probe order mismatch");
+    }
+    dev.download(g, mlp);
+    out = std::move(g);
+}
+
+// train (trainer.cpp:81-220) with the step body and the LOD transitions on
+// the GPU.  Identical schedule arithmetic, batch order (mt19937_64 shuffle,
+// trainer.cpp:98, 119-145), per-LOD Adam reset, log line and checkpoint
+// cursor handling.  The grid stays resident across LODs: raise_sh_order and
+// subdivide run on the device (psdf_raise_sh_order / psdf_subdivide, same
+// tile and probe order as the reference); only the per-LOD image downscale
+// (image.cpp:110-137) is host code; the trained grid is synchronised back
+// into ckpt.grid at the end.
 inline sdfrecon::TrainStats train(const sdfrecon::Dataset& ds, const sdfrecon::TrainSchedule& sched,
                                   sdfrecon::Checkpoint& ckpt, std::ostream* log = nullptr,
                                   int device = 0) {
@@ -224,9 +256,16 @@ inline sdfrecon::TrainStats train(const sdfrecon::Dataset& ds, const sdfrecon::T
     TrainStats stats;
     long global_step = 0;
     Device dev(device);
+    dev.upload(grid, mlp);
+    int lod = grid.lod;
+    psdf_grid_desc cur{};
     for (; ckpt.lod_cursor < static_cast<int>(sched.lods.size()); ++ckpt.lod_cursor) {
         const LodSchedule& ls = sched.lods[ckpt.lod_cursor];
-        if (grid.sh_order < ls.sh_order) grid.raise_sh_order(ls.sh_order);
+        check(psdf_grid_info(dev.ctx(), &cur), dev.ctx());
+        if (cur.sh_order < ls.sh_order) {
+            check(psdf_raise_sh_order(dev.ctx(), ls.sh_order), dev.ctx());
+            check(psdf_grid_info(dev.ctx(), &cur), dev.ctx());
+        }
         // per-LOD views, resident in HBM for the whole LOD
         std::vector<psdf_camera> cams;
         std::vector<std::vector<float>> rgb;
@@ -247,7 +286,7 @@ inline sdfrecon::TrainStats train(const sdfrecon::Dataset& ds, const sdfrecon::T
             rp.push_back(rgb[i].data());
             mp.push_back(msk[i].data());
         }
-        dev.upload(grid, mlp);  // also resets Adam (trainer.cpp:115)
+        check(psdf_train_reset(dev.ctx()), dev.ctx());  // per-LOD optimizer (trainer.cpp:115)
         check(psdf_upload_views(dev.ctx(), (int)cams.size(), cams.data(), rp.data(), mp.data()), dev.ctx());
         std::vector<int> order(ds.views.size());
         std::iota(order.begin(), order.end(), 0);
@@ -263,7 +302,7 @@ inline sdfrecon::TrainStats train(const sdfrecon::Dataset& ds, const sdfrecon::T
             hp.l_norm = ls.lambda_normal.at(it, total);
             hp.l_feat = ls.lambda_features.at(it, total);
             hp.l_probe = ls.lambda_probes.at(it, total);
-            hp.tau = ls.tau.at_geometric(it, total) / grid.voxel_size;
+            hp.tau = ls.tau.at_geometric(it, total) / cur.voxel_size;
             hp.photo_scale = sched.lambda_photo / ls.images_per_batch;
             hp.use_camera_bias = sched.camera_bias;
             std::vector<int32_t> batch(ls.images_per_batch);
@@ -285,11 +324,14 @@ inline sdfrecon::TrainStats train(const sdfrecon::Dataset& ds, const sdfrecon::T
                        << " features " << L.features << " probes " << L.probes << " total "
                        << L.total << " psnr " << L.psnr << '\n';
         }
-        dev.download(grid, mlp);
         global_step += total;
         ckpt.iteration = 0;
-        if (ckpt.lod_cursor + 1 < static_cast<int>(sched.lods.size())) grid = grid.subdivide();
+        if (ckpt.lod_cursor + 1 < static_cast<int>(sched.lods.size())) {
+            check(psdf_subdivide(dev.ctx(), (double)grid.band_voxels, nullptr, nullptr), dev.ctx());
+            ++lod;
+        }
     }
+    sync_grid_from_device(dev, grid, lod, grid, mlp);
     ckpt.lod_cursor = static_cast<int>(sched.lods.size()) - 1;
     ckpt.iteration = sched.lods.back().iterations;
     return stats;
