@@ -52,7 +52,7 @@ RADIUS = 0.32
 # acceptance schedule's final-LOD values (acceptance.cpp:98-100) scaled by the
 # 64^3 -> 512^3 voxel-size ratio, so the timed steps keep a surface-like SDF
 # (the paper's 0.01 is 5 voxels per Adam step at 512^3 and destroys the scene).
-HP = dict(lr_vox=8e-4 / 8, lr_mlp=8e-4, l_sdf=0.2, l_eik=0.1, l_norm=0.05, l_feat=0.05, l_probe=0.2)
+HP = dict(lr_vox=8e-4 * 64 / RES, lr_mlp=8e-4, l_sdf=0.2, l_eik=0.1, l_norm=0.05, l_feat=0.05, l_probe=0.2)
 LAMBDA_PHOTO = 40.0
 
 
@@ -211,7 +211,7 @@ def run_reference(args, rank, world):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_dict(world),
         "cpu_baseline": {"value": sps, "unit": "samples/s", "cores": cores, "kind": "reference",
-                         "sample": f"1 of the {BATCH} batch views per step (1600x1200 rays), full "
+                         "sample": f"1 of the {BATCH} batch views per step ({WIDTH}x{HEIGHT} rays), full "
                                    f"per-step grid work (regularizers, G^T fold, Adam, smoothing "
                                    f"over all {g.T} tiles)"},
         "e2e": {"value": sps, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -220,8 +220,16 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def workload_name():
+    if (RES, N_VIEWS, WIDTH, HEIGHT) == (512, 49, 1600, 1200):
+        return "configs[1]: DTU-scale synthetic object"
+    if (N_VIEWS, WIDTH, HEIGHT) == (68, 2048, 1536):
+        return "configs[2]-scale: 68 cameras at 2048x1536 (MVMannequins-scale), synthetic object"
+    return f"configs[4] sweep point: synthetic object at {RES}^3"
+
+
 def config_dict(world):
-    return {"workload": f"configs[1]: DTU-scale synthetic object, {RES}^3 sparse SDF grid "
+    return {"workload": f"{workload_name()}, {RES}^3 sparse SDF grid "
                         f"(sphere r={RADIUS}, band 6), probes at tile corners ({RES // 16 + 1}^3 lattice; "
                         f"the reference fixes the probe lattice, SURVEY 8d), (n_s,n_a,l)=({NS},{NA},{SH_ORDER}), "
                         f"{N_VIEWS} views at {WIDTH}x{HEIGHT}, batch {BATCH} views/step/GPU, tau={TAU_VOX:g}/voxel",
@@ -233,6 +241,7 @@ def config_dict(world):
 
 # --------------------------------------------------------------------------
 def main():
+    global RES, N_VIEWS, WIDTH, HEIGHT
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -240,10 +249,16 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-render", action="store_true")
+    ap.add_argument("--res", type=int, default=RES, help="grid resolution (configs[4] sweep)")
+    ap.add_argument("--views", type=int, default=N_VIEWS)
+    ap.add_argument("--width", type=int, default=WIDTH)
+    ap.add_argument("--height", type=int, default=HEIGHT)
     ap.add_argument("--profile", action="store_true",
                     help="setup + warm-up + 2 train steps + 1 render, no JSON (for ncu)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    RES, N_VIEWS, WIDTH, HEIGHT = args.res, args.views, args.width, args.height
+    HP["lr_vox"] = 8e-4 * 64 / RES  # acceptance final-LOD rate scaled to the voxel size
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -369,13 +384,16 @@ def main():
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "kernel": "K2 ray pass: march_fwd + shade_fwd<4,4> + alpha_bwd + shade_bwd<4,4>",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": "K2 ray pass: march_scan + march_fwd (2 rounds) + record sort + shade_fwd<4,4> + "
+                          "alpha_bwd + shade_bwd<4,4> + shade_geo<4,4>",
                 "algorithmic_bytes_per_launch": k2_bytes, "kernel_ms": k2_ms, "peak_source": peak_src,
                 "k2_share_of_step": k2_ms / statistics.mean(step_ms),
-                "k2_kernels_ms": dict(zip(["march_fwd", "shade_fwd", "alpha_bwd", "shade_bwd"],
+                "k2_kernels_ms": dict(zip(["scan+march+sort", "shade_fwd", "alpha_bwd", "shade_bwd+geo"],
                                           [statistics.mean(p[k] for p in k2_parts) for k in range(4)])),
-                "note": "K2 = the four ray-pass kernels (psdf_train.cuh), timed together as one "
-                        "ray-pass unit; bytes per SURVEY 8(d)"}
+                "note": "K2 = the ray-pass kernels (psdf_train.cuh) timed together as one unit with CUDA "
+                        "events on the context stream; bytes per SURVEY 8(d); the regularizer kernel "
+                        "runs concurrently on a side stream"}
 
     # e2e: the reference-facing C-ABI call with pinned host buffers; H2D of the
     # step's images and the D2H loss read inside the timed region (wall clock)
@@ -482,7 +500,7 @@ def render_fps(api, torch, ctx, peak, frames=20):
     ms = e0.elapsed_time(e1) / frames
     c = cnt.as_dict()
     b = algorithmic_bytes(c, "render")
-    return {"config": "configs[3]: 1920x1080 view of the 512^3 scene, tau=3000/voxel",
+    return {"config": f"configs[3]: 1920x1080 view of the {RES}^3 scene, tau=3000/voxel",
             "fps": 1000.0 / ms, "ms_per_frame": ms, "kernel_ms": statistics.mean(kms),
             "marched_samples": c["n_marched"], "shaded_samples": c["n_shaded"],
             "samples_per_s": c["n_marched"] / (ms / 1000.0),
