@@ -668,6 +668,16 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     CK(cudaMemcpyAsync(c->h_wave_counters, W.counters, sizeof(unsigned) * 8, cudaMemcpyDeviceToHost, s));
 }
 
+// Stage-0 gradient copies (psdf_set_keep_raypass_grads); (re)allocated after
+// every grid upload, which frees them.
+void ensure_keep_buffers(psdf_ctx* c) {
+    if (!c->keep_raypass || c->d_grads0) return;
+    CK(cudaMalloc(&c->d_grads0, sizeof(float) * c->n_params));
+    CK(cudaMalloc(&c->d_gsmooth0, sizeof(float) * std::max<int64_t>(c->desc.T * TV, 4)));
+    CK(cudaMemsetAsync(c->d_grads0, 0, sizeof(float) * c->n_params, c->stream));
+    CK(cudaMemsetAsync(c->d_gsmooth0, 0, sizeof(float) * std::max<int64_t>(c->desc.T * TV, 4), c->stream));
+}
+
 RayPassParams base_params(psdf_ctx* c) {
     RayPassParams P{};
     P.g = c->view();
@@ -849,6 +859,7 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
     wave_overflow_kernel<<<1, 32, 0, s>>>(c->wave, c->d_counts + 7);
     CK(cudaGetLastError());
     if (c->keep_raypass) {
+        ensure_keep_buffers(c);
         CK(cudaMemcpyAsync(c->d_grads0, c->d_grads, sizeof(float) * c->n_params,
                            cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(c->d_gsmooth0, c->d_gsmooth, sizeof(float) * c->desc.T * TV,
@@ -1392,13 +1403,7 @@ int psdf_set_keep_raypass_grads(psdf_ctx* c, int keep) {
         need_grid(c);
         set_device(c);
         c->keep_raypass = keep != 0;
-        if (c->keep_raypass && !c->d_grads0) {
-            CK(cudaMalloc(&c->d_grads0, sizeof(float) * c->n_params));
-            CK(cudaMalloc(&c->d_gsmooth0, sizeof(float) * std::max<int64_t>(c->desc.T * TV, 4)));
-            CK(cudaMemsetAsync(c->d_grads0, 0, sizeof(float) * c->n_params, c->stream));
-            CK(cudaMemsetAsync(c->d_gsmooth0, 0, sizeof(float) * std::max<int64_t>(c->desc.T * TV, 4), c->stream));
-            CK(cudaStreamSynchronize(c->stream));
-        }
+        ensure_keep_buffers(c);
     });
 }
 

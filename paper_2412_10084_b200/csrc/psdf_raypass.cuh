@@ -331,6 +331,10 @@ __device__ __forceinline__ void mlp_forward(const float* __restrict__ sm, const 
     }
 }
 
+template <int NS, int NA>
+__device__ __forceinline__ void store_geo(const ShadeGeo& geo, const float (&pv)[3][NS],
+                                          const float (&x)[NS + NA + NPOW], float* geo_out);
+
 // decode_fused (renderer.cpp:88-147): features + MLP.  geo_out (optional)
 // receives the GeoRec block for the backward.
 template <int NS, int NA>
@@ -342,7 +346,16 @@ __device__ __forceinline__ void decode_forward(const RayPassParams& P, const flo
     float x[IN], pv[3][NS];
     decode_features<NS, NA>(P, tile, p, dneg, geo, x, pv);
     mlp_forward<IN>(sm, L, x, cam_row, rgb, nullptr, nullptr);
-    if (geo_out) {
+    if (geo_out) store_geo<NS, NA>(geo, pv, x, geo_out);
+}
+
+// The GeoRec block of a shaded sample (K2b -> K2e): geometry, plane taps,
+// probe weights, plane samples and the MLP input.
+template <int NS, int NA>
+__device__ __forceinline__ void store_geo(const ShadeGeo& geo, const float (&pv)[3][NS],
+                                          const float (&x)[NS + NA + NPOW], float* geo_out) {
+    constexpr int IN = NS + NA + NPOW;
+    {
         using GR = GeoRec<NS, NA>;
         float r[GR::STRIDE];
         r[0] = (float)geo.n[0];
