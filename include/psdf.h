@@ -205,6 +205,8 @@ int psdf_last_k2_breakdown(psdf_ctx* ctx, double* ms4, int64_t* entries, int64_t
 /* Raw CUDA stream of the context (cudaStream_t), for callers that time or
  * overlap work around the context. */
 void* psdf_stream(psdf_ctx* ctx);
+/* Host -> device bytes the last psdf_train_step copied (images + masks). */
+int64_t psdf_last_h2d_bytes(psdf_ctx* ctx);
 /* Page-locked host memory for staging images (cudaMallocHost). */
 void* psdf_host_alloc(size_t bytes);
 void psdf_host_free(void* p);

@@ -170,9 +170,10 @@ struct psdf_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool fork_regs = false;              // the ray pass records ev_fork (do_train_step)
     cudaEvent_t ev_copied = nullptr, ev_copy_free = nullptr;
-    std::vector<cudaEvent_t> view_ready;   // per staged view: its images are in HBM
-    int n_view_ready = 0;                  // > 0 only inside psdf_train_step
-    std::vector<int64_t> view_tiles;       // first global work tile per view (+ end)
+    bool images_pending = false;           // inside psdf_train_step: the copies may still run
+    cudaEvent_t ev_masks = nullptr, ev_rgb = nullptr;  // masks / colours of the step copied
+    unsigned* d_hand_bits = nullptr;       // [work tiles] scan hand-over lanes
+    int64_t hand_cap = 0;
     cudaEvent_t ev_ray0 = nullptr, ev_ray1 = nullptr, ev_step0 = nullptr, ev_step1 = nullptr;
 
     bool has_grid = false;
@@ -234,6 +235,7 @@ struct psdf_ctx {
     float last_k2_ms[4] = {0.f, 0.f, 0.f, 0.f};  // K2a, K2b, K2d, K2e
     int last_launches = 0;
     int64_t last_entries = 0, last_records = 0;
+    int64_t last_h2d_bytes = 0;    // host -> device bytes of the last psdf_train_step
     cudaEvent_t ev_k[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 
     // wavefront buffers of the train ray pass (psdf_train.cuh)
@@ -556,41 +558,31 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     const int64_t grid_s = std::max<int64_t>(1, std::min<int64_t>((n_work + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
                                                                    (int64_t)per_sm_s * c->sm_count));
     const int grid_a = blocks_per_sm((const void*)march_fwd_kernel, smem_bits) * c->sm_count;
-    const WaveBufs& W = c->wave;
+    WaveBufs W = c->wave;
     CK(cudaEventRecord(c->ev_ray0, s));
     CK(cudaEventRecord(c->ev_k[0], s));
     CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(W.counters, 0, sizeof(unsigned) * 8, s));
     P.work_counter = c->d_work;
-    if (c->n_view_ready == 0) {
-        P.scan_lo = 0;
-        P.scan_hi = n_work;
-        march_scan_kernel<<<(unsigned)grid_s, BLOCK, smem_bits, s>>>(P, W);
-        CK(cudaGetLastError());
-        ++c->last_launches;
-    } else {
-        // psdf_train_step: each view's scan starts as soon as its images have
-        // arrived (the copies of the next views overlap it)
-        for (int v = 0; v < c->n_view_ready; ++v) {
-            const int64_t lo = std::max<int64_t>(c->view_tiles[v], P.tile_begin) - P.tile_begin;
-            const int64_t hi = std::min<int64_t>(c->view_tiles[v + 1], P.tile_end) - P.tile_begin;
-            if (hi <= lo) continue;
-            CK(cudaStreamWaitEvent(s, c->view_ready[v], 0));
-            CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
-            RayPassParams Pv = P;
-            Pv.scan_lo = lo;
-            Pv.scan_hi = hi;
-            const int64_t gv = std::max<int64_t>(1, std::min<int64_t>((hi - lo + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
-                                                                      (int64_t)per_sm_s * c->sm_count));
-            march_scan_kernel<<<(unsigned)gv, BLOCK, smem_bits, s>>>(Pv, W);
-            CK(cudaGetLastError());
-            ++c->last_launches;
-        }
+    if (c->hand_cap < n_work) {  // per work tile: which lanes the scan handed over
+        if (c->d_hand_bits) cudaFree(c->d_hand_bits);
+        c->d_hand_bits = nullptr;
+        CK(cudaMalloc(&c->d_hand_bits, sizeof(unsigned) * std::max<int64_t>(n_work, 1)));
+        c->hand_cap = n_work;
     }
+    c->wave.hand_bits = W.hand_bits = c->d_hand_bits;
+    // the scan reads no image: with psdf_train_step it runs under the copies
+    P.scan_lo = 0;
+    P.scan_hi = n_work;
+    march_scan_kernel<<<(unsigned)grid_s, BLOCK, smem_bits, s>>>(P, W);
+    CK(cudaGetLastError());
+    ++c->last_launches;
     // handovers in append order: a warp's handovers come from one 8x4 pixel
     // tile and neighbouring warps from neighbouring work tiles (a sort by
     // pixel measured slower than it saved)
     CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
+    // the composite pass reads the masks (which rays are shaded)
+    if (c->images_pending) CK(cudaStreamWaitEvent(s, c->ev_masks, 0));
     // (render: one round; its rays are short at the render tau)
     march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, W, 0, P.mode == 1 ? INT_MAX : c->composite_steps);
     CK(cudaGetLastError());
@@ -650,6 +642,8 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
         ++c->last_launches;
         for (int k = 3; k <= 4; ++k) CK(cudaEventRecord(c->ev_k[k], s));
     } else {
+        // the photo terms read the ground-truth colours
+        if (c->images_pending) CK(cudaStreamWaitEvent(s, c->ev_rgb, 0));
         const int grid_ab = blocks_per_sm((const void*)alpha_bwd_kernel, 0) * c->sm_count;
         alpha_bwd_kernel<<<grid_ab, BLOCK, 0, s>>>(P, W);
         CK(cudaGetLastError());
@@ -676,6 +670,18 @@ void ensure_keep_buffers(psdf_ctx* c) {
     CK(cudaMalloc(&c->d_gsmooth0, sizeof(float) * std::max<int64_t>(c->desc.T * TV, 4)));
     CK(cudaMemsetAsync(c->d_grads0, 0, sizeof(float) * c->n_params, c->stream));
     CK(cudaMemsetAsync(c->d_gsmooth0, 0, sizeof(float) * std::max<int64_t>(c->desc.T * TV, 4), c->stream));
+}
+
+// The photo terms of the rays the scan finished (stats only), on `st`.
+void launch_empty_ray_loss(psdf_ctx* c, const RayPassParams& P, cudaStream_t st) {
+    const int64_t n_work = P.tile_end - P.tile_begin;
+    if (n_work <= 0) return;
+    if (c->images_pending) CK(cudaStreamWaitEvent(st, c->ev_rgb, 0));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n_work + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
+                                                                (int64_t)16 * c->sm_count));
+    empty_ray_loss_kernel<<<(unsigned)grid, BLOCK, 0, st>>>(P, c->wave, n_work);
+    CK(cudaGetLastError());
+    ++c->last_launches;
 }
 
 RayPassParams base_params(psdf_ctx* c) {
@@ -817,7 +823,10 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
                 g, c->d_params + c->off_raw, t0, (float)hp->l_sdf, (float)hp->l_eik, (float)hp->l_norm,
                 (float)(1.0 / (2.0 * c->desc.voxel_size)), c->d_gsmooth, c->d_grads + c->off_raw, c->d_stats);
             CK(cudaGetLastError());
-            if (overlap) CK(cudaEventRecord(c->ev_join, c->side_stream));
+            if (overlap) {  // the empty rays' photo terms also run on the side stream
+                launch_empty_ray_loss(c, P, c->side_stream);
+                CK(cudaEventRecord(c->ev_join, c->side_stream));
+            }
             dispatch_ns(c->desc.n_s, [&]<int NS>() {
                 loss_features_kernel<NS><<<3 * (t1 - t0), 256, 0, s>>>(g, t0, (float)hp->l_feat,
                                                                        c->d_grads + c->off_planes, c->d_stats);
@@ -837,8 +846,7 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
     const bool overlap = !c->keep_raypass;
     // images still arriving (psdf_train_step): the regularizer runs under the
     // copies; resident images: under the ray pass's tail (forked by it)
-    c->fork_regs = overlap && c->n_view_ready == 0;
-    if (overlap && !c->fork_regs) CK(cudaEventRecord(c->ev_fork, s));
+    c->fork_regs = overlap;
     if (images_ready) CK(cudaStreamWaitEvent(s, images_ready, 0));
     const int64_t tiles = upload_viewdev(c, vd);
     // ray-batch data parallelism: contiguous 1/N slice of the batch's work tiles
@@ -868,6 +876,7 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
     c->fork_regs = false;
     regularizers(overlap);
     if (overlap) CK(cudaStreamWaitEvent(s, c->ev_join, 0));
+    else launch_empty_ray_loss(c, P, s);
     // G^T fold (grads.cpp:67-96): raw_grad += G^T * staged
     launch_fold(c, c->d_gsmooth, c->d_grads + c->off_raw);
     // all-reduce across ranks (GradBuffers::add, trainer.cpp:184-185, across GPUs)
@@ -985,6 +994,8 @@ int psdf_create(int device, psdf_ctx** out) {
         CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_copied, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_masks, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_rgb, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_copy_free, cudaEventDisableTiming));
         CK(cudaEventRecord(c->ev_copy_free, c->stream));
         CK(cudaEventCreate(&c->ev_ray0));
@@ -1036,7 +1047,9 @@ int psdf_destroy(psdf_ctx* c) {
         cudaEventDestroy(c->ev_join);
         cudaEventDestroy(c->ev_copied);
         cudaEventDestroy(c->ev_copy_free);
-        for (auto e : c->view_ready) cudaEventDestroy(e);
+        cudaEventDestroy(c->ev_masks);
+        cudaEventDestroy(c->ev_rgb);
+        if (c->d_hand_bits) cudaFree(c->d_hand_bits);
         delete c;
     });
 }
@@ -1505,37 +1518,37 @@ int psdf_train_step(psdf_ctx* c, int n_views, const psdf_camera* cams, const flo
         std::vector<DevView> tmp(n_views);
         std::vector<DevView*> batch(n_views);
         size_t off = 0;
-        while ((int)c->view_ready.size() < n_views) {
-            cudaEvent_t e;
-            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-            c->view_ready.push_back(e);
-        }
-        c->view_tiles.assign(n_views + 1, 0);
         CK(cudaStreamWaitEvent(c->copy_stream, c->ev_copy_free, 0));  // staging no longer read
+        // masks first (the composite pass needs them), then the colours (the
+        // photo terms); the scan reads neither and runs under the copies
+        c->last_h2d_bytes = 0;
         for (int i = 0; i < n_views; ++i) {
             const size_t n = (size_t)cams[i].width * cams[i].height;
             tmp[i].cam = cams[i];
             tmp[i].rgb = c->d_stage_rgb + 3 * off;
             tmp[i].mask = c->d_stage_mask + off;
-            CK(cudaMemcpyAsync(tmp[i].rgb, gt_rgb[i], sizeof(float) * 3 * n, cudaMemcpyHostToDevice,
-                               c->copy_stream));
             CK(cudaMemcpyAsync(tmp[i].mask, mask[i], n, cudaMemcpyHostToDevice, c->copy_stream));
-            CK(cudaEventRecord(c->view_ready[i], c->copy_stream));
-            c->view_tiles[i + 1] = c->view_tiles[i] + (int64_t)((cams[i].width + 7) / 8) * ((cams[i].height + 3) / 4);
             batch[i] = &tmp[i];
             off += n;
+            c->last_h2d_bytes += (int64_t)n;
         }
-        // the copies overlap the step's image-independent kernels (regularizers)
-        // and, view by view, the saturated-prefix scans
+        CK(cudaEventRecord(c->ev_masks, c->copy_stream));
+        for (int i = 0; i < n_views; ++i) {
+            const size_t n = (size_t)cams[i].width * cams[i].height;
+            CK(cudaMemcpyAsync(tmp[i].rgb, gt_rgb[i], sizeof(float) * 3 * n, cudaMemcpyHostToDevice,
+                               c->copy_stream));
+            c->last_h2d_bytes += (int64_t)(sizeof(float) * 3 * n);
+        }
+        CK(cudaEventRecord(c->ev_rgb, c->copy_stream));
         CK(cudaEventRecord(c->ev_copied, c->copy_stream));
-        c->n_view_ready = n_views;
+        c->images_pending = true;
         try {
             do_train_step(c, batch, hp, losses, counts, nullptr);
         } catch (...) {
-            c->n_view_ready = 0;
+            c->images_pending = false;
             throw;
         }
-        c->n_view_ready = 0;
+        c->images_pending = false;
         CK(cudaStreamWaitEvent(c->stream, c->ev_copied, 0));
         CK(cudaEventRecord(c->ev_copy_free, c->stream));
         tmp.clear();
@@ -1673,6 +1686,8 @@ int psdf_last_timing(psdf_ctx* c, double* ray_ms, double* step_ms, int* launches
 }
 
 void* psdf_stream(psdf_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int64_t psdf_last_h2d_bytes(psdf_ctx* c) { return c ? c->last_h2d_bytes : -1; }
 
 void* psdf_host_alloc(size_t bytes) {
     void* p = nullptr;

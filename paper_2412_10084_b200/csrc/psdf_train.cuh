@@ -88,6 +88,7 @@ struct WaveBufs {
     int4* a_i;         // [cap] (tile of the sample, tile of the next point or -1 for the
                        //        one-past-the-end point, record or -1, next alpha sample or -1)
     int* e_ahead;      // first alpha sample of the entry
+    unsigned* hand_bits;  // [work tiles] lanes of each 8x4 pixel tile handed over by the scan (train)
     unsigned* counters;  // [0] entries, [1] records, [2] handovers, [3] continuations, [4] alpha samples
     int e_cap, r_cap, h_cap, k_cap, a_cap;
 };
@@ -246,14 +247,14 @@ __global__ void __launch_bounds__(BLOCK, PSDF_SCAN_MINB) march_scan_kernel(RayPa
             if (P.out_depth) P.out_depth[R.px] = 0.f;
         } else if (R.valid) {
             // every settle had alpha 0: acc = 0, nothing shaded, nothing to
-            // back-propagate; the loss is final now
+            // back-propagate; its photo term (stats only) is taken by
+            // empty_ray_loss_kernel once the images are in HBM, so the scan
+            // itself reads no image and can run under the image copies
             c_m += k;
-            const bool in_mask = __ldg(R.V->mask + R.px) != 0;
-            const double col[3] = {P.bg[0], P.bg[1], P.bg[2]};
-            double g0, g1, g2, dA;
-            if (photo_term(P, in_mask, R.V->gt + 3 * R.px, col, 0.0, g0, g1, g2, dA, st_photo, st_sq,
-                           st_mask))
-                ++c_bwd;
+        }
+        if (P.mode != 1) {
+            const unsigned hb = __ballot_sync(FULL, hand);
+            if (lane == 0) W.hand_bits[wi] = hb;
         }
     }
     st_photo = warp_sum_d(st_photo);
@@ -269,6 +270,49 @@ __global__ void __launch_bounds__(BLOCK, PSDF_SCAN_MINB) march_scan_kernel(RayPa
         atomicAdd(P.counts + 1, m);
         atomicAdd(P.counts + 2, x);
         atomicAdd(P.counts + 5, bw);
+    }
+}
+
+// photo_pixel (losses.cpp:8-38) of the rays the scan finished (no alpha > 0
+// settle: colour = background, acc = 0, so only the loss statistics and the
+// backward-ray count change — nothing is back-propagated).  One warp per
+// 8x4 pixel work tile.
+__global__ void __launch_bounds__(BLOCK) empty_ray_loss_kernel(RayPassParams P, WaveBufs W, int64_t n_work) {
+    const int lane = threadIdx.x & 31;
+    double st_photo = 0.0, st_sq = 0.0;
+    unsigned long long st_mask = 0, c_bwd = 0;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t wi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); wi < n_work; wi += warps) {
+        const unsigned hb = __ldg(W.hand_bits + wi);
+        if (hb == FULL) continue;
+        const LaneRay R = lane_ray(P, (int)wi, lane);
+        if (!R.valid || ((hb >> lane) & 1u)) continue;
+        const bool in_mask = __ldg(R.V->mask + R.px) != 0;
+        const double col[3] = {P.bg[0], P.bg[1], P.bg[2]};
+        double g0, g1, g2, dA;
+        if (photo_term(P, in_mask, R.V->gt + 3 * R.px, col, 0.0, g0, g1, g2, dA, st_photo, st_sq, st_mask))
+            ++c_bwd;
+    }
+    // block-wide sums, one atomic per value per block
+    st_photo = warp_sum_d(st_photo);
+    st_sq = warp_sum_d(st_sq);
+    st_mask = warp_sum_u(st_mask);
+    c_bwd = warp_sum_u(c_bwd);
+    __shared__ double red[WARPS_PER_BLOCK][4];
+    if (lane == 0) {
+        red[threadIdx.x >> 5][0] = st_photo;
+        red[threadIdx.x >> 5][1] = st_sq;
+        red[threadIdx.x >> 5][2] = (double)st_mask;
+        red[threadIdx.x >> 5][3] = (double)c_bwd;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double v = 0.0;
+        for (int w = 0; w < WARPS_PER_BLOCK; ++w) v += red[w][threadIdx.x];
+        if (v != 0.0) {
+            if (threadIdx.x < 3) atomicAdd(P.stats + threadIdx.x, v);
+            else atomicAdd(P.counts + 5, (unsigned long long)v);
+        }
     }
 }
 
