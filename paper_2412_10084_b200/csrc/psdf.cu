@@ -185,8 +185,6 @@ struct psdf_ctx {
     int32_t* d_tile_table = nullptr;
     uint32_t* d_tile_bits = nullptr;
     uint8_t* d_tile_dist = nullptr;
-    float* d_tile_min = nullptr;   // [T] minimum of each tile's apron brick
-    float* d_block_min = nullptr;  // [T][64] minimum of each 4^3 block's brick
     int32_t* d_tile_nbr = nullptr; // [T][27] neighbour tile ids
     int occ_tlo[3] = {0, 0, 0}, occ_thi[3] = {-1, -1, -1};  // allocated tiles' bounding box (tile coords)
     uint8_t* d_sat_dist = nullptr; // [T][17^3] per-cell saturation distances of the current ray pass
@@ -267,8 +265,6 @@ struct psdf_ctx {
         g.tile_table = d_tile_table;
         g.tile_bits = d_tile_bits;
         g.tile_dist = d_tile_dist;
-        g.tile_min = d_tile_min;
-        g.block_min = d_block_min;
         g.tile_nbr = d_tile_nbr;
         g.sat_dist = d_sat_dist;
         // decision margin of the marcher's fast paths; PSDF_TEST_MARGIN widens
@@ -286,7 +282,7 @@ struct psdf_ctx {
     }
 
     void free_grid() {
-        for (void* p : {(void*)d_tile_table, (void*)d_tile_bits, (void*)d_tile_dist, (void*)d_tile_min, (void*)d_block_min, (void*)d_tile_nbr, (void*)d_sat_dist, (void*)d_tile_coords, (void*)d_probe_ids,
+        for (void* p : {(void*)d_tile_table, (void*)d_tile_bits, (void*)d_tile_dist, (void*)d_tile_nbr, (void*)d_sat_dist, (void*)d_tile_coords, (void*)d_probe_ids,
                         (void*)d_probe_table, (void*)d_probe_coords, (void*)d_params,
                         (void*)d_smooth, (void*)d_smooth_ap, (void*)d_grads, (void*)d_gsmooth, (void*)d_grads0,
                         (void*)d_gsmooth0, (void*)d_m, (void*)d_v})
@@ -294,8 +290,6 @@ struct psdf_ctx {
         d_tile_table = nullptr;
         d_tile_bits = nullptr;
         d_tile_dist = nullptr;
-        d_tile_min = nullptr;
-        d_block_min = nullptr;
         d_tile_nbr = nullptr;
         d_sat_dist = nullptr;
         d_tile_coords = nullptr;
@@ -395,8 +389,7 @@ void launch_fold(psdf_ctx* c, const float* src, float* dst) {
 // Refreshes the apron copy (and brick minima) from the current smoothed grid.
 void fill_apron(psdf_ctx* c) {
     if (c->desc.T == 0) return;
-    apron_fill_kernel<<<c->desc.T, 256, 0, c->stream>>>(c->view(), c->d_smooth, c->d_smooth_ap,
-                                                         c->d_tile_min, c->d_block_min);
+    apron_fill_kernel<<<c->desc.T, 256, 0, c->stream>>>(c->view(), c->d_smooth, c->d_smooth_ap);
     CK(cudaGetLastError());
     ++c->last_launches;
 }
@@ -412,7 +405,7 @@ void smooth_all(psdf_ctx* c) {
     }
     smooth_apron_kernel<<<c->desc.T, PSDF_SMOOTH_THREADS, kSmoothApronSmem, c->stream>>>(
         c->view(), c->d_params + c->off_raw, (float)(c->desc.far_field_voxels * c->desc.voxel_size),
-        c->d_smooth, c->d_smooth_ap, c->d_tile_min, c->d_block_min, gaussian_taps());
+        c->d_smooth, c->d_smooth_ap, gaussian_taps());
     CK(cudaGetLastError());
     ++c->last_launches;
 }
@@ -1181,8 +1174,6 @@ int psdf_upload_grid(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_c
         CK(cudaMalloc(&c->d_v, sizeof(float) * c->n_params));
         CK(cudaMalloc(&c->d_smooth, sizeof(float) * std::max<int64_t>(T * TV, 4)));
         CK(cudaMalloc(&c->d_smooth_ap, sizeof(float) * std::max<int64_t>(T * AV, 4)));
-        CK(cudaMalloc(&c->d_tile_min, sizeof(float) * std::max<int64_t>(T, 1)));
-        CK(cudaMalloc(&c->d_block_min, sizeof(float) * std::max<int64_t>(64 * T, 1)));
         CK(cudaMalloc(&c->d_sat_dist, std::max<int64_t>((int64_t)kCellN * T, 1)));
         CK(cudaMalloc(&c->d_gsmooth, sizeof(float) * std::max<int64_t>(T * TV, 4)));
         CK(cudaMemsetAsync(c->d_params, 0, sizeof(float) * c->n_params, c->stream));

@@ -65,8 +65,6 @@ struct GridView {
     const int32_t* __restrict__ probe_ids;    // [T][8]
     const float* __restrict__ smooth;         // [T][4096]
     const float* __restrict__ smooth_ap;      // [T][18^3] smooth with a 1-voxel apron
-    const float* __restrict__ tile_min;       // [T] min of each apron brick
-    const float* __restrict__ block_min;      // [T][64] min over each 4^3 block's 6^3 brick
     const uint8_t* __restrict__ sat_dist;     // [T][17^3] per-cell saturation distances of this pass (sat_dist_kernel)
     const float* __restrict__ planes;         // [T][3][256][n_s]
     const float* __restrict__ probes;         // [P][order^2][n_a]

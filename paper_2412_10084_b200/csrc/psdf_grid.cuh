@@ -165,8 +165,7 @@ constexpr size_t kFoldSmem = sizeof(float) * (HV + 16 * HE * HE);
 // unallocated / outside the grid) come from one 22^3 raw halo, so no second
 // pass over the smoothed grid is needed; every smoothed value is the same
 // fp32 expression (same taps, same summation order) whichever tile's block
-// computes it.  Also writes the brick minima of the saturation test
-// (tile_min, block_min; psdf_device.cuh kSatX).
+// computes it.
 constexpr int SE = 22;  // raw halo edge: local voxels [-3, 19)
 constexpr int SZ = SE + 1;  // padded z stride of the y-pass output
 constexpr size_t kSmoothApronSmem = sizeof(float) * (SE * SE * SE + AE * SE * SE);
@@ -175,11 +174,9 @@ constexpr size_t kSmoothApronSmem = sizeof(float) * (SE * SE * SE + AE * SE * SE
 #endif
 __global__ void __launch_bounds__(PSDF_SMOOTH_THREADS) smooth_apron_kernel(GridView g, const float* __restrict__ raw,
                                                            float fill, float* __restrict__ smooth,
-                                                           float* __restrict__ ap, float* __restrict__ tmin,
-                                                           float* __restrict__ bmin, Taps taps) {
+                                                           float* __restrict__ ap, Taps taps) {
     extern __shared__ __align__(16) float sh[];
     __shared__ int nb[27];
-    __shared__ float red[2];
     float* A = sh;                  // [22][22][22] raw halo; later [18][18][23]
     float* B = sh + SE * SE * SE;   // [18][22][22] after the x pass; later the 18^3 apron
     const int t = blockIdx.x;
@@ -209,36 +206,17 @@ __global__ void __launch_bounds__(PSDF_SMOOTH_THREADS) smooth_apron_kernel(GridV
             sm[vox_index(lx, ly, lz)] = s;
         } else if (nb[((lx >> 4) + 1) * 9 + ((ly >> 4) + 1) * 3 + (lz >> 4) + 1] < 0) {
             s = (float)g.far;  // smooth_value (grid.cpp:87-94)
-            B[i] = s;
         }
         apt[i] = s;
     }
-    __syncthreads();
-    // brick minima: each 4^3 block's 6^3 brick (voxels 4b-1 .. 4b+4) and the tile
-    if (threadIdx.x < 64) {
-        const int bx = threadIdx.x >> 4, by = (threadIdx.x >> 2) & 3, bz = threadIdx.x & 3;
-        float mn = 3.4e38f;
-        for (int x = 0; x < 6; ++x)
-            for (int y = 0; y < 6; ++y)
-#pragma unroll
-                for (int z = 0; z < 6; ++z) mn = fminf(mn, B[((4 * bx + x) * AE + 4 * by + y) * AE + 4 * bz + z]);
-        bmin[(int64_t)t * 64 + threadIdx.x] = mn;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mn;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) tmin[t] = fminf(red[0], red[1]);
 }
 
-// The apron copy (and brick minima) from an already smoothed grid: used when
-// the host uploads its own smoothed values (psdf_upload_grid with `smooth`).
+// The apron copy from an already smoothed grid: used when the host uploads
+// its own smoothed values (psdf_upload_grid with `smooth`).
 __global__ void __launch_bounds__(256) apron_fill_kernel(GridView g, const float* __restrict__ smooth,
-                                                         float* __restrict__ ap, float* __restrict__ tmin,
-                                                         float* __restrict__ bmin) {
+                                                         float* __restrict__ ap) {
     __shared__ float B[AV];
     __shared__ int nb[27];
-    __shared__ float red[2];
     const int t = blockIdx.x;
     stage_nbr(g, t, nb);
     __syncthreads();
@@ -246,20 +224,6 @@ __global__ void __launch_bounds__(256) apron_fill_kernel(GridView g, const float
     __syncthreads();
     float* apt = ap + (int64_t)t * AV;
     for (int i = threadIdx.x; i < AV; i += blockDim.x) apt[i] = B[i];
-    if (threadIdx.x < 64) {
-        const int bx = threadIdx.x >> 4, by = (threadIdx.x >> 2) & 3, bz = threadIdx.x & 3;
-        float mn = 3.4e38f;
-        for (int x = 0; x < 6; ++x)
-            for (int y = 0; y < 6; ++y)
-#pragma unroll
-                for (int z = 0; z < 6; ++z) mn = fminf(mn, B[((4 * bx + x) * AE + 4 * by + y) * AE + 4 * bz + z]);
-        bmin[(int64_t)t * 64 + threadIdx.x] = mn;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mn;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) tmin[t] = fminf(red[0], red[1]);
 }
 
 // Saturation distances for one ray pass (its tau), per trilinear cell: cell b
