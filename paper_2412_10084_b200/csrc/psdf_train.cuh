@@ -1113,11 +1113,11 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
 // atomics (grid.cpp:189-202), the probe direction gradient (sh.cpp:151-169),
 // probe coefficient gradients aggregated over the warp's lanes sharing a
 // tile, and the SDF-gradient chain of the normal (renderer.cpp:216-235).
-constexpr int PWS = 33;  // row stride of the per-warp probe staging (w8 | Y[16] | gfa)
+constexpr int PWS = 36;  // row stride of the per-warp probe staging (w8 | Y[16] | gfa), float4 aligned
 template <int NS, int NA>
 __global__ void __launch_bounds__(BLOCK) shade_geo_kernel(RayPassParams P, WaveBufs W) {
     const int n_rec = n_records(W);
-    __shared__ float s_pw[WARPS_PER_BLOCK][32 * PWS];
+    __shared__ __align__(16) float s_pw[WARPS_PER_BLOCK][32 * PWS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* PW = s_pw[warp];
     const GridView& g = P.g;
@@ -1253,22 +1253,35 @@ __global__ void __launch_bounds__(BLOCK) shade_geo_kernel(RayPassParams P, WaveB
                 const unsigned grp = __ballot_sync(FULL, ((rem >> lane) & 1u) && tile == t0);
                 rem &= ~grp;
                 const int32_t* pid = g.probe_ids + (int64_t)t0 * 8;
-                for (int q = lane; q < 8 * nc; q += 32) {
-                    const int c = q / nc, j = q - (q / nc) * nc;
-                    float a[NA];
+                // A[c][j][k] = sum_s w_c(s) Y_j(s) gfa_k(s): lane = (corner half, j),
+                // all k; the group's rows are shared-memory broadcasts
+                const int half = lane >> 4, j = lane & 15;
+                if (j < nc) {
+                    float a[4][NA];
+                    bool anyc[4] = {false, false, false, false};
 #pragma unroll
-                    for (int k = 0; k < NA; ++k) a[k] = 0.f;
-                    bool any = false;
+                    for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+                        for (int k = 0; k < NA; ++k) a[cc][k] = 0.f;
                     for (unsigned m = grp; m; m &= m - 1) {
-                        const int s = __ffs(m) - 1;
-                        const float wc = PW[s * PWS + c];
-                        if (wc == 0.f) continue;
-                        any = true;
-                        const float f = wc * PW[s * PWS + 8 + j];
+                        const float* row = PW + (__ffs(m) - 1) * PWS;
+                        const float4 w4 = *reinterpret_cast<const float4*>(row + 4 * half);
+                        const float wc[4] = {w4.x, w4.y, w4.z, w4.w};
+                        const float y = row[8 + j];
+                        float u[NA];
 #pragma unroll
-                        for (int k = 0; k < NA; ++k) a[k] += f * PW[s * PWS + 24 + k];
+                        for (int k = 0; k < NA; ++k) u[k] = y * row[24 + k];
+#pragma unroll
+                        for (int cc = 0; cc < 4; ++cc) {
+                            anyc[cc] |= wc[cc] != 0.f;
+#pragma unroll
+                            for (int k = 0; k < NA; ++k) a[cc][k] += wc[cc] * u[k];
+                        }
                     }
-                    if (any) red_vec<NA>(P.g_probes + (int64_t)__ldg(pid + c) * stride + j * NA, a);
+#pragma unroll
+                    for (int cc = 0; cc < 4; ++cc)
+                        if (anyc[cc])
+                            red_vec<NA>(P.g_probes + (int64_t)__ldg(pid + 4 * half + cc) * stride + j * NA, a[cc]);
                 }
             }
             __syncwarp();
