@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(LG_THREADS, 2) loss_grid_kernel(GridView g, co
                                                                  float* __restrict__ g_raw, double* stats) {
     extern __shared__ __align__(16) float sh[];
     float* val = sh;                                    // [20^3] smoothed values (far field outside)
-    float4* P = reinterpret_cast<float4*>(sh + HV);     // [17^3] (gradient, 1/|gradient|), then D
+    float4* P = reinterpret_cast<float4*>(sh + HV);     // [17^3] (gradient, proximity weight), then D
     uint32_t* alloc = reinterpret_cast<uint32_t*>(sh + HV + 4 * DN);  // [20^3] bits
     __shared__ int nb[27];
     __shared__ double red[6 * (LG_THREADS / 32)];
@@ -389,8 +389,9 @@ __global__ void __launch_bounds__(LG_THREADS, 2) loss_grid_kernel(GridView g, co
             const float gx = (val[hidx(x + 1, y, z)] - val[hidx(x - 1, y, z)]) * inv2h;
             const float gy = (val[hidx(x, y + 1, z)] - val[hidx(x, y - 1, z)]) * inv2h;
             const float gz = (val[hidx(x, y, z + 1)] - val[hidx(x, y, z - 1)]) * inv2h;
-            const float q = gx * gx + gy * gy + gz * gz;
-            P[i] = make_float4(gx, gy, gz, q > 0.f ? rsqrtf(q) : 0.f);
+            // (gradient, proximity weight): the weight once per centre; 1/|g|
+            // is recomputed where needed (one rsqrt)
+            P[i] = make_float4(gx, gy, gz, weight(x, y, z));
         }
     }
     __syncthreads();
@@ -408,10 +409,10 @@ __global__ void __launch_bounds__(LG_THREADS, 2) loss_grid_kernel(GridView g, co
                 const int x = c.x + 2, y = c.y + 2, z = c.z + 2;
                 const float4 pc = P[i];
                 const float q = pc.x * pc.x + pc.y * pc.y + pc.z * pc.z;
-                const float inv = pc.w;
+                const float inv = q > 0.f ? rsqrtf(q) : 0.f;
                 const float len = q * inv;  // |g|
                 if (in_tile(x, y, z)) {
-                    const float w = weight(x, y, z);
+                    const float w = pc.w;
                     const float e = len - 1.f;
                     acc[2] += (double)(l_eik * e * e);
                     acc[3] += (double)(l_eik * w * e * e);
@@ -428,8 +429,10 @@ __global__ void __launch_bounds__(LG_THREADS, 2) loss_grid_kernel(GridView g, co
                             const int nx = x + (a == 0), ny = y + (a == 1), nz = z + (a == 2);
                             if (!bit_at(alloc, hidx(nx, ny, nz))) continue;
                             const float4 ph = P[i + (a == 0 ? SX : a == 1 ? SY : 1)];
-                            if (ph.x * ph.x + ph.y * ph.y + ph.z * ph.z < 1e-16f) continue;
-                            const float ddx = ph.x * ph.w - n1x, ddy = ph.y * ph.w - n1y, ddz = ph.z * ph.w - n1z;
+                            const float qh = ph.x * ph.x + ph.y * ph.y + ph.z * ph.z;
+                            if (qh < 1e-16f) continue;
+                            const float ih = rsqrtf(qh);
+                            const float ddx = ph.x * ih - n1x, ddy = ph.y * ih - n1y, ddz = ph.z * ih - n1z;
                             const float vv = ddx * ddx + ddy * ddy + ddz * ddz;
                             acc[4] += (double)(l_norm * vv);
                             acc[5] += (double)(l_norm * w * vv);
@@ -451,10 +454,12 @@ __global__ void __launch_bounds__(LG_THREADS, 2) loss_grid_kernel(GridView g, co
                         const int px = x - (a == 0), py = y - (a == 1), pz = z - (a == 2);
                         if (!in_tile(px, py, pz)) continue;
                         const float4 ph = P[i - (a == 0 ? SX : a == 1 ? SY : 1)];
-                        if (ph.x * ph.x + ph.y * ph.y + ph.z * ph.z < 1e-16f) continue;
-                        const float cn = 2.f * l_norm * weight(px, py, pz);
-                        const float m2x = cn * (n2x - ph.x * ph.w), m2y = cn * (n2y - ph.y * ph.w),
-                                    m2z = cn * (n2z - ph.z * ph.w);
+                        const float qh = ph.x * ph.x + ph.y * ph.y + ph.z * ph.z;
+                        if (qh < 1e-16f) continue;
+                        const float ih = rsqrtf(qh);
+                        const float cn = 2.f * l_norm * ph.w;
+                        const float m2x = cn * (n2x - ph.x * ih), m2y = cn * (n2y - ph.y * ih),
+                                    m2z = cn * (n2z - ph.z * ih);
                         const float p2 = m2x * n2x + m2y * n2y + m2z * n2z;
                         dx += (m2x - n2x * p2) * inv;
                         dy += (m2y - n2y * p2) * inv;
