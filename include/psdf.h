@@ -147,6 +147,18 @@ int psdf_subdivide(psdf_ctx* ctx, double band_voxels, int32_t* out_T, int32_t* o
  * exceeds 4; new bands start at zero.  Optimizer state is reset. */
 int psdf_raise_sh_order(psdf_ctx* ctx, int new_order);
 
+/* Replaces init_grid_visual_hull(cfg, cameras, masks) (grid.cpp:470-504,
+ * SURVEY.md 8f row 3; the CLI default init, main.cpp:188-192): the context's
+ * grid becomes the visual-hull initialisation — occupancy by projection into
+ * every mask (uint8, > 127 = foreground), squared EDTs to the occupied and the
+ * free set, seed SDF, tiles within band_voxels — with the reference's tile /
+ * probe order and defaults (planes 0.5, probes 0, smoothed).  desc gives the
+ * configuration (res, voxel_size, origin, n_s, n_a, sh_order,
+ * far_field_voxels, ncam; T / P ignored); the MLP is zero until
+ * psdf_upload_mlp.  out_T / out_P may be NULL. */
+int psdf_init_visual_hull(psdf_ctx* ctx, const psdf_grid_desc* desc, int band_voxels, int n_cams,
+                          const psdf_camera* cams, const uint8_t* const* masks, int32_t* out_T, int32_t* out_P);
+
 /* Keep a copy of the stage-0 (post ray pass) gradients on every step. */
 int psdf_set_keep_raypass_grads(psdf_ctx* ctx, int keep);
 int psdf_download_grads(psdf_ctx* ctx, int stage, float* raw, float* smooth, float* planes,

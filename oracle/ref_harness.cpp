@@ -280,6 +280,41 @@ RefScene* ref_scene_analytic(int res, double voxel_size, double ox, double oy, d
 
 void ref_scene_free(RefScene* s) { delete s; }
 
+// init_grid_visual_hull (grid.cpp:470-504) through the reference's own code.
+RefScene* ref_scene_hull(int res, double voxel_size, double ox, double oy, double oz, int n_s, int n_a,
+                         int sh_order, int band_voxels, double far_field_voxels, int n_cams,
+                         const RefCamera* cams, const uint8_t* const* masks, int ncam_bias,
+                         uint64_t mlp_seed) {
+    try {
+        GridConfig cfg;
+        cfg.resolution = {res, res, res};
+        cfg.voxel_size = voxel_size;
+        cfg.origin = {ox, oy, oz};
+        cfg.n_s = n_s;
+        cfg.n_a = n_a;
+        cfg.sh_order = sh_order;
+        cfg.band_voxels = band_voxels;
+        cfg.far_field_voxels = far_field_voxels;
+        std::vector<Camera> cv;
+        std::vector<MaskImage> mv;
+        for (int i = 0; i < n_cams; ++i) {
+            cv.push_back(to_cam(cams + i));
+            MaskImage m;
+            m.width = cams[i].width;
+            m.height = cams[i].height;
+            m.data.assign(masks[i], masks[i] + (size_t)m.width * m.height);
+            mv.push_back(std::move(m));
+        }
+        auto* s = new RefScene;
+        s->grid = init_grid_visual_hull(cfg, cv, mv);
+        s->mlp = DecoderMlp::glorot_init(n_s, n_a, ncam_bias, mlp_seed);
+        return s;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
 // Seeded "trained-like" parameters: the pattern of test_renderer.cpp:32-43 and
 // gradcheck.cpp:40-53 (raw jitter, planes 0.5 +- plane_amp, probes +- probe_amp,
 // camera bias +- bias_amp), then smooth_all.

@@ -106,6 +106,10 @@ def reflib():
                                      _dp, _dp, C.c_int, C.c_uint64]
     L.ref_scene_free.argtypes = [C.c_void_p]
     L.ref_subdivide.argtypes = [C.c_void_p]
+    L.ref_scene_hull.restype = C.c_void_p
+    L.ref_scene_hull.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int,
+                                 C.c_int, C.c_int, C.c_double, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                                 C.c_uint64]
     L.ref_raise_sh_order.argtypes = [C.c_void_p, C.c_int]
     L.ref_scene_randomize.argtypes = [C.c_void_p, C.c_uint64, C.c_double, C.c_double, C.c_double,
                                       C.c_double]
@@ -185,6 +189,21 @@ class RefScene:
         h = L.ref_scene_sphere(res, 1.0 / res, origin[0], origin[1], origin[2], n_s, n_a, sh_order,
                                band_voxels, far_field_voxels, center[0], center[1], center[2], radius,
                                ncam, mlp_seed)
+        if not h:
+            raise RuntimeError(L.ref_last_error().decode())
+        return cls(h)
+
+    @classmethod
+    def hull(cls, cams, masks, res=32, n_s=2, n_a=2, sh_order=2, band_voxels=6, far_field_voxels=4.0,
+             ncam=0, mlp_seed=1, origin=(-0.5, -0.5, -0.5)):
+        """init_grid_visual_hull (grid.cpp:470-504): masks are uint8 images (> 127 = foreground)."""
+        L = reflib()
+        n = len(cams)
+        carr = (RefCamera * n)(*cams)
+        ms = [np.ascontiguousarray(m, np.uint8) for m in masks]
+        mp = (C.c_void_p * n)(*[m.ctypes.data for m in ms])
+        h = L.ref_scene_hull(res, 1.0 / res, origin[0], origin[1], origin[2], n_s, n_a, sh_order, band_voxels,
+                             far_field_voxels, n, C.cast(carr, C.c_void_p), C.cast(mp, C.c_void_p), ncam, mlp_seed)
         if not h:
             raise RuntimeError(L.ref_last_error().decode())
         return cls(h)

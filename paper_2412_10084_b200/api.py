@@ -418,6 +418,26 @@ class Context:
         self._check(self.L.psdf_subdivide(self.h, float(bv), None, None))
         return self._refresh_grid()
 
+    def init_visual_hull(self, cfg: GridConfig, cameras, masks, ncam=0):
+        """init_grid_visual_hull (grid.cpp:470-504) on the device; masks are uint8
+        images (> 127 = foreground).  Returns the new HostGrid (MLP zero)."""
+        d = psdf_grid_desc()
+        d.n_s, d.n_a, d.sh_order = cfg.n_s, cfg.n_a, cfg.sh_order
+        d.res[:] = list(cfg.resolution)
+        d.voxel_size = cfg.voxel_size
+        d.origin[:] = list(cfg.origin)
+        d.far_field_voxels = cfg.far_field_voxels
+        d.ncam = ncam
+        n = len(cameras)
+        cam_arr = (psdf_camera * n)(*cameras)
+        ms = [np.ascontiguousarray(m, np.uint8) for m in masks]
+        mp = (C.POINTER(C.c_uint8) * n)(*[m.ctypes.data_as(C.POINTER(C.c_uint8)) for m in ms])
+        self._check(self.L.psdf_init_visual_hull(self.h, C.byref(d), int(cfg.band_voxels), n, cam_arr, mp,
+                                                 None, None))
+        self.grid = HostGrid(cfg, np.zeros((0, 3)), np.zeros((0, 8)), np.zeros((0, 3)), np.zeros((0, 4096)),
+                             np.zeros(0), np.zeros(0), np.zeros(self.L.psdf_mlp_size(cfg.n_s, cfg.n_a, ncam)), ncam=ncam)
+        return self._refresh_grid()
+
     def raise_sh_order(self, order):
         """SparseGrid::raise_sh_order (grid.cpp:252-262) on the device."""
         self._check(self.L.psdf_raise_sh_order(self.h, int(order)))

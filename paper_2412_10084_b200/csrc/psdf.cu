@@ -1402,6 +1402,146 @@ int psdf_subdivide(psdf_ctx* c, double band_voxels, int32_t* out_T, int32_t* out
     });
 }
 
+// init_grid_visual_hull (grid.cpp:470-504) on the device: occupancy,
+// two squared EDTs, the seed SDF and the per-tile allocation decision are
+// kernels (psdf_lod.cuh); the tile / probe lists are built on the host in
+// init_common's order (tiles x-major, allocate_tile -> ensure_probe), then
+// uploaded with the reference's defaults (planes 0.5, probes 0, smoothed on
+// the device).  The MLP is zero until psdf_upload_mlp.
+int psdf_init_visual_hull(psdf_ctx* c, const psdf_grid_desc* cfg, int band_voxels, int n_cams,
+                          const psdf_camera* cams, const uint8_t* const* masks, int32_t* out_T, int32_t* out_P) {
+    return guarded([&] {
+        if (!c || !cfg) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
+        if (n_cams <= 0 || !cams || !masks) fail(PSDF_ERR_INVALID_ARGUMENT, "visual hull: need one mask per camera");
+        for (int a = 0; a < 3; ++a)
+            if (cfg->res[a] <= 0 || cfg->res[a] % TE)
+                fail(PSDF_ERR_INVALID_ARGUMENT, "grid resolution must be a multiple of 16");
+        for (int i = 0; i < n_cams; ++i) {
+            check_camera(cams[i]);
+            if (!masks[i]) fail(PSDF_ERR_INVALID_ARGUMENT, "visual hull: need one mask per camera");
+        }
+        set_device(c);
+        cudaStream_t s = c->stream;
+        const int3 res = make_int3(cfg->res[0], cfg->res[1], cfg->res[2]);
+        const int64_t nv = (int64_t)res.x * res.y * res.z;
+        const double h = cfg->voxel_size;
+        std::vector<void*> tmp;
+        auto dalloc = [&](size_t bytes) {
+            void* p = nullptr;
+            CK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+            tmp.push_back(p);
+            return p;
+        };
+        try {
+            // cameras and masks
+            std::vector<Cam> hc(n_cams);
+            std::vector<const uint8_t*> hm(n_cams);
+            for (int i = 0; i < n_cams; ++i) {
+                hc[i] = to_cam(cams[i]);
+                const size_t n = (size_t)cams[i].width * cams[i].height;
+                auto* dm = (uint8_t*)dalloc(n);
+                CK(cudaMemcpyAsync(dm, masks[i], n, cudaMemcpyHostToDevice, s));
+                hm[i] = dm;
+            }
+            auto* d_cams = (Cam*)dalloc(sizeof(Cam) * n_cams);
+            auto* d_masks = (const uint8_t**)dalloc(sizeof(uint8_t*) * n_cams);
+            CK(cudaMemcpyAsync(d_cams, hc.data(), sizeof(Cam) * n_cams, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(d_masks, hm.data(), sizeof(uint8_t*) * n_cams, cudaMemcpyHostToDevice, s));
+            // occupancy (grid.cpp:477-491)
+            auto* occ = (uint8_t*)dalloc(nv);
+            const unsigned gv = (unsigned)std::min<int64_t>((nv + 255) / 256, 64 * c->sm_count);
+            hull_occ_kernel<<<gv, 256, 0, s>>>(d_cams, d_masks, n_cams, res,
+                                               make_double3(cfg->origin[0], cfg->origin[1], cfg->origin[2]), h, occ);
+            CK(cudaGetLastError());
+            // squared EDTs to the occupied and to the free set (edt3d, grid.cpp:430-468)
+            const int maxn = std::max({res.x, res.y, res.z});
+            const int batch = 65536;
+            auto* fbuf = (double*)dalloc(sizeof(double) * (size_t)batch * maxn);
+            auto* vbuf = (int*)dalloc(sizeof(int) * (size_t)batch * maxn);
+            auto* zbuf = (double*)dalloc(sizeof(double) * (size_t)batch * (maxn + 1));
+            const int64_t syz = (int64_t)res.y * res.z;
+            const EdtLines passes[3] = {
+                {res.x * res.y, res.z, 1, syz, res.z, res.y},          // along z, lines (x, y)
+                {res.x * res.z, res.y, res.z, syz, 1, res.z},          // along y, lines (x, z)
+                {res.y * res.z, res.x, (int)syz, res.z, 1, res.z}};    // along x, lines (y, z)
+            double* dist[2];
+            for (int w = 0; w < 2; ++w) {
+                dist[w] = (double*)dalloc(sizeof(double) * nv);
+                edt_init_kernel<<<gv, 256, 0, s>>>(occ, nv, w == 0 ? 1 : 0, dist[w]);
+                CK(cudaGetLastError());
+                for (const EdtLines& L : passes)
+                    for (int l0 = 0; l0 < L.n_lines; l0 += batch) {
+                        edt_pass_kernel<<<(batch + 127) / 128, 128, 0, s>>>(dist[w], L, l0, batch, fbuf, vbuf, zbuf);
+                        CK(cudaGetLastError());
+                    }
+            }
+            // seed SDF + allocation decision per tile (init_common, grid.cpp:358-397)
+            const int nt[3] = {res.x / TE, res.y / TE, res.z / TE};
+            const int64_t ntt = (int64_t)nt[0] * nt[1] * nt[2];
+            auto* raw_all = (float*)dalloc(sizeof(float) * TV * ntt);
+            auto* keep_d = (uint8_t*)dalloc(ntt);
+            const double max_s = (double)maxn * h;
+            hull_tiles_kernel<<<(unsigned)ntt, 256, 0, s>>>(dist[0], dist[1], res, h, max_s, band_voxels * h, raw_all,
+                                                            keep_d);
+            CK(cudaGetLastError());
+            std::vector<uint8_t> keep(ntt);
+            CK(cudaMemcpyAsync(keep.data(), keep_d, ntt, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            std::vector<int32_t> tc, pid, pco;
+            std::vector<int> src;
+            std::unordered_map<int64_t, int> probe_of;
+            auto key = [&](int x, int y, int z) { return ((int64_t)x * (nt[1] + 1) + y) * (nt[2] + 1) + z; };
+            for (int64_t t = 0; t < ntt; ++t) {
+                if (!keep[t]) continue;
+                const int q[3] = {(int)(t / ((int64_t)nt[1] * nt[2])), (int)((t / nt[2]) % nt[1]), (int)(t % nt[2])};
+                tc.insert(tc.end(), q, q + 3);
+                src.push_back((int)t);
+                for (int i = 0; i < 8; ++i) {
+                    const int g[3] = {q[0] + (i & 1), q[1] + ((i >> 1) & 1), q[2] + ((i >> 2) & 1)};
+                    auto it = probe_of.find(key(g[0], g[1], g[2]));
+                    int id;
+                    if (it == probe_of.end()) {
+                        id = (int)(pco.size() / 3);
+                        probe_of.emplace(key(g[0], g[1], g[2]), id);
+                        pco.insert(pco.end(), g, g + 3);
+                    } else {
+                        id = it->second;
+                    }
+                    pid.push_back(id);
+                }
+            }
+            const int64_t T = (int64_t)src.size(), P = (int64_t)(pco.size() / 3);
+            std::vector<float> raw((size_t)T * TV);
+            if (T) {
+                auto* d_src = (int*)dalloc(sizeof(int) * T);
+                auto* d_raw = (float*)dalloc(sizeof(float) * TV * T);
+                CK(cudaMemcpyAsync(d_src, src.data(), sizeof(int) * T, cudaMemcpyHostToDevice, s));
+                subdiv_gather_raw_kernel<<<(unsigned)T, 256, 0, s>>>(raw_all, d_src, (int)T, d_raw);
+                CK(cudaGetLastError());
+                CK(cudaMemcpyAsync(raw.data(), d_raw, sizeof(float) * raw.size(), cudaMemcpyDeviceToHost, s));
+            }
+            CK(cudaStreamSynchronize(s));
+            for (void* p : tmp) cudaFree(p);
+            tmp.clear();
+            psdf_grid_desc d = *cfg;
+            d.T = (int)T;
+            d.P = (int)P;
+            std::vector<float> planes((size_t)T * 3 * 256 * d.n_s, 0.5f);  // allocate_tile (grid.cpp:66-69)
+            std::vector<float> probes((size_t)P * d.sh_order * d.sh_order * d.n_a, 0.f);  // ensure_probe
+            std::vector<float> mlp(psdf_mlp_size(d.n_s, d.n_a, d.ncam), 0.f);
+            if (psdf_upload_grid(c, &d, tc.data(), pid.data(), pco.data(), raw.data(), nullptr, planes.data(),
+                                 probes.data()) != PSDF_OK ||
+                psdf_upload_mlp(c, mlp.data(), (int64_t)mlp.size()) != PSDF_OK)
+                fail(PSDF_ERR_RUNTIME, "%s", g_err.c_str());
+            if (out_T) *out_T = (int32_t)T;
+            if (out_P) *out_P = (int32_t)P;
+        } catch (...) {
+            for (void* p : tmp) cudaFree(p);
+            throw;
+        }
+    });
+}
+
 int psdf_set_keep_raypass_grads(psdf_ctx* c, int keep) {
     return guarded([&] {
         need_grid(c);

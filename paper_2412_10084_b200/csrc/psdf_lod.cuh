@@ -158,3 +158,145 @@ __global__ void __launch_bounds__(128) subdiv_probes_kernel(const int32_t* __res
 }
 
 }  // namespace psdf
+
+namespace psdf {
+
+// ------------------------------------------------------------ visual hull
+// init_grid_visual_hull (grid.cpp:470-504) on the device:
+// occupancy by projection into every mask, two exact squared EDTs
+// (Felzenszwalb, grid.cpp:400-468), the seed SDF, and init_common's
+// allocation decision (grid.cpp:358-397) per tile.  f64 in the reference's
+// operation order throughout, so occupancy, distances and decisions are the
+// reference's bit for bit.
+
+// voxel (x, y, z) -> index (x * ry + y) * rz + z, as the reference's idx
+__global__ void __launch_bounds__(256) hull_occ_kernel(const Cam* __restrict__ cams,
+                                                       const uint8_t* const* __restrict__ masks, int n_cams,
+                                                       int3 res, double3 org, double h,
+                                                       uint8_t* __restrict__ occ) {
+    const int64_t n = (int64_t)res.x * res.y * res.z;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int z = (int)(i % res.z), y = (int)((i / res.z) % res.y), x = (int)(i / ((int64_t)res.y * res.z));
+        const double p[3] = {dadd(org.x, dmul((double)x + 0.5, h)), dadd(org.y, dmul((double)y + 0.5, h)),
+                             dadd(org.z, dmul((double)z + 0.5, h))};
+        uint8_t o = 1;
+        for (int c = 0; c < n_cams; ++c) {
+            const Cam& k = cams[c];
+            // Camera::project (camera.hpp:38-44): rotate_inv(p - pos)
+            const double d[3] = {dsub(p[0], k.pos[0]), dsub(p[1], k.pos[1]), dsub(p[2], k.pos[2])};
+            const double cx = dadd(dadd(dmul(k.rot[0], d[0]), dmul(k.rot[3], d[1])), dmul(k.rot[6], d[2]));
+            const double cy = dadd(dadd(dmul(k.rot[1], d[0]), dmul(k.rot[4], d[1])), dmul(k.rot[7], d[2]));
+            const double cz = dadd(dadd(dmul(k.rot[2], d[0]), dmul(k.rot[5], d[1])), dmul(k.rot[8], d[2]));
+            bool fg = false;
+            if (cz > 1e-9) {
+                const double u = dadd(ddiv(dmul(k.fx, cx), cz), k.cx);
+                const double v = dadd(ddiv(dmul(k.fy, cy), cz), k.cy);
+                const long lu = lround(u), lv = lround(v);  // MaskImage::foreground (grid.hpp:143-146)
+                fg = lu >= 0 && lv >= 0 && lu < k.width && lv < k.height &&
+                     __ldg(masks[c] + (size_t)lv * k.width + lu) > 127;
+            }
+            if (!fg) {
+                o = 0;
+                break;
+            }
+        }
+        occ[i] = o;
+    }
+}
+
+// One pass of edt3d (grid.cpp:430-468): dt1d along every line of `n` elements
+// at `stride` (line l starts at base(l)); one thread per line, the lower
+// envelope in per-line global scratch.
+struct EdtLines {
+    int n_lines, n, stride;
+    int64_t step_a, step_b;  // line l = (la, lb): base = la * step_a + lb * step_b
+    int n_b;
+};
+__global__ void __launch_bounds__(128) edt_pass_kernel(double* __restrict__ d, EdtLines L, int line0, int n_batch,
+                                                       double* __restrict__ fbuf, int* __restrict__ vbuf,
+                                                       double* __restrict__ zbuf) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_batch || line0 + t >= L.n_lines) return;
+    const int l = line0 + t;
+    double* line = d + (int64_t)(l / L.n_b) * L.step_a + (int64_t)(l % L.n_b) * L.step_b;
+    const int n = L.n;
+    double* f = fbuf + (int64_t)t * n;
+    int* v = vbuf + (int64_t)t * n;
+    double* z = zbuf + (int64_t)t * (n + 1);
+    for (int q = 0; q < n; ++q) f[q] = line[(int64_t)q * L.stride];
+    // Felzenszwalb 1D squared distance transform (grid.cpp:400-427)
+    int k = 0;
+    v[0] = 0;
+    z[0] = -INFINITY;
+    z[1] = INFINITY;
+    for (int q = 1; q < n; ++q) {
+        double s;
+        for (;;) {
+            const int vk = v[k];
+            s = ddiv(dsub(dadd(f[q], (double)(q * q)), dadd(f[vk], (double)(vk * vk))),
+                     dsub(dmul(2.0, (double)q), dmul(2.0, (double)vk)));
+            if (s <= z[k]) --k;
+            else break;
+        }
+        ++k;
+        v[k] = q;
+        z[k] = s;
+        z[k + 1] = INFINITY;
+    }
+    k = 0;
+    for (int q = 0; q < n; ++q) {
+        while (z[k + 1] < (double)q) ++k;
+        const int dq = q - v[k];
+        line[(int64_t)q * L.stride] = dadd(dmul((double)dq, (double)dq), f[v[k]]);
+    }
+}
+
+__global__ void __launch_bounds__(256) edt_init_kernel(const uint8_t* __restrict__ occ, int64_t n, int want,
+                                                       double* __restrict__ d) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        d[i] = (occ[i] != 0) == (want != 0) ? 0.0 : 1e18;  // edt3d: the `inside` set is at distance 0
+}
+
+// The seed SDF of every voxel of tile (tx, ty, tz) and init_common's
+// allocation decision (grid.cpp:376-393): raw in tile layout, keep flag.
+__global__ void __launch_bounds__(256) hull_tiles_kernel(const double* __restrict__ d_occ,
+                                                         const double* __restrict__ d_free, int3 res, double h,
+                                                         double max_s, double band, float* __restrict__ raw,
+                                                         uint8_t* __restrict__ keep) {
+    const int nty = res.y / TE, ntz = res.z / TE;
+    const int t = blockIdx.x;
+    const int tx = t / (nty * ntz), ty = (t / ntz) % nty, tz = t % ntz;
+    double mn = 1.79769313486231570e308;
+    int fl = 0;
+    for (int i = threadIdx.x; i < TV; i += blockDim.x) {
+        const int x = tx * TE + (i >> 8), y = ty * TE + ((i >> 4) & 15), z = tz * TE + (i & 15);
+        const int64_t j = ((int64_t)x * res.y + y) * res.z + z;
+        const double a = d_occ[j] < 1e12 ? d_occ[j] : 1e12, b = d_free[j] < 1e12 ? d_free[j] : 1e12;
+        double s = dmul(dsub(dsqrt(a), dsqrt(b)), h);
+        s = fmin(fmax(s, -max_s), max_s);  // clampd (vec.hpp:63)
+        raw[(int64_t)t * TV + i] = (float)s;
+        mn = fmin(mn, fabs(s));
+        fl |= s >= 0.0 ? 1 : 2;
+    }
+    __shared__ double s_mn[8];
+    __shared__ int s_fl[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        fl |= __shfl_xor_sync(0xffffffffu, fl, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_mn[threadIdx.x >> 5] = mn;
+        s_fl[threadIdx.x >> 5] = fl;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            mn = fmin(mn, s_mn[w]);
+            fl |= s_fl[w];
+        }
+        keep[t] = (mn > band && fl != 3) ? 0 : 1;
+    }
+}
+
+}  // namespace psdf

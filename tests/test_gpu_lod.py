@@ -114,3 +114,58 @@ def test_raise_sh_order(ctx):
         ctx.raise_sh_order(3)
     with pytest.raises(ValueError):
         s.raise_sh_order(3)
+
+
+def _sphere_masks(cams, radius):
+    """uint8 silhouettes (255 / 0) of a sphere at the origin, pixel-centre rays."""
+    out = []
+    for c in cams:
+        R = np.array(list(c.rot)).reshape(3, 3)
+        o = np.array(list(c.pos))
+        u, v = np.meshgrid(np.arange(c.width) + 0.5, np.arange(c.height) + 0.5)
+        d = np.stack([(u - c.cx) / c.fx, (v - c.cy) / c.fy, np.ones_like(u)], -1) @ R.T
+        d /= np.linalg.norm(d, axis=-1, keepdims=True)
+        b = d @ o
+        disc = b * b - (o @ o - radius * radius)
+        out.append(np.where((disc >= 0) & (-b > 0), 255, 0).astype(np.uint8))
+    return out
+
+
+@pytest.mark.parametrize("res,band", [(32, 4), (64, 6)])
+def test_visual_hull_parity(ctx, res, band):
+    """init_grid_visual_hull on the device vs the reference's own (occupancy,
+    EDTs, seed SDF, allocation and order bit-exact; raw stored as fp32)."""
+    from paper_2412_10084_b200 import api
+    from oracle.refcore import RefCamera, RefScene
+    cams = api.make_ring_cameras(8, 48)
+    masks = _sphere_masks(cams, 0.3)
+    rcams = []
+    for c in cams:
+        rc = RefCamera()
+        for k in ("fx", "fy", "cx", "cy", "width", "height", "id"):
+            setattr(rc, k, getattr(c, k))
+        rc.rot[:] = list(c.rot)
+        rc.pos[:] = list(c.pos)
+        rcams.append(rc)
+    cfg = api.GridConfig(voxel_size=1.0 / res, resolution=(res, res, res), n_s=2, n_a=2, sh_order=2,
+                         band_voxels=band)
+    ng = ctx.init_visual_hull(cfg, cams, masks)
+    b = RefScene.hull(rcams, masks, res=res, n_s=2, n_a=2, sh_order=2, band_voxels=band).export()
+    assert ng.T == b.T and ng.P == b.P and ng.T > 0, (ng.T, b.T, ng.P, b.P)
+    assert np.array_equal(ng.tile_coords, b.tile_coords)
+    assert np.array_equal(ng.probe_ids, b.probe_ids)
+    assert np.array_equal(ng.probe_coords, b.probe_coords)
+    _close_f32(ng.raw, b.raw, "raw")
+    _close_f32(ng.planes, b.planes, "planes")
+    _close_f32(ng.probes, b.probes, "probes")
+    assert np.abs(ng.smooth - b.smooth).max() <= 1e-5
+
+
+def test_visual_hull_errors(ctx):
+    from paper_2412_10084_b200 import api, _lib
+    cfg = api.GridConfig(voxel_size=1.0 / 24, resolution=(24, 24, 24), n_s=2, n_a=2, sh_order=2)
+    cams = api.make_ring_cameras(2, 16)
+    with pytest.raises(_lib.PsdfInvalidArgument):
+        ctx.init_visual_hull(cfg, cams, _sphere_masks(cams, 0.3))
+    with pytest.raises(_lib.PsdfInvalidArgument):
+        ctx.init_visual_hull(api.GridConfig(voxel_size=1 / 32, resolution=(32, 32, 32)), [], [])
