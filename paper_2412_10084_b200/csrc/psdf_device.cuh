@@ -340,9 +340,9 @@ __device__ unsigned long long g_cont_hist[2][16];  // K2a rays by log2(steps), p
 // reference step).
 __device__ __forceinline__ double lattice_advance(double t, double m, double h) {
     for (;;) {
-        int e;
-        frexp(t, &e);
-        const double p2 = ldexp(1.0, e);                // next power of two above t
+        // next power of two above t (t > 0, normal): exponent field + 1, mantissa 0
+        const double p2 = __longlong_as_double((__double_as_longlong(t) & 0x7FF0000000000000LL) +
+                                               0x0010000000000000LL);
         if (t + m * h < 2.0 * p2) return dadd(t, dmul(m, h));
         const double m1 = ceil((p2 - t) / h);          // any m1 >= 1 landing in [p2, 2 p2)
         t = dadd(t, dmul(m1, h));
