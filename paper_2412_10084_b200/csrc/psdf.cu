@@ -796,6 +796,17 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
         const int t0 = (int)((int64_t)T * c->rank / c->world), t1 = (int)((int64_t)T * (c->rank + 1) / c->world);
         const int p0 = (int)((int64_t)Pn * c->rank / c->world), p1 = (int)((int64_t)Pn * (c->rank + 1) / c->world);
         const int stride = c->desc.sh_order * c->desc.sh_order * c->desc.n_a;
+        // with `overlap`, the eikonal / normal / sdf kernel (the one that
+        // touches only raw gradients and, atomically, the staged SDF
+        // gradient) and the empty rays' photo terms run on the low-priority
+        // side stream under the ray pass, filling the SMs its kernels' tails
+        // leave idle (ev_fork: recorded by the ray pass after its first
+        // composite round)
+        cudaStream_t sl = s;
+        if (overlap) {
+            CK(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+            sl = c->side_stream;
+        }
         if (t1 > t0) {
             static bool attr = false;
             if (!attr) {
@@ -803,23 +814,10 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
                                         (int)kLossGridSmem));
                 attr = true;
             }
-            // with `overlap`, the eikonal / normal / sdf kernel (the one that
-            // touches only raw gradients and, atomically, the staged SDF
-            // gradient) runs on the low-priority side stream under the ray
-            // pass, filling the SMs its kernels' tails leave idle
-            cudaStream_t sl = s;
-            if (overlap) {  // ev_fork: recorded by the ray pass after its first composite round
-                CK(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
-                sl = c->side_stream;
-            }
             loss_grid_kernel<<<t1 - t0, LG_THREADS, kLossGridSmem, sl>>>(
                 g, c->d_params + c->off_raw, t0, (float)hp->l_sdf, (float)hp->l_eik, (float)hp->l_norm,
                 (float)(1.0 / (2.0 * c->desc.voxel_size)), c->d_gsmooth, c->d_grads + c->off_raw, c->d_stats);
             CK(cudaGetLastError());
-            if (overlap) {  // the empty rays' photo terms also run on the side stream
-                launch_empty_ray_loss(c, P, c->side_stream);
-                CK(cudaEventRecord(c->ev_join, c->side_stream));
-            }
             dispatch_ns(c->desc.n_s, [&]<int NS>() {
                 loss_features_kernel<NS><<<3 * (t1 - t0), 256, 0, s>>>(g, t0, (float)hp->l_feat,
                                                                        c->d_grads + c->off_planes, c->d_stats);
@@ -835,6 +833,8 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
             CK(cudaGetLastError());
             ++c->last_launches;
         }
+        launch_empty_ray_loss(c, P, sl);
+        if (overlap) CK(cudaEventRecord(c->ev_join, c->side_stream));
     };
     const bool overlap = !c->keep_raypass;
     // images still arriving (psdf_train_step): the regularizer runs under the
@@ -869,7 +869,6 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
     c->fork_regs = false;
     regularizers(overlap);
     if (overlap) CK(cudaStreamWaitEvent(s, c->ev_join, 0));
-    else launch_empty_ray_loss(c, P, s);
     // G^T fold (grads.cpp:67-96): raw_grad += G^T * staged
     launch_fold(c, c->d_gsmooth, c->d_grads + c->off_raw);
     // all-reduce across ranks (GradBuffers::add, trainer.cpp:184-185, across GPUs)
