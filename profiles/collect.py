@@ -19,7 +19,11 @@ COLS = {
     "issue_active_pct": ("smsp__issue_active.avg.pct_of_peak_sustained_active", 1.0),
     "threads_per_inst": ("smsp__thread_inst_executed_per_inst_executed.ratio", 1.0),
     "regs": ("launch__registers_per_thread", 1.0),
+    "dram_gbs": ("dram__bytes.sum.per_second", 1.0),
+    "l2_hit_pct": ("lts__t_sector_hit_rate.pct", 1.0),
+    "l1_hit_pct": ("l1tex__t_sector_hit_rate.pct", 1.0),
 }
+RATE_SCALE = {"Tbyte/s": 1e3, "Gbyte/s": 1.0, "Mbyte/s": 1e-3, "byte/s": 1e-9, "Kbyte/s": 1e-6}
 UNIT_SCALE = {"ms": 1e3, "us": 1.0, "usecond": 1.0, "msecond": 1e3, "nsecond": 1e-3, "ns": 1e-3,
               "Gbyte": 1e3, "Mbyte": 1.0, "Kbyte": 1e-3, "byte": 1e-6}
 
@@ -38,6 +42,8 @@ def main(path, out):
             u = units[i]
             if k == "time_us":
                 v *= UNIT_SCALE.get(u, 1.0)
+            elif k == "dram_gbs":
+                v *= RATE_SCALE.get(u, 1.0)
             elif k.startswith("dram"):
                 v *= UNIT_SCALE.get(u, 1.0)
             r[k] = v
@@ -51,11 +57,15 @@ def main(path, out):
                        "--clock-control none, cold caches per replay"},
               open(out + "_k2_traffic.json", "w"), indent=1)
     with open(out + "_summary.md", "w") as f:
-        f.write("| kernel | time (us, serialised) | DRAM read MB | DRAM write MB | warps active % | "
-                "issue active % | threads/inst | regs |\n|---|---|---|---|---|---|---|---|\n")
+        f.write("| kernel | time (us, serialised) | DRAM read MB | DRAM write MB | DRAM GB/s (% of 6455) | "
+                "L2 hit % | L1 hit % | warps active % | issue active % | threads/inst | regs |\n"
+                "|---|---|---|---|---|---|---|---|---|---|---|\n")
         for r in res:
+            g = r.get('dram_gbs', 0)
             f.write(f"| {r['kernel'][:60]} | {r['time_us']:.1f} | {r.get('dram_read_MB', 0):.1f} | "
-                    f"{r.get('dram_write_MB', 0):.1f} | {r.get('warps_active_pct', 0):.1f} | "
+                    f"{r.get('dram_write_MB', 0):.1f} | {g:.0f} ({100 * g / 6455.3:.0f} %) | "
+                    f"{r.get('l2_hit_pct', 0):.1f} | {r.get('l1_hit_pct', 0):.1f} | "
+                    f"{r.get('warps_active_pct', 0):.1f} | "
                     f"{r.get('issue_active_pct', 0):.1f} | {r.get('threads_per_inst', 0):.1f} | "
                     f"{r.get('regs', 0):.0f} |\n")
         f.write(f"\nK2 (ray pass) DRAM traffic per step: {k2_bytes / 1e6:.1f} MB; "
