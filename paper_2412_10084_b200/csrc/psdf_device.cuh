@@ -390,6 +390,7 @@ struct Marcher {
     int count, n_max;
     double vo[3], vd[3];  // (o - org)/h, d/h
     double dinv_max;      // 1 / max_a |d_a|: lattice steps per voxel of L-inf travel
+    double rinv_max;      // max_a |1 / d_a| (error scale of the skip counts)
     double t_sync;        // < 0: synchronised with the reference; else its last t
     bool no_jump;         // replaying after a rewind
     unsigned n_exact;     // exact-path fallbacks taken (diagnostics)
@@ -409,6 +410,7 @@ struct Marcher {
             dm = fmax(dm, fabs(d[a]));
         }
         dinv_max = dm > 0.0 ? 1.0 / dm : 0.0;
+        rinv_max = fmax(fmax(fabs(inv_d[0]), fabs(inv_d[1])), fabs(inv_d[2]));
         t_sync = -1.0;
         no_jump = false;
         c_b = c_blk = -1;
@@ -493,15 +495,14 @@ struct Marcher {
     __device__ __forceinline__ double run_length(const GridView& g, const double v[3], double t,
                                                  double h) const {
         if (!g.h_pow2 || t < 64.0 * h) return 1.0;
-        double q = 1e300, rmax = 0.0;
+        double q = 1e300;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             if (inv_d[a] == 0.0) continue;
             const double B = 16.0 * (floor(v[a] * 0.0625) + (d[a] > 0.0 ? 1.0 : 0.0));
             q = fmin(q, (B - v[a]) * inv_d[a]);
-            rmax = fmax(rmax, fabs(inv_d[a]));
         }
-        const double mq = g.margin + 1e-11 * rmax;
+        const double mq = g.margin + 1e-11 * rinv_max;
         const double fq = q - floor(q);
         if (!(q < 1e300) || fq <= mq || fq >= 1.0 - mq) return 1.0;
         // the reference's own loop test t_j < t1, t_j = t + j h exactly
@@ -590,16 +591,19 @@ struct Marcher {
                         // L-inf (Ds - 1) + (distance to the cell faces)
                         // voxels, up to the tile exit, lies in a saturated
                         // cell
+                        // (the distance to the cell faces only shortens the
+                        // run: fp32 with a 1e-5 voxel allowance)
                         int ci = 0;
                         bool ok = true;
-                        double edge = 1.0;
+                        float edge = 1.f;
 #pragma unroll
                         for (int a = 0; a < 3; ++a) {
                             const double cc = r[a] - 0.5;
                             const double fb = floor(cc);
                             const double f = cc - fb;
                             ok &= f > kMargin && f < 1.0 - kMargin;
-                            edge = fmin(edge, fmin(f, 1.0 - f));
+                            const float ff = (float)f;
+                            edge = fminf(edge, fminf(ff, 1.f - ff));
                             ci = ci * kCellE + ((int)fb + 1);
                         }
                         int ds = 0;
@@ -614,7 +618,8 @@ struct Marcher {
                         if (ds > 0) {
                             run.sat = true;
                             double n = run_length(g, v, t, h);  // lattice points left in the tile
-                            if (ds != kCellNone) n = fmin(n, floor(((double)(ds - 1) + edge - 1e-6) * dinv_max) + 1.0);
+                            if (ds != kCellNone)
+                                n = fmin(n, floor(((double)(ds - 1) + (double)edge - 1e-5) * dinv_max) + 1.0);
                             if (n > 1.0) {
                                 const int ni = (int)fmin(n, (double)(n_max - count));
                                 run.n = ni;
@@ -642,10 +647,13 @@ struct Marcher {
             if (in_grid && !near && !no_jump && g.h_pow2 && t >= 64.0 * h) {
                 const int D = __ldg(g.tile_dist + b);
                 if (D >= 2) {
-                    double edge = 16.0;
+                    float edge = 16.f;  // fp32 with a 1e-5 voxel allowance (it only shortens the jump)
 #pragma unroll
-                    for (int a = 0; a < 3; ++a) edge = fmin(edge, fmin(r[a], 16.0 - r[a]));
-                    const double m = floor((16.0 * (D - 1) + edge - 1e-6) * dinv_max);
+                    for (int a = 0; a < 3; ++a) {
+                        const float rf = (float)r[a];
+                        edge = fminf(edge, fminf(rf, 16.f - rf));
+                    }
+                    const double m = floor((16.0 * (D - 1) + (double)edge - 1e-5) * dinv_max);
                     if (m >= 2.0) {
                         PSDF_STAT(4);
                         if (t_sync < 0.0) t_sync = t;
@@ -657,16 +665,15 @@ struct Marcher {
             // --- skip the empty tile.  p(t) is inside the tile and off its
             // faces (not `near`), so the box test passes and e1 > t; the skip
             // is ceil(q + 1e-9) with q = (e1 - t)/h = min_a (B_a - v_a) / d_a.
-            double q = 1e300, rmax = 0.0;
+            double q = 1e300;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 if (inv_d[a] == 0.0) continue;
                 const double B = 16.0 * (double)(tc[a] + (d[a] > 0.0 ? 1 : 0));
                 q = fmin(q, (B - v[a]) * inv_d[a]);
-                rmax = fmax(rmax, fabs(inv_d[a]));
             }
             const double fq = q - floor(q);
-            const double mq = kMargin + 1e-11 * rmax;  // q error <~ 1e-12 |1/d|
+            const double mq = kMargin + 1e-11 * rinv_max;  // q error <~ 1e-12 |1/d|
             if (!near && q < 1e300 && fq > mq && fq < 1.0 - mq) {
                 const double k = ceil(q);  // the + 1e-9 is inside the margin
                 t = dadd(t, dmul(k > 1.0 ? k : 1.0, h));
