@@ -340,13 +340,52 @@ void check_camera(const psdf_camera& c) {
 }
 
 // Copies the batch's view table to the device and returns the work-tile count.
+// The pixel rectangle of a view whose rays can reach the allocated tiles'
+// bounding box (Camera::project of its eight corners, padded by 2 pixels);
+// the whole image unless every corner is well in front of the camera.
+void occ_rect(const GridView& g, ViewDev& v) {
+    const Cam& k = v.cam;
+    v.occ_u0 = 0;
+    v.occ_u1 = k.width - 1;
+    v.occ_v0 = 0;
+    v.occ_v1 = k.height - 1;
+    if (!g.occ_any) {  // nothing allocated: no ray has a sample
+        v.occ_u0 = v.occ_v0 = 1;
+        v.occ_u1 = v.occ_v1 = 0;
+        return;
+    }
+    double umin = 1e300, umax = -1e300, vmin = 1e300, vmax = -1e300;
+    for (int i = 0; i < 8; ++i) {
+        const double p[3] = {(i & 1) ? g.occ_hi[0] : g.occ_lo[0], (i & 2) ? g.occ_hi[1] : g.occ_lo[1],
+                             (i & 4) ? g.occ_hi[2] : g.occ_lo[2]};
+        const double d[3] = {p[0] - k.pos[0], p[1] - k.pos[1], p[2] - k.pos[2]};
+        const double cx = k.rot[0] * d[0] + k.rot[3] * d[1] + k.rot[6] * d[2];
+        const double cy = k.rot[1] * d[0] + k.rot[4] * d[1] + k.rot[7] * d[2];
+        const double cz = k.rot[2] * d[0] + k.rot[5] * d[1] + k.rot[8] * d[2];
+        if (!(cz > 1e-3)) return;  // a corner beside / behind the camera: no culling
+        const double u = k.fx * cx / cz + k.cx, w = k.fy * cy / cz + k.cy;
+        umin = std::min(umin, u);
+        umax = std::max(umax, u);
+        vmin = std::min(vmin, w);
+        vmax = std::max(vmax, w);
+    }
+    // pixel u's ray passes through the image point u + 1/2
+    auto clampi = [](double x, int lo, int hi) { return (int)std::max<double>(lo, std::min<double>(hi, x)); };
+    v.occ_u0 = clampi(std::floor(umin) - 2.0, 0, k.width);
+    v.occ_u1 = clampi(std::ceil(umax) + 2.0, -1, k.width - 1);
+    v.occ_v0 = clampi(std::floor(vmin) - 2.0, 0, k.height);
+    v.occ_v1 = clampi(std::ceil(vmax) + 2.0, -1, k.height - 1);
+}
+
 int64_t upload_viewdev(psdf_ctx* c, std::vector<ViewDev>& vd) {
     int64_t tiles = 0;
+    const GridView g = c->view();
     for (auto& v : vd) {
         v.tiles_x = (v.cam.width + 7) / 8;
         v.tiles_y = (v.cam.height + 3) / 4;
         v.tile_begin = tiles;
         tiles += (int64_t)v.tiles_x * v.tiles_y;
+        occ_rect(g, v);
     }
     if ((int)vd.size() > c->viewdev_cap) {
         if (c->d_viewdev) cudaFree(c->d_viewdev);

@@ -38,6 +38,10 @@ struct ViewDev {
     int64_t tile_begin;   // first global work tile of this view
     int cam_bias_row;     // camera-bias row for this view, -1 = none
     int pad_;
+    // pixels whose ray can meet the allocated tiles' bounding box: the box's
+    // projection, padded by 2 pixels (the whole image when the camera is not
+    // in front of every box corner); rays outside yield no sample
+    int occ_u0, occ_u1, occ_v0, occ_v1;
 };
 
 struct RayPassParams {

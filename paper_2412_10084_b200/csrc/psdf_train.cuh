@@ -192,7 +192,8 @@ __global__ void __launch_bounds__(BLOCK, PSDF_SCAN_MINB) march_scan_kernel(RayPa
         int k = 0, tile_prev = -1;
         double t_prev = 0.0, h_t = 0.0;
         bool hand = false;
-        if (R.valid) {
+        const ViewDev& V = *R.V;
+        if (R.valid && R.u >= V.occ_u0 && R.u <= V.occ_u1 && R.v >= V.occ_v0 && R.v <= V.occ_v1) {
             const D3 dir = pixel_dir(R.V->cam, (double)R.u + 0.5, (double)R.v + 0.5);
             const double dd[3] = {dir.x, dir.y, dir.z};
             if (mr.init(g, R.V->cam.pos, dd, P.n_max) && mr.enter_occupied(g)) {
