@@ -159,6 +159,18 @@ int psdf_raise_sh_order(psdf_ctx* ctx, int new_order);
 int psdf_init_visual_hull(psdf_ctx* ctx, const psdf_grid_desc* desc, int band_voxels, int n_cams,
                           const psdf_camera* cams, const uint8_t* const* masks, int32_t* out_T, int32_t* out_P);
 
+/* ---- SDFC v1 checkpoints -------------------------------
+ * Replace save_checkpoint / load_checkpoint (checkpoint.cpp:54-181): the same
+ * file layout (little-endian f32 tensors, tile / probe order, decoder, LOD
+ * cursor), read into / written from the device grid; the grid description has
+ * no lod / band_voxels, so they travel as arguments.  Errors are
+ * PSDF_ERR_RUNTIME (std::runtime_error) with the reference's messages.  A
+ * load re-smooths on the device and resets the optimizer. */
+int psdf_save_checkpoint(psdf_ctx* ctx, const char* path, int32_t lod, int32_t band_voxels, int32_t lod_cursor,
+                         int64_t iteration, uint64_t seed);
+int psdf_load_checkpoint(psdf_ctx* ctx, const char* path, int32_t* lod, int32_t* band_voxels, int32_t* lod_cursor,
+                         int64_t* iteration, uint64_t* seed);
+
 /* Keep a copy of the stage-0 (post ray pass) gradients on every step. */
 int psdf_set_keep_raypass_grads(psdf_ctx* ctx, int keep);
 int psdf_download_grads(psdf_ctx* ctx, int stage, float* raw, float* smooth, float* planes,

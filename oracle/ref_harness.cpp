@@ -426,6 +426,38 @@ void ref_scene_import(RefScene* s, const double* raw, const double* smooth, cons
 
 void ref_smooth_all(RefScene* s) { s->grid.smooth_all(); }
 
+// SDFC checkpoints through the reference's own save / load (checkpoint.cpp).
+int ref_save_checkpoint(const RefScene* s, const char* path, int lod_cursor, int64_t iteration, uint64_t seed) {
+    try {
+        Checkpoint ck;
+        ck.grid = s->grid;
+        ck.mlp = s->mlp;
+        ck.lod_cursor = lod_cursor;
+        ck.iteration = iteration;
+        ck.seed = seed;
+        save_checkpoint(path, ck);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+RefScene* ref_load_checkpoint(const char* path, int64_t* cursor_iter_seed) {
+    try {
+        Checkpoint ck = load_checkpoint(path);
+        auto* s = new RefScene;
+        s->grid = ck.grid;
+        s->mlp = ck.mlp;
+        cursor_iter_seed[0] = ck.lod_cursor;
+        cursor_iter_seed[1] = ck.iteration;
+        cursor_iter_seed[2] = (int64_t)ck.seed;
+        return s;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
 // LOD transitions through the reference's own members (grid.cpp:252-345).
 int ref_subdivide(RefScene* s) {
     try {

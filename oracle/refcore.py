@@ -106,6 +106,9 @@ def reflib():
                                      _dp, _dp, C.c_int, C.c_uint64]
     L.ref_scene_free.argtypes = [C.c_void_p]
     L.ref_subdivide.argtypes = [C.c_void_p]
+    L.ref_save_checkpoint.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_int64, C.c_uint64]
+    L.ref_load_checkpoint.restype = C.c_void_p
+    L.ref_load_checkpoint.argtypes = [C.c_char_p, C.c_void_p]
     L.ref_scene_hull.restype = C.c_void_p
     L.ref_scene_hull.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int,
                                  C.c_int, C.c_int, C.c_double, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
@@ -257,6 +260,20 @@ class RefScene:
                                 ptr(a.probes))
         self.L.ref_mlp_export(self.h, ptr(a.mlp))
         return a
+
+    def save_checkpoint(self, path, lod_cursor=0, iteration=0, seed=0):
+        """save_checkpoint (checkpoint.cpp:54-104), the reference's own writer."""
+        _check(self.L.ref_save_checkpoint(self.h, str(path).encode(), lod_cursor, iteration, seed), self.L)
+
+    @classmethod
+    def load_checkpoint(cls, path):
+        """load_checkpoint (checkpoint.cpp:106-181); returns (scene, (lod_cursor, iteration, seed))."""
+        L = reflib()
+        out = (C.c_int64 * 3)()
+        h = L.ref_load_checkpoint(str(path).encode(), out)
+        if not h:
+            raise RuntimeError(L.ref_last_error().decode())
+        return cls(h), (int(out[0]), int(out[1]), int(out[2]) & 0xFFFFFFFFFFFFFFFF)
 
     def subdivide(self):
         """grid = grid.subdivide() (grid.cpp:271-345), the reference's own member."""

@@ -83,7 +83,8 @@ EXPORTS = [
     "psdf_comm_unique_id", "psdf_comm_init", "psdf_last_timing", "psdf_stream",
     "psdf_host_alloc", "psdf_host_free", "psdf_march_rays", "psdf_pixel_dirs",
     "psdf_last_k2_breakdown", "psdf_grid_info", "psdf_download_structure", "psdf_subdivide",
-    "psdf_raise_sh_order", "psdf_last_h2d_bytes", "psdf_init_visual_hull",
+    "psdf_raise_sh_order", "psdf_last_h2d_bytes", "psdf_init_visual_hull", "psdf_save_checkpoint",
+    "psdf_load_checkpoint",
 ]
 
 _lib = None
@@ -143,6 +144,9 @@ def load():
     L.psdf_subdivide.argtypes = [vp, C.c_double, _ip, _ip]
     L.psdf_raise_sh_order.argtypes = [vp, C.c_int]
     L.psdf_last_h2d_bytes.restype = C.c_int64
+    L.psdf_save_checkpoint.argtypes = [vp, C.c_char_p, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_uint64]
+    L.psdf_load_checkpoint.argtypes = [vp, C.c_char_p, _ip, _ip, _ip, C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_uint64)]
     L.psdf_init_visual_hull.argtypes = [vp, C.POINTER(psdf_grid_desc), C.c_int, C.c_int, C.POINTER(psdf_camera),
                                         C.POINTER(C.POINTER(C.c_uint8)), _ip, _ip]
     L.psdf_last_h2d_bytes.argtypes = [vp]

@@ -418,6 +418,31 @@ class Context:
         self._check(self.L.psdf_subdivide(self.h, float(bv), None, None))
         return self._refresh_grid()
 
+    def save_checkpoint(self, path, lod=0, lod_cursor=0, iteration=0, seed=0):
+        """save_checkpoint (checkpoint.cpp:54-104) of the device grid + decoder."""
+        self._check(self.L.psdf_save_checkpoint(self.h, str(path).encode(), int(lod),
+                                                int(self.grid.cfg.band_voxels), int(lod_cursor),
+                                                int(iteration), int(seed)))
+
+    def load_checkpoint(self, path):
+        """load_checkpoint (checkpoint.cpp:106-181) into the device; returns
+        (HostGrid, dict(lod, band_voxels, lod_cursor, iteration, seed))."""
+        lod, band, cur = C.c_int32(), C.c_int32(), C.c_int32()
+        it, sd = C.c_int64(), C.c_uint64()
+        self._check(self.L.psdf_load_checkpoint(self.h, str(path).encode(), C.byref(lod), C.byref(band),
+                                                C.byref(cur), C.byref(it), C.byref(sd)))
+        d = psdf_grid_desc()
+        self._check(self.L.psdf_grid_info(self.h, C.byref(d)))
+        cfg = GridConfig(voxel_size=d.voxel_size, origin=tuple(d.origin), resolution=tuple(d.res), n_s=d.n_s,
+                         n_a=d.n_a, sh_order=d.sh_order, far_field_voxels=d.far_field_voxels,
+                         band_voxels=band.value)
+        self.grid = HostGrid(cfg, np.zeros((0, 3)), np.zeros((0, 8)), np.zeros((0, 3)), np.zeros((0, 4096)),
+                             np.zeros(0), np.zeros(0), np.zeros(self.L.psdf_mlp_size(d.n_s, d.n_a, d.ncam)),
+                             ncam=d.ncam)
+        g = self._refresh_grid()
+        return g, dict(lod=lod.value, band_voxels=band.value, lod_cursor=cur.value, iteration=it.value,
+                       seed=sd.value)
+
     def init_visual_hull(self, cfg: GridConfig, cameras, masks, ncam=0):
         """init_grid_visual_hull (grid.cpp:470-504) on the device; masks are uint8
         images (> 127 = foreground).  Returns the new HostGrid (MLP zero)."""

@@ -1580,6 +1580,206 @@ int psdf_init_visual_hull(psdf_ctx* c, const psdf_grid_desc* cfg, int band_voxel
     });
 }
 
+// ---- SDFC v1 checkpoints (checkpoint.cpp:12-181) -----
+// The on-disk tensors are little-endian f32, the device's own storage type,
+// so a load is one parse + upload and a save one download + write;
+// save(load(file)) reproduces the reference's bytes.
+}  // extern "C"
+namespace {
+constexpr char kSdfcMagic[4] = {'S', 'D', 'F', 'C'};
+constexpr uint32_t kSdfcVersion = 1;
+
+struct SdfcWriter {
+    FILE* f;
+    const char* path;
+    template <typename T> void pod(const T& v) {
+        if (fwrite(&v, sizeof(T), 1, f) != 1) fail(PSDF_ERR_RUNTIME, "checkpoint: failed while writing: %s", path);
+    }
+    void tensor(const float* v, uint64_t n) {
+        pod(n);
+        if (n && fwrite(v, sizeof(float), n, f) != n) fail(PSDF_ERR_RUNTIME, "checkpoint: failed while writing: %s", path);
+    }
+};
+struct SdfcReader {
+    FILE* f;
+    const char* path;
+    template <typename T> void pod(T& v) {
+        if (fread(&v, sizeof(T), 1, f) != 1) fail(PSDF_ERR_RUNTIME, "checkpoint: truncated file: %s", path);
+    }
+    void tensor(float* out, uint64_t expected) {
+        uint64_t n = 0;
+        pod(n);
+        if (n != expected) fail(PSDF_ERR_RUNTIME, "checkpoint: tensor size mismatch in %s", path);
+        if (n && fread(out, sizeof(float), n, f) != n) fail(PSDF_ERR_RUNTIME, "checkpoint: truncated file: %s", path);
+    }
+};
+struct FileCloser {
+    FILE* f;
+    ~FileCloser() {
+        if (f) fclose(f);
+    }
+};
+}  // namespace
+extern "C" {
+
+int psdf_save_checkpoint(psdf_ctx* c, const char* path, int32_t lod, int32_t band_voxels, int32_t lod_cursor,
+                         int64_t iteration, uint64_t seed) {
+    return guarded([&] {
+        need_grid(c);
+        if (!path) fail(PSDF_ERR_INVALID_ARGUMENT, "null path");
+        const psdf_grid_desc d = c->desc;
+        const int64_t T = d.T, P = d.P;
+        const int64_t ps = 256 * d.n_s, pc = (int64_t)d.sh_order * d.sh_order * d.n_a;
+        std::vector<int32_t> tc(3 * std::max<int64_t>(T, 1)), pco(3 * std::max<int64_t>(P, 1));
+        std::vector<float> raw(T * TV), planes(T * 3 * ps), probes(P * pc), mlp(c->mlp_size);
+        if (psdf_download_structure(c, tc.data(), nullptr, pco.data()) != PSDF_OK ||
+            psdf_download_params(c, raw.data(), nullptr, planes.data(), probes.data(), mlp.data()) != PSDF_OK)
+            fail(PSDF_ERR_RUNTIME, "%s", g_err.c_str());
+        FileCloser fc{fopen(path, "wb")};
+        if (!fc.f) fail(PSDF_ERR_RUNTIME, "checkpoint: cannot open for writing: %s", path);
+        SdfcWriter w{fc.f, path};
+        if (fwrite(kSdfcMagic, 1, 4, fc.f) != 4) fail(PSDF_ERR_RUNTIME, "checkpoint: failed while writing: %s", path);
+        w.pod(kSdfcVersion);
+        w.pod(d.voxel_size);
+        for (int a = 0; a < 3; ++a) w.pod(d.origin[a]);
+        w.pod(d.far_field_voxels);
+        const int32_t ints[8] = {d.res[0], d.res[1], d.res[2], d.n_s, d.n_a, d.sh_order, lod, band_voxels};
+        w.pod(ints);
+        w.pod((uint32_t)T);
+        for (int64_t t = 0; t < T; ++t) {
+            const int32_t q[3] = {tc[3 * t], tc[3 * t + 1], tc[3 * t + 2]};
+            w.pod(q);
+        }
+        for (int64_t t = 0; t < T; ++t) {
+            w.tensor(raw.data() + t * TV, TV);
+            for (int q = 0; q < 3; ++q) w.tensor(planes.data() + (t * 3 + q) * ps, ps);
+        }
+        w.pod((uint32_t)P);
+        for (int64_t p = 0; p < P; ++p) {
+            const int32_t q[3] = {pco[3 * p], pco[3 * p + 1], pco[3 * p + 2]};
+            w.pod(q);
+            w.tensor(probes.data() + p * pc, pc);
+        }
+        const MlpLayout G = MlpLayout::make(d.n_s + d.n_a + NPOW);
+        const int32_t mints[3] = {d.n_s, d.n_a, d.ncam};
+        w.pod(mints);
+        w.tensor(mlp.data() + G.w1, G.b1 - G.w1);
+        w.tensor(mlp.data() + G.b1, HID);
+        w.tensor(mlp.data() + G.w2, HID * HID);
+        w.tensor(mlp.data() + G.b2, HID);
+        w.tensor(mlp.data() + G.w3, 3 * HID);
+        w.tensor(mlp.data() + G.b3, 3);
+        w.tensor(mlp.data() + G.cam, (uint64_t)d.ncam * HID);
+        w.pod(lod_cursor);
+        w.pod(iteration);
+        w.pod(seed);
+    });
+}
+
+int psdf_load_checkpoint(psdf_ctx* c, const char* path, int32_t* lod, int32_t* band_voxels, int32_t* lod_cursor,
+                         int64_t* iteration, uint64_t* seed) {
+    return guarded([&] {
+        if (!c || !path) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
+        FileCloser fc{fopen(path, "rb")};
+        if (!fc.f) fail(PSDF_ERR_RUNTIME, "checkpoint: cannot open: %s", path);
+        SdfcReader r{fc.f, path};
+        char magic[4];
+        if (fread(magic, 1, 4, fc.f) != 4 || std::memcmp(magic, kSdfcMagic, 4) != 0)
+            fail(PSDF_ERR_RUNTIME, "checkpoint: bad magic in %s", path);
+        uint32_t version = 0;
+        r.pod(version);
+        if (version != kSdfcVersion) fail(PSDF_ERR_RUNTIME, "checkpoint: unsupported version %u in %s", version, path);
+        psdf_grid_desc d{};
+        r.pod(d.voxel_size);
+        for (int a = 0; a < 3; ++a) r.pod(d.origin[a]);
+        r.pod(d.far_field_voxels);
+        int32_t ints[8];
+        r.pod(ints);
+        for (int a = 0; a < 3; ++a) d.res[a] = ints[a];
+        d.n_s = ints[3];
+        d.n_a = ints[4];
+        d.sh_order = ints[5];
+        if (d.sh_order < 1 || d.sh_order > 4 || d.n_s < 1 || d.n_a < 1)
+            fail(PSDF_ERR_RUNTIME, "checkpoint: bad grid header in %s", path);
+        uint32_t n_tiles = 0;
+        r.pod(n_tiles);
+        // tiles in file order; probes allocated corner by corner
+        // (allocate_tile -> ensure_probe, grid.cpp:44-72)
+        const int nt[3] = {d.res[0] / TE, d.res[1] / TE, d.res[2] / TE};
+        std::vector<int32_t> tc(3 * (size_t)n_tiles), pid(8 * (size_t)n_tiles), pco;
+        std::unordered_map<int64_t, int> probe_of;
+        auto key = [&](int64_t x, int64_t y, int64_t z) { return (x * (nt[1] + 2) + y) * (nt[2] + 2) + z; };
+        for (uint32_t t = 0; t < n_tiles; ++t) {
+            int32_t q[3];
+            r.pod(q);
+            for (int a = 0; a < 3; ++a) tc[3 * t + a] = q[a];
+            for (int i = 0; i < 8; ++i) {
+                const int g[3] = {q[0] + (i & 1), q[1] + ((i >> 1) & 1), q[2] + ((i >> 2) & 1)};
+                auto it = probe_of.find(key(g[0], g[1], g[2]));
+                int id;
+                if (it == probe_of.end()) {
+                    id = (int)(pco.size() / 3);
+                    probe_of.emplace(key(g[0], g[1], g[2]), id);
+                    pco.insert(pco.end(), g, g + 3);
+                } else {
+                    id = it->second;
+                }
+                pid[8 * t + i] = id;
+            }
+        }
+        const int64_t T = n_tiles, ps = 256 * (int64_t)d.n_s, pc = (int64_t)d.sh_order * d.sh_order * d.n_a;
+        std::vector<float> raw(T * TV), planes(T * 3 * ps);
+        for (int64_t t = 0; t < T; ++t) {
+            r.tensor(raw.data() + t * TV, TV);
+            for (int q = 0; q < 3; ++q) r.tensor(planes.data() + (t * 3 + q) * ps, ps);
+        }
+        uint32_t n_probes = 0;
+        r.pod(n_probes);
+        const int64_t P = (int64_t)(pco.size() / 3);
+        if ((int64_t)n_probes != P) fail(PSDF_ERR_RUNTIME, "checkpoint: probe table inconsistent with tiles in %s", path);
+        std::vector<float> probes(P * pc);
+        for (uint32_t i = 0; i < n_probes; ++i) {
+            int32_t q[3];
+            r.pod(q);
+            auto it = probe_of.find(key(q[0], q[1], q[2]));
+            if (q[0] < 0 || q[1] < 0 || q[2] < 0 || it == probe_of.end())
+                fail(PSDF_ERR_RUNTIME, "checkpoint: unknown probe coordinate in %s", path);
+            r.tensor(probes.data() + (int64_t)it->second * pc, pc);
+        }
+        int32_t mints[3];
+        r.pod(mints);
+        if (mints[0] != d.n_s || mints[1] != d.n_a || mints[2] < 0)
+            fail(PSDF_ERR_RUNTIME, "checkpoint: decoder does not match the grid's channels in %s", path);
+        d.ncam = mints[2];
+        const MlpLayout G = MlpLayout::make(d.n_s + d.n_a + NPOW);
+        std::vector<float> mlp(psdf_mlp_size(d.n_s, d.n_a, d.ncam));
+        r.tensor(mlp.data() + G.w1, G.b1 - G.w1);
+        r.tensor(mlp.data() + G.b1, HID);
+        r.tensor(mlp.data() + G.w2, HID * HID);
+        r.tensor(mlp.data() + G.b2, HID);
+        r.tensor(mlp.data() + G.w3, 3 * HID);
+        r.tensor(mlp.data() + G.b3, 3);
+        r.tensor(mlp.data() + G.cam, (uint64_t)d.ncam * HID);
+        int32_t cursor = 0;
+        int64_t iter = 0;
+        uint64_t sd = 0;
+        r.pod(cursor);
+        r.pod(iter);
+        r.pod(sd);
+        d.T = (int)T;
+        d.P = (int)P;
+        if (psdf_upload_grid(c, &d, tc.data(), pid.data(), pco.data(), raw.data(), nullptr, planes.data(),
+                             probes.data()) != PSDF_OK ||
+            psdf_upload_mlp(c, mlp.data(), (int64_t)mlp.size()) != PSDF_OK)
+            fail(PSDF_ERR_RUNTIME, "%s", g_err.c_str());
+        if (lod) *lod = ints[6];
+        if (band_voxels) *band_voxels = ints[7];
+        if (lod_cursor) *lod_cursor = cursor;
+        if (iteration) *iteration = iter;
+        if (seed) *seed = sd;
+    });
+}
+
 int psdf_set_keep_raypass_grads(psdf_ctx* c, int keep) {
     return guarded([&] {
         need_grid(c);
