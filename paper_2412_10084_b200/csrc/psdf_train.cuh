@@ -686,7 +686,10 @@ __global__ void __launch_bounds__(256) rec_tile_scatter_kernel(WaveBufs W, int* 
 
 // ------------------------------------------------------------------ K2b
 template <int NS, int NA, bool GEO>
-__global__ void __launch_bounds__(BLOCK) shade_fwd_kernel(RayPassParams P, WaveBufs W) {
+#ifndef PSDF_FWD_MINB
+#define PSDF_FWD_MINB 5  // <= 102 registers: 5 blocks per SM (measured best)
+#endif
+__global__ void __launch_bounds__(BLOCK, PSDF_FWD_MINB) shade_fwd_kernel(RayPassParams P, WaveBufs W) {
     const int n_rec = n_records(W);
     constexpr int IN = NS + NA + NPOW;
     extern __shared__ __align__(16) float smem[];
