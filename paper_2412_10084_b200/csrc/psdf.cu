@@ -919,7 +919,7 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
     // G^T fold (grads.cpp:67-96): raw_grad += G^T * staged
     launch_fold(c, c->d_gsmooth, c->d_grads + c->off_raw);
     // all-reduce across ranks (GradBuffers::add, trainer.cpp:184-185, across GPUs)
-    if (c->world > 1) {
+    if (c->comm) {
         NK(g_nccl.AllReduce(c->d_grads, c->d_grads, (size_t)c->n_params, ncclFloat, ncclSum, c->comm, s));
         NK(g_nccl.AllReduce(c->d_stats, c->d_stats, 16, ncclDouble, ncclSum, c->comm, s));
         NK(g_nccl.AllReduce(c->d_counts, c->d_counts, 8, ncclUint64, ncclSum, c->comm, s));
@@ -1992,7 +1992,9 @@ int psdf_comm_init(psdf_ctx* c, const void* unique_id, int rank, int world_size)
         set_device(c);
         c->rank = rank;
         c->world = world_size;
-        if (world_size == 1) return;
+        // a single rank has nothing to exchange — unless PSDF_FORCE_NCCL asks
+        // for the communicator anyway (tests: the NCCL path on one GPU)
+        if (world_size == 1 && !std::getenv("PSDF_FORCE_NCCL")) return;
         g_nccl.load();
         ncclUniqueId id;
         std::memcpy(&id, unique_id, sizeof id);

@@ -129,3 +129,37 @@ def _train_parity(ctx, case):
         og = og2
         og.train_reset()
         ctx.train_reset()
+
+
+def test_train_step_through_nccl_single_rank(ctx, monkeypatch):
+    """The multi-GPU exchange path (ncclAllReduce of the gradient buffer, the
+    loss statistics and the counts, psdf.cu do_train_step) exercised on one
+    GPU with a one-rank communicator: results equal the no-communicator step
+    (a one-rank sum is the identity)."""
+    from paper_2412_10084_b200 import api
+    monkeypatch.setenv("PSDF_FORCE_NCCL", "1")
+    g, a = make_scene(res=64, n_s=4, n_a=4, sh_order=4, band=6, ncam=0)
+    cams = api.make_ring_cameras(2, 32)
+    rng = np.random.default_rng(3)
+    gts = [rng.uniform(0, 1, (32, 32, 3)).astype(np.float32) for _ in cams]
+    masks = [np.ones((32, 32)) for _ in cams]
+    hp = api.step_params(tau=300.0 * 64, lr_vox=1e-4, lr_mlp=6e-5, photo_scale=20.0)
+    out = []
+    c2 = api.Context(0)
+    try:
+        c2.comm_init(api.Context.unique_id(), 0, 1)
+        for c in (ctx, c2):
+            c.upload(g, smooth=False)
+            c.keep_raypass_grads(True)
+            c.train_reset()
+            losses, counts = c.train_step(cams, gts, masks, hp)
+            out.append((losses, counts, c.grads(1), c.download()))
+    finally:
+        c2.close()
+    (l0, n0, g0, p0), (l1, n1, g1, p1) = out
+    assert n0 == n1
+    for k in ("photo", "sdf", "eik", "normal", "features", "probes"):
+        assert abs(l0[k] - l1[k]) <= 1e-9 * max(abs(l0[k]), 1e-9), (k, l0[k], l1[k])
+    for k in ("raw", "planes", "probes", "mlp"):
+        np.testing.assert_allclose(g1[k], g0[k], rtol=1e-5, atol=1e-7 * max(np.abs(g0[k]).max(), 1e-30))
+        np.testing.assert_allclose(p1[k], p0[k], rtol=1e-5, atol=1e-6)
