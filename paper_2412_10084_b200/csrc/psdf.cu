@@ -7,9 +7,10 @@
 //   gsmooth = [T*4096]                     (smooth-staged SDF gradient)
 //   adam m, v = same layout as params
 //   tile_table [nt0*nt1*nt2] int32, probe_table [(nt0+1)(nt1+1)(nt2+1)] int32
-// A train step is the kernel sequence K2 (fused ray pass) -> K3..K6
-// (regularizers) -> K7 (G^T fold) -> [NCCL all-reduce] -> K8 (Adam) -> K9
-// (smoothing), all on the context's stream.
+// A train step: sat_dist -> K2 (the ray pass, psdf_train.cuh) with K3..K6
+// (regularizers) and the empty rays' photo terms on a low-priority side
+// stream -> K7 (G^T fold) -> [NCCL all-reduce] -> K8 (Adam) -> K9 (smoothing
+// + apron); one host synchronisation at the end (buffer overflow -> redo).
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 #include <dlfcn.h>

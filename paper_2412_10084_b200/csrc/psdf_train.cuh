@@ -1,28 +1,32 @@
 // psdf_train.cuh — K2, the ray pass of one train step (trainer.cpp:157-182:
 // render_ray + photo_pixel + render_ray_backward + scatter_smooth_grad) as a
-// wavefront pipeline of four kernels.
+// wavefront pipeline (render, K1, reuses its forward half):
 //
-//  K2a march_fwd    one lane per ray (8x4 pixel tile per warp): the exact f64
-//                   march / alpha / T / weight chain.  Samples that the
-//                   reference decodes (w > 0 on an in-mask ray) are appended
-//                   to a record queue (warp-aggregated atomics) linked per
-//                   ray; rays with an alpha > 0 sample get a ray entry.  Rays
-//                   without one finish here (their loss needs no colour).
-//  K2b shade_fwd    one lane per record: decode_fused, colour stored in the
-//                   record, c_raw[ray] += w C (f64 atomics).
-//  K2d alpha_bwd    one lane per ray entry: photo_pixel, then the alpha /
-//                   transmittance chain of renderer.cpp:247-276 over the ray's
-//                   alpha > 0 samples (listed by K2a, no second march), SDF-
-//                   sample gradient scatters; writes each record's upstream
-//                   dL/dC = w g.
-//  K2e shade_bwd    one lane per record, 32 records per warp: decode forward
-//                   again + decode_backward with warp-cooperative MLP weight
-//                   gradients (lane j owns row j), tri-plane atomics, probe
-//                   gradients aggregated over lanes of the same tile, and the
-//                   normal chain (renderer.cpp:216-235).
+//  K2a-scan  march_scan   one lane per ray (8x4 pixel tile per warp): the
+//                         saturated prefix of the exact f64 march (empty-space
+//                         jumps, cell-saturated runs; no image read); rays that
+//                         reach a cell that can hold sigmoid < 1 are handed
+//                         over, the others only counted.
+//  K2a       march_fwd    two rounds (16 steps, then the still-alive rays
+//                         compacted): the exact alpha / T / weight chain of the
+//                         handed-over rays; shading records (samples the
+//                         reference decodes), ray entries and alpha-sample
+//                         lists appended with warp-aggregated atomics.
+//            rec_tile_*   shading records grouped by tile (counting sort).
+//  K2b       shade_fwd    one lane per record: decode_fused, colour stored in
+//                         the record, c_raw[ray] += w C (f64 atomics).
+//            empty_ray_loss  (side stream) photo terms of the finished rays.
+//  K2d       alpha_bwd    one lane per ray entry: photo_pixel, then the alpha /
+//                         transmittance chain of renderer.cpp:247-276 over the
+//                         ray's alpha > 0 samples (no second march), SDF-sample
+//                         gradient scatters; each record's upstream w g.
+//  K2e       shade_bwd    32 records per warp: decoder MLP backward as
+//                         3xTF32 mma.sync GEMMs, weight gradients in
+//                         registers, feature gradients per record.
+//  K2e-geo   shade_geo    tri-plane / probe / normal-chain gradients (probe
+//                         gradients aggregated over the records of one tile).
 //
-// The per-lane register footprint of the march sweeps no longer carries the
-// decoder, and the decode passes run with every lane busy.
+// Item counts are read on device (no host round trip inside the pass).
 //
 // Suffix sums: the reverse traversal of renderer.cpp:254-261 is replaced by
 // suffix_i = Total - prefix_i, Total = g.(c_raw - bg acc) + dA acc (known
