@@ -122,6 +122,12 @@ def test_render_parity(ctx, scene, tau_vox):
     _render_parity(ctx, scene, tau_vox)
 
 
+@pytest.mark.parametrize("tau_vox", [300.0, 3000.0])
+def test_render_parity_production_grid(ctx, tau_vox):
+    """configs[1] / [3] grid (512^3, (4, 4, 4), T = 2848) on a 48x48 view."""
+    _render_parity(ctx, dict(res=512, n_s=4, n_a=4, sh_order=4, band=6, radius=0.32), tau_vox)
+
+
 def test_render_parity_wave_overflow(monkeypatch):
     """Undersized ray-pass buffers: the render overflows, grows and redoes."""
     from paper_2412_10084_b200 import api

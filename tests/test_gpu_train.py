@@ -55,6 +55,14 @@ def test_train_step_parity(ctx, case):
     _train_parity(ctx, case)
 
 
+def test_train_step_parity_production_grid(ctx):
+    """The bench's grid (configs[1]: 512^3, (n_s, n_a, l) = (4, 4, 4), sphere
+    band 6, T = 2848) at the bench's tau, on small views: counts exact,
+    losses / gradients / post-Adam parameters within the contract."""
+    _train_parity(ctx, dict(scene=dict(res=512, n_s=4, n_a=4, sh_order=4, band=6, radius=0.32), tau=300.0,
+                            size=40, ncam=0, bias=False))
+
+
 def test_train_step_parity_wave_overflow(monkeypatch):
     """Ray-pass buffers far too small for the batch: the step overflows, Adam
     is skipped on device, the host grows the buffers and redoes the step —
@@ -115,7 +123,12 @@ def _train_parity(ctx, case):
             sig = np.abs(gk) > 1e-4 * max(np.abs(gk).max(), 1e-30)
             d = np.abs(p[k].astype(np.float64) - op[k])
             assert d[sig].max(initial=0) <= 2e-3 * kw["lr_vox"] + 1e-6, (step, k, d[sig].max(initial=0))
-        assert np.abs(p["smooth"] - op["smooth"]).max() <= 1e-5, np.abs(p["smooth"] - op["smooth"]).max()
+        # the re-smoothed SDF: 1e-5, plus the smoothing footprint of one Adam
+        # step where the f64 gradient is ~0 and the fp32 one has the other
+        # sign (Adam normalises both to +-lr; centre tap of the 5^3 Gaussian
+        # 0.4026^3 = 0.065, so 2 lr 0.065 ~ 0.13 lr per flipped voxel)
+        tol_sm = 1e-5 + 0.3 * kw["lr_vox"]
+        assert np.abs(p["smooth"] - op["smooth"]).max() <= tol_sm, np.abs(p["smooth"] - op["smooth"]).max()
         # re-sync the oracle onto the GPU's parameters so step 2 compares one
         # step from identical state (isolates per-step error from drift)
         b = a.copy()
