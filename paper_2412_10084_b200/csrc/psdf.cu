@@ -860,7 +860,7 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
                 (float)(1.0 / (2.0 * c->desc.voxel_size)), c->d_gsmooth, c->d_grads + c->off_raw, c->d_stats);
             CK(cudaGetLastError());
             dispatch_ns(c->desc.n_s, [&]<int NS>() {
-                loss_features_kernel<NS><<<3 * (t1 - t0), 256, 0, s>>>(g, t0, (float)hp->l_feat,
+                loss_features_kernel<NS><<<3 * (t1 - t0), 256, 0, sl>>>(g, t0, (float)hp->l_feat,
                                                                        c->d_grads + c->off_planes, c->d_stats);
             });
             CK(cudaGetLastError());
@@ -869,7 +869,7 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
         if (p1 > p0) {
             GridMut m{g, c->d_params + c->off_raw, c->d_probe_table, c->d_probe_coords};
             const int64_t n = (int64_t)(p1 - p0) * stride;
-            loss_probes_kernel<<<(unsigned)std::min<int64_t>(4 * c->sm_count, n / 256 + 1), 256, 0, s>>>(
+            loss_probes_kernel<<<(unsigned)std::min<int64_t>(4 * c->sm_count, n / 256 + 1), 256, 0, sl>>>(
                 m, p0, p1, stride, (float)hp->l_probe, c->d_grads + c->off_probes, c->d_stats);
             CK(cudaGetLastError());
             ++c->last_launches;

@@ -538,8 +538,9 @@ __global__ void __launch_bounds__(LG_THREADS, 2) loss_grid_kernel(GridView g, co
 }
 
 // K5: loss_features (losses.cpp:222-257); block = one (tile, plane), thread =
-// one texel with its NS channels, gathering the pair terms it belongs to (no
-// atomics: the plane's gradient is owned by this block).
+// one texel with its NS channels, gathering the pair terms it belongs to (one
+// atomic per texel channel: the ray pass may scatter into the same planes
+// concurrently).
 template <int NS>
 __global__ void __launch_bounds__(256) loss_features_kernel(GridView g, int t0, float lambda,
                                                             float* __restrict__ g_planes,
@@ -575,9 +576,10 @@ __global__ void __launch_bounds__(256) loss_features_kernel(GridView g, int t0, 
     if (b + 1 < 16) pair(ab, ab + 1, true, -1.f);    // pair (i0, (a, b+1))
     if (a >= 1) pair(ab - 16, ab, false, 1.f);       // pair ((a-1, b), i0): +g to i0
     if (b >= 1) pair(ab - 1, ab, false, 1.f);        // pair ((a, b-1), i0)
+    // atomic: the kernel may run beside the ray pass's plane-gradient scatters
 #pragma unroll
     for (int k = 0; k < NS; ++k)
-        if (gsum[k] != 0.f) gp[ab * NS + k] += gsum[k];
+        if (gsum[k] != 0.f) atomicAdd(gp + ab * NS + k, gsum[k]);
     block_add_f64(stats + 6, (double)pw, red);
     block_add_f64(stats + 11, (double)ww, red);
 }
