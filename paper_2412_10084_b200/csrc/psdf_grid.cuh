@@ -239,12 +239,14 @@ constexpr int kSatThreads = 320;  // >= 17 * 17 rows of cells
 __global__ void __launch_bounds__(kSatThreads) sat_dist_kernel(GridView g, double tau, uint8_t* __restrict__ sd) {
     constexpr int E = kCellE, NR = kCellE * kCellE;  // rows (x, y) of 17 cells along z: one bit each
     constexpr uint32_t FULLROW = (1u << kCellE) - 1u;
-    __shared__ float ap[AV];
+    __shared__ __align__(16) float ap[AV];
     __shared__ uint32_t M[2][NR];
     __shared__ uint8_t out[kCellN];
     const int t = blockIdx.x, r = threadIdx.x;
     const float* src = g.smooth_ap + (int64_t)t * AV;
-    for (int i = threadIdx.x; i < AV; i += blockDim.x) ap[i] = __ldg(src + i);
+    static_assert(AV % 4 == 0, "apron bricks are float4 aligned");
+    for (int i = threadIdx.x; i < AV / 4; i += blockDim.x)
+        reinterpret_cast<float4*>(ap)[i] = __ldg(reinterpret_cast<const float4*>(src) + i);
     __syncthreads();
     // unsaturated cells of row r as a bit mask
     uint32_t m = 0;
