@@ -170,6 +170,8 @@ struct psdf_ctx {
     cudaStream_t side_stream = nullptr;  // low priority: regularizers under the ray pass
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool fork_regs = false;              // the ray pass records ev_fork (do_train_step)
+    bool grads_clear_pending = false;    // gradient clear on the side stream (ev_zeroed)
+    cudaEvent_t ev_start = nullptr, ev_zeroed = nullptr;
     bool regs_early = false;             // PSDF_REGS_EARLY: fork the regularizer at step start
     cudaEvent_t ev_copied = nullptr, ev_copy_free = nullptr;
     bool images_pending = false;           // inside psdf_train_step: the copies may still run
@@ -678,6 +680,7 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     } else {
         // the photo terms read the ground-truth colours
         if (c->images_pending) CK(cudaStreamWaitEvent(s, c->ev_rgb, 0));
+        if (c->grads_clear_pending) CK(cudaStreamWaitEvent(s, c->ev_zeroed, 0));
         const int grid_ab = blocks_per_sm((const void*)alpha_bwd_kernel, 0) * c->sm_count;
         alpha_bwd_kernel<<<grid_ab, BLOCK, 0, s>>>(P, W);
         CK(cudaGetLastError());
@@ -805,9 +808,21 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
     c->last_launches = 0;
     cudaStream_t s = c->stream;
     CK(cudaEventRecord(c->ev_step0, s));
-    // gradient clear (trainer.cpp:136)
-    CK(cudaMemsetAsync(c->d_grads, 0, sizeof(float) * c->n_params, s));
-    CK(cudaMemsetAsync(c->d_gsmooth, 0, sizeof(float) * c->desc.T * TV, s));
+    // gradient clear (trainer.cpp:136).  Nothing writes a gradient before the
+    // α backward / the regularizers, so with the side stream the clear runs
+    // there under the saturation map and the scan (the α backward waits for
+    // ev_zeroed)
+    const bool overlap_clear = !c->keep_raypass;
+    cudaStream_t sc = s;
+    if (overlap_clear) {
+        CK(cudaEventRecord(c->ev_start, s));
+        CK(cudaStreamWaitEvent(c->side_stream, c->ev_start, 0));
+        sc = c->side_stream;
+    }
+    CK(cudaMemsetAsync(c->d_grads, 0, sizeof(float) * c->n_params, sc));
+    CK(cudaMemsetAsync(c->d_gsmooth, 0, sizeof(float) * c->desc.T * TV, sc));
+    if (overlap_clear) CK(cudaEventRecord(c->ev_zeroed, sc));
+    c->grads_clear_pending = overlap_clear;
     CK(cudaMemsetAsync(c->d_counts, 0, sizeof(unsigned long long) * 8, s));
     CK(cudaMemsetAsync(c->d_stats, 0, sizeof(double) * 16, s));
 
@@ -1036,6 +1051,8 @@ int psdf_create(int device, psdf_ctx** out) {
         CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_copied, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_masks, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_zeroed, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_rgb, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_copy_free, cudaEventDisableTiming));
         CK(cudaEventRecord(c->ev_copy_free, c->stream));
@@ -1089,6 +1106,8 @@ int psdf_destroy(psdf_ctx* c) {
         cudaEventDestroy(c->ev_copied);
         cudaEventDestroy(c->ev_copy_free);
         cudaEventDestroy(c->ev_masks);
+        cudaEventDestroy(c->ev_start);
+        cudaEventDestroy(c->ev_zeroed);
         cudaEventDestroy(c->ev_rgb);
         if (c->d_hand_bits) cudaFree(c->d_hand_bits);
         delete c;
