@@ -187,6 +187,13 @@ int psdf_render(psdf_ctx* ctx, const psdf_camera* cam, const psdf_render_opts* o
 /* Same, device-resident outputs (pointers into device memory). */
 int psdf_render_device(psdf_ctx* ctx, const psdf_camera* cam, const psdf_render_opts* opt,
                        float* d_rgb, float* d_alpha, float* d_depth, psdf_counts* counts);
+/* Evaluation: psnr_masked (metrics.cpp:196-211, metrics.hpp:51) of this
+   context's render of `cam` (with `opt`) against a host ground-truth view.
+   gt_rgb: H*W*3 f32 row-major; mask: H*W u8, nonzero = inside (the reference's
+   mask > 0.5, as psdf_train_step).  Squared error summed in f64 on the device;
+   99 dB when the mask is empty or the error is 0, capped at 99. */
+int psdf_eval_psnr(psdf_ctx* ctx, const psdf_camera* cam, const psdf_render_opts* opt,
+                   const float* gt_rgb, const uint8_t* mask, double* psnr, psdf_counts* counts);
 
 /* ---- train ------------------------------------------------------------------
  * One iteration of the train() loop body (trainer.cpp:136-195): clear

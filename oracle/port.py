@@ -261,3 +261,32 @@ def kat_adam(params, grads_seq, lrs):
     lr = np.ascontiguousarray(lrs, np.float64)
     lib().og_adam_steps(p.size, ptr(p), ptr(g), len(lr), ptr(lr))
     return p
+
+
+def psnr_masked(img, gt, mask):
+    """metrics.cpp:196-211 restated: squared error over the three channels of
+    every pixel with mask > 0.5, summed in row-major pixel order in f64; 99 dB
+    when no pixel is masked or the error is 0, capped at 99.  Pure Python loop
+    (small images only) so the summation order is the reference's."""
+    img = np.asarray(img, np.float64)
+    gt = np.asarray(gt, np.float64)
+    mask = np.asarray(mask, np.float64)
+    if img.shape != gt.shape:
+        raise ValueError("psnr_masked: image shape mismatch")
+    h, w = mask.shape
+    sq, n = 0.0, 0
+    for v in range(h):
+        for u in range(w):
+            if mask[v, u] <= 0.5:
+                continue
+            dx = img[v, u, 0] - gt[v, u, 0]
+            dy = img[v, u, 1] - gt[v, u, 1]
+            dz = img[v, u, 2] - gt[v, u, 2]
+            sq += (dx * dx + dy * dy) + dz * dz  # Vec3::norm2 (vec.hpp)
+            n += 3
+    if n == 0:
+        return 99.0
+    mse = sq / n
+    if mse <= 0.0:
+        return 99.0
+    return min(99.0, 10.0 * np.log10(1.0 / mse))

@@ -32,6 +32,7 @@
 #include "sdfrecon/grads.hpp"
 #include "sdfrecon/grid.hpp"
 #include "sdfrecon/losses.hpp"
+#include "sdfrecon/metrics.hpp"
 #include "sdfrecon/renderer.hpp"
 #include "sdfrecon/schedule.hpp"
 #include "sdfrecon/synth.hpp"
@@ -962,6 +963,22 @@ void ref_gaussian_kernel(double* out) {
 void ref_adam_steps(int n, double* params, const double* grads_seq, int steps, const double* lrs) {
     AdamState a(n);
     for (int t = 0; t < steps; ++t) a.step(params, grads_seq + static_cast<size_t>(t) * n, lrs[t]);
+}
+
+// metrics.cpp:196-211 psnr_masked (evaluation of a rendered view).
+int ref_psnr_masked(const double* img, const double* gt, const double* mask, int w, int h, double* out) {
+    try {
+        ImageRGB a(w, h), b(w, h);
+        ImageGray m(w, h);
+        std::memcpy(a.data.data(), img, a.data.size() * sizeof(double));
+        std::memcpy(b.data.data(), gt, b.data.size() * sizeof(double));
+        std::memcpy(m.data.data(), mask, m.data.size() * sizeof(double));
+        *out = psnr_masked(a, b, m);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
 }
 
 } // extern "C"

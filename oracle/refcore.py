@@ -155,6 +155,7 @@ def reflib():
     L.ref_fresnel_powers.argtypes = [C.c_double, _dp]
     L.ref_gaussian_kernel.argtypes = [_dp]
     L.ref_adam_steps.argtypes = [C.c_int, _dp, _dp, C.c_int, _dp]
+    L.ref_psnr_masked.argtypes = [_dp, _dp, _dp, C.c_int, C.c_int, _dp]
     _ref = L
     return L
 

@@ -84,7 +84,7 @@ EXPORTS = [
     "psdf_host_alloc", "psdf_host_free", "psdf_march_rays", "psdf_pixel_dirs",
     "psdf_last_k2_breakdown", "psdf_grid_info", "psdf_download_structure", "psdf_subdivide",
     "psdf_raise_sh_order", "psdf_last_h2d_bytes", "psdf_init_visual_hull", "psdf_save_checkpoint",
-    "psdf_load_checkpoint",
+    "psdf_load_checkpoint", "psdf_eval_psnr",
 ]
 
 _lib = None
@@ -118,6 +118,8 @@ def load():
                               C.POINTER(psdf_counts)]
     L.psdf_render_device.argtypes = [vp, C.POINTER(psdf_camera), C.POINTER(psdf_render_opts), vp, vp,
                                      vp, C.POINTER(psdf_counts)]
+    L.psdf_eval_psnr.argtypes = [vp, C.POINTER(psdf_camera), C.POINTER(psdf_render_opts), _fp,
+                                 C.POINTER(C.c_uint8), C.POINTER(C.c_double), C.POINTER(psdf_counts)]
     L.psdf_train_reset.argtypes = [vp]
     L.psdf_train_step.argtypes = [vp, C.c_int, C.POINTER(psdf_camera), C.POINTER(_fp),
                                   C.POINTER(C.POINTER(C.c_uint8)), C.POINTER(psdf_step_params),

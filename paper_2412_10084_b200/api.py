@@ -496,6 +496,24 @@ class Context:
                                        _fptr(dep), C.byref(counts)))
         return rgb, alpha, dep, counts.as_dict()
 
+    def eval_psnr(self, camera, opts: RenderOptions, gt_rgb, mask):
+        """psnr_masked(render_image(...).rgb, gt, mask) (metrics.cpp:196-211) with
+        the render and the masked reduction on the GPU; `mask` as in train_step
+        (u8 nonzero = inside, or floats thresholded at > 0.5)."""
+        cam = camera_from(camera)
+        gt = np.ascontiguousarray(gt_rgb, np.float32)
+        m = np.asarray(mask)
+        m = np.ascontiguousarray(m > 0.5, np.uint8) if m.dtype != np.uint8 else np.ascontiguousarray(m)
+        if gt.shape != (cam.height, cam.width, 3) or m.shape != (cam.height, cam.width):
+            raise ValueError("psnr_masked: image shape mismatch")
+        out = C.c_double()
+        counts = psdf_counts()
+        o = opts.to_c()
+        self._check(self.L.psdf_eval_psnr(self.h, C.byref(cam), C.byref(o), _fptr(gt),
+                                          m.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(out),
+                                          C.byref(counts)))
+        return out.value
+
     # -- train (trainer.cpp:136-195)
     def train_reset(self):
         self._check(self.L.psdf_train_reset(self.h))
@@ -593,3 +611,10 @@ def work_tiles(cameras):
 def render_image(ctx: Context, camera, opts: RenderOptions):
     """render_image(grid, mlp, camera, opt) (renderer.hpp:98-99) on the GPU."""
     return ctx.render_image(camera, opts)
+
+
+def psnr_masked_view(ctx: Context, camera, opts: RenderOptions, gt_rgb, mask) -> float:
+    """psnr_masked(render_image(grid, mlp, cam, opt).rgb, gt, mask)
+    (metrics.cpp:196-211) on the GPU: the evaluation loop of main.cpp's
+    `eval` per view."""
+    return ctx.eval_psnr(camera, opts, gt_rgb, mask)

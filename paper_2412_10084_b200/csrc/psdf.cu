@@ -1649,6 +1649,31 @@ struct FileCloser {
     }
 };
 }  // namespace
+// metrics.cpp:196-211 psnr_masked: squared error (three channels) over the
+// pixels inside the mask, accumulated in f64 from the fp32 render; one f64 /
+// u64 atomic pair per block.
+__global__ void __launch_bounds__(256) psnr_partial_kernel(const float* __restrict__ rgb,
+                                                           const float* __restrict__ gt,
+                                                           const uint8_t* __restrict__ mask, int64_t px,
+                                                           double* __restrict__ sq,
+                                                           unsigned long long* __restrict__ n) {
+    __shared__ double red[8];
+    double s = 0.0;
+    unsigned long long cnt = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < px; i += (int64_t)gridDim.x * blockDim.x) {
+        if (!mask[i]) continue;
+        const double dx = (double)rgb[3 * i] - (double)gt[3 * i];
+        const double dy = (double)rgb[3 * i + 1] - (double)gt[3 * i + 1];
+        const double dz = (double)rgb[3 * i + 2] - (double)gt[3 * i + 2];
+        s += (dx * dx + dy * dy) + dz * dz;  // Vec3::norm2
+        cnt += 3;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(n, cnt);
+    block_add_f64(sq, s, red);
+}
+
 extern "C" {
 
 int psdf_save_checkpoint(psdf_ctx* c, const char* path, int32_t lod, int32_t band_voxels, int32_t lod_cursor,
@@ -1875,6 +1900,44 @@ int psdf_render(psdf_ctx* c, const psdf_camera* cam, const psdf_render_opts* opt
         if (depth)
             CK(cudaMemcpyAsync(depth, d_depth, sizeof(float) * px, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int psdf_eval_psnr(psdf_ctx* c, const psdf_camera* cam, const psdf_render_opts* opt, const float* gt_rgb,
+                   const uint8_t* mask, double* psnr, psdf_counts* counts) {
+    return guarded([&] {
+        need_grid(c);
+        if (!cam || !gt_rgb || !mask || !psnr) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
+        check_camera(*cam);
+        set_device(c);
+        const size_t px = (size_t)cam->width * cam->height;
+        // render scratch rgb | alpha | depth (unused) | gt rgb | mask bytes
+        ensure_dev(c->d_render, c->render_px, 8 * px + px / 4 + 1);
+        float* d_rgb = c->d_render;
+        float* d_alpha = d_rgb + 3 * px;
+        float* d_gt = d_rgb + 5 * px;
+        uint8_t* d_mask = reinterpret_cast<uint8_t*>(d_rgb + 8 * px);
+        CK(cudaMemcpyAsync(d_gt, gt_rgb, sizeof(float) * 3 * px, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(d_mask, mask, px, cudaMemcpyHostToDevice, c->stream));
+        do_render(c, cam, opt, d_rgb, d_alpha, nullptr, counts);
+        CK(cudaMemsetAsync(c->d_stats, 0, sizeof(double), c->stream));
+        CK(cudaMemsetAsync(c->d_counts, 0, sizeof(unsigned long long), c->stream));
+        const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(4 * c->sm_count, (int64_t)(px + 255) / 256));
+        psnr_partial_kernel<<<blocks, 256, 0, c->stream>>>(d_rgb, d_gt, d_mask, (int64_t)px, c->d_stats,
+                                                           c->d_counts);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->h_counts, c->d_counts, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        const double sq = c->h_stats[0];
+        const unsigned long long n = c->h_counts[0];
+        double r = 99.0;
+        if (n > 0) {
+            const double mse = sq / (double)n;
+            if (mse > 0.0) r = std::min(99.0, 10.0 * std::log10(1.0 / mse));
+        }
+        *psnr = r;
     });
 }
 

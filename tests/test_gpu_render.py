@@ -201,3 +201,30 @@ def test_render_errors(ctx):
     rgb, alpha, _, counts = ctx.render_image(far, api.RenderOptions(tau=100.0, background=(0.25, 0.5, 0.75)))
     assert counts["n_marched"] == 0 and np.all(alpha == 0)
     assert np.allclose(rgb, [0.25, 0.5, 0.75])
+
+
+@pytest.mark.parametrize("scene", [SCENES[1], dict(res=512, n_s=4, n_a=4, sh_order=4, band=6, radius=0.32)])
+def test_eval_psnr(ctx, scene):
+    """psdf_eval_psnr (metrics.cpp:196-211 on the device): the masked-error
+    reduction of the GPU's own render matches the restated psnr_masked on
+    that render to 1e-9 dB (only the f64 summation order differs), and the
+    oracle's f64 render to 1e-3 dB; an empty mask and an exact match give 99."""
+    from oracle.port import psnr_masked
+    from paper_2412_10084_b200 import api
+    g, a = make_scene(**scene)
+    og, sm = oracle_with_f32_smooth(a)
+    _upload(ctx, g, sm)
+    cam = api.make_lookat_camera(0, (1.3, 0.2, 0.4), (0, 0, 0), (0, 1, 0), 1.2 * 48, 1.2 * 48, 48, 40)
+    opts = api.RenderOptions(tau=300.0 * scene["res"], camera_id=0)
+    rng = np.random.default_rng(7)
+    gt = rng.uniform(0, 1, (40, 48, 3)).astype(np.float32)
+    mask = rng.uniform(0, 1, (40, 48))
+    got = ctx.eval_psnr(cam, opts, gt, mask)
+    rgb, _, _, _ = ctx.render_image(cam, opts)
+    assert abs(got - psnr_masked(rgb, gt, mask)) <= 1e-9
+    orgb = og.render_image(_oracle_cam(cam), _oracle_opts(opts))[0]
+    assert abs(got - psnr_masked(orgb, gt.astype(np.float64), mask)) <= 1e-3
+    assert ctx.eval_psnr(cam, opts, gt, np.zeros((40, 48))) == 99.0
+    assert ctx.eval_psnr(cam, opts, rgb, mask) == 99.0
+    with pytest.raises(ValueError, match="shape mismatch"):
+        ctx.eval_psnr(cam, opts, gt[:-1], mask)

@@ -120,3 +120,22 @@ def test_step_mirror_matches_reference_train():
     pa, pb = a.export(), b.export()
     for k in ("raw", "planes", "probes", "mlp"):
         assert np.allclose(getattr(pa, k), getattr(pb, k), rtol=0, atol=1e-12), k
+
+
+def test_psnr_masked_bit_exact():
+    """oracle.port.psnr_masked against the reference's psnr_masked
+    (metrics.cpp:196-211) through the harness: random images, a random mask,
+    an empty mask and an exact match."""
+    import ctypes as C
+    from oracle import refcore as R
+    from oracle.port import psnr_masked
+    L = R.reflib()
+    rng = np.random.default_rng(3)
+    h, w = 23, 37
+    img, gt = rng.uniform(0, 1, (h, w, 3)), rng.uniform(0, 1, (h, w, 3))
+    for mask in (rng.uniform(0, 1, (h, w)), np.zeros((h, w)), np.ones((h, w))):
+        for a in (img, gt):
+            out = np.zeros(1)
+            R._check(L.ref_psnr_masked(R.ptr(np.ascontiguousarray(a)), R.ptr(gt), R.ptr(mask), w, h,
+                                       R.ptr(out)), L)
+            assert psnr_masked(a, gt, mask) == out[0]
