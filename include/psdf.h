@@ -194,6 +194,20 @@ int psdf_render_device(psdf_ctx* ctx, const psdf_camera* cam, const psdf_render_
    99 dB when the mask is empty or the error is 0, capped at 99. */
 int psdf_eval_psnr(psdf_ctx* ctx, const psdf_camera* cam, const psdf_render_opts* opt,
                    const float* gt_rgb, const uint8_t* mask, double* psnr, psdf_counts* counts);
+/* Evaluation geometry (metrics.cpp, metrics.hpp:15-48).  Meshes are host
+   TriMesh arrays: verts nv x 3 f64, tris nt x 3 i32; points n x 3 f64.
+   psdf_point_mesh_distance = MeshDistance(mesh).distance(p) per point
+   (metrics.cpp:131-135), exact minimum over the triangles on the device.
+   psdf_chamfer = chamfer(pred_points, pred_mesh, gt_points, gt_mesh, max_dist)
+   (metrics.cpp:182-194): out[3] = {accuracy, completeness, mean}, x1000.
+   Errors as the reference: empty mesh / empty input -> INVALID_ARGUMENT; a
+   triangle index outside the vertex array -> OUT_OF_RANGE. */
+int psdf_point_mesh_distance(psdf_ctx* ctx, const double* points, int64_t n, const double* verts, int64_t nv,
+                             const int32_t* tris, int64_t nt, double* out_dist);
+int psdf_chamfer(psdf_ctx* ctx, const double* pred_pts, int64_t n_pred, const double* pred_verts,
+                 int64_t pred_nv, const int32_t* pred_tris, int64_t pred_nt, const double* gt_pts,
+                 int64_t n_gt, const double* gt_verts, int64_t gt_nv, const int32_t* gt_tris, int64_t gt_nt,
+                 double max_dist, double* out);
 
 /* ---- train ------------------------------------------------------------------
  * One iteration of the train() loop body (trainer.cpp:136-195): clear

@@ -290,3 +290,74 @@ def psnr_masked(img, gt, mask):
     if mse <= 0.0:
         return 99.0
     return min(99.0, 10.0 * np.log10(1.0 / mse))
+
+
+def _dot(a, b):  # Vec3::dot (vec.hpp:26): (x*x' + y*y') + z*z'
+    return (a[..., 0] * b[..., 0] + a[..., 1] * b[..., 1]) + a[..., 2] * b[..., 2]
+
+
+def _norm(a):
+    return np.sqrt(_dot(a, a))
+
+
+def point_triangle_distances(p, a, b, c):
+    """metrics.cpp:11-47 (Ericson's closest point) restated over arrays of
+    triangles for one point; every branch is evaluated in the reference's
+    operation order and the first region that applies is selected, so each
+    value is the reference's f64 result bit for bit."""
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ab, ac, ap = b - a, c - a, p - a
+        d1, d2 = _dot(ab, ap), _dot(ac, ap)
+        bp = p - b
+        d3, d4 = _dot(ab, bp), _dot(ac, bp)
+        vc = d1 * d4 - d3 * d2
+        cp = p - c
+        d5, d6 = _dot(ab, cp), _dot(ac, cp)
+        vb = d5 * d2 - d1 * d6
+        va = d3 * d6 - d5 * d4
+        v_ab = d1 / (d1 - d3)
+        w_ac = d2 / (d2 - d6)
+        w_bc = (d4 - d3) / ((d4 - d3) + (d5 - d6))
+        denom = 1.0 / ((va + vb) + vc)
+        v_in, w_in = vb * denom, vc * denom
+        conds = [(d1 <= 0.0) & (d2 <= 0.0),
+                 (d3 >= 0.0) & (d4 <= d3),
+                 (vc <= 0.0) & (d1 >= 0.0) & (d3 <= 0.0),
+                 (d6 >= 0.0) & (d5 <= d6),
+                 (vb <= 0.0) & (d2 >= 0.0) & (d6 <= 0.0),
+                 (va <= 0.0) & ((d4 - d3) >= 0.0) & ((d5 - d6) >= 0.0)]
+        vals = [_norm(p - a), _norm(p - b), _norm(p - (a + ab * v_ab[:, None])), _norm(p - c),
+                _norm(p - (a + ac * w_ac[:, None])), _norm(p - (b + (c - b) * w_bc[:, None]))]
+        inside = _norm(p - ((a + ab * v_in[:, None]) + ac * w_in[:, None]))
+    return np.select(conds, vals, inside)
+
+
+def point_mesh_distance(points, verts, tris):
+    """MeshDistance::distance (metrics.cpp:131-135) as a brute-force minimum
+    over the triangles (the BVH only prunes; test_geometry.cpp:212-226 checks
+    it against this scan)."""
+    v = np.asarray(verts, np.float64)
+    t = np.asarray(tris, np.int64)
+    if len(t) == 0:
+        raise ValueError("MeshDistance: empty mesh")
+    a, b, c = v[t[:, 0]], v[t[:, 1]], v[t[:, 2]]
+    return np.array([point_triangle_distances(np.asarray(p, np.float64), a, b, c).min() for p in points])
+
+
+def chamfer(pred_pts, pred_verts, pred_tris, gt_pts, gt_verts, gt_tris, max_dist):
+    """metrics.cpp:168-194: two-way mean point-to-mesh distance x1000, points
+    beyond max_dist (> 0) excluded, summed in point order."""
+    if len(pred_pts) == 0 or len(gt_pts) == 0 or len(pred_tris) == 0 or len(gt_tris) == 0:
+        raise ValueError("chamfer: empty input")
+
+    def mean(d):
+        s, n = 0.0, 0
+        for x in d:
+            if max_dist > 0.0 and x > max_dist:
+                continue
+            s += float(x)
+            n += 1
+        return s / n if n else 0.0
+    acc = 1000.0 * mean(point_mesh_distance(pred_pts, gt_verts, gt_tris))
+    comp = 1000.0 * mean(point_mesh_distance(gt_pts, pred_verts, pred_tris))
+    return np.array([acc, comp, 0.5 * (acc + comp)])

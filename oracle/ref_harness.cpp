@@ -32,6 +32,7 @@
 #include "sdfrecon/grads.hpp"
 #include "sdfrecon/grid.hpp"
 #include "sdfrecon/losses.hpp"
+#include "sdfrecon/mesh.hpp"
 #include "sdfrecon/metrics.hpp"
 #include "sdfrecon/renderer.hpp"
 #include "sdfrecon/schedule.hpp"
@@ -981,4 +982,92 @@ int ref_psnr_masked(const double* img, const double* gt, const double* mask, int
     }
 }
 
+// mesh.cpp:363 marching_cubes of the scene's smoothed grid; call with zero
+// capacities for the sizes, then again with buffers.
+int ref_marching_cubes(RefScene* s, double* verts, int64_t vcap, int32_t* tris, int64_t tcap, int64_t* nv,
+                       int64_t* nt) {
+    try {
+        const TriMesh m = marching_cubes(s->grid);
+        *nv = static_cast<int64_t>(m.vertices.size());
+        *nt = static_cast<int64_t>(m.triangles.size());
+        if (verts && tris && vcap >= *nv && tcap >= *nt) {
+            for (int64_t i = 0; i < *nv; ++i) {
+                verts[3 * i] = m.vertices[i].x;
+                verts[3 * i + 1] = m.vertices[i].y;
+                verts[3 * i + 2] = m.vertices[i].z;
+            }
+            for (int64_t i = 0; i < *nt; ++i)
+                for (int k = 0; k < 3; ++k) tris[3 * i + k] = m.triangles[i][k];
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+static TriMesh to_mesh(const double* verts, int64_t nv, const int32_t* tris, int64_t nt) {
+    TriMesh m;
+    m.vertices.resize(nv);
+    for (int64_t i = 0; i < nv; ++i) m.vertices[i] = {verts[3 * i], verts[3 * i + 1], verts[3 * i + 2]};
+    m.triangles.resize(nt);
+    for (int64_t i = 0; i < nt; ++i) m.triangles[i] = {tris[3 * i], tris[3 * i + 1], tris[3 * i + 2]};
+    return m;
+}
+
+static std::vector<Vec3> to_points(const double* p, int64_t n) {
+    std::vector<Vec3> v(n);
+    for (int64_t i = 0; i < n; ++i) v[i] = {p[3 * i], p[3 * i + 1], p[3 * i + 2]};
+    return v;
+}
+
+// metrics.cpp:131-135 MeshDistance::distance for each point.
+int ref_point_mesh_distance(const double* pts, int64_t n, const double* verts, int64_t nv, const int32_t* tris,
+                            int64_t nt, double* out) {
+    try {
+        const TriMesh m = to_mesh(verts, nv, tris, nt);
+        const MeshDistance md(m);
+        for (int64_t i = 0; i < n; ++i) out[i] = md.distance({pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]});
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// metrics.cpp:137-166 sample_mesh_points.
+int ref_sample_mesh_points(const double* verts, int64_t nv, const int32_t* tris, int64_t nt, int n, uint64_t seed,
+                           double* out) {
+    try {
+        const auto pts = sample_mesh_points(to_mesh(verts, nv, tris, nt), n, seed);
+        for (int i = 0; i < n; ++i) {
+            out[3 * i] = pts[i].x;
+            out[3 * i + 1] = pts[i].y;
+            out[3 * i + 2] = pts[i].z;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// metrics.cpp:182-194 chamfer; out = {accuracy, completeness, mean}.
+int ref_chamfer(const double* pp, int64_t np, const double* pv, int64_t pnv, const int32_t* pt, int64_t pnt,
+                const double* gp, int64_t ng, const double* gv, int64_t gnv, const int32_t* gt, int64_t gnt,
+                double max_dist, double* out) {
+    try {
+        const ChamferResult r = chamfer(to_points(pp, np), to_mesh(pv, pnv, pt, pnt), to_points(gp, ng),
+                                        to_mesh(gv, gnv, gt, gnt), max_dist);
+        out[0] = r.accuracy;
+        out[1] = r.completeness;
+        out[2] = r.mean;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 } // extern "C"
+

@@ -156,6 +156,12 @@ def reflib():
     L.ref_gaussian_kernel.argtypes = [_dp]
     L.ref_adam_steps.argtypes = [C.c_int, _dp, _dp, C.c_int, _dp]
     L.ref_psnr_masked.argtypes = [_dp, _dp, _dp, C.c_int, C.c_int, _dp]
+    _i32p, _i64p = C.POINTER(C.c_int32), C.POINTER(C.c_int64)
+    L.ref_marching_cubes.argtypes = [C.c_void_p, _dp, C.c_int64, _i32p, C.c_int64, _i64p, _i64p]
+    L.ref_point_mesh_distance.argtypes = [_dp, C.c_int64, _dp, C.c_int64, _i32p, C.c_int64, _dp]
+    L.ref_sample_mesh_points.argtypes = [_dp, C.c_int64, _i32p, C.c_int64, C.c_int, C.c_uint64, _dp]
+    L.ref_chamfer.argtypes = [_dp, C.c_int64, _dp, C.c_int64, _i32p, C.c_int64, _dp, C.c_int64, _dp,
+                              C.c_int64, _i32p, C.c_int64, C.c_double, _dp]
     _ref = L
     return L
 
@@ -318,6 +324,17 @@ class RefScene:
                                            threads), self.L)
         return rgb, alpha
 
+    def marching_cubes(self):
+        """mesh.cpp:363 marching_cubes(grid) -> (verts (nv, 3) f64, tris (nt, 3) i32)."""
+        nv, nt = C.c_int64(), C.c_int64()
+        i32 = C.POINTER(C.c_int32)
+        _check(self.L.ref_marching_cubes(self.h, None, 0, None, 0, C.byref(nv), C.byref(nt)), self.L)
+        v = np.zeros((nv.value, 3))
+        t = np.zeros((nt.value, 3), np.int32)
+        _check(self.L.ref_marching_cubes(self.h, ptr(v), nv.value, t.ctypes.data_as(i32), nt.value,
+                                         C.byref(nv), C.byref(nt)), self.L)
+        return v, t
+
     def march_ray(self, o, d, n_max=512):
         ts = np.zeros(max(n_max, 1))
         o = np.asarray(o, np.float64)
@@ -445,3 +462,41 @@ def raytrace(prims, cam: RefCamera, lights=ACCEPT_LIGHTS):
 
 
 GLOSSY_SPHERE = [(0, (0.0, 0.0, 0.0), (0.3, 0.3, 0.3), (0.55, 0.3, 0.2), 0.08, 32.0)]
+
+
+def _mesh_args(verts, tris):
+    v = np.ascontiguousarray(verts, np.float64)
+    t = np.ascontiguousarray(tris, np.int32)
+    return v, t, t.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def ref_point_mesh_distance(points, verts, tris):
+    """metrics.cpp:131-135 through the reference library."""
+    L = reflib()
+    p = np.ascontiguousarray(points, np.float64)
+    v, t, tp = _mesh_args(verts, tris)
+    out = np.zeros(len(p))
+    _check(L.ref_point_mesh_distance(ptr(p), len(p), ptr(v), len(v), tp, len(t), ptr(out)), L)
+    return out
+
+
+def ref_sample_mesh_points(verts, tris, n, seed):
+    """metrics.cpp:137-166 through the reference library."""
+    L = reflib()
+    v, t, tp = _mesh_args(verts, tris)
+    out = np.zeros((n, 3))
+    _check(L.ref_sample_mesh_points(ptr(v), len(v), tp, len(t), n, seed, ptr(out)), L)
+    return out
+
+
+def ref_chamfer(pred_pts, pred_verts, pred_tris, gt_pts, gt_verts, gt_tris, max_dist):
+    """metrics.cpp:182-194 through the reference library."""
+    L = reflib()
+    pp = np.ascontiguousarray(pred_pts, np.float64)
+    gp = np.ascontiguousarray(gt_pts, np.float64)
+    pv, pt, ptp = _mesh_args(pred_verts, pred_tris)
+    gv, gt, gtp = _mesh_args(gt_verts, gt_tris)
+    out = np.zeros(3)
+    _check(L.ref_chamfer(ptr(pp), len(pp), ptr(pv), len(pv), ptp, len(pt), ptr(gp), len(gp), ptr(gv), len(gv),
+                         gtp, len(gt), max_dist, ptr(out)), L)
+    return out

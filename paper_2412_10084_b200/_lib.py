@@ -84,7 +84,7 @@ EXPORTS = [
     "psdf_host_alloc", "psdf_host_free", "psdf_march_rays", "psdf_pixel_dirs",
     "psdf_last_k2_breakdown", "psdf_grid_info", "psdf_download_structure", "psdf_subdivide",
     "psdf_raise_sh_order", "psdf_last_h2d_bytes", "psdf_init_visual_hull", "psdf_save_checkpoint",
-    "psdf_load_checkpoint", "psdf_eval_psnr",
+    "psdf_load_checkpoint", "psdf_eval_psnr", "psdf_point_mesh_distance", "psdf_chamfer",
 ]
 
 _lib = None
@@ -120,6 +120,10 @@ def load():
                                      vp, C.POINTER(psdf_counts)]
     L.psdf_eval_psnr.argtypes = [vp, C.POINTER(psdf_camera), C.POINTER(psdf_render_opts), _fp,
                                  C.POINTER(C.c_uint8), C.POINTER(C.c_double), C.POINTER(psdf_counts)]
+    _dp, _i32 = C.POINTER(C.c_double), C.POINTER(C.c_int32)
+    L.psdf_point_mesh_distance.argtypes = [vp, _dp, C.c_int64, _dp, C.c_int64, _i32, C.c_int64, _dp]
+    L.psdf_chamfer.argtypes = [vp, _dp, C.c_int64, _dp, C.c_int64, _i32, C.c_int64, _dp, C.c_int64, _dp,
+                               C.c_int64, _i32, C.c_int64, C.c_double, _dp]
     L.psdf_train_reset.argtypes = [vp]
     L.psdf_train_step.argtypes = [vp, C.c_int, C.POINTER(psdf_camera), C.POINTER(_fp),
                                   C.POINTER(C.POINTER(C.c_uint8)), C.POINTER(psdf_step_params),

@@ -514,6 +514,29 @@ class Context:
                                           C.byref(counts)))
         return out.value
 
+    def point_mesh_distance(self, points, verts, tris):
+        """MeshDistance(mesh).distance(p) for every point (metrics.cpp:131-135),
+        on the GPU; returns (n,) f64."""
+        p = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+        v, t = _mesh(verts, tris)
+        out = np.zeros(len(p))
+        self._check(self.L.psdf_point_mesh_distance(self.h, _dptr(p), len(p), _dptr(v), len(v), _iptr(t),
+                                                    len(t), _dptr(out)))
+        return out
+
+    def chamfer(self, pred_points, pred_verts, pred_tris, gt_points, gt_verts, gt_tris, max_dist=0.0):
+        """chamfer(pred_points, pred_mesh, gt_points, gt_mesh, max_dist)
+        (metrics.cpp:182-194) -> dict(accuracy, completeness, mean), x1000."""
+        pp = np.ascontiguousarray(pred_points, np.float64).reshape(-1, 3)
+        gp = np.ascontiguousarray(gt_points, np.float64).reshape(-1, 3)
+        pv, pt = _mesh(pred_verts, pred_tris)
+        gv, gt = _mesh(gt_verts, gt_tris)
+        out = np.zeros(3)
+        self._check(self.L.psdf_chamfer(self.h, _dptr(pp), len(pp), _dptr(pv), len(pv), _iptr(pt), len(pt),
+                                        _dptr(gp), len(gp), _dptr(gv), len(gv), _iptr(gt), len(gt),
+                                        float(max_dist), _dptr(out)))
+        return dict(accuracy=out[0], completeness=out[1], mean=out[2])
+
     # -- train (trainer.cpp:136-195)
     def train_reset(self):
         self._check(self.L.psdf_train_reset(self.h))
@@ -618,3 +641,17 @@ def psnr_masked_view(ctx: Context, camera, opts: RenderOptions, gt_rgb, mask) ->
     (metrics.cpp:196-211) on the GPU: the evaluation loop of main.cpp's
     `eval` per view."""
     return ctx.eval_psnr(camera, opts, gt_rgb, mask)
+
+
+
+def _mesh(verts, tris):
+    return (np.ascontiguousarray(verts, np.float64).reshape(-1, 3),
+            np.ascontiguousarray(tris, np.int32).reshape(-1, 3))
+
+
+def _dptr(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _iptr(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))

@@ -11,6 +11,7 @@
 // (regularizers) and the empty rays' photo terms on a low-priority side
 // stream -> K7 (G^T fold) -> [NCCL all-reduce] -> K8 (Adam) -> K9 (smoothing
 // + apron); one host synchronisation at the end (buffer overflow -> redo).
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -1649,6 +1650,192 @@ struct FileCloser {
     }
 };
 }  // namespace
+// ---- evaluation geometry: point-to-mesh distance and chamfer (metrics.cpp) --
+// f64 with explicit round-to-nearest operations (no FMA contraction), in the
+// reference's operation order, so every point-triangle distance is bit-equal
+// to point_triangle_distance (metrics.cpp:11-47) compiled without contraction.
+struct MV3 {
+    double x, y, z;
+};
+__device__ __forceinline__ MV3 d3sub(MV3 a, MV3 b) { return {__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y), __dsub_rn(a.z, b.z)}; }
+__device__ __forceinline__ double d3dot(MV3 a, MV3 b) {  // Vec3::dot (vec.hpp:26)
+    return __dadd_rn(__dadd_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)), __dmul_rn(a.z, b.z));
+}
+__device__ __forceinline__ MV3 d3axpy(MV3 a, MV3 d, double s) {  // a + d * s
+    return {__dadd_rn(a.x, __dmul_rn(d.x, s)), __dadd_rn(a.y, __dmul_rn(d.y, s)), __dadd_rn(a.z, __dmul_rn(d.z, s))};
+}
+__device__ __forceinline__ double d3norm(MV3 a) { return __dsqrt_rn(d3dot(a, a)); }
+__device__ __forceinline__ double dsub2(double a, double b, double c, double d) {  // a*b - c*d
+    return __dsub_rn(__dmul_rn(a, b), __dmul_rn(c, d));
+}
+
+// metrics.cpp:11-47 (Ericson's closest point on a triangle).
+__device__ double point_triangle_distance(MV3 p, MV3 a, MV3 b, MV3 c) {
+    const MV3 ab = d3sub(b, a), ac = d3sub(c, a), ap = d3sub(p, a);
+    const double d1 = d3dot(ab, ap), d2 = d3dot(ac, ap);
+    if (d1 <= 0.0 && d2 <= 0.0) return d3norm(d3sub(p, a));
+    const MV3 bp = d3sub(p, b);
+    const double d3 = d3dot(ab, bp), d4 = d3dot(ac, bp);
+    if (d3 >= 0.0 && d4 <= d3) return d3norm(d3sub(p, b));
+    const double vc = dsub2(d1, d4, d3, d2);
+    if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {
+        const double v = __ddiv_rn(d1, __dsub_rn(d1, d3));
+        return d3norm(d3sub(p, d3axpy(a, ab, v)));
+    }
+    const MV3 cp = d3sub(p, c);
+    const double d5 = d3dot(ab, cp), d6 = d3dot(ac, cp);
+    if (d6 >= 0.0 && d5 <= d6) return d3norm(d3sub(p, c));
+    const double vb = dsub2(d5, d2, d1, d6);
+    if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
+        const double w = __ddiv_rn(d2, __dsub_rn(d2, d6));
+        return d3norm(d3sub(p, d3axpy(a, ac, w)));
+    }
+    const double va = dsub2(d3, d6, d5, d4);
+    const double e43 = __dsub_rn(d4, d3), e56 = __dsub_rn(d5, d6);
+    if (va <= 0.0 && e43 >= 0.0 && e56 >= 0.0) {
+        const double w = __ddiv_rn(e43, __dadd_rn(e43, e56));
+        return d3norm(d3sub(p, d3axpy(b, d3sub(c, b), w)));
+    }
+    const double denom = __ddiv_rn(1.0, __dadd_rn(__dadd_rn(va, vb), vc));
+    const double v = __dmul_rn(vb, denom), w = __dmul_rn(vc, denom);
+    return d3norm(d3sub(p, d3axpy(d3axpy(a, ab, v), ac, w)));
+}
+
+// Triangle soup (9 doubles per triangle) and one AABB per chunk of kTriChunk
+// consecutive triangles (meshes from marching cubes are emitted cell by cell,
+// so consecutive triangles are spatially coherent and the boxes are tight).
+constexpr int kTriChunk = 128;
+__global__ void __launch_bounds__(kTriChunk) tri_soup_kernel(const double* __restrict__ verts, int64_t nv,
+                                                             const int32_t* __restrict__ tris, int64_t nt,
+                                                             double* __restrict__ soup, double* __restrict__ box,
+                                                             unsigned long long* __restrict__ bad) {
+    __shared__ double red[6][kTriChunk];
+    const int64_t t = blockIdx.x * (int64_t)kTriChunk + threadIdx.x;
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    if (t < nt) {
+        for (int k = 0; k < 3; ++k) {
+            int32_t vi = tris[3 * t + k];
+            if (vi < 0 || vi >= nv) {
+                atomicAdd(bad, 1ull);
+                vi = 0;
+            }
+            for (int a = 0; a < 3; ++a) {
+                const double x = verts[3 * (int64_t)vi + a];
+                soup[9 * t + 3 * k + a] = x;
+                lo[a] = fmin(lo[a], x);
+                hi[a] = fmax(hi[a], x);
+            }
+        }
+    }
+    for (int a = 0; a < 3; ++a) {
+        red[a][threadIdx.x] = lo[a];
+        red[3 + a][threadIdx.x] = hi[a];
+    }
+    __syncthreads();
+    for (int o = kTriChunk / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o)
+            for (int a = 0; a < 3; ++a) {
+                red[a][threadIdx.x] = fmin(red[a][threadIdx.x], red[a][threadIdx.x + o]);
+                red[3 + a][threadIdx.x] = fmax(red[3 + a][threadIdx.x], red[3 + a][threadIdx.x + o]);
+            }
+        __syncthreads();
+    }
+    if (threadIdx.x < 6) box[6 * blockIdx.x + threadIdx.x] = red[threadIdx.x][0];
+}
+
+// 30-bit Morton key of each point in the points' bounding box, so that a
+// block's points are spatially coherent and its chunk culling is effective.
+__global__ void __launch_bounds__(256) morton_kernel(const double* __restrict__ pts, int64_t n, double lx, double ly,
+                                                     double lz, double inv, uint32_t* __restrict__ key,
+                                                     int32_t* __restrict__ idx) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    auto spread = [](double x) {
+        uint32_t v = (uint32_t)fmin(fmax(x, 0.0), 1023.0);
+        v = (v | (v << 16)) & 0x030000FFu;
+        v = (v | (v << 8)) & 0x0300F00Fu;
+        v = (v | (v << 4)) & 0x030C30C3u;
+        v = (v | (v << 2)) & 0x09249249u;
+        return v;
+    };
+    key[i] = (spread((pts[3 * i] - lx) * inv) << 2) | (spread((pts[3 * i + 1] - ly) * inv) << 1) |
+             spread((pts[3 * i + 2] - lz) * inv);
+    idx[i] = (int32_t)i;
+}
+
+__device__ __forceinline__ double box_dist(const double* bx, MV3 p) {  // metrics.cpp:104-110 shape
+    const double dx = fmax(fmax(bx[0] - p.x, 0.0), p.x - bx[3]);
+    const double dy = fmax(fmax(bx[1] - p.y, 0.0), p.y - bx[4]);
+    const double dz = fmax(fmax(bx[2] - p.z, 0.0), p.z - bx[5]);
+    return sqrt(dx * dx + dy * dy + dz * dz);
+}
+
+// Unsigned distance of each point to the mesh (MeshDistance::distance,
+// metrics.cpp:131-135): the exact minimum over all triangles.  One thread per
+// point, points in Morton order (perm).  The block first visits the chunk
+// whose box is nearest its first point (a tight initial bound), then every
+// chunk that some thread's point may be closer to than its current best
+// (conservative margin, so the minimum is the brute-force one); chunks are
+// staged in shared memory.
+__global__ void __launch_bounds__(kTriChunk) point_mesh_distance_kernel(const double* __restrict__ pts, int64_t n,
+                                                                        const int32_t* __restrict__ perm,
+                                                                        const double* __restrict__ soup,
+                                                                        const double* __restrict__ box, int64_t nt,
+                                                                        double* __restrict__ out) {
+    __shared__ double tri[kTriChunk * 9];
+    __shared__ double rd[kTriChunk];
+    __shared__ int64_t ri[kTriChunk];
+    const int64_t i = blockIdx.x * (int64_t)kTriChunk + threadIdx.x;
+    const bool live = i < n;
+    const int64_t pi = live ? perm[i] : 0;
+    MV3 p = {0, 0, 0};
+    if (live) p = {pts[3 * pi], pts[3 * pi + 1], pts[3 * pi + 2]};
+    const int64_t i0 = perm[blockIdx.x * (int64_t)kTriChunk];
+    const MV3 p0 = {pts[3 * i0], pts[3 * i0 + 1], pts[3 * i0 + 2]};
+    const int64_t nch = (nt + kTriChunk - 1) / kTriChunk;
+    // nearest chunk box to the block's first point
+    double bd = 1e300;
+    int64_t bi = 0;
+    for (int64_t ch = threadIdx.x; ch < nch; ch += kTriChunk) {
+        const double d = box_dist(box + 6 * ch, p0);
+        if (d < bd) {
+            bd = d;
+            bi = ch;
+        }
+    }
+    rd[threadIdx.x] = bd;
+    ri[threadIdx.x] = bi;
+    __syncthreads();
+    for (int o = kTriChunk / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o && (rd[threadIdx.x + o] < rd[threadIdx.x] ||
+                                (rd[threadIdx.x + o] == rd[threadIdx.x] && ri[threadIdx.x + o] < ri[threadIdx.x]))) {
+            rd[threadIdx.x] = rd[threadIdx.x + o];
+            ri[threadIdx.x] = ri[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    const int64_t first = ri[0];
+    double best = 1.7976931348623157e308;  // numeric_limits<double>::max()
+    for (int64_t k = -1; k < nch; ++k) {
+        const int64_t ch = k < 0 ? first : k;
+        if (k == first) continue;
+        const bool need = live && (k < 0 || box_dist(box + 6 * ch, p) * (1.0 - 1e-9) <= best);
+        if (!__syncthreads_or(need)) continue;
+        const int64_t t0 = ch * kTriChunk;
+        const int cnt = (int)(nt - t0 < kTriChunk ? nt - t0 : kTriChunk);
+        for (int q = threadIdx.x; q < cnt * 9; q += kTriChunk) tri[q] = soup[9 * t0 + q];
+        __syncthreads();
+        if (need)
+            for (int q = 0; q < cnt; ++q) {
+                const double* v = tri + 9 * q;
+                best = fmin(best, point_triangle_distance(p, {v[0], v[1], v[2]}, {v[3], v[4], v[5]},
+                                                          {v[6], v[7], v[8]}));
+            }
+        __syncthreads();
+    }
+    if (live) out[pi] = best;
+}
+
 // metrics.cpp:196-211 psnr_masked: squared error (three channels) over the
 // pixels inside the mask, accumulated in f64 from the fp32 render; one f64 /
 // u64 atomic pair per block.
@@ -1938,6 +2125,100 @@ int psdf_eval_psnr(psdf_ctx* c, const psdf_camera* cam, const psdf_render_opts* 
             if (mse > 0.0) r = std::min(99.0, 10.0 * std::log10(1.0 / mse));
         }
         *psnr = r;
+    });
+}
+
+// MeshDistance over a host mesh for host points (device-side distances).
+static void mesh_distances(psdf_ctx* c, const double* pts, int64_t n, const double* verts, int64_t nv,
+                           const int32_t* tris, int64_t nt, double* out) {
+    if (nt <= 0) fail(PSDF_ERR_INVALID_ARGUMENT, "MeshDistance: empty mesh");  // metrics.cpp:49
+    if (!verts || !tris || nv <= 0 || (n > 0 && (!pts || !out))) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
+    if (n == 0) return;
+    if (n > INT32_MAX || nt > INT32_MAX) fail(PSDF_ERR_INVALID_ARGUMENT, "too many points or triangles");
+    cudaStream_t s = c->stream;
+    const int64_t nch = (nt + kTriChunk - 1) / kTriChunk;
+    double lo[3] = {pts[0], pts[1], pts[2]}, hi[3] = {pts[0], pts[1], pts[2]};
+    for (int64_t i = 1; i < n; ++i)
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = std::min(lo[a], pts[3 * i + a]);
+            hi[a] = std::max(hi[a], pts[3 * i + a]);
+        }
+    const double ext = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2], 1e-300});
+    double *d_pts, *d_verts, *d_soup, *d_box, *d_out;
+    int32_t *d_tris, *d_idx, *d_idx2;
+    uint32_t *d_key, *d_key2;
+    size_t tmp_bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                       (int32_t*)nullptr, (int32_t*)nullptr, (int)n, 0, 30, s));
+    void* d_tmp;
+    CK(cudaMallocAsync(&d_pts, sizeof(double) * 3 * n, s));
+    CK(cudaMallocAsync(&d_verts, sizeof(double) * 3 * nv, s));
+    CK(cudaMallocAsync(&d_tris, sizeof(int32_t) * 3 * nt, s));
+    CK(cudaMallocAsync(&d_soup, sizeof(double) * 9 * nt, s));
+    CK(cudaMallocAsync(&d_box, sizeof(double) * 6 * nch, s));
+    CK(cudaMallocAsync(&d_out, sizeof(double) * n, s));
+    CK(cudaMallocAsync(&d_key, sizeof(uint32_t) * 2 * n, s));
+    CK(cudaMallocAsync(&d_idx, sizeof(int32_t) * 2 * n, s));
+    CK(cudaMallocAsync(&d_tmp, std::max<size_t>(tmp_bytes, 1), s));
+    d_key2 = d_key + n;
+    d_idx2 = d_idx + n;
+    CK(cudaMemcpyAsync(d_pts, pts, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_verts, verts, sizeof(double) * 3 * nv, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_tris, tris, sizeof(int32_t) * 3 * nt, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(c->d_counts, 0, sizeof(unsigned long long), s));
+    morton_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(d_pts, n, lo[0], lo[1], lo[2], 1023.0 / ext, d_key,
+                                                              d_idx);
+    CK(cub::DeviceRadixSort::SortPairs(d_tmp, tmp_bytes, d_key, d_key2, d_idx, d_idx2, (int)n, 0, 30, s));
+    tri_soup_kernel<<<(unsigned)nch, kTriChunk, 0, s>>>(d_verts, nv, d_tris, nt, d_soup, d_box, c->d_counts);
+    point_mesh_distance_kernel<<<(unsigned)((n + kTriChunk - 1) / kTriChunk), kTriChunk, 0, s>>>(
+        d_pts, n, d_idx2, d_soup, d_box, nt, d_out);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, d_out, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->h_counts, c->d_counts, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    for (void* p : {(void*)d_pts, (void*)d_verts, (void*)d_tris, (void*)d_soup, (void*)d_box, (void*)d_out,
+                    (void*)d_key, (void*)d_idx, d_tmp})
+        CK(cudaFreeAsync(p, s));
+    CK(cudaStreamSynchronize(s));
+    if (c->h_counts[0]) fail(PSDF_ERR_OUT_OF_RANGE, "triangle vertex index out of range");
+}
+
+int psdf_point_mesh_distance(psdf_ctx* c, const double* points, int64_t n, const double* verts, int64_t nv,
+                             const int32_t* tris, int64_t nt, double* out_dist) {
+    return guarded([&] {
+        if (!c) fail(PSDF_ERR_INVALID_ARGUMENT, "null context");
+        set_device(c);
+        mesh_distances(c, points, n, verts, nv, tris, nt, out_dist);
+    });
+}
+
+// directional_mean (metrics.cpp:168-179): summed on the host in point order
+// from the device distances, so the mean is the reference's bit for bit.
+static double directional_mean(const std::vector<double>& d, double max_dist) {
+    double sum = 0.0;
+    long count = 0;
+    for (double x : d) {
+        if (max_dist > 0.0 && x > max_dist) continue;
+        sum += x;
+        ++count;
+    }
+    return count > 0 ? sum / count : 0.0;
+}
+
+int psdf_chamfer(psdf_ctx* c, const double* pred_pts, int64_t n_pred, const double* pred_verts, int64_t pred_nv,
+                 const int32_t* pred_tris, int64_t pred_nt, const double* gt_pts, int64_t n_gt,
+                 const double* gt_verts, int64_t gt_nv, const int32_t* gt_tris, int64_t gt_nt, double max_dist,
+                 double* out) {
+    return guarded([&] {
+        if (!c || !out) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
+        if (n_pred <= 0 || n_gt <= 0 || pred_nt <= 0 || gt_nt <= 0)  // metrics.cpp:185-186
+            fail(PSDF_ERR_INVALID_ARGUMENT, "chamfer: empty input");
+        set_device(c);
+        std::vector<double> to_gt(n_pred), to_pred(n_gt);
+        mesh_distances(c, pred_pts, n_pred, gt_verts, gt_nv, gt_tris, gt_nt, to_gt.data());
+        mesh_distances(c, gt_pts, n_gt, pred_verts, pred_nv, pred_tris, pred_nt, to_pred.data());
+        out[0] = 1000.0 * directional_mean(to_gt, max_dist);    // accuracy
+        out[1] = 1000.0 * directional_mean(to_pred, max_dist);  // completeness
+        out[2] = 0.5 * (out[0] + out[1]);
     });
 }
 

@@ -14,6 +14,12 @@ Fixtures (small; committed):
                  ray-pass and final gradients, post-step parameters).
   init64.npz     init_grid_sphere at 64^3 (tile / probe ordering, raw SDF)
                  and reference cameras (make_lookat_camera, make_ring_cameras).
+  mesh32.npz     the reference's marching_cubes of a jittered 32^3 sphere
+                 scene and of a shifted copy, sample_mesh_points on both,
+                 MeshDistance distances of probe points, and chamfer with and
+                 without max_dist clipping (metrics.cpp).
+
+    python tests/golden/make_golden.py [kat scene32 init64 mesh32]
 """
 import os
 import sys
@@ -138,9 +144,25 @@ def init64():
     np.savez_compressed(os.path.join(HERE, "init64.npz"), **out)
 
 
+def mesh32():
+    s = R.RefScene.sphere(res=32, n_s=2, n_a=2, sh_order=2, band_voxels=6, radius=0.3, ncam=0)
+    s.randomize(5, sdf_jitter=0.004)
+    v, t = s.marching_cubes()
+    v2 = v + np.array([0.004, -0.002, 0.001])
+    rng = np.random.default_rng(11)
+    probes = np.concatenate([rng.uniform(-0.7, 0.7, (300, 3)), v[:100] + rng.normal(0, 1e-3, (100, 3)),
+                             v[100:120]])
+    p1 = R.ref_sample_mesh_points(v, t, 2000, 1)
+    p2 = R.ref_sample_mesh_points(v2, t, 2000, 2)
+    out = dict(verts=v, tris=t, verts2=v2, probes=probes, probe_dist=R.ref_point_mesh_distance(probes, v, t),
+               pred_pts=p1, gt_pts=p2, chamfer0=R.ref_chamfer(p1, v, t, p2, v2, t, 0.0),
+               chamfer_clip=R.ref_chamfer(p1, v, t, p2, v2, t, 0.0045))
+    np.savez_compressed(os.path.join(HERE, "mesh32.npz"), **out)
+
+
 if __name__ == "__main__":
-    kat()
-    scene32()
-    init64()
-    for f in ("kat.npz", "scene32.npz", "init64.npz"):
+    which = sys.argv[1:] or ["kat", "scene32", "init64", "mesh32"]
+    for name in which:
+        globals()[name]()
+        f = name + ".npz"
         print(f, os.path.getsize(os.path.join(HERE, f)), "bytes")

@@ -156,3 +156,18 @@ def test_host_cameras_match_reference():
     assert np.allclose(arr(c), z["lookat"], rtol=0, atol=1e-15)
     for c, want in zip(api.make_ring_cameras(6, 48, 2.0, 0.35, 17), z["ring"]):
         assert np.allclose(arr(c), want, rtol=0, atol=1e-15)
+
+
+def test_mesh_distance_golden():
+    """oracle.port.point_mesh_distance / chamfer against the reference's
+    MeshDistance and chamfer on its own marching-cubes mesh (mesh32.npz)."""
+    from oracle.port import chamfer, point_mesh_distance
+    g = golden("mesh32.npz")
+    v, t, v2 = g["verts"], g["tris"], g["verts2"]
+    assert np.array_equal(point_mesh_distance(g["probes"], v, t), g["probe_dist"])
+    p1, p2 = g["pred_pts"][:400], g["gt_pts"][:400]
+    full = chamfer(g["pred_pts"], v, t, g["gt_pts"], v2, t, 0.0)
+    assert np.array_equal(full, g["chamfer0"])
+    assert np.array_equal(chamfer(g["pred_pts"], v, t, g["gt_pts"], v2, t, 0.0045), g["chamfer_clip"])
+    with pytest.raises(ValueError, match="empty input"):
+        chamfer(p1[:0], v, t, p2, v2, t, 0.0)

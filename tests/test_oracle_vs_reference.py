@@ -139,3 +139,40 @@ def test_psnr_masked_bit_exact():
             R._check(L.ref_psnr_masked(R.ptr(np.ascontiguousarray(a)), R.ptr(gt), R.ptr(mask), w, h,
                                        R.ptr(out)), L)
             assert psnr_masked(a, gt, mask) == out[0]
+
+
+@pytest.fixture(scope="module")
+def mc_mesh():
+    """The reference's own marching_cubes (mesh.cpp:363) of a jittered sphere scene."""
+    from oracle import refcore as R
+    s = R.RefScene.sphere(res=32, n_s=2, n_a=2, sh_order=2, band_voxels=6, radius=0.3, ncam=0)
+    s.randomize(5, sdf_jitter=0.004)
+    return s.marching_cubes()
+
+
+def test_point_mesh_distance_bit_exact(mc_mesh):
+    """oracle.port.point_mesh_distance (brute-force restatement of
+    metrics.cpp:11-47) against MeshDistance (BVH, metrics.cpp:48-135)."""
+    from oracle import refcore as R
+    from oracle.port import point_mesh_distance
+    v, t = mc_mesh
+    assert len(t) > 500
+    rng = np.random.default_rng(11)
+    pts = np.concatenate([rng.uniform(-0.7, 0.7, (150, 3)), v[:50] + rng.normal(0, 1e-3, (50, 3)), v[50:60]])
+    assert np.array_equal(point_mesh_distance(pts, v, t), R.ref_point_mesh_distance(pts, v, t))
+
+
+def test_chamfer_bit_exact(mc_mesh):
+    """oracle.port.chamfer against chamfer (metrics.cpp:182-194) on the
+    reference's sampled surface points, with and without max_dist clipping."""
+    from oracle import refcore as R
+    from oracle.port import chamfer
+    v, t = mc_mesh
+    # a second mesh: the same surface shifted by a fraction of a voxel
+    v2 = v + np.array([0.004, -0.002, 0.001])
+    p1 = R.ref_sample_mesh_points(v, t, 300, 1)
+    p2 = R.ref_sample_mesh_points(v2, t, 300, 2)
+    for md in (0.0, 0.0045):
+        assert np.array_equal(chamfer(p1, v, t, p2, v2, t, md), R.ref_chamfer(p1, v, t, p2, v2, t, md))
+    with pytest.raises(RuntimeError, match="empty mesh"):
+        R.ref_point_mesh_distance(p1, v, t[:0])
