@@ -26,6 +26,8 @@
 #include "psdf.h"
 #include "sdfrecon/checkpoint.hpp"
 #include "sdfrecon/dataset.hpp"
+#include "sdfrecon/mesh.hpp"
+#include "sdfrecon/metrics.hpp"
 #include "sdfrecon/renderer.hpp"
 #include "sdfrecon/schedule.hpp"
 #include "sdfrecon/trainer.hpp"
@@ -335,6 +337,60 @@ inline sdfrecon::TrainStats train(const sdfrecon::Dataset& ds, const sdfrecon::T
     ckpt.lod_cursor = static_cast<int>(sched.lods.size()) - 1;
     ckpt.iteration = sched.lods.back().iterations;
     return stats;
+}
+
+// psnr_masked (metrics.cpp:196-211) of a render of the resident grid against
+// a ground-truth view, render and reduction on the device.
+inline double psnr_masked_render(Device& dev, const sdfrecon::Camera& camera, const sdfrecon::RenderOptions& opt,
+                                 const sdfrecon::ImageRGB& gt, const sdfrecon::ImageGray& mask) {
+    if (gt.width != camera.width || gt.height != camera.height || mask.width != gt.width ||
+        mask.height != gt.height)
+        throw std::invalid_argument("psnr_masked: image shape mismatch");
+    const psdf_camera c = to_c(camera);
+    const psdf_render_opts o = to_c(opt);
+    std::vector<float> g(gt.data.begin(), gt.data.end());
+    std::vector<uint8_t> m(mask.data.size());
+    for (size_t i = 0; i < m.size(); ++i) m[i] = mask.data[i] > 0.5 ? 1 : 0;
+    double psnr = 0.0;
+    check(psdf_eval_psnr(dev.ctx(), &c, &o, g.data(), m.data(), &psnr, nullptr), dev.ctx());
+    return psnr;
+}
+
+// Same signature as sdfrecon::chamfer (metrics.hpp:46-48); the point-to-mesh
+// distances run on `dev`, bit-identical to MeshDistance.
+inline sdfrecon::ChamferResult chamfer(Device& dev, const std::vector<sdfrecon::Vec3>& pred_points,
+                                       const sdfrecon::TriMesh& pred_mesh,
+                                       const std::vector<sdfrecon::Vec3>& gt_points,
+                                       const sdfrecon::TriMesh& gt_mesh, double max_dist) {
+    auto flat_pts = [](const std::vector<sdfrecon::Vec3>& p) {
+        std::vector<double> f(3 * p.size());
+        for (size_t i = 0; i < p.size(); ++i) {
+            f[3 * i] = p[i].x;
+            f[3 * i + 1] = p[i].y;
+            f[3 * i + 2] = p[i].z;
+        }
+        return f;
+    };
+    auto flat_tris = [](const sdfrecon::TriMesh& m) {
+        std::vector<int32_t> t(3 * m.triangles.size());
+        for (size_t i = 0; i < m.triangles.size(); ++i)
+            for (int k = 0; k < 3; ++k) t[3 * i + k] = m.triangles[i][k];
+        return t;
+    };
+    const auto pp = flat_pts(pred_points), gp = flat_pts(gt_points);
+    const auto pv = flat_pts(pred_mesh.vertices), gv = flat_pts(gt_mesh.vertices);
+    const auto pt = flat_tris(pred_mesh), gt = flat_tris(gt_mesh);
+    double out[3];
+    check(psdf_chamfer(dev.ctx(), pp.data(), (int64_t)pred_points.size(), pv.data(),
+                       (int64_t)pred_mesh.vertices.size(), pt.data(), (int64_t)pred_mesh.triangles.size(),
+                       gp.data(), (int64_t)gt_points.size(), gv.data(), (int64_t)gt_mesh.vertices.size(),
+                       gt.data(), (int64_t)gt_mesh.triangles.size(), max_dist, out),
+          dev.ctx());
+    sdfrecon::ChamferResult r;
+    r.accuracy = out[0];
+    r.completeness = out[1];
+    r.mean = out[2];
+    return r;
 }
 
 }  // namespace sdfrecon_gpu

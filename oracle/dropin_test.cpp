@@ -122,5 +122,25 @@ int main() {
     const std::string lc = log_cpu.str(), lg = log_gpu.str();
     std::printf("log_lines %zu %zu\n", (size_t)std::count(lc.begin(), lc.end(), '\n'),
                 (size_t)std::count(lg.begin(), lg.end(), '\n'));
+
+    // evaluation (acceptance.cpp:266-300 pattern): chamfer of the two trained
+    // grids' marching-cubes meshes, and psnr_masked of a render of view 0
+    const TriMesh ma = marching_cubes(ck_cpu.grid), mb = marching_cubes(ck_gpu.grid);
+    const auto pa = sample_mesh_points(ma, 3000, 1), pb = sample_mesh_points(mb, 3000, 2);
+    sdfrecon_gpu::Device dev(0);
+    for (double md : {0.0, 0.01}) {
+        const ChamferResult ca = chamfer(pa, ma, pb, mb, md);
+        const ChamferResult cb = sdfrecon_gpu::chamfer(dev, pa, ma, pb, mb, md);
+        std::printf("chamfer_equal %d\n", ca.accuracy == cb.accuracy && ca.completeness == cb.completeness &&
+                                               ca.mean == cb.mean ? 1 : 0);
+    }
+    dev.upload(ck_gpu.grid, ck_gpu.mlp);
+    RenderOptions eo;
+    eo.tau = 60.0 / ck_gpu.grid.voxel_size;
+    const RenderedImage ri = render_image(ck_gpu.grid, ck_gpu.mlp, ds.views[0].camera, eo);
+    const double psnr_cpu = psnr_masked(ri.color, ds.views[0].image, ds.views[0].mask);
+    const double psnr_gpu = sdfrecon_gpu::psnr_masked_render(dev, ds.views[0].camera, eo, ds.views[0].image,
+                                                             ds.views[0].mask);
+    std::printf("eval_psnr %.6f %.6f\n", psnr_cpu, psnr_gpu);
     return 0;
 }

@@ -341,7 +341,10 @@ def point_mesh_distance(points, verts, tris):
     if len(t) == 0:
         raise ValueError("MeshDistance: empty mesh")
     a, b, c = v[t[:, 0]], v[t[:, 1]], v[t[:, 2]]
-    return np.array([point_triangle_distances(np.asarray(p, np.float64), a, b, c).min() for p in points])
+    # best = std::min(best, d) from numeric_limits<double>::max(): a NaN
+    # distance (degenerate triangle) never replaces best, which fmin mirrors
+    return np.array([np.fmin.reduce(point_triangle_distances(np.asarray(p, np.float64), a, b, c),
+                                    initial=np.finfo(np.float64).max) for p in points])
 
 
 def chamfer(pred_pts, pred_verts, pred_tris, gt_pts, gt_verts, gt_tris, max_dist):

@@ -1772,16 +1772,20 @@ __device__ __forceinline__ double box_dist(const double* bx, MV3 p) {  // metric
 
 // Unsigned distance of each point to the mesh (MeshDistance::distance,
 // metrics.cpp:131-135): the exact minimum over all triangles.  One thread per
-// point, points in Morton order (perm).  The block first visits the chunk
-// whose box is nearest its first point (a tight initial bound), then every
-// chunk that some thread's point may be closer to than its current best
+// point, points in Morton order (perm); blockIdx.y splits the chunk range so
+// the grid fills the GPU.  Each block first visits the chunk whose box is
+// nearest its first point (a tight initial bound), then every chunk of its
+// range that some thread's point may be closer to than its current best
 // (conservative margin, so the minimum is the brute-force one); chunks are
-// staged in shared memory.
+// staged in shared memory.  Partial minima meet in a u64 atomicMin on the
+// f64 bit patterns (non-negative doubles order like their bits; out starts at
+// all-ones).  NaN distances (degenerate triangles) never win, as with
+// std::min(best, d).
 __global__ void __launch_bounds__(kTriChunk) point_mesh_distance_kernel(const double* __restrict__ pts, int64_t n,
                                                                         const int32_t* __restrict__ perm,
                                                                         const double* __restrict__ soup,
                                                                         const double* __restrict__ box, int64_t nt,
-                                                                        double* __restrict__ out) {
+                                                                        unsigned long long* __restrict__ out) {
     __shared__ double tri[kTriChunk * 9];
     __shared__ double rd[kTriChunk];
     __shared__ int64_t ri[kTriChunk];
@@ -1793,7 +1797,8 @@ __global__ void __launch_bounds__(kTriChunk) point_mesh_distance_kernel(const do
     const int64_t i0 = perm[blockIdx.x * (int64_t)kTriChunk];
     const MV3 p0 = {pts[3 * i0], pts[3 * i0 + 1], pts[3 * i0 + 2]};
     const int64_t nch = (nt + kTriChunk - 1) / kTriChunk;
-    // nearest chunk box to the block's first point
+    const int64_t c0 = nch * blockIdx.y / gridDim.y, c1 = nch * (blockIdx.y + 1) / gridDim.y;
+    // nearest chunk box to the block's first point (over all chunks)
     double bd = 1e300;
     int64_t bi = 0;
     for (int64_t ch = threadIdx.x; ch < nch; ch += kTriChunk) {
@@ -1816,10 +1821,11 @@ __global__ void __launch_bounds__(kTriChunk) point_mesh_distance_kernel(const do
     }
     const int64_t first = ri[0];
     double best = 1.7976931348623157e308;  // numeric_limits<double>::max()
-    for (int64_t k = -1; k < nch; ++k) {
-        const int64_t ch = k < 0 ? first : k;
-        if (k == first) continue;
-        const bool need = live && (k < 0 || box_dist(box + 6 * ch, p) * (1.0 - 1e-9) <= best);
+    for (int64_t k = c0 - 1; k < c1; ++k) {
+        const bool seed = k < c0;
+        const int64_t ch = seed ? first : k;
+        if (!seed && k == first) continue;
+        const bool need = live && (seed || box_dist(box + 6 * ch, p) * (1.0 - 1e-9) <= best);
         if (!__syncthreads_or(need)) continue;
         const int64_t t0 = ch * kTriChunk;
         const int cnt = (int)(nt - t0 < kTriChunk ? nt - t0 : kTriChunk);
@@ -1833,7 +1839,7 @@ __global__ void __launch_bounds__(kTriChunk) point_mesh_distance_kernel(const do
             }
         __syncthreads();
     }
-    if (live) out[pi] = best;
+    if (live) atomicMin(out + pi, (unsigned long long)__double_as_longlong(best));
 }
 
 // metrics.cpp:196-211 psnr_masked: squared error (three channels) over the
@@ -2170,8 +2176,12 @@ static void mesh_distances(psdf_ctx* c, const double* pts, int64_t n, const doub
                                                               d_idx);
     CK(cub::DeviceRadixSort::SortPairs(d_tmp, tmp_bytes, d_key, d_key2, d_idx, d_idx2, (int)n, 0, 30, s));
     tri_soup_kernel<<<(unsigned)nch, kTriChunk, 0, s>>>(d_verts, nv, d_tris, nt, d_soup, d_box, c->d_counts);
-    point_mesh_distance_kernel<<<(unsigned)((n + kTriChunk - 1) / kTriChunk), kTriChunk, 0, s>>>(
-        d_pts, n, d_idx2, d_soup, d_box, nt, d_out);
+    // split the chunk range over blockIdx.y until the grid holds ~16 blocks per SM
+    const int64_t nblk = (n + kTriChunk - 1) / kTriChunk;
+    const int64_t split = std::max<int64_t>(1, std::min<int64_t>({64, nch, (16 * c->sm_count + nblk - 1) / nblk}));
+    CK(cudaMemsetAsync(d_out, 0xff, sizeof(double) * n, s));
+    point_mesh_distance_kernel<<<dim3((unsigned)nblk, (unsigned)split), kTriChunk, 0, s>>>(
+        d_pts, n, d_idx2, d_soup, d_box, nt, reinterpret_cast<unsigned long long*>(d_out));
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(out, d_out, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->h_counts, c->d_counts, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));

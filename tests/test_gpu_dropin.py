@@ -27,3 +27,6 @@ def test_cpp_dropin_matches_reference():
     assert float(kv["train_raw_maxdiff"][0]) <= 1e-3 * float(kv["train_raw_maxdiff"][2])
     assert kv["train_cursor"][0] == kv["train_cursor"][1]
     assert kv["log_lines"][0] == kv["log_lines"][1] == "40"
+    # evaluation drop-ins: chamfer bit-exact, psnr_masked of a render to 1e-3 dB
+    assert [l for l in out.splitlines() if l.startswith("chamfer_equal")] == ["chamfer_equal 1"] * 2
+    assert abs(float(kv["eval_psnr"][0]) - float(kv["eval_psnr"][1])) <= 1e-3

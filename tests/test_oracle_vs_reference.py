@@ -176,3 +176,19 @@ def test_chamfer_bit_exact(mc_mesh):
         assert np.array_equal(chamfer(p1, v, t, p2, v2, t, md), R.ref_chamfer(p1, v, t, p2, v2, t, md))
     with pytest.raises(RuntimeError, match="empty mesh"):
         R.ref_point_mesh_distance(p1, v, t[:0])
+
+
+def test_point_mesh_distance_degenerate_soup():
+    """Unstructured triangles with a repeated corner and a collinear sliver
+    (NaN closest-point parameters): the restatement keeps std::min's NaN
+    behaviour."""
+    from oracle import refcore as R
+    from oracle.port import point_mesh_distance
+    rng = np.random.default_rng(0)
+    nt = 300
+    v = rng.uniform(-0.5, 0.5, (3 * nt, 3))
+    v[3 * 5 + 1] = v[3 * 5]
+    v[3 * 9 + 2] = 0.5 * (v[3 * 9] + v[3 * 9 + 1])
+    t = np.arange(3 * nt, dtype=np.int32).reshape(nt, 3)
+    pts = np.concatenate([rng.uniform(-0.8, 0.8, (100, 3)), v[:40]])
+    assert np.array_equal(point_mesh_distance(pts, v, t), R.ref_point_mesh_distance(pts, v, t))
