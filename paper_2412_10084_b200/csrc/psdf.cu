@@ -224,6 +224,8 @@ struct psdf_ctx {
     int viewdev_cap = 0;
     float* d_render = nullptr;  // render scratch: rgb | alpha | depth
     size_t render_px = 0;
+    uint8_t* d_eval = nullptr;  // point-to-mesh scratch (grow-only arena)
+    size_t eval_cap = 0;
 
     unsigned long long* d_work = nullptr;
     unsigned long long* d_counts = nullptr;
@@ -1084,7 +1086,7 @@ int psdf_destroy(psdf_ctx* c) {
             if (v.mask) cudaFree(v.mask);
         }
         for (void* p : {(void*)c->d_stage_rgb, (void*)c->d_stage_mask, (void*)c->d_viewdev,
-                        (void*)c->d_render, (void*)c->d_work, (void*)c->d_counts, (void*)c->d_stats})
+                        (void*)c->d_render, (void*)c->d_eval, (void*)c->d_work, (void*)c->d_counts, (void*)c->d_stats})
             if (p) cudaFree(p);
         free_wave(c);
         if (c->wave.counters) cudaFree(c->wave.counters);
@@ -1705,6 +1707,7 @@ __device__ double point_triangle_distance(MV3 p, MV3 a, MV3 b, MV3 c) {
 // consecutive triangles (meshes from marching cubes are emitted cell by cell,
 // so consecutive triangles are spatially coherent and the boxes are tight).
 constexpr int kTriChunk = 128;
+constexpr int kSeeds = 3;  // initial-bound chunks per block
 __global__ void __launch_bounds__(kTriChunk) tri_soup_kernel(const double* __restrict__ verts, int64_t nv,
                                                              const int32_t* __restrict__ tris, int64_t nt,
                                                              double* __restrict__ soup, double* __restrict__ box,
@@ -1773,8 +1776,8 @@ __device__ __forceinline__ double box_dist(const double* bx, MV3 p) {  // metric
 // Unsigned distance of each point to the mesh (MeshDistance::distance,
 // metrics.cpp:131-135): the exact minimum over all triangles.  One thread per
 // point, points in Morton order (perm); blockIdx.y splits the chunk range so
-// the grid fills the GPU.  Each block first visits the chunk whose box is
-// nearest its first point (a tight initial bound), then every chunk of its
+// the grid fills the GPU.  Each block first visits the chunks whose boxes are
+// nearest its first, middle and last point (tight initial bounds), then every chunk of its
 // range that some thread's point may be closer to than its current best
 // (conservative margin, so the minimum is the brute-force one); chunks are
 // staged in shared memory.  Partial minima meet in a u64 atomicMin on the
@@ -1787,53 +1790,80 @@ __global__ void __launch_bounds__(kTriChunk) point_mesh_distance_kernel(const do
                                                                         const double* __restrict__ box, int64_t nt,
                                                                         unsigned long long* __restrict__ out) {
     __shared__ double tri[kTriChunk * 9];
-    __shared__ double rd[kTriChunk];
-    __shared__ int64_t ri[kTriChunk];
+    __shared__ double rd[kSeeds][kTriChunk];
+    __shared__ int64_t ri[kSeeds][kTriChunk];
     const int64_t i = blockIdx.x * (int64_t)kTriChunk + threadIdx.x;
     const bool live = i < n;
     const int64_t pi = live ? perm[i] : 0;
     MV3 p = {0, 0, 0};
     if (live) p = {pts[3 * pi], pts[3 * pi + 1], pts[3 * pi + 2]};
-    const int64_t i0 = perm[blockIdx.x * (int64_t)kTriChunk];
-    const MV3 p0 = {pts[3 * i0], pts[3 * i0 + 1], pts[3 * i0 + 2]};
     const int64_t nch = (nt + kTriChunk - 1) / kTriChunk;
     const int64_t c0 = nch * blockIdx.y / gridDim.y, c1 = nch * (blockIdx.y + 1) / gridDim.y;
-    // nearest chunk box to the block's first point (over all chunks)
-    double bd = 1e300;
-    int64_t bi = 0;
-    for (int64_t ch = threadIdx.x; ch < nch; ch += kTriChunk) {
-        const double d = box_dist(box + 6 * ch, p0);
-        if (d < bd) {
-            bd = d;
-            bi = ch;
-        }
+    // seeds: the chunk box nearest the block's first, middle and last point
+    // (a block's Morton range can straddle a code discontinuity)
+    const int64_t blk0 = blockIdx.x * (int64_t)kTriChunk, nb = n - blk0 < kTriChunk ? n - blk0 : kTriChunk;
+    MV3 q[kSeeds];
+    double bd[kSeeds];
+    int64_t bi[kSeeds];
+#pragma unroll
+    for (int j = 0; j < kSeeds; ++j) {
+        const int64_t qi = perm[blk0 + (nb - 1) * j / (kSeeds - 1)];
+        q[j] = {pts[3 * qi], pts[3 * qi + 1], pts[3 * qi + 2]};
+        bd[j] = 1e300;
+        bi[j] = 0;
     }
-    rd[threadIdx.x] = bd;
-    ri[threadIdx.x] = bi;
+    for (int64_t ch = threadIdx.x; ch < nch; ch += kTriChunk)
+#pragma unroll
+        for (int j = 0; j < kSeeds; ++j) {
+            const double d = box_dist(box + 6 * ch, q[j]);
+            if (d < bd[j]) {
+                bd[j] = d;
+                bi[j] = ch;
+            }
+        }
+#pragma unroll
+    for (int j = 0; j < kSeeds; ++j) {
+        rd[j][threadIdx.x] = bd[j];
+        ri[j][threadIdx.x] = bi[j];
+    }
     __syncthreads();
     for (int o = kTriChunk / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o && (rd[threadIdx.x + o] < rd[threadIdx.x] ||
-                                (rd[threadIdx.x + o] == rd[threadIdx.x] && ri[threadIdx.x + o] < ri[threadIdx.x]))) {
-            rd[threadIdx.x] = rd[threadIdx.x + o];
-            ri[threadIdx.x] = ri[threadIdx.x + o];
-        }
+        if (threadIdx.x < o)
+#pragma unroll
+            for (int j = 0; j < kSeeds; ++j) {
+                const int t = threadIdx.x;
+                if (rd[j][t + o] < rd[j][t] || (rd[j][t + o] == rd[j][t] && ri[j][t + o] < ri[j][t])) {
+                    rd[j][t] = rd[j][t + o];
+                    ri[j][t] = ri[j][t + o];
+                }
+            }
         __syncthreads();
     }
-    const int64_t first = ri[0];
+    int64_t seed[kSeeds];
+#pragma unroll
+    for (int j = 0; j < kSeeds; ++j) seed[j] = ri[j][0];
     double best = 1.7976931348623157e308;  // numeric_limits<double>::max()
-    for (int64_t k = c0 - 1; k < c1; ++k) {
-        const bool seed = k < c0;
-        const int64_t ch = seed ? first : k;
-        if (!seed && k == first) continue;
-        const bool need = live && (seed || box_dist(box + 6 * ch, p) * (1.0 - 1e-9) <= best);
+    for (int64_t k = c0 - kSeeds; k < c1; ++k) {
+        const bool is_seed = k < c0;
+        int64_t ch = k;
+        bool dup = false;
+        if (is_seed) {
+            const int j = (int)(k - (c0 - kSeeds));
+            ch = seed[j];
+            for (int jj = 0; jj < j; ++jj) dup |= seed[jj] == ch;
+        } else {
+            for (int jj = 0; jj < kSeeds; ++jj) dup |= seed[jj] == ch;
+        }
+        if (dup) continue;  // block-uniform
+        const bool need = live && (is_seed || box_dist(box + 6 * ch, p) * (1.0 - 1e-9) <= best);
         if (!__syncthreads_or(need)) continue;
         const int64_t t0 = ch * kTriChunk;
         const int cnt = (int)(nt - t0 < kTriChunk ? nt - t0 : kTriChunk);
-        for (int q = threadIdx.x; q < cnt * 9; q += kTriChunk) tri[q] = soup[9 * t0 + q];
+        for (int qq = threadIdx.x; qq < cnt * 9; qq += kTriChunk) tri[qq] = soup[9 * t0 + qq];
         __syncthreads();
         if (need)
-            for (int q = 0; q < cnt; ++q) {
-                const double* v = tri + 9 * q;
+            for (int qq = 0; qq < cnt; ++qq) {
+                const double* v = tri + 9 * qq;
                 best = fmin(best, point_triangle_distance(p, {v[0], v[1], v[2]}, {v[3], v[4], v[5]},
                                                           {v[6], v[7], v[8]}));
             }
@@ -2150,22 +2180,31 @@ static void mesh_distances(psdf_ctx* c, const double* pts, int64_t n, const doub
             hi[a] = std::max(hi[a], pts[3 * i + a]);
         }
     const double ext = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2], 1e-300});
-    double *d_pts, *d_verts, *d_soup, *d_box, *d_out;
-    int32_t *d_tris, *d_idx, *d_idx2;
-    uint32_t *d_key, *d_key2;
     size_t tmp_bytes = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                        (int32_t*)nullptr, (int32_t*)nullptr, (int)n, 0, 30, s));
-    void* d_tmp;
-    CK(cudaMallocAsync(&d_pts, sizeof(double) * 3 * n, s));
-    CK(cudaMallocAsync(&d_verts, sizeof(double) * 3 * nv, s));
-    CK(cudaMallocAsync(&d_tris, sizeof(int32_t) * 3 * nt, s));
-    CK(cudaMallocAsync(&d_soup, sizeof(double) * 9 * nt, s));
-    CK(cudaMallocAsync(&d_box, sizeof(double) * 6 * nch, s));
-    CK(cudaMallocAsync(&d_out, sizeof(double) * n, s));
-    CK(cudaMallocAsync(&d_key, sizeof(uint32_t) * 2 * n, s));
-    CK(cudaMallocAsync(&d_idx, sizeof(int32_t) * 2 * n, s));
-    CK(cudaMallocAsync(&d_tmp, std::max<size_t>(tmp_bytes, 1), s));
+    // one grow-only arena: points | verts | soup | boxes | out | tris | keys | idx | sort temp
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t sz[9] = {al(24 * n), al(24 * nv), al(72 * nt), al(48 * nch), al(8 * n), al(12 * nt),
+                          al(8 * n), al(8 * n), al(std::max<size_t>(tmp_bytes, 1))};
+    size_t off[9], total = 0;
+    for (int k = 0; k < 9; ++k) {
+        off[k] = total;
+        total += sz[k];
+    }
+    ensure_dev(c->d_eval, c->eval_cap, total);
+    uint8_t* base = c->d_eval;
+    double* d_pts = reinterpret_cast<double*>(base + off[0]);
+    double* d_verts = reinterpret_cast<double*>(base + off[1]);
+    double* d_soup = reinterpret_cast<double*>(base + off[2]);
+    double* d_box = reinterpret_cast<double*>(base + off[3]);
+    double* d_out = reinterpret_cast<double*>(base + off[4]);
+    int32_t* d_tris = reinterpret_cast<int32_t*>(base + off[5]);
+    uint32_t* d_key = reinterpret_cast<uint32_t*>(base + off[6]);
+    int32_t* d_idx = reinterpret_cast<int32_t*>(base + off[7]);
+    void* d_tmp = base + off[8];
+    uint32_t* d_key2;
+    int32_t* d_idx2;
     d_key2 = d_key + n;
     d_idx2 = d_idx + n;
     CK(cudaMemcpyAsync(d_pts, pts, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
@@ -2185,9 +2224,6 @@ static void mesh_distances(psdf_ctx* c, const double* pts, int64_t n, const doub
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(out, d_out, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->h_counts, c->d_counts, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    for (void* p : {(void*)d_pts, (void*)d_verts, (void*)d_tris, (void*)d_soup, (void*)d_box, (void*)d_out,
-                    (void*)d_key, (void*)d_idx, d_tmp})
-        CK(cudaFreeAsync(p, s));
     CK(cudaStreamSynchronize(s));
     if (c->h_counts[0]) fail(PSDF_ERR_OUT_OF_RANGE, "triangle vertex index out of range");
 }
