@@ -228,3 +228,26 @@ def test_eval_psnr(ctx, scene):
     assert ctx.eval_psnr(cam, opts, rgb, mask) == 99.0
     with pytest.raises(ValueError, match="shape mismatch"):
         ctx.eval_psnr(cam, opts, gt[:-1], mask)
+
+
+@pytest.mark.parametrize("tau_vox", [300.0, 3000.0])
+def test_render_parity_bench_view(ctx, tau_vox):
+    """Maximum size: a full configs[1] view (1600x1200 = 1.92 M rays) of the
+    512^3 production grid — sample counts (march, early termination, shaded
+    set) identical to the oracle over every ray, colours / alpha / depth
+    within the 1e-4 contract."""
+    from paper_2412_10084_b200 import api
+    g, a = make_scene(res=512, n_s=4, n_a=4, sh_order=4, band=6, radius=0.32)
+    og, sm = oracle_with_f32_smooth(a)
+    _upload(ctx, g, sm)
+    cam = api.make_ring_cameras(2, 1600, height=1200)[1]
+    opts = api.RenderOptions(tau=tau_vox * 512, camera_id=0)
+    rgb, alpha, depth, counts = ctx.render_image(cam, opts)
+    orgb, oalpha, odepth, ocounts = og.render_image(_oracle_cam(cam), _oracle_opts(opts))
+    assert counts["n_rays"] == 1600 * 1200
+    assert (counts["n_marched"], counts["n_extra"], counts["n_shaded"]) == tuple(ocounts[1:4])
+    assert counts["n_marched"] > 10 * counts["n_shaded"] > 0
+    tol = 1e-4
+    assert np.all(np.abs(rgb - orgb) <= tol * np.maximum(np.abs(orgb), 1e-2)), np.abs(rgb - orgb).max()
+    assert np.all(np.abs(alpha - oalpha) <= tol * np.maximum(np.abs(oalpha), 1e-2))
+    assert np.all(np.abs(depth - odepth) <= tol * np.maximum(np.abs(odepth), 1e-2))

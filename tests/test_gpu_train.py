@@ -63,6 +63,14 @@ def test_train_step_parity_production_grid(ctx):
                             size=40, ncam=0, bias=False))
 
 
+def test_train_step_parity_bench_view(ctx):
+    """Maximum size: one configs[1] view (1600x1200 = 1.92 M rays) on the
+    512^3 production grid at the bench's tau — every ray's counts exact,
+    losses / gradients / post-Adam parameters within the contract."""
+    _train_parity(ctx, dict(scene=dict(res=512, n_s=4, n_a=4, sh_order=4, band=6, radius=0.32), tau=300.0,
+                            size=1600, height=1200, n_views=1, batches=[[0]], ncam=0, bias=False))
+
+
 def test_train_step_parity_wave_overflow(monkeypatch):
     """Ray-pass buffers far too small for the batch: the step overflows, Adam
     is skipped on device, the host grows the buffers and redoes the step —
@@ -88,7 +96,7 @@ def _train_parity(ctx, case):
     ctx.train_reset()
     og.train_reset()
     res = case["scene"]["res"]
-    cams = api.make_ring_cameras(4, case["size"])
+    cams = api.make_ring_cameras(case.get("n_views", 4), case["size"], height=case.get("height"))
     ocams = []
     for c in cams:
         oc = RefCamera()
@@ -100,7 +108,7 @@ def _train_parity(ctx, case):
     gts, masks = _views(og, ocams, 5)
     kw = dict(tau=case["tau"] * res, lr_vox=5e-3 / 50, lr_mlp=3e-3 / 50, photo_scale=40.0 / 2,
               use_camera_bias=case["bias"])
-    for step, batch in enumerate([[0, 1], [2, 3]]):
+    for step, batch in enumerate(case.get("batches", [[0, 1], [2, 3]])):
         hp = api.step_params(**kw)
         losses, counts = ctx.train_step([cams[i] for i in batch], [gts[i] for i in batch],
                                         [masks[i] for i in batch], hp)
