@@ -1706,7 +1706,10 @@ __device__ double point_triangle_distance(MV3 p, MV3 a, MV3 b, MV3 c) {
 // Triangle soup (9 doubles per triangle) and one AABB per chunk of kTriChunk
 // consecutive triangles (meshes from marching cubes are emitted cell by cell,
 // so consecutive triangles are spatially coherent and the boxes are tight).
-constexpr int kTriChunk = 128;
+#ifndef PSDF_TRI_CHUNK
+#define PSDF_TRI_CHUNK 64  // A/B 128 / 64 / 32 (profiles/r01/v19_eval_timing.log)
+#endif
+constexpr int kTriChunk = PSDF_TRI_CHUNK;
 constexpr int kSeeds = 3;  // initial-bound chunks per block
 __global__ void __launch_bounds__(kTriChunk) tri_soup_kernel(const double* __restrict__ verts, int64_t nv,
                                                              const int32_t* __restrict__ tris, int64_t nt,
