@@ -97,9 +97,23 @@ struct WaveBufs {
     int e_cap, r_cap, h_cap, k_cap, a_cap;
 };
 
-// Items in the entry / record queues, read on device (clamped to capacity).
-__device__ __forceinline__ int n_entries(const WaveBufs& W) { return (int)min(*(volatile unsigned*)W.counters, (unsigned)W.e_cap); }
-__device__ __forceinline__ int n_records(const WaveBufs& W) { return (int)min(*(volatile unsigned*)(W.counters + 1), (unsigned)W.r_cap); }
+// True when any wave buffer overflowed this pass (the host redoes it).
+__device__ __forceinline__ bool wave_over(const WaveBufs& W) {
+    const volatile unsigned* c = W.counters;
+    return c[0] > (unsigned)W.e_cap || c[1] > (unsigned)W.r_cap || c[2] > (unsigned)W.h_cap ||
+           c[3] > (unsigned)W.k_cap || c[4] > (unsigned)W.a_cap;
+}
+
+// Items in the entry / record queues, read on device by the kernels after the
+// march.  An overflowed pass is redone, and its queues can hold allocated but
+// unwritten slots (a record whose entry overflowed), so after an overflow the
+// downstream kernels see empty queues.
+__device__ __forceinline__ int n_entries(const WaveBufs& W) {
+    return wave_over(W) ? 0 : (int)min(*(volatile unsigned*)W.counters, (unsigned)W.e_cap);
+}
+__device__ __forceinline__ int n_records(const WaveBufs& W) {
+    return wave_over(W) ? 0 : (int)min(*(volatile unsigned*)(W.counters + 1), (unsigned)W.r_cap);
+}
 
 // Warp-aggregated slot allocation inside divergent code.
 __device__ __forceinline__ int warp_alloc(unsigned* counter, bool want, int lane) {
@@ -650,12 +664,7 @@ __device__ __forceinline__ const ViewDev& entry_view(const RayPassParams& P, con
 
 // 1 in *flag when any wave buffer overflowed this pass (the step is redone).
 __global__ void wave_overflow_kernel(WaveBufs W, unsigned long long* flag) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        const unsigned* c = W.counters;
-        const bool over = c[0] > (unsigned)W.e_cap || c[1] > (unsigned)W.r_cap || c[2] > (unsigned)W.h_cap ||
-                          c[3] > (unsigned)W.k_cap || c[4] > (unsigned)W.a_cap;
-        *flag = over ? 1ull : 0ull;
-    }
+    if (threadIdx.x == 0 && blockIdx.x == 0) *flag = wave_over(W) ? 1ull : 0ull;
 }
 
 // Shading records grouped by tile (K2b / K2e order: decode gathers and the

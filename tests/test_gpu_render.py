@@ -251,3 +251,18 @@ def test_render_parity_bench_view(ctx, tau_vox):
     assert np.all(np.abs(rgb - orgb) <= tol * np.maximum(np.abs(orgb), 1e-2)), np.abs(rgb - orgb).max()
     assert np.all(np.abs(alpha - oalpha) <= tol * np.maximum(np.abs(oalpha), 1e-2))
     assert np.all(np.abs(depth - odepth) <= tol * np.maximum(np.abs(odepth), 1e-2))
+
+
+def test_render_parity_bench_view_after_overflow(monkeypatch):
+    """Regression: a context whose ray-pass buffers were sized for tiny passes
+    (PSDF_WAVE_INIT) renders a full 1600x1200 view — the first pass overflows
+    by orders of magnitude (records allocated past an overflowed entry stay
+    unwritten), the kernels after the march must ignore its queues, and the
+    redo matches the oracle."""
+    from paper_2412_10084_b200 import api
+    monkeypatch.setenv("PSDF_WAVE_INIT", "64")
+    c = api.Context(0)
+    try:
+        test_render_parity_bench_view(c, 300.0)
+    finally:
+        c.close()
