@@ -2171,7 +2171,8 @@ int psdf_eval_psnr(psdf_ctx* c, const psdf_camera* cam, const psdf_render_opts* 
 static void mesh_distances(psdf_ctx* c, const double* pts, int64_t n, const double* verts, int64_t nv,
                            const int32_t* tris, int64_t nt, double* out) {
     if (nt <= 0) fail(PSDF_ERR_INVALID_ARGUMENT, "MeshDistance: empty mesh");  // metrics.cpp:49
-    if (!verts || !tris || nv <= 0 || (n > 0 && (!pts || !out))) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
+    if (!verts || !tris || (n > 0 && (!pts || !out))) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
+    if (nv <= 0) fail(PSDF_ERR_OUT_OF_RANGE, "triangle vertex index out of range");  // no vertex to index
     if (n == 0) return;
     if (n > INT32_MAX || nt > INT32_MAX) fail(PSDF_ERR_INVALID_ARGUMENT, "too many points or triangles");
     cudaStream_t s = c->stream;
