@@ -420,11 +420,11 @@ int blocks_per_sm(const void* fn, size_t smem) {
 // G^T fold: dst += G * src (src filled with 0 outside allocated tiles).
 void launch_fold(psdf_ctx* c, const float* src, float* dst) {
     if (c->desc.T == 0) return;
-    static bool attr = false;
-    if (!attr) {
+    static uint64_t attr = 0;  // per device: function attributes are per context
+    if (!((attr >> c->device) & 1ull)) {
         CK(cudaFuncSetAttribute(smooth_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kFoldSmem));
-        attr = true;
+        attr |= 1ull << c->device;
     }
     smooth_fold_kernel<<<c->desc.T, PSDF_FOLD_THREADS, kFoldSmem, c->stream>>>(c->view(), src, 0.f, dst, 1,
                                                                  gaussian_taps());
@@ -443,11 +443,11 @@ void fill_apron(psdf_ctx* c) {
 // SparseGrid::smooth_all (grid.cpp:247-250) + apron + brick minima, one pass.
 void smooth_all(psdf_ctx* c) {
     if (c->desc.T == 0) return;
-    static bool attr = false;
-    if (!attr) {
+    static uint64_t attr = 0;  // per device: function attributes are per context
+    if (!((attr >> c->device) & 1ull)) {
         CK(cudaFuncSetAttribute(smooth_apron_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kSmoothApronSmem));
-        attr = true;
+        attr |= 1ull << c->device;
     }
     smooth_apron_kernel<<<c->desc.T, PSDF_SMOOTH_THREADS, kSmoothApronSmem, c->stream>>>(
         c->view(), c->d_params + c->off_raw, (float)(c->desc.far_field_voxels * c->desc.voxel_size),
@@ -582,8 +582,8 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     const size_t smem_f = render_smem_bytes<NS, NA>();
     const size_t smem_b = shade_bwd_smem_bytes<NS, NA>();
     const size_t smem_bits = sizeof(uint32_t) * P.bits_sm_words;
-    static bool attr = false;
-    if (!attr) {
+    static uint64_t attr = 0;  // per device: function attributes are per context
+    if (!((attr >> c->device) & 1ull)) {
         CK(cudaFuncSetAttribute(shade_fwd_kernel<NS, NA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
         CK(cudaFuncSetAttribute(shade_fwd_kernel<NS, NA, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
         CK(cudaFuncSetAttribute(shade_bwd_kernel<NS, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
@@ -591,7 +591,7 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
                                 (int)(sizeof(uint32_t) * kMaxSmemBitWords)));
         CK(cudaFuncSetAttribute(march_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(sizeof(uint32_t) * kMaxSmemBitWords)));
-        attr = true;
+        attr |= 1ull << c->device;
     }
     const int per_sm_s = blocks_per_sm((const void*)march_scan_kernel, smem_bits);
     const int64_t grid_s = std::max<int64_t>(1, std::min<int64_t>((n_work + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
@@ -867,11 +867,11 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
             sl = c->side_stream;
         }
         if (t1 > t0) {
-            static bool attr = false;
-            if (!attr) {
+            static uint64_t attr = 0;  // per device: function attributes are per context
+            if (!((attr >> c->device) & 1ull)) {
                 CK(cudaFuncSetAttribute(loss_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)kLossGridSmem));
-                attr = true;
+                attr |= 1ull << c->device;
             }
             loss_grid_kernel<<<t1 - t0, LG_THREADS, kLossGridSmem, sl>>>(
                 g, c->d_params + c->off_raw, t0, (float)hp->l_sdf, (float)hp->l_eik, (float)hp->l_norm,
