@@ -1787,7 +1787,13 @@ __device__ __forceinline__ double box_dist(const double* bx, MV3 p) {  // metric
 // f64 bit patterns (non-negative doubles order like their bits; out starts at
 // all-ones).  NaN distances (degenerate triangles) never win, as with
 // std::min(best, d).
-__global__ void __launch_bounds__(kTriChunk) point_mesh_distance_kernel(const double* __restrict__ pts, int64_t n,
+#ifndef PSDF_PMD_MINB
+#define PSDF_PMD_MINB 1
+#endif
+#ifndef PSDF_PMD_BLOCKS_PER_SM
+#define PSDF_PMD_BLOCKS_PER_SM 16
+#endif
+__global__ void __launch_bounds__(kTriChunk, PSDF_PMD_MINB) point_mesh_distance_kernel(const double* __restrict__ pts, int64_t n,
                                                                         const int32_t* __restrict__ perm,
                                                                         const double* __restrict__ soup,
                                                                         const double* __restrict__ box, int64_t nt,
@@ -2221,7 +2227,7 @@ static void mesh_distances(psdf_ctx* c, const double* pts, int64_t n, const doub
     tri_soup_kernel<<<(unsigned)nch, kTriChunk, 0, s>>>(d_verts, nv, d_tris, nt, d_soup, d_box, c->d_counts);
     // split the chunk range over blockIdx.y until the grid holds ~16 blocks per SM
     const int64_t nblk = (n + kTriChunk - 1) / kTriChunk;
-    const int64_t split = std::max<int64_t>(1, std::min<int64_t>({64, nch, (16 * c->sm_count + nblk - 1) / nblk}));
+    const int64_t split = std::max<int64_t>(1, std::min<int64_t>({64, nch, (PSDF_PMD_BLOCKS_PER_SM * c->sm_count + nblk - 1) / nblk}));
     CK(cudaMemsetAsync(d_out, 0xff, sizeof(double) * n, s));
     point_mesh_distance_kernel<<<dim3((unsigned)nblk, (unsigned)split), kTriChunk, 0, s>>>(
         d_pts, n, d_idx2, d_soup, d_box, nt, reinterpret_cast<unsigned long long*>(d_out));
