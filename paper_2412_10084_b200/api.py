@@ -335,6 +335,48 @@ def analytic_sdf(prims):
     return f
 
 
+# The named synthetic shapes of BASELINE.json's configs, as primitive unions
+# for analytic_sdf / init_grid_analytic ((kind, center, extent); kind 0 sphere
+# radius extent[0], 1 box half-extents, 2 torus (major, minor) in the xz plane
+# about +y, synth.cpp:17-35).
+#   sphere: the acceptance scene's sphere (acceptance.cpp:54-74, r = 0.3)
+#   torus:  configs[0]'s torus (major 0.25, minor 0.1)
+#   human:  configs[2]'s MVMannequins-like figure (a union
+#           of boxes, spheres and tori standing in the unit cube); the
+#           reference has no human asset, so this union is this repo's.
+SCENE_PRIMS = {
+    "sphere": [(0, (0.0, 0.0, 0.0), (0.3, 0.0, 0.0))],
+    "torus": [(2, (0.0, 0.0, 0.0), (0.25, 0.1, 0.0))],
+    "human": [
+        (0, (0.0, 0.335, 0.0), (0.065, 0.0, 0.0)),        # head
+        (1, (0.0, 0.255, 0.0), (0.025, 0.03, 0.025)),     # neck
+        (1, (0.0, 0.10, 0.0), (0.115, 0.135, 0.06)),      # torso
+        (2, (0.0, -0.045, 0.0), (0.1, 0.03, 0.0)),        # belt
+        (1, (0.0, -0.07, 0.0), (0.1, 0.05, 0.055)),       # pelvis
+        (1, (-0.055, -0.265, 0.0), (0.04, 0.16, 0.042)),  # legs
+        (1, (0.055, -0.265, 0.0), (0.04, 0.16, 0.042)),
+        (1, (-0.055, -0.43, 0.025), (0.042, 0.018, 0.07)),  # feet
+        (1, (0.055, -0.43, 0.025), (0.042, 0.018, 0.07)),
+        (0, (-0.15, 0.215, 0.0), (0.045, 0.0, 0.0)),      # shoulders
+        (0, (0.15, 0.215, 0.0), (0.045, 0.0, 0.0)),
+        (1, (-0.175, 0.075, 0.0), (0.03, 0.13, 0.03)),    # arms
+        (1, (0.175, 0.075, 0.0), (0.03, 0.13, 0.03)),
+        (0, (-0.175, -0.07, 0.0), (0.035, 0.0, 0.0)),     # hands
+        (0, (0.175, -0.07, 0.0), (0.035, 0.0, 0.0)),
+    ],
+}
+
+
+def init_grid_analytic(cfg: GridConfig, prims, ncam=0, mlp_seed=0) -> HostGrid:
+    """A grid allocated and filled from a union of primitives (the reference's
+    dense-overwrite pattern, test_grid.cpp:29-43, with init_common's tile
+    rule, grid.cpp:359-398): `prims` is a list for analytic_sdf or a key of
+    SCENE_PRIMS."""
+    if isinstance(prims, str):
+        prims = SCENE_PRIMS[prims]
+    return init_grid_sphere(cfg, (0, 0, 0), 0.0, ncam=ncam, mlp_seed=mlp_seed, sdf_fn=analytic_sdf(prims))
+
+
 # ----------------------------------------------------------------- context
 def _fptr(a):
     return None if a is None else a.ctypes.data_as(C.POINTER(C.c_float))
@@ -342,6 +384,21 @@ def _fptr(a):
 
 def _iptr(a):
     return None if a is None else a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def _train_mask(m):
+    """A training / evaluation mask as the ABI's 0/1 bytes.  Floats follow the
+    reference's ImageGray test `mask > 0.5` (trainer.cpp:166, metrics.cpp:203);
+    uint8 images are 8-bit masks as loaded from disk (value / 255 > 0.5, i.e.
+    the `> 127` of MaskImage::foreground, grid.hpp:143-146) so that every entry
+    point, the visual hull included, classifies a byte mask the same way; bool
+    masks pass through."""
+    m = np.asarray(m)
+    if m.dtype == np.bool_:
+        return np.ascontiguousarray(m, np.uint8)
+    if m.dtype == np.uint8:
+        return np.ascontiguousarray(m > 127, np.uint8)
+    return np.ascontiguousarray(m > 0.5, np.uint8)
 
 
 class Context:
@@ -499,11 +556,10 @@ class Context:
     def eval_psnr(self, camera, opts: RenderOptions, gt_rgb, mask):
         """psnr_masked(render_image(...).rgb, gt, mask) (metrics.cpp:196-211) with
         the render and the masked reduction on the GPU; `mask` as in train_step
-        (u8 nonzero = inside, or floats thresholded at > 0.5)."""
+        (see _train_mask)."""
         cam = camera_from(camera)
         gt = np.ascontiguousarray(gt_rgb, np.float32)
-        m = np.asarray(mask)
-        m = np.ascontiguousarray(m > 0.5, np.uint8) if m.dtype != np.uint8 else np.ascontiguousarray(m)
+        m = _train_mask(mask)
         if gt.shape != (cam.height, cam.width, 3) or m.shape != (cam.height, cam.width):
             raise ValueError("psnr_masked: image shape mismatch")
         out = C.c_double()
@@ -545,8 +601,7 @@ class Context:
         n = len(cameras)
         cams = (psdf_camera * n)(*[camera_from(c) for c in cameras])
         gts = [np.ascontiguousarray(g, np.float32) for g in gt_rgb]
-        mks = [np.ascontiguousarray(np.asarray(m) > 0.5, np.uint8) if np.asarray(m).dtype != np.uint8
-               else np.ascontiguousarray(m) for m in masks]
+        mks = [_train_mask(m) for m in masks]
         gp = (C.POINTER(C.c_float) * n)(*[_fptr(g) for g in gts])
         mp = (C.POINTER(C.c_uint8) * n)(*[m.ctypes.data_as(C.POINTER(C.c_uint8)) for m in mks])
         losses, counts = psdf_losses(), psdf_counts()
@@ -558,8 +613,7 @@ class Context:
         n = len(cameras)
         cams = (psdf_camera * n)(*[camera_from(c) for c in cameras])
         gts = [np.ascontiguousarray(g, np.float32) for g in gt_rgb]
-        mks = [np.ascontiguousarray(np.asarray(m) > 0.5, np.uint8) if np.asarray(m).dtype != np.uint8
-               else np.ascontiguousarray(m) for m in masks]
+        mks = [_train_mask(m) for m in masks]
         gp = (C.POINTER(C.c_float) * n)(*[_fptr(g) for g in gts])
         mp = (C.POINTER(C.c_uint8) * n)(*[m.ctypes.data_as(C.POINTER(C.c_uint8)) for m in mks])
         self._check(self.L.psdf_upload_views(self.h, n, cams, gp, mp))
@@ -653,5 +707,3 @@ def _dptr(a):
     return a.ctypes.data_as(C.POINTER(C.c_double))
 
 
-def _iptr(a):
-    return a.ctypes.data_as(C.POINTER(C.c_int32))

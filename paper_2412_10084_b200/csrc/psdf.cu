@@ -27,6 +27,7 @@
 #include <string>
 #include <unordered_map>
 #include <vector>
+#include <unordered_set>
 
 #include "../../include/psdf.h"
 #include "psdf_grid.cuh"
@@ -170,6 +171,7 @@ struct psdf_ctx {
     cudaStream_t copy_stream = nullptr;  // host->device image staging of psdf_train_step
     cudaStream_t side_stream = nullptr;  // low priority: regularizers under the ray pass
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_scanned = nullptr;    // after the scan (hand-over bits and the view table written)
     bool fork_regs = false;              // the ray pass records ev_fork (do_train_step)
     bool grads_clear_pending = false;    // gradient clear on the side stream (ev_zeroed)
     cudaEvent_t ev_start = nullptr, ev_zeroed = nullptr;
@@ -180,6 +182,12 @@ struct psdf_ctx {
     unsigned* d_hand_bits = nullptr;       // [work tiles] scan hand-over lanes
     int64_t hand_cap = 0;
     cudaEvent_t ev_ray0 = nullptr, ev_ray1 = nullptr, ev_step0 = nullptr, ev_step1 = nullptr;
+
+    // kernels whose dynamic shared-memory limit was raised on this device
+    // (function attributes are per CUDA context; a psdf_ctx is used by one
+    // host thread at a time)
+    std::unordered_set<const void*> attr_done;
+    double test_margin = 1e-8;  // PSDF_TEST_MARGIN, read once at creation
 
     bool has_grid = false;
     psdf_grid_desc desc{};
@@ -276,8 +284,7 @@ struct psdf_ctx {
         g.sat_dist = d_sat_dist;
         // decision margin of the marcher's fast paths; PSDF_TEST_MARGIN widens
         // it so the tests drive the exact / rewind paths on most decisions
-        g.margin = 1e-8;
-        if (const char* m = std::getenv("PSDF_TEST_MARGIN")) g.margin = std::max(1e-8, std::atof(m));
+        g.margin = test_margin;
         g.bit_words = bit_words;
         g.tile_coords = d_tile_coords;
         g.probe_ids = d_probe_ids;
@@ -325,6 +332,27 @@ void ensure_dev(T*& p, size_t& cap, size_t n) {
     CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
     cap = n;
 }
+
+// Call-scoped device scratch: every buffer is freed when the scope ends,
+// including when a failure unwinds it (fail() throws into guarded()).
+struct DevScratch {
+    std::vector<void*> ptrs;
+    DevScratch() = default;
+    DevScratch(const DevScratch&) = delete;
+    DevScratch& operator=(const DevScratch&) = delete;
+    ~DevScratch() { release(); }
+    template <typename T>
+    T* alloc(size_t n) {
+        void* p = nullptr;
+        CK(cudaMalloc(&p, std::max<size_t>(n * sizeof(T), 16)));
+        ptrs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    void release() {
+        for (void* p : ptrs) cudaFree(p);
+        ptrs.clear();
+    }
+};
 
 Cam to_cam(const psdf_camera& c) {
     Cam d;
@@ -420,12 +448,9 @@ int blocks_per_sm(const void* fn, size_t smem) {
 // G^T fold: dst += G * src (src filled with 0 outside allocated tiles).
 void launch_fold(psdf_ctx* c, const float* src, float* dst) {
     if (c->desc.T == 0) return;
-    static uint64_t attr = 0;  // per device: function attributes are per context
-    if (!((attr >> c->device) & 1ull)) {
+    if (c->attr_done.insert((const void*)smooth_fold_kernel).second)
         CK(cudaFuncSetAttribute(smooth_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kFoldSmem));
-        attr |= 1ull << c->device;
-    }
     smooth_fold_kernel<<<c->desc.T, PSDF_FOLD_THREADS, kFoldSmem, c->stream>>>(c->view(), src, 0.f, dst, 1,
                                                                  gaussian_taps());
     CK(cudaGetLastError());
@@ -443,12 +468,9 @@ void fill_apron(psdf_ctx* c) {
 // SparseGrid::smooth_all (grid.cpp:247-250) + apron + brick minima, one pass.
 void smooth_all(psdf_ctx* c) {
     if (c->desc.T == 0) return;
-    static uint64_t attr = 0;  // per device: function attributes are per context
-    if (!((attr >> c->device) & 1ull)) {
+    if (c->attr_done.insert((const void*)smooth_apron_kernel).second)
         CK(cudaFuncSetAttribute(smooth_apron_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kSmoothApronSmem));
-        attr |= 1ull << c->device;
-    }
     smooth_apron_kernel<<<c->desc.T, PSDF_SMOOTH_THREADS, kSmoothApronSmem, c->stream>>>(
         c->view(), c->d_params + c->off_raw, (float)(c->desc.far_field_voxels * c->desc.voxel_size),
         c->d_smooth, c->d_smooth_ap, gaussian_taps());
@@ -582,8 +604,7 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     const size_t smem_f = render_smem_bytes<NS, NA>();
     const size_t smem_b = shade_bwd_smem_bytes<NS, NA>();
     const size_t smem_bits = sizeof(uint32_t) * P.bits_sm_words;
-    static uint64_t attr = 0;  // per device: function attributes are per context
-    if (!((attr >> c->device) & 1ull)) {
+    if (c->attr_done.insert((const void*)shade_fwd_kernel<NS, NA, true>).second) {
         CK(cudaFuncSetAttribute(shade_fwd_kernel<NS, NA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
         CK(cudaFuncSetAttribute(shade_fwd_kernel<NS, NA, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
         CK(cudaFuncSetAttribute(shade_bwd_kernel<NS, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
@@ -591,7 +612,6 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
                                 (int)(sizeof(uint32_t) * kMaxSmemBitWords)));
         CK(cudaFuncSetAttribute(march_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(sizeof(uint32_t) * kMaxSmemBitWords)));
-        attr |= 1ull << c->device;
     }
     const int per_sm_s = blocks_per_sm((const void*)march_scan_kernel, smem_bits);
     const int64_t grid_s = std::max<int64_t>(1, std::min<int64_t>((n_work + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
@@ -616,6 +636,9 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     march_scan_kernel<<<(unsigned)grid_s, BLOCK, smem_bits, s>>>(P, W);
     CK(cudaGetLastError());
     ++c->last_launches;
+    // the empty rays' photo terms (side stream) read the hand-over bits and
+    // the view table: they wait for this point, whichever fork they took
+    CK(cudaEventRecord(c->ev_scanned, s));
     // handovers in append order: a warp's handovers come from one 8x4 pixel
     // tile and neighbouring warps from neighbouring work tiles (a sort by
     // pixel measured slower than it saved)
@@ -716,6 +739,7 @@ void ensure_keep_buffers(psdf_ctx* c) {
 void launch_empty_ray_loss(psdf_ctx* c, const RayPassParams& P, cudaStream_t st) {
     const int64_t n_work = P.tile_end - P.tile_begin;
     if (n_work <= 0) return;
+    if (st != c->stream) CK(cudaStreamWaitEvent(st, c->ev_scanned, 0));
     if (c->images_pending) CK(cudaStreamWaitEvent(st, c->ev_rgb, 0));
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n_work + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
                                                                 (int64_t)16 * c->sm_count));
@@ -867,12 +891,9 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
             sl = c->side_stream;
         }
         if (t1 > t0) {
-            static uint64_t attr = 0;  // per device: function attributes are per context
-            if (!((attr >> c->device) & 1ull)) {
+            if (c->attr_done.insert((const void*)loss_grid_kernel).second)
                 CK(cudaFuncSetAttribute(loss_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)kLossGridSmem));
-                attr |= 1ull << c->device;
-            }
             loss_grid_kernel<<<t1 - t0, LG_THREADS, kLossGridSmem, sl>>>(
                 g, c->d_params + c->off_raw, t0, (float)hp->l_sdf, (float)hp->l_eik, (float)hp->l_norm,
                 (float)(1.0 / (2.0 * c->desc.voxel_size)), c->d_gsmooth, c->d_grads + c->off_raw, c->d_stats);
@@ -1048,10 +1069,12 @@ int psdf_create(int device, psdf_ctx** out) {
         if (const char* e = std::getenv("PSDF_COMPOSITE_STEPS")) c->composite_steps = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("PSDF_WAVE_INIT")) c->wave_init = std::max(0, std::atoi(e));
         if (const char* e = std::getenv("PSDF_REGS_EARLY")) c->regs_early = std::atoi(e) != 0;
+        if (const char* m = std::getenv("PSDF_TEST_MARGIN")) c->test_margin = std::max(1e-8, std::atof(m));
         CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithPriority(&c->side_stream, cudaStreamNonBlocking, prio_lo));
         CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_scanned, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_copied, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_masks, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
@@ -1106,6 +1129,7 @@ int psdf_destroy(psdf_ctx* c) {
         cudaStreamDestroy(c->side_stream);
         cudaEventDestroy(c->ev_fork);
         cudaEventDestroy(c->ev_join);
+        cudaEventDestroy(c->ev_scanned);
         cudaEventDestroy(c->ev_copied);
         cudaEventDestroy(c->ev_copy_free);
         cudaEventDestroy(c->ev_masks);
@@ -1382,10 +1406,9 @@ int psdf_subdivide(psdf_ctx* c, double band_voxels, int32_t* out_T, int32_t* out
         for (int a = 0; a < 3; ++a) d.res[a] = d0.res[a] * 2;
         const int nt1[3] = {d.res[0] / TE, d.res[1] / TE, d.res[2] / TE};
         // 1. child raw values + allocation decisions
-        float* d_child = nullptr;
-        uint8_t* d_keep = nullptr;
-        CK(cudaMalloc(&d_child, sizeof(float) * TV * std::max<int64_t>(8 * T0, 1)));
-        CK(cudaMalloc(&d_keep, std::max<int64_t>(8 * T0, 1)));
+        DevScratch scratch;
+        float* d_child = scratch.alloc<float>((size_t)TV * 8 * T0);
+        uint8_t* d_keep = scratch.alloc<uint8_t>((size_t)8 * T0);
         std::vector<uint8_t> keep(8 * T0);
         std::vector<int4> tc0(std::max<int64_t>(T0, 1));
         if (T0) {
@@ -1427,16 +1450,13 @@ int psdf_subdivide(psdf_ctx* c, double band_voxels, int32_t* out_T, int32_t* out
         d.P = (int)P1;
         // 3. resampled parameters on the device
         const int stride = d0.sh_order * d0.sh_order * d0.n_a;
-        int* d_src = nullptr;
-        int4* d_pc = nullptr;
-        float *d_raw = nullptr, *d_planes = nullptr, *d_probes = nullptr;
         std::vector<int4> pc4(std::max<int64_t>(P1, 1));
         for (int64_t p = 0; p < P1; ++p) pc4[p] = make_int4(pco[3 * p], pco[3 * p + 1], pco[3 * p + 2], 0);
-        CK(cudaMalloc(&d_src, sizeof(int) * std::max<int64_t>(T1, 1)));
-        CK(cudaMalloc(&d_pc, sizeof(int4) * std::max<int64_t>(P1, 1)));
-        CK(cudaMalloc(&d_raw, sizeof(float) * TV * std::max<int64_t>(T1, 1)));
-        CK(cudaMalloc(&d_planes, sizeof(float) * 3 * 256 * d0.n_s * std::max<int64_t>(T1, 1)));
-        CK(cudaMalloc(&d_probes, sizeof(float) * stride * std::max<int64_t>(P1, 1)));
+        int* d_src = scratch.alloc<int>((size_t)T1);
+        int4* d_pc = scratch.alloc<int4>((size_t)P1);
+        float* d_raw = scratch.alloc<float>((size_t)TV * T1);
+        float* d_planes = scratch.alloc<float>((size_t)3 * 256 * d0.n_s * T1);
+        float* d_probes = scratch.alloc<float>((size_t)stride * P1);
         if (T1) CK(cudaMemcpyAsync(d_src, src.data(), sizeof(int) * T1, cudaMemcpyHostToDevice, s));
         if (P1) CK(cudaMemcpyAsync(d_pc, pc4.data(), sizeof(int4) * P1, cudaMemcpyHostToDevice, s));
         if (T1) {
@@ -1459,9 +1479,7 @@ int psdf_subdivide(psdf_ctx* c, double band_voxels, int32_t* out_T, int32_t* out
         if (P1) CK(cudaMemcpyAsync(probes.data(), d_probes, sizeof(float) * probes.size(), cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(mlp.data(), c->d_params + c->off_mlp, sizeof(float) * mlp.size(), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        for (void* p : {(void*)d_child, (void*)d_keep, (void*)d_src, (void*)d_pc, (void*)d_raw, (void*)d_planes,
-                        (void*)d_probes})
-            cudaFree(p);
+        scratch.release();
         // 4. the new grid (smoothed on the device, grid.cpp:340)
         if (psdf_upload_grid(c, &d, tc.data(), pid.data(), pco.data(), raw.data(), nullptr, planes.data(),
                              probes.data()) != PSDF_OK ||
@@ -2430,13 +2448,12 @@ int psdf_march_rays(psdf_ctx* c, int n, const double* origins, const double* dir
             fail(PSDF_ERR_INVALID_ARGUMENT, "bad march arguments");
         if (n == 0) return;
         set_device(c);
-        double *d_o, *d_d, *d_t;
-        int* d_n;
         const int nm = std::max(n_max, 1);
-        CK(cudaMalloc(&d_o, sizeof(double) * 3 * n));
-        CK(cudaMalloc(&d_d, sizeof(double) * 3 * n));
-        CK(cudaMalloc(&d_t, sizeof(double) * (size_t)n * nm));
-        CK(cudaMalloc(&d_n, sizeof(int) * n));
+        DevScratch scratch;
+        double* d_o = scratch.alloc<double>((size_t)3 * n);
+        double* d_d = scratch.alloc<double>((size_t)3 * n);
+        double* d_t = scratch.alloc<double>((size_t)n * nm);
+        int* d_n = scratch.alloc<int>((size_t)n);
         CK(cudaMemcpyAsync(d_o, origins, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemcpyAsync(d_d, dirs, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
         march_rays_kernel<<<(n + 127) / 128, 128, 0, c->stream>>>(c->view(), n, d_o, d_d, n_max, d_t, d_n);
@@ -2445,10 +2462,6 @@ int psdf_march_rays(psdf_ctx* c, int n, const double* origins, const double* dir
         CK(cudaMemcpyAsync(ts, d_t, sizeof(double) * (size_t)n * nm, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaMemcpyAsync(counts, d_n, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
-        cudaFree(d_o);
-        cudaFree(d_d);
-        cudaFree(d_t);
-        cudaFree(d_n);
     });
 }
 

@@ -45,6 +45,50 @@ def oracle_with_f32_smooth(a):
     return OracleGrid(b, smooth=True), sm
 
 
+def check_grads(got, want, what, tol=1e-3, kink_outliers=False):
+    """The gradient contract (north_star 1e-3; SURVEY hard part 6): per tensor
+    ||d||_2 <= tol ||g||_2 and element-wise |d| <= tol max|g|.
+
+    kink_outliers: the decoder runs in fp32 and the oracle in f64, so a
+    ReLU mask (decoder.cpp:93-101), the n.v clamp (decoder.cpp:57) or a plane
+    tap boundary can be decided differently for a sample whose pre-activation
+    is within fp32 rounding of the kink; that one sample's feature gradient
+    then differs by O(its own size).  Over ~10^6 shaded samples (the bench
+    step) a few such samples occur (measured: 20 of 3.5 M plane entries, all
+    in one tile, identical on every GPU run and in the serialised and
+    overlapped schedules, profiles/r02/prod_diag.log).  With this flag up to
+    max(32, 1e-5 n) entries may exceed the element-wise bound, each by at
+    most 50x; the L2 bound is unchanged."""
+    for k in ("raw", "smooth", "planes", "probes", "mlp"):
+        g = np.asarray(got[k], np.float64)
+        w = np.asarray(want[k], np.float64)
+        scale = np.abs(w).max()
+        if scale == 0:
+            assert np.abs(g).max() == 0, (what, k)
+            continue
+        assert rel_l2(g, w) <= tol, (what, k, rel_l2(g, w))
+        d = np.abs(g - w)
+        if not kink_outliers:
+            assert d.max() <= tol * scale, (what, k, d.max() / scale)
+        else:
+            n_out = int((d > tol * scale).sum())
+            assert n_out <= max(32, 1e-5 * d.size), (what, k, n_out)
+            assert d.max() <= 50 * tol * scale, (what, k, d.max() / scale)
+
+
+def check_same_schedule(got, ref, what, tol=2e-5):
+    """Two GPU runs of the same step (e.g. the overlapped production schedule
+    against the serialised one): only the fp32 atomic order may differ, so
+    every entry agrees to tol x max (measured 1e-7 .. 7e-7 at the bench
+    step); a missing stream-ordering edge would clear or double-count whole
+    blocks of gradient and fail this by orders of magnitude."""
+    for k in ("raw", "smooth", "planes", "probes", "mlp"):
+        g = np.asarray(got[k], np.float64)
+        r = np.asarray(ref[k], np.float64)
+        scale = max(np.abs(r).max(), 1e-30)
+        assert np.abs(g - r).max() <= tol * scale, (what, k, np.abs(g - r).max() / scale)
+
+
 def rel_l2(x, y):
     x = np.asarray(x, np.float64).ravel()
     y = np.asarray(y, np.float64).ravel()
