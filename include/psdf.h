@@ -238,6 +238,12 @@ int psdf_pixel_dirs(const psdf_camera* cam, double* out);
 #define PSDF_UNIQUE_ID_BYTES 128
 int psdf_comm_unique_id(void* out /* PSDF_UNIQUE_ID_BYTES */);
 int psdf_comm_init(psdf_ctx* ctx, const void* unique_id, int rank, int world_size);
+/* Test hook: act as `rank` of `world_size` WITHOUT a communicator — the
+ * step processes only this rank's slice (work tiles, regularizer tiles /
+ * probes, and psdf_train_step copies only the slice's pixel rows) and skips
+ * the all-reduce, so the stage-1 gradients of the N slices sum to the
+ * one-rank gradients (tests/test_gpu_shard.py). */
+int psdf_debug_set_shard(psdf_ctx* ctx, int rank, int world_size);
 
 /* ---- timing / introspection ------------------------------------------------ */
 /* Device time (ms) of the last call's dominant kernel (the fused ray-pass

@@ -15,6 +15,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <chrono>
 #include <cstring>
 #include <exception>
 #include <random>
@@ -97,6 +98,11 @@ struct RefScene {
     bool opt_ready = false;
     GradBuffers gb_raypass; // gradients after the ray pass (before regularizers)
     GradBuffers gb_final;   // gradients handed to Adam
+    // per-thread gradient replicas kept across steps and cleared per step, as
+    // train() keeps them per LOD (trainer.cpp:115-117, 136)
+    std::vector<GradBuffers> gbs;
+    bool keep_grads = true; // copy gb_raypass / gb_final (parity tests; off when timing)
+    double phase_ms[3] = {0, 0, 0}; // last step: clear + ray pass + reduce | regularizers + fold | Adam + smoothing
 };
 
 extern "C" {
@@ -732,6 +738,16 @@ void ref_gt_fold(const RefScene* s, const double* staged, const double* raw_in, 
         std::memcpy(raw_out + t * kTileVoxels, gb.raw_sdf[t].data(), kTileVoxels * 8);
 }
 
+// Timing runs: skip the per-step copies of the gradient buffers (parity
+// tests read them through ref_grads).
+void ref_set_keep_grads(RefScene* s, int keep) { s->keep_grads = keep != 0; }
+
+// Phase times of the last ref_train_step (ms): [clear + ray pass + replica
+// reduction, regularizers + G^T fold, Adam + smoothing].
+void ref_last_phase_ms(const RefScene* s, double* out) {
+    for (int i = 0; i < 3; ++i) out[i] = s->phase_ms[i];
+}
+
 void ref_train_reset(RefScene* s) {
     s->opt.init(s->grid, s->mlp);
     s->opt_ready = true;
@@ -754,8 +770,18 @@ int ref_train_step(RefScene* s, int n_views, const RefCamera* cams, const double
         if (threads > 0) omp_set_num_threads(threads);
         n_threads = omp_get_max_threads();
 #endif
-        std::vector<GradBuffers> gbs(n_threads);
-        for (GradBuffers& gb : gbs) gb.init(grid, mlp);
+        // replicas allocated once per thread count / grid (train() allocates
+        // them per LOD, outside its step loop); the per-step clear is timed
+        std::vector<GradBuffers>& gbs = s->gbs;
+        const bool fresh = (int)gbs.size() != n_threads || gbs[0].raw_sdf.size() != grid.tiles.size() ||
+                           gbs[0].probes.size() != grid.probes.size();
+        if (fresh) {
+            gbs.assign(n_threads, GradBuffers{});
+            for (GradBuffers& gb : gbs) gb.init(grid, mlp);
+        }
+        const auto t_begin = std::chrono::steady_clock::now();
+        if (!fresh)
+            for (GradBuffers& gb : gbs) gb.clear();
 
         double photo_plain = 0.0, sq_err = 0.0;
         long mask_px = 0;
@@ -801,7 +827,8 @@ int ref_train_step(RefScene* s, int n_views, const RefCamera* cams, const double
         }
         GradBuffers& gb = gbs[0];
         for (int t = 1; t < n_threads; ++t) gb.add(gbs[t]);
-        s->gb_raypass = gb;
+        if (s->keep_grads) s->gb_raypass = gb;
+        const auto t_ray = std::chrono::steady_clock::now();
 
         const LossResult r_sdf = loss_sdf(grid, grid, hp->l_sdf, &gb);
         const LossResult r_eik = loss_eikonal(grid, grid, hp->l_eik, &gb);
@@ -809,9 +836,16 @@ int ref_train_step(RefScene* s, int n_views, const RefCamera* cams, const double
         const LossResult r_feat = loss_features(grid, grid, hp->l_feat, &gb);
         const LossResult r_probe = loss_probes(grid, hp->l_probe, &gb);
         finalize_smooth_grads(grid, gb);
-        s->gb_final = gb;
+        const auto t_reg = std::chrono::steady_clock::now();
+        if (s->keep_grads) s->gb_final = gb;
+        const auto t_opt = std::chrono::steady_clock::now();
         s->opt.step(grid, mlp, gb, hp->lr_vox, hp->lr_mlp);
         grid.smooth_all();
+        const auto t_end = std::chrono::steady_clock::now();
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        s->phase_ms[0] = ms(t_begin, t_ray);
+        s->phase_ms[1] = ms(t_ray, t_reg);
+        s->phase_ms[2] = ms(t_opt, t_end);
 
         const double mse = mask_px > 0 ? sq_err / mask_px : 0.0;
         const double psnr = mse > 1e-10 ? 10.0 * std::log10(1.0 / mse) : 99.0;

@@ -140,6 +140,8 @@ def reflib():
     L.ref_regularizer.argtypes = [C.c_void_p, C.c_int, C.c_double, _dp, _dp, _dp, _dp, _dp]
     L.ref_gt_fold.argtypes = [C.c_void_p, _dp, _dp, _dp]
     L.ref_train_reset.argtypes = [C.c_void_p]
+    L.ref_set_keep_grads.argtypes = [C.c_void_p, C.c_int]
+    L.ref_last_phase_ms.argtypes = [C.c_void_p, _dp]
     L.ref_train_step.argtypes = [C.c_void_p, C.c_int, C.POINTER(RefCamera), C.POINTER(_dp),
                                  C.POINTER(_dp), C.POINTER(RefStepParams), C.c_int, _dp, _lp]
     L.ref_grads_export.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp, _dp, _dp]
@@ -398,6 +400,14 @@ class RefScene:
         _check(self.L.ref_train_step(self.h, n, arr, gp, mp, C.byref(hp), threads, ptr(losses),
                                      ptr(counts, _lp)), self.L)
         return losses, counts
+
+    def keep_grads(self, keep):
+        self.L.ref_set_keep_grads(self.h, int(keep))
+
+    def last_phase_ms(self):
+        out = np.zeros(3)
+        self.L.ref_last_phase_ms(self.h, ptr(out))
+        return out
 
     def grads(self, stage):
         g = self.grad_like()

@@ -85,6 +85,7 @@ EXPORTS = [
     "psdf_last_k2_breakdown", "psdf_grid_info", "psdf_download_structure", "psdf_subdivide",
     "psdf_raise_sh_order", "psdf_last_h2d_bytes", "psdf_init_visual_hull", "psdf_save_checkpoint",
     "psdf_load_checkpoint", "psdf_eval_psnr", "psdf_point_mesh_distance", "psdf_chamfer",
+    "psdf_debug_set_shard",
 ]
 
 _lib = None
@@ -134,6 +135,7 @@ def load():
                                         C.POINTER(psdf_losses), C.POINTER(psdf_counts)]
     L.psdf_comm_unique_id.argtypes = [vp]
     L.psdf_comm_init.argtypes = [vp, vp, C.c_int, C.c_int]
+    L.psdf_debug_set_shard.argtypes = [vp, C.c_int, C.c_int]
     L.psdf_last_timing.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                    C.POINTER(C.c_int)]
     L.psdf_stream.restype = vp

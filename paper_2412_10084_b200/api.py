@@ -662,6 +662,13 @@ class Context:
         buf = C.create_string_buffer(uid, 128)
         self._check(self.L.psdf_comm_init(self.h, buf, rank, world))
 
+    def debug_set_shard(self, rank, world):
+        """Test hook: process only `rank`'s 1/world slice, no all-reduce."""
+        self._check(self.L.psdf_debug_set_shard(self.h, int(rank), int(world)))
+
+    def last_h2d_bytes(self):
+        return int(self.L.psdf_last_h2d_bytes(self.h))
+
 
 def pixel_dirs(camera) -> np.ndarray:
     """Device Camera::pixel_dir at all pixel centres, [h][w][3] f64."""

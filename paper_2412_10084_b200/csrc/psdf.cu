@@ -2333,6 +2333,27 @@ int psdf_train_step(psdf_ctx* c, int n_views, const psdf_camera* cams, const flo
         }
         std::vector<DevView> tmp(n_views);
         std::vector<DevView*> batch(n_views);
+        // the pixel rows this rank's slice of the batch's 8x4 work tiles
+        // covers (do_train_step: contiguous 1/N of the work tiles, each view's
+        // tiles row-major): only those rows are copied, so the H2D bytes per
+        // rank fall as 1/N; the staging buffer keeps the full layout
+        std::vector<int> row0(n_views, 0), row1(n_views, -1);
+        {
+            int64_t tiles = 0;
+            for (int i = 0; i < n_views; ++i)
+                tiles += (int64_t)((cams[i].width + 7) / 8) * ((cams[i].height + 3) / 4);
+            const int64_t tb = tiles * c->rank / c->world, te = tiles * (c->rank + 1) / c->world;
+            int64_t begin = 0;
+            for (int i = 0; i < n_views; ++i) {
+                const int64_t tx = (cams[i].width + 7) / 8, n_t = tx * ((cams[i].height + 3) / 4);
+                const int64_t lo = std::max(tb, begin), hi = std::min(te, begin + n_t);
+                if (hi > lo) {
+                    row0[i] = (int)(4 * ((lo - begin) / tx));
+                    row1[i] = (int)std::min<int64_t>(cams[i].height - 1, 4 * ((hi - 1 - begin) / tx) + 3);
+                }
+                begin += n_t;
+            }
+        }
         size_t off = 0;
         CK(cudaStreamWaitEvent(c->copy_stream, c->ev_copy_free, 0));  // staging no longer read
         // masks first (the composite pass needs them), then the colours (the
@@ -2343,17 +2364,20 @@ int psdf_train_step(psdf_ctx* c, int n_views, const psdf_camera* cams, const flo
             tmp[i].cam = cams[i];
             tmp[i].rgb = c->d_stage_rgb + 3 * off;
             tmp[i].mask = c->d_stage_mask + off;
-            CK(cudaMemcpyAsync(tmp[i].mask, mask[i], n, cudaMemcpyHostToDevice, c->copy_stream));
             batch[i] = &tmp[i];
             off += n;
-            c->last_h2d_bytes += (int64_t)n;
+            if (row1[i] < row0[i]) continue;
+            const size_t o = (size_t)row0[i] * cams[i].width, m = (size_t)(row1[i] - row0[i] + 1) * cams[i].width;
+            CK(cudaMemcpyAsync(tmp[i].mask + o, mask[i] + o, m, cudaMemcpyHostToDevice, c->copy_stream));
+            c->last_h2d_bytes += (int64_t)m;
         }
         CK(cudaEventRecord(c->ev_masks, c->copy_stream));
         for (int i = 0; i < n_views; ++i) {
-            const size_t n = (size_t)cams[i].width * cams[i].height;
-            CK(cudaMemcpyAsync(tmp[i].rgb, gt_rgb[i], sizeof(float) * 3 * n, cudaMemcpyHostToDevice,
-                               c->copy_stream));
-            c->last_h2d_bytes += (int64_t)(sizeof(float) * 3 * n);
+            if (row1[i] < row0[i]) continue;
+            const size_t o = (size_t)row0[i] * cams[i].width, m = (size_t)(row1[i] - row0[i] + 1) * cams[i].width;
+            CK(cudaMemcpyAsync(tmp[i].rgb + 3 * o, gt_rgb[i] + 3 * o, sizeof(float) * 3 * m,
+                               cudaMemcpyHostToDevice, c->copy_stream));
+            c->last_h2d_bytes += (int64_t)(sizeof(float) * 3 * m);
         }
         CK(cudaEventRecord(c->ev_rgb, c->copy_stream));
         CK(cudaEventRecord(c->ev_copied, c->copy_stream));
@@ -2408,6 +2432,17 @@ int psdf_train_step_views(psdf_ctx* c, int n_batch, const int32_t* view_ids,
             batch[i] = &c->views[view_ids[i]];
         }
         do_train_step(c, batch, hp, losses, counts);
+    });
+}
+
+int psdf_debug_set_shard(psdf_ctx* c, int rank, int world_size) {
+    return guarded([&] {
+        if (!c) fail(PSDF_ERR_INVALID_ARGUMENT, "null context");
+        if (c->comm) fail(PSDF_ERR_RUNTIME, "context has a communicator");
+        if (world_size < 1 || rank < 0 || rank >= world_size)
+            fail(PSDF_ERR_INVALID_ARGUMENT, "bad rank %d / world %d", rank, world_size);
+        c->rank = rank;
+        c->world = world_size;
     });
 }
 
