@@ -209,6 +209,15 @@ int psdf_chamfer(psdf_ctx* ctx, const double* pred_pts, int64_t n_pred, const do
                  int64_t n_gt, const double* gt_verts, int64_t gt_nv, const int32_t* gt_tris, int64_t gt_nt,
                  double max_dist, double* out);
 
+/* Marching cubes (mesh.cpp:305-394, marching_cubes(grid)) of the context's
+   smoothed SDF on the device: the reference's mesh exactly (same vertex ids
+   and f64 positions, same triangles in the same order; cells with a corner in
+   an unallocated tile vetoed, zero-area triangles dropped).  The mesh stays in
+   the context; psdf_download_mesh copies it out (verts nv x 3 f64, tris nt x 3
+   i32).  An empty grid gives an empty mesh. */
+int psdf_marching_cubes(psdf_ctx* ctx, int64_t* nv, int64_t* nt);
+int psdf_download_mesh(psdf_ctx* ctx, double* verts, int32_t* tris);
+
 /* ---- train ------------------------------------------------------------------
  * One iteration of the train() loop body (trainer.cpp:136-195): clear
  * gradients, ray pass over every pixel of the batch views (render_ray +

@@ -1040,6 +1040,32 @@ int ref_marching_cubes(RefScene* s, double* verts, int64_t vcap, int32_t* tris, 
     }
 }
 
+// mesh.cpp:396 marching_cubes_field over a dense field (x-major), same
+// two-call protocol as ref_marching_cubes.
+int ref_marching_cubes_field(const double* values, int nx, int ny, int nz, const double origin[3],
+                             double spacing, double* verts, int64_t vcap, int32_t* tris, int64_t tcap,
+                             int64_t* nv, int64_t* nt) {
+    try {
+        std::vector<double> vals(values, values + static_cast<size_t>(nx) * ny * nz);
+        const TriMesh m = marching_cubes_field(vals, nx, ny, nz, Vec3(origin[0], origin[1], origin[2]), spacing);
+        *nv = static_cast<int64_t>(m.vertices.size());
+        *nt = static_cast<int64_t>(m.triangles.size());
+        if (verts && tris && vcap >= *nv && tcap >= *nt) {
+            for (int64_t i = 0; i < *nv; ++i) {
+                verts[3 * i] = m.vertices[i].x;
+                verts[3 * i + 1] = m.vertices[i].y;
+                verts[3 * i + 2] = m.vertices[i].z;
+            }
+            for (int64_t i = 0; i < *nt; ++i)
+                for (int k = 0; k < 3; ++k) tris[3 * i + k] = m.triangles[i][k];
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 static TriMesh to_mesh(const double* verts, int64_t nv, const int32_t* tris, int64_t nt) {
     TriMesh m;
     m.vertices.resize(nv);

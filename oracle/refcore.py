@@ -160,6 +160,8 @@ def reflib():
     L.ref_psnr_masked.argtypes = [_dp, _dp, _dp, C.c_int, C.c_int, _dp]
     _i32p, _i64p = C.POINTER(C.c_int32), C.POINTER(C.c_int64)
     L.ref_marching_cubes.argtypes = [C.c_void_p, _dp, C.c_int64, _i32p, C.c_int64, _i64p, _i64p]
+    L.ref_marching_cubes_field.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _dp, C.c_double, _dp, C.c_int64,
+                                           _i32p, C.c_int64, _i64p, _i64p]
     L.ref_point_mesh_distance.argtypes = [_dp, C.c_int64, _dp, C.c_int64, _i32p, C.c_int64, _dp]
     L.ref_sample_mesh_points.argtypes = [_dp, C.c_int64, _i32p, C.c_int64, C.c_int, C.c_uint64, _dp]
     L.ref_chamfer.argtypes = [_dp, C.c_int64, _dp, C.c_int64, _i32p, C.c_int64, _dp, C.c_int64, _dp,
@@ -510,3 +512,21 @@ def ref_chamfer(pred_pts, pred_verts, pred_tris, gt_pts, gt_verts, gt_tris, max_
     _check(L.ref_chamfer(ptr(pp), len(pp), ptr(pv), len(pv), ptp, len(pt), ptr(gp), len(gp), ptr(gv), len(gv),
                          gtp, len(gt), max_dist, ptr(out)), L)
     return out
+
+
+def ref_marching_cubes_field(values, origin=(0.0, 0.0, 0.0), spacing=1.0):
+    """mesh.cpp:396 marching_cubes_field(values[x][y][z]) through the reference library
+    -> (verts (nv, 3) f64, tris (nt, 3) i32)."""
+    L = reflib()
+    f = np.ascontiguousarray(values, np.float64)
+    nx, ny, nz = f.shape
+    o = np.ascontiguousarray(origin, np.float64)
+    nv, nt = C.c_int64(), C.c_int64()
+    i32 = C.POINTER(C.c_int32)
+    _check(L.ref_marching_cubes_field(ptr(f), nx, ny, nz, ptr(o), spacing, None, 0, None, 0,
+                                      C.byref(nv), C.byref(nt)), L)
+    v = np.zeros((nv.value, 3))
+    t = np.zeros((nt.value, 3), np.int32)
+    _check(L.ref_marching_cubes_field(ptr(f), nx, ny, nz, ptr(o), spacing, ptr(v), nv.value,
+                                      t.ctypes.data_as(i32), nt.value, C.byref(nv), C.byref(nt)), L)
+    return v, t

@@ -85,7 +85,7 @@ EXPORTS = [
     "psdf_last_k2_breakdown", "psdf_grid_info", "psdf_download_structure", "psdf_subdivide",
     "psdf_raise_sh_order", "psdf_last_h2d_bytes", "psdf_init_visual_hull", "psdf_save_checkpoint",
     "psdf_load_checkpoint", "psdf_eval_psnr", "psdf_point_mesh_distance", "psdf_chamfer",
-    "psdf_debug_set_shard",
+    "psdf_debug_set_shard", "psdf_marching_cubes", "psdf_download_mesh",
 ]
 
 _lib = None
@@ -125,6 +125,8 @@ def load():
     L.psdf_point_mesh_distance.argtypes = [vp, _dp, C.c_int64, _dp, C.c_int64, _i32, C.c_int64, _dp]
     L.psdf_chamfer.argtypes = [vp, _dp, C.c_int64, _dp, C.c_int64, _i32, C.c_int64, _dp, C.c_int64, _dp,
                                C.c_int64, _i32, C.c_int64, C.c_double, _dp]
+    L.psdf_marching_cubes.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    L.psdf_download_mesh.argtypes = [vp, _dp, _i32]
     L.psdf_train_reset.argtypes = [vp]
     L.psdf_train_step.argtypes = [vp, C.c_int, C.POINTER(psdf_camera), C.POINTER(_fp),
                                   C.POINTER(C.POINTER(C.c_uint8)), C.POINTER(psdf_step_params),

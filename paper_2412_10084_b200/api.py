@@ -593,6 +593,17 @@ class Context:
                                         float(max_dist), _dptr(out)))
         return dict(accuracy=out[0], completeness=out[1], mean=out[2])
 
+    def marching_cubes(self):
+        """marching_cubes(grid) (mesh.cpp:363-394) of the device grid's smoothed
+        SDF, on the GPU -> (verts (nv, 3) f64, tris (nt, 3) i32), the reference's
+        mesh exactly."""
+        nv, nt = C.c_int64(), C.c_int64()
+        self._check(self.L.psdf_marching_cubes(self.h, C.byref(nv), C.byref(nt)))
+        v = np.zeros((nv.value, 3))
+        t = np.zeros((nt.value, 3), np.int32)
+        self._check(self.L.psdf_download_mesh(self.h, _dptr(v), _iptr(t)))
+        return v, t
+
     # -- train (trainer.cpp:136-195)
     def train_reset(self):
         self._check(self.L.psdf_train_reset(self.h))

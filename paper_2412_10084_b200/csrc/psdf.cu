@@ -34,6 +34,7 @@
 #include "psdf_raypass.cuh"
 #include "psdf_train.cuh"
 #include "psdf_lod.cuh"
+#include "psdf_mesh.cuh"
 
 using namespace psdf;
 
@@ -233,6 +234,11 @@ struct psdf_ctx {
     float* d_render = nullptr;  // render scratch: rgb | alpha | depth
     size_t render_px = 0;
     uint8_t* d_eval = nullptr;  // point-to-mesh scratch (grow-only arena)
+    uint8_t* d_mc = nullptr;    // marching-cubes cell arrays + scan storage (grow-only)
+    size_t mc_cap = 0;
+    uint8_t* d_mesh = nullptr;  // the last extracted mesh: verts f64 | tris i32 (grow-only)
+    size_t mesh_cap = 0;
+    int64_t mesh_nv = -1, mesh_nt = -1;  // -1: no mesh extracted
     size_t eval_cap = 0;
 
     unsigned long long* d_work = nullptr;
@@ -1109,7 +1115,7 @@ int psdf_destroy(psdf_ctx* c) {
             if (v.mask) cudaFree(v.mask);
         }
         for (void* p : {(void*)c->d_stage_rgb, (void*)c->d_stage_mask, (void*)c->d_viewdev,
-                        (void*)c->d_render, (void*)c->d_eval, (void*)c->d_work, (void*)c->d_counts, (void*)c->d_stats})
+                        (void*)c->d_render, (void*)c->d_eval, (void*)c->d_mc, (void*)c->d_mesh, (void*)c->d_work, (void*)c->d_counts, (void*)c->d_stats})
             if (p) cudaFree(p);
         free_wave(c);
         if (c->wave.counters) cudaFree(c->wave.counters);
@@ -2293,6 +2299,95 @@ int psdf_chamfer(psdf_ctx* c, const double* pred_pts, int64_t n_pred, const doub
         out[0] = 1000.0 * directional_mean(to_gt, max_dist);    // accuracy
         out[1] = 1000.0 * directional_mean(to_pred, max_dist);  // completeness
         out[2] = 0.5 * (out[0] + out[1]);
+    });
+}
+
+// marching_cubes(grid) (mesh.cpp:363-394) of the context's smoothed SDF on the
+// device (psdf_mesh.cuh); the mesh stays in the context for psdf_download_mesh.
+int psdf_marching_cubes(psdf_ctx* c, int64_t* nv, int64_t* nt) {
+    return guarded([&] {
+        need_grid(c);
+        if (!nv || !nt) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
+        set_device(c);
+        cudaStream_t s = c->stream;
+        const int64_t n = (int64_t)c->desc.T * TV;
+        c->mesh_nv = c->mesh_nt = -1;
+        if (n == 0) {
+            c->mesh_nv = c->mesh_nt = 0;
+            *nv = *nt = 0;
+            return;
+        }
+        if (n > INT32_MAX) fail(PSDF_ERR_INVALID_ARGUMENT, "grid too large for marching cubes");
+        size_t tmp_bytes = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (int*)nullptr, (int*)nullptr, (int)n, s));
+        auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+        const size_t o_own = al(2 * n), o_vc = o_own + al(2 * n), o_tc = o_vc + al(4 * n), o_tmp = o_tc + al(4 * n),
+                     total = o_tmp + al(std::max<size_t>(tmp_bytes, 1));
+        ensure_dev(c->d_mc, c->mc_cap, total);
+        McView M{};
+        M.g = c->view();
+        M.cell = reinterpret_cast<uint16_t*>(c->d_mc);
+        M.own = reinterpret_cast<uint16_t*>(c->d_mc + o_own);
+        M.vcount = reinterpret_cast<int*>(c->d_mc + o_vc);
+        M.tcount = reinterpret_cast<int*>(c->d_mc + o_tc);
+        void* d_tmp = c->d_mc + o_tmp;
+        for (int a = 0; a < 3; ++a) M.o[a] = c->desc.origin[a] + 0.5 * c->desc.voxel_size;  // voxel_center(0,0,0)
+        const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 8 * c->sm_count);
+        mc_case_kernel<<<blocks, 256, 0, s>>>(M);
+        mc_own_kernel<<<blocks, 256, 0, s>>>(M);
+        // vertex base per cell: exclusive scan of the owned-edge counts (in place)
+        int last[2];
+        CK(cudaMemcpyAsync(&last[0], M.vcount + n - 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, M.vcount, M.vcount, (int)n, s));
+        CK(cudaMemcpyAsync(&last[1], M.vcount + n - 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const int64_t n_v = (int64_t)last[0] + last[1];
+        // vertices first (the triangle pass reads them); triangles are counted,
+        // scanned, and then the array is sized exactly
+        ensure_dev(c->d_mesh, c->mesh_cap, al(24 * n_v) + 256);
+        M.verts = reinterpret_cast<double*>(c->d_mesh);
+        mc_vert_kernel<<<blocks, 256, 0, s>>>(M);
+        mc_tri_kernel<false><<<blocks, 256, 0, s>>>(M);
+        CK(cudaMemcpyAsync(&last[0], M.tcount + n - 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, M.tcount, M.tcount, (int)n, s));
+        CK(cudaMemcpyAsync(&last[1], M.tcount + n - 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const int64_t n_t = (int64_t)last[0] + last[1];
+        const size_t need = al(24 * n_v) + al(12 * n_t) + 256;
+        if (need > c->mesh_cap) {  // grow, keeping the vertices
+            uint8_t* p = nullptr;
+            CK(cudaMalloc(&p, need));
+            CK(cudaMemcpyAsync(p, c->d_mesh, 24 * n_v, cudaMemcpyDeviceToDevice, s));
+            CK(cudaStreamSynchronize(s));
+            cudaFree(c->d_mesh);
+            c->d_mesh = p;
+            c->mesh_cap = need;
+            M.verts = reinterpret_cast<double*>(c->d_mesh);
+        }
+        M.tris = reinterpret_cast<int32_t*>(c->d_mesh + al(24 * n_v));
+        mc_tri_kernel<true><<<blocks, 256, 0, s>>>(M);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(s));
+        c->mesh_nv = n_v;
+        c->mesh_nt = n_t;
+        *nv = n_v;
+        *nt = n_t;
+    });
+}
+
+int psdf_download_mesh(psdf_ctx* c, double* verts, int32_t* tris) {
+    return guarded([&] {
+        if (!c) fail(PSDF_ERR_INVALID_ARGUMENT, "null context");
+        if (c->mesh_nv < 0) fail(PSDF_ERR_RUNTIME, "no mesh extracted (psdf_marching_cubes)");
+        if ((c->mesh_nv > 0 && !verts) || (c->mesh_nt > 0 && !tris)) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
+        set_device(c);
+        auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+        if (c->mesh_nv > 0)
+            CK(cudaMemcpyAsync(verts, c->d_mesh, 24 * c->mesh_nv, cudaMemcpyDeviceToHost, c->stream));
+        if (c->mesh_nt > 0)
+            CK(cudaMemcpyAsync(tris, c->d_mesh + al(24 * c->mesh_nv), 12 * c->mesh_nt, cudaMemcpyDeviceToHost,
+                               c->stream));
+        CK(cudaStreamSynchronize(c->stream));
     });
 }
 

@@ -2,10 +2,12 @@
 unmodified reference (tests/golden/make_golden.py) and against the published
 known-answer constants of the reference's own unit tests."""
 import math
+import os
 
 import numpy as np
 import pytest
 
+from conftest import have_ref
 from helpers import cam_from_array, golden, scene32_arrays, step_params_from
 
 
@@ -171,3 +173,29 @@ def test_mesh_distance_golden():
     assert np.array_equal(chamfer(g["pred_pts"], v, t, g["gt_pts"], v2, t, 0.0045), g["chamfer_clip"])
     with pytest.raises(ValueError, match="empty input"):
         chamfer(p1[:0], v, t, p2, v2, t, 0.0)
+
+
+@pytest.mark.skipif(not have_ref(), reason="oracle/_ref not built")
+def test_mc_case_table_matches_reference():
+    """The device's packed 256-case triangle table (psdf_mesh.cuh kMcTri)
+    emits, for every case of a single cell, the reference's triangles in the
+    reference's order (marching_cubes_field over a 2x2x2 field of +-1)."""
+    import re
+    from oracle.refcore import ref_marching_cubes_field
+    src = open(os.path.join(os.path.dirname(__file__), "..", "paper_2412_10084_b200", "csrc",
+                            "psdf_mesh.cuh")).read()
+    body = src[src.index("kMcTri[256] = {"):]
+    words = [int(w, 16) for w in re.findall(r"0x([0-9a-f]{16})ull", body[:body.index("};")])]
+    assert len(words) == 256
+    corner = [(0, 0, 0), (1, 0, 0), (1, 1, 0), (0, 1, 0), (0, 0, 1), (1, 0, 1), (1, 1, 1), (0, 1, 1)]
+    edges = [(0, 1), (1, 2), (2, 3), (3, 0), (4, 5), (5, 6), (6, 7), (7, 4), (0, 4), (1, 5), (2, 6), (3, 7)]
+    mid = {tuple((np.array(corner[a]) + np.array(corner[b])) / 2): e for e, (a, b) in enumerate(edges)}
+    for ci in range(256):
+        f = np.zeros((2, 2, 2))
+        for c, (x, y, z) in enumerate(corner):
+            f[x, y, z] = -1.0 if (ci >> c) & 1 else 1.0
+        v, t = ref_marching_cubes_field(f)
+        want = [mid[tuple(v[i])] for tri in t for i in tri]
+        w = words[ci]
+        got = [(w >> (4 * k)) & 15 for k in range(3 * (w >> 60))]
+        assert got == want, (ci, got, want)
