@@ -253,6 +253,9 @@ int psdf_comm_init(psdf_ctx* ctx, const void* unique_id, int rank, int world_siz
  * the all-reduce, so the stage-1 gradients of the N slices sum to the
  * one-rank gradients (tests/test_gpu_shard.py). */
 int psdf_debug_set_shard(psdf_ctx* ctx, int rank, int world_size);
+/* Diagnostics: raw copy of n items of one ray-pass queue of the last pass
+   (psdf.cu psdf_debug_wave lists the queues and item sizes). */
+int psdf_debug_wave(psdf_ctx* ctx, int which, void* out, int64_t n);
 
 /* ---- timing / introspection ------------------------------------------------ */
 /* Device time (ms) of the last call's dominant kernel (the fused ray-pass
@@ -262,6 +265,9 @@ int psdf_last_timing(psdf_ctx* ctx, double* ray_kernel_ms, double* step_ms, int*
 /* Device time (ms) of the four K2 kernels of the last train step (march_fwd,
  * shade_fwd, alpha_bwd, shade_bwd) and the ray-entry / shading-record counts. */
 int psdf_last_k2_breakdown(psdf_ctx* ctx, double* ms4, int64_t* entries, int64_t* records);
+/* Queue sizes of the last train step's ray pass: ray entries, shading
+   records, scan hand-overs, round-1 continuations, alpha samples. */
+int psdf_last_wave_counts(psdf_ctx* ctx, int64_t* out5);
 /* Raw CUDA stream of the context (cudaStream_t), for callers that time or
  * overlap work around the context. */
 void* psdf_stream(psdf_ctx* ctx);

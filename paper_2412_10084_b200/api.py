@@ -656,6 +656,13 @@ class Context:
         self._check(self.L.psdf_last_k2_breakdown(self.h, ms, C.byref(ne), C.byref(nr)))
         return list(ms), ne.value, nr.value
 
+    def last_wave_counts(self):
+        """Queue sizes of the last train step's ray pass: dict(entries, records,
+        handovers, continuations, alpha_samples)."""
+        out = (C.c_int64 * 5)()
+        self._check(self.L.psdf_last_wave_counts(self.h, out))
+        return dict(zip(("entries", "records", "handovers", "continuations", "alpha_samples"), list(out)))
+
     def last_timing(self):
         r, s, n = C.c_double(), C.c_double(), C.c_int()
         self._check(self.L.psdf_last_timing(self.h, C.byref(r), C.byref(s), C.byref(n)))

@@ -203,6 +203,7 @@ struct psdf_ctx {
     int occ_tlo[3] = {0, 0, 0}, occ_thi[3] = {-1, -1, -1};  // allocated tiles' bounding box (tile coords)
     uint8_t* d_sat_dist = nullptr; // [T][17^3] per-cell saturation distances of the current ray pass
     int composite_steps = kComposite0Steps;
+    bool coop_round1 = true;       // K2a round 1 one warp per ray (PSDF_COOP=0: one lane per ray, A/B)
     int* d_tile_cnt = nullptr;     // [2T] shading records per tile, then their offsets
     void* scan_tmp = nullptr;      // CUB scan storage of the counting sort
     size_t scan_tmp_bytes = 0;
@@ -254,6 +255,7 @@ struct psdf_ctx {
     float last_k2_ms[4] = {0.f, 0.f, 0.f, 0.f};  // K2a, K2b, K2d, K2e
     int last_launches = 0;
     int64_t last_entries = 0, last_records = 0;
+    int64_t last_wave[5] = {0, 0, 0, 0, 0};  // entries, records, handovers, continuations, alpha samples
     int64_t last_h2d_bytes = 0;    // host -> device bytes of the last psdf_train_step
     cudaEvent_t ev_k[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 
@@ -618,11 +620,14 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
                                 (int)(sizeof(uint32_t) * kMaxSmemBitWords)));
         CK(cudaFuncSetAttribute(march_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(sizeof(uint32_t) * kMaxSmemBitWords)));
+        CK(cudaFuncSetAttribute(march_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(sizeof(uint32_t) * kMaxSmemBitWords)));
     }
     const int per_sm_s = blocks_per_sm((const void*)march_scan_kernel, smem_bits);
     const int64_t grid_s = std::max<int64_t>(1, std::min<int64_t>((n_work + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
                                                                    (int64_t)per_sm_s * c->sm_count));
     const int grid_a = blocks_per_sm((const void*)march_fwd_kernel, smem_bits) * c->sm_count;
+    const int grid_c1 = blocks_per_sm((const void*)march_coop_kernel, smem_bits) * c->sm_count;
     WaveBufs W = c->wave;
     CK(cudaEventRecord(c->ev_ray0, s));
     CK(cudaEventRecord(c->ev_k[0], s));
@@ -656,7 +661,10 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
     if (c->fork_regs) CK(cudaEventRecord(c->ev_fork, s));
-    march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, W, 1, INT_MAX);
+    if (c->coop_round1 && P.mode != 1)
+        march_coop_kernel<<<(unsigned)grid_c1, BLOCK, smem_bits, s>>>(P, W);
+    else
+        march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, W, 1, INT_MAX);
     CK(cudaGetLastError());
     c->last_launches += 2;
     if (getenv("PSDF_DEBUG_MARCH")) {
@@ -678,6 +686,11 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
         CK(cudaMemcpyFromSymbol(hh, g_cont_hist, sizeof hh));
         const unsigned long long z2[2][16] = {};
         CK(cudaMemcpyToSymbol(g_cont_hist, z2, sizeof z2));
+        unsigned long long cs[8];
+        CK(cudaMemcpyFromSymbol(cs, g_coop_stats, sizeof cs));
+        CK(cudaMemcpyToSymbol(g_coop_stats, zero, sizeof cs));
+        fprintf(stderr, "[psdf] coop: rays %llu steps %llu sat-runs %llu batches %llu batch-samples %llu "
+                "single-sample batches %llu\n", cs[0], cs[1], cs[2], cs[3], cs[4], cs[5]);
         for (int r = 0; r < 2; ++r) {
             fprintf(stderr, "[psdf] K2a round %d rays by steps [2^(b-1), 2^b):", r);
             for (int b = 0; b < 16; ++b) fprintf(stderr, " %llu", hh[r][b]);
@@ -995,6 +1008,7 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
     }
     c->last_entries = c->h_wave_counters[0];
     c->last_records = c->h_wave_counters[1];
+    for (int k = 0; k < 5; ++k) c->last_wave[k] = c->h_wave_counters[k];
     CK(cudaEventElapsedTime(&c->last_ray_ms, c->ev_ray0, c->ev_ray1));
     CK(cudaEventElapsedTime(&c->last_step_ms, c->ev_step0, c->ev_step1));
     for (int k = 0; k < 4; ++k) CK(cudaEventElapsedTime(&c->last_k2_ms[k], c->ev_k[k], c->ev_k[k + 1]));
@@ -1074,6 +1088,7 @@ int psdf_create(int device, psdf_ctx** out) {
         CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi));
         if (const char* e = std::getenv("PSDF_COMPOSITE_STEPS")) c->composite_steps = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("PSDF_WAVE_INIT")) c->wave_init = std::max(0, std::atoi(e));
+        if (const char* e = std::getenv("PSDF_COOP")) c->coop_round1 = std::atoi(e) != 0;
         if (const char* e = std::getenv("PSDF_REGS_EARLY")) c->regs_early = std::atoi(e) != 0;
         if (const char* m = std::getenv("PSDF_TEST_MARGIN")) c->test_margin = std::max(1e-8, std::atof(m));
         CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
@@ -2541,6 +2556,41 @@ int psdf_debug_set_shard(psdf_ctx* c, int rank, int world_size) {
     });
 }
 
+// Diagnostics: raw copies of the last ray pass's queues (which: 0 e_slot i32,
+// 1 e_acc f64, 2 e_craw f64x3, 3 e_nlive i32, 4 e_cfirst i32, 5 e_tfirst f64,
+// 6 r_pos f64x3, 7 r_w f64, 8 r_tile i32, 9 r_entry i32, 10 a_t f64x2,
+// 11 a_s f64x3, 12 a_i i32x4, 13 e_head i32, 14 e_ahead i32, 15 r_next i32).
+int psdf_debug_wave(psdf_ctx* c, int which, void* out, int64_t n) {
+    return guarded([&] {
+        if (!c || !out) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
+        const WaveBufs& W = c->wave;
+        const void* src = nullptr;
+        size_t es = 0;
+        switch (which) {
+            case 0: src = W.e_slot; es = 4; break;
+            case 1: src = W.e_acc; es = 8; break;
+            case 2: src = W.e_craw; es = 24; break;
+            case 3: src = W.e_nlive; es = 4; break;
+            case 4: src = W.e_cfirst; es = 4; break;
+            case 5: src = W.e_tfirst; es = 8; break;
+            case 6: src = W.r_pos; es = 24; break;
+            case 7: src = W.r_w; es = 8; break;
+            case 8: src = W.r_tile; es = 4; break;
+            case 9: src = W.r_entry; es = 4; break;
+            case 10: src = W.a_t; es = 16; break;
+            case 11: src = W.a_s; es = 24; break;
+            case 12: src = W.a_i; es = 16; break;
+            case 13: src = W.e_head; es = 4; break;
+            case 14: src = W.e_ahead; es = 4; break;
+            case 15: src = W.r_next; es = 4; break;
+            default: fail(PSDF_ERR_INVALID_ARGUMENT, "bad queue %d", which);
+        }
+        if (!src) fail(PSDF_ERR_RUNTIME, "no ray pass yet");
+        set_device(c);
+        CK(cudaMemcpy(out, src, es * (size_t)n, cudaMemcpyDeviceToHost));
+    });
+}
+
 int psdf_comm_unique_id(void* out) {
     return guarded([&] {
         if (!out) fail(PSDF_ERR_INVALID_ARGUMENT, "null output");
@@ -2616,6 +2666,13 @@ int psdf_last_k2_breakdown(psdf_ctx* c, double* ms4, int64_t* entries, int64_t* 
             if (ms4) ms4[k] = c->last_k2_ms[k];
         if (entries) *entries = c->last_entries;
         if (records) *records = c->last_records;
+    });
+}
+
+int psdf_last_wave_counts(psdf_ctx* c, int64_t* out5) {
+    return guarded([&] {
+        if (!c || !out5) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
+        for (int k = 0; k < 5; ++k) out5[k] = c->last_wave[k];
     });
 }
 

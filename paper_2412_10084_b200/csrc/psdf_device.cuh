@@ -327,6 +327,9 @@ __device__ __noinline__ int4 exact_tile(GridLite g, D3 o, D3 d, double t) {
 // fast skips, exact fallbacks, rewinds]
 __device__ unsigned long long g_march_stats[12];
 __device__ unsigned long long g_cont_hist[2][16];  // K2a rays by log2(steps), per round
+// march_coop_kernel: rays, loop steps, saturated runs, batches, batch samples,
+// batches of one sample, marcher iterations inside its next_run calls
+__device__ unsigned long long g_coop_stats[8];
 #define PSDF_STAT(i) atomicAdd(&g_march_stats[i], 1ull)
 #else
 #define PSDF_STAT(i) ((void)0)
@@ -489,27 +492,34 @@ struct Marcher {
     }
 
     // Lattice points t + j h (j >= 0) still inside the current tile and
-    // before the box exit t1, or 1 when either boundary is within the
-    // decision margin (then the caller steps one sample at a time).  Only
-    // with the lattice preconditions (power-of-two h, t >= 64 h).
+    // before the box exit t1, each at least the decision margin (in voxels)
+    // off every face of the tile — so the fast form's tile is the exact one
+    // for all of them, also on a ray that runs along a face (the per-axis
+    // exit distance divided by |d_a|, the voxels the ray advances per
+    // lattice step along a) — or 1 when t itself is that close to a face or
+    // the box exit is within its margin (then the caller steps one sample at
+    // a time).  Only with the lattice preconditions (power-of-two h, t >= 64 h).
     __device__ __forceinline__ double run_length(const GridView& g, const double v[3], double t,
                                                  double h) const {
         if (!g.h_pow2 || t < 64.0 * h) return 1.0;
-        double q = 1e300;
+        const double M = g.margin + 1e-9;  // voxels: decision margin + the fast form's error
+        double n = 1e300;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            if (inv_d[a] == 0.0) continue;
-            const double B = 16.0 * (floor(v[a] * 0.0625) + (d[a] > 0.0 ? 1.0 : 0.0));
-            q = fmin(q, (B - v[a]) * inv_d[a]);
+            const double r = v[a] - 16.0 * floor(v[a] * 0.0625);
+            if (r <= M || r >= 16.0 - M) return 1.0;
+            // |d_a| voxels per lattice step along a; 1/|d_a| from the
+            // correctly rounded reciprocal, shrunk by 1e-13 so the floor never
+            // exceeds the exact quotient (the margin absorbs the rest)
+            if (inv_d[a] == 0.0) continue;  // parallel to the faces: r stays put
+            const double dist = d[a] > 0.0 ? 16.0 - r : r;  // voxels to the exit face
+            n = fmin(n, floor((dist - M) * fabs(inv_d[a]) * (1.0 - 1e-13)) + 1.0);
         }
-        const double mq = g.margin + 1e-11 * rinv_max;
-        const double fq = q - floor(q);
-        if (!(q < 1e300) || fq <= mq || fq >= 1.0 - mq) return 1.0;
         // the reference's own loop test t_j < t1, t_j = t + j h exactly
         const double r1 = (t1 - t) * g.inv_h;
         const double f1 = r1 - floor(r1);
         if (f1 <= 1e-9 || f1 >= 1.0 - 1e-9) return 1.0;
-        return fmin(ceil(q), ceil(r1));
+        return fmax(1.0, fmin(n, ceil(r1)));
     }
 
     // Next sample distance inside an allocated tile; false when exhausted.

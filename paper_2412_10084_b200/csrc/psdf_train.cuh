@@ -634,6 +634,285 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
     }
 }
 
+// ------------------------------------------------------------------ K2a round 1
+#ifndef PSDF_COOP_MINB
+#define PSDF_COOP_MINB 4  // <= 128 registers: 16 warps (rays) per SM
+#endif
+// The continuations (rays still alive after round 0's `cap` steps: grazing
+// rays with long tails, ~12 K at the bench step with 16-64 more samples
+// each) as ONE WARP PER RAY.  With one lane per ray they leave a few warps per
+// SM in a latency-bound tail (round 1 of march_fwd: 6.5 % warps active, 9
+// threads per instruction): such a ray alternates short saturated runs (~4
+// samples) with short unsaturated stretches, ~20 sequential marcher steps.
+// Here the marcher's control (tile decisions, jumps) runs warp-uniformly, and
+// the first lattice point of an allocated tile opens a batch of up to 32
+// consecutive lattice points of that tile (Marcher::run_length), one per
+// lane, whose SDF and sigmoid are evaluated in parallel — exactly the samples
+// the reference visits (a point of a saturated cell evaluates to sigmoid 1
+// exactly, so no saturated-run shortcut is needed).  The settles stay in the reference's order: lane j's
+// transmittance is trans * (1 - alpha_0) * ... * (1 - alpha_{j-1}) multiplied
+// left to right through shuffles, acc / depth are summed in lane order, and
+// early termination cuts the batch at the first lane below the threshold, so
+// every value, count and queue entry equals the one-lane march's.
+__global__ void __launch_bounds__(BLOCK, PSDF_COOP_MINB) march_coop_kernel(RayPassParams P, WaveBufs W) {
+    extern __shared__ __align__(16) uint32_t sm_bits[];
+    const int n_cont = (int)min(*(volatile unsigned*)(W.counters + 3), (unsigned)W.k_cap);
+    const int lane = threadIdx.x & 31;
+    const unsigned below = (1u << lane) - 1u;
+    const GridView& g = P.g;
+    const uint32_t* bits = stage_tile_bits(g, sm_bits, P.bits_sm_words);
+    __syncthreads();
+    const double tau = P.tau, h = g.h;
+    double st_photo = 0.0, st_sq = 0.0;
+    unsigned long long st_mask = 0, c_m = 0, c_x = 0, c_sh = 0, c_bwd = 0, c_ex = 0;
+    for (;;) {
+        int ki = 0;
+        if (lane == 0) ki = (int)atomicAdd(P.work_counter, 1ull);
+        ki = __shfl_sync(FULL, ki, 0);
+        if (ki >= n_cont) break;
+        const ContRec* kr = W.k_rec + ki;
+        const int slot = kr->slot;
+        const LaneRay R = lane_ray(P, slot >> 5, slot & 31);
+        Marcher mr;
+        mr.init_from(g, R.V->cam.pos, kr->dir, P.n_max, kr->t1);
+        mr.t = kr->t;
+        mr.count = kr->count;
+        mr.n_exact = kr->n_exact;
+        double t_cur = kr->t_cur, a_cur = kr->a_cur, acc = kr->acc, trans = kr->trans, depth = kr->depth,
+               t_first = kr->t_first;
+        int tile_cur = kr->tile, n_live = kr->n_live, entry = kr->entry, prev = kr->prev, head = kr->head,
+            cnt_first = kr->cnt_first, ahead = kr->ahead, aprev = kr->aprev;
+        bool have_cur = kr->flags & 1;
+        const bool in_mask = (kr->flags >> 1) & 1;
+#ifdef PSDF_MARCH_STATS
+        if (lane == 0) atomicAdd(&g_coop_stats[0], 1ull);
+#endif
+        for (;;) {
+#ifdef PSDF_MARCH_STATS
+            if (lane == 0) atomicAdd(&g_coop_stats[1], 1ull);
+#endif
+            double t_nxt = 0.0;
+            int tile_nxt = -1;
+            int4 tc_nxt;
+            SampleRun run;
+            // no saturated-run shortcut here: a batch evaluates a whole tile's
+            // lattice points at once (saturated ones to sigmoid 1 exactly)
+            const bool has_next = mr.next_run(g, t_nxt, tile_nxt, bits, &tc_nxt, 0.0, run);
+            if (!has_next && !have_cur) break;  // no sample at all
+            if (has_next && run.sat) {
+#ifdef PSDF_MARCH_STATS
+                if (lane == 0) atomicAdd(&g_coop_stats[2], 1ull);
+#endif
+                // saturated run: every settle has alpha 0 (acc, trans, depth
+                // unchanged; never terminates); its last sample is pending
+                n_live += run.n - (have_cur ? 0 : 1);
+                if (!have_cur) {
+                    have_cur = true;
+                    c_x += lane == 0;
+                }
+                t_cur = run.t_last;
+                tile_cur = tile_nxt;
+                a_cur = 1.0;
+                continue;
+            }
+            // the batch: sample 0 at t_nxt (or the one-past-the-end point
+            // t_cur + h), then the tile's next lattice points
+            const int cnt0 = mr.count;  // samples fetched including sample 0
+            int n = 1;
+            if (has_next) {
+                double v[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) v[a] = fma(mr.vd[a], t_nxt, mr.vo[a]);
+                n = (int)fmin(fmin(mr.run_length(g, v, t_nxt, h), 32.0), (double)(mr.n_max - cnt0 + 1));
+                if (n > 1) {  // the marcher continues after the batch's last point
+                    mr.t = lattice_advance(t_nxt, (double)n, h);
+                    mr.count = cnt0 + n - 1;
+                }
+            }
+#ifdef PSDF_MARCH_STATS
+            if (lane == 0) {
+                atomicAdd(&g_coop_stats[3], 1ull);
+                atomicAdd(&g_coop_stats[4], (unsigned long long)n);
+                if (n == 1) atomicAdd(&g_coop_stats[5], 1ull);
+            }
+#endif
+            const bool act = lane < n;
+            double tj = t_nxt, aj = 1.0;
+            if (act) {
+                if (lane > 0) tj = lattice_advance(t_nxt, (double)lane, h);
+                double pn[3];
+                mr.pos(has_next ? tj : dadd(t_cur, h), pn);
+                const double sv = has_next ? sample_sdf_in(g, pn[0], pn[1], pn[2], tile_nxt, tc_nxt)
+                                           : sample_sdf(g, pn[0], pn[1], pn[2]);
+                aj = sigmoid_sat(dmul(tau, sv));
+            }
+            // lane j settles the sample before it (the pending one for lane 0)
+            const double a_up = __shfl_up_sync(FULL, aj, 1), t_up = __shfl_up_sync(FULL, tj, 1);
+            const double a_prev = lane == 0 ? a_cur : a_up;
+            const double t_prev = lane == 0 ? t_cur : t_up;
+            const int tile_prev = lane == 0 ? tile_cur : tile_nxt;
+            const bool settles = act && (lane > 0 || have_cur);
+            const double alpha = (settles && aj != 1.0) ? alpha_from(a_prev, aj) : 0.0;
+            const double om = dsub(1.0, alpha);
+            double tj_before = trans;  // trans * om_0 * ... * om_{lane-1}, in order
+            for (int i = 0; i + 1 < n; ++i) {
+                const double omi = __shfl_sync(FULL, om, i);
+                if (i < lane) tj_before = dmul(tj_before, omi);
+            }
+            const double t_after = dmul(tj_before, om);
+            const bool term = settles && P.early_stop > 0.0 && t_after < P.early_stop;
+            const unsigned tm = __ballot_sync(FULL, term);
+            const int n_eff = tm ? __ffs(tm) : n;  // lanes [0, n_eff) take part
+            const bool live = settles && lane < n_eff;
+            const double w = live ? dmul(tj_before, alpha) : 0.0;
+            // first alpha > 0 settle (trainer statistics)
+            const unsigned mpos = __ballot_sync(FULL, live && alpha > 0.0);
+            if (mpos && cnt_first < 0) {
+                const int j = __ffs(mpos) - 1;
+                cnt_first = cnt0 + j - 1 - (has_next ? 1 : 0);
+                t_first = __shfl_sync(FULL, t_prev, j);
+            }
+            // ray entry (once), shading records, alpha samples
+            if (mpos && entry < 0) {
+                unsigned e0 = 0;
+                if (lane == 0) e0 = atomicAdd(W.counters + 0, 1u);
+                e0 = __shfl_sync(FULL, e0, 0);
+                entry = (int)e0 < W.e_cap ? (int)e0 : -2;  // -2: overflow, host retries
+            }
+            const bool shade = live && in_mask && w > 0.0 && tile_prev >= 0;
+            const unsigned msh = __ballot_sync(FULL, shade);
+            const unsigned mal = P.mode != 1 ? mpos : 0u;
+            unsigned br = 0, ba = 0;
+            if (lane == 0) {
+                if (msh) br = atomicAdd(W.counters + 1, (unsigned)__popc(msh));
+                if (mal) ba = atomicAdd(W.counters + 4, (unsigned)__popc(mal));
+            }
+            br = __shfl_sync(FULL, br, 0);
+            ba = __shfl_sync(FULL, ba, 0);
+            int rec_now = -1;
+            if (msh) {
+                c_sh += lane == 0 ? (unsigned long long)__popc(msh) : 0ull;
+                const int r_first = (int)br, r_last = (int)br + __popc(msh) - 1;
+                if (shade) {
+                    const int r = (int)br + __popc(msh & below);
+                    if (r < W.r_cap && entry >= 0) {
+                        rec_now = r;
+                        double pc[3];
+                        mr.pos(t_prev, pc);
+                        W.r_pos[3 * (int64_t)r] = pc[0];
+                        W.r_pos[3 * (int64_t)r + 1] = pc[1];
+                        W.r_pos[3 * (int64_t)r + 2] = pc[2];
+                        W.r_w[r] = w;
+                        W.r_tile[r] = tile_prev;
+                        W.r_entry[r] = entry;
+                        W.r_next[r] = (r < r_last && r + 1 < W.r_cap) ? r + 1 : -1;
+                    }
+                }
+                if (entry >= 0 && r_first < W.r_cap) {
+                    if (prev >= 0) {
+                        if (lane == 0) W.r_next[prev] = r_first;
+                    } else {
+                        head = r_first;
+                    }
+                    prev = min(r_last, W.r_cap - 1);
+                }
+            }
+            if (mal) {
+                const int a_first = (int)ba, a_last = (int)ba + __popc(mal) - 1;
+                if ((mal >> lane) & 1u) {
+                    const int a = (int)ba + __popc(mal & below);
+                    if (a < W.a_cap && entry >= 0) {
+                        W.a_t[2 * (int64_t)a] = t_prev;
+                        W.a_t[2 * (int64_t)a + 1] = has_next ? tj : dadd(t_cur, h);
+                        W.a_s[3 * (int64_t)a] = a_prev;
+                        W.a_s[3 * (int64_t)a + 1] = aj;
+                        W.a_s[3 * (int64_t)a + 2] = tj_before;
+                        W.a_i[a] = make_int4(tile_prev, has_next ? tile_nxt : -1, rec_now,
+                                             (a < a_last && a + 1 < W.a_cap) ? a + 1 : -1);
+                    }
+                }
+                if (entry >= 0 && a_first < W.a_cap) {
+                    if (aprev >= 0) {
+                        if (lane == 0) W.a_i[aprev].w = a_first;
+                    } else {
+                        ahead = a_first;
+                    }
+                    aprev = min(a_last, W.a_cap - 1);
+                }
+            }
+            // acc / depth in march order; the batch's settles
+            for (int i = 0; i < n_eff; ++i) {
+                const double wi = __shfl_sync(FULL, w, i);
+                if (P.mode == 1) depth = dadd(depth, dmul(wi, __shfl_sync(FULL, t_prev, i)));
+                acc = dadd(acc, wi);
+            }
+            n_live += __popc(__ballot_sync(FULL, live));
+            trans = __shfl_sync(FULL, t_after, n_eff - 1);
+            if (!have_cur) {
+                have_cur = true;
+                c_x += lane == 0;
+            }
+            if (tm || !has_next) break;  // early termination / end of the ray
+            t_cur = __shfl_sync(FULL, tj, n - 1);
+            a_cur = __shfl_sync(FULL, aj, n - 1);
+            tile_cur = tile_nxt;
+        }
+        if (lane != 0) continue;
+        c_m += n_live;
+        c_ex += mr.n_exact;
+        if (entry >= 0) {
+            W.e_slot[entry] = slot;
+            W.e_dir[3 * (int64_t)entry] = mr.d[0];
+            W.e_dir[3 * (int64_t)entry + 1] = mr.d[1];
+            W.e_dir[3 * (int64_t)entry + 2] = mr.d[2];
+            W.e_tfirst[entry] = t_first;
+            W.e_cfirst[entry] = cnt_first;
+            W.e_nlive[entry] = n_live;
+            W.e_acc[entry] = acc;
+            W.e_t1[entry] = mr.t1;
+            W.e_head[entry] = head;
+            W.e_ahead[entry] = ahead;
+            W.e_craw[3 * (int64_t)entry] = 0.0;
+            W.e_craw[3 * (int64_t)entry + 1] = 0.0;
+            W.e_craw[3 * (int64_t)entry + 2] = 0.0;
+        }
+        if (P.mode == 1) {
+            P.out_alpha[R.px] = (float)acc;
+            if (P.out_depth) P.out_depth[R.px] = (float)depth;
+            if (head < 0) {
+                const double om = dsub(1.0, acc);
+                P.out_rgb[3 * R.px] = (float)dmul(P.bg[0], om);
+                P.out_rgb[3 * R.px + 1] = (float)dmul(P.bg[1], om);
+                P.out_rgb[3 * R.px + 2] = (float)dmul(P.bg[2], om);
+            }
+        } else if (entry < 0 && cnt_first < 0) {
+            const double om = dsub(1.0, acc);
+            const double col[3] = {dmul(P.bg[0], om), dmul(P.bg[1], om), dmul(P.bg[2], om)};
+            double g0, g1, g2, dA;
+            if (photo_term(P, in_mask, R.V->gt + 3 * R.px, col, acc, g0, g1, g2, dA, st_photo, st_sq, st_mask))
+                ++c_bwd;
+        }
+    }
+    st_photo = warp_sum_d(st_photo);
+    st_sq = warp_sum_d(st_sq);
+    st_mask = warp_sum_u(st_mask);
+    c_m = warp_sum_u(c_m);
+    c_x = warp_sum_u(c_x);
+    c_sh = warp_sum_u(c_sh);
+    c_bwd = warp_sum_u(c_bwd);
+    c_ex = warp_sum_u(c_ex);
+    if (lane == 0) {
+        atomicAdd(P.counts + 6, c_ex);
+        atomicAdd(P.stats + 0, st_photo);
+        atomicAdd(P.stats + 1, st_sq);
+        atomicAdd(P.stats + 2, (double)st_mask);
+        atomicAdd(P.counts + 1, c_m);
+        atomicAdd(P.counts + 2, c_x);
+        atomicAdd(P.counts + 3, c_sh);
+        atomicAdd(P.counts + 5, c_bwd);
+    }
+}
+
 // K1 tail: colour of every rendered ray with shaded samples, c_raw + bg (1 - acc)
 // (renderer.cpp:330-335).
 __global__ void __launch_bounds__(BLOCK) render_finish_kernel(RayPassParams P, WaveBufs W) {

@@ -1,0 +1,72 @@
+"""K2a round 1 as one warp per ray (march_coop_kernel) against the one-lane
+march (march_fwd_kernel round 1, PSDF_COOP=0) on the same inputs, and against
+the oracle through the ordinary parity tests (test_gpu_train's bench view).
+
+Contract: the cooperative batch evaluates exactly the reference's samples and
+settles them in the reference's order, so every count is identical, the
+losses differ only by the f64 atomic order of their partial sums (measured
+1.4e-12 relative at the bench view; bound 1e-9), and
+the gradients only by the fp32 atomic order (check_same_schedule); the ray
+pass must actually have continuations for the comparison to mean anything."""
+import numpy as np
+import pytest
+
+from helpers import check_same_schedule, make_scene, oracle_with_f32_smooth
+
+pytestmark = pytest.mark.gpu
+
+COUNTS = ("n_rays", "n_marched", "n_extra", "n_shaded", "n_alpha", "n_bwd_rays")
+
+
+def _step(monkeypatch, coop, g, cams, gts, masks, hp, steps=2, keep=True):
+    from paper_2412_10084_b200 import api
+    monkeypatch.setenv("PSDF_COOP", "1" if coop else "0")
+    c = api.Context(0)
+    try:
+        c.upload(g, smooth=True)
+        c.keep_raypass_grads(keep)
+        c.train_reset()
+        out = []
+        for _ in range(steps):
+            losses, counts = c.train_step(cams, gts, masks, hp)
+            out.append((losses, counts, c.grads(0) if keep else None, c.grads(1), c.last_wave_counts()))
+        return out, c.download()
+    finally:
+        c.close()
+
+
+@pytest.mark.parametrize("res,size,height,tau_vox", [(512, 1600, 1200, 300.0), (256, 800, 600, 300.0),
+                                                     (128, 512, 512, 30.0)])
+def test_coop_round1_matches_one_lane(monkeypatch, res, size, height, tau_vox):
+    from oracle.refcore import RefCamera, render_opts
+    from paper_2412_10084_b200 import api
+    g, a = make_scene(res=res, n_s=4, n_a=4, sh_order=4, band=6, radius=0.32, ncam=0, jitter=0.002 * 64 / res)
+    og, sm = oracle_with_f32_smooth(a)
+    g.smooth = sm
+    cams = api.make_ring_cameras(2, size, height=height)
+    rng = np.random.default_rng(3)
+    gts, masks = [], []
+    for cam in cams:
+        oc = RefCamera()
+        for k in ("fx", "fy", "cx", "cy", "width", "height", "id"):
+            setattr(oc, k, getattr(cam, k))
+        oc.rot[:] = list(cam.rot)
+        oc.pos[:] = list(cam.pos)
+        _, alpha, _, _ = og.render_image(oc, render_opts(tau=3000.0 * res))
+        masks.append((alpha > 0.5).astype(np.uint8))
+        gts.append(rng.uniform(0, 1, (cam.height, cam.width, 3)).astype(np.float32))
+    hp = api.step_params(tau=tau_vox * res, lr_vox=1e-4, lr_mlp=6e-5, photo_scale=20.0)
+    one, p1 = _step(monkeypatch, False, g, cams, gts, masks, hp)
+    coop, p2 = _step(monkeypatch, True, g, cams, gts, masks, hp)
+    for (l1, c1, g01, g11, w1), (l2, c2, g02, g12, w2) in zip(one, coop):
+        assert w2["continuations"] > 0, w2
+        assert [c1[k] for k in COUNTS] == [c2[k] for k in COUNTS], (c1, c2)
+        assert {k: w1[k] for k in ("entries", "records", "alpha_samples")} == \
+               {k: w2[k] for k in ("entries", "records", "alpha_samples")}, (w1, w2)
+        for k in ("photo", "sdf", "eik", "normal", "features", "probes", "psnr"):
+            assert abs(l1[k] - l2[k]) <= 1e-9 * max(abs(l1[k]), 1.0), (k, l1[k], l2[k])
+        check_same_schedule(g02, g01, "ray pass")
+        check_same_schedule(g12, g11, "final")
+    for k in ("raw", "smooth", "planes", "probes", "mlp"):
+        d = np.abs(p1[k].astype(np.float64) - p2[k])
+        assert d.max() <= 1e-5 * max(np.abs(p1[k]).max(), 1e-30), (k, d.max())
