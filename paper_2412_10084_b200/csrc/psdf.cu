@@ -181,6 +181,7 @@ struct psdf_ctx {
     bool images_pending = false;           // inside psdf_train_step: the copies may still run
     cudaEvent_t ev_masks = nullptr, ev_rgb = nullptr;  // masks / colours of the step copied
     unsigned* d_hand_bits = nullptr;       // [work tiles] scan hand-over lanes
+    int64_t active_tiles = 0;              // work tiles on the scan's list (upload_viewdev)
     int64_t hand_cap = 0;
     cudaEvent_t ev_ray0 = nullptr, ev_ray1 = nullptr, ev_step0 = nullptr, ev_step1 = nullptr;
 
@@ -204,6 +205,8 @@ struct psdf_ctx {
     uint8_t* d_sat_dist = nullptr; // [T][17^3] per-cell saturation distances of the current ray pass
     int composite_steps = kComposite0Steps;
     bool coop_round1 = true;       // K2a round 1 one warp per ray (PSDF_COOP=0: one lane per ray, A/B)
+    bool fwd_mma = false;          // K2b decoder MLP on the tensor cores (PSDF_FWD_MMA=1; measured slower, A/B)
+    bool stage_fwd = true;         // K2b probe blocks bulk-copied to shared memory (PSDF_STAGE_FWD=0 off)
     int* d_tile_cnt = nullptr;     // [2T] shading records per tile, then their offsets
     void* scan_tmp = nullptr;      // CUB scan storage of the counting sort
     size_t scan_tmp_bytes = 0;
@@ -421,7 +424,7 @@ void occ_rect(const GridView& g, ViewDev& v) {
 }
 
 int64_t upload_viewdev(psdf_ctx* c, std::vector<ViewDev>& vd) {
-    int64_t tiles = 0;
+    int64_t tiles = 0, active = 0;
     const GridView g = c->view();
     for (auto& v : vd) {
         v.tiles_x = (v.cam.width + 7) / 8;
@@ -429,7 +432,18 @@ int64_t upload_viewdev(psdf_ctx* c, std::vector<ViewDev>& vd) {
         v.tile_begin = tiles;
         tiles += (int64_t)v.tiles_x * v.tiles_y;
         occ_rect(g, v);
+        // work tiles overlapping the occupancy rectangle (the scan's list)
+        v.act_begin = active;
+        v.act_tx0 = v.act_ty0 = v.act_w = v.act_n = 0;
+        if (v.occ_u1 >= v.occ_u0 && v.occ_v1 >= v.occ_v0) {
+            v.act_tx0 = v.occ_u0 / 8;
+            v.act_ty0 = v.occ_v0 / 4;
+            v.act_w = v.occ_u1 / 8 - v.act_tx0 + 1;
+            v.act_n = v.act_w * (v.occ_v1 / 4 - v.act_ty0 + 1);
+        }
+        active += v.act_n;
     }
+    c->active_tiles = active;
     if ((int)vd.size() > c->viewdev_cap) {
         if (c->d_viewdev) cudaFree(c->d_viewdev);
         CK(cudaMalloc(&c->d_viewdev, sizeof(ViewDev) * vd.size()));
@@ -611,10 +625,13 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     ensure_tile_sort(c);
     const size_t smem_f = render_smem_bytes<NS, NA>();
     const size_t smem_b = shade_bwd_smem_bytes<NS, NA>();
+    const size_t smem_fm = shade_fwd_mma_smem_bytes<NS, NA>();
     const size_t smem_bits = sizeof(uint32_t) * P.bits_sm_words;
     if (c->attr_done.insert((const void*)shade_fwd_kernel<NS, NA, true>).second) {
         CK(cudaFuncSetAttribute(shade_fwd_kernel<NS, NA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
         CK(cudaFuncSetAttribute(shade_fwd_kernel<NS, NA, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
+        CK(cudaFuncSetAttribute(shade_fwd_mma_kernel<NS, NA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fm));
+        CK(cudaFuncSetAttribute(shade_fwd_mma_kernel<NS, NA, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fm));
         CK(cudaFuncSetAttribute(shade_bwd_kernel<NS, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
         CK(cudaFuncSetAttribute(march_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(sizeof(uint32_t) * kMaxSmemBitWords)));
@@ -642,8 +659,17 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     }
     c->wave.hand_bits = W.hand_bits = c->d_hand_bits;
     // the scan reads no image: with psdf_train_step it runs under the copies
+    // the scan visits only the active work tiles; the others keep hand-over
+    // bits 0 (train: empty-ray terms) / the background (render: filled here)
     P.scan_lo = 0;
-    P.scan_hi = n_work;
+    P.scan_hi = c->active_tiles;
+    if (P.mode != 1) {
+        CK(cudaMemsetAsync(W.hand_bits, 0, sizeof(unsigned) * std::max<int64_t>(n_work, 1), s));
+    } else {
+        render_fill_kernel<<<4 * c->sm_count, 256, 0, s>>>(P, n_work);
+        CK(cudaGetLastError());
+        ++c->last_launches;
+    }
     march_scan_kernel<<<(unsigned)grid_s, BLOCK, smem_bits, s>>>(P, W);
     CK(cudaGetLastError());
     ++c->last_launches;
@@ -709,11 +735,19 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     CK(cudaGetLastError());
     c->last_launches += 3;
     CK(cudaEventRecord(c->ev_k[1], s));
-    const int grid_f = blocks_per_sm((const void*)shade_fwd_kernel<NS, NA, true>, smem_f) * c->sm_count;
-    if (P.mode == 1)  // render: no geometry records for a backward
-        shade_fwd_kernel<NS, NA, false><<<grid_f, BLOCK, smem_f, s>>>(P, W);
-    else
-        shade_fwd_kernel<NS, NA, true><<<grid_f, BLOCK, smem_f, s>>>(P, W);
+    if (c->fwd_mma) {  // decoder MLP on the tensor cores
+        const int grid_m = blocks_per_sm((const void*)shade_fwd_mma_kernel<NS, NA, true>, smem_fm) * c->sm_count;
+        if (P.mode == 1)  // render: no geometry records for a backward
+            shade_fwd_mma_kernel<NS, NA, false><<<grid_m, BLOCK, smem_fm, s>>>(P, W);
+        else
+            shade_fwd_mma_kernel<NS, NA, true><<<grid_m, BLOCK, smem_fm, s>>>(P, W);
+    } else {
+        const int grid_f = blocks_per_sm((const void*)shade_fwd_kernel<NS, NA, true>, smem_f) * c->sm_count;
+        if (P.mode == 1)
+            shade_fwd_kernel<NS, NA, false><<<grid_f, BLOCK, smem_f, s>>>(P, W);
+        else
+            shade_fwd_kernel<NS, NA, true><<<grid_f, BLOCK, smem_f, s>>>(P, W);
+    }
     CK(cudaGetLastError());
     ++c->last_launches;
     CK(cudaEventRecord(c->ev_k[2], s));
@@ -777,6 +811,7 @@ RayPassParams base_params(psdf_ctx* c) {
     P.n_max = 512;
     P.early_stop = 1e-4;
     P.bits_sm_words = c->bit_words <= kMaxSmemBitWords ? c->bit_words : 0;
+    P.stage_fwd = c->stage_fwd;
     P.work_counter = c->d_work;
     P.counts = c->d_counts;
     P.stats = c->d_stats;
@@ -1089,6 +1124,8 @@ int psdf_create(int device, psdf_ctx** out) {
         if (const char* e = std::getenv("PSDF_COMPOSITE_STEPS")) c->composite_steps = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("PSDF_WAVE_INIT")) c->wave_init = std::max(0, std::atoi(e));
         if (const char* e = std::getenv("PSDF_COOP")) c->coop_round1 = std::atoi(e) != 0;
+        if (const char* e = std::getenv("PSDF_FWD_MMA")) c->fwd_mma = std::atoi(e) != 0;
+        if (const char* e = std::getenv("PSDF_STAGE_FWD")) c->stage_fwd = std::atoi(e) != 0;
         if (const char* e = std::getenv("PSDF_REGS_EARLY")) c->regs_early = std::atoi(e) != 0;
         if (const char* m = std::getenv("PSDF_TEST_MARGIN")) c->test_margin = std::max(1e-8, std::atof(m));
         CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));

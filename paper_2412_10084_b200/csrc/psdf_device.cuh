@@ -825,6 +825,33 @@ __device__ __forceinline__ VecF<N> ldg_vec(const float* p) {
     return r;
 }
 
+// The same from shared memory (a staged block).
+template <int N>
+__device__ __forceinline__ VecF<N> lds_vec(const float* p) {
+    VecF<N> r;
+    if constexpr (N % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < N / 4; ++i) {
+            const float4 q = reinterpret_cast<const float4*>(p)[i];
+            r.v[4 * i] = q.x;
+            r.v[4 * i + 1] = q.y;
+            r.v[4 * i + 2] = q.z;
+            r.v[4 * i + 3] = q.w;
+        }
+    } else if constexpr (N % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < N / 2; ++i) {
+            const float2 q = reinterpret_cast<const float2*>(p)[i];
+            r.v[2 * i] = q.x;
+            r.v[2 * i + 1] = q.y;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) r.v[i] = p[i];
+    }
+    return r;
+}
+
 // Vector atomics (sm_90+ float2/float4 red.global.add).
 template <int N>
 __device__ __forceinline__ void red_vec(float* p, const float* v) {

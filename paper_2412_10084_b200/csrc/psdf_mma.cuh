@@ -77,6 +77,38 @@ __device__ __forceinline__ void warp_gemm3(float (&c)[MT][NT][4], FA A, FB B) {
     }
 }
 
+// As warp_gemm3, with B already split (constant weights staged once per block
+// as TF32 hi / lo words): Bh(n, k) / Bl(n, k) -> uint32.  Halves the split
+// work of the weight GEMMs.
+template <int MT, int NT, int KT, class FA, class FBH, class FBL>
+__device__ __forceinline__ void warp_gemm3w(float (&c)[MT][NT][4], FA A, FBH Bh, FBL Bl) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) {
+        const int k0 = kt * 8;
+        Split4 a[MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            const int m0 = mt * 16;
+            const float v[4] = {A(m0 + g, k0 + t), A(m0 + g + 8, k0 + t), A(m0 + g, k0 + t + 4),
+                                A(m0 + g + 8, k0 + t + 4)};
+            split<4>(v, a[mt]);
+        }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            const int n0 = nt * 8;
+            const uint32_t bh[2] = {Bh(n0 + g, k0 + t), Bh(n0 + g, k0 + t + 4)};
+            const uint32_t bl[2] = {Bl(n0 + g, k0 + t), Bl(n0 + g, k0 + t + 4)};
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                mma_tf32(c[mt][nt], a[mt].lo, bh);
+                mma_tf32(c[mt][nt], a[mt].hi, bl);
+                mma_tf32(c[mt][nt], a[mt].hi, bh);
+            }
+        }
+    }
+}
+
 // Visits every C element held by this lane: f(m, n, value&).
 template <int MT, int NT, class F>
 __device__ __forceinline__ void for_c(float (&c)[MT][NT][4], F f) {

@@ -19,6 +19,7 @@
 // subtraction enters ds only multiplied by (1 - alpha_i), see DESIGN.md.
 #pragma once
 
+#include "psdf_bulk.cuh"
 #include "psdf_device.cuh"
 
 namespace psdf {
@@ -42,6 +43,11 @@ struct ViewDev {
     // projection, padded by 2 pixels (the whole image when the camera is not
     // in front of every box corner); rays outside yield no sample
     int occ_u0, occ_u1, occ_v0, occ_v1;
+    // the work tiles (8x4 pixels) that overlap that rectangle: the scan's
+    // work list is these tiles only (the others have no sample: their rays
+    // are the empty-ray term, hand-over bits 0)
+    int act_tx0, act_ty0, act_w, act_n;
+    int64_t act_begin;    // first active tile of this view in the batch's active list
 };
 
 struct RayPassParams {
@@ -53,12 +59,13 @@ struct RayPassParams {
     int n_max;
     int mode;             // 0: train ray pass, 1: render (K1 through the same pipeline)
     int bits_sm_words;    // words of the tile bitmap staged in shared memory (0 = use global)
+    int stage_fwd;        // K2b: bulk-copy the tiles' probe blocks into shared memory
     double tau, early_stop, bg[3];
     double photo_scale;
     const ViewDev* views;
     int n_views;
     int64_t tile_begin, tile_end;  // this rank's slice of the global work tiles
-    int64_t scan_lo, scan_hi;      // K2a-scan: local work tiles [lo, hi) of this launch
+    int64_t scan_lo, scan_hi;      // K2a-scan: active-tile list range [lo, hi) (ViewDev::act_*)
     unsigned long long* work_counter;
     // render outputs (K1)
     float* out_rgb;
@@ -169,7 +176,8 @@ struct GeoRec {
 template <int NS, int NA>
 __device__ __forceinline__ void decode_features(const RayPassParams& P, int tile, const double p[3],
                                                 const double dneg[3], ShadeGeo& geo,
-                                                float x[NS + NA + NPOW], float pv[3][NS]) {
+                                                float x[NS + NA + NPOW], float pv[3][NS],
+                                                const float* psm = nullptr) {
     const GridView& g = P.g;
     const double h = g.h;
     // central-difference normal of the smoothed SDF, exact f64
@@ -257,20 +265,33 @@ __device__ __forceinline__ void decode_features(const RayPassParams& P, int tile
         const int nc = P.order * P.order;
         const int stride = g.order * g.order * NA;
         const int32_t* pid = g.probe_ids + (int64_t)tile * 8;
+        // psm: the tile's 8 probe blocks staged in shared memory (ProbeStage)
 #pragma unroll 1
         for (int i = 0; i < 8; ++i) {
             const float w = geo.w8[i];
             if (w == 0.f) continue;
-            const float* c = g.probes + (int64_t)__ldg(pid + i) * stride;
             float acc[NA];
 #pragma unroll
             for (int k = 0; k < NA; ++k) acc[k] = 0.f;
+            if (psm) {
+                const float* c = psm + i * stride;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                if (j < nc) {
-                    const VecF<NA> cv = ldg_vec<NA>(c + j * NA);
+                for (int j = 0; j < 16; ++j) {
+                    if (j < nc) {
+                        const VecF<NA> cv = lds_vec<NA>(c + j * NA);
 #pragma unroll
-                    for (int k = 0; k < NA; ++k) acc[k] += Y[j] * cv.v[k];
+                        for (int k = 0; k < NA; ++k) acc[k] += Y[j] * cv.v[k];
+                    }
+                }
+            } else {
+                const float* c = g.probes + (int64_t)__ldg(pid + i) * stride;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    if (j < nc) {
+                        const VecF<NA> cv = ldg_vec<NA>(c + j * NA);
+#pragma unroll
+                        for (int k = 0; k < NA; ++k) acc[k] += Y[j] * cv.v[k];
+                    }
                 }
             }
 #pragma unroll
@@ -345,10 +366,11 @@ template <int NS, int NA>
 __device__ __forceinline__ void decode_forward(const RayPassParams& P, const float* __restrict__ sm,
                                                const SmemMlp& L, int tile, const double p[3],
                                                const double dneg[3], const float* cam_row,
-                                               float rgb[3], ShadeGeo& geo, float* geo_out) {
+                                               float rgb[3], ShadeGeo& geo, float* geo_out,
+                                               const float* psm = nullptr) {
     constexpr int IN = NS + NA + NPOW;
     float x[IN], pv[3][NS];
-    decode_features<NS, NA>(P, tile, p, dneg, geo, x, pv);
+    decode_features<NS, NA>(P, tile, p, dneg, geo, x, pv, psm);
     mlp_forward<IN>(sm, L, x, cam_row, rgb, nullptr, nullptr);
     if (geo_out) store_geo<NS, NA>(geo, pv, x, geo_out);
 }
@@ -403,6 +425,16 @@ __device__ __forceinline__ unsigned long long warp_sum_u(unsigned long long v) {
     return v;
 }
 
+// The scan's k-th active work tile (ViewDev::act_*) as a global work tile.
+__device__ __forceinline__ int64_t active_tile(const RayPassParams& P, int64_t k) {
+    int v = 0;
+    while (v + 1 < P.n_views && P.views[v + 1].act_begin <= k) ++v;
+    const ViewDev& V = P.views[v];
+    const int64_t a = k - V.act_begin;
+    const int ay = (int)(a / V.act_w), ax = (int)(a - (int64_t)ay * V.act_w);
+    return V.tile_begin + (int64_t)(V.act_ty0 + ay) * V.tiles_x + V.act_tx0 + ax;
+}
+
 // Maps a global work tile to (view, pixel) for this lane.
 __device__ __forceinline__ int locate_view(const RayPassParams& P, int64_t tile) {
     int v = 0;
@@ -425,9 +457,17 @@ __device__ __forceinline__ void load_mlp_smem(const float* __restrict__ mlp, flo
     }
 }
 
+// Per-warp probe staging (ProbeStage): two slots of 8 probe blocks of at most
+// 16 coefficients x n_a floats.
+template <int NA>
+constexpr int probe_stage_floats() {
+    return 2 * 8 * 16 * NA;
+}
+__host__ __device__ constexpr int up4i(int x) { return (x + 3) & ~3; }
+
 template <int NS, int NA>
 size_t render_smem_bytes() {
-    return sizeof(float) * SmemMlp::make(NS + NA + NPOW).total;
+    return sizeof(float) * (up4i(SmemMlp::make(NS + NA + NPOW).total) + WARPS_PER_BLOCK * probe_stage_floats<NA>());
 }
 
 }  // namespace psdf

@@ -201,10 +201,15 @@ __global__ void __launch_bounds__(BLOCK, PSDF_SCAN_MINB) march_scan_kernel(RayPa
     unsigned long long st_mask = 0;
     unsigned c_m = 0, c_x = 0, c_bwd = 0, c_ex = 0;
     for (;;) {
-        int wi = 0;
-        if (lane == 0) wi = (int)(P.scan_lo + atomicAdd(P.work_counter, 1ull));
-        wi = __shfl_sync(FULL, wi, 0);
-        if (wi >= P.scan_hi) break;
+        // the next active work tile (overlapping some view's projected box of
+        // the allocated tiles) inside this rank's slice
+        long long ak = 0;
+        if (lane == 0) ak = (long long)(P.scan_lo + atomicAdd(P.work_counter, 1ull));
+        ak = __shfl_sync(FULL, ak, 0);
+        if (ak >= P.scan_hi) break;
+        const int64_t gt = active_tile(P, ak);
+        if (gt < P.tile_begin || gt >= P.tile_end) continue;
+        const int wi = (int)(gt - P.tile_begin);
         const LaneRay R = lane_ray(P, wi, lane);
         Marcher mr;
         int k = 0, tile_prev = -1;
@@ -289,6 +294,22 @@ __global__ void __launch_bounds__(BLOCK, PSDF_SCAN_MINB) march_scan_kernel(RayPa
         atomicAdd(P.counts + 1, m);
         atomicAdd(P.counts + 2, x);
         atomicAdd(P.counts + 5, bw);
+    }
+}
+
+// K1: every pixel of this pass's work tiles starts as background with zero
+// opacity and depth (renderer.cpp:330-335 for a ray without samples); the
+// scan / composite pass overwrite the pixels of the active tiles.
+__global__ void __launch_bounds__(256) render_fill_kernel(RayPassParams P, int64_t n_work) {
+    const int64_t n = n_work * 32;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        const LaneRay R = lane_ray(P, (int)(q >> 5), (int)(q & 31));
+        if (!R.valid) continue;
+        P.out_rgb[3 * R.px] = (float)P.bg[0];
+        P.out_rgb[3 * R.px + 1] = (float)P.bg[1];
+        P.out_rgb[3 * R.px + 2] = (float)P.bg[2];
+        P.out_alpha[R.px] = 0.f;
+        if (P.out_depth) P.out_depth[R.px] = 0.f;
     }
 }
 
@@ -985,12 +1006,28 @@ __global__ void __launch_bounds__(BLOCK, PSDF_FWD_MINB) shade_fwd_kernel(RayPass
     const int n_rec = n_records(W);
     constexpr int IN = NS + NA + NPOW;
     extern __shared__ __align__(16) float smem[];
+    __shared__ uint64_t s_bar[WARPS_PER_BLOCK];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const SmemMlp L = SmemMlp::make(IN);
     const MlpLayout G = MlpLayout::make(IN);
+    ProbeStage ps;
+    ps.init(smem + up4i(L.total) + warp * probe_stage_floats<NA>(), &s_bar[warp], P.g.order * P.g.order * NA);
     load_mlp_smem(P.mlp, smem, G, L);
     __syncthreads();
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_rec; q += gridDim.x * blockDim.x) {
-        const int i = W.r_perm[q];
+    const bool stage = P.stage_fwd && !P.no_angular;
+    // one record per lane; a warp's 32 records are consecutive in tile order,
+    // and the probe blocks of their first / last tile are bulk-copied into
+    // this warp's staging slots
+    for (int base = (blockIdx.x * WARPS_PER_BLOCK + warp) * 32; base < n_rec; base += gridDim.x * BLOCK) {
+        const bool in_range = base + lane < n_rec;
+        const int i = in_range ? W.r_perm[base + lane] : 0;
+        const int tile = in_range ? W.r_tile[i] : -1;
+        const float* psm = nullptr;
+        if (stage) {
+            const int tA = __shfl_sync(FULL, tile, 0), tB = __shfl_sync(FULL, tile, min(31, n_rec - 1 - base));
+            psm = ps.fetch(tA, tB, tile, P.g.probes, P.g.probe_ids);
+        }
+        if (!in_range) continue;
         const int e = W.r_entry[i];
         const ViewDev& V = entry_view(P, W, e);
         const float* cam_row =
@@ -1001,13 +1038,172 @@ __global__ void __launch_bounds__(BLOCK, PSDF_FWD_MINB) shade_fwd_kernel(RayPass
                                 -W.e_dir[3 * (int64_t)e + 2]};
         float rgb[3];
         ShadeGeo geo;
-        decode_forward<NS, NA>(P, smem, L, W.r_tile[i], pc, dneg, cam_row, rgb, geo,
-                               GEO ? W.r_geo + (int64_t)i * GeoRec<NS, NA>::STRIDE : nullptr);
+        decode_forward<NS, NA>(P, smem, L, tile, pc, dneg, cam_row, rgb, geo,
+                               GEO ? W.r_geo + (int64_t)i * GeoRec<NS, NA>::STRIDE : nullptr, psm);
         reinterpret_cast<float4*>(W.r_c)[i] = make_float4(rgb[0], rgb[1], rgb[2], 0.f);
         const double w = W.r_w[i];
         atomicAdd(W.e_craw + 3 * (int64_t)e, dmul((double)rgb[0], w));
         atomicAdd(W.e_craw + 3 * (int64_t)e + 1, dmul((double)rgb[1], w));
         atomicAdd(W.e_craw + 3 * (int64_t)e + 2, dmul((double)rgb[2], w));
+    }
+}
+
+// K2b on the tensor cores: decode_features per lane (one shading record per
+// lane, records in tile order), then the decoder MLP for the warp's 32
+// records as three warp GEMMs (3xTF32 mma.sync, weights pre-split in shared
+// memory once per block): A1 = relu(X W1^T + b1 (+ camera bias)), A2 =
+// relu(A1 W2^T + b2), Z = A2 W3^T + b3, colour = sigmoid(Z).  The FFMA
+// form (shade_fwd_kernel) spends ~42 % of its instructions on the MLP
+// (profiles/r02/v3); here it is ~170 MMAs per 32 records.
+template <int IN>
+struct FwdDims {
+    static constexpr int K1 = (IN + 7) & ~7;  // input width padded to the MMA k step
+    static constexpr int XS = K1 + 4;         // row stride of W1 (conflict-free B fragments)
+    static constexpr int HS = 36;             // row stride of 32-wide rows
+    // pre-split weights (uint32 TF32 words): hi, then lo
+    static constexpr int W1 = 0;              // [32][XS]
+    static constexpr int W2 = W1 + 32 * XS;   // [32][HS]
+    static constexpr int W3 = W2 + 32 * HS;   // [8][HS], rows 3..7 zero
+    static constexpr int WN = W3 + 8 * HS;    // words per split half
+    static constexpr int B1 = 2 * WN, B2 = B1 + 32, B3 = B2 + 32;  // biases (float)
+    static constexpr int MLP = B3 + 4;
+    // per-warp scratch: S0 = X (row stride HS), later A2; S1 = A1, later Z
+    static constexpr int S0 = 0, S1 = 32 * HS, SCR = 64 * HS;
+};
+
+template <int NS, int NA>
+size_t shade_fwd_mma_smem_bytes() {
+    using D = FwdDims<NS + NA + NPOW>;
+    return sizeof(float) * (D::MLP + WARPS_PER_BLOCK * (D::SCR + probe_stage_floats<NA>()));
+}
+
+#ifndef PSDF_FWDM_MINB
+#define PSDF_FWDM_MINB 4
+#endif
+template <int NS, int NA, bool GEO>
+__global__ void __launch_bounds__(BLOCK, PSDF_FWDM_MINB) shade_fwd_mma_kernel(RayPassParams P, WaveBufs W) {
+    const int n_rec = n_records(W);
+    constexpr int IN = NS + NA + NPOW;
+    using D = FwdDims<IN>;
+    extern __shared__ __align__(16) float smem[];
+    uint32_t* wsp = reinterpret_cast<uint32_t*>(smem);
+    const MlpLayout G = MlpLayout::make(IN);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // weights, split once: W1 [32][IN] (zero padded to K1), W2 [32][32], W3 [3][32]
+    for (int i = threadIdx.x; i < D::WN; i += blockDim.x) {
+        float v = 0.f;
+        if (i < D::W2) {
+            const int j = i / D::XS, k = i % D::XS;
+            if (k < IN) v = __ldg(P.mlp + G.w1 + j * IN + k);
+        } else if (i < D::W3) {
+            const int j = (i - D::W2) / D::HS, k = (i - D::W2) % D::HS;
+            if (k < 32) v = __ldg(P.mlp + G.w2 + j * 32 + k);
+        } else {
+            const int j = (i - D::W3) / D::HS, k = (i - D::W3) % D::HS;
+            if (j < 3 && k < 32) v = __ldg(P.mlp + G.w3 + j * 32 + k);
+        }
+        const uint32_t hi = tf32(v);
+        wsp[i] = hi;
+        wsp[D::WN + i] = tf32(v - __uint_as_float(hi));
+    }
+    for (int i = threadIdx.x; i < 32; i += blockDim.x) {
+        smem[D::B1 + i] = __ldg(P.mlp + G.b1 + i);
+        smem[D::B2 + i] = __ldg(P.mlp + G.b2 + i);
+        if (i < 3) smem[D::B3 + i] = __ldg(P.mlp + G.b3 + i);
+    }
+    __syncthreads();
+    float* S0 = smem + D::MLP + warp * D::SCR + D::S0;
+    float* S1 = smem + D::MLP + warp * D::SCR + D::S1;
+    __shared__ uint64_t s_bar[WARPS_PER_BLOCK];
+    ProbeStage ps;
+    ps.init(smem + D::MLP + WARPS_PER_BLOCK * D::SCR + warp * probe_stage_floats<NA>(), &s_bar[warp],
+            P.g.order * P.g.order * NA);
+    __shared__ int s_cam[WARPS_PER_BLOCK][32];
+    int* cam = s_cam[warp];
+    const float* cam_base = P.mlp + G.cam;
+    const int warps_total = gridDim.x * WARPS_PER_BLOCK;
+    for (int base = (blockIdx.x * WARPS_PER_BLOCK + warp) * 32; base < n_rec; base += warps_total * 32) {
+        const bool in_range = base + lane < n_rec;
+        int i = 0, e = 0, cam_row = -1;
+        float x[IN];
+#pragma unroll
+        for (int k = 0; k < IN; ++k) x[k] = 0.f;
+        if (in_range) i = W.r_perm[base + lane];
+        const int tile = in_range ? W.r_tile[i] : -1;
+        const float* psm = nullptr;
+        if (P.stage_fwd && !P.no_angular) {
+            const int tA = __shfl_sync(FULL, tile, 0), tB = __shfl_sync(FULL, tile, min(31, n_rec - 1 - base));
+            psm = ps.fetch(tA, tB, tile, P.g.probes, P.g.probe_ids);
+        }
+        if (in_range) {
+            e = W.r_entry[i];
+            const ViewDev& V = entry_view(P, W, e);
+            if (P.ncam > 0 && V.cam_bias_row >= 0) cam_row = V.cam_bias_row;
+            const double pc[3] = {W.r_pos[3 * (int64_t)i], W.r_pos[3 * (int64_t)i + 1],
+                                  W.r_pos[3 * (int64_t)i + 2]};
+            const double dneg[3] = {-W.e_dir[3 * (int64_t)e], -W.e_dir[3 * (int64_t)e + 1],
+                                    -W.e_dir[3 * (int64_t)e + 2]};
+            ShadeGeo geo;
+            float pv[3][NS];
+            decode_features<NS, NA>(P, tile, pc, dneg, geo, x, pv, psm);
+            if (GEO) store_geo<NS, NA>(geo, pv, x, W.r_geo + (int64_t)i * GeoRec<NS, NA>::STRIDE);
+        }
+#pragma unroll
+        for (int k = 0; k < D::K1; ++k) S0[lane * D::HS + k] = k < IN ? x[k] : 0.f;
+        cam[lane] = cam_row;
+        __syncwarp();
+        {  // A1 = relu(X W1^T + b1 + camera bias)
+            float c[2][4][4];
+            zero_c(c);
+            warp_gemm3w<2, 4, D::K1 / 8>(
+                c, [&](int m, int k) { return S0[m * D::HS + k]; },
+                [&](int n, int k) { return wsp[D::W1 + n * D::XS + k]; },
+                [&](int n, int k) { return wsp[D::WN + D::W1 + n * D::XS + k]; });
+            for_c(c, [&](int m, int n, float& v) {
+                float z = v + smem[D::B1 + n];
+                if (cam[m] >= 0) z += __ldg(cam_base + cam[m] * HID + n);
+                S1[m * D::HS + n] = z > 0.f ? z : 0.f;
+            });
+        }
+        __syncwarp();
+        {  // A2 = relu(A1 W2^T + b2)  (into S0: X is dead)
+            float c[2][4][4];
+            zero_c(c);
+            warp_gemm3w<2, 4, 4>(
+                c, [&](int m, int k) { return S1[m * D::HS + k]; },
+                [&](int n, int k) { return wsp[D::W2 + n * D::HS + k]; },
+                [&](int n, int k) { return wsp[D::WN + D::W2 + n * D::HS + k]; });
+            __syncwarp();
+            for_c(c, [&](int m, int n, float& v) {
+                const float z = v + smem[D::B2 + n];
+                S0[m * D::HS + n] = z > 0.f ? z : 0.f;
+            });
+        }
+        __syncwarp();
+        {  // Z = A2 W3^T (columns 0..2 of one 8-wide tile), into S1
+            float c[2][1][4];
+            zero_c(c);
+            warp_gemm3w<2, 1, 4>(
+                c, [&](int m, int k) { return S0[m * D::HS + k]; },
+                [&](int n, int k) { return wsp[D::W3 + n * D::HS + k]; },
+                [&](int n, int k) { return wsp[D::WN + D::W3 + n * D::HS + k]; });
+            __syncwarp();
+            for_c(c, [&](int m, int n, float& v) {
+                if (n < 3) S1[m * 4 + n] = v;
+            });
+        }
+        __syncwarp();
+        if (in_range) {
+            float rgb[3];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) rgb[j] = sigmoidf_(S1[lane * 4 + j] + smem[D::B3 + j]);
+            reinterpret_cast<float4*>(W.r_c)[i] = make_float4(rgb[0], rgb[1], rgb[2], 0.f);
+            const double w = W.r_w[i];
+            atomicAdd(W.e_craw + 3 * (int64_t)e, dmul((double)rgb[0], w));
+            atomicAdd(W.e_craw + 3 * (int64_t)e + 1, dmul((double)rgb[1], w));
+            atomicAdd(W.e_craw + 3 * (int64_t)e + 2, dmul((double)rgb[2], w));
+        }
+        __syncwarp();
     }
 }
 
