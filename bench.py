@@ -309,6 +309,9 @@ def workload_name():
     return f"configs[4] sweep point: synthetic {W['scene']} at {W['res']}^3"
 
 
+EXCHANGE = ["allreduce"]  # --grad-exchange (set in main)
+
+
 def config_dict(world):
     shape = "sphere r=0.32" if W["scene"] == "sphere" else f"{W['scene']} union (api.SCENE_PRIMS)"
     return {"workload": f"{workload_name()}, {W['res']}^3 sparse SDF grid ({shape}, band 6), probes at tile "
@@ -318,7 +321,7 @@ def config_dict(world):
                         f"({W['scaling']} scaling), tau={TAU_VOX:g}/voxel",
             "global_batch_views": global_batch(world),
             "rays_per_step": global_batch(world) * W["width"] * W["height"],
-            "parallelism": f"dp{world} (ray-batch data parallel, NCCL all-reduce of grid gradients)",
+            "parallelism": f"dp{world} (ray-batch data parallel, NCCL {EXCHANGE[0]} of grid gradients)",
             "l2": "no flush; per-step working set (params+grads+Adam moments 4x83 MB, smoothed SDF "
                   "47 MB + apron 66 MB, the batch's images >= 100 MB) exceeds the 126 MB L2"}
 
@@ -345,6 +348,8 @@ def main():
     ap.add_argument("--views", type=int, default=None)
     ap.add_argument("--width", type=int, default=None)
     ap.add_argument("--height", type=int, default=None)
+    ap.add_argument("--grad-exchange", choices=["allreduce", "bucketed", "sharded"], default="allreduce",
+                    help="how ranks combine gradients (psdf_set_grad_exchange; N > 1 only)")
     ap.add_argument("--profile", action="store_true",
                     help="setup + warm-up + 2 train steps + 1 render, no JSON (for ncu)")
     args = ap.parse_args()
@@ -392,6 +397,9 @@ def main():
             uid.copy_(torch.frombuffer(bytearray(api.Context.unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
         ctx.comm_init(bytes(uid.cpu().numpy().tobytes()), rank, world)
+        ctx.set_grad_exchange(args.grad_exchange)
+    EXCHANGE[0] = {"allreduce": "all-reduce", "bucketed": "bucketed all-reduce (planes/probes/MLP under the fold)",
+                   "sharded": "reduce-scatter + sharded Adam + all-gather"}[args.grad_exchange]
 
     g, tgt = build_scene(api, seed=1)
     cams = cameras(api)

@@ -80,7 +80,14 @@ typedef struct {
 /* SparseGrid metadata (grid.hpp:57-70). */
 typedef struct {
     int32_t T, P;              /* allocated tiles, pool probes */
-    int32_t n_s, n_a, sh_order;
+    int32_t n_s, n_a, sh_order; /* channel widths: the kernels are instantiated for
+                                  (n_s, n_a) in {(2,2), (4,4), (8,8), (4,8), (8,4)}
+                                  (the paper's configurations and their neighbours);
+                                  the reference's DecoderMlp accepts any width
+                                  (decoder.hpp:17-31), here any other pair is
+                                  PSDF_ERR_INVALID_ARGUMENT at psdf_upload_grid /
+                                  psdf_init_visual_hull / psdf_load_checkpoint
+                                  ("unsupported (n_s, n_a)"), before any work */
     int32_t res[3];            /* voxels per axis, multiples of 16 */
     double voxel_size;
     double origin[3];
@@ -253,6 +260,18 @@ int psdf_comm_init(psdf_ctx* ctx, const void* unique_id, int rank, int world_siz
  * the all-reduce, so the stage-1 gradients of the N slices sum to the
  * one-rank gradients (tests/test_gpu_shard.py). */
 int psdf_debug_set_shard(psdf_ctx* ctx, int rank, int world_size);
+/* How the ranks combine gradients each step (effective with a communicator):
+   ALLREDUCE (default): G^T fold, then one all-reduce of the flat gradient;
+   BUCKETED: the [planes | probes | mlp] bucket all-reduced on a second stream
+     under the fold, then the raw-SDF bucket;
+   SHARDED: fold, reduce-scatter into world-size chunks, Adam on this rank's
+     chunk, all-gather of the updated parameters (same bytes as an
+     all-reduce, 1/N of the Adam work per rank).
+   All three give every rank the same parameters as the single-rank step
+   (with SHARDED, psdf_download_grads(stage 1) holds the summed gradient only
+   on this rank's chunk). */
+enum { PSDF_EXCHANGE_ALLREDUCE = 0, PSDF_EXCHANGE_BUCKETED = 1, PSDF_EXCHANGE_SHARDED = 2 };
+int psdf_set_grad_exchange(psdf_ctx* ctx, int mode);
 /* Diagnostics: raw copy of n items of one ray-pass queue of the last pass
    (psdf.cu psdf_debug_wave lists the queues and item sizes). */
 int psdf_debug_wave(psdf_ctx* ctx, int which, void* out, int64_t n);

@@ -8,9 +8,10 @@
 // with sdfrecon_gpu::render_image / sdfrecon_gpu::train (same arguments,
 // same return types, same exceptions).  The reference's own types
 // (SparseGrid, DecoderMlp, Camera, RenderOptions, Dataset, TrainSchedule,
-// Checkpoint) are used unchanged; the per-LOD machinery that is not on the
-// hot path (raise_sh_order, subdivide, image downscaling) stays the
-// reference's host code.
+// Checkpoint) are used unchanged.  Inside train() the grid stays resident on
+// the device across LODs: raise_sh_order and subdivide run there
+// (psdf_raise_sh_order / psdf_subdivide, same tile and probe order as the
+// reference); only the per-LOD image downscaling stays host code.
 #pragma once
 
 #include <algorithm>
@@ -354,6 +355,22 @@ inline double psnr_masked_render(Device& dev, const sdfrecon::Camera& camera, co
     double psnr = 0.0;
     check(psdf_eval_psnr(dev.ctx(), &c, &o, g.data(), m.data(), &psnr, nullptr), dev.ctx());
     return psnr;
+}
+
+// marching_cubes (mesh.hpp:24, mesh.cpp:363-394) of the grid resident on
+// `dev`: the reference's mesh exactly (same vertices, same triangle order).
+inline sdfrecon::TriMesh marching_cubes(Device& dev) {
+    int64_t nv = 0, nt = 0;
+    check(psdf_marching_cubes(dev.ctx(), &nv, &nt), dev.ctx());
+    std::vector<double> v(3 * (size_t)nv);
+    std::vector<int32_t> t(3 * (size_t)nt);
+    check(psdf_download_mesh(dev.ctx(), v.data(), t.data()), dev.ctx());
+    sdfrecon::TriMesh m;
+    m.vertices.resize((size_t)nv);
+    for (int64_t i = 0; i < nv; ++i) m.vertices[i] = sdfrecon::Vec3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+    m.triangles.resize((size_t)nt);
+    for (int64_t i = 0; i < nt; ++i) m.triangles[i] = {t[3 * i], t[3 * i + 1], t[3 * i + 2]};
+    return m;
 }
 
 // Same signature as sdfrecon::chamfer (metrics.hpp:46-48); the point-to-mesh

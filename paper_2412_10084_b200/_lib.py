@@ -86,7 +86,7 @@ EXPORTS = [
     "psdf_raise_sh_order", "psdf_last_h2d_bytes", "psdf_init_visual_hull", "psdf_save_checkpoint",
     "psdf_load_checkpoint", "psdf_eval_psnr", "psdf_point_mesh_distance", "psdf_chamfer",
     "psdf_debug_set_shard", "psdf_marching_cubes", "psdf_download_mesh",
-    "psdf_last_wave_counts", "psdf_debug_wave",
+    "psdf_last_wave_counts", "psdf_debug_wave", "psdf_set_grad_exchange",
 ]
 
 _lib = None
@@ -152,6 +152,7 @@ def load():
     L.psdf_last_k2_breakdown.argtypes = [vp, _dp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     L.psdf_last_wave_counts.argtypes = [vp, C.POINTER(C.c_int64)]
     L.psdf_debug_wave.argtypes = [vp, C.c_int, vp, C.c_int64]
+    L.psdf_set_grad_exchange.argtypes = [vp, C.c_int]
     L.psdf_grid_info.argtypes = [vp, C.POINTER(psdf_grid_desc)]
     L.psdf_download_structure.argtypes = [vp, _ip, _ip, _ip]
     L.psdf_subdivide.argtypes = [vp, C.c_double, _ip, _ip]

@@ -669,6 +669,15 @@ class Context:
         return r.value, s.value, n.value
 
     # -- multi-GPU
+    GRAD_EXCHANGE = {"allreduce": 0, "bucketed": 1, "sharded": 2}
+
+    def set_grad_exchange(self, mode):
+        """How ranks combine gradients (psdf.h psdf_set_grad_exchange):
+        'allreduce' (default), 'bucketed' (planes/probes/MLP bucket reduced
+        under the fold) or 'sharded' (reduce-scatter, Adam on this rank's
+        chunk, all-gather)."""
+        self._check(self.L.psdf_set_grad_exchange(self.h, self.GRAD_EXCHANGE[mode]))
+
     @staticmethod
     def unique_id() -> bytes:
         L = _lib.load()

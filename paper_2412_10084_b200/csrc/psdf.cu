@@ -83,6 +83,9 @@ struct Nccl {
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
+    ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                  cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 
@@ -95,9 +98,12 @@ struct Nccl {
         GetUniqueId = (decltype(GetUniqueId))dlsym(so, "ncclGetUniqueId");
         CommInitRank = (decltype(CommInitRank))dlsym(so, "ncclCommInitRank");
         AllReduce = (decltype(AllReduce))dlsym(so, "ncclAllReduce");
+        ReduceScatter = (decltype(ReduceScatter))dlsym(so, "ncclReduceScatter");
+        AllGather = (decltype(AllGather))dlsym(so, "ncclAllGather");
         CommDestroy = (decltype(CommDestroy))dlsym(so, "ncclCommDestroy");
         GetErrorString = (decltype(GetErrorString))dlsym(so, "ncclGetErrorString");
-        if (!GetUniqueId || !CommInitRank || !AllReduce || !CommDestroy || !GetErrorString)
+        if (!GetUniqueId || !CommInitRank || !AllReduce || !ReduceScatter || !AllGather || !CommDestroy ||
+            !GetErrorString)
             fail(PSDF_ERR_NCCL, "libnccl.so.2 lacks the expected symbols");
     }
 };
@@ -159,6 +165,11 @@ int64_t up4(int64_t x) { return (x + 3) & ~int64_t(3); }
 
 // K2a round 0 steps before the remaining rays continue, compacted, in round 1.
 constexpr int kComposite0Steps = 16;  // default; PSDF_COMPOSITE_STEPS overrides (tuning)
+
+// Zero floats after the flat parameter / gradient / moment vectors: the
+// sharded exchange splits them into world-size chunks of a multiple of 4
+// floats (<= n_params + 4 * world).
+constexpr int64_t kParamPad = 4096;
 
 // Tile bitmaps up to 32 KB (1024^3 grids) are staged in shared memory.
 constexpr int kMaxSmemBitWords = 8192;
@@ -253,6 +264,9 @@ struct psdf_ctx {
 
     ncclComm_t comm = nullptr;
     int rank = 0, world = 1;
+    int grad_exchange = PSDF_EXCHANGE_ALLREDUCE;  // psdf_set_grad_exchange
+    cudaStream_t comm_stream = nullptr;           // bucketed exchange: the [planes|probes|mlp] bucket
+    cudaEvent_t ev_bucket = nullptr, ev_bucket_done = nullptr;
 
     float last_ray_ms = 0.f, last_step_ms = 0.f;
     float last_k2_ms[4] = {0.f, 0.f, 0.f, 0.f};  // K2a, K2b, K2d, K2e
@@ -1010,11 +1024,39 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
     c->fork_regs = false;
     regularizers(overlap);
     if (overlap) CK(cudaStreamWaitEvent(s, c->ev_join, 0));
-    // G^T fold (grads.cpp:67-96): raw_grad += G^T * staged
+    // gradient exchange across ranks (GradBuffers::add, trainer.cpp:184-185,
+    // across GPUs) around the G^T fold (grads.cpp:67-96: raw_grad += G^T
+    // staged; Gt is linear, so each rank folds its own staged buffer):
+    //  ALLREDUCE  fold, then one all-reduce of the flat gradient;
+    //  BUCKETED   the [planes | probes | mlp] bucket (final once the
+    //             regularizers joined) all-reduced on the comm stream under the
+    //             fold, then the raw bucket;
+    //  SHARDED    fold, reduce-scatter into world-size chunks, Adam on this
+    //             rank's chunk only, all-gather of the updated parameters.
+    const bool bucketed = c->comm && c->grad_exchange == PSDF_EXCHANGE_BUCKETED;
+    const bool sharded = c->comm && c->grad_exchange == PSDF_EXCHANGE_SHARDED;
+    if (bucketed) {
+        CK(cudaEventRecord(c->ev_bucket, s));
+        CK(cudaStreamWaitEvent(c->comm_stream, c->ev_bucket, 0));
+        NK(g_nccl.AllReduce(c->d_grads + c->off_planes, c->d_grads + c->off_planes,
+                            (size_t)(c->n_params - c->off_planes), ncclFloat, ncclSum, c->comm, c->comm_stream));
+        CK(cudaEventRecord(c->ev_bucket_done, c->comm_stream));
+    }
     launch_fold(c, c->d_gsmooth, c->d_grads + c->off_raw);
-    // all-reduce across ranks (GradBuffers::add, trainer.cpp:184-185, across GPUs)
+    int64_t a_lo = 0, a_n = c->n_params;  // the Adam range of this rank
     if (c->comm) {
-        NK(g_nccl.AllReduce(c->d_grads, c->d_grads, (size_t)c->n_params, ncclFloat, ncclSum, c->comm, s));
+        if (bucketed) {
+            NK(g_nccl.AllReduce(c->d_grads + c->off_raw, c->d_grads + c->off_raw, (size_t)c->off_planes, ncclFloat,
+                                ncclSum, c->comm, s));
+            CK(cudaStreamWaitEvent(s, c->ev_bucket_done, 0));
+        } else if (sharded) {
+            const int64_t chunk = (c->n_params + 4 * c->world - 1) / (4 * c->world) * 4;
+            a_lo = chunk * c->rank;
+            a_n = std::max<int64_t>(0, std::min<int64_t>(chunk, c->n_params - a_lo));
+            NK(g_nccl.ReduceScatter(c->d_grads, c->d_grads + a_lo, (size_t)chunk, ncclFloat, ncclSum, c->comm, s));
+        } else {
+            NK(g_nccl.AllReduce(c->d_grads, c->d_grads, (size_t)c->n_params, ncclFloat, ncclSum, c->comm, s));
+        }
         NK(g_nccl.AllReduce(c->d_stats, c->d_stats, 16, ncclDouble, ncclSum, c->comm, s));
         NK(g_nccl.AllReduce(c->d_counts, c->d_counts, 8, ncclUint64, ncclSum, c->comm, s));
     }
@@ -1022,11 +1064,17 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
     c->adam_t += 1;
     const double c1 = 1.0 - std::pow(0.9, (double)c->adam_t);
     const double c2 = 1.0 - std::pow(0.995, (double)c->adam_t);
-    adam_kernel<<<(unsigned)std::min<int64_t>(8 * c->sm_count, c->n_params / 1024 + 1), 256, 0, s>>>(
-        c->d_params, c->d_grads, c->d_m, c->d_v, c->n_params, c->off_probes, (float)hp->lr_vox,
-        (float)hp->lr_mlp, (float)(1.0 / c1), (float)(1.0 / c2), c->d_counts + 7);
-    CK(cudaGetLastError());
-    ++c->last_launches;
+    if (a_n > 0) {
+        adam_kernel<<<(unsigned)std::min<int64_t>(8 * c->sm_count, a_n / 1024 + 1), 256, 0, s>>>(
+            c->d_params + a_lo, c->d_grads + a_lo, c->d_m + a_lo, c->d_v + a_lo, a_n, c->off_probes - a_lo,
+            (float)hp->lr_vox, (float)hp->lr_mlp, (float)(1.0 / c1), (float)(1.0 / c2), c->d_counts + 7);
+        CK(cudaGetLastError());
+        ++c->last_launches;
+    }
+    if (sharded) {  // every rank's updated chunk to every rank (in place)
+        const int64_t chunk = (c->n_params + 4 * c->world - 1) / (4 * c->world) * 4;
+        NK(g_nccl.AllGather(c->d_params + a_lo, c->d_params, (size_t)chunk, ncclFloat, c->comm, s));
+    }
     // re-smoothing (trainer.cpp:195)
     smooth_all(c);
     CK(cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(double) * 16, cudaMemcpyDeviceToHost, s));
@@ -1178,6 +1226,9 @@ int psdf_destroy(psdf_ctx* c) {
         if (c->h_stats) cudaFreeHost(c->h_stats);
         if (c->h_counts) cudaFreeHost(c->h_counts);
         if (c->comm) g_nccl.CommDestroy(c->comm);
+        if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+        if (c->ev_bucket) cudaEventDestroy(c->ev_bucket);
+        if (c->ev_bucket_done) cudaEventDestroy(c->ev_bucket_done);
         cudaEventDestroy(c->ev_ray0);
         cudaEventDestroy(c->ev_ray1);
         cudaEventDestroy(c->ev_step0);
@@ -1320,18 +1371,18 @@ int psdf_upload_grid(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_c
         CK(cudaMalloc(&c->d_tile_coords, sizeof(int4) * tc4.size()));
         CK(cudaMalloc(&c->d_probe_coords, sizeof(int4) * pc4.size()));
         CK(cudaMalloc(&c->d_probe_ids, sizeof(int32_t) * std::max<int64_t>(8 * T, 1)));
-        CK(cudaMalloc(&c->d_params, sizeof(float) * c->n_params));
-        CK(cudaMalloc(&c->d_grads, sizeof(float) * c->n_params));
-        CK(cudaMalloc(&c->d_m, sizeof(float) * c->n_params));
-        CK(cudaMalloc(&c->d_v, sizeof(float) * c->n_params));
+        CK(cudaMalloc(&c->d_params, sizeof(float) * (c->n_params + kParamPad)));
+        CK(cudaMalloc(&c->d_grads, sizeof(float) * (c->n_params + kParamPad)));
+        CK(cudaMalloc(&c->d_m, sizeof(float) * (c->n_params + kParamPad)));
+        CK(cudaMalloc(&c->d_v, sizeof(float) * (c->n_params + kParamPad)));
         CK(cudaMalloc(&c->d_smooth, sizeof(float) * std::max<int64_t>(T * TV, 4)));
         CK(cudaMalloc(&c->d_smooth_ap, sizeof(float) * std::max<int64_t>(T * AV, 4)));
         CK(cudaMalloc(&c->d_sat_dist, std::max<int64_t>((int64_t)kCellN * T, 1)));
         CK(cudaMalloc(&c->d_gsmooth, sizeof(float) * std::max<int64_t>(T * TV, 4)));
-        CK(cudaMemsetAsync(c->d_params, 0, sizeof(float) * c->n_params, c->stream));
-        CK(cudaMemsetAsync(c->d_grads, 0, sizeof(float) * c->n_params, c->stream));
-        CK(cudaMemsetAsync(c->d_m, 0, sizeof(float) * c->n_params, c->stream));
-        CK(cudaMemsetAsync(c->d_v, 0, sizeof(float) * c->n_params, c->stream));
+        CK(cudaMemsetAsync(c->d_params, 0, sizeof(float) * (c->n_params + kParamPad), c->stream));
+        CK(cudaMemsetAsync(c->d_grads, 0, sizeof(float) * (c->n_params + kParamPad), c->stream));
+        CK(cudaMemsetAsync(c->d_m, 0, sizeof(float) * (c->n_params + kParamPad), c->stream));
+        CK(cudaMemsetAsync(c->d_v, 0, sizeof(float) * (c->n_params + kParamPad), c->stream));
         CK(cudaMemcpyAsync(c->d_tile_table, tt.data(), sizeof(int32_t) * ntt, cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemcpyAsync(c->d_probe_table, pt.data(), sizeof(int32_t) * npt, cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemcpyAsync(c->d_tile_coords, tc4.data(), sizeof(int4) * tc4.size(), cudaMemcpyHostToDevice, c->stream));
@@ -2654,6 +2705,21 @@ int psdf_comm_init(psdf_ctx* c, const void* unique_id, int rank, int world_size)
         ncclUniqueId id;
         std::memcpy(&id, unique_id, sizeof id);
         NK(g_nccl.CommInitRank(&c->comm, world_size, id, rank));
+    });
+}
+
+int psdf_set_grad_exchange(psdf_ctx* c, int mode) {
+    return guarded([&] {
+        if (!c) fail(PSDF_ERR_INVALID_ARGUMENT, "null context");
+        if (mode < PSDF_EXCHANGE_ALLREDUCE || mode > PSDF_EXCHANGE_SHARDED)
+            fail(PSDF_ERR_INVALID_ARGUMENT, "unknown gradient exchange %d", mode);
+        set_device(c);
+        c->grad_exchange = mode;
+        if (mode == PSDF_EXCHANGE_BUCKETED && !c->comm_stream) {
+            CK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&c->ev_bucket, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->ev_bucket_done, cudaEventDisableTiming));
+        }
     });
 }
 

@@ -152,11 +152,13 @@ def _train_parity(ctx, case):
         ctx.train_reset()
 
 
-def test_train_step_through_nccl_single_rank(ctx, monkeypatch):
-    """The multi-GPU exchange path (ncclAllReduce of the gradient buffer, the
-    loss statistics and the counts, psdf.cu do_train_step) exercised on one
-    GPU with a one-rank communicator: results equal the no-communicator step
-    (a one-rank sum is the identity)."""
+@pytest.mark.parametrize("exchange", ["allreduce", "bucketed", "sharded"])
+def test_train_step_through_nccl_single_rank(ctx, monkeypatch, exchange):
+    """The multi-GPU exchange paths (psdf.cu do_train_step: one ncclAllReduce
+    of the gradient buffer; the bucketed all-reduce on a second stream under
+    the fold; reduce-scatter + chunk Adam + all-gather) plus the loss
+    statistics and counts, exercised on one GPU with a one-rank communicator:
+    results equal the no-communicator step (a one-rank sum is the identity)."""
     from paper_2412_10084_b200 import api
     monkeypatch.setenv("PSDF_FORCE_NCCL", "1")
     g, a = make_scene(res=64, n_s=4, n_a=4, sh_order=4, band=6, ncam=0)
@@ -169,6 +171,7 @@ def test_train_step_through_nccl_single_rank(ctx, monkeypatch):
     c2 = api.Context(0)
     try:
         c2.comm_init(api.Context.unique_id(), 0, 1)
+        c2.set_grad_exchange(exchange)
         for c in (ctx, c2):
             c.upload(g, smooth=False)
             c.keep_raypass_grads(True)
@@ -184,3 +187,15 @@ def test_train_step_through_nccl_single_rank(ctx, monkeypatch):
     for k in ("raw", "planes", "probes", "mlp"):
         np.testing.assert_allclose(g1[k], g0[k], rtol=1e-5, atol=1e-7 * max(np.abs(g0[k]).max(), 1e-30))
         np.testing.assert_allclose(p1[k], p0[k], rtol=1e-5, atol=1e-6)
+
+
+def test_unsupported_channel_widths_fail_loudly(ctx):
+    """psdf.h psdf_grid_desc: channel widths outside the instantiated set are
+    an invalid argument before any work (the reference's DecoderMlp takes any
+    width, decoder.hpp:17-31 — documented limitation)."""
+    from paper_2412_10084_b200 import api
+    from paper_2412_10084_b200._lib import PsdfInvalidArgument
+    g, _ = make_scene(res=32, n_s=2, n_a=2, sh_order=2, band=6, ncam=0)
+    g.cfg.n_s, g.cfg.n_a = 3, 5
+    with pytest.raises(PsdfInvalidArgument, match=r"unsupported \(n_s, n_a\) = \(3, 5\)"):
+        ctx.upload(g, smooth=False)
