@@ -20,7 +20,7 @@
 // cover train() only (per-LOD image downscale + upload, every step, the LOD
 // transitions, the final download), not the dataset synthesis or the init.
 //
-//   train_loop <gpu|ref|both> <iter_scale> <n_views> <W> <H> <final_res> <eval_views>
+//   train_loop <gpu|ref|both> <iter_scale> <n_views> <W> <H> <final_res> <eval_views> [acc|dtu]
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -57,7 +57,11 @@ static AnalyticScene glossy_sphere() {
     return sc;
 }
 
-static TrainSchedule dtu_schedule(double scale, int n_lods) {
+// variant "acc": the acceptance schedule's constant loss weights on every
+// level; "dtu": the paper's DTU weights (decaying within LOD 4, then
+// [0.2, 0.1] / [0.4, 0.2] / [0.1, 0.05] / [0.1, 0.05] / [0.4, 0.2] for
+// eikonal / sdf / features / normal / probes).
+static TrainSchedule dtu_schedule(double scale, int n_lods, const std::string& variant) {
     TrainSchedule s;
     s.lambda_photo = 40.0;
     struct L {
@@ -78,11 +82,26 @@ static TrainSchedule dtu_schedule(double scale, int n_lods) {
         l.image_divisor = t.div;
         l.lr_voxels = Bracket{t.lrv0, t.lrv1};
         l.lr_mlp = Bracket{t.lrm0, t.lrm1};
-        l.lambda_eik = Bracket{0.3};
-        l.lambda_sdf = Bracket{0.7};
-        l.lambda_features = Bracket{0.15};
-        l.lambda_normal = Bracket{0.2};
-        l.lambda_probes = Bracket{0.25};
+        if (variant == "eik") {  // the acceptance weights with stronger geometric terms
+            l.lambda_eik = Bracket{1.0};
+            l.lambda_sdf = Bracket{1.0};
+            l.lambda_features = Bracket{0.15};
+            l.lambda_normal = Bracket{0.2};
+            l.lambda_probes = Bracket{0.25};
+        } else if (variant == "dtu") {
+            const bool first = i == 0;
+            l.lambda_eik = first ? Bracket{1.0, 0.1} : Bracket{0.2, 0.1};
+            l.lambda_sdf = first ? Bracket{2.0, 0.2} : Bracket{0.4, 0.2};
+            l.lambda_features = first ? Bracket{0.5, 0.05} : Bracket{0.1, 0.05};
+            l.lambda_normal = first ? Bracket{0.5, 0.05} : Bracket{0.1, 0.05};
+            l.lambda_probes = first ? Bracket{2.0, 0.2} : Bracket{0.4, 0.2};
+        } else {
+            l.lambda_eik = Bracket{0.3};
+            l.lambda_sdf = Bracket{0.7};
+            l.lambda_features = Bracket{0.15};
+            l.lambda_normal = Bracket{0.2};
+            l.lambda_probes = Bracket{0.25};
+        }
         l.tau = Bracket{t.tau0, t.tau1};
         s.lods.push_back(l);
     }
@@ -98,6 +117,7 @@ int main(int argc, char** argv) {
     const double scale = std::atof(argv[2]);
     const int n_views = std::atoi(argv[3]), W = std::atoi(argv[4]), H = std::atoi(argv[5]);
     const int final_res = std::atoi(argv[6]), n_eval = std::atoi(argv[7]);
+    const std::string variant = argc > 8 ? argv[8] : "acc";
     const int n_lods = 5;
     const int res0 = final_res >> (n_lods - 1);
 
@@ -112,7 +132,7 @@ int main(int argc, char** argv) {
         ds.views.push_back(DatasetView{cam, std::move(r.image), std::move(r.mask)});
     }
     std::printf("dataset_s %.2f\n", now_s() - t0);
-    const TrainSchedule sched = dtu_schedule(scale, n_lods);
+    const TrainSchedule sched = dtu_schedule(scale, n_lods, variant);
 
     // visual-hull init at the coarsest level (acceptance.cpp:119-134 pattern)
     GridConfig cfg;
@@ -156,8 +176,12 @@ int main(int argc, char** argv) {
         const double secs = now_s() - a;
         dev.upload(ck.grid, ck.mlp);
         const TriMesh mesh = gpu ? sdfrecon_gpu::marching_cubes(dev) : marching_cubes(ck.grid);
-        const std::vector<Vec3> pts = sample_mesh_points(mesh, 20000, 1);
-        const ChamferResult ch = sdfrecon_gpu::chamfer(dev, pts, mesh, gt_pts, gt_mesh, 0.0);
+        ChamferResult ch;
+        ch.mean = ch.accuracy = ch.completeness = -1.0;  // no surface left
+        if (!mesh.triangles.empty()) {
+            const std::vector<Vec3> pts = sample_mesh_points(mesh, 20000, 1);
+            ch = sdfrecon_gpu::chamfer(dev, pts, mesh, gt_pts, gt_mesh, 0.0);
+        }
         RenderOptions eo;
         eo.tau = 3000.0 / ck.grid.voxel_size;
         double psnr = 0.0;
@@ -167,23 +191,25 @@ int main(int argc, char** argv) {
         }
         psnr /= n_eval;
         std::printf("%s_train_s %.3f\n%s_steps %ld\n%s_last_batch_psnr %.4f\n%s_eval_psnr %.4f\n"
-                    "%s_chamfer_x1000 %.5f\n%s_tiles %zu\n%s_mesh_tris %zu\n",
+                    "%s_chamfer_x1000 %.5f\n%s_accuracy_x1000 %.5f\n%s_completeness_x1000 %.5f\n%s_tiles %zu\n"
+                    "%s_mesh_tris %zu\n",
                     name, secs, name, st.steps_run, name, st.final_psnr, name, psnr, name, ch.mean, name,
-                    ck.grid.tiles.size(), name, mesh.triangles.size());
-        char buf[512];
+                    ch.accuracy, name, ch.completeness, name, ck.grid.tiles.size(), name, mesh.triangles.size());
+        char buf[768];
         std::snprintf(buf, sizeof buf,
                       "%s\"%s\": {\"train_s\": %.3f, \"steps\": %ld, \"last_batch_psnr\": %.4f, \"eval_psnr\": %.4f, "
-                      "\"chamfer_x1000\": %.5f, \"tiles\": %zu, \"final_res\": %d}",
-                      json.size() > 1 ? ", " : "", name, secs, st.steps_run, st.final_psnr, psnr, ch.mean,
-                      ck.grid.tiles.size(), ck.grid.resolution.x);
+                      "\"chamfer_x1000\": %.5f, \"accuracy_x1000\": %.5f, \"completeness_x1000\": %.5f, "
+                      "\"tiles\": %zu, \"final_res\": %d}",
+                      json.size() > 1 ? ", " : "", name, secs, st.steps_run, st.final_psnr, psnr, ch.mean, ch.accuracy,
+                      ch.completeness, ck.grid.tiles.size(), ck.grid.resolution.x);
         json += buf;
         std::fflush(stdout);
     };
     if (mode == "gpu" || mode == "both") arm("gpu", true);
     if (mode == "ref" || mode == "both") arm("ref", false);
     char hdr[256];
-    std::snprintf(hdr, sizeof hdr, ", \"iter_scale\": %g, \"views\": %d, \"width\": %d, \"height\": %d}", scale, n_views,
-                  W, H);
+    std::snprintf(hdr, sizeof hdr, ", \"iter_scale\": %g, \"views\": %d, \"width\": %d, \"height\": %d, \"variant\": \"%s\"}",
+                  scale, n_views, W, H, variant.c_str());
     std::printf("%s%s\n", json.c_str(), hdr);
     return 0;
 }

@@ -188,6 +188,7 @@ struct psdf_ctx {
     bool grads_clear_pending = false;    // gradient clear on the side stream (ev_zeroed)
     cudaEvent_t ev_start = nullptr, ev_zeroed = nullptr;
     bool regs_early = false;             // PSDF_REGS_EARLY: fork the regularizer at step start
+    bool fork_after_scan = false;        // PSDF_REGS_AFTER_SCAN: fork it after the scan, not after round 0
     cudaEvent_t ev_copied = nullptr, ev_copy_free = nullptr;
     bool images_pending = false;           // inside psdf_train_step: the copies may still run
     cudaEvent_t ev_masks = nullptr, ev_rgb = nullptr;  // masks / colours of the step copied
@@ -216,6 +217,7 @@ struct psdf_ctx {
     uint8_t* d_sat_dist = nullptr; // [T][17^3] per-cell saturation distances of the current ray pass
     int composite_steps = kComposite0Steps;
     bool coop_round1 = true;       // K2a round 1 one warp per ray (PSDF_COOP=0: one lane per ray, A/B)
+    bool coop_render = true;       // renders too: round 0 capped, the tail one warp per ray (PSDF_COOP_RENDER=0)
     bool fwd_mma = false;          // K2b decoder MLP on the tensor cores (PSDF_FWD_MMA=1; measured slower, A/B)
     bool stage_fwd = true;         // K2b probe blocks bulk-copied to shared memory (PSDF_STAGE_FWD=0 off)
     int* d_tile_cnt = nullptr;     // [2T] shading records per tile, then their offsets
@@ -694,14 +696,18 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     // tile and neighbouring warps from neighbouring work tiles (a sort by
     // pixel measured slower than it saved)
     CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
+    if (c->fork_regs && c->fork_after_scan) CK(cudaEventRecord(c->ev_fork, s));
     // the composite pass reads the masks (which rays are shaded)
     if (c->images_pending) CK(cudaStreamWaitEvent(s, c->ev_masks, 0));
-    // (render: one round; its rays are short at the render tau)
-    march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, W, 0, P.mode == 1 ? INT_MAX : c->composite_steps);
+    // round 0 one lane per ray for `composite_steps` steps, then the rays
+    // still alive one warp per ray (march_coop_kernel); PSDF_COOP=0 keeps
+    // one lane per ray (a render then runs one uncapped round)
+    const bool coop = c->coop_round1 && (P.mode != 1 || c->coop_render);
+    march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, W, 0, P.mode == 1 && !coop ? INT_MAX : c->composite_steps);
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(c->d_work, 0, sizeof(unsigned long long), s));
-    if (c->fork_regs) CK(cudaEventRecord(c->ev_fork, s));
-    if (c->coop_round1 && P.mode != 1)
+    if (c->fork_regs && !c->fork_after_scan) CK(cudaEventRecord(c->ev_fork, s));
+    if (coop)
         march_coop_kernel<<<(unsigned)grid_c1, BLOCK, smem_bits, s>>>(P, W);
     else
         march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, W, 1, INT_MAX);
@@ -1172,9 +1178,11 @@ int psdf_create(int device, psdf_ctx** out) {
         if (const char* e = std::getenv("PSDF_COMPOSITE_STEPS")) c->composite_steps = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("PSDF_WAVE_INIT")) c->wave_init = std::max(0, std::atoi(e));
         if (const char* e = std::getenv("PSDF_COOP")) c->coop_round1 = std::atoi(e) != 0;
+        if (const char* e = std::getenv("PSDF_COOP_RENDER")) c->coop_render = std::atoi(e) != 0;
         if (const char* e = std::getenv("PSDF_FWD_MMA")) c->fwd_mma = std::atoi(e) != 0;
         if (const char* e = std::getenv("PSDF_STAGE_FWD")) c->stage_fwd = std::atoi(e) != 0;
         if (const char* e = std::getenv("PSDF_REGS_EARLY")) c->regs_early = std::atoi(e) != 0;
+        if (const char* e = std::getenv("PSDF_REGS_AFTER_SCAN")) c->fork_after_scan = std::atoi(e) != 0;
         if (const char* m = std::getenv("PSDF_TEST_MARGIN")) c->test_margin = std::max(1e-8, std::atof(m));
         CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithPriority(&c->side_stream, cudaStreamNonBlocking, prio_lo));
