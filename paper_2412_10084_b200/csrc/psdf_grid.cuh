@@ -398,7 +398,9 @@ __global__ void __launch_bounds__(LG_THREADS, 2) loss_grid_kernel(GridView g, co
     }
     __syncthreads();
     // phase B
-    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // sdf pl/wt, eik pl/wt, normal pl/wt
+    // sdf pl/wt, eik pl/wt, normal pl/wt: fp32 partial sums over this
+    // thread's <= 30 terms, then f64 across the block (block_add_f64v)
+    float acc[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     float D[LG_PER][3];
     constexpr int SX = DE * DE, SY = DE;
     {
@@ -416,8 +418,8 @@ __global__ void __launch_bounds__(LG_THREADS, 2) loss_grid_kernel(GridView g, co
                 if (in_tile(x, y, z)) {
                     const float w = pc.w;
                     const float e = len - 1.f;
-                    acc[2] += (double)(l_eik * e * e);
-                    acc[3] += (double)(l_eik * w * e * e);
+                    acc[2] += l_eik * e * e;
+                    acc[3] += l_eik * w * e * e;
                     if (q > 1e-24f) {  // len > 1e-12
                         const float cc = 2.f * l_eik * w * e * inv;
                         dx += cc * pc.x;
@@ -436,8 +438,8 @@ __global__ void __launch_bounds__(LG_THREADS, 2) loss_grid_kernel(GridView g, co
                             const float ih = rsqrtf(qh);
                             const float ddx = ph.x * ih - n1x, ddy = ph.y * ih - n1y, ddz = ph.z * ih - n1z;
                             const float vv = ddx * ddx + ddy * ddy + ddz * ddz;
-                            acc[4] += (double)(l_norm * vv);
-                            acc[5] += (double)(l_norm * w * vv);
+                            acc[4] += l_norm * vv;
+                            acc[5] += l_norm * w * vv;
                             const float cn = 2.f * l_norm * w;
                             // dn1 = -c d ; dg1 = (dn1 - n1 (dn1 . n1)) / l1
                             const float m1x = -cn * ddx, m1y = -cn * ddy, m1z = -cn * ddz;
@@ -498,8 +500,8 @@ __global__ void __launch_bounds__(LG_THREADS, 2) loss_grid_kernel(GridView g, co
                 const float d = sv - ra[k];
                 const float as = fabsf(sv), ar = fabsf(ra[k]);
                 const float w = __frcp_rn((as > ar ? as : ar) + (float)kPhotoEps) * __frcp_rn(1.f + as * 5.f);
-                acc[0] += (double)(l_sdf * d * d);
-                acc[1] += (double)(l_sdf * w * d * d);
+                acc[0] += l_sdf * d * d;
+                acc[1] += l_sdf * w * d * d;
                 const float gg = 2.f * l_sdf * w * d;
                 ga[k] -= gg;
                 cell = gg;
@@ -536,7 +538,10 @@ __global__ void __launch_bounds__(LG_THREADS, 2) loss_grid_kernel(GridView g, co
         }
     }
     double* dst[6] = {stats + 3, stats + 8, stats + 4, stats + 9, stats + 5, stats + 10};
-    block_add_f64v<6>(dst, acc, red);
+    double accd[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) accd[k] = (double)acc[k];
+    block_add_f64v<6>(dst, accd, red);
 }
 
 // K5: loss_features (losses.cpp:222-257); block = one (tile, plane), thread =
