@@ -4,13 +4,18 @@ occupancy and issue activity, plus the K2 ray-pass DRAM bytes that bench.py
 reports as roofline.traffic (profiles/ncu_k2_traffic.json).
 
     ncu -i REPORT --page raw --csv > raw.csv
-    python profiles/collect.py raw.csv OUT_PREFIX
+    python profiles/collect.py raw.csv OUT_PREFIX [SOURCE_NOTE [WORKLOAD]]
+
+SOURCE_NOTE (e.g. "profiles/r02/v9 at commit abc1234") and WORKLOAD (the
+bench's workload name) are stored in the traffic json: bench.py reports the
+traffic only for the workload it was captured on, and names its source.
 """
 import csv
 import json
 import sys
 
-K2 = ("march_scan", "march_fwd", "rec_tile", "DeviceScan", "shade_fwd", "alpha_bwd", "shade_bwd", "shade_geo")
+K2 = ("march_scan", "march_fwd", "march_coop", "rec_tile", "DeviceScan", "shade_fwd", "alpha_bwd", "shade_bwd",
+      "shade_geo")
 COLS = {
     "time_us": ("gpu__time_duration.sum", 1e-3),
     "dram_read_MB": ("dram__bytes_read.sum", 1e-6),
@@ -28,7 +33,7 @@ UNIT_SCALE = {"ms": 1e3, "us": 1.0, "usecond": 1.0, "msecond": 1e3, "nsecond": 1
               "Gbyte": 1e3, "Mbyte": 1.0, "Kbyte": 1e-3, "byte": 1e-6}
 
 
-def main(path, out):
+def main(path, out, source=None, workload=None):
     rows = list(csv.reader(open(path)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     res = []
@@ -51,7 +56,8 @@ def main(path, out):
     k2 = [r for r in res if any(s in r["kernel"] for s in K2)]
     k2_bytes = sum((r.get("dram_read_MB", 0) + r.get("dram_write_MB", 0)) * 1e6 for r in k2)
     k2_time = sum(r["time_us"] for r in k2)
-    json.dump({"dram_bytes_per_launch": k2_bytes, "k2_kernels": [r["kernel"] for r in k2],
+    json.dump({"dram_bytes_per_launch": k2_bytes, "source": source, "workload": workload,
+               "k2_kernels": [r["kernel"] for r in k2],
                "k2_time_us_serialised": k2_time,
                "note": "K2 = the ray-pass kernels of one train step (incl. CUB sorts); ncu --set full, "
                        "--clock-control none, cold caches per replay"},
@@ -74,4 +80,4 @@ def main(path, out):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], *(sys.argv[3:5]))
