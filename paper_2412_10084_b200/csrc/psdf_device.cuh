@@ -412,7 +412,7 @@ struct Marcher {
             vd[a] = d[a] * inv_h;
             dm = fmax(dm, fabs(d[a]));
         }
-        dinv_max = dm > 0.0 ? 1.0 / dm : 0.0;
+        dinv_max = dm > 0.0 ? __drcp_rn(dm) : 0.0;  // = 1.0 / dm (correctly rounded), no division sequence
         rinv_max = fmax(fmax(fabs(inv_d[0]), fabs(inv_d[1])), fabs(inv_d[2]));
         t_sync = -1.0;
         no_jump = false;

@@ -430,8 +430,8 @@ __device__ __forceinline__ int64_t active_tile(const RayPassParams& P, int64_t k
     int v = 0;
     while (v + 1 < P.n_views && P.views[v + 1].act_begin <= k) ++v;
     const ViewDev& V = P.views[v];
-    const int64_t a = k - V.act_begin;
-    const int ay = (int)(a / V.act_w), ax = (int)(a - (int64_t)ay * V.act_w);
+    const int a = (int)(k - V.act_begin);  // < the view's tile count: 32-bit division
+    const int ay = a / V.act_w, ax = a - ay * V.act_w;
     return V.tile_begin + (int64_t)(V.act_ty0 + ay) * V.tiles_x + V.act_tx0 + ax;
 }
 

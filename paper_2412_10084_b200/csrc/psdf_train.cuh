@@ -139,9 +139,11 @@ __device__ __forceinline__ LaneRay lane_ray(const RayPassParams& P, int wi, int 
     const int vi = locate_view(P, tile_id);
     LaneRay r;
     r.V = &P.views[vi];
-    const int64_t lt = tile_id - r.V->tile_begin;
-    r.u = (int)(lt % r.V->tiles_x) * 8 + (lane & 7);
-    r.v = (int)(lt / r.V->tiles_x) * 4 + (lane >> 3);
+    // the tile inside its view (< 2^31: 32-bit division)
+    const int lt = (int)(tile_id - r.V->tile_begin);
+    const int ty = lt / r.V->tiles_x;
+    r.u = (lt - ty * r.V->tiles_x) * 8 + (lane & 7);
+    r.v = ty * 4 + (lane >> 3);
     r.valid = r.u < r.V->cam.width && r.v < r.V->cam.height;
     r.px = r.valid ? (int64_t)r.v * r.V->cam.width + r.u : 0;
     return r;
