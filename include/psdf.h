@@ -285,7 +285,9 @@ int psdf_last_timing(psdf_ctx* ctx, double* ray_kernel_ms, double* step_ms, int*
  * shade_fwd, alpha_bwd, shade_bwd) and the ray-entry / shading-record counts. */
 int psdf_last_k2_breakdown(psdf_ctx* ctx, double* ms4, int64_t* entries, int64_t* records);
 /* Queue sizes of the last train step's ray pass: ray entries, shading
-   records, scan hand-overs, round-1 continuations, alpha samples. */
+   records, scan hand-overs, round-1 continuations, alpha samples.  Records
+   are the valid ones; the entry and alpha-sample counts include the holes
+   of the march's abandoned allocation chunks (slots never written). */
 int psdf_last_wave_counts(psdf_ctx* ctx, int64_t* out5);
 /* Raw CUDA stream of the context (cudaStream_t), for callers that time or
  * overlap work around the context. */

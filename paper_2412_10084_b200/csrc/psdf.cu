@@ -1096,8 +1096,9 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
         return;
     }
     c->last_entries = c->h_wave_counters[0];
-    c->last_records = c->h_wave_counters[1];
+    c->last_records = c->h_wave_counters[5];  // sorted records (the queue minus allocation holes)
     for (int k = 0; k < 5; ++k) c->last_wave[k] = c->h_wave_counters[k];
+    c->last_wave[1] = c->h_wave_counters[5];
     CK(cudaEventElapsedTime(&c->last_ray_ms, c->ev_ray0, c->ev_ray1));
     CK(cudaEventElapsedTime(&c->last_step_ms, c->ev_step0, c->ev_step1));
     for (int k = 0; k < 4; ++k) CK(cudaEventElapsedTime(&c->last_k2_ms[k], c->ev_k[k], c->ev_k[k + 1]));

@@ -114,6 +114,11 @@ __device__ __forceinline__ int n_entries(const WaveBufs& W) {
 __device__ __forceinline__ int n_records(const WaveBufs& W) {
     return wave_over(W) ? 0 : (int)min(*(volatile unsigned*)(W.counters + 1), (unsigned)W.r_cap);
 }
+// The records in the tile-sorted permutation r_perm (the queue minus the
+// holes of abandoned allocation chunks), counted by rec_tile_count_kernel.
+__device__ __forceinline__ int n_sorted(const WaveBufs& W) {
+    return wave_over(W) ? 0 : (int)min(*(volatile unsigned*)(W.counters + 5), (unsigned)W.r_cap);
+}
 
 // Warp-aggregated slot allocation inside divergent code.
 __device__ __forceinline__ int warp_alloc(unsigned* counter, bool want, int lane) {
@@ -125,6 +130,37 @@ __device__ __forceinline__ int warp_alloc(unsigned* counter, bool want, int lane
     if (lane == leader) base = atomicAdd(counter, (unsigned)__popc(m));
     base = __shfl_sync(m, base, leader);
     return (int)(base + __popc(m & ((1u << lane) - 1u)));
+}
+
+// Per-warp chunked allocation from a queue counter: the warp takes slots
+// for its (warp-uniform) k requests from a private chunk and fetches a fresh
+// chunk of max(CH, k) slots with one atomic when the chunk runs short, instead
+// of one same-address atomic per step (those were 19 % of round 0's stalls).
+// The rest of an abandoned chunk becomes holes, marked by `hole(slot)` so the
+// queue's readers skip them (records: tile -1; entries: slot -1, head -1).
+struct WarpChunk {
+    unsigned base, left;
+};
+constexpr unsigned kChunk = 64;
+template <class F>
+__device__ __forceinline__ unsigned chunk_take(unsigned* counter, WarpChunk& c, unsigned k, int lane, F hole) {
+    if (k > c.left) {
+        for (unsigned i = lane; i < c.left; i += 32) hole(c.base + i);
+        const unsigned n = k > kChunk ? k : kChunk;
+        unsigned b = 0;
+        if (lane == 0) b = atomicAdd(counter, n);
+        c.base = __shfl_sync(FULL, b, 0);
+        c.left = n;
+    }
+    const unsigned r = c.base;
+    c.base += k;
+    c.left -= k;
+    return r;
+}
+template <class F>
+__device__ __forceinline__ void chunk_close(WarpChunk& c, int lane, F hole) {
+    for (unsigned i = lane; i < c.left; i += 32) hole(c.base + i);
+    c.left = 0;
 }
 
 struct LaneRay {
@@ -379,6 +415,17 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
     const double tau_run = P.early_stop > 1.0 ? 0.0 : tau;  // see render_kernel
     double st_photo = 0.0, st_sq = 0.0;
     unsigned long long st_mask = 0, c_m = 0, c_x = 0, c_sh = 0, c_bwd = 0, c_ex = 0;
+    WarpChunk ch_e{0, 0}, ch_r{0, 0}, ch_a{0, 0};
+    auto hole_e = [&](unsigned e) {
+        if (e < (unsigned)W.e_cap) {
+            W.e_slot[e] = -1;
+            W.e_head[e] = -1;
+        }
+    };
+    auto hole_r = [&](unsigned r) {
+        if (r < (unsigned)W.r_cap) W.r_tile[r] = -1;
+    };
+    auto hole_a = [](unsigned) {};  // alpha samples are reached only through their entry's list
     for (;;) {
         int base = 0;
         if (lane == 0) base = (int)atomicAdd(P.work_counter, 32ull);
@@ -526,21 +573,16 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
                     }
                 }
             }
-            // warp-aggregated allocation of ray entries / shading records
+            // warp-chunked allocation of ray entries / shading records / alpha samples
             {
                 const unsigned me = __ballot_sync(FULL, want_entry);
                 const unsigned mr_ = __ballot_sync(FULL, shade);
                 const unsigned ma = __ballot_sync(FULL, want_alpha);
                 const unsigned below = (1u << lane) - 1u;
                 unsigned be = 0, br = 0, ba = 0;
-                if (lane == 0) {
-                    if (me) be = atomicAdd(W.counters + 0, (unsigned)__popc(me));
-                    if (mr_) br = atomicAdd(W.counters + 1, (unsigned)__popc(mr_));
-                    if (ma) ba = atomicAdd(W.counters + 4, (unsigned)__popc(ma));
-                }
-                be = __shfl_sync(FULL, be, 0);
-                br = __shfl_sync(FULL, br, 0);
-                ba = __shfl_sync(FULL, ba, 0);
+                if (me) be = chunk_take(W.counters + 0, ch_e, (unsigned)__popc(me), lane, hole_e);
+                if (mr_) br = chunk_take(W.counters + 1, ch_r, (unsigned)__popc(mr_), lane, hole_r);
+                if (ma) ba = chunk_take(W.counters + 4, ch_a, (unsigned)__popc(ma), lane, hole_a);
                 if (want_entry) {
                     const int e = (int)(be + __popc(me & below));
                     entry = e < W.e_cap ? e : -2;  // -2: overflow, host retries
@@ -637,6 +679,8 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
                 ++c_bwd;
         }
     }
+    chunk_close(ch_e, lane, hole_e);
+    chunk_close(ch_r, lane, hole_r);
     st_photo = warp_sum_d(st_photo);
     st_sq = warp_sum_d(st_sq);
     st_mask = warp_sum_u(st_mask);
@@ -688,6 +732,16 @@ __global__ void __launch_bounds__(BLOCK, PSDF_COOP_MINB) march_coop_kernel(RayPa
     const double tau = P.tau, h = g.h;
     double st_photo = 0.0, st_sq = 0.0;
     unsigned long long st_mask = 0, c_m = 0, c_x = 0, c_sh = 0, c_bwd = 0, c_ex = 0;
+    WarpChunk ch_e{0, 0}, ch_r{0, 0}, ch_a{0, 0};  // chunked queue allocation (chunk_take)
+    auto hole_e = [&](unsigned e) {
+        if (e < (unsigned)W.e_cap) {
+            W.e_slot[e] = -1;
+            W.e_head[e] = -1;
+        }
+    };
+    auto hole_r = [&](unsigned r) {
+        if (r < (unsigned)W.r_cap) W.r_tile[r] = -1;
+    };
     for (;;) {
         int ki = 0;
         if (lane == 0) ki = (int)atomicAdd(P.work_counter, 1ull);
@@ -797,21 +851,15 @@ __global__ void __launch_bounds__(BLOCK, PSDF_COOP_MINB) march_coop_kernel(RayPa
             }
             // ray entry (once), shading records, alpha samples
             if (mpos && entry < 0) {
-                unsigned e0 = 0;
-                if (lane == 0) e0 = atomicAdd(W.counters + 0, 1u);
-                e0 = __shfl_sync(FULL, e0, 0);
+                const unsigned e0 = chunk_take(W.counters + 0, ch_e, 1u, lane, hole_e);
                 entry = (int)e0 < W.e_cap ? (int)e0 : -2;  // -2: overflow, host retries
             }
             const bool shade = live && in_mask && w > 0.0 && tile_prev >= 0;
             const unsigned msh = __ballot_sync(FULL, shade);
             const unsigned mal = P.mode != 1 ? mpos : 0u;
             unsigned br = 0, ba = 0;
-            if (lane == 0) {
-                if (msh) br = atomicAdd(W.counters + 1, (unsigned)__popc(msh));
-                if (mal) ba = atomicAdd(W.counters + 4, (unsigned)__popc(mal));
-            }
-            br = __shfl_sync(FULL, br, 0);
-            ba = __shfl_sync(FULL, ba, 0);
+            if (msh) br = chunk_take(W.counters + 1, ch_r, (unsigned)__popc(msh), lane, hole_r);
+            if (mal) ba = chunk_take(W.counters + 4, ch_a, (unsigned)__popc(mal), lane, [](unsigned) {});
             int rec_now = -1;
             if (msh) {
                 c_sh += lane == 0 ? (unsigned long long)__popc(msh) : 0ull;
@@ -916,6 +964,8 @@ __global__ void __launch_bounds__(BLOCK, PSDF_COOP_MINB) march_coop_kernel(RayPa
                 ++c_bwd;
         }
     }
+    chunk_close(ch_e, lane, hole_e);
+    chunk_close(ch_r, lane, hole_r);
     st_photo = warp_sum_d(st_photo);
     st_sq = warp_sum_d(st_sq);
     st_mask = warp_sum_u(st_mask);
@@ -976,12 +1026,20 @@ __global__ void __launch_bounds__(256) rec_tile_count_kernel(WaveBufs W, int* __
     const int n = n_records(W);
     const int lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
+    __shared__ unsigned s_valid;  // records of this block (holes excluded), one atomic per block
+    if (threadIdx.x == 0) s_valid = 0;
+    __syncthreads();
+    unsigned valid = 0;
     for (int b = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; b < n; b += warps * 32) {
         const int i = b + lane;
         const int t = i < n ? W.r_tile[i] : -1;
         const unsigned m = __match_any_sync(FULL, t);
         if (t >= 0 && lane == __ffs(m) - 1) atomicAdd(cnt + t, __popc(m));
+        valid += (unsigned)__popc(__ballot_sync(FULL, t >= 0));
     }
+    if (lane == 0 && valid) atomicAdd(&s_valid, valid);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_valid) atomicAdd(W.counters + 5, s_valid);
 }
 __global__ void __launch_bounds__(256) rec_tile_scatter_kernel(WaveBufs W, int* __restrict__ off) {
     const int n = n_records(W);
@@ -1005,7 +1063,7 @@ template <int NS, int NA, bool GEO>
 #define PSDF_FWD_MINB 5  // <= 102 registers: 5 blocks per SM (measured best)
 #endif
 __global__ void __launch_bounds__(BLOCK, PSDF_FWD_MINB) shade_fwd_kernel(RayPassParams P, WaveBufs W) {
-    const int n_rec = n_records(W);
+    const int n_rec = n_sorted(W);
     constexpr int IN = NS + NA + NPOW;
     extern __shared__ __align__(16) float smem[];
     __shared__ uint64_t s_bar[WARPS_PER_BLOCK];
@@ -1084,7 +1142,7 @@ size_t shade_fwd_mma_smem_bytes() {
 #endif
 template <int NS, int NA, bool GEO>
 __global__ void __launch_bounds__(BLOCK, PSDF_FWDM_MINB) shade_fwd_mma_kernel(RayPassParams P, WaveBufs W) {
-    const int n_rec = n_records(W);
+    const int n_rec = n_sorted(W);
     constexpr int IN = NS + NA + NPOW;
     using D = FwdDims<IN>;
     extern __shared__ __align__(16) float smem[];
@@ -1219,6 +1277,7 @@ __global__ void __launch_bounds__(BLOCK) alpha_bwd_kernel(RayPassParams P, WaveB
     unsigned long long st_mask = 0, c_al = 0, c_bwd = 0;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_ent; e += gridDim.x * blockDim.x) {
         const int slot = W.e_slot[e];
+        if (slot < 0) continue;  // a hole of an abandoned allocation chunk
         const LaneRay R = lane_ray(P, slot >> 5, slot & 31);
         const bool in_mask = __ldg(R.V->mask + R.px) != 0;
         const double acc = W.e_acc[e];
@@ -1370,7 +1429,7 @@ struct MmaDims {
 
 template <int NS, int NA>
 __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveBufs W) {
-    const int n_rec = n_records(W);
+    const int n_rec = n_sorted(W);
     constexpr int IN = NS + NA + NPOW;
     using D = MmaDims<IN>;
     using GR = GeoRec<NS, NA>;
@@ -1610,7 +1669,7 @@ __global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveB
 constexpr int PWS = 36;  // row stride of the per-warp probe staging (w8 | Y[16] | gfa), float4 aligned
 template <int NS, int NA>
 __global__ void __launch_bounds__(BLOCK) shade_geo_kernel(RayPassParams P, WaveBufs W) {
-    const int n_rec = n_records(W);
+    const int n_rec = n_sorted(W);
     __shared__ __align__(16) float s_pw[WARPS_PER_BLOCK][32 * PWS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* PW = s_pw[warp];
