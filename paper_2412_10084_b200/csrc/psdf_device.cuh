@@ -35,6 +35,17 @@ __device__ __forceinline__ double ddiv_r(double a, double b, double rb) {
     return __fma_rn(__fma_rn(-b, q0, a), rb, q0);
 }
 __device__ __forceinline__ double dsqrt(double a) { return __dsqrt_rn(a); }
+// RN(a / b) without the software division: ddiv_r from the correctly rounded
+// reciprocal when a and b are normal and far from overflow (every value the
+// march, the alpha chain and the photo terms divide by), the division
+// sequence otherwise (zero, subnormal, huge or non-finite operands).
+__device__ __forceinline__ double ddiv_fast(double a, double b) {
+    const double ab = fabs(a), bb = fabs(b);
+    // both in [1e-150, 1e150] (or a == 0): the quotient is normal, no
+    // intermediate overflows or underflows
+    if (bb > 1e-150 && bb < 1e150 && ab < 1e150 && (ab > 1e-150 || a == 0.0)) return ddiv_r(a, b, __drcp_rn(b));
+    return ddiv(a, b);
+}
 
 struct D3 {
     double x, y, z;
@@ -721,7 +732,7 @@ __device__ __forceinline__ double alpha_from(double a, double b) {
 #ifdef PSDF_ABL_ALPHA
     const double al = (a - b) * __drcp_rn(a);
 #else
-    const double al = ddiv(dsub(a, b), a);
+    const double al = ddiv_fast(dsub(a, b), a);
 #endif
     return al > 0.0 ? al : 0.0;
 }

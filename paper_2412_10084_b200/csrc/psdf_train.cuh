@@ -199,7 +199,7 @@ __device__ __forceinline__ bool photo_term(const RayPassParams& P, bool in_mask,
         for (int k = 0; k < 3; ++k) {
             const double gtk = (double)__ldg(gtp + k);
             const double d = dsub(col[k], gtk);
-            const double wk = ddiv(1.0, dadd(col[k] > gtk ? col[k] : gtk, kPhotoEps));
+            const double wk = __drcp_rn(dadd(col[k] > gtk ? col[k] : gtk, kPhotoEps));  // = 1.0 / x
             st_photo = dadd(st_photo, dmul(dmul(scale, d), d));
             st_sq = dadd(st_sq, dmul(d, d));
             gg[k] = dmul(dmul(dmul(scale, 2.0), wk), d);
@@ -210,7 +210,7 @@ __device__ __forceinline__ bool photo_term(const RayPassParams& P, bool in_mask,
         st_mask += 3;
     } else {
         const double am = acc > 0.0 ? acc : 0.0;
-        const double wa = ddiv(1.0, dadd(am, kPhotoEps));
+        const double wa = __drcp_rn(dadd(am, kPhotoEps));  // = 1.0 / x
         st_photo = dadd(st_photo, dmul(dmul(scale, acc), acc));
         dA = dmul(dmul(dmul(scale, 2.0), wa), acc);
     }
@@ -1335,12 +1335,12 @@ __global__ void __launch_bounds__(BLOCK) alpha_bwd_kernel(RayPassParams P, WaveB
             pre = dadd(pre, dmul(dw, w));
             double own = 0.0, nxt = 0.0;
             const double om_a = dsub(1.0, alpha);
-            const double dalpha = dsub(dmul(dw, T), om_a > 1e-12 ? ddiv(dsub(total, pre), om_a) : 0.0);
+            const double dalpha = dsub(dmul(dw, T), om_a > 1e-12 ? ddiv_fast(dsub(total, pre), om_a) : 0.0);
             if (dalpha != 0.0) {  // renderer.cpp:266-276
                 const double da = dmul(dmul(tau, a_cur), dsub(1.0, a_cur));
                 const double db = dmul(dmul(tau, a_nxt), dsub(1.0, a_nxt));
-                own = ddiv(dmul(dmul(dalpha, a_nxt), da), dmul(a_cur, a_cur));
-                nxt = dmul(dalpha, ddiv(-db, a_cur));
+                own = ddiv_fast(dmul(dmul(dalpha, a_nxt), da), dmul(a_cur, a_cur));
+                nxt = dmul(dalpha, ddiv_fast(-db, a_cur));
             }
             double p[3];
             // the previous alpha sample's term lands here, or at a sample of its own
