@@ -98,16 +98,17 @@ struct MlpLayout {
     }
 };
 
-// Shared-memory MLP copy with 16-byte aligned segments.
+// Shared-memory MLP copy, input-major for the paired-FMA forward (mlp_forward):
+// w1t[i][j] = W1[j][i] (IN x 32), w2t[i][j] = W2[j][i] (32 x 32), rows of 32
+// outputs 16-byte aligned; w3 row-major [3][32]; biases.
 struct SmemMlp {
-    int w1, b1, w2, b2, w3, b3, total;
+    int w1t, b1, w2t, b2, w3, b3, total;
     __host__ __device__ static SmemMlp make(int in) {
-        auto up4 = [](int x) { return (x + 3) & ~3; };
         SmemMlp s;
-        s.w1 = 0;
-        s.b1 = up4(32 * in);
-        s.w2 = s.b1 + 32;
-        s.b2 = s.w2 + 1024;
+        s.w1t = 0;
+        s.b1 = 32 * in;
+        s.w2t = s.b1 + 32;
+        s.b2 = s.w2t + 1024;
         s.w3 = s.b2 + 32;
         s.b3 = s.w3 + 96;
         s.total = s.b3 + 4;
@@ -307,43 +308,77 @@ __device__ __forceinline__ void decode_features(const RayPassParams& P, int tile
     }
 }
 
-// decode_color (decoder.cpp:61-109) from the MLP input; a1 / a2 optional
-// outputs (post-ReLU activations).
+// c += a * (b, b) on a pair of fp32 lanes (FFMA2, sm_100): two outputs per
+// instruction, each rounded exactly as a scalar FFMA.
+__device__ __forceinline__ void ffma2(float2& c, float2 a, float b) {
+    unsigned long long& cc = *reinterpret_cast<unsigned long long*>(&c);
+    const float2 bb = make_float2(b, b);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;"
+        : "+l"(cc)
+        : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&bb)));
+}
+
+// decode_color (decoder.cpp:61-109) from the MLP input.  Layers 1 and 2 run
+// input-major: for each input i one broadcast float4 of the transposed weight
+// row feeds two paired FMAs (FFMA2), half the issue of per-output FFMA dot
+// products (those were ~35 % of shade_fwd's instructions, profiles/r02/v15).
 template <int IN>
 __device__ __forceinline__ void mlp_forward(const float* __restrict__ sm, const SmemMlp& L,
                                             const float x[IN], const float* cam_row, float rgb[3],
                                             float* a1_row, float* a2_row) {
+    float2 z[HID / 2];
+#pragma unroll
+    for (int j = 0; j < HID / 2; ++j) {
+        z[j] = reinterpret_cast<const float2*>(sm + L.b1)[j];
+        if (cam_row) {
+            z[j].x += __ldg(cam_row + 2 * j);
+            z[j].y += __ldg(cam_row + 2 * j + 1);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < IN; ++i) {
+        const float4* row = reinterpret_cast<const float4*>(sm + L.w1t + i * HID);
+#pragma unroll
+        for (int q = 0; q < HID / 4; ++q) {
+            const float4 w = row[q];
+            ffma2(z[2 * q], make_float2(w.x, w.y), x[i]);
+            ffma2(z[2 * q + 1], make_float2(w.z, w.w), x[i]);
+        }
+    }
     float a1[HID];
 #pragma unroll
-    for (int j = 0; j < HID; ++j) {
-        float z = sm[L.b1 + j] + (cam_row ? __ldg(cam_row + j) : 0.f);
-        const float* row = sm + L.w1 + j * IN;
+    for (int j = 0; j < HID / 2; ++j) {
+        a1[2 * j] = z[j].x > 0.f ? z[j].x : 0.f;
+        a1[2 * j + 1] = z[j].y > 0.f ? z[j].y : 0.f;
+    }
 #pragma unroll
-        for (int i = 0; i < IN; ++i) z += row[i] * x[i];
-        a1[j] = z > 0.f ? z : 0.f;
+    for (int j = 0; j < HID / 2; ++j) z[j] = reinterpret_cast<const float2*>(sm + L.b2)[j];
+#pragma unroll
+    for (int i = 0; i < HID; ++i) {
+        const float4* row = reinterpret_cast<const float4*>(sm + L.w2t + i * HID);
+#pragma unroll
+        for (int q = 0; q < HID / 4; ++q) {
+            const float4 w = row[q];
+            ffma2(z[2 * q], make_float2(w.x, w.y), a1[i]);
+            ffma2(z[2 * q + 1], make_float2(w.z, w.w), a1[i]);
+        }
     }
     float a2[HID];
 #pragma unroll
-    for (int j = 0; j < HID; ++j) {
-        float z = sm[L.b2 + j];
-        const float4* row = reinterpret_cast<const float4*>(sm + L.w2 + j * HID);
-#pragma unroll
-        for (int i = 0; i < HID / 4; ++i) {
-            const float4 w = row[i];
-            z += w.x * a1[4 * i] + w.y * a1[4 * i + 1] + w.z * a1[4 * i + 2] + w.w * a1[4 * i + 3];
-        }
-        a2[j] = z > 0.f ? z : 0.f;
+    for (int j = 0; j < HID / 2; ++j) {
+        a2[2 * j] = z[j].x > 0.f ? z[j].x : 0.f;
+        a2[2 * j + 1] = z[j].y > 0.f ? z[j].y : 0.f;
     }
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-        float z = sm[L.b3 + j];
+        float zz = sm[L.b3 + j];
         const float4* row = reinterpret_cast<const float4*>(sm + L.w3 + j * HID);
 #pragma unroll
         for (int i = 0; i < HID / 4; ++i) {
             const float4 w = row[i];
-            z += w.x * a2[4 * i] + w.y * a2[4 * i + 1] + w.z * a2[4 * i + 2] + w.w * a2[4 * i + 3];
+            zz += w.x * a2[4 * i] + w.y * a2[4 * i + 1] + w.z * a2[4 * i + 2] + w.w * a2[4 * i + 3];
         }
-        rgb[j] = sigmoidf_(z);
+        rgb[j] = sigmoidf_(zz);
     }
     if (a1_row) {
 #pragma unroll
@@ -442,14 +477,16 @@ __device__ __forceinline__ int locate_view(const RayPassParams& P, int64_t tile)
     return v;
 }
 
-// Copies the flat MLP (without camera bias) into 16-byte aligned smem slots.
+// Copies the flat MLP (without camera bias) into the shared-memory layout
+// (W1 and W2 transposed to input-major).
 __device__ __forceinline__ void load_mlp_smem(const float* __restrict__ mlp, float* sm,
                                               const MlpLayout& G, const SmemMlp& L) {
+    const int in = G.b1 / HID;
     for (int i = threadIdx.x; i < G.total_nocam; i += blockDim.x) {
         int dst;
-        if (i < G.b1) dst = L.w1 + i;
+        if (i < G.b1) dst = L.w1t + (i % in) * HID + i / in;                   // W1[j][k] -> w1t[k][j]
         else if (i < G.w2) dst = L.b1 + (i - G.b1);
-        else if (i < G.b2) dst = L.w2 + (i - G.w2);
+        else if (i < G.b2) dst = L.w2t + ((i - G.w2) & 31) * HID + ((i - G.w2) >> 5);  // W2[j][k] -> w2t[k][j]
         else if (i < G.w3) dst = L.b2 + (i - G.b2);
         else if (i < G.b3) dst = L.w3 + (i - G.w3);
         else dst = L.b3 + (i - G.b3);
