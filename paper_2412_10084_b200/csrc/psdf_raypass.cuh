@@ -171,6 +171,29 @@ struct GeoRec {
     static constexpr int STRIDE = (X + IN + 3) & ~3;
 };
 
+// c += a * (b, b) on a pair of fp32 lanes (FFMA2, sm_100): two outputs per
+// instruction, each rounded exactly as a scalar FFMA.
+__device__ __forceinline__ void ffma2(float2& c, float2 a, float b) {
+    unsigned long long& cc = *reinterpret_cast<unsigned long long*>(&c);
+    const float2 bb = make_float2(b, b);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;"
+        : "+l"(cc)
+        : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&bb)));
+}
+
+// acc[k] += y * v[k] over an even channel count, two channels per FFMA2.
+template <int N>
+__device__ __forceinline__ void axpy_pairs(float (&acc)[N], const VecF<N>& v, float y) {
+    static_assert(N % 2 == 0, "channel counts are even");
+#pragma unroll
+    for (int k = 0; k < N; k += 2) {
+        float2 a = make_float2(acc[k], acc[k + 1]);
+        ffma2(a, make_float2(v.v[k], v.v[k + 1]), y);
+        acc[k] = a.x;
+        acc[k + 1] = a.y;
+    }
+}
+
 // decode_fused (renderer.cpp:88-147), geometry + feature part, for one sample
 // at p (f64 world point); dneg = -dir = view vector toward the camera.
 // Produces the MLP input x and the tri-plane samples pv.
@@ -279,9 +302,7 @@ __device__ __forceinline__ void decode_features(const RayPassParams& P, int tile
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
                     if (j < nc) {
-                        const VecF<NA> cv = lds_vec<NA>(c + j * NA);
-#pragma unroll
-                        for (int k = 0; k < NA; ++k) acc[k] += Y[j] * cv.v[k];
+                        axpy_pairs<NA>(acc, lds_vec<NA>(c + j * NA), Y[j]);
                     }
                 }
             } else {
@@ -289,9 +310,7 @@ __device__ __forceinline__ void decode_features(const RayPassParams& P, int tile
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
                     if (j < nc) {
-                        const VecF<NA> cv = ldg_vec<NA>(c + j * NA);
-#pragma unroll
-                        for (int k = 0; k < NA; ++k) acc[k] += Y[j] * cv.v[k];
+                        axpy_pairs<NA>(acc, ldg_vec<NA>(c + j * NA), Y[j]);
                     }
                 }
             }
@@ -306,16 +325,6 @@ __device__ __forceinline__ void decode_features(const RayPassParams& P, int tile
 #pragma unroll
         for (int k = 1; k < NPOW; ++k) x[NS + NA + k] = x[NS + NA + k - 1] * u;
     }
-}
-
-// c += a * (b, b) on a pair of fp32 lanes (FFMA2, sm_100): two outputs per
-// instruction, each rounded exactly as a scalar FFMA.
-__device__ __forceinline__ void ffma2(float2& c, float2 a, float b) {
-    unsigned long long& cc = *reinterpret_cast<unsigned long long*>(&c);
-    const float2 bb = make_float2(b, b);
-    asm("fma.rn.f32x2 %0, %1, %2, %0;"
-        : "+l"(cc)
-        : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&bb)));
 }
 
 // decode_color (decoder.cpp:61-109) from the MLP input.  Layers 1 and 2 run

@@ -1821,14 +1821,13 @@ __global__ void __launch_bounds__(BLOCK) shade_geo_kernel(RayPassParams P, WaveB
                         const float4 w4 = *reinterpret_cast<const float4*>(row + 4 * half);
                         const float wc[4] = {w4.x, w4.y, w4.z, w4.w};
                         const float y = row[8 + j];
-                        float u[NA];
+                        VecF<NA> u;
 #pragma unroll
-                        for (int k = 0; k < NA; ++k) u[k] = y * row[24 + k];
+                        for (int k = 0; k < NA; ++k) u.v[k] = y * row[24 + k];
 #pragma unroll
                         for (int cc = 0; cc < 4; ++cc) {
                             anyc[cc] |= wc[cc] != 0.f;
-#pragma unroll
-                            for (int k = 0; k < NA; ++k) a[cc][k] += wc[cc] * u[k];
+                            axpy_pairs<NA>(a[cc], u, wc[cc]);  // FFMA2
                         }
                     }
 #pragma unroll
