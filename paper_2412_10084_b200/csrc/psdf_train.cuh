@@ -1428,7 +1428,10 @@ struct MmaDims {
 };
 
 template <int NS, int NA>
-__global__ void __launch_bounds__(BLOCK) shade_bwd_kernel(RayPassParams P, WaveBufs W) {
+#ifndef PSDF_BWD_MINB
+#define PSDF_BWD_MINB 1
+#endif
+__global__ void __launch_bounds__(BLOCK, PSDF_BWD_MINB) shade_bwd_kernel(RayPassParams P, WaveBufs W) {
     const int n_rec = n_sorted(W);
     constexpr int IN = NS + NA + NPOW;
     using D = MmaDims<IN>;
