@@ -814,8 +814,8 @@ void launch_empty_ray_loss(psdf_ctx* c, const RayPassParams& P, cudaStream_t st)
     if (n_work <= 0) return;
     if (st != c->stream) CK(cudaStreamWaitEvent(st, c->ev_scanned, 0));
     if (c->images_pending) CK(cudaStreamWaitEvent(st, c->ev_rgb, 0));
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n_work + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
-                                                                (int64_t)16 * c->sm_count));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n_work + 4 * WARPS_PER_BLOCK - 1) / (4 * WARPS_PER_BLOCK),
+                                                                (int64_t)8 * c->sm_count));
     empty_ray_loss_kernel<<<(unsigned)grid, BLOCK, 0, st>>>(P, c->wave, n_work);
     CK(cudaGetLastError());
     ++c->last_launches;

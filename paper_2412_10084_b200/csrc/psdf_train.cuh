@@ -360,16 +360,36 @@ __global__ void __launch_bounds__(BLOCK) empty_ray_loss_kernel(RayPassParams P, 
     double st_photo = 0.0, st_sq = 0.0;
     unsigned long long st_mask = 0, c_bwd = 0;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t wi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); wi < n_work; wi += warps) {
-        const unsigned hb = __ldg(W.hand_bits + wi);
-        if (hb == FULL) continue;
-        const LaneRay R = lane_ray(P, (int)wi, lane);
-        if (!R.valid || ((hb >> lane) & 1u)) continue;
-        const bool in_mask = __ldg(R.V->mask + R.px) != 0;
-        const double col[3] = {P.bg[0], P.bg[1], P.bg[2]};
-        double g0, g1, g2, dA;
-        if (photo_term(P, in_mask, R.V->gt + 3 * R.px, col, 0.0, g0, g1, g2, dA, st_photo, st_sq, st_mask))
-            ++c_bwd;
+    // four work tiles per warp and iteration, their hand-over words and mask
+    // bytes loaded before any is used (the one-tile loop was latency bound on
+    // these two dependent loads)
+    constexpr int U = 4;
+    for (int64_t w0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * U; w0 < n_work;
+         w0 += warps * U) {
+        unsigned hb[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) hb[u] = w0 + u < n_work ? __ldg(W.hand_bits + w0 + u) : FULL;
+        LaneRay R[U];
+        bool act[U];
+        uint8_t m[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            act[u] = hb[u] != FULL;
+            if (act[u]) {
+                R[u] = lane_ray(P, (int)(w0 + u), lane);
+                act[u] = R[u].valid && !((hb[u] >> lane) & 1u);
+            }
+            m[u] = act[u] ? __ldg(R[u].V->mask + R[u].px) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (!act[u]) continue;
+            const double col[3] = {P.bg[0], P.bg[1], P.bg[2]};
+            double g0, g1, g2, dA;
+            if (photo_term(P, m[u] != 0, R[u].V->gt + 3 * R[u].px, col, 0.0, g0, g1, g2, dA, st_photo, st_sq,
+                           st_mask))
+                ++c_bwd;
+        }
     }
     // block-wide sums, one atomic per value per block
     st_photo = warp_sum_d(st_photo);
