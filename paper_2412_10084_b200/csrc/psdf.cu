@@ -193,6 +193,9 @@ struct psdf_ctx {
     bool images_pending = false;           // inside psdf_train_step: the copies may still run
     cudaEvent_t ev_masks = nullptr, ev_rgb = nullptr;  // masks / colours of the step copied
     unsigned* d_hand_bits = nullptr;       // [work tiles] scan hand-over lanes
+    float* d_tmin = nullptr;               // [work tiles] first allocated-tile hit bound (tile_raster_kernel)
+    int64_t tmin_cap = 0;
+    int64_t batch_tiles = 0;               // work tiles of the current view table (upload_viewdev)
     int64_t active_tiles = 0;              // work tiles on the scan's list (upload_viewdev)
     int64_t hand_cap = 0;
     cudaEvent_t ev_ray0 = nullptr, ev_ray1 = nullptr, ev_step0 = nullptr, ev_step1 = nullptr;
@@ -460,6 +463,7 @@ int64_t upload_viewdev(psdf_ctx* c, std::vector<ViewDev>& vd) {
         active += v.act_n;
     }
     c->active_tiles = active;
+    c->batch_tiles = tiles;
     if ((int)vd.size() > c->viewdev_cap) {
         if (c->d_viewdev) cudaFree(c->d_viewdev);
         CK(cudaMalloc(&c->d_viewdev, sizeof(ViewDev) * vd.size()));
@@ -679,6 +683,24 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     // bits 0 (train: empty-ray terms) / the background (render: filled here)
     P.scan_lo = 0;
     P.scan_hi = c->active_tiles;
+    // per work tile: lower bound on the first allocated-tile hit (tile_raster_kernel)
+    const int64_t all_tiles = c->batch_tiles;  // every view's work tiles (this rank scans its slice)
+    if (c->tmin_cap < all_tiles) {
+        if (c->d_tmin) cudaFree(c->d_tmin);
+        c->d_tmin = nullptr;
+        CK(cudaMalloc(&c->d_tmin, sizeof(float) * std::max<int64_t>(all_tiles, 1)));
+        c->tmin_cap = all_tiles;
+    }
+    {
+        CK(cudaMemsetAsync(c->d_tmin, 0x7F, sizeof(float) * std::max<int64_t>(all_tiles, 1), s));
+        const int64_t warps = (int64_t)c->desc.T * P.n_views;
+        if (warps > 0) {
+            tile_raster_kernel<<<(unsigned)((warps + 3) / 4), 128, 0, s>>>(P.g, P.views, P.n_views, c->d_tmin);
+            CK(cudaGetLastError());
+            ++c->last_launches;
+        }
+    }
+    P.tile_tmin = c->d_tmin;
     if (P.mode != 1) {
         CK(cudaMemsetAsync(W.hand_bits, 0, sizeof(unsigned) * std::max<int64_t>(n_work, 1), s));
     } else {
@@ -1224,7 +1246,7 @@ int psdf_destroy(psdf_ctx* c) {
             if (v.mask) cudaFree(v.mask);
         }
         for (void* p : {(void*)c->d_stage_rgb, (void*)c->d_stage_mask, (void*)c->d_viewdev,
-                        (void*)c->d_render, (void*)c->d_eval, (void*)c->d_mc, (void*)c->d_mesh, (void*)c->d_work, (void*)c->d_counts, (void*)c->d_stats})
+                        (void*)c->d_render, (void*)c->d_eval, (void*)c->d_mc, (void*)c->d_mesh, (void*)c->d_tmin, (void*)c->d_work, (void*)c->d_counts, (void*)c->d_stats})
             if (p) cudaFree(p);
         free_wave(c);
         if (c->wave.counters) cudaFree(c->wave.counters);

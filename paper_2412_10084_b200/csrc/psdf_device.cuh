@@ -482,6 +482,24 @@ struct Marcher {
         return true;
     }
 
+    // A jump to the last lattice point before `tl`, a lower bound on the
+    // distance at which the ray can first meet an allocated tile (the scan's
+    // per-work-tile bound, tile_raster_kernel): every lattice point it passes
+    // lies in unallocated tiles, so the lattice argument of next_impl's jumps
+    // applies (the marcher stays desynchronised until its next tile skip and
+    // rewinds to t_sync on an ambiguous decision).  Call after init() /
+    // enter_occupied().
+    __device__ __forceinline__ void jump_to(const GridView& g, double tl) {
+        if (g.h_pow2 && t >= 64.0 * g.h && tl > t) {
+            const double m = floor((tl - t) * g.inv_h) - 1.0;
+            if (m >= 2.0) {
+                PSDF_STAT(4);
+                if (t_sync < 0.0) t_sync = t;
+                t = lattice_advance(t, m, g.h);
+            }
+        }
+    }
+
     // Resumes a ray whose box exit t1 is known (the caller sets t and count
     // to a point the reference visited).
     __device__ __forceinline__ void init_from(const GridView& g, const double* o_, const double* d_,

@@ -66,6 +66,7 @@ struct RayPassParams {
     int n_views;
     int64_t tile_begin, tile_end;  // this rank's slice of the global work tiles
     int64_t scan_lo, scan_hi;      // K2a-scan: active-tile list range [lo, hi) (ViewDev::act_*)
+    const float* tile_tmin;        // [global work tiles] lower bound on the first allocated-tile hit (kTminNone: none)
     unsigned long long* work_counter;
     // render outputs (K1)
     float* out_rgb;

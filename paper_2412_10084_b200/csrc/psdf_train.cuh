@@ -163,6 +163,8 @@ __device__ __forceinline__ void chunk_close(WarpChunk& c, int lane, F hole) {
     c.left = 0;
 }
 
+constexpr float kTminNone = 3.0e38f;  // at or above: "no tile" (the byte memset 0x7F7F7F7F is 3.396e38; tile_raster_kernel)
+
 struct LaneRay {
     const ViewDev* V;
     int u, v;
@@ -247,6 +249,8 @@ __global__ void __launch_bounds__(BLOCK, PSDF_SCAN_MINB) march_scan_kernel(RayPa
         if (ak >= P.scan_hi) break;
         const int64_t gt = active_tile(P, ak);
         if (gt < P.tile_begin || gt >= P.tile_end) continue;
+        const float tl = __ldg(P.tile_tmin + gt);
+        if (tl >= kTminNone) continue;  // no allocated tile in this work tile's frustum: no sample
         const int wi = (int)(gt - P.tile_begin);
         const LaneRay R = lane_ray(P, wi, lane);
         Marcher mr;
@@ -258,6 +262,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_SCAN_MINB) march_scan_kernel(RayPa
             const D3 dir = pixel_dir(R.V->cam, (double)R.u + 0.5, (double)R.v + 0.5);
             const double dd[3] = {dir.x, dir.y, dir.z};
             if (mr.init(g, R.V->cam.pos, dd, P.n_max) && mr.enter_occupied(g)) {
+                mr.jump_to(g, (double)tl);
                 for (;;) {
                     double ts;
                     int tile;
@@ -332,6 +337,75 @@ __global__ void __launch_bounds__(BLOCK, PSDF_SCAN_MINB) march_scan_kernel(RayPa
         atomicAdd(P.counts + 1, m);
         atomicAdd(P.counts + 2, x);
         atomicAdd(P.counts + 5, bw);
+    }
+}
+
+// Per 8x4 work tile of every view, a lower bound on the distance along its
+// rays to the first allocated tile (the scan jumps there at once; a work tile
+// with no bound has no sample at all).  One warp per (allocated tile, view):
+// the tile's AABB projected through its 8 corners (padded by a pixel) marks
+// the work tiles whose pixel rays can meet it, each receiving the camera's
+// distance to the AABB minus 2 voxels (a point of the ray at parameter t is
+// at distance t from the camera: directions are unit).  Tiles with a corner
+// beside or behind the camera mark the whole view.  atomicMin on the float
+// bits (non-negative floats order as integers).
+__global__ void __launch_bounds__(128) tile_raster_kernel(GridView g, const ViewDev* views, int n_views,
+                                                          float* __restrict__ tmin) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (gw >= (int64_t)g.T * n_views) return;
+    const int tile = (int)(gw / n_views), vi = (int)(gw - (int64_t)tile * n_views);
+    const ViewDev& V = views[vi];
+    const Cam& k = V.cam;
+    const int4 tc = __ldg(g.tile_coords + tile);
+    const double s16 = 16.0 * g.h;
+    const double lo[3] = {g.org[0] + s16 * tc.x, g.org[1] + s16 * tc.y, g.org[2] + s16 * tc.z};
+    float u = 0.f, v = 0.f;
+    bool bad = false;
+    if (lane < 8) {
+        const double p[3] = {lo[0] + ((lane & 1) ? s16 : 0.0), lo[1] + ((lane & 2) ? s16 : 0.0),
+                             lo[2] + ((lane & 4) ? s16 : 0.0)};
+        const double d[3] = {p[0] - k.pos[0], p[1] - k.pos[1], p[2] - k.pos[2]};
+        const double cx = k.rot[0] * d[0] + k.rot[3] * d[1] + k.rot[6] * d[2];
+        const double cy = k.rot[1] * d[0] + k.rot[4] * d[1] + k.rot[7] * d[2];
+        const double cz = k.rot[2] * d[0] + k.rot[5] * d[1] + k.rot[8] * d[2];
+        bad = !(cz > 1e-6);
+        u = bad ? 0.f : (float)(k.fx * cx / cz + k.cx);
+        v = bad ? 0.f : (float)(k.fy * cy / cz + k.cy);
+    }
+    float umin = lane < 8 ? u : 3e38f, umax = lane < 8 ? u : -3e38f;
+    float vmin = lane < 8 ? v : 3e38f, vmax = lane < 8 ? v : -3e38f;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+        umin = fminf(umin, __shfl_xor_sync(FULL, umin, o));
+        umax = fmaxf(umax, __shfl_xor_sync(FULL, umax, o));
+        vmin = fminf(vmin, __shfl_xor_sync(FULL, vmin, o));
+        vmax = fmaxf(vmax, __shfl_xor_sync(FULL, vmax, o));
+    }
+    umin = __shfl_sync(FULL, umin, 0);
+    umax = __shfl_sync(FULL, umax, 0);
+    vmin = __shfl_sync(FULL, vmin, 0);
+    vmax = __shfl_sync(FULL, vmax, 0);
+    bad = __any_sync(FULL, bad);
+    // distance from the camera to the AABB, minus 2 voxels, rounded down
+    double q = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double e = fmax(fmax(lo[a] - k.pos[a], k.pos[a] - (lo[a] + s16)), 0.0);
+        q += e * e;
+    }
+    const float tv = __double2float_rd(fmax(sqrt(q) - 2.0 * g.h, 0.0));
+    int tx0 = 0, tx1 = V.tiles_x - 1, ty0 = 0, ty1 = V.tiles_y - 1;
+    if (!bad) {  // work tile tx spans image points [8 tx + 0.5, 8 tx + 7.5]
+        tx0 = max(tx0, (int)ceilf((umin - 1.f - 7.5f) * 0.125f));
+        tx1 = min(tx1, (int)floorf((umax + 1.f - 0.5f) * 0.125f));
+        ty0 = max(ty0, (int)ceilf((vmin - 1.f - 3.5f) * 0.25f));
+        ty1 = min(ty1, (int)floorf((vmax + 1.f - 0.5f) * 0.25f));
+    }
+    const int w = tx1 - tx0 + 1, n = w > 0 && ty1 >= ty0 ? w * (ty1 - ty0 + 1) : 0;
+    for (int i = lane; i < n; i += 32) {
+        const int ty = ty0 + i / w, tx = tx0 + (i - (i / w) * w);
+        atomicMin(reinterpret_cast<int*>(tmin) + V.tile_begin + (int64_t)ty * V.tiles_x + tx, __float_as_int(tv));
     }
 }
 
