@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(256) loss_features_kernel(GridView g, int t0, 
                                                             float* __restrict__ g_planes,
                                                             double* stats) {
     __shared__ __align__(16) float pl[256 * NS];
-    __shared__ double red[8];
+    __shared__ double red[16];  // block_add_f64v<2>: 2 values x 8 warps
     const int t = t0 + blockIdx.x / 3, q = blockIdx.x % 3;
     const float* p = g.planes + ((int64_t)t * 3 + q) * 256 * NS;
     float* gp = g_planes + ((int64_t)t * 3 + q) * 256 * NS;
@@ -583,12 +583,15 @@ __global__ void __launch_bounds__(256) loss_features_kernel(GridView g, int t0, 
     if (b + 1 < 16) pair(ab, ab + 1, true, -1.f);    // pair (i0, (a, b+1))
     if (a >= 1) pair(ab - 16, ab, false, 1.f);       // pair ((a-1, b), i0): +g to i0
     if (b >= 1) pair(ab - 1, ab, false, 1.f);        // pair ((a, b-1), i0)
-    // atomic: the kernel may run beside the ray pass's plane-gradient scatters
+    // atomic (the kernel may run beside the ray pass's plane-gradient
+    // scatters), one vector reduction per texel
+    bool any = false;
 #pragma unroll
-    for (int k = 0; k < NS; ++k)
-        if (gsum[k] != 0.f) atomicAdd(gp + ab * NS + k, gsum[k]);
-    block_add_f64(stats + 6, (double)pw, red);
-    block_add_f64(stats + 11, (double)ww, red);
+    for (int k = 0; k < NS; ++k) any |= gsum[k] != 0.f;
+    if (any) red_vec<NS>(gp + ab * NS, gsum);
+    double* dst[2] = {stats + 6, stats + 11};
+    double v2[2] = {(double)pw, (double)ww};
+    block_add_f64v<2>(dst, v2, red);
 }
 
 // K6: loss_probes (losses.cpp:259-283) over probes [p0, p1); one thread per
