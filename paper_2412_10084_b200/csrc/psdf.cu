@@ -189,6 +189,7 @@ struct psdf_ctx {
     cudaEvent_t ev_start = nullptr, ev_zeroed = nullptr;
     bool regs_early = false;             // PSDF_REGS_EARLY: fork the regularizer at step start
     bool fork_after_scan = false;        // PSDF_REGS_AFTER_SCAN: fork it after the scan, not after round 0
+    bool regs_serial = false;            // PSDF_REGS_SERIAL: regularizers after the ray pass, main stream
     cudaEvent_t ev_copied = nullptr, ev_copy_free = nullptr;
     bool images_pending = false;           // inside psdf_train_step: the copies may still run
     cudaEvent_t ev_masks = nullptr, ev_rgb = nullptr;  // masks / colours of the step copied
@@ -1012,7 +1013,9 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
         launch_empty_ray_loss(c, P, sl);
         if (overlap) CK(cudaEventRecord(c->ev_join, c->side_stream));
     };
-    const bool overlap = !c->keep_raypass;
+    // the regularizers on the side stream under the ray pass, or after it on
+    // the main stream (PSDF_REGS_SERIAL, A/B)
+    const bool overlap = !c->keep_raypass && !c->regs_serial;
     // images still arriving (psdf_train_step): the regularizer runs under the
     // copies; resident images: under the ray pass's tail (forked by it)
     // the regularizer forks after the first composite round (it fills the
@@ -1206,6 +1209,7 @@ int psdf_create(int device, psdf_ctx** out) {
         if (const char* e = std::getenv("PSDF_STAGE_FWD")) c->stage_fwd = std::atoi(e) != 0;
         if (const char* e = std::getenv("PSDF_REGS_EARLY")) c->regs_early = std::atoi(e) != 0;
         if (const char* e = std::getenv("PSDF_REGS_AFTER_SCAN")) c->fork_after_scan = std::atoi(e) != 0;
+        if (const char* e = std::getenv("PSDF_REGS_SERIAL")) c->regs_serial = std::atoi(e) != 0;
         if (const char* m = std::getenv("PSDF_TEST_MARGIN")) c->test_margin = std::max(1e-8, std::atof(m));
         CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithPriority(&c->side_stream, cudaStreamNonBlocking, prio_lo));
