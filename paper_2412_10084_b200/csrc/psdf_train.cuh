@@ -1212,6 +1212,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_FWD_MINB) shade_fwd_kernel(RayPass
 template <int IN>
 struct FwdDims {
     static constexpr int K1 = (IN + 7) & ~7;  // input width padded to the MMA k step
+    static_assert(K1 > IN, "the bias-gradient ones column needs a padding slot");
     static constexpr int XS = K1 + 4;         // row stride of W1 (conflict-free B fragments)
     static constexpr int HS = 36;             // row stride of 32-wide rows
     // pre-split weights (uint32 TF32 words): hi, then lo
@@ -1563,8 +1564,9 @@ __global__ void __launch_bounds__(BLOCK, PSDF_BWD_MINB) shade_bwd_kernel(RayPass
     zero_c(gw2);
     zero_c(gw1);
     zero_c(gw3);
-    float gb1 = 0.f, gb2 = 0.f, gb3 = 0.f;
+    float gb2 = 0.f, gb3 = 0.f;  // db1 comes out of the dW1 GEMM (ones column)
     const float* cam_base = P.mlp + G.cam;
+    const bool has_cam = P.ncam > 0;
     float* X = scr + D::SX;
     float* A1 = scr + D::SA1;
     float* A2 = scr + D::SA2;
@@ -1593,6 +1595,10 @@ __global__ void __launch_bounds__(BLOCK, PSDF_BWD_MINB) shade_bwd_kernel(RayPass
                 const float* rg = W.r_geo + (int64_t)i * GR::STRIDE;
 #pragma unroll
                 for (int q = 0; q < IN; ++q) x[q] = rg[GR::X + q];
+                // a ones column in the first padding slot: the dW1 GEMM's
+                // column IN is then db1 = sum_m DZ1[m] (W1's padding is zero,
+                // so the forward recompute and DIN are unchanged)
+                x[IN] = 1.f;
                 ndv = rg[7];
                 const float4 cr = reinterpret_cast<const float4*>(W.r_c)[i];
                 d3[0] = up.x * cr.x * (1.f - cr.x);  // sigmoid'
@@ -1613,11 +1619,18 @@ __global__ void __launch_bounds__(BLOCK, PSDF_BWD_MINB) shade_bwd_kernel(RayPass
             warp_gemm3<2, 4, D::K1 / 8>(
                 c, [&](int m, int k) { return X[m * D::XS + k]; },
                 [&](int n, int k) { return sm[D::W1 + n * D::XS + k]; });
-            for_c(c, [&](int m, int n, float& v) {
-                float z = v + sm[D::B1 + n];
-                if (cam[m] >= 0) z += __ldg(cam_base + cam[m] * HID + n);
-                A1[m * D::HS + n] = z > 0.f ? z : 0.f;
-            });
+            if (has_cam) {
+                for_c(c, [&](int m, int n, float& v) {
+                    float z = v + sm[D::B1 + n];
+                    if (cam[m] >= 0) z += __ldg(cam_base + cam[m] * HID + n);
+                    A1[m * D::HS + n] = z > 0.f ? z : 0.f;
+                });
+            } else {
+                for_c(c, [&](int m, int n, float& v) {
+                    const float z = v + sm[D::B1 + n];
+                    A1[m * D::HS + n] = z > 0.f ? z : 0.f;
+                });
+            }
         }
         __syncwarp();
         // A2 = relu(A1 W2^T + b2)
@@ -1683,7 +1696,6 @@ __global__ void __launch_bounds__(BLOCK, PSDF_BWD_MINB) shade_bwd_kernel(RayPass
             warp_gemm3<2, D::K1 / 8, 4>(
                 gw1, [&](int m, int k) { return A1[k * D::HS + m]; },
                 [&](int n, int k) { return X[k * D::XS + n]; });
-            for (int r = 0; r < 32; ++r) gb1 += A1[r * D::HS + lane];
             if (P.ncam > 0) {
                 const int my = cam[lane];
                 unsigned rem = __ballot_sync(FULL, my >= 0);
@@ -1738,14 +1750,13 @@ __global__ void __launch_bounds__(BLOCK, PSDF_BWD_MINB) shade_bwd_kernel(RayPass
     for_c(gw3, [&](int m, int n, float& v) {
         if (m < 3) gacc[D::GW3 + m * D::HS + n] = v;
     });
-    gacc[D::GB1 + lane] = gb1;
     gacc[D::GB2 + lane] = gb2;
     if (lane < 3) gacc[D::GB3 + lane] = gb3;
     __syncthreads();
     for (int q = threadIdx.x; q < G.total_nocam; q += blockDim.x) {
         int a;
         if (q < G.b1) a = D::GW1 + (q / IN) * D::XS + (q % IN);
-        else if (q < G.w2) a = D::GB1 + (q - G.b1);
+        else if (q < G.w2) a = D::GW1 + (q - G.b1) * D::XS + IN;  // db1: the ones column
         else if (q < G.b2) a = D::GW2 + ((q - G.w2) >> 5) * D::HS + ((q - G.w2) & 31);
         else if (q < G.w3) a = D::GB2 + (q - G.b2);
         else if (q < G.b3) a = D::GW3 + ((q - G.w3) >> 5) * D::HS + ((q - G.w3) & 31);
