@@ -494,8 +494,8 @@ def main():
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                "kernel": "K2 ray pass: march_scan + march_fwd (2 rounds) + record sort + shade_fwd<4,4> + "
-                          "alpha_bwd + shade_bwd<4,4> + shade_geo<4,4>",
+                "kernel": "K2 ray pass: tile_raster + march_scan + march_fwd (round 0) + march_coop (round 1) + "
+                          "record sort + shade_fwd<4,4> + alpha_bwd + shade_bwd<4,4> + shade_geo<4,4>",
                 "algorithmic_bytes_per_launch": k2_bytes, "kernel_ms": k2_ms, "peak_source": peak_src,
                 "k2_share_of_step": k2_ms / statistics.mean(step_ms),
                 "k2_kernels_ms": dict(zip(["scan+march+sort", "shade_fwd", "alpha_bwd", "shade_bwd+geo"],
