@@ -38,7 +38,7 @@
 #include "psdf_raypass.cuh"
 
 #ifndef PSDF_MARCH_MINB
-#define PSDF_MARCH_MINB 4
+#define PSDF_MARCH_MINB 3  // r02: round 0 218 vs 229 us at 4
 #endif
 
 namespace psdf {
@@ -1154,7 +1154,7 @@ __global__ void __launch_bounds__(256) rec_tile_scatter_kernel(WaveBufs W, int* 
 // ------------------------------------------------------------------ K2b
 template <int NS, int NA, bool GEO>
 #ifndef PSDF_FWD_MINB
-#define PSDF_FWD_MINB 5  // <= 102 registers: 5 blocks per SM (measured best)
+#define PSDF_FWD_MINB 4  // 4 blocks per SM (r02: 299 vs 332 us at 5; with FFMA2 the register cap cost more)
 #endif
 __global__ void __launch_bounds__(BLOCK, PSDF_FWD_MINB) shade_fwd_kernel(RayPassParams P, WaveBufs W) {
     const int n_rec = n_sorted(W);
