@@ -183,7 +183,7 @@ struct psdf_ctx {
     cudaStream_t copy_stream = nullptr;  // host->device image staging of psdf_train_step
     cudaStream_t side_stream = nullptr;  // low priority: regularizers under the ray pass
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    cudaEvent_t ev_scanned = nullptr;    // after the scan (hand-over bits and the view table written)
+    cudaEvent_t ev_scanned = nullptr;    // after the composite pass (hand-over bits final, view table written)
     bool fork_regs = false;              // the ray pass records ev_fork (do_train_step)
     bool grads_clear_pending = false;    // gradient clear on the side stream (ev_zeroed)
     cudaEvent_t ev_start = nullptr, ev_zeroed = nullptr;
@@ -712,9 +712,6 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     march_scan_kernel<<<(unsigned)grid_s, BLOCK, smem_bits, s>>>(P, W);
     CK(cudaGetLastError());
     ++c->last_launches;
-    // the empty rays' photo terms (side stream) read the hand-over bits and
-    // the view table: they wait for this point, whichever fork they took
-    CK(cudaEventRecord(c->ev_scanned, s));
     // handovers in append order: a warp's handovers come from one 8x4 pixel
     // tile and neighbouring warps from neighbouring work tiles (a sort by
     // pixel measured slower than it saved)
@@ -735,6 +732,10 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     else
         march_fwd_kernel<<<(unsigned)grid_a, BLOCK, smem_bits, s>>>(P, W, 1, INT_MAX);
     CK(cudaGetLastError());
+    // the empty rays' photo terms (side stream) read the hand-over bits (the
+    // scan's, less the rays the composite pass ended without an alpha > 0
+    // settle) and the view table: they wait for this point
+    CK(cudaEventRecord(c->ev_scanned, s));
     c->last_launches += 2;
     if (getenv("PSDF_DEBUG_MARCH")) {
         unsigned long long cc[8];

@@ -425,7 +425,9 @@ __global__ void __launch_bounds__(256) render_fill_kernel(RayPassParams P, int64
     }
 }
 
-// photo_pixel (losses.cpp:8-38) of the rays the scan finished (no alpha > 0
+// photo_pixel (losses.cpp:8-38) of the rays the scan finished and of the
+// handed-over rays the composite pass ended without an alpha > 0 settle (it
+// clears their hand-over bit) (no alpha > 0
 // settle: colour = background, acc = 0, so only the loss statistics and the
 // backward-ray count change — nothing is back-propagated).  One warp per
 // 8x4 pixel work tile.
@@ -763,14 +765,11 @@ __global__ void __launch_bounds__(BLOCK, PSDF_MARCH_MINB) march_fwd_kernel(RayPa
                 P.out_rgb[3 * R.px + 2] = (float)dmul(P.bg[2], om);
             }
         } else if (valid && entry < 0 && cnt_first < 0) {
-            // no alpha > 0 sample: acc = 0, no shaded sample, nothing to
-            // back-propagate; the loss is final now
-            const double om = dsub(1.0, acc);
-            const double col[3] = {dmul(P.bg[0], om), dmul(P.bg[1], om), dmul(P.bg[2], om)};
-            double g0, g1, g2, dA;
-            if (photo_term(P, in_mask, R.V->gt + 3 * R.px, col, acc, g0, g1, g2, dA, st_photo,
-                           st_sq, st_mask))
-                ++c_bwd;
+            // no alpha > 0 sample: acc = 0, colour = background, nothing to
+            // back-propagate — exactly the empty-ray term, taken by
+            // empty_ray_loss_kernel once the colours are in HBM (this kernel
+            // only waits for the masks)
+            atomicAnd(W.hand_bits + (slot >> 5), ~(1u << (slot & 31)));
         }
     }
     chunk_close(ch_e, lane, hole_e);
@@ -1050,12 +1049,8 @@ __global__ void __launch_bounds__(BLOCK, PSDF_COOP_MINB) march_coop_kernel(RayPa
                 P.out_rgb[3 * R.px + 1] = (float)dmul(P.bg[1], om);
                 P.out_rgb[3 * R.px + 2] = (float)dmul(P.bg[2], om);
             }
-        } else if (entry < 0 && cnt_first < 0) {
-            const double om = dsub(1.0, acc);
-            const double col[3] = {dmul(P.bg[0], om), dmul(P.bg[1], om), dmul(P.bg[2], om)};
-            double g0, g1, g2, dA;
-            if (photo_term(P, in_mask, R.V->gt + 3 * R.px, col, acc, g0, g1, g2, dA, st_photo, st_sq, st_mask))
-                ++c_bwd;
+        } else if (entry < 0 && cnt_first < 0) {  // the empty-ray term (see march_fwd_kernel)
+            atomicAnd(W.hand_bits + (slot >> 5), ~(1u << (slot & 31)));
         }
     }
     chunk_close(ch_e, lane, hole_e);
