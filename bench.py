@@ -352,6 +352,8 @@ def main():
                     help="how ranks combine gradients (psdf_set_grad_exchange; N > 1 only)")
     ap.add_argument("--profile", action="store_true",
                     help="setup + warm-up + 2 train steps + 1 render, no JSON (for ncu)")
+    ap.add_argument("--profile-render", action="store_true",
+                    help="setup + warm-up, then one configs[3] render inside cudaProfilerStart/Stop (for ncu)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     W.update(CONFIGS[args.config])
@@ -413,6 +415,10 @@ def main():
     stream = torch.cuda.ExternalStream(L.psdf_stream(ctx.h))
     for it in range(args.warmup):
         ctx.train_step_views(batch_ids(it, world), hp)
+    if args.profile_render:
+        render_fps(api, torch, ctx, 6455.3, frames=1, profile=True)
+        ctx.close()
+        return
     if args.profile:
         # the second step runs inside cudaProfilerStart/Stop, so
         # `ncu --profile-from-start off` captures exactly one train step
@@ -589,7 +595,7 @@ def main():
         dist.destroy_process_group()
 
 
-def render_fps(api, torch, ctx, peak, frames=20):
+def render_fps(api, torch, ctx, peak, frames=20, profile=False):
     """configs[3]: 1080p inference render of the R^3 scene (K1) — device
     outputs (kernel / FPS) and through psdf_render with host outputs (e2e,
     the D2H of the RGB, alpha and depth images inside the timed region)."""
@@ -604,6 +610,15 @@ def render_fps(api, torch, ctx, peak, frames=20):
     for _ in range(3):
         _lib.check(L.psdf_render_device(ctx.h, C.byref(cam), C.byref(opts), C.c_void_p(rgb),
                                         C.c_void_p(alpha), C.c_void_p(depth), C.byref(cnt)), ctx.h)
+    if profile:  # one frame for `ncu --profile-from-start off`
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStart()
+        _lib.check(L.psdf_render_device(ctx.h, C.byref(cam), C.byref(opts), C.c_void_p(rgb),
+                                        C.c_void_p(alpha), C.c_void_p(depth), C.byref(cnt)), ctx.h)
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStop()
+        print(cnt.as_dict())
+        return None
     kms = []
     stream = torch.cuda.ExternalStream(L.psdf_stream(ctx.h))
     torch.cuda.synchronize()
@@ -628,7 +643,20 @@ def render_fps(api, torch, ctx, peak, frames=20):
     L.psdf_host_free(C.c_void_p(hp))
     c = cnt.as_dict()
     b = algorithmic_bytes(c, "render")
+    # measured DRAM bytes per marched sample of the render kernels (one ncu
+    # capture of `bench.py --profile-render`, profiles/render_traffic.json)
+    meas = None
+    rp = os.path.join(ROOT, "profiles", "render_traffic.json")
+    if os.path.exists(rp):
+        try:
+            rj = json.load(open(rp))
+            if rj.get("res") == W["res"]:
+                meas = {"dram_bytes_per_marched_sample": rj["dram_bytes"] / max(rj["n_marched"], 1),
+                        "dram_bytes_per_frame": rj["dram_bytes"], "source": rj.get("source")}
+        except Exception:
+            meas = None
     return {"config": f"configs[3]: 1920x1080 view of the {W['res']}^3 scene, tau=3000/voxel",
+            "measured_traffic": meas,
             "fps": 1000.0 / ms, "ms_per_frame": ms, "kernel_ms": statistics.mean(kms),
             "e2e_fps": 1000.0 / e2e_ms, "e2e_ms_per_frame": e2e_ms, "e2e_d2h_bytes_per_frame": 20 * px,
             "marched_samples": c["n_marched"], "shaded_samples": c["n_shaded"],

@@ -80,14 +80,17 @@ typedef struct {
 /* SparseGrid metadata (grid.hpp:57-70). */
 typedef struct {
     int32_t T, P;              /* allocated tiles, pool probes */
-    int32_t n_s, n_a, sh_order; /* channel widths: the kernels are instantiated for
-                                  (n_s, n_a) in {(2,2), (4,4), (8,8), (4,8), (8,4)}
-                                  (the paper's configurations and their neighbours);
-                                  the reference's DecoderMlp accepts any width
-                                  (decoder.hpp:17-31), here any other pair is
-                                  PSDF_ERR_INVALID_ARGUMENT at psdf_upload_grid /
-                                  psdf_init_visual_hull / psdf_load_checkpoint
-                                  ("unsupported (n_s, n_a)"), before any work */
+    int32_t n_s, n_a, sh_order; /* channel widths, any pair in [1, 8] x [1, 8] (the
+                                  reference's DecoderMlp takes any width,
+                                  decoder.hpp:17-31).  The kernels are
+                                  instantiated for (2,2), (4,4), (8,8), (4,8),
+                                  (8,4); another pair runs on the smallest of
+                                  those that holds it, its extra channels zero
+                                  planes / probes / W1 columns (results
+                                  unchanged), and every array crossing this ABI
+                                  stays at the caller's widths.  Wider pairs are
+                                  PSDF_ERR_INVALID_ARGUMENT ("unsupported (n_s,
+                                  n_a)") before any work */
     int32_t res[3];            /* voxels per axis, multiples of 16 */
     double voxel_size;
     double origin[3];

@@ -446,11 +446,16 @@ class Context:
                                                 _fptr(out["mlp"])))
         return out
 
+    def info(self):
+        """psdf_grid_info: the device grid's metadata at the caller's widths."""
+        d = psdf_grid_desc()
+        self._check(self.L.psdf_grid_info(self.h, C.byref(d)))
+        return d
+
     # -- LOD transitions (trainer.cpp:105, 213)
     def _refresh_grid(self):
         """Re-reads the device grid's structure and parameters into self.grid."""
-        d = psdf_grid_desc()
-        self._check(self.L.psdf_grid_info(self.h, C.byref(d)))
+        d = self.info()
         old = self.grid.cfg
         cfg = GridConfig(voxel_size=d.voxel_size, origin=tuple(d.origin), resolution=tuple(d.res),
                          n_s=d.n_s, n_a=d.n_a, sh_order=d.sh_order, far_field_voxels=d.far_field_voxels,

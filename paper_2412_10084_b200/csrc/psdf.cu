@@ -141,6 +141,57 @@ bool supported_channels(int ns, int na) {
            (ns == 4 && na == 8) || (ns == 8 && na == 4);
 }
 
+// Kernel widths for a caller's (n_s, n_a): the instantiated pair itself, or
+// the smallest instantiated pair that holds it.  The extra channels are zero
+// planes / probes with zero W1 columns, which leaves every result unchanged:
+// the MLP input gains 0 * 0 terms, the feature and probe gradients of a zero
+// W1 column are zero, so Adam keeps them at zero, and the feature / probe
+// regularizers (losses.cpp:222-290) are plain sums whose zero channels add 0.
+bool kernel_widths(int ns, int na, int* ks, int* ka) {
+    if (supported_channels(ns, na)) {
+        *ks = ns;
+        *ka = na;
+        return true;
+    }
+    if (ns < 1 || na < 1) return false;
+    static const int pairs[5][2] = {{2, 2}, {4, 4}, {4, 8}, {8, 4}, {8, 8}};
+    for (const auto& q : pairs)
+        if (q[0] >= ns && q[1] >= na && supported_channels(q[0], q[1])) {
+            *ks = q[0];
+            *ka = q[1];
+            return true;
+        }
+    return false;
+}
+
+// Row-wise repack of a [rows][ws] array into [rows][wd] (zero fill / strip).
+void repack_rows(const float* src, int64_t rows, int ws, float* dst, int wd) {
+    const int w = std::min(ws, wd);
+    for (int64_t r = 0; r < rows; ++r) {
+        std::copy(src + r * ws, src + r * ws + w, dst + r * wd);
+        std::fill(dst + r * wd + w, dst + (r + 1) * wd, 0.f);
+    }
+}
+
+// DecoderMlp blob (decoder.hpp:17-31, W1 [32][n_s + n_a + 6] first) between
+// the caller's widths (s0, a0) and (s1, a1): W1 columns re-indexed per input
+// group (spatial, angular, Fresnel powers), columns of padded channels zero,
+// everything after W1 copied.
+void repack_mlp(const float* src, int s0, int a0, float* dst, int s1, int a1, int ncam) {
+    const int in0 = s0 + a0 + NPOW, in1 = s1 + a1 + NPOW;
+    for (int j = 0; j < HID; ++j) {
+        float* row = dst + (int64_t)j * in1;
+        std::fill(row, row + in1, 0.f);
+        const float* r0 = src + (int64_t)j * in0;
+        for (int i = 0; i < std::min(s0, s1); ++i) row[i] = r0[i];
+        for (int i = 0; i < std::min(a0, a1); ++i) row[s1 + i] = r0[s0 + i];
+        for (int i = 0; i < NPOW; ++i) row[s1 + a1 + i] = r0[s0 + a0 + i];
+    }
+    const MlpLayout L0 = MlpLayout::make(in0), L1 = MlpLayout::make(in1);
+    const int64_t tail = (int64_t)L0.cam + (int64_t)ncam * HID - L0.b1;
+    std::copy(src + L0.b1, src + L0.b1 + tail, dst + L1.b1);
+}
+
 template <typename F>
 void dispatch_channels(int ns, int na, F&& f) {
     if (ns == 2 && na == 2) f.template operator()<2, 2>();
@@ -208,7 +259,10 @@ struct psdf_ctx {
     double test_margin = 1e-8;  // PSDF_TEST_MARGIN, read once at creation
 
     bool has_grid = false;
-    psdf_grid_desc desc{};
+    psdf_grid_desc desc{};  // device layout: n_s / n_a are the kernel widths
+    // the caller's channel widths (the reference's n_s / n_a, any value in
+    // [1, 8]); desc holds the instantiated pair they are zero-padded to
+    int hns = 0, hna = 0;
     int in_dim = 0;
     int nt[3] = {0, 0, 0};
     int64_t off_raw = 0, off_planes = 0, off_probes = 0, off_mlp = 0, n_params = 0;
@@ -219,6 +273,10 @@ struct psdf_ctx {
     int32_t* d_tile_nbr = nullptr; // [T][27] neighbour tile ids
     int occ_tlo[3] = {0, 0, 0}, occ_thi[3] = {-1, -1, -1};  // allocated tiles' bounding box (tile coords)
     uint8_t* d_sat_dist = nullptr; // [T][17^3] per-cell saturation distances of the current ray pass
+    // d_sat_dist is a pure function of (d_smooth_ap, tau): kept across ray
+    // passes until either changes (every writer of d_smooth_ap clears sat_ok)
+    bool sat_ok = false;
+    double sat_tau = 0.0;
     int composite_steps = kComposite0Steps;
     bool coop_round1 = true;       // K2a round 1 one warp per ray (PSDF_COOP=0: one lane per ray, A/B)
     bool coop_render = true;       // renders too: round 0 capped, the tail one warp per ray (PSDF_COOP_RENDER=0)
@@ -503,6 +561,7 @@ void launch_fold(psdf_ctx* c, const float* src, float* dst) {
 // Refreshes the apron copy (and brick minima) from the current smoothed grid.
 void fill_apron(psdf_ctx* c) {
     if (c->desc.T == 0) return;
+    c->sat_ok = false;
     apron_fill_kernel<<<c->desc.T, 256, 0, c->stream>>>(c->view(), c->d_smooth, c->d_smooth_ap);
     CK(cudaGetLastError());
     ++c->last_launches;
@@ -511,6 +570,7 @@ void fill_apron(psdf_ctx* c) {
 // SparseGrid::smooth_all (grid.cpp:247-250) + apron + brick minima, one pass.
 void smooth_all(psdf_ctx* c) {
     if (c->desc.T == 0) return;
+    c->sat_ok = false;
     if (c->attr_done.insert((const void*)smooth_apron_kernel).second)
         CK(cudaFuncSetAttribute(smooth_apron_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kSmoothApronSmem));
@@ -525,6 +585,9 @@ void smooth_all(psdf_ctx* c) {
 // with runs disabled (tau_run <= 0) every block reads as unsaturated.
 void prepare_sat(psdf_ctx* c, double tau_run) {
     if (c->desc.T == 0) return;
+    if (c->sat_ok && c->sat_tau == tau_run) return;  // same stream: the last pass's table stands
+    c->sat_ok = true;
+    c->sat_tau = tau_run;
     sat_dist_kernel<<<c->desc.T, kSatThreads, 0, c->stream>>>(c->view(), tau_run, c->d_sat_dist);
     CK(cudaGetLastError());
     ++c->last_launches;
@@ -1317,10 +1380,11 @@ static std::vector<uint8_t> tile_distance(const std::vector<int32_t>& tt, const 
     return a;
 }
 
-int psdf_upload_grid(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_coords,
-                     const int32_t* probe_ids, const int32_t* probe_coords, const float* raw,
-                     const float* smooth, const float* planes, const float* probes) {
-    return guarded([&] {
+// The device upload proper: d is in device layout (kernel widths).
+static void upload_grid_dev(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_coords,
+                            const int32_t* probe_ids, const int32_t* probe_coords, const float* raw,
+                            const float* smooth, const float* planes, const float* probes) {
+    {
         if (!c || !d) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
         for (int a = 0; a < 3; ++a)
             if (d->res[a] <= 0 || d->res[a] % TE)
@@ -1328,7 +1392,7 @@ int psdf_upload_grid(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_c
         if (d->sh_order < 1 || d->sh_order > 4)
             fail(PSDF_ERR_INVALID_ARGUMENT, "SH order must be in [1,4]");
         if (!supported_channels(d->n_s, d->n_a))
-            fail(PSDF_ERR_INVALID_ARGUMENT, "unsupported (n_s, n_a) = (%d, %d)", d->n_s, d->n_a);
+            fail(PSDF_ERR_INVALID_ARGUMENT, "unsupported kernel widths (n_s, n_a) = (%d, %d)", d->n_s, d->n_a);
         if (d->T < 0 || d->P < 0 || d->ncam < 0) fail(PSDF_ERR_INVALID_ARGUMENT, "negative count");
         if (d->T > 0 && (!tile_coords || !probe_ids || !raw || !planes))
             fail(PSDF_ERR_INVALID_ARGUMENT, "missing tile arrays");
@@ -1414,6 +1478,7 @@ int psdf_upload_grid(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_c
         CK(cudaMalloc(&c->d_smooth, sizeof(float) * std::max<int64_t>(T * TV, 4)));
         CK(cudaMalloc(&c->d_smooth_ap, sizeof(float) * std::max<int64_t>(T * AV, 4)));
         CK(cudaMalloc(&c->d_sat_dist, std::max<int64_t>((int64_t)kCellN * T, 1)));
+        c->sat_ok = false;
         CK(cudaMalloc(&c->d_gsmooth, sizeof(float) * std::max<int64_t>(T * TV, 4)));
         CK(cudaMemsetAsync(c->d_params, 0, sizeof(float) * (c->n_params + kParamPad), c->stream));
         CK(cudaMemsetAsync(c->d_grads, 0, sizeof(float) * (c->n_params + kParamPad), c->stream));
@@ -1441,35 +1506,106 @@ int psdf_upload_grid(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_c
             smooth_all(c);
         }
         CK(cudaStreamSynchronize(c->stream));
+    }
+}
+
+// SparseGrid upload in the caller's layout (psdf.h); widths without their own
+// kernel instantiation are zero-padded to kernel_widths().
+int psdf_upload_grid(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_coords,
+                     const int32_t* probe_ids, const int32_t* probe_coords, const float* raw,
+                     const float* smooth, const float* planes, const float* probes) {
+    return guarded([&] {
+        if (!c || !d) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
+        int ks = 0, ka = 0;
+        if (!kernel_widths(d->n_s, d->n_a, &ks, &ka))
+            fail(PSDF_ERR_INVALID_ARGUMENT, "unsupported (n_s, n_a) = (%d, %d)", d->n_s, d->n_a);
+        if (ks == d->n_s && ka == d->n_a) {
+            upload_grid_dev(c, d, tile_coords, probe_ids, probe_coords, raw, smooth, planes, probes);
+        } else {
+            if (d->T < 0 || d->P < 0 || d->sh_order < 1 || d->sh_order > 4)
+                fail(PSDF_ERR_INVALID_ARGUMENT, "invalid grid counts or SH order");
+            psdf_grid_desc dk = *d;
+            dk.n_s = ks;
+            dk.n_a = ka;
+            const int64_t nc = (int64_t)d->sh_order * d->sh_order;
+            std::vector<float> pl, pr;
+            if (planes) {
+                pl.resize((size_t)d->T * 3 * 256 * ks);
+                repack_rows(planes, (int64_t)d->T * 3 * 256, d->n_s, pl.data(), ks);
+            }
+            if (probes) {
+                pr.resize((size_t)d->P * nc * ka);
+                repack_rows(probes, (int64_t)d->P * nc, d->n_a, pr.data(), ka);
+            }
+            upload_grid_dev(c, &dk, tile_coords, probe_ids, probe_coords, raw, smooth,
+                            planes ? pl.data() : nullptr, probes ? pr.data() : nullptr);
+        }
+        c->hns = d->n_s;
+        c->hna = d->n_a;
     });
 }
+
+// MLP blob in device layout (kernel widths)
+static void upload_mlp_dev(psdf_ctx* c, const float* mlp, int64_t n) {
+    need_grid(c);
+    if (!mlp || n != c->mlp_size)
+        fail(PSDF_ERR_INVALID_ARGUMENT, "MLP size %lld does not match the grid (%lld)",
+             (long long)n, (long long)c->mlp_size);
+    set_device(c);
+    CK(cudaMemcpyAsync(c->d_params + c->off_mlp, mlp, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+}
+
+static bool padded(const psdf_ctx* c) { return c->hns != c->desc.n_s || c->hna != c->desc.n_a; }
 
 int psdf_upload_mlp(psdf_ctx* c, const float* mlp, int64_t n) {
     return guarded([&] {
         need_grid(c);
-        if (!mlp || n != c->mlp_size)
-            fail(PSDF_ERR_INVALID_ARGUMENT, "MLP size %lld does not match the grid (%lld)",
-                 (long long)n, (long long)c->mlp_size);
-        set_device(c);
-        CK(cudaMemcpyAsync(c->d_params + c->off_mlp, mlp, sizeof(float) * n, cudaMemcpyHostToDevice,
-                           c->stream));
-        CK(cudaStreamSynchronize(c->stream));
+        if (!padded(c)) return upload_mlp_dev(c, mlp, n);
+        const int64_t nh = psdf_mlp_size(c->hns, c->hna, c->desc.ncam);
+        if (!mlp || n != nh)
+            fail(PSDF_ERR_INVALID_ARGUMENT, "MLP size %lld does not match the grid (%lld)", (long long)n,
+                 (long long)nh);
+        std::vector<float> k((size_t)c->mlp_size);
+        repack_mlp(mlp, c->hns, c->hna, k.data(), c->desc.n_s, c->desc.n_a, c->desc.ncam);
+        upload_mlp_dev(c, k.data(), (int64_t)k.size());
     });
+}
+
+// Parameters (or gradients: base / smooth_src) in device layout.
+static void download_params_dev(psdf_ctx* c, const float* base, const float* smooth_src, float* raw, float* smooth,
+                                float* planes, float* probes, float* mlp) {
+    need_grid(c);
+    set_device(c);
+    const int64_t T = c->desc.T;
+    cudaStream_t s = c->stream;
+    if (raw && T) CK(cudaMemcpyAsync(raw, base + c->off_raw, sizeof(float) * T * TV, cudaMemcpyDeviceToHost, s));
+    if (smooth && T) CK(cudaMemcpyAsync(smooth, smooth_src, sizeof(float) * T * TV, cudaMemcpyDeviceToHost, s));
+    if (planes && T) CK(cudaMemcpyAsync(planes, base + c->off_planes, sizeof(float) * c->n_planes, cudaMemcpyDeviceToHost, s));
+    if (probes && c->n_probes) CK(cudaMemcpyAsync(probes, base + c->off_probes, sizeof(float) * c->n_probes, cudaMemcpyDeviceToHost, s));
+    if (mlp) CK(cudaMemcpyAsync(mlp, base + c->off_mlp, sizeof(float) * c->mlp_size, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+}
+
+// The same in the caller's layout: padded channels stripped.
+static void download_params_host(psdf_ctx* c, const float* base, const float* smooth_src, float* raw,
+                                 float* smooth, float* planes, float* probes, float* mlp) {
+    need_grid(c);
+    if (!padded(c)) return download_params_dev(c, base, smooth_src, raw, smooth, planes, probes, mlp);
+    std::vector<float> pl(planes ? c->n_planes : 0), pr(probes ? c->n_probes : 0), ml(mlp ? c->mlp_size : 0);
+    download_params_dev(c, base, smooth_src, raw, smooth, planes ? pl.data() : nullptr,
+                        probes ? pr.data() : nullptr, mlp ? ml.data() : nullptr);
+    const psdf_grid_desc& d = c->desc;
+    if (planes) repack_rows(pl.data(), (int64_t)d.T * 3 * 256, d.n_s, planes, c->hns);
+    if (probes) repack_rows(pr.data(), (int64_t)d.P * d.sh_order * d.sh_order, d.n_a, probes, c->hna);
+    if (mlp) repack_mlp(ml.data(), d.n_s, d.n_a, mlp, c->hns, c->hna, d.ncam);
 }
 
 int psdf_download_params(psdf_ctx* c, float* raw, float* smooth, float* planes, float* probes,
                          float* mlp) {
     return guarded([&] {
         need_grid(c);
-        set_device(c);
-        const int64_t T = c->desc.T;
-        cudaStream_t s = c->stream;
-        if (raw && T) CK(cudaMemcpyAsync(raw, c->d_params + c->off_raw, sizeof(float) * T * TV, cudaMemcpyDeviceToHost, s));
-        if (smooth && T) CK(cudaMemcpyAsync(smooth, c->d_smooth, sizeof(float) * T * TV, cudaMemcpyDeviceToHost, s));
-        if (planes && T) CK(cudaMemcpyAsync(planes, c->d_params + c->off_planes, sizeof(float) * c->n_planes, cudaMemcpyDeviceToHost, s));
-        if (probes && c->n_probes) CK(cudaMemcpyAsync(probes, c->d_params + c->off_probes, sizeof(float) * c->n_probes, cudaMemcpyDeviceToHost, s));
-        if (mlp) CK(cudaMemcpyAsync(mlp, c->d_params + c->off_mlp, sizeof(float) * c->mlp_size, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        download_params_host(c, c->d_params, c->d_smooth, raw, smooth, planes, probes, mlp);
     });
 }
 
@@ -1478,6 +1614,8 @@ int psdf_grid_info(psdf_ctx* c, psdf_grid_desc* out) {
         need_grid(c);
         if (!out) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
         *out = c->desc;
+        out->n_s = c->hns;  // the caller's widths
+        out->n_a = c->hna;
     });
 }
 
@@ -1519,18 +1657,17 @@ int psdf_raise_sh_order(psdf_ctx* c, int new_order) {
             pco(3 * std::max<int64_t>(P, 1));
         std::vector<float> raw((size_t)T * TV), sm((size_t)T * TV), planes(c->n_planes), probes(c->n_probes),
             mlp(c->mlp_size);
-        if (psdf_download_structure(c, tc.data(), pid.data(), pco.data()) != PSDF_OK ||
-            psdf_download_params(c, raw.data(), sm.data(), planes.data(), probes.data(), mlp.data()) != PSDF_OK)
+        if (psdf_download_structure(c, tc.data(), pid.data(), pco.data()) != PSDF_OK)
             fail(PSDF_ERR_RUNTIME, "%s", g_err.c_str());
+        download_params_dev(c, c->d_params, c->d_smooth, raw.data(), sm.data(), planes.data(), probes.data(),
+                            mlp.data());
         const int oc = d.sh_order * d.sh_order * d.n_a, nc = new_order * new_order * d.n_a;
         std::vector<float> np((size_t)P * nc, 0.f);
         for (int64_t p = 0; p < P; ++p)
             std::copy(probes.begin() + p * oc, probes.begin() + (p + 1) * oc, np.begin() + p * nc);
         d.sh_order = new_order;
-        if (psdf_upload_grid(c, &d, tc.data(), pid.data(), pco.data(), raw.data(), sm.data(), planes.data(),
-                             np.data()) != PSDF_OK ||
-            psdf_upload_mlp(c, mlp.data(), (int64_t)mlp.size()) != PSDF_OK)
-            fail(PSDF_ERR_RUNTIME, "%s", g_err.c_str());
+        upload_grid_dev(c, &d, tc.data(), pid.data(), pco.data(), raw.data(), sm.data(), planes.data(), np.data());
+        upload_mlp_dev(c, mlp.data(), (int64_t)mlp.size());
     });
 }
 
@@ -1626,10 +1763,9 @@ int psdf_subdivide(psdf_ctx* c, double band_voxels, int32_t* out_T, int32_t* out
         CK(cudaStreamSynchronize(s));
         scratch.release();
         // 4. the new grid (smoothed on the device, grid.cpp:340)
-        if (psdf_upload_grid(c, &d, tc.data(), pid.data(), pco.data(), raw.data(), nullptr, planes.data(),
-                             probes.data()) != PSDF_OK ||
-            psdf_upload_mlp(c, mlp.data(), (int64_t)mlp.size()) != PSDF_OK)
-            fail(PSDF_ERR_RUNTIME, "%s", g_err.c_str());
+        upload_grid_dev(c, &d, tc.data(), pid.data(), pco.data(), raw.data(), nullptr, planes.data(),
+                        probes.data());
+        upload_mlp_dev(c, mlp.data(), (int64_t)mlp.size());
         if (out_T) *out_T = (int32_t)T1;
         if (out_P) *out_P = (int32_t)P1;
     });
@@ -2076,11 +2212,13 @@ int psdf_save_checkpoint(psdf_ctx* c, const char* path, int32_t lod, int32_t ban
     return guarded([&] {
         need_grid(c);
         if (!path) fail(PSDF_ERR_INVALID_ARGUMENT, "null path");
-        const psdf_grid_desc d = c->desc;
+        psdf_grid_desc d = c->desc;
+        d.n_s = c->hns;  // the file holds the caller's widths
+        d.n_a = c->hna;
         const int64_t T = d.T, P = d.P;
         const int64_t ps = 256 * d.n_s, pc = (int64_t)d.sh_order * d.sh_order * d.n_a;
         std::vector<int32_t> tc(3 * std::max<int64_t>(T, 1)), pco(3 * std::max<int64_t>(P, 1));
-        std::vector<float> raw(T * TV), planes(T * 3 * ps), probes(P * pc), mlp(c->mlp_size);
+        std::vector<float> raw(T * TV), planes(T * 3 * ps), probes(P * pc), mlp(psdf_mlp_size(d.n_s, d.n_a, d.ncam));
         if (psdf_download_structure(c, tc.data(), nullptr, pco.data()) != PSDF_OK ||
             psdf_download_params(c, raw.data(), nullptr, planes.data(), probes.data(), mlp.data()) != PSDF_OK)
             fail(PSDF_ERR_RUNTIME, "%s", g_err.c_str());
@@ -2248,14 +2386,7 @@ int psdf_download_grads(psdf_ctx* c, int stage, float* raw, float* smooth, float
             fail(PSDF_ERR_RUNTIME, "stage-0 gradients not kept (psdf_set_keep_raypass_grads)");
         const float* G = stage == 0 ? c->d_grads0 : c->d_grads;
         const float* S = stage == 0 ? c->d_gsmooth0 : c->d_gsmooth;
-        const int64_t T = c->desc.T;
-        cudaStream_t s = c->stream;
-        if (raw && T) CK(cudaMemcpyAsync(raw, G + c->off_raw, sizeof(float) * T * TV, cudaMemcpyDeviceToHost, s));
-        if (smooth && T) CK(cudaMemcpyAsync(smooth, S, sizeof(float) * T * TV, cudaMemcpyDeviceToHost, s));
-        if (planes && T) CK(cudaMemcpyAsync(planes, G + c->off_planes, sizeof(float) * c->n_planes, cudaMemcpyDeviceToHost, s));
-        if (probes && c->n_probes) CK(cudaMemcpyAsync(probes, G + c->off_probes, sizeof(float) * c->n_probes, cudaMemcpyDeviceToHost, s));
-        if (mlp) CK(cudaMemcpyAsync(mlp, G + c->off_mlp, sizeof(float) * c->mlp_size, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        download_params_host(c, G, S, raw, smooth, planes, probes, mlp);
     });
 }
 

@@ -10,15 +10,18 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _ref_scene():
+def _ref_scene(n_s=4, n_a=4):
     from oracle.refcore import RefScene
-    s = RefScene.sphere(res=32, n_s=4, n_a=4, sh_order=3, band_voxels=4, radius=0.3, ncam=3, mlp_seed=7)
+    s = RefScene.sphere(res=32, n_s=n_s, n_a=n_a, sh_order=3, band_voxels=4, radius=0.3, ncam=3, mlp_seed=7)
     s.randomize(11, sdf_jitter=0.003, plane_amp=0.2, probe_amp=0.3, bias_amp=0.1)
     return s
 
 
-def test_checkpoint_roundtrip_bytes(ctx, tmp_path):
-    s = _ref_scene()
+@pytest.mark.parametrize("ns,na", [(4, 4), (3, 5)])
+def test_checkpoint_roundtrip_bytes(ctx, tmp_path, ns, na):
+    """(3, 5) has no kernel instantiation: the device holds it zero-padded to
+    (4, 8) and the file keeps the reference's widths byte for byte."""
+    s = _ref_scene(ns, na)
     f_ref, f_gpu = tmp_path / "ref.sdfc", tmp_path / "gpu.sdfc"
     s.save_checkpoint(f_ref, lod_cursor=2, iteration=17, seed=12345678901)
     g, meta = ctx.load_checkpoint(f_ref)

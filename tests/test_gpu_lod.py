@@ -38,6 +38,8 @@ def _close_f32(got, want, what):
 CASES = [
     dict(res=32, n_s=4, n_a=4, sh_order=3, band=4, radius=0.3, jitter=0.004),
     dict(res=64, n_s=2, n_a=2, sh_order=2, band=6, radius=0.27, jitter=0.002),
+    # widths without their own kernels (zero-padded to (4, 8) on the device)
+    dict(res=32, n_s=3, n_a=5, sh_order=3, band=4, radius=0.3, jitter=0.004),
 ]
 
 
@@ -99,10 +101,11 @@ def test_subdivide_then_train_step(ctx):
     assert abs(losses["photo"] - ol[0]) <= 1e-4 * abs(ol[0])
 
 
-def test_raise_sh_order(ctx):
+@pytest.mark.parametrize("ns,na", [(4, 4), (3, 5)])
+def test_raise_sh_order(ctx, ns, na):
     from paper_2412_10084_b200 import _lib
-    case = dict(res=32, n_s=4, n_a=4, sh_order=2, band=4, radius=0.3)
-    g, a = make_scene(res=32, n_s=4, n_a=4, sh_order=2, band=4, ncam=0)
+    case = dict(res=32, n_s=ns, n_a=na, sh_order=2, band=4, radius=0.3)
+    g, a = make_scene(res=32, n_s=ns, n_a=na, sh_order=2, band=4, ncam=0)
     s = _ref_scene(a, case)
     ctx.upload(g, smooth=False)
     ng = ctx.raise_sh_order(4)

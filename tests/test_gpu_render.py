@@ -113,6 +113,7 @@ SCENES = [
     dict(res=64, n_s=4, n_a=4, sh_order=4, band=6),
     dict(res=32, n_s=8, n_a=8, sh_order=3, band=32),
     dict(res=256, n_s=4, n_a=4, sh_order=4, band=3),  # empty-space jumps
+    dict(res=32, n_s=3, n_a=5, sh_order=3, band=32),  # no own kernels: zero-padded to (4, 8)
 ]
 
 

@@ -189,13 +189,41 @@ def test_train_step_through_nccl_single_rank(ctx, monkeypatch, exchange):
         np.testing.assert_allclose(p1[k], p0[k], rtol=1e-5, atol=1e-6)
 
 
-def test_unsupported_channel_widths_fail_loudly(ctx):
-    """psdf.h psdf_grid_desc: channel widths outside the instantiated set are
-    an invalid argument before any work (the reference's DecoderMlp takes any
-    width, decoder.hpp:17-31 — documented limitation)."""
+@pytest.mark.parametrize("ns,na,ncam", [(3, 5, 4), (1, 1, 0), (6, 3, 0)])
+def test_train_step_parity_padded_widths(ctx, ns, na, ncam):
+    """Any (n_s, n_a) in [1, 8]^2 (the reference's DecoderMlp takes any
+    width, decoder.hpp:17-31): pairs without their own kernels run on the
+    smallest instantiated pair that holds them, zero-padded (psdf.cu
+    kernel_widths); two steps match the oracle at the caller's widths."""
+    _train_parity(ctx, dict(scene=dict(res=64, n_s=ns, n_a=na, sh_order=3, band=6), tau=300.0, size=32,
+                            ncam=ncam, bias=ncam > 0))
+    d = ctx.info()
+    assert (d.n_s, d.n_a) == (ns, na)
+
+
+def test_padded_widths_roundtrip(ctx):
+    """Upload -> download is the identity at the caller's widths (planes,
+    probes, MLP incl. camera rows), and gradients come back at those widths."""
     from paper_2412_10084_b200 import api
+    g, _ = make_scene(res=32, n_s=3, n_a=5, sh_order=3, band=6, ncam=2)
+    ctx.upload(g, smooth=False)
+    p = ctx.download()
+    for k in ("raw", "planes", "probes", "mlp"):
+        np.testing.assert_array_equal(p[k], np.asarray(getattr(g, k), np.float32).reshape(p[k].shape), k)
+    ctx.keep_raypass_grads(True)
+    ctx.train_reset()
+    cams = api.make_ring_cameras(1, 16)
+    ctx.train_step(cams, [np.full((16, 16, 3), 0.5, np.float32)], [np.ones((16, 16))],
+                   api.step_params(tau=300.0 * 32, lr_vox=1e-4, lr_mlp=6e-5, photo_scale=20.0))
+    gr = ctx.grads(1)
+    assert gr["planes"].size == p["planes"].size and gr["mlp"].size == p["mlp"].size
+
+
+def test_unsupported_channel_widths_fail_loudly(ctx):
+    """psdf.h psdf_grid_desc: widths above the largest instantiated pair (8, 8)
+    are an invalid argument before any work."""
     from paper_2412_10084_b200._lib import PsdfInvalidArgument
     g, _ = make_scene(res=32, n_s=2, n_a=2, sh_order=2, band=6, ncam=0)
-    g.cfg.n_s, g.cfg.n_a = 3, 5
-    with pytest.raises(PsdfInvalidArgument, match=r"unsupported \(n_s, n_a\) = \(3, 5\)"):
+    g.cfg.n_s, g.cfg.n_a = 16, 4
+    with pytest.raises(PsdfInvalidArgument, match=r"unsupported \(n_s, n_a\) = \(16, 4\)"):
         ctx.upload(g, smooth=False)
