@@ -1380,10 +1380,19 @@ static std::vector<uint8_t> tile_distance(const std::vector<int32_t>& tt, const 
     return a;
 }
 
-// The device upload proper: d is in device layout (kernel widths).
+// Fresh-tile defaults generated on the device instead of uploaded: planes =
+// value in the first hs channels (zero in padded ones), probes = 0.
+struct FreshFill {
+    float plane_value;
+    int plane_hs;
+};
+
+// The device upload proper: d is in device layout (kernel widths); raw may
+// be a device pointer (copies are cudaMemcpyDefault).
 static void upload_grid_dev(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_coords,
                             const int32_t* probe_ids, const int32_t* probe_coords, const float* raw,
-                            const float* smooth, const float* planes, const float* probes) {
+                            const float* smooth, const float* planes, const float* probes,
+                            const FreshFill* fresh = nullptr) {
     {
         if (!c || !d) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
         for (int a = 0; a < 3; ++a)
@@ -1394,9 +1403,10 @@ static void upload_grid_dev(psdf_ctx* c, const psdf_grid_desc* d, const int32_t*
         if (!supported_channels(d->n_s, d->n_a))
             fail(PSDF_ERR_INVALID_ARGUMENT, "unsupported kernel widths (n_s, n_a) = (%d, %d)", d->n_s, d->n_a);
         if (d->T < 0 || d->P < 0 || d->ncam < 0) fail(PSDF_ERR_INVALID_ARGUMENT, "negative count");
-        if (d->T > 0 && (!tile_coords || !probe_ids || !raw || !planes))
+        if (d->T > 0 && (!tile_coords || !probe_ids || !raw || (!planes && !fresh)))
             fail(PSDF_ERR_INVALID_ARGUMENT, "missing tile arrays");
-        if (d->P > 0 && (!probe_coords || !probes)) fail(PSDF_ERR_INVALID_ARGUMENT, "missing probe arrays");
+        if (d->P > 0 && (!probe_coords || (!probes && !fresh)))
+            fail(PSDF_ERR_INVALID_ARGUMENT, "missing probe arrays");
         set_device(c);
         CK(cudaStreamSynchronize(c->stream));
         c->free_grid();
@@ -1490,11 +1500,18 @@ static void upload_grid_dev(psdf_ctx* c, const psdf_grid_desc* d, const int32_t*
         CK(cudaMemcpyAsync(c->d_probe_coords, pc4.data(), sizeof(int4) * pc4.size(), cudaMemcpyHostToDevice, c->stream));
         if (T > 0) {
             CK(cudaMemcpyAsync(c->d_probe_ids, probe_ids, sizeof(int32_t) * 8 * T, cudaMemcpyHostToDevice, c->stream));
-            CK(cudaMemcpyAsync(c->d_params + c->off_raw, raw, sizeof(float) * T * TV, cudaMemcpyHostToDevice, c->stream));
-            CK(cudaMemcpyAsync(c->d_params + c->off_planes, planes, sizeof(float) * c->n_planes,
-                               cudaMemcpyHostToDevice, c->stream));
+            CK(cudaMemcpyAsync(c->d_params + c->off_raw, raw, sizeof(float) * T * TV, cudaMemcpyDefault, c->stream));
+            if (planes) {
+                CK(cudaMemcpyAsync(c->d_params + c->off_planes, planes, sizeof(float) * c->n_planes,
+                                   cudaMemcpyHostToDevice, c->stream));
+            } else {
+                const unsigned nb = (unsigned)std::min<int64_t>((c->n_planes + 255) / 256, 8 * c->sm_count);
+                plane_fill_kernel<<<nb, 256, 0, c->stream>>>(c->d_params + c->off_planes, c->n_planes, d->n_s,
+                                                             fresh->plane_hs, fresh->plane_value);
+                CK(cudaGetLastError());
+            }
         }
-        if (P > 0)
+        if (P > 0 && probes)  // fresh probes: the zeroed buffer
             CK(cudaMemcpyAsync(c->d_params + c->off_probes, probes, sizeof(float) * c->n_probes,
                                cudaMemcpyHostToDevice, c->stream));
         c->has_grid = true;
@@ -1782,6 +1799,9 @@ int psdf_init_visual_hull(psdf_ctx* c, const psdf_grid_desc* cfg, int band_voxel
     return guarded([&] {
         if (!c || !cfg) fail(PSDF_ERR_INVALID_ARGUMENT, "null argument");
         if (n_cams <= 0 || !cams || !masks) fail(PSDF_ERR_INVALID_ARGUMENT, "visual hull: need one mask per camera");
+        int ks0 = 0, ka0 = 0;
+        if (!kernel_widths(cfg->n_s, cfg->n_a, &ks0, &ka0))
+            fail(PSDF_ERR_INVALID_ARGUMENT, "unsupported (n_s, n_a) = (%d, %d)", cfg->n_s, cfg->n_a);
         for (int a = 0; a < 3; ++a)
             if (cfg->res[a] <= 0 || cfg->res[a] % TE)
                 fail(PSDF_ERR_INVALID_ARGUMENT, "grid resolution must be a multiple of 16");
@@ -1794,14 +1814,29 @@ int psdf_init_visual_hull(psdf_ctx* c, const psdf_grid_desc* cfg, int band_voxel
         const int3 res = make_int3(cfg->res[0], cfg->res[1], cfg->res[2]);
         const int64_t nv = (int64_t)res.x * res.y * res.z;
         const double h = cfg->voxel_size;
-        std::vector<void*> tmp;
+        // one call-scoped arena for every temporary (sizes known up front)
+        const int maxn = std::max({res.x, res.y, res.z});
+        const int64_t n_lines_max = std::max({(int64_t)res.x * res.y, (int64_t)res.x * res.z, (int64_t)res.y * res.z});
+        const int batch = (int)std::min<int64_t>(n_lines_max, 131072);
+        const int nt[3] = {res.x / TE, res.y / TE, res.z / TE};
+        const int64_t ntt = (int64_t)nt[0] * nt[1] * nt[2];
+        size_t mask_bytes = 0;
+        for (int i = 0; i < n_cams; ++i) mask_bytes += ((size_t)cams[i].width * cams[i].height + 255) & ~(size_t)255;
+        auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+        const size_t arena_bytes = mask_bytes + al(sizeof(Cam) * n_cams) + al(sizeof(uint8_t*) * n_cams) + al(nv) +
+                                   al(sizeof(double) * (size_t)batch * maxn) + al(sizeof(int) * (size_t)batch * maxn) +
+                                   al(sizeof(double) * (size_t)batch * (maxn + 1)) + 2 * al(sizeof(double) * nv) +
+                                   al(sizeof(float) * TV * ntt) + al(ntt) + al(sizeof(int) * ntt);
+        DevScratch scratch;
+        uint8_t* arena = scratch.alloc<uint8_t>(arena_bytes);
+        size_t used = 0;
         auto dalloc = [&](size_t bytes) {
-            void* p = nullptr;
-            CK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
-            tmp.push_back(p);
+            void* p = arena + used;
+            used += al(bytes);
+            if (used > arena_bytes) fail(PSDF_ERR_RUNTIME, "visual hull: scratch arena overflow");
             return p;
         };
-        try {
+        {
             // cameras and masks
             std::vector<Cam> hc(n_cams);
             std::vector<const uint8_t*> hm(n_cams);
@@ -1823,8 +1858,6 @@ int psdf_init_visual_hull(psdf_ctx* c, const psdf_grid_desc* cfg, int band_voxel
                                                make_double3(cfg->origin[0], cfg->origin[1], cfg->origin[2]), h, occ);
             CK(cudaGetLastError());
             // squared EDTs to the occupied and to the free set (edt3d, grid.cpp:430-468)
-            const int maxn = std::max({res.x, res.y, res.z});
-            const int batch = 65536;
             auto* fbuf = (double*)dalloc(sizeof(double) * (size_t)batch * maxn);
             auto* vbuf = (int*)dalloc(sizeof(int) * (size_t)batch * maxn);
             auto* zbuf = (double*)dalloc(sizeof(double) * (size_t)batch * (maxn + 1));
@@ -1845,8 +1878,6 @@ int psdf_init_visual_hull(psdf_ctx* c, const psdf_grid_desc* cfg, int band_voxel
                     }
             }
             // seed SDF + allocation decision per tile (init_common, grid.cpp:358-397)
-            const int nt[3] = {res.x / TE, res.y / TE, res.z / TE};
-            const int64_t ntt = (int64_t)nt[0] * nt[1] * nt[2];
             auto* raw_all = (float*)dalloc(sizeof(float) * TV * ntt);
             auto* keep_d = (uint8_t*)dalloc(ntt);
             const double max_s = (double)maxn * h;
@@ -1880,33 +1911,33 @@ int psdf_init_visual_hull(psdf_ctx* c, const psdf_grid_desc* cfg, int band_voxel
                 }
             }
             const int64_t T = (int64_t)src.size(), P = (int64_t)(pco.size() / 3);
-            std::vector<float> raw((size_t)T * TV);
+            // the kept tiles' raw values, gathered on the device into the
+            // (finished) occupied-set EDT buffer and uploaded from there
+            float* d_raw = reinterpret_cast<float*>(dist[0]);
             if (T) {
                 auto* d_src = (int*)dalloc(sizeof(int) * T);
-                auto* d_raw = (float*)dalloc(sizeof(float) * TV * T);
                 CK(cudaMemcpyAsync(d_src, src.data(), sizeof(int) * T, cudaMemcpyHostToDevice, s));
                 subdiv_gather_raw_kernel<<<(unsigned)T, 256, 0, s>>>(raw_all, d_src, (int)T, d_raw);
                 CK(cudaGetLastError());
-                CK(cudaMemcpyAsync(raw.data(), d_raw, sizeof(float) * raw.size(), cudaMemcpyDeviceToHost, s));
             }
-            CK(cudaStreamSynchronize(s));
-            for (void* p : tmp) cudaFree(p);
-            tmp.clear();
             psdf_grid_desc d = *cfg;
             d.T = (int)T;
             d.P = (int)P;
-            std::vector<float> planes((size_t)T * 3 * 256 * d.n_s, 0.5f);  // allocate_tile (grid.cpp:66-69)
-            std::vector<float> probes((size_t)P * d.sh_order * d.sh_order * d.n_a, 0.f);  // ensure_probe
-            std::vector<float> mlp(psdf_mlp_size(d.n_s, d.n_a, d.ncam), 0.f);
-            if (psdf_upload_grid(c, &d, tc.data(), pid.data(), pco.data(), raw.data(), nullptr, planes.data(),
-                                 probes.data()) != PSDF_OK ||
-                psdf_upload_mlp(c, mlp.data(), (int64_t)mlp.size()) != PSDF_OK)
-                fail(PSDF_ERR_RUNTIME, "%s", g_err.c_str());
+            int ks = 0, ka = 0;
+            if (!kernel_widths(d.n_s, d.n_a, &ks, &ka))
+                fail(PSDF_ERR_INVALID_ARGUMENT, "unsupported (n_s, n_a) = (%d, %d)", d.n_s, d.n_a);
+            psdf_grid_desc dk = d;
+            dk.n_s = ks;
+            dk.n_a = ka;
+            // planes 0.5 (allocate_tile, grid.cpp:66-69), probes 0
+            // (ensure_probe), MLP 0 until psdf_upload_mlp: generated on the
+            // device; the raw copy is device to device
+            const FreshFill fresh{0.5f, d.n_s};
+            upload_grid_dev(c, &dk, tc.data(), pid.data(), pco.data(), d_raw, nullptr, nullptr, nullptr, &fresh);
+            c->hns = d.n_s;
+            c->hna = d.n_a;
             if (out_T) *out_T = (int32_t)T;
             if (out_P) *out_P = (int32_t)P;
-        } catch (...) {
-            for (void* p : tmp) cudaFree(p);
-            throw;
         }
     });
 }

@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(256) hull_occ_kernel(const Cam* __restrict__ c
 
 // One pass of edt3d (grid.cpp:430-468): dt1d along every line of `n` elements
 // at `stride` (line l starts at base(l)); one thread per line, the lower
-// envelope in per-line global scratch.
+// envelope in global scratch interleaved across the batch's lines.
 struct EdtLines {
     int n_lines, n, stride;
     int64_t step_a, step_b;  // line l = (la, lb): base = la * step_a + lb * step_b
@@ -220,35 +220,47 @@ __global__ void __launch_bounds__(128) edt_pass_kernel(double* __restrict__ d, E
     const int l = line0 + t;
     double* line = d + (int64_t)(l / L.n_b) * L.step_a + (int64_t)(l % L.n_b) * L.step_b;
     const int n = L.n;
-    double* f = fbuf + (int64_t)t * n;
-    int* v = vbuf + (int64_t)t * n;
-    double* z = zbuf + (int64_t)t * (n + 1);
-    for (int q = 0; q < n; ++q) f[q] = line[(int64_t)q * L.stride];
+    // scratch interleaved across the batch (element q of every line's copy
+    // adjacent): the lock-step f[q] loads / stores of a warp coalesce
+    const int64_t nb = n_batch;
+    double* f = fbuf + t;
+    int* v = vbuf + t;
+    double* z = zbuf + t;
+    for (int q = 0; q < n; ++q) f[q * nb] = line[(int64_t)q * L.stride];
     // Felzenszwalb 1D squared distance transform (grid.cpp:400-427)
     int k = 0;
     v[0] = 0;
     z[0] = -INFINITY;
-    z[1] = INFINITY;
+    z[nb] = INFINITY;
     for (int q = 1; q < n; ++q) {
         double s;
+        const double fq = dadd(f[q * nb], (double)(q * q));
         for (;;) {
-            const int vk = v[k];
-            s = ddiv(dsub(dadd(f[q], (double)(q * q)), dadd(f[vk], (double)(vk * vk))),
-                     dsub(dmul(2.0, (double)q), dmul(2.0, (double)vk)));
-            if (s <= z[k]) --k;
+            const int vk = v[k * nb];
+            s = ddiv(dsub(fq, dadd(f[vk * nb], (double)(vk * vk))), dsub(dmul(2.0, (double)q), dmul(2.0, (double)vk)));
+            if (s <= z[k * nb]) --k;
             else break;
         }
         ++k;
-        v[k] = q;
-        z[k] = s;
-        z[k + 1] = INFINITY;
+        v[k * nb] = q;
+        z[k * nb] = s;
+        z[(k + 1) * nb] = INFINITY;
     }
     k = 0;
     for (int q = 0; q < n; ++q) {
-        while (z[k + 1] < (double)q) ++k;
-        const int dq = q - v[k];
-        line[(int64_t)q * L.stride] = dadd(dmul((double)dq, (double)dq), f[v[k]]);
+        while (z[(k + 1) * nb] < (double)q) ++k;
+        const int vk = v[k * nb];
+        const int dq = q - vk;
+        line[(int64_t)q * L.stride] = dadd(dmul((double)dq, (double)dq), f[vk * nb]);
     }
+}
+
+// planes of freshly allocated tiles (allocate_tile, grid.cpp:66-69): `value`
+// in the first `hs` of every `ks` channels, zero in padded ones
+__global__ void __launch_bounds__(256) plane_fill_kernel(float* __restrict__ p, int64_t n, int ks, int hs,
+                                                         float value) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = (int)(i % ks) < hs ? value : 0.f;
 }
 
 __global__ void __launch_bounds__(256) edt_init_kernel(const uint8_t* __restrict__ occ, int64_t n, int want,

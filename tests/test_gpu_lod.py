@@ -134,10 +134,12 @@ def _sphere_masks(cams, radius):
     return out
 
 
-@pytest.mark.parametrize("res,band", [(32, 4), (64, 6)])
-def test_visual_hull_parity(ctx, res, band):
+@pytest.mark.parametrize("res,band,ns,na", [(32, 4, 2, 2), (64, 6, 2, 2), (48, 4, 3, 5)])
+def test_visual_hull_parity(ctx, res, band, ns, na):
     """init_grid_visual_hull on the device vs the reference's own (occupancy,
-    EDTs, seed SDF, allocation and order bit-exact; raw stored as fp32)."""
+    EDTs, seed SDF, allocation and order bit-exact; raw stored as fp32;
+    planes 0.5 / probes 0 / MLP 0 at the caller's widths, also for a pair
+    the device zero-pads)."""
     from paper_2412_10084_b200 import api
     from oracle.refcore import RefCamera, RefScene
     cams = api.make_ring_cameras(8, 48)
@@ -150,10 +152,10 @@ def test_visual_hull_parity(ctx, res, band):
         rc.rot[:] = list(c.rot)
         rc.pos[:] = list(c.pos)
         rcams.append(rc)
-    cfg = api.GridConfig(voxel_size=1.0 / res, resolution=(res, res, res), n_s=2, n_a=2, sh_order=2,
+    cfg = api.GridConfig(voxel_size=1.0 / res, resolution=(res, res, res), n_s=ns, n_a=na, sh_order=2,
                          band_voxels=band)
     ng = ctx.init_visual_hull(cfg, cams, masks)
-    b = RefScene.hull(rcams, masks, res=res, n_s=2, n_a=2, sh_order=2, band_voxels=band).export()
+    b = RefScene.hull(rcams, masks, res=res, n_s=ns, n_a=na, sh_order=2, band_voxels=band).export()
     assert ng.T == b.T and ng.P == b.P and ng.T > 0, (ng.T, b.T, ng.P, b.P)
     assert np.array_equal(ng.tile_coords, b.tile_coords)
     assert np.array_equal(ng.probe_ids, b.probe_ids)
@@ -162,6 +164,7 @@ def test_visual_hull_parity(ctx, res, band):
     _close_f32(ng.planes, b.planes, "planes")
     _close_f32(ng.probes, b.probes, "probes")
     assert np.abs(ng.smooth - b.smooth).max() <= 1e-5
+    assert not np.any(ng.mlp)
 
 
 def test_visual_hull_errors(ctx):
