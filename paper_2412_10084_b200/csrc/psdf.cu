@@ -1387,8 +1387,8 @@ struct FreshFill {
     int plane_hs;
 };
 
-// The device upload proper: d is in device layout (kernel widths); raw may
-// be a device pointer (copies are cudaMemcpyDefault).
+// The device upload proper: d is in device layout (kernel widths); raw, smooth,
+// planes and probes may be device pointers (copies are cudaMemcpyDefault).
 static void upload_grid_dev(psdf_ctx* c, const psdf_grid_desc* d, const int32_t* tile_coords,
                             const int32_t* probe_ids, const int32_t* probe_coords, const float* raw,
                             const float* smooth, const float* planes, const float* probes,
@@ -1503,7 +1503,7 @@ static void upload_grid_dev(psdf_ctx* c, const psdf_grid_desc* d, const int32_t*
             CK(cudaMemcpyAsync(c->d_params + c->off_raw, raw, sizeof(float) * T * TV, cudaMemcpyDefault, c->stream));
             if (planes) {
                 CK(cudaMemcpyAsync(c->d_params + c->off_planes, planes, sizeof(float) * c->n_planes,
-                                   cudaMemcpyHostToDevice, c->stream));
+                                   cudaMemcpyDefault, c->stream));
             } else {
                 const unsigned nb = (unsigned)std::min<int64_t>((c->n_planes + 255) / 256, 8 * c->sm_count);
                 plane_fill_kernel<<<nb, 256, 0, c->stream>>>(c->d_params + c->off_planes, c->n_planes, d->n_s,
@@ -1513,11 +1513,11 @@ static void upload_grid_dev(psdf_ctx* c, const psdf_grid_desc* d, const int32_t*
         }
         if (P > 0 && probes)  // fresh probes: the zeroed buffer
             CK(cudaMemcpyAsync(c->d_params + c->off_probes, probes, sizeof(float) * c->n_probes,
-                               cudaMemcpyHostToDevice, c->stream));
+                               cudaMemcpyDefault, c->stream));
         c->has_grid = true;
         c->adam_t = 0;
         if (smooth && T > 0) {
-            CK(cudaMemcpyAsync(c->d_smooth, smooth, sizeof(float) * T * TV, cudaMemcpyHostToDevice, c->stream));
+            CK(cudaMemcpyAsync(c->d_smooth, smooth, sizeof(float) * T * TV, cudaMemcpyDefault, c->stream));
             fill_apron(c);
         } else {
             smooth_all(c);
@@ -1569,7 +1569,7 @@ static void upload_mlp_dev(psdf_ctx* c, const float* mlp, int64_t n) {
         fail(PSDF_ERR_INVALID_ARGUMENT, "MLP size %lld does not match the grid (%lld)",
              (long long)n, (long long)c->mlp_size);
     set_device(c);
-    CK(cudaMemcpyAsync(c->d_params + c->off_mlp, mlp, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_params + c->off_mlp, mlp, sizeof(float) * n, cudaMemcpyDefault, c->stream));
     CK(cudaStreamSynchronize(c->stream));
 }
 
@@ -1668,23 +1668,40 @@ int psdf_raise_sh_order(psdf_ctx* c, int new_order) {
             fail(PSDF_ERR_INVALID_ARGUMENT, "raise_sh_order: order must not decrease and must be <= 4");
         if (new_order == c->desc.sh_order) return;
         set_device(c);
+        cudaStream_t s = c->stream;
         psdf_grid_desc d = c->desc;
         const int64_t T = d.T, P = d.P;
         std::vector<int32_t> tc(3 * std::max<int64_t>(T, 1)), pid(8 * std::max<int64_t>(T, 1)),
             pco(3 * std::max<int64_t>(P, 1));
-        std::vector<float> raw((size_t)T * TV), sm((size_t)T * TV), planes(c->n_planes), probes(c->n_probes),
-            mlp(c->mlp_size);
         if (psdf_download_structure(c, tc.data(), pid.data(), pco.data()) != PSDF_OK)
             fail(PSDF_ERR_RUNTIME, "%s", g_err.c_str());
-        download_params_dev(c, c->d_params, c->d_smooth, raw.data(), sm.data(), planes.data(), probes.data(),
-                            mlp.data());
+        // raw / smoothed SDF, planes and MLP are unchanged: device copies;
+        // the (small) probe pool is re-laid out band-major on the host
+        DevScratch scratch;
+        float* d_raw = scratch.alloc<float>((size_t)T * TV);
+        float* d_sm = scratch.alloc<float>((size_t)T * TV);
+        float* d_planes = scratch.alloc<float>((size_t)c->n_planes);
+        float* d_mlp = scratch.alloc<float>((size_t)c->mlp_size);
+        const int64_t n_mlp = c->mlp_size;
+        if (T) {
+            CK(cudaMemcpyAsync(d_raw, c->d_params + c->off_raw, sizeof(float) * T * TV, cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(d_sm, c->d_smooth, sizeof(float) * T * TV, cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(d_planes, c->d_params + c->off_planes, sizeof(float) * c->n_planes,
+                               cudaMemcpyDeviceToDevice, s));
+        }
+        CK(cudaMemcpyAsync(d_mlp, c->d_params + c->off_mlp, sizeof(float) * n_mlp, cudaMemcpyDeviceToDevice, s));
+        std::vector<float> probes(c->n_probes);
+        if (c->n_probes)
+            CK(cudaMemcpyAsync(probes.data(), c->d_params + c->off_probes, sizeof(float) * c->n_probes,
+                               cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
         const int oc = d.sh_order * d.sh_order * d.n_a, nc = new_order * new_order * d.n_a;
         std::vector<float> np((size_t)P * nc, 0.f);
         for (int64_t p = 0; p < P; ++p)
             std::copy(probes.begin() + p * oc, probes.begin() + (p + 1) * oc, np.begin() + p * nc);
         d.sh_order = new_order;
-        upload_grid_dev(c, &d, tc.data(), pid.data(), pco.data(), raw.data(), sm.data(), planes.data(), np.data());
-        upload_mlp_dev(c, mlp.data(), (int64_t)mlp.size());
+        upload_grid_dev(c, &d, tc.data(), pid.data(), pco.data(), d_raw, T ? d_sm : nullptr, d_planes, np.data());
+        upload_mlp_dev(c, d_mlp, n_mlp);
     });
 }
 
@@ -1771,18 +1788,14 @@ int psdf_subdivide(psdf_ctx* c, double band_voxels, int32_t* out_T, int32_t* out
                                                               stride, d_pc, (int)P1, d_probes);
             CK(cudaGetLastError());
         }
-        std::vector<float> raw((size_t)T1 * TV), planes((size_t)T1 * 3 * 256 * d0.n_s), probes((size_t)P1 * stride),
-            mlp(c->mlp_size);
-        if (T1) CK(cudaMemcpyAsync(raw.data(), d_raw, sizeof(float) * raw.size(), cudaMemcpyDeviceToHost, s));
-        if (T1) CK(cudaMemcpyAsync(planes.data(), d_planes, sizeof(float) * planes.size(), cudaMemcpyDeviceToHost, s));
-        if (P1) CK(cudaMemcpyAsync(probes.data(), d_probes, sizeof(float) * probes.size(), cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(mlp.data(), c->d_params + c->off_mlp, sizeof(float) * mlp.size(), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        const int64_t n_mlp = c->mlp_size;
+        float* d_mlp = scratch.alloc<float>((size_t)n_mlp);
+        CK(cudaMemcpyAsync(d_mlp, c->d_params + c->off_mlp, sizeof(float) * n_mlp, cudaMemcpyDeviceToDevice, s));
+        // 4. the new grid (smoothed on the device, grid.cpp:340), uploaded
+        // device to device from the resampled buffers
+        upload_grid_dev(c, &d, tc.data(), pid.data(), pco.data(), d_raw, nullptr, d_planes, d_probes);
+        upload_mlp_dev(c, d_mlp, n_mlp);
         scratch.release();
-        // 4. the new grid (smoothed on the device, grid.cpp:340)
-        upload_grid_dev(c, &d, tc.data(), pid.data(), pco.data(), raw.data(), nullptr, planes.data(),
-                        probes.data());
-        upload_mlp_dev(c, mlp.data(), (int64_t)mlp.size());
         if (out_T) *out_T = (int32_t)T1;
         if (out_P) *out_P = (int32_t)P1;
     });
