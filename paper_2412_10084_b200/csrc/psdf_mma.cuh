@@ -36,12 +36,21 @@ struct Split4 {
 struct Split2 {
     uint32_t hi[2], lo[2];
 };
+// hi = v with the 13 mantissa bits of a TF32 operand cleared (an exact
+// prefix of v, one LOP), lo = v - hi (exact in fp32) rounded to TF32 by an
+// integer add + mask (round half away from zero on the magnitude, as
+// cvt.rna): |v - hi - lo| <= 2^-22 |v|.  Measured on the bench step
+// (profiles/r02/v42-v45): cvt.rna for both halves 0.705 ms for shade_bwd +
+// shade_geo, this split 0.636 ms, same accuracy (ray-pass plane gradients
+// 6e-7 relative to the f64 oracle); passing lo unrounded is NOT equivalent —
+// the tensor core does not simply ignore the low 13 bits (plane gradients
+// drifted to 2e-4).
 template <int N, class S>
 __device__ __forceinline__ void split(const float* v, S& s) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-        s.hi[i] = tf32(v[i]);
-        s.lo[i] = tf32(v[i] - __uint_as_float(s.hi[i]));
+        s.hi[i] = __float_as_uint(v[i]) & 0xffffe000u;
+        s.lo[i] = (__float_as_uint(v[i] - __uint_as_float(s.hi[i])) + 0x1000u) & 0xffffe000u;
     }
 }
 

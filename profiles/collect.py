@@ -14,7 +14,7 @@ import csv
 import json
 import sys
 
-K2 = ("march_scan", "march_fwd", "march_coop", "rec_tile", "DeviceScan", "shade_fwd", "alpha_bwd", "shade_bwd",
+K2 = ("tile_raster", "march_scan", "march_fwd", "march_coop", "rec_tile", "DeviceScan", "shade_fwd", "alpha_bwd", "shade_bwd",
       "shade_geo")
 COLS = {
     "time_us": ("gpu__time_duration.sum", 1e-3),
