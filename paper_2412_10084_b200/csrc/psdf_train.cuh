@@ -1519,7 +1519,7 @@ struct MmaDims {
 
 template <int NS, int NA>
 #ifndef PSDF_BWD_MINB
-#define PSDF_BWD_MINB 1  // measured: 224 registers / 2 blocks per SM beat a 170-register cap (297 vs 318 us)
+#define PSDF_BWD_MINB 1  // measured: 224 registers / 2 blocks per SM beat a 170-register cap (297 vs 318 us); after the conversion-free split all caps are within noise (profiles/r02/v50_bwd_regcap_ab.txt)
 #endif
 __global__ void __launch_bounds__(BLOCK, PSDF_BWD_MINB) shade_bwd_kernel(RayPassParams P, WaveBufs W) {
     const int n_rec = n_sorted(W);
