@@ -24,6 +24,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -338,6 +339,17 @@ struct psdf_ctx {
     int64_t last_entries = 0, last_records = 0;
     int64_t last_wave[5] = {0, 0, 0, 0, 0};  // entries, records, handovers, continuations, alpha samples
     int64_t last_h2d_bytes = 0;    // host -> device bytes of the last psdf_train_step
+    // psdf_train_step: enqueues the colour copies (and records ev_rgb); run
+    // once, by the ray pass right after the scan launch (the host scans the
+    // masks while the GPU marches) and in any case before the first wait on
+    // ev_rgb (run_rgb_copy)
+    std::function<void()> rgb_copy;
+    // per view [first, last] pixel row holding a mask pixel (mask_rows_kernel
+    // on the copy stream, read back into pinned h_rows; ev_rows)
+    int* d_rows = nullptr;
+    int* h_rows = nullptr;
+    int rows_cap = 0;
+    cudaEvent_t ev_rows = nullptr;
     cudaEvent_t ev_k[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 
     // wavefront buffers of the train ray pass (psdf_train.cuh)
@@ -695,6 +707,31 @@ bool wave_overflowed(psdf_ctx* c) {
 // tile] -> K2b -> K2d -> K2e (psdf_train.cuh), with no host round trip: the
 // kernels read their item counts on device, the counters are copied back with
 // the step's results (wave_overflowed() checks them).
+// First / last row in [r0, r1] of a mask with a nonzero byte (warp per row):
+// rows[0] atomicMin as unsigned, rows[1] atomicMax (both preset to -1).
+__global__ void __launch_bounds__(256) mask_rows_kernel(const uint8_t* __restrict__ mask, int w, int r0, int r1,
+                                                        int* __restrict__ rows) {
+    const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+    for (int r = r0 + blockIdx.x * wpb + (threadIdx.x >> 5); r <= r1; r += gridDim.x * wpb) {
+        const uint8_t* q = mask + (size_t)r * w;
+        bool any = false;
+        for (int k = lane; k < w; k += 32) any |= q[k] != 0;
+        if (__any_sync(0xffffffffu, any) && lane == 0) {
+            atomicMin(reinterpret_cast<unsigned*>(rows), (unsigned)r);
+            atomicMax(rows + 1, r);
+        }
+    }
+}
+
+// The deferred colour copies of psdf_train_step (no-op once done / for
+// resident images).  Every wait on ev_rgb is preceded by this call.
+void run_rgb_copy(psdf_ctx* c) {
+    if (!c->rgb_copy) return;
+    std::function<void()> f = std::move(c->rgb_copy);
+    c->rgb_copy = nullptr;
+    f();
+}
+
 template <int NS, int NA>
 void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     cudaStream_t s = c->stream;
@@ -865,6 +902,7 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
         for (int k = 3; k <= 4; ++k) CK(cudaEventRecord(c->ev_k[k], s));
     } else {
         // the photo terms read the ground-truth colours
+        run_rgb_copy(c);
         if (c->images_pending) CK(cudaStreamWaitEvent(s, c->ev_rgb, 0));
         if (c->grads_clear_pending) CK(cudaStreamWaitEvent(s, c->ev_zeroed, 0));
         const int grid_ab = blocks_per_sm((const void*)alpha_bwd_kernel, 0) * c->sm_count;
@@ -900,6 +938,7 @@ void launch_empty_ray_loss(psdf_ctx* c, const RayPassParams& P, cudaStream_t st)
     const int64_t n_work = P.tile_end - P.tile_begin;
     if (n_work <= 0) return;
     if (st != c->stream) CK(cudaStreamWaitEvent(st, c->ev_scanned, 0));
+    run_rgb_copy(c);
     if (c->images_pending) CK(cudaStreamWaitEvent(st, c->ev_rgb, 0));
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n_work + 4 * WARPS_PER_BLOCK - 1) / (4 * WARPS_PER_BLOCK),
                                                                 (int64_t)8 * c->sm_count));
@@ -1285,6 +1324,7 @@ int psdf_create(int device, psdf_ctx** out) {
         CK(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_zeroed, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_rgb, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_rows, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_copy_free, cudaEventDisableTiming));
         CK(cudaEventRecord(c->ev_copy_free, c->stream));
         CK(cudaEventCreate(&c->ev_ray0));
@@ -1344,6 +1384,9 @@ int psdf_destroy(psdf_ctx* c) {
         cudaEventDestroy(c->ev_start);
         cudaEventDestroy(c->ev_zeroed);
         cudaEventDestroy(c->ev_rgb);
+        cudaEventDestroy(c->ev_rows);
+        if (c->d_rows) cudaFree(c->d_rows);
+        if (c->h_rows) cudaFreeHost(c->h_rows);
         if (c->d_hand_bits) cudaFree(c->d_hand_bits);
         delete c;
     });
@@ -2781,20 +2824,59 @@ int psdf_train_step(psdf_ctx* c, int n_views, const psdf_camera* cams, const flo
             c->last_h2d_bytes += (int64_t)m;
         }
         CK(cudaEventRecord(c->ev_masks, c->copy_stream));
+        // the colours are read only at in-mask pixels (photo_pixel,
+        // losses.cpp:8-38): only the rows between a view's first and last
+        // row holding a mask pixel are copied.  The GPU finds those rows in
+        // the copied masks (mask_rows_kernel on the copy stream, 8 bytes per
+        // view back to pinned memory); the colour copies are enqueued from
+        // inside the ray pass once its forward kernels are queued (the host
+        // waits for the row extents there, long ready, while the GPU marches)
+        if (n_views > c->rows_cap) {
+            if (c->d_rows) cudaFree(c->d_rows);
+            if (c->h_rows) cudaFreeHost(c->h_rows);
+            c->d_rows = nullptr;
+            c->h_rows = nullptr;
+            c->rows_cap = 0;
+            CK(cudaMalloc(&c->d_rows, sizeof(int) * 2 * n_views));
+            CK(cudaMallocHost(&c->h_rows, sizeof(int) * 2 * n_views));
+            c->rows_cap = n_views;
+        }
+        CK(cudaMemsetAsync(c->d_rows, 0xff, sizeof(int) * 2 * n_views, c->copy_stream));
         for (int i = 0; i < n_views; ++i) {
             if (row1[i] < row0[i]) continue;
-            const size_t o = (size_t)row0[i] * cams[i].width, m = (size_t)(row1[i] - row0[i] + 1) * cams[i].width;
-            CK(cudaMemcpyAsync(tmp[i].rgb + 3 * o, gt_rgb[i] + 3 * o, sizeof(float) * 3 * m,
-                               cudaMemcpyHostToDevice, c->copy_stream));
-            c->last_h2d_bytes += (int64_t)(sizeof(float) * 3 * m);
+            const int nr = row1[i] - row0[i] + 1;
+            mask_rows_kernel<<<(unsigned)std::min(c->sm_count, (nr + 7) / 8), 256, 0, c->copy_stream>>>(
+                tmp[i].mask, cams[i].width, row0[i], row1[i], c->d_rows + 2 * i);
+            CK(cudaGetLastError());
         }
-        CK(cudaEventRecord(c->ev_rgb, c->copy_stream));
-        CK(cudaEventRecord(c->ev_copied, c->copy_stream));
+        CK(cudaMemcpyAsync(c->h_rows, c->d_rows, sizeof(int) * 2 * n_views, cudaMemcpyDeviceToHost,
+                           c->copy_stream));
+        CK(cudaEventRecord(c->ev_rows, c->copy_stream));
+        c->rgb_copy = [&, n_views]() {
+            CK(cudaEventSynchronize(c->ev_rows));
+            for (int i = 0; i < n_views; ++i) {
+                const int m0 = c->h_rows[2 * i], m1 = c->h_rows[2 * i + 1];
+                if (m0 < 0 || m1 < m0) continue;  // no mask pixel in the rank's rows
+                const int w = cams[i].width;
+                const size_t o = (size_t)m0 * w, m = (size_t)(m1 - m0 + 1) * w;
+                CK(cudaMemcpyAsync(tmp[i].rgb + 3 * o, gt_rgb[i] + 3 * o, sizeof(float) * 3 * m,
+                                   cudaMemcpyHostToDevice, c->copy_stream));
+                c->last_h2d_bytes += (int64_t)(sizeof(float) * 3 * m);
+            }
+            CK(cudaEventRecord(c->ev_rgb, c->copy_stream));
+            CK(cudaEventRecord(c->ev_copied, c->copy_stream));
+        };
         c->images_pending = true;
         try {
             do_train_step(c, batch, hp, losses, counts, nullptr);
+            run_rgb_copy(c);  // (already run by the ray pass; ev_copied must exist below)
         } catch (...) {
             c->images_pending = false;
+            if (c->rgb_copy) {  // keep ev_copied ordered after the masks at least
+                c->rgb_copy = nullptr;
+                cudaEventRecord(c->ev_rgb, c->copy_stream);
+                cudaEventRecord(c->ev_copied, c->copy_stream);
+            }
             throw;
         }
         c->images_pending = false;

@@ -227,3 +227,63 @@ def test_unsupported_channel_widths_fail_loudly(ctx):
     g.cfg.n_s, g.cfg.n_a = 16, 4
     with pytest.raises(PsdfInvalidArgument, match=r"unsupported \(n_s, n_a\) = \(16, 4\)"):
         ctx.upload(g, smooth=False)
+
+
+def test_colour_rows_outside_masks_not_needed(ctx):
+    """psdf_train_step copies the colours only between each view's first and
+    last row holding a mask pixel (found on the GPU): colour rows outside
+    them are never read.  NaN there must change nothing, and the step equals
+    the oracle's; a view with an empty mask copies no colours at all."""
+    from paper_2412_10084_b200 import api
+    from oracle.port import step_params as ostep
+    from oracle.refcore import RefCamera
+    g, a = make_scene(res=64, n_s=4, n_a=4, sh_order=3, band=6, ncam=0)
+    og, sm = oracle_with_f32_smooth(a)
+    g.smooth = sm
+    ctx.upload(g, smooth=True)
+    cams = api.make_ring_cameras(3, 40, height=28)
+    rng = np.random.default_rng(11)
+    masks, clean, dirty = [], [], []
+    for i, c in enumerate(cams):
+        m = np.zeros((c.height, c.width))
+        if i < 2:  # rows [5, 20] (view 0) / [0, 9] (view 1) hold mask pixels
+            lo, hi = (5, 20) if i == 0 else (0, 9)
+            m[lo:hi + 1] = rng.uniform(0, 1, (hi - lo + 1, c.width)) > 0.4
+            m[lo, 0] = m[hi, c.width - 1] = 1
+        masks.append(m)
+        gt = rng.uniform(0, 1, (c.height, c.width, 3)).astype(np.float32)
+        clean.append(gt)
+        d = gt.copy()
+        rows = np.flatnonzero(m.any(axis=1))
+        out = np.ones(c.height, bool)
+        if rows.size:
+            out[rows.min():rows.max() + 1] = False
+        d[out] = np.nan
+        dirty.append(d)
+    kw = dict(tau=300.0 * 64, lr_vox=1e-4, lr_mlp=6e-5, photo_scale=20.0)
+    res = []
+    for gts in (clean, dirty):
+        ctx.upload(g, smooth=True)
+        ctx.keep_raypass_grads(True)
+        ctx.train_reset()
+        losses, counts = ctx.train_step(cams, gts, masks, api.step_params(**kw))
+        res.append((losses, counts, ctx.grads(1), ctx.last_h2d_bytes()))
+    (l0, c0, g0, b0), (l1, c1, g1, b1) = res
+    assert c0 == c1 and b0 == b1
+    assert b0 == sum(c.width * c.height for c in cams) + 12 * 40 * (16 + 10)  # masks + rows 5..20, 0..9
+    for k in l0:
+        assert np.isfinite(l1[k]) and abs(l0[k] - l1[k]) <= 1e-9 * max(abs(l0[k]), 1e-9), (k, l0[k], l1[k])
+    for k in ("raw", "planes", "probes", "mlp"):
+        np.testing.assert_allclose(g1[k], g0[k], rtol=1e-5, atol=1e-7 * max(np.abs(g0[k]).max(), 1e-30))
+    ocams = []
+    for c in cams:
+        oc = RefCamera()
+        for k in ("fx", "fy", "cx", "cy", "width", "height", "id"):
+            setattr(oc, k, getattr(c, k))
+        oc.rot[:] = list(c.rot)
+        oc.pos[:] = list(c.pos)
+        ocams.append(oc)
+    ol, oc = og.train_step(ocams, [x.astype(np.float64) for x in clean], masks, ostep(**kw))
+    assert [c0[k] for k in ("n_rays", "n_marched", "n_extra", "n_shaded", "n_alpha", "n_bwd_rays")] == list(oc)
+    for i, k in enumerate(("photo", "sdf", "eik", "normal", "features", "probes")):
+        assert abs(l0[k] - ol[i]) <= 1e-4 * max(abs(ol[i]), 1e-6), (k, l0[k], ol[i])
