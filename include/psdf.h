@@ -232,7 +232,9 @@ int psdf_download_mesh(psdf_ctx* ctx, double* verts, int32_t* tris);
  * One iteration of the train() loop body (trainer.cpp:136-195): clear
  * gradients, ray pass over every pixel of the batch views (render_ray +
  * photo_pixel + render_ray_backward), regularizers, G^T fold, Adam, re-smooth.
- * Host images: gt_rgb[i] [h][w][3] f32, mask[i] [h][w] u8.  With a
+ * Host images: gt_rgb[i] [h][w][3] f32, mask[i] [h][w] u8 (nonzero = in
+ * mask); colours are read only at in-mask pixels, and only the rows between a
+ * view's first and last mask row are copied to the device.  With a
  * communicator (psdf_comm_init) each rank processes its contiguous 1/N slice
  * of the batch's pixels and the gradients are all-reduced before Adam. */
 int psdf_train_reset(psdf_ctx* ctx); /* fresh Adam state (trainer.cpp:115) */
