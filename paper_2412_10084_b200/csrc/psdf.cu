@@ -725,11 +725,12 @@ __global__ void __launch_bounds__(256) mask_rows_kernel(const uint8_t* __restric
 
 // The deferred colour copies of psdf_train_step (no-op once done / for
 // resident images).  Every wait on ev_rgb is preceded by this call.
-void run_rgb_copy(psdf_ctx* c) {
-    if (!c->rgb_copy) return;
+bool run_rgb_copy(psdf_ctx* c) {
+    if (!c->rgb_copy) return false;
     std::function<void()> f = std::move(c->rgb_copy);
     c->rgb_copy = nullptr;
     f();
+    return true;
 }
 
 template <int NS, int NA>
@@ -2869,7 +2870,9 @@ int psdf_train_step(psdf_ctx* c, int n_views, const psdf_camera* cams, const flo
         c->images_pending = true;
         try {
             do_train_step(c, batch, hp, losses, counts, nullptr);
-            run_rgb_copy(c);  // (already run by the ray pass; ev_copied must exist below)
+            // normally run by the ray pass; if not, the copies are issued now
+            // and must land before the caller's buffers are released
+            if (run_rgb_copy(c)) CK(cudaStreamSynchronize(c->copy_stream));
         } catch (...) {
             c->images_pending = false;
             if (c->rgb_copy) {  // keep ev_copied ordered after the masks at least
