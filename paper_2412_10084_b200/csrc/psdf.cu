@@ -2880,6 +2880,7 @@ int psdf_train_step(psdf_ctx* c, int n_views, const psdf_camera* cams, const flo
                 cudaEventRecord(c->ev_rgb, c->copy_stream);
                 cudaEventRecord(c->ev_copied, c->copy_stream);
             }
+            cudaStreamSynchronize(c->copy_stream);  // no copy may outlive the call
             throw;
         }
         c->images_pending = false;
