@@ -1130,6 +1130,9 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
     const bool early = c->regs_early || (int64_t)c->desc.T * 1000 > n_rays;
     c->fork_regs = overlap && !early;
     if (overlap && early) CK(cudaEventRecord(c->ev_fork, s));
+    // the saturation table needs only the grid and tau: launched before the
+    // host builds the view table, so the GPU starts the step sooner
+    prepare_sat(c, P.early_stop > 1.0 ? 0.0 : P.tau);
     if (images_ready) CK(cudaStreamWaitEvent(s, images_ready, 0));
     const int64_t tiles = upload_viewdev(c, vd);
     // ray-batch data parallelism: contiguous 1/N slice of the batch's work tiles
@@ -1141,7 +1144,6 @@ void do_train_step(psdf_ctx* c, const std::vector<DevView*>& batch, const psdf_s
     P.g_planes = c->d_grads + c->off_planes;
     P.g_probes = c->d_grads + c->off_probes;
     P.g_mlp = c->d_grads + c->off_mlp;
-    prepare_sat(c, P.early_stop > 1.0 ? 0.0 : P.tau);
     dispatch_channels(c->desc.n_s, c->desc.n_a, [&]<int NS, int NA>() {
         launch_train_raypass<NS, NA>(c, P, n_rays);
     });
