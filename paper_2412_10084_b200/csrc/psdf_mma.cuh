@@ -45,13 +45,14 @@ struct Split2 {
 // 6e-7 relative to the f64 oracle); passing lo unrounded is NOT equivalent —
 // the tensor core does not simply ignore the low 13 bits (plane gradients
 // drifted to 2e-4).
+__device__ __forceinline__ void split1(float v, uint32_t& hi, uint32_t& lo) {
+    hi = __float_as_uint(v) & 0xffffe000u;
+    lo = (__float_as_uint(v - __uint_as_float(hi)) + 0x1000u) & 0xffffe000u;
+}
 template <int N, class S>
 __device__ __forceinline__ void split(const float* v, S& s) {
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-        s.hi[i] = __float_as_uint(v[i]) & 0xffffe000u;
-        s.lo[i] = (__float_as_uint(v[i] - __uint_as_float(s.hi[i])) + 0x1000u) & 0xffffe000u;
-    }
+    for (int i = 0; i < N; ++i) split1(v[i], s.hi[i], s.lo[i]);
 }
 
 // C[MT*16 x NT*8] += A(m, k) B(n, k) over k in [0, KT*8); A and B are element

@@ -1503,6 +1503,10 @@ struct MmaDims {
     static constexpr int W3 = W2T + 32 * HS;  // [8][HS]    rows 3..7 zero
     static constexpr int B1 = W3 + 8 * HS, B2 = B1 + 32, B3 = B2 + 32;
     static constexpr int MLP = B3 + 4;
+    // the weights [0, B1) are kept pre-split for the 3xTF32 products: TF32
+    // high halves in place, low halves at WLO + the same offset
+    static constexpr int WLO = MLP;
+    static constexpr int MLPX = WLO + B1;     // shared MLP incl. the low halves
     // per-warp scratch
     static constexpr int SX = 0;                // [32][XS]  X, later DIN
     static constexpr int SA1 = SX + 32 * XS;    // [32][HS]  A1, later DZ1
@@ -1530,7 +1534,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_BWD_MINB) shade_bwd_kernel(RayPass
     const MlpLayout G = MlpLayout::make(IN);
     float* sm = smem;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* scr = smem + D::MLP + warp * D::SCR;
+    float* scr = smem + D::MLPX + warp * D::SCR;
     __shared__ int s_cam[WARPS_PER_BLOCK][32];
     int* cam = s_cam[warp];
     // MLP into shared memory: padded W1 / W1^T / W2 / W2^T / W3, biases
@@ -1553,6 +1557,15 @@ __global__ void __launch_bounds__(BLOCK, PSDF_BWD_MINB) shade_bwd_kernel(RayPass
         sm[D::B2 + i] = __ldg(P.mlp + G.b2 + i);
     }
     __syncthreads();
+    for (int i = threadIdx.x; i < D::B1; i += blockDim.x) {  // pre-split weights (once per block)
+        uint32_t hi, lo;
+        split1(sm[i], hi, lo);
+        sm[i] = __uint_as_float(hi);
+        sm[D::WLO + i] = __uint_as_float(lo);
+    }
+    __syncthreads();
+    auto wh = [&](int a) { return __float_as_uint(sm[a]); };
+    auto wl = [&](int a) { return __float_as_uint(sm[D::WLO + a]); };
     // weight-gradient accumulators: this warp's C fragments, kept in registers
     // across its batches (dW2 32x32, dW1 32xK1, dW3 rows 0..2) + bias sums
     float gw2[2][4][4], gw1[2][D::K1 / 8][4], gw3[1][4][4];
@@ -1611,9 +1624,10 @@ __global__ void __launch_bounds__(BLOCK, PSDF_BWD_MINB) shade_bwd_kernel(RayPass
         {
             float c[2][4][4];
             zero_c(c);
-            warp_gemm3<2, 4, D::K1 / 8>(
+            warp_gemm3w<2, 4, D::K1 / 8>(
                 c, [&](int m, int k) { return X[m * D::XS + k]; },
-                [&](int n, int k) { return sm[D::W1 + n * D::XS + k]; });
+                [&](int n, int k) { return wh(D::W1 + n * D::XS + k); },
+                [&](int n, int k) { return wl(D::W1 + n * D::XS + k); });
             if (has_cam) {
                 for_c(c, [&](int m, int n, float& v) {
                     float z = v + sm[D::B1 + n];
@@ -1632,9 +1646,10 @@ __global__ void __launch_bounds__(BLOCK, PSDF_BWD_MINB) shade_bwd_kernel(RayPass
         {
             float c[2][4][4];
             zero_c(c);
-            warp_gemm3<2, 4, 4>(
+            warp_gemm3w<2, 4, 4>(
                 c, [&](int m, int k) { return A1[m * D::HS + k]; },
-                [&](int n, int k) { return sm[D::W2 + n * D::HS + k]; });
+                [&](int n, int k) { return wh(D::W2 + n * D::HS + k); },
+                [&](int n, int k) { return wl(D::W2 + n * D::HS + k); });
             for_c(c, [&](int m, int n, float& v) {
                 const float z = v + sm[D::B2 + n];
                 A2[m * D::HS + n] = z > 0.f ? z : 0.f;
@@ -1654,9 +1669,10 @@ __global__ void __launch_bounds__(BLOCK, PSDF_BWD_MINB) shade_bwd_kernel(RayPass
         {
             float c[2][4][4];
             zero_c(c);
-            warp_gemm3<2, 4, 1>(
+            warp_gemm3w<2, 4, 1>(
                 c, [&](int m, int k) { return D3[m * D::DS + k]; },
-                [&](int n, int k) { return sm[D::W3 + k * D::HS + n]; });
+                [&](int n, int k) { return wh(D::W3 + k * D::HS + n); },
+                [&](int n, int k) { return wl(D::W3 + k * D::HS + n); });
             __syncwarp();
             for_c(c, [&](int m, int n, float& v) {
                 float& a = A2[m * D::HS + n];
@@ -1676,9 +1692,10 @@ __global__ void __launch_bounds__(BLOCK, PSDF_BWD_MINB) shade_bwd_kernel(RayPass
         {
             float c[2][4][4];
             zero_c(c);
-            warp_gemm3<2, 4, 4>(
+            warp_gemm3w<2, 4, 4>(
                 c, [&](int m, int k) { return A2[m * D::HS + k]; },
-                [&](int n, int k) { return sm[D::W2T + n * D::HS + k]; });
+                [&](int n, int k) { return wh(D::W2T + n * D::HS + k); },
+                [&](int n, int k) { return wl(D::W2T + n * D::HS + k); });
             __syncwarp();
             for_c(c, [&](int m, int n, float& v) {
                 float& a = A1[m * D::HS + n];
@@ -1709,9 +1726,10 @@ __global__ void __launch_bounds__(BLOCK, PSDF_BWD_MINB) shade_bwd_kernel(RayPass
         {
             float c[2][D::K1 / 8][4];
             zero_c(c);
-            warp_gemm3<2, D::K1 / 8, 4>(
+            warp_gemm3w<2, D::K1 / 8, 4>(
                 c, [&](int m, int k) { return A1[m * D::HS + k]; },
-                [&](int n, int k) { return sm[D::W1T + n * D::HS + k]; });
+                [&](int n, int k) { return wh(D::W1T + n * D::HS + k); },
+                [&](int n, int k) { return wl(D::W1T + n * D::HS + k); });
             __syncwarp();
             for_c(c, [&](int m, int n, float& v) { X[m * D::XS + n] = v; });
         }
@@ -1758,7 +1776,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_BWD_MINB) shade_bwd_kernel(RayPass
         else a = D::GB3 + (q - G.b3);
         float v = 0.f;
 #pragma unroll
-        for (int w = 0; w < WARPS_PER_BLOCK; ++w) v += smem[D::MLP + w * D::SCR + a];
+        for (int w = 0; w < WARPS_PER_BLOCK; ++w) v += smem[D::MLPX + w * D::SCR + a];
         if (v != 0.f) atomicAdd(P.g_mlp + q, v);
     }
 }
@@ -1969,7 +1987,7 @@ template <int NS, int NA>
 size_t shade_bwd_smem_bytes() {
     using D = MmaDims<NS + NA + NPOW>;
     static_assert(D::GACC <= D::SCR, "accumulator flush reuses the warp scratch");
-    return sizeof(float) * (D::MLP + WARPS_PER_BLOCK * D::SCR);
+    return sizeof(float) * (D::MLPX + WARPS_PER_BLOCK * D::SCR);
 }
 
 }  // namespace psdf
