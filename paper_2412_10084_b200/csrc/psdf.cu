@@ -246,7 +246,7 @@ struct psdf_ctx {
     bool images_pending = false;           // inside psdf_train_step: the copies may still run
     cudaEvent_t ev_masks = nullptr, ev_rgb = nullptr;  // masks / colours of the step copied
     unsigned* d_hand_bits = nullptr;       // [work tiles] scan hand-over lanes
-    float* d_tmin = nullptr;               // [work tiles] first allocated-tile hit bound (tile_raster_kernel)
+    float* d_tmin = nullptr;               // [2][work tiles] first / last allocated-tile hit bounds (tile_raster_kernel)
     int64_t tmin_cap = 0;
     int64_t batch_tiles = 0;               // work tiles of the current view table (upload_viewdev)
     int64_t active_tiles = 0;              // work tiles on the scan's list (upload_viewdev)
@@ -790,19 +790,23 @@ void launch_train_raypass(psdf_ctx* c, RayPassParams& P, int64_t n_rays) {
     if (c->tmin_cap < all_tiles) {
         if (c->d_tmin) cudaFree(c->d_tmin);
         c->d_tmin = nullptr;
-        CK(cudaMalloc(&c->d_tmin, sizeof(float) * std::max<int64_t>(all_tiles, 1)));
+        CK(cudaMalloc(&c->d_tmin, 2 * sizeof(float) * std::max<int64_t>(all_tiles, 1)));
         c->tmin_cap = all_tiles;
     }
     {
-        CK(cudaMemsetAsync(c->d_tmin, 0x7F, sizeof(float) * std::max<int64_t>(all_tiles, 1), s));
+        const int64_t nt = std::max<int64_t>(all_tiles, 1);
+        CK(cudaMemsetAsync(c->d_tmin, 0x7F, sizeof(float) * nt, s));
+        CK(cudaMemsetAsync(c->d_tmin + c->tmin_cap, 0, sizeof(float) * nt, s));
         const int64_t warps = (int64_t)c->desc.T * P.n_views;
         if (warps > 0) {
-            tile_raster_kernel<<<(unsigned)((warps + 3) / 4), 128, 0, s>>>(P.g, P.views, P.n_views, c->d_tmin);
+            tile_raster_kernel<<<(unsigned)((warps + 3) / 4), 128, 0, s>>>(P.g, P.views, P.n_views, c->d_tmin,
+                                                                          c->d_tmin + c->tmin_cap);
             CK(cudaGetLastError());
             ++c->last_launches;
         }
     }
     P.tile_tmin = c->d_tmin;
+    P.tile_tmax = c->d_tmin + c->tmin_cap;
     if (P.mode != 1) {
         CK(cudaMemsetAsync(W.hand_bits, 0, sizeof(unsigned) * std::max<int64_t>(n_work, 1), s));
     } else {

@@ -67,6 +67,7 @@ struct RayPassParams {
     int64_t tile_begin, tile_end;  // this rank's slice of the global work tiles
     int64_t scan_lo, scan_hi;      // K2a-scan: active-tile list range [lo, hi) (ViewDev::act_*)
     const float* tile_tmin;        // [global work tiles] lower bound on the first allocated-tile hit (kTminNone: none)
+    const float* tile_tmax;        // [global work tiles] upper bound on the distance of any sample (last allocated tile)
     unsigned long long* work_counter;
     // render outputs (K1)
     float* out_rgb;

@@ -263,6 +263,11 @@ __global__ void __launch_bounds__(BLOCK, PSDF_SCAN_MINB) march_scan_kernel(RayPa
             const double dd[3] = {dir.x, dir.y, dir.z};
             if (mr.init(g, R.V->cam.pos, dd, P.n_max) && mr.enter_occupied(g)) {
                 mr.jump_to(g, (double)tl);
+                // no sample lies beyond the work tile's farthest allocated
+                // tile: the march ends there instead of at the grid exit
+                // (t1 only bounds the loop; every sample before it is kept)
+                const double tf = (double)__ldg(P.tile_tmax + gt);
+                if (tf < mr.t1) mr.t1 = tf;
                 for (;;) {
                     double ts;
                     int tile;
@@ -350,7 +355,7 @@ __global__ void __launch_bounds__(BLOCK, PSDF_SCAN_MINB) march_scan_kernel(RayPa
 // beside or behind the camera mark the whole view.  atomicMin on the float
 // bits (non-negative floats order as integers).
 __global__ void __launch_bounds__(128) tile_raster_kernel(GridView g, const ViewDev* views, int n_views,
-                                                          float* __restrict__ tmin) {
+                                                          float* __restrict__ tmin, float* __restrict__ tmax) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (gw >= (int64_t)g.T * n_views) return;
@@ -395,6 +400,15 @@ __global__ void __launch_bounds__(128) tile_raster_kernel(GridView g, const View
         q += e * e;
     }
     const float tv = __double2float_rd(fmax(sqrt(q) - 2.0 * g.h, 0.0));
+    // and to its farthest corner, plus 2 voxels, rounded up: no sample in the
+    // tile lies farther along a unit-direction ray from the camera
+    double qf = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double e = fmax(fabs(lo[a] - k.pos[a]), fabs(lo[a] + s16 - k.pos[a]));
+        qf += e * e;
+    }
+    const float tf = __double2float_ru(sqrt(qf) + 2.0 * g.h);
     int tx0 = 0, tx1 = V.tiles_x - 1, ty0 = 0, ty1 = V.tiles_y - 1;
     if (!bad) {  // work tile tx spans image points [8 tx + 0.5, 8 tx + 7.5]
         tx0 = max(tx0, (int)ceilf((umin - 1.f - 7.5f) * 0.125f));
@@ -406,6 +420,7 @@ __global__ void __launch_bounds__(128) tile_raster_kernel(GridView g, const View
     for (int i = lane; i < n; i += 32) {
         const int ty = ty0 + i / w, tx = tx0 + (i - (i / w) * w);
         atomicMin(reinterpret_cast<int*>(tmin) + V.tile_begin + (int64_t)ty * V.tiles_x + tx, __float_as_int(tv));
+        atomicMax(reinterpret_cast<int*>(tmax) + V.tile_begin + (int64_t)ty * V.tiles_x + tx, __float_as_int(tf));
     }
 }
 
